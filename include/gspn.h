@@ -1,0 +1,119 @@
+/*
+ * gspn.h — C ABI of the B200-native GSPN / GSPN-2 line-scan propagation (arxiv 2512.07884).
+ *
+ * Operation (§3.2 Eq. 1; §4.2 Eq. 3; §3.2):
+ *   In scan coordinates (step t = 0..L-1, position r = 0..P-1) of one direction, one batch b and one
+ *   channel c in weight group g = c / (C/G):
+ *
+ *     h_t[r] = a_t[r] h_{t-1}[r-1] + b_t[r] h_{t-1}[r] + c_t[r] h_{t-1}[r+1] + lam_t[r] x_t[r],  h_{-1} = 0
+ *
+ *   (a, b, c) are the row-normalised ("row-stochastic") tridiagonal taps of the raw
+ *   per-pixel taps (w_l, w_m, w_r):  S = w_m + [r>=1] w_l + [r<=P-2] w_r,
+ *   a = [r>=1] w_l / S,  b = w_m / S,  c = [r<=P-2] w_r / S   (out-of-range taps are dropped and the
+ *   row renormalised over the in-range ones; readings R1, R2). h_{-1} = 0 follows from
+ *   Eq. 4's first block row Lambda_1. With GSPN_FLAG_PRENORMALIZED the taps are used
+ *   as given (still dropped out of range) and no division happens.
+ *
+ *   Directions ("four complementary directional passes"); canonical pixel (i, j):
+ *     T2B: t = i,       r = j   (L = H, P = W)       B2T: t = H-1-i, r = j   (L = H, P = W)
+ *     L2R: t = j,       r = i   (L = W, P = H)       R2L: t = W-1-j, r = i   (L = W, P = H)
+ *   w_l always multiplies the neighbour with the smaller canonical parallel index (R4).
+ *   The taps stored at pixel (i, j) are the row of the step matrix that produces pixel (i, j) (R5).
+ *
+ * Layout (all tensors dense, contiguous, row-major, element type = dtype):
+ *   x                 [B, C, H, W]        shared by all directions (R6)
+ *   w_l, w_m, w_r     [D, B, G, H, W]     one tap triple per pixel per group (G = C: per-channel
+ *                                          weights, Eq. 1; G = 1: channel-shared weights, Eq. 3)
+ *   lam, h, dh, dlam  [D, B, C, H, W]
+ *   dx                [B, C, H, W]        sum over the D directions
+ *   dw_l, dw_m, dw_r  [D, B, G, H, W]     gradient w.r.t. the RAW taps, summed over the group's channels
+ *   D = popcount(dirs); direction slabs appear in bit order T2B, B2T, L2R, R2L.
+ *
+ * Ownership: every tensor pointer is a caller-owned DEVICE pointer (cudaMalloc / torch). The library
+ *   allocates nothing, keeps no pointer after return, and writes only the listed outputs (and the
+ *   caller's workspace). Outputs are fully overwritten, never accumulated into.
+ * Execution: stream-ordered and asynchronous on `stream`; no host synchronisation inside. Device-side
+ *   faults surface at the caller's next synchronisation (CUDA convention).
+ * Errors: arguments are validated on the host BEFORE any CUDA call; on failure nothing is launched
+ *   or written and the call returns GSPN_ERR_INVALID_ARG (detail in gspn_last_error_detail()).
+ *   No C++ exception crosses this boundary.
+ * Preconditions not checked on the device: taps >= 0 with S > 0 at every position, inputs finite.
+ */
+#ifndef GSPN_H_
+#define GSPN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  GSPN_OK = 0,
+  GSPN_ERR_INVALID_ARG = 1, /* bad pointer / dim / flag / dtype / alignment / aliasing */
+  GSPN_ERR_UNSUPPORTED = 2, /* shape the kernels cannot tile (never for BASELINE.json's configs) */
+  GSPN_ERR_CUDA = 3,        /* a CUDA runtime / driver call or launch failed */
+  GSPN_ERR_INTERNAL = 4     /* anything else (caught exception) */
+} gspn_status_t;
+
+typedef enum { GSPN_F32 = 0, GSPN_BF16 = 1 } gspn_dtype_t;
+
+#define GSPN_DIR_T2B 0x1u /* step = row i ascending,     position = column j */
+#define GSPN_DIR_B2T 0x2u /* step = row i descending,    position = column j */
+#define GSPN_DIR_L2R 0x4u /* step = column j ascending,  position = row i    */
+#define GSPN_DIR_R2L 0x8u /* step = column j descending, position = row i    */
+#define GSPN_DIR_ALL 0xFu
+
+#define GSPN_FLAG_PRENORMALIZED 0x1u /* taps already row-normalised: no division (out-of-range taps still dropped) */
+#define GSPN_FLAG_FORCE_GENERIC 0x2u /* testing: force the generic (non-TMA) kernels */
+
+/* cudaStream_t without including CUDA headers (ABI-identical: an opaque pointer). */
+typedef struct CUstream_st* gspn_stream_t;
+
+/*
+ * Forward scan, all requested directions in one persistent launch.
+ *   x [B,C,H,W]; w_l/w_m/w_r [D,B,G,H,W]; lam [D,B,C,H,W]  -> h [D,B,C,H,W]
+ *   B, C, H, W, groups >= 1; C % groups == 0; dirs in [1, 15]; flags subset of GSPN_FLAG_*.
+ *   Every pointer non-null and 16-byte aligned; h must not overlap any input.
+ */
+gspn_status_t gspn_fwd(const void* x, const void* w_l, const void* w_m, const void* w_r, const void* lam,
+                       void* h, int64_t B, int64_t C, int64_t H, int64_t W, uint32_t dirs, int64_t groups,
+                       gspn_dtype_t dtype, uint32_t flags, gspn_stream_t stream);
+
+/*
+ * Backward (adjoint, reverse-order) scan given the saved forward output h and the upstream gradient dh.
+ *   Produces dx [B,C,H,W] (summed over directions), dlam [D,B,C,H,W] and dw_l/dw_m/dw_r [D,B,G,H,W]
+ *   (gradient w.r.t. the raw taps, chained through the row normalisation and summed over the group's
+ *   channels; zero for out-of-range taps and for every tap at step t = 0, whose h_{-1} = 0).
+ *   workspace: caller-owned device scratch of at least gspn_bwd_workspace_bytes(...) bytes (16-byte
+ *   aligned; may be NULL when that size is 0). Its contents on entry are ignored; the library
+ *   initialises it on `stream`. No output may overlap any input, another output or the workspace.
+ */
+gspn_status_t gspn_bwd(const void* x, const void* w_l, const void* w_m, const void* w_r, const void* lam,
+                       const void* h, const void* dh, void* dx, void* dw_l, void* dw_m, void* dw_r, void* dlam,
+                       int64_t B, int64_t C, int64_t H, int64_t W, uint32_t dirs, int64_t groups,
+                       gspn_dtype_t dtype, uint32_t flags, void* workspace, size_t workspace_bytes,
+                       gspn_stream_t stream);
+
+/* Workspace bytes gspn_bwd needs for this problem (0 on invalid arguments). */
+size_t gspn_bwd_workspace_bytes(int64_t B, int64_t C, int64_t H, int64_t W, uint32_t dirs, int64_t groups,
+                                gspn_dtype_t dtype);
+
+/* Algorithmic HBM bytes of one call (each input read once, each output written once):
+ *   fwd = s * (N (1 + 2D) + 3 D N_w),  bwd = 2 * fwd,  N = B C H W,  N_w = B G H W. */
+double gspn_algorithmic_bytes(int64_t B, int64_t C, int64_t H, int64_t W, uint32_t dirs, int64_t groups,
+                              gspn_dtype_t dtype, int backward);
+
+const char* gspn_status_string(gspn_status_t s);
+/* Thread-local detail string of the last failing call on this thread (names the offending argument). */
+const char* gspn_last_error_detail(void);
+/* Name of the kernel path the last successful call on this thread launched ("generic", "stream", ...). */
+const char* gspn_last_path(void);
+/* Number of kernel launches the last successful call on this thread issued (memsets excluded). */
+int gspn_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GSPN_H_ */

@@ -1,0 +1,89 @@
+"""fp64 CPU oracle of the GSPN line scan — TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / ``--impl reference`` legs may
+import this package. The product path (paper_2512_07884_b200) never imports, links or calls it.
+
+The arithmetic lives in oracle/gspn_oracle.c (plain C loops, fp64, -ffp-contract=off); this module
+only builds/loads it and marshals numpy float64 arrays. Layouts are those of include/gspn.h.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "gspn_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle_gspn.so")
+_lib = None
+
+PRENORMALIZED = 1
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with plain gcc (no fast-math, no FMA contraction)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
+                               "-pthread", "-o", tmp, _SRC])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        lib = ctypes.CDLL(build())
+        d = ctypes.POINTER(ctypes.c_double)
+        i64 = ctypes.c_int64
+        lib.gspn_oracle_fwd.argtypes = [d] * 6 + [i64] * 4 + [ctypes.c_uint, i64, ctypes.c_uint, ctypes.c_int]
+        lib.gspn_oracle_fwd.restype = ctypes.c_int
+        lib.gspn_oracle_bwd.argtypes = [d] * 12 + [i64] * 4 + [ctypes.c_uint, i64, ctypes.c_uint, ctypes.c_int]
+        lib.gspn_oracle_bwd.restype = ctypes.c_int
+        lib.gspn_oracle_detail.restype = ctypes.c_char_p
+        _lib = lib
+    return _lib
+
+
+class OracleError(RuntimeError):
+    pass
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def default_threads() -> int:
+    return len(os.sched_getaffinity(0))
+
+
+def fwd(x, wl, wm, wr, lam, dirs: int, groups: int, flags: int = 0, threads: int = 1) -> np.ndarray:
+    """h [D,B,C,H,W] from x [B,C,H,W], w_* [D,B,G,H,W], lam [D,B,C,H,W] (float64)."""
+    x, wl, wm, wr, lam = map(_f64, (x, wl, wm, wr, lam))
+    B, C, H, W = x.shape
+    h = np.empty(lam.shape, dtype=np.float64)
+    st = _load().gspn_oracle_fwd(_p(x), _p(wl), _p(wm), _p(wr), _p(lam), _p(h), B, C, H, W, dirs, groups,
+                                 flags, threads)
+    if st:
+        raise OracleError(f"oracle fwd status {st}: {_load().gspn_oracle_detail().decode()}")
+    return h
+
+
+def bwd(x, wl, wm, wr, lam, h, dh, dirs: int, groups: int, flags: int = 0, threads: int = 1):
+    """(dx, dw_l, dw_m, dw_r, dlam) given saved h and upstream dh (float64)."""
+    x, wl, wm, wr, lam, h, dh = map(_f64, (x, wl, wm, wr, lam, h, dh))
+    B, C, H, W = x.shape
+    dx = np.empty(x.shape)
+    dwl, dwm, dwr = np.empty(wl.shape), np.empty(wl.shape), np.empty(wl.shape)
+    dlam = np.empty(lam.shape)
+    st = _load().gspn_oracle_bwd(_p(x), _p(wl), _p(wm), _p(wr), _p(lam), _p(h), _p(dh), _p(dx), _p(dwl), _p(dwm),
+                                 _p(dwr), _p(dlam), B, C, H, W, dirs, groups, flags, threads)
+    if st:
+        raise OracleError(f"oracle bwd status {st}: {_load().gspn_oracle_detail().decode()}")
+    return dx, dwl, dwm, dwr, dlam

@@ -1,0 +1,292 @@
+/*
+ * oracle/gspn_oracle.c — plain, slow, obviously-correct fp64 CPU oracle of the GSPN line scan.
+ *
+ * TEST INFRASTRUCTURE ONLY. Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference legs may load this. The product path (paper_2512_07884_b200/) never links,
+ * imports or calls it, and this file shares no code, header or table with the CUDA path.
+ *
+ * What it computes (the plain definition; every step in the paper's order and notation):
+ *   PAPER.md:80-83 (§3.2, Eq. 1)      h_i = w_i h_{i-1} + Diag(lambda_i) x_i, per channel
+ *   PAPER.md:144-146 (§4.2, Eq. 3)    the same recurrence with w_i shared by a group of channels
+ *   PAPER.md:89 (§3.2)                w_i tridiagonal (3 neighbours of the previous row), row-stochastic,
+ *                                     four directional passes T2B, B2T, L2R, R2L
+ *   PAPER.md:155 (§4.2, Eq. 4)        first block row is Lambda_1, i.e. h_{-1} = 0
+ *   Backward: the adjoint (reverse-order) recurrence of the same linear map; the paper gives no
+ *   formula, so this is the chain rule written out step by step.
+ * Readings of silent points (R1-R16): row-stochastic = divide the in-range raw taps by
+ * their sum; out-of-range taps dropped; w_l multiplies the smaller canonical parallel index; taps
+ * stored at the output pixel; x shared by all directions; contiguous channel groups g = c / (C/G).
+ *
+ * Layout: x [B,C,H,W]; w_l,w_m,w_r [D,B,G,H,W]; lam,h,dh,dlam [D,B,C,H,W]; dx [B,C,H,W];
+ * dw_* [D,B,G,H,W]; D = popcount(dirs), slabs in bit order T2B, B2T, L2R, R2L. All float64.
+ * Build: gcc -O2 -ffp-contract=off -fPIC -shared -pthread (no fast-math; no FMA contraction).
+ */
+#include <pthread.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define T2B 1u
+#define B2T 2u
+#define L2R 4u
+#define R2L 8u
+#define PRENORMALIZED 1u
+
+enum { ORACLE_OK = 0, ORACLE_BAD_ARG = 1, ORACLE_NONPOSITIVE_SUM = 5, ORACLE_NOMEM = 6 };
+
+static char g_detail[256];
+
+const char* gspn_oracle_detail(void) { return g_detail; }
+
+/* Scan length L and parallel width P of a direction (gspn.h table). */
+static void scan_shape(unsigned dir, int64_t H, int64_t W, int64_t* L, int64_t* P) {
+  if (dir == T2B || dir == B2T) { *L = H; *P = W; } else { *L = W; *P = H; }
+}
+
+/* Canonical offset i*W + j of scan coordinate (t, r). */
+static int64_t pixel(unsigned dir, int64_t H, int64_t W, int64_t t, int64_t r) {
+  int64_t i = 0, j = 0;
+  if (dir == T2B) { i = t; j = r; }
+  else if (dir == B2T) { i = H - 1 - t; j = r; }
+  else if (dir == L2R) { i = r; j = t; }
+  else { i = r; j = W - 1 - t; }
+  return i * W + j;
+}
+
+/* Normalised taps (a, b, c) at scan position r of width P from raw taps (wl, wm, wr).
+ * Returns the row sum S through *S (1 when prenormalised). */
+static int taps(double wl, double wm, double wr, int64_t r, int64_t P, unsigned flags,
+                double* a, double* b, double* c, double* S) {
+  const int has_l = (r >= 1), has_r = (r <= P - 2);
+  if (flags & PRENORMALIZED) {
+    *a = has_l ? wl : 0.0; *b = wm; *c = has_r ? wr : 0.0; *S = 1.0;
+    return 0;
+  }
+  double s = wm;
+  if (has_l) s += wl;
+  if (has_r) s += wr;
+  if (!(s > 0.0)) return 1;
+  *a = has_l ? wl / s : 0.0;
+  *b = wm / s;
+  *c = has_r ? wr / s : 0.0;
+  *S = s;
+  return 0;
+}
+
+typedef struct {
+  const double *x, *wl, *wm, *wr, *lam, *h, *dh;
+  double *hout, *dx, *dwl, *dwm, *dwr, *dlam;
+  int64_t B, C, H, W, G;
+  unsigned dirs, flags;
+  int backward;
+  int64_t next_unit; /* guarded by mu */
+  pthread_mutex_t mu;
+  int status;
+} job_t;
+
+static int dir_list(unsigned dirs, unsigned* out) {
+  int n = 0;
+  const unsigned all[4] = {T2B, B2T, L2R, R2L};
+  for (int k = 0; k < 4; ++k) if (dirs & all[k]) out[n++] = all[k];
+  return n;
+}
+
+/* Forward of unit (b, g): every channel of the group, every direction. Eq. 1 / Eq. 3 step by step. */
+static int forward_unit(job_t* J, int64_t b, int64_t g) {
+  const int64_t HW = J->H * J->W, Cg = J->C / J->G;
+  unsigned dl[4];
+  const int D = dir_list(J->dirs, dl);
+  for (int k = 0; k < D; ++k) {
+    int64_t L, P;
+    scan_shape(dl[k], J->H, J->W, &L, &P);
+    const double* wl = J->wl + ((int64_t)k * J->B * J->G + b * J->G + g) * HW;
+    const double* wm = J->wm + ((int64_t)k * J->B * J->G + b * J->G + g) * HW;
+    const double* wr = J->wr + ((int64_t)k * J->B * J->G + b * J->G + g) * HW;
+    for (int64_t c = g * Cg; c < (g + 1) * Cg; ++c) {
+      const double* x = J->x + (b * J->C + c) * HW;
+      const double* lam = J->lam + ((int64_t)k * J->B * J->C + b * J->C + c) * HW;
+      double* h = J->hout + ((int64_t)k * J->B * J->C + b * J->C + c) * HW;
+      for (int64_t t = 0; t < L; ++t) {
+        for (int64_t r = 0; r < P; ++r) {
+          const int64_t p = pixel(dl[k], J->H, J->W, t, r);
+          double a, bb, cc, S;
+          if (taps(wl[p], wm[p], wr[p], r, P, J->flags, &a, &bb, &cc, &S)) {
+            snprintf(g_detail, sizeof g_detail, "row sum S<=0 at dir=%u b=%lld g=%lld t=%lld r=%lld", dl[k],
+                     (long long)b, (long long)g, (long long)t, (long long)r);
+            return ORACLE_NONPOSITIVE_SUM;
+          }
+          double acc = 0.0; /* w_i h_{i-1}: zero at t = 0 because h_{-1} = 0 */
+          if (t > 0) {
+            if (r >= 1) acc += a * h[pixel(dl[k], J->H, J->W, t - 1, r - 1)];
+            acc += bb * h[pixel(dl[k], J->H, J->W, t - 1, r)];
+            if (r <= P - 2) acc += cc * h[pixel(dl[k], J->H, J->W, t - 1, r + 1)];
+          }
+          h[p] = acc + lam[p] * x[p]; /* + Diag(lambda_i) x_i */
+        }
+      }
+    }
+  }
+  return ORACLE_OK;
+}
+
+/* Backward of unit (b, g): the adjoint of forward_unit, reverse step order, given saved h. */
+static int backward_unit(job_t* J, int64_t b, int64_t g) {
+  const int64_t HW = J->H * J->W, Cg = J->C / J->G;
+  unsigned dl[4];
+  const int D = dir_list(J->dirs, dl);
+  int64_t maxP = J->H > J->W ? J->H : J->W;
+  double* gnext = (double*)calloc((size_t)maxP, sizeof(double));
+  double* gcur = (double*)calloc((size_t)maxP, sizeof(double));
+  double* Da = (double*)calloc((size_t)HW, sizeof(double));
+  double* Db = (double*)calloc((size_t)HW, sizeof(double));
+  double* Dc = (double*)calloc((size_t)HW, sizeof(double));
+  int st = ORACLE_OK;
+  if (!gnext || !gcur || !Da || !Db || !Dc) { st = ORACLE_NOMEM; goto done; }
+  for (int64_t c = g * Cg; c < (g + 1) * Cg; ++c)
+    memset(J->dx + (b * J->C + c) * HW, 0, (size_t)HW * sizeof(double));
+  for (int k = 0; k < D; ++k) {
+    int64_t L, P;
+    scan_shape(dl[k], J->H, J->W, &L, &P);
+    const int64_t wofs = ((int64_t)k * J->B * J->G + b * J->G + g) * HW;
+    const double *wl = J->wl + wofs, *wm = J->wm + wofs, *wr = J->wr + wofs;
+    memset(Da, 0, (size_t)HW * sizeof(double));
+    memset(Db, 0, (size_t)HW * sizeof(double));
+    memset(Dc, 0, (size_t)HW * sizeof(double));
+    for (int64_t c = g * Cg; c < (g + 1) * Cg; ++c) {
+      const int64_t cofs = ((int64_t)k * J->B * J->C + b * J->C + c) * HW;
+      const double* x = J->x + (b * J->C + c) * HW;
+      const double *lam = J->lam + cofs, *h = J->h + cofs, *dh = J->dh + cofs;
+      double* dlam = J->dlam + cofs;
+      double* dx = J->dx + (b * J->C + c) * HW;
+      for (int64_t r = 0; r < P; ++r) gnext[r] = 0.0;
+      for (int64_t t = L - 1; t >= 0; --t) {
+        /* g_t = dh_t + w_{t+1}^T g_{t+1}  (adjoint of h_{t+1} = w_{t+1} h_t + ...) */
+        for (int64_t r = 0; r < P; ++r) {
+          double gt = dh[pixel(dl[k], J->H, J->W, t, r)];
+          if (t + 1 < L) {
+            double a, bb, cc, S;
+            /* row r of w_{t+1} reaches h_t[r] through its centre tap */
+            taps(wl[pixel(dl[k], J->H, J->W, t + 1, r)], wm[pixel(dl[k], J->H, J->W, t + 1, r)],
+                 wr[pixel(dl[k], J->H, J->W, t + 1, r)], r, P, J->flags, &a, &bb, &cc, &S);
+            gt += bb * gnext[r];
+            if (r + 1 <= P - 1) { /* row r+1 reaches h_t[r] through its left tap */
+              const int64_t q = pixel(dl[k], J->H, J->W, t + 1, r + 1);
+              taps(wl[q], wm[q], wr[q], r + 1, P, J->flags, &a, &bb, &cc, &S);
+              gt += a * gnext[r + 1];
+            }
+            if (r - 1 >= 0) { /* row r-1 reaches h_t[r] through its right tap */
+              const int64_t q = pixel(dl[k], J->H, J->W, t + 1, r - 1);
+              taps(wl[q], wm[q], wr[q], r - 1, P, J->flags, &a, &bb, &cc, &S);
+              gt += cc * gnext[r - 1];
+            }
+          }
+          gcur[r] = gt;
+        }
+        for (int64_t r = 0; r < P; ++r) {
+          const int64_t p = pixel(dl[k], J->H, J->W, t, r);
+          dlam[p] = gcur[r] * x[p]; /* d/dlambda of lambda_t x_t */
+          dx[p] += gcur[r] * lam[p]; /* d/dx, summed over directions (R6) */
+          if (t >= 1) {               /* d/d(normalised taps); h_{-1} = 0 gives zero at t = 0 */
+            if (r >= 1) Da[p] += gcur[r] * h[pixel(dl[k], J->H, J->W, t - 1, r - 1)];
+            Db[p] += gcur[r] * h[pixel(dl[k], J->H, J->W, t - 1, r)];
+            if (r <= P - 2) Dc[p] += gcur[r] * h[pixel(dl[k], J->H, J->W, t - 1, r + 1)];
+          }
+        }
+        double* tmp = gnext; gnext = gcur; gcur = tmp;
+      }
+    }
+    /* chain through the row normalisation a = w_l/S, b = w_m/S, c = w_r/S (sum over the group done) */
+    double *dwl = J->dwl + wofs, *dwm = J->dwm + wofs, *dwr = J->dwr + wofs;
+    for (int64_t t = 0; t < L; ++t) {
+      for (int64_t r = 0; r < P; ++r) {
+        const int64_t p = pixel(dl[k], J->H, J->W, t, r);
+        double a, bb, cc, S;
+        if (taps(wl[p], wm[p], wr[p], r, P, J->flags, &a, &bb, &cc, &S)) {
+          snprintf(g_detail, sizeof g_detail, "row sum S<=0 at dir=%u b=%lld g=%lld t=%lld r=%lld", dl[k],
+                   (long long)b, (long long)g, (long long)t, (long long)r);
+          st = ORACLE_NONPOSITIVE_SUM;
+          goto done;
+        }
+        const int has_l = (r >= 1), has_r = (r <= P - 2);
+        if (J->flags & PRENORMALIZED) {
+          dwl[p] = has_l ? Da[p] : 0.0;
+          dwm[p] = Db[p];
+          dwr[p] = has_r ? Dc[p] : 0.0;
+        } else {
+          /* dL/dw_k = sum_j dL/dtap_j * dtap_j/dw_k = (Dtap_k - q) / S with q = a Da + b Db + c Dc */
+          const double q = a * Da[p] + bb * Db[p] + cc * Dc[p];
+          dwl[p] = has_l ? (Da[p] - q) / S : 0.0;
+          dwm[p] = (Db[p] - q) / S;
+          dwr[p] = has_r ? (Dc[p] - q) / S : 0.0;
+        }
+      }
+    }
+  }
+done:
+  free(gnext); free(gcur); free(Da); free(Db); free(Dc);
+  return st;
+}
+
+static void* worker(void* arg) {
+  job_t* J = (job_t*)arg;
+  for (;;) {
+    pthread_mutex_lock(&J->mu);
+    const int64_t u = J->next_unit++;
+    const int bad = J->status;
+    pthread_mutex_unlock(&J->mu);
+    if (bad || u >= J->B * J->G) break;
+    const int st = J->backward ? backward_unit(J, u / J->G, u % J->G) : forward_unit(J, u / J->G, u % J->G);
+    if (st) {
+      pthread_mutex_lock(&J->mu);
+      if (!J->status) J->status = st;
+      pthread_mutex_unlock(&J->mu);
+    }
+  }
+  return NULL;
+}
+
+static int run(job_t* J, int threads) {
+  if (J->B < 1 || J->C < 1 || J->H < 1 || J->W < 1 || J->G < 1 || J->C % J->G != 0 || J->dirs == 0 ||
+      J->dirs > 15 || (J->flags & ~PRENORMALIZED)) {
+    snprintf(g_detail, sizeof g_detail, "invalid argument");
+    return ORACLE_BAD_ARG;
+  }
+  if (threads < 1) threads = 1;
+  if (threads > 512) threads = 512;
+  J->next_unit = 0;
+  J->status = 0;
+  pthread_mutex_init(&J->mu, NULL);
+  pthread_t tid[512];
+  int started = 0;
+  for (int i = 1; i < threads; ++i)
+    if (pthread_create(&tid[started], NULL, worker, J) == 0) ++started;
+  worker(J);
+  for (int i = 0; i < started; ++i) pthread_join(tid[i], NULL);
+  pthread_mutex_destroy(&J->mu);
+  return J->status;
+}
+
+int gspn_oracle_fwd(const double* x, const double* wl, const double* wm, const double* wr, const double* lam,
+                    double* h, int64_t B, int64_t C, int64_t H, int64_t W, unsigned dirs, int64_t G,
+                    unsigned flags, int threads) {
+  if (!x || !wl || !wm || !wr || !lam || !h) return ORACLE_BAD_ARG;
+  job_t J;
+  memset(&J, 0, sizeof J);
+  J.x = x; J.wl = wl; J.wm = wm; J.wr = wr; J.lam = lam; J.hout = h;
+  J.B = B; J.C = C; J.H = H; J.W = W; J.G = G; J.dirs = dirs; J.flags = flags; J.backward = 0;
+  return run(&J, threads);
+}
+
+int gspn_oracle_bwd(const double* x, const double* wl, const double* wm, const double* wr, const double* lam,
+                    const double* h, const double* dh, double* dx, double* dwl, double* dwm, double* dwr,
+                    double* dlam, int64_t B, int64_t C, int64_t H, int64_t W, unsigned dirs, int64_t G,
+                    unsigned flags, int threads) {
+  if (!x || !wl || !wm || !wr || !lam || !h || !dh || !dx || !dwl || !dwm || !dwr || !dlam) return ORACLE_BAD_ARG;
+  job_t J;
+  memset(&J, 0, sizeof J);
+  J.x = x; J.wl = wl; J.wm = wm; J.wr = wr; J.lam = lam; J.h = h; J.dh = dh;
+  J.dx = dx; J.dwl = dwl; J.dwm = dwm; J.dwr = dwr; J.dlam = dlam;
+  J.B = B; J.C = C; J.H = H; J.W = W; J.G = G; J.dirs = dirs; J.flags = flags; J.backward = 1;
+  return run(&J, threads);
+}
