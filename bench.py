@@ -1,0 +1,419 @@
+#!/usr/bin/env python
+"""Benchmark of the GSPN line-scan hot path (fwd + bwd, all directions) on B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl ours|reference]
+
+One "step" = one gspn_fwd + one gspn_bwd call (every SURVEY.md §8(a) row) over one batch of synthetic,
+device-generated inputs already resident in HBM. Metric (BASELINE.json): algorithmic HBM GB/s of the
+fwd+bwd scan, (bytes_fwd + bytes_bwd) / device time, bytes per SURVEY.md §8(d). Multi-GPU: one process
+per GPU (torchrun), units (b, g) sharded across ranks with no data-path collective; by default each
+rank owns one full configuration's worth of units (weak scaling); --scaling strong splits the one
+configuration instead (config 5 then needs the dw all-reduce over NCCL). Timing: CUDA events on the
+launching stream, barrier + synchronize around the timed region, max over ranks.
+
+--impl reference times the fp64 CPU oracle (oracle/, the tier's reference arm) on bounded samples of
+the same workload on this host's cores; it never touches the GPU path.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "GSPN fwd+bwd scan GB/s vs B200 HBM peak; latency @1/2/4/8 GPUs"
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "traffic.json")
+L2_BYTES = 126 * 1024 * 1024
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="4")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--flags", type=int, default=0)
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(PEAKS_FILE) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        sms, maxs, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [v.strip() for v in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sms.append(float(f[1]))
+                maxs.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sms) if sms else None,
+                "sm_max_mhz": max(maxs) if maxs else None,
+                "reasons": sorted(reasons), "samples": len(sms)}
+
+
+def traffic_for(config_name: str, kernel: str):
+    try:
+        with open(TRAFFIC_FILE) as f:
+            t = json.load(f)
+        return t.get(config_name, {}).get(kernel)
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------------------------------ oracle arm
+
+def oracle_sample(cfg, seconds: float):
+    """Time the fp64 oracle (as it stands) on consecutive units of `cfg` until ~`seconds` of CPU work.
+    Returns (algorithmic bytes processed, wall seconds, threads, description)."""
+    import numpy as np
+
+    import oracle
+    import synth
+    from tests.parity_utils import unit_inputs
+
+    threads = oracle.default_threads()
+    U = cfg.B * cfg.G
+    Cg = cfg.C // cfg.G
+    unit_cfg = cfg.with_(B=1, C=Cg, G=1)
+    per_unit = unit_cfg.fwd_bytes() + unit_cfg.bwd_bytes()
+    # probe one unit single-threaded to size the batch
+    inp = unit_inputs(cfg, 0, 0)
+    f = {k: v[1] for k, v in inp.items()}
+    t0 = time.perf_counter()
+    h = oracle.fwd(f["x"], f["w_l"], f["w_m"], f["w_r"], f["lam"], cfg.dirs, 1, threads=1)
+    oracle.bwd(f["x"], f["w_l"], f["w_m"], f["w_r"], f["lam"], h, f["dh"], cfg.dirs, 1, threads=1)
+    t_unit = max(time.perf_counter() - t0, 1e-6)
+    n_units = int(max(1, min(U, round(seconds * threads / t_unit))))
+    # batch of consecutive units as one (B'=n, C=Cg, G=1) problem; inputs regenerated on the host
+    seed = synth.seed_for(cfg.cfg_id)
+    HW = cfg.H * cfg.W
+    D = cfg.D
+    x = synth.as_f64(synth.tensor(seed, "x", (n_units, Cg, cfg.H, cfg.W), cfg.dtype), cfg.dtype)
+    ws = [synth.as_f64(synth.tensor(seed, n, (D, n_units, 1, cfg.H, cfg.W), cfg.dtype, 0, n_units * HW,
+                                    U * HW), cfg.dtype) for n in ("w_l", "w_m", "w_r")]
+    lam = synth.as_f64(synth.tensor(seed, "lam", (D, n_units, Cg, cfg.H, cfg.W), cfg.dtype, 0,
+                                    n_units * Cg * HW, cfg.B * cfg.C * HW), cfg.dtype)
+    dh = synth.as_f64(synth.tensor(seed, "dh", (D, n_units, Cg, cfg.H, cfg.W), cfg.dtype, 0,
+                                   n_units * Cg * HW, cfg.B * cfg.C * HW), cfg.dtype)
+    t0 = time.perf_counter()
+    h = oracle.fwd(x, ws[0], ws[1], ws[2], lam, cfg.dirs, 1, threads=threads)
+    oracle.bwd(x, ws[0], ws[1], ws[2], lam, h, dh, cfg.dirs, 1, threads=threads)
+    wall = time.perf_counter() - t0
+    del np
+    desc = (f"{n_units} of {U} units (b,g) of config {cfg.name} (fwd+bwd, all {D} directions, fp64 oracle, "
+            f"{threads} threads); bytes counted at the I/O dtype")
+    return n_units * per_unit, wall, threads, desc
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    from synth.configs import get_config
+
+    cfg = get_config(args.config)
+    per_step = max(2.0, min(args.cpu_seconds, 60.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        oracle_sample(cfg, per_step / 2)
+    vals, walls, desc, threads = [], [], "", 1
+    for _ in range(args.steps):
+        b, w, threads, desc = oracle_sample(cfg, per_step)
+        vals.append(b / w / 1e9)
+        walls.append(w)
+    value = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": statistics.median(walls) * 1e3,
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded counter-based generator)",
+        "config": {"workload": f"config {cfg.name}: {cfg.text}", "sample": desc},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "oracle", "sample": desc},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------------------ our arm
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2512_07884_b200 as gspn
+    from synth.configs import get_config
+    from synth.device import make_inputs, shard_for
+
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        if rank == 0:
+            print(f"warning: WORLD_SIZE={world} but --gpus {args.gpus}; using WORLD_SIZE", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    base = get_config(args.config)
+    if args.scaling == "weak":
+        gcfg = base.with_(B=base.B * world)  # each rank owns one configuration's worth of units
+    else:
+        gcfg = base
+    sh = shard_for(gcfg, rank, world)
+    t = make_inputs(gcfg, dev, sh)
+    D = gcfg.D
+    dt_code = gspn.DTYPE_BF16 if gcfg.dtype == "bf16" else gspn.DTYPE_F32
+    h = torch.empty_like(t["lam"])
+    outs = (torch.empty_like(t["x"]), torch.empty_like(t["w_l"]), torch.empty_like(t["w_m"]),
+            torch.empty_like(t["w_r"]), torch.empty_like(t["lam"]))
+    wsb = gspn.workspace_bytes(sh.B, sh.C, gcfg.H, gcfg.W, gcfg.dirs, sh.G, dt_code)
+    ws = torch.empty(max(wsb, 16), dtype=torch.uint8, device=dev)
+    bytes_f = gspn.algorithmic_bytes(sh.B, sh.C, gcfg.H, gcfg.W, gcfg.dirs, sh.G, dt_code, False)
+    bytes_b = gspn.algorithmic_bytes(sh.B, sh.C, gcfg.H, gcfg.W, gcfg.dirs, sh.G, dt_code, True)
+    need_allreduce = sh.kind == "channels"  # one unit split by channel: dw partial sums must be reduced
+    work_bytes = sum(v.numel() * v.element_size() for v in t.values() if v is not None) + \
+        h.numel() * h.element_size() + sum(o.numel() * o.element_size() for o in outs)
+    flush = work_bytes < 4 * L2_BYTES
+    flush_buf = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=dev) if flush else None
+    stream = torch.cuda.current_stream(dev)
+    launches = {"fwd": 0, "bwd": 0}
+
+    def step(evs=None):
+        if evs:
+            evs[0].record(stream)
+        gspn.fwd(t["x"], t["w_l"], t["w_m"], t["w_r"], t["lam"], gcfg.dirs, sh.G, flags=args.flags, out=h)
+        launches["fwd"] = gspn.last_launch_count()
+        if evs:
+            evs[1].record(stream)
+        gspn.bwd(t["x"], t["w_l"], t["w_m"], t["w_r"], t["lam"], h, t["dh"], gcfg.dirs, sh.G, flags=args.flags,
+                 outs=outs, workspace=ws)
+        launches["bwd"] = gspn.last_launch_count()
+        if need_allreduce:
+            for o in outs[1:4]:
+                dist.all_reduce(o)  # bf16/fp32 in place; NCCL over NVLink
+        if evs:
+            evs[2].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+        if flush:
+            flush_buf.zero_()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    clocks = ClockSampler(local)
+    clocks.start()
+    evs_all = []
+    t_wall0 = time.perf_counter()
+    ev_start = torch.cuda.Event(enable_timing=True)
+    ev_end = torch.cuda.Event(enable_timing=True)
+    ev_start.record(stream)
+    for _ in range(args.steps):
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        step(evs)
+        evs_all.append(evs)
+        if flush:
+            flush_buf.zero_()
+    ev_end.record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    t_wall = time.perf_counter() - t_wall0
+    clk = clocks.stop()
+    f_ms = [e[0].elapsed_time(e[1]) for e in evs_all]
+    b_ms = [e[1].elapsed_time(e[2]) for e in evs_all]
+    step_ms = sum(f_ms[i] + b_ms[i] for i in range(args.steps)) / args.steps
+    region_ms = ev_start.elapsed_time(ev_end) / args.steps
+    mean_f, mean_b = sum(f_ms) / len(f_ms), sum(b_ms) / len(b_ms)
+    stats = torch.tensor([step_ms, mean_f, mean_b], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(stats, op=dist.ReduceOp.MAX)
+    step_ms, mean_f, mean_b = [float(v) for v in stats.tolist()]
+    total_bytes = (bytes_f + bytes_b) * world  # every rank processes the same amount of work
+    if args.scaling == "strong":
+        total_bytes = gcfg.fwd_bytes() + gcfg.bwd_bytes()
+
+    # ---- end to end through the public API with host buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, gspn, gcfg, sh, t, h, outs, ws, dev, world, dist)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            b_cpu, w_cpu, thr, desc = oracle_sample(base, args.cpu_seconds)
+            cpu = {"value": b_cpu / w_cpu / 1e9, "unit": "GB/s", "cores": thr, "kind": "oracle", "sample": desc}
+        except Exception as ex:  # the baseline is reported, never required
+            cpu = {"value": None, "unit": "GB/s", "cores": None, "kind": "oracle", "sample": f"failed: {ex}"}
+
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank != 0:
+        return 0
+    peak, peak_src = peaks()
+    dominant = "bwd" if bytes_b / max(mean_b, 1e-9) <= bytes_f / max(mean_f, 1e-9) or mean_b >= mean_f else "fwd"
+    dom_ms = mean_b if dominant == "bwd" else mean_f
+    dom_bytes = bytes_b if dominant == "bwd" else bytes_f
+    achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
+    value = total_bytes / (step_ms * 1e-3) / 1e9
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "GB/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": step_ms,
+        "higher_is_better": True,
+        "scaling": args.scaling,
+        "vs_baseline": None,
+        "dtype": gcfg.dtype,
+        "data": "synthetic (seeded counter-based generator, device-generated; SURVEY.md §8(d) distributions)",
+        "config": {
+            "workload": f"config {base.name} (BASELINE.json configs[{base.cfg_id - 1}]): {base.text}",
+            "B": gcfg.B, "C": gcfg.C, "G": gcfg.G, "H": gcfg.H, "W": gcfg.W, "dirs": gcfg.dirs,
+            "per_rank": {"B": sh.B, "C": sh.C, "G": sh.G, "kind": sh.kind},
+            "fwd_ms": mean_f, "bwd_ms": mean_b, "region_ms_per_step": region_ms,
+            "fwd_gbs": bytes_f / (mean_f * 1e-3) / 1e9, "bwd_gbs": bytes_b / (mean_b * 1e-3) / 1e9,
+            "algorithmic_bytes_per_step": total_bytes,
+            "l2": ("L2 flushed (2x126 MB memset) between steps, outside the event pairs" if flush else
+                   f"inputs+outputs {work_bytes / 1e9:.1f} GB > 126 MB L2, no flush"),
+            "path": gspn.last_path(),
+            "wall_s_timed_region": t_wall,
+        },
+        "roofline": {
+            "bound": "hbm", "kernel": f"gspn_{dominant} ({gspn.last_path()} path)",
+            "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "peak_source": peak_src,
+            "traffic": traffic_for(base.name, dominant),
+            "algorithmic_bytes_per_launch": dom_bytes,
+        },
+        "clocks": clk,
+        "gpu_launches": args.steps * (launches["fwd"] + launches["bwd"]),
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_e2e(args, gspn, cfg, sh, t, h, outs, ws, dev, world, dist):
+    """Same metric through the public API with pinned HOST buffers: every step copies its inputs
+    host->device, runs fwd + bwd, and copies every output device->host (CUDA events on the stream)."""
+    import torch
+
+    stream = torch.cuda.current_stream(dev)
+    names = ["x", "w_l", "w_m", "w_r", "lam", "dh"]
+    host_in = {}
+    for n in names:
+        host_in[n] = torch.empty(t[n].shape, dtype=t[n].dtype, pin_memory=True)
+        host_in[n].copy_(t[n])
+    host_out = [torch.empty(o.shape, dtype=o.dtype, pin_memory=True) for o in (h, *outs)]
+    h2d = sum(v.numel() * v.element_size() for v in host_in.values())
+    d2h = sum(v.numel() * v.element_size() for v in host_out)
+
+    def step():
+        for n in names:
+            t[n].copy_(host_in[n], non_blocking=True)
+        gspn.fwd(t["x"], t["w_l"], t["w_m"], t["w_r"], t["lam"], cfg.dirs, sh.G, out=h)
+        gspn.bwd(t["x"], t["w_l"], t["w_m"], t["w_r"], t["lam"], h, t["dh"], cfg.dirs, sh.G, outs=outs, workspace=ws)
+        for ho, o in zip(host_out, (h, *outs)):
+            ho.copy_(o, non_blocking=True)
+
+    step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n = max(1, args.e2e_steps)
+    e0.record(stream)
+    for _ in range(n):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = torch.tensor([e0.elapsed_time(e1) / n], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item())
+    total = (cfg.fwd_bytes() + cfg.bwd_bytes()) if args.scaling == "strong" else \
+        (gspn.algorithmic_bytes(sh.B, sh.C, cfg.H, cfg.W, cfg.dirs, sh.G,
+                                gspn.DTYPE_BF16 if cfg.dtype == "bf16" else gspn.DTYPE_F32, False) * 3 * world)
+    return {"value": total / (ms * 1e-3) / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d * world,
+            "d2h_bytes_per_step": d2h * world, "ms_per_step": ms, "steps": n,
+            "note": "pinned host buffers; H2D of x,w,lam,dh + fwd + bwd + D2H of h,dx,dw,dlam on one stream"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

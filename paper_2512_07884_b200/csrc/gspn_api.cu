@@ -1,0 +1,266 @@
+// gspn_api.cu — the C ABI declared in include/gspn.h: host-side validation (before any CUDA call),
+// workspace carving, path selection (TMA streaming fast path, else the generic path) and launch.
+#include <cstdio>
+#include <cstring>
+#include <exception>
+
+#include "gspn_internal.h"
+
+namespace {
+
+thread_local char t_detail[512] = "";
+thread_local const char* t_path = "none";
+thread_local int t_launches = 0;
+
+gspn_status_t fail(gspn_status_t st, const char* fmt, const char* what, long long v = 0) {
+  snprintf(t_detail, sizeof t_detail, fmt, what, v);
+  return st;
+}
+
+int popcount4(uint32_t d) { return (d & 1) + ((d >> 1) & 1) + ((d >> 2) & 1) + ((d >> 3) & 1); }
+
+struct Span {
+  const char* name;
+  uintptr_t lo, hi;
+};
+
+bool overlap(const Span& a, const Span& b) { return a.lo < b.hi && b.lo < a.hi; }
+
+constexpr size_t kAlign = 256;
+size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
+
+// Common dimension checks. Returns GSPN_OK or GSPN_ERR_INVALID_ARG with the detail set.
+gspn_status_t check_dims(int64_t B, int64_t C, int64_t H, int64_t W, uint32_t dirs, int64_t G, gspn_dtype_t dt,
+                         uint32_t flags) {
+  if (B < 1) return fail(GSPN_ERR_INVALID_ARG, "%s must be >= 1 (got %lld)", "B", B);
+  if (C < 1) return fail(GSPN_ERR_INVALID_ARG, "%s must be >= 1 (got %lld)", "C", C);
+  if (H < 1) return fail(GSPN_ERR_INVALID_ARG, "%s must be >= 1 (got %lld)", "H", H);
+  if (W < 1) return fail(GSPN_ERR_INVALID_ARG, "%s must be >= 1 (got %lld)", "W", W);
+  if (G < 1) return fail(GSPN_ERR_INVALID_ARG, "%s must be >= 1 (got %lld)", "groups", G);
+  if (C % G != 0) return fail(GSPN_ERR_INVALID_ARG, "%s: C %% groups != 0 (groups=%lld)", "groups", G);
+  if (dirs == 0 || dirs > 15) return fail(GSPN_ERR_INVALID_ARG, "%s must be in [1, 15] (got %lld)", "dirs", dirs);
+  if (dt != GSPN_F32 && dt != GSPN_BF16) return fail(GSPN_ERR_INVALID_ARG, "%s unknown (%lld)", "dtype", (long long)dt);
+  if (flags & ~(GSPN_FLAG_PRENORMALIZED | GSPN_FLAG_FORCE_GENERIC))
+    return fail(GSPN_ERR_INVALID_ARG, "%s has unknown bits (0x%llx)", "flags", flags);
+  // Overflow guard: the largest tensor (D*B*C*H*W elements) must stay far below 2^62 bytes, and the
+  // chain count must fit a 1-D grid.
+  const double n = (double)popcount4(dirs) * (double)B * (double)C * (double)H * (double)W * 4.0;
+  if (n >= 4.0e18) return fail(GSPN_ERR_INVALID_ARG, "%s: tensor too large (%lld elements per plane)", "shape", H * W);
+  if ((double)popcount4(dirs) * (double)B * (double)C >= 2147483647.0)
+    return fail(GSPN_ERR_INVALID_ARG, "%s: D*B*C chains exceed 2^31-1 (B*C=%lld)", "shape", B * C);
+  return GSPN_OK;
+}
+
+gspn_status_t check_ptr(const void* p, const char* name) {
+  if (p == nullptr) {
+    snprintf(t_detail, sizeof t_detail, "%s is NULL", name);
+    return GSPN_ERR_INVALID_ARG;
+  }
+  if (reinterpret_cast<uintptr_t>(p) % 16 != 0) {
+    snprintf(t_detail, sizeof t_detail, "%s is not 16-byte aligned", name);
+    return GSPN_ERR_INVALID_ARG;
+  }
+  return GSPN_OK;
+}
+
+gspn_status_t check_aliasing(const Span* outs, int n_out, const Span* ins, int n_in) {
+  for (int i = 0; i < n_out; ++i) {
+    for (int j = 0; j < n_in; ++j)
+      if (overlap(outs[i], ins[j])) {
+        snprintf(t_detail, sizeof t_detail, "output %s overlaps input %s", outs[i].name, ins[j].name);
+        return GSPN_ERR_INVALID_ARG;
+      }
+    for (int j = i + 1; j < n_out; ++j)
+      if (overlap(outs[i], outs[j])) {
+        snprintf(t_detail, sizeof t_detail, "output %s overlaps output %s", outs[i].name, outs[j].name);
+        return GSPN_ERR_INVALID_ARG;
+      }
+  }
+  return GSPN_OK;
+}
+
+Span span(const char* name, const void* p, size_t bytes) {
+  return Span{name, reinterpret_cast<uintptr_t>(p), reinterpret_cast<uintptr_t>(p) + bytes};
+}
+
+void fill_dirs(gspn::ScanParams& p, uint32_t dirs) {
+  int k = 0;
+  const uint32_t order[4] = {GSPN_DIR_T2B, GSPN_DIR_B2T, GSPN_DIR_L2R, GSPN_DIR_R2L};
+  for (int i = 0; i < 4; ++i)
+    if (dirs & order[i]) p.dirbit[k++] = order[i];
+  for (; k < 4; ++k) p.dirbit[k] = 0;
+}
+
+size_t generic_workspace(int64_t B, int64_t C, int64_t H, int64_t W, int64_t D, int64_t G) {
+  size_t n = align_up((size_t)(B * C * H * W) * sizeof(float));                  // dx_acc
+  if (G < C) n += 3 * align_up((size_t)(D * B * G * H * W) * sizeof(float));     // dwa_l/m/r
+  return n;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* gspn_status_string(gspn_status_t s) {
+  switch (s) {
+    case GSPN_OK: return "GSPN_OK";
+    case GSPN_ERR_INVALID_ARG: return "GSPN_ERR_INVALID_ARG";
+    case GSPN_ERR_UNSUPPORTED: return "GSPN_ERR_UNSUPPORTED";
+    case GSPN_ERR_CUDA: return "GSPN_ERR_CUDA";
+    case GSPN_ERR_INTERNAL: return "GSPN_ERR_INTERNAL";
+  }
+  return "GSPN_ERR_UNKNOWN";
+}
+
+const char* gspn_last_error_detail(void) { return t_detail; }
+const char* gspn_last_path(void) { return t_path; }
+int gspn_last_launch_count(void) { return t_launches; }
+
+double gspn_algorithmic_bytes(int64_t B, int64_t C, int64_t H, int64_t W, uint32_t dirs, int64_t groups,
+                              gspn_dtype_t dtype, int backward) {
+  if (check_dims(B, C, H, W, dirs, groups, dtype, 0) != GSPN_OK) return 0.0;
+  const double s = dtype == GSPN_BF16 ? 2.0 : 4.0;
+  const double D = popcount4(dirs);
+  const double N = (double)B * C * H * W, Nw = (double)B * groups * H * W;
+  const double fwd = s * (N * (1.0 + 2.0 * D) + 3.0 * D * Nw);
+  return backward ? 2.0 * fwd : fwd;
+}
+
+size_t gspn_bwd_workspace_bytes(int64_t B, int64_t C, int64_t H, int64_t W, uint32_t dirs, int64_t groups,
+                                gspn_dtype_t dtype) {
+  if (check_dims(B, C, H, W, dirs, groups, dtype, 0) != GSPN_OK) return 0;
+  const int64_t D = popcount4(dirs);
+  size_t a = generic_workspace(B, C, H, W, D, groups);
+  size_t b = gspn::stream_bwd_workspace_bytes(B, C, H, W, D, groups, dtype);
+  return a > b ? a : b;
+}
+
+gspn_status_t gspn_fwd(const void* x, const void* w_l, const void* w_m, const void* w_r, const void* lam, void* h,
+                       int64_t B, int64_t C, int64_t H, int64_t W, uint32_t dirs, int64_t groups,
+                       gspn_dtype_t dtype, uint32_t flags, gspn_stream_t stream) {
+  try {
+    gspn_status_t st;
+    if ((st = check_ptr(x, "x")) || (st = check_ptr(w_l, "w_l")) || (st = check_ptr(w_m, "w_m")) ||
+        (st = check_ptr(w_r, "w_r")) || (st = check_ptr(lam, "lam")) || (st = check_ptr(h, "h")))
+      return st;
+    if ((st = check_dims(B, C, H, W, dirs, groups, dtype, flags))) return st;
+    const int64_t D = popcount4(dirs);
+    const size_t s = dtype == GSPN_BF16 ? 2 : 4;
+    const size_t nx = (size_t)(B * C * H * W) * s, nl = (size_t)D * nx, nw = (size_t)(D * B * groups * H * W) * s;
+    const Span ins[5] = {span("x", x, nx), span("w_l", w_l, nw), span("w_m", w_m, nw), span("w_r", w_r, nw),
+                         span("lam", lam, nl)};
+    const Span outs[1] = {span("h", h, nl)};
+    if ((st = check_aliasing(outs, 1, ins, 5))) return st;
+    if (H > gspn::generic_max_P() || W > gspn::generic_max_P()) {
+      snprintf(t_detail, sizeof t_detail, "H or W above %lld is not tiled", (long long)gspn::generic_max_P());
+      return GSPN_ERR_UNSUPPORTED;
+    }
+
+    gspn::ScanParams p;
+    memset(&p, 0, sizeof p);
+    p.x = x; p.wl = w_l; p.wm = w_m; p.wr = w_r; p.lam = lam; p.hout = h;
+    p.B = B; p.C = C; p.H = H; p.W = W; p.G = groups; p.D = D; p.flags = flags;
+    fill_dirs(p, dirs);
+    cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+    int launches = 0;
+    bool handled = false;
+    cudaError_t e = cudaSuccess;
+    if (!(flags & GSPN_FLAG_FORCE_GENERIC)) e = gspn::launch_fwd_stream(p, dtype, cs, &launches, &handled);
+    if (e == cudaSuccess && !handled) e = gspn::launch_fwd_generic(p, dtype, cs, &launches);
+    if (e != cudaSuccess) {
+      snprintf(t_detail, sizeof t_detail, "CUDA error: %s", cudaGetErrorString(e));
+      return GSPN_ERR_CUDA;
+    }
+    t_path = handled ? "stream" : "generic";
+    t_launches = launches;
+    return GSPN_OK;
+  } catch (const std::exception& ex) {
+    snprintf(t_detail, sizeof t_detail, "internal: %s", ex.what());
+    return GSPN_ERR_INTERNAL;
+  } catch (...) {
+    snprintf(t_detail, sizeof t_detail, "internal error");
+    return GSPN_ERR_INTERNAL;
+  }
+}
+
+gspn_status_t gspn_bwd(const void* x, const void* w_l, const void* w_m, const void* w_r, const void* lam,
+                       const void* h, const void* dh, void* dx, void* dw_l, void* dw_m, void* dw_r, void* dlam,
+                       int64_t B, int64_t C, int64_t H, int64_t W, uint32_t dirs, int64_t groups,
+                       gspn_dtype_t dtype, uint32_t flags, void* workspace, size_t workspace_bytes,
+                       gspn_stream_t stream) {
+  try {
+    gspn_status_t st;
+    if ((st = check_ptr(x, "x")) || (st = check_ptr(w_l, "w_l")) || (st = check_ptr(w_m, "w_m")) ||
+        (st = check_ptr(w_r, "w_r")) || (st = check_ptr(lam, "lam")) || (st = check_ptr(h, "h")) ||
+        (st = check_ptr(dh, "dh")) || (st = check_ptr(dx, "dx")) || (st = check_ptr(dw_l, "dw_l")) ||
+        (st = check_ptr(dw_m, "dw_m")) || (st = check_ptr(dw_r, "dw_r")) || (st = check_ptr(dlam, "dlam")))
+      return st;
+    if ((st = check_dims(B, C, H, W, dirs, groups, dtype, flags))) return st;
+    const int64_t D = popcount4(dirs);
+    const size_t need = gspn_bwd_workspace_bytes(B, C, H, W, dirs, groups, dtype);
+    if (need > 0) {
+      if ((st = check_ptr(workspace, "workspace"))) return st;
+      if (workspace_bytes < need) {
+        snprintf(t_detail, sizeof t_detail, "workspace too small: %zu < %zu bytes", workspace_bytes, need);
+        return GSPN_ERR_INVALID_ARG;
+      }
+    }
+    const size_t s = dtype == GSPN_BF16 ? 2 : 4;
+    const size_t nx = (size_t)(B * C * H * W) * s, nl = (size_t)D * nx, nw = (size_t)(D * B * groups * H * W) * s;
+    const Span ins[7] = {span("x", x, nx),   span("w_l", w_l, nw), span("w_m", w_m, nw), span("w_r", w_r, nw),
+                         span("lam", lam, nl), span("h", h, nl),     span("dh", dh, nl)};
+    Span outs[6] = {span("dx", dx, nx),     span("dw_l", dw_l, nw), span("dw_m", dw_m, nw),
+                    span("dw_r", dw_r, nw), span("dlam", dlam, nl), span("workspace", workspace, need)};
+    if ((st = check_aliasing(outs, need > 0 ? 6 : 5, ins, 7))) return st;
+    if (H > gspn::generic_max_P() || W > gspn::generic_max_P()) {
+      snprintf(t_detail, sizeof t_detail, "H or W above %lld is not tiled", (long long)gspn::generic_max_P());
+      return GSPN_ERR_UNSUPPORTED;
+    }
+
+    gspn::ScanParams p;
+    memset(&p, 0, sizeof p);
+    p.x = x; p.wl = w_l; p.wm = w_m; p.wr = w_r; p.lam = lam; p.h = h; p.dh = dh;
+    p.dx = dx; p.dwl = dw_l; p.dwm = dw_m; p.dwr = dw_r; p.dlam = dlam;
+    p.B = B; p.C = C; p.H = H; p.W = W; p.G = groups; p.D = D; p.flags = flags;
+    fill_dirs(p, dirs);
+    cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+    int launches = 0;
+    bool handled = false;
+    cudaError_t e = cudaSuccess;
+    if (!(flags & GSPN_FLAG_FORCE_GENERIC)) {
+      // the streaming path carves the workspace itself
+      p.ws = workspace;
+      p.ws_bytes = workspace_bytes;
+      e = gspn::launch_bwd_stream(p, dtype, cs, &launches, &handled);
+    }
+    if (e == cudaSuccess && !handled) {
+      char* ws = static_cast<char*>(workspace);
+      p.dx_acc = reinterpret_cast<float*>(ws);
+      size_t off = align_up((size_t)(B * C * H * W) * sizeof(float));
+      const size_t zero_bytes = generic_workspace(B, C, H, W, D, groups);
+      if (groups < C) {
+        const size_t nwb = align_up((size_t)(D * B * groups * H * W) * sizeof(float));
+        p.dwa_l = reinterpret_cast<float*>(ws + off); off += nwb;
+        p.dwa_m = reinterpret_cast<float*>(ws + off); off += nwb;
+        p.dwa_r = reinterpret_cast<float*>(ws + off); off += nwb;
+      }
+      e = cudaMemsetAsync(workspace, 0, zero_bytes, cs);
+      if (e == cudaSuccess) e = gspn::launch_bwd_generic(p, dtype, cs, &launches);
+    }
+    if (e != cudaSuccess) {
+      snprintf(t_detail, sizeof t_detail, "CUDA error: %s", cudaGetErrorString(e));
+      return GSPN_ERR_CUDA;
+    }
+    t_path = handled ? "stream" : "generic";
+    t_launches = launches;
+    return GSPN_OK;
+  } catch (const std::exception& ex) {
+    snprintf(t_detail, sizeof t_detail, "internal: %s", ex.what());
+    return GSPN_ERR_INTERNAL;
+  } catch (...) {
+    snprintf(t_detail, sizeof t_detail, "internal error");
+    return GSPN_ERR_INTERNAL;
+  }
+}
+
+}  // extern "C"

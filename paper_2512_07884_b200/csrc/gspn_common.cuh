@@ -1,0 +1,109 @@
+// gspn_common.cuh — shared device-side definitions of the CUDA path (never used by oracle/).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/gspn.h"
+
+namespace gspn {
+
+// Parameters of one gspn_fwd / gspn_bwd call as seen by every kernel (passed by value).
+struct ScanParams {
+  const void* x;    // [B,C,H,W]
+  const void* wl;   // [D,B,G,H,W]
+  const void* wm;
+  const void* wr;
+  const void* lam;  // [D,B,C,H,W]
+  const void* h;    // bwd: saved forward output [D,B,C,H,W]
+  const void* dh;   // bwd: upstream gradient   [D,B,C,H,W]
+  void* hout;       // fwd output [D,B,C,H,W]
+  void* dx;         // bwd outputs
+  void* dwl;
+  void* dwm;
+  void* dwr;
+  void* dlam;
+  float* dx_acc;    // workspace: fp32 sum over directions [B,C,H,W]
+  float* dwa_l;     // workspace: fp32 group sums of the normalised-tap gradients [D,B,G,H,W] (G < C)
+  float* dwa_m;
+  float* dwa_r;
+  unsigned int* counters;  // workspace: completion counters (fast path)
+  void* ws;                // bwd: caller workspace (carved by the launcher of the chosen path)
+  size_t ws_bytes;
+  int64_t B, C, H, W, G, D;
+  uint32_t dirbit[4];      // direction bit (GSPN_DIR_*) of slab k
+  uint32_t flags;
+};
+
+// Scan geometry of one direction inside an H x W plane: canonical offset of (t, r) is
+// base + t * ts + r * rs (gspn.h direction table; R4).
+struct DirGeom {
+  int64_t L, P, base, ts, rs;
+};
+
+__host__ __device__ __forceinline__ DirGeom dir_geom(uint32_t dirbit, int64_t H, int64_t W) {
+  DirGeom g;
+  switch (dirbit) {
+    case GSPN_DIR_T2B: g.L = H; g.P = W; g.base = 0;           g.ts = W;  g.rs = 1; break;
+    case GSPN_DIR_B2T: g.L = H; g.P = W; g.base = (H - 1) * W; g.ts = -W; g.rs = 1; break;
+    case GSPN_DIR_L2R: g.L = W; g.P = H; g.base = 0;           g.ts = 1;  g.rs = W; break;
+    default:           g.L = W; g.P = H; g.base = W - 1;       g.ts = -1; g.rs = W; break;  // R2L
+  }
+  return g;
+}
+
+__device__ __forceinline__ bool is_vertical(uint32_t dirbit) {
+  return dirbit == GSPN_DIR_T2B || dirbit == GSPN_DIR_B2T;
+}
+
+template <typename T> __device__ __forceinline__ float to_f(T v);
+template <> __device__ __forceinline__ float to_f<float>(float v) { return v; }
+template <> __device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
+
+template <typename T> __device__ __forceinline__ T from_f(float v);
+template <> __device__ __forceinline__ float from_f<float>(float v) { return v; }
+template <> __device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+
+// Row-normalised taps of one position (R1/R2): out-of-range taps dropped,
+// the in-range ones divided by their sum S. inv = 1/S (1 when the caller pre-normalised).
+struct Taps {
+  float a, b, c, inv;
+};
+
+__device__ __forceinline__ Taps make_taps(float wl, float wm, float wr, bool has_l, bool has_r, bool prenorm) {
+  Taps t;
+  const float l = has_l ? wl : 0.f;
+  const float r = has_r ? wr : 0.f;
+  if (prenorm) {
+    t.a = l; t.b = wm; t.c = r; t.inv = 1.f;
+  } else {
+    t.inv = __frcp_rn(wm + l + r);
+    t.a = l * t.inv; t.b = wm * t.inv; t.c = r * t.inv;
+  }
+  return t;
+}
+
+// Chain rule through the row normalisation (a, b, c) = (l, m, r) / S, S = l + m + r over the
+// in-range raw taps (out-of-range taps are constant 0): with q = a Da + b Db + c Dc,
+//   dw_l = (Da - q)/S = ((m + r) Da - m Db - r Dc) / S^2
+//   dw_m = (Db - q)/S = ((l + r) Db - l Da - r Dc) / S^2
+//   dw_r = (Dc - q)/S = ((l + m) Dc - l Da - m Db) / S^2
+// The right-hand forms avoid the cancellation of q against D and are exactly 0 when only one tap is
+// in range (P = 1). With pre-normalised taps the map is the identity on the in-range taps.
+__device__ __forceinline__ void jacobian(float wl, float wm, float wr, bool has_l, bool has_r, bool prenorm,
+                                         float Da, float Db, float Dc, float& dwl, float& dwm, float& dwr) {
+  const float l = has_l ? wl : 0.f;
+  const float r = has_r ? wr : 0.f;
+  if (prenorm) {
+    dwl = has_l ? Da : 0.f; dwm = Db; dwr = has_r ? Dc : 0.f;
+    return;
+  }
+  const float inv = __frcp_rn(wm + l + r);
+  const float inv2 = inv * inv;
+  dwl = has_l ? fmaf(wm + r, Da, -fmaf(wm, Db, r * Dc)) * inv2 : 0.f;
+  dwm = fmaf(l + r, Db, -fmaf(l, Da, r * Dc)) * inv2;
+  dwr = has_r ? fmaf(l + wm, Dc, -fmaf(l, Da, wm * Db)) * inv2 : 0.f;
+}
+
+}  // namespace gspn

@@ -1,0 +1,19 @@
+// gspn_internal.h — host-side interfaces between the C-ABI front end and the kernel launchers.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "gspn_common.cuh"
+
+namespace gspn {
+
+int64_t generic_max_P();
+cudaError_t launch_fwd_generic(const ScanParams& p, gspn_dtype_t dt, cudaStream_t s, int* launches);
+cudaError_t launch_bwd_generic(const ScanParams& p, gspn_dtype_t dt, cudaStream_t s, int* launches);
+
+// Fast TMA-streaming path (gspn_stream.cu). *handled = false when the shape is not eligible.
+cudaError_t launch_fwd_stream(const ScanParams& p, gspn_dtype_t dt, cudaStream_t s, int* launches, bool* handled);
+cudaError_t launch_bwd_stream(const ScanParams& p, gspn_dtype_t dt, cudaStream_t s, int* launches, bool* handled);
+size_t stream_bwd_workspace_bytes(int64_t B, int64_t C, int64_t H, int64_t W, int64_t D, int64_t G, gspn_dtype_t dt);
+
+}  // namespace gspn

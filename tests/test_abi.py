@@ -1,0 +1,120 @@
+"""C ABI: the library loads on a CPU-only box, exports every symbol include/gspn.h declares, and every
+validation error path returns the right status before any CUDA call (no device needed)."""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+import paper_2512_07884_b200 as gspn
+from paper_2512_07884_b200.build import LIBGSPN, ROOT
+
+HEADER = os.path.join(ROOT, "include", "gspn.h")
+A = 0x10000  # fake, 16-byte aligned, never dereferenced (validation fails first)
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:[\w\s\*]+?)\b(gspn_\w+)\s*\(", src, re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    names = declared_functions()
+    assert {"gspn_fwd", "gspn_bwd", "gspn_bwd_workspace_bytes", "gspn_status_string",
+            "gspn_last_error_detail", "gspn_algorithmic_bytes"} <= set(names)
+    out = subprocess.check_output(["nm", "-D", "--defined-only", LIBGSPN]).decode()
+    exported = set(re.findall(r"\bT (gspn_\w+)", out))
+    missing = [n for n in names if n not in exported]
+    assert not missing, f"declared but not exported: {missing}"
+    L = gspn.lib()
+    for n in names:
+        assert hasattr(L, n)
+
+
+def fwd_call(**kw):
+    a = dict(x=A, wl=A, wm=A, wr=A, lam=A, h=A + (1 << 30), B=1, C=4, H=8, W=8, dirs=0xF, G=4, dt=1, flags=0)
+    a.update(kw)
+    return gspn.lib().gspn_fwd(a["x"], a["wl"], a["wm"], a["wr"], a["lam"], a["h"], a["B"], a["C"], a["H"], a["W"],
+                               a["dirs"], a["G"], a["dt"], a["flags"], None)
+
+
+def detail():
+    return gspn.lib().gspn_last_error_detail().decode()
+
+
+@pytest.mark.parametrize("kw,needle", [
+    (dict(x=None), "x is NULL"),
+    (dict(lam=None), "lam is NULL"),
+    (dict(h=None), "h is NULL"),
+    (dict(wm=A + 8), "w_m is not 16-byte aligned"),
+    (dict(B=0), "B must be"),
+    (dict(C=-1), "C must be"),
+    (dict(H=0), "H must be"),
+    (dict(W=0), "W must be"),
+    (dict(G=0), "groups must be"),
+    (dict(G=3), "C % groups"),
+    (dict(dirs=0), "dirs"),
+    (dict(dirs=16), "dirs"),
+    (dict(flags=0x80), "flags"),
+    (dict(dt=7), "dtype"),
+])
+def test_fwd_validation(kw, needle):
+    assert fwd_call(**kw) == 1
+    assert needle in detail()
+
+
+def test_fwd_aliasing_rejected():
+    # h overlaps lam
+    assert fwd_call(lam=A + (1 << 20), h=A + (1 << 20) + 1024) == 1
+    assert "overlaps" in detail()
+
+
+def bwd_call(ws=A + (40 << 30), ws_bytes=1 << 40, **kw):
+    base = 1 << 30
+    p = dict(x=A, wl=A + base, wm=A + 2 * base, wr=A + 3 * base, lam=A + 4 * base, h=A + 5 * base,
+             dh=A + 6 * base, dx=A + 7 * base, dwl=A + 8 * base, dwm=A + 9 * base, dwr=A + 10 * base,
+             dlam=A + 11 * base)
+    p.update(kw)
+    return gspn.lib().gspn_bwd(p["x"], p["wl"], p["wm"], p["wr"], p["lam"], p["h"], p["dh"], p["dx"], p["dwl"],
+                               p["dwm"], p["dwr"], p["dlam"], 2, 4, 16, 16, 0xF, 2, 1, 0, ws, ws_bytes, None)
+
+
+def test_bwd_validation():
+    assert bwd_call(dh=None) == 1 and "dh is NULL" in detail()
+    assert bwd_call(dlam=A + 3) == 1 and "dlam is not 16-byte aligned" in detail()
+    assert bwd_call(ws=None) == 1 and "workspace is NULL" in detail()
+    assert bwd_call(ws_bytes=16) == 1 and "workspace too small" in detail()
+    assert bwd_call(dx=A + 4 * (1 << 30)) == 1 and "overlaps" in detail()  # dx on lam
+    assert bwd_call(dwm=A + 8 * (1 << 30)) == 1 and "overlaps" in detail()  # dw_m on dw_l
+
+
+def test_workspace_and_bytes():
+    L = gspn.lib()
+    assert L.gspn_bwd_workspace_bytes(4, 320, 512, 512, 0xF, 320, 1) > 0
+    assert L.gspn_bwd_workspace_bytes(4, 320, 512, 512, 0xF, 3, 1) == 0  # invalid groups
+    # config 4 fwd+bwd = 42,278.58 MB, fwd = s[N(1+2D) + 3 D N_w]
+    f = L.gspn_algorithmic_bytes(4, 320, 512, 512, 0xF, 320, 1, 0)
+    b = L.gspn_algorithmic_bytes(4, 320, 512, 512, 0xF, 320, 1, 1)
+    assert abs((f + b) / 1e6 - 42278.58) < 0.01
+    assert b == 2 * f
+    # config 5 (G = 1): 9,361.69 MB
+    f5 = L.gspn_algorithmic_bytes(1, 40, 2048, 2048, 0xF, 1, 1, 0)
+    assert abs(3 * f5 / 1e6 - 9361.69) < 0.01
+
+
+def test_status_strings():
+    L = gspn.lib()
+    assert L.gspn_status_string(0) == b"GSPN_OK"
+    assert L.gspn_status_string(2) == b"GSPN_ERR_UNSUPPORTED"
+
+
+def test_python_binding_refuses_cpu_tensors():
+    torch = pytest.importorskip("torch")
+    x = torch.zeros(1, 2, 4, 4)
+    w = torch.ones(1, 1, 2, 4, 4)
+    lam = torch.ones(1, 1, 2, 4, 4)
+    with pytest.raises(ValueError, match="CUDA tensor"):
+        gspn.fwd(x, w, w, w, lam, dirs=1, groups=2)

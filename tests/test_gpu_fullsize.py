@@ -1,0 +1,158 @@
+"""GPU parity at BASELINE.json's full sizes, in the launch configuration bench.py times (device-generated
+inputs, one fwd and one bwd call through the C ABI, the bwd consuming the GPU's own h).
+
+The oracle recomputes sampled units (b, g) — all their channels and directions — from host-regenerated
+inputs (synth, flat indices of the unsharded tensors), and the device generator is checked bit-exact
+against the host generator on the same samples. Whole-tensor properties that hold at any size
+(adjoint dot test, Euler identity of the normalisation) cover everything the samples do not.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2512_07884_b200 as gspn
+import synth
+from synth.configs import get_config
+from synth.device import make_inputs
+from tests.parity_utils import TOL, from_torch, normwise, unit_inputs
+
+pytestmark = pytest.mark.gpu
+NTHREADS = oracle.default_threads()
+
+
+def _run(cfg, device):
+    t = make_inputs(cfg, device)
+    h = gspn.fwd(t["x"], t["w_l"], t["w_m"], t["w_r"], t["lam"], cfg.dirs, cfg.G)
+    g = gspn.bwd(t["x"], t["w_l"], t["w_m"], t["w_r"], t["lam"], h, t["dh"], cfg.dirs, cfg.G)
+    return t, h, g
+
+
+def _sample_units(cfg, n):
+    U = cfg.B * cfg.G
+    picks = {0, U - 1}
+    rng = np.random.default_rng(cfg.cfg_id)
+    while len(picks) < min(n, U):
+        picks.add(int(rng.integers(0, U)))
+    return sorted(picks)
+
+
+def _check_unit(cfg, t, h, grads, u):
+    b, g = divmod(u, cfg.G)
+    Cg = cfg.C // cfg.G
+    c0 = g * Cg
+    inp = unit_inputs(cfg, b, g)
+    # the device generator reproduces the host generator bit for bit on this unit
+    x_dev = t["x"][b, c0:c0 + Cg].contiguous().cpu()
+    x_host = inp["x"][0][0]
+    if cfg.dtype == "bf16":
+        assert np.array_equal(x_dev.view(dtype=__import__("torch").int16).numpy().view(np.uint16), x_host)
+    else:
+        assert np.array_equal(x_dev.numpy(), x_host)
+    f = {k: v[1] for k, v in inp.items()}
+    h_ref = oracle.fwd(f["x"], f["w_l"], f["w_m"], f["w_r"], f["lam"], cfg.dirs, 1, threads=1)
+    gr = oracle.bwd(f["x"], f["w_l"], f["w_m"], f["w_r"], f["lam"], h_ref, f["dh"], cfg.dirs, 1, threads=1)
+    tol = TOL[cfg.dtype]
+    got_h = from_torch(h[:, b:b + 1, c0:c0 + Cg])
+    for k in range(cfg.D):
+        assert normwise(got_h[k], h_ref[k]) <= tol, f"unit {u} h slab {k}"
+    got = [from_torch(grads[0][b:b + 1, c0:c0 + Cg])] + \
+          [from_torch(grads[i][:, b:b + 1, g:g + 1]) for i in (1, 2, 3)] + \
+          [from_torch(grads[4][:, b:b + 1, c0:c0 + Cg])]
+    for name, a, r in zip(("dx", "dw_l", "dw_m", "dw_r", "dlam"), got, gr):
+        if a.ndim == 5:
+            for k in range(cfg.D):
+                assert normwise(a[k], r[k]) <= tol, f"unit {u} {name} slab {k}: {normwise(a[k], r[k]):.3e}"
+        else:
+            assert normwise(a, r) <= tol, f"unit {u} {name}: {normwise(a, r):.3e}"
+
+
+def _dot(a, b):
+    import torch
+
+    return float(torch.sum(a.to(torch.float64) * b.to(torch.float64)))
+
+
+def _check_identities(cfg, t, h, grads):
+    """<dh, h> = <dx, x> = sum_d <dlam_d, lam_d>; w_l dw_l + w_m dw_m + w_r dw_r = 0 per pixel."""
+    import torch
+
+    dx, dwl, dwm, dwr, dlam = grads
+    a = _dot(t["dh"], h)
+    bx = _dot(dx, t["x"])
+    bl = _dot(dlam, t["lam"])
+    scale = float(torch.sum(torch.abs(t["dh"].to(torch.float64) * h.to(torch.float64))))
+    tol = 1e-4 if cfg.dtype == "f32" else 2e-2
+    assert abs(bx - a) <= tol * scale, (a, bx)
+    assert abs(bl - a) <= tol * scale, (a, bl)
+    f = lambda v: v.to(torch.float32)
+    e = f(t["w_l"]) * f(dwl) + f(t["w_m"]) * f(dwm) + f(t["w_r"]) * f(dwr)
+    mag = torch.maximum(torch.maximum((f(t["w_l"]) * f(dwl)).abs(), (f(t["w_m"]) * f(dwm)).abs()),
+                        (f(t["w_r"]) * f(dwr)).abs())
+    assert float(e.abs().max()) <= 4 * tol * float(mag.max())
+
+
+@pytest.mark.parametrize("name,nunits", [("1", 8), ("2", 4), ("3a", 64), ("3b", 3), ("4", 3)])
+def test_config_sampled_parity(name, nunits, cuda_device):
+    cfg = get_config(name)
+    t, h, grads = _run(cfg, cuda_device)
+    for u in _sample_units(cfg, nunits):
+        _check_unit(cfg, t, h, grads, u)
+    _check_identities(cfg, t, h, grads)
+
+
+@pytest.mark.slow
+def test_config5_parity(cuda_device):
+    """Config 5: one unit of 40 channels over 2048^2. h, dx, dlam on sampled channels from per-channel
+    oracle runs; dw (summed over all 40 channels) from the sum of per-channel oracle runs, which equals
+    the grouped result because the normalisation Jacobian is linear in the tap gradients
+    (tests/test_oracle.py::test_grouped_dw_is_channel_sum_of_per_channel)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    cfg = get_config("5")
+    t, h, grads = _run(cfg, cuda_device)
+    _check_identities(cfg, t, h, grads)
+    HW = cfg.H * cfg.W
+    seed = synth.seed_for(cfg.cfg_id)
+    D = cfg.D
+
+    def w_planes():
+        out = {}
+        for n in ("w_l", "w_m", "w_r"):
+            v = synth.tensor(seed, n, (D, 1, 1, cfg.H, cfg.W), cfg.dtype)
+            out[n] = synth.as_f64(v, cfg.dtype)
+        return out
+
+    W = w_planes()
+
+    def one_channel(c):
+        x = synth.as_f64(synth.tensor(seed, "x", (1, 1, cfg.H, cfg.W), cfg.dtype, c * HW), cfg.dtype)
+        lam = synth.as_f64(synth.tensor(seed, "lam", (D, 1, 1, cfg.H, cfg.W), cfg.dtype, c * HW, HW, cfg.C * HW),
+                           cfg.dtype)
+        dh = synth.as_f64(synth.tensor(seed, "dh", (D, 1, 1, cfg.H, cfg.W), cfg.dtype, c * HW, HW, cfg.C * HW),
+                          cfg.dtype)
+        hr = oracle.fwd(x, W["w_l"], W["w_m"], W["w_r"], lam, cfg.dirs, 1)
+        gr = oracle.bwd(x, W["w_l"], W["w_m"], W["w_r"], lam, hr, dh, cfg.dirs, 1)
+        return c, hr, gr
+
+    sampled = {0, 17, cfg.C - 1}
+    dw_sum = [np.zeros((D, 1, 1, cfg.H, cfg.W)) for _ in range(3)]
+    tol = TOL[cfg.dtype]
+    with ThreadPoolExecutor(max_workers=min(NTHREADS, 16)) as ex:
+        for c, hr, gr in ex.map(one_channel, range(cfg.C)):
+            for i in range(3):
+                dw_sum[i] += gr[1 + i]
+            if c in sampled:
+                gh = from_torch(h[:, 0:1, c:c + 1])
+                for k in range(D):
+                    assert normwise(gh[k], hr[k]) <= tol
+                assert normwise(from_torch(grads[0][0:1, c:c + 1]), gr[0]) <= tol
+                gl = from_torch(grads[4][:, 0:1, c:c + 1])
+                for k in range(D):
+                    assert normwise(gl[k], gr[4][k]) <= tol
+    for i in range(3):
+        got = from_torch(grads[1 + i])
+        for k in range(D):
+            e = normwise(got[k], dw_sum[i][k])
+            assert e <= tol, f"dw[{i}] slab {k}: {e:.3e}"
