@@ -54,7 +54,8 @@ struct Plan {
   int nin, nout;       // input / output tensors per tile
   int nstages;
   uint32_t tile_bytes;   // one tensor's tile in SMEM: K * ppad * es (= 16 * ppad)
-  uint32_t stage_bytes;  // nin * tile_bytes
+  uint32_t stage_bytes;  // (nin + h_wide) * tile_bytes
+  int h_wide;            // bwd: the h slot (last input) holds 2K steps for horizontal chains
   uint32_t out_bytes;    // nout * tile_bytes (one staging buffer; two are allocated)
   uint32_t tx_v, tx_h;   // TMA bytes landing per stage (vertical / horizontal chains)
   int64_t nchains;
@@ -299,8 +300,12 @@ __device__ void producer_loop(const StreamArgs& A, uint8_t* ring, uint64_t* full
       const uint32_t st = smem_u32(ring + static_cast<size_t>(stage) * pl.stage_bytes);
       for (int t = 0; t < pl.nin; ++t) {
         const int plane = static_cast<int>(plane_of<kBwd>(ch, t));
-        // h_{t-1} view for the backward: one step against the scan direction (zero fill = h_{-1})
-        const int shift = (kBwd && t == B_H) ? (ch.rev ? 1 : -1) : 0;
+        // h_{t-1} view for the backward, one step against the scan direction (its zero fill is
+        // h_{-1} = 0). Vertical: the row coordinate shifts by one. Horizontal: TMA needs a 16-byte
+        // aligned inner coordinate, so a 2K-step box [s0-K, s0+K) (L2R) / [s0, s0+2K) (R2L) is loaded
+        // with a 32-byte swizzle and the consumer picks element K+kk-1 / kk+1.
+        const bool hview = kBwd && t == B_H;
+        const int shift = (hview && ch.vert) ? (ch.rev ? 1 : -1) : 0;
         // x is re-read by the plane's other directions; horizontal 16-byte row chunks are re-read
         // by the next tiles through the 128-byte L2 promotion: keep those at normal priority.
         const uint64_t pol = (t == 0 || !ch.vert) ? pol_keep : pol_stream;
@@ -309,8 +314,14 @@ __device__ void producer_loop(const StreamArgs& A, uint8_t* ring, uint64_t* full
           for (int q = 0; q < pl.nbw; ++q)
             tma_load3(dst + q * pl.K * pl.bw * pl.es, &A.in[o][t], q * pl.bw, s0 + shift, plane, fb, pol);
         } else {
-          for (int q = 0; q < pl.nbh; ++q)
-            tma_load3(dst + q * pl.bh * 16, &A.in[o][t], s0 + shift, q * pl.bh, plane, fb, pol);
+          if (hview) {
+            const int c0h = ch.rev ? s0 : s0 - pl.K;
+            for (int q = 0; q < pl.nbh; ++q)
+              tma_load3(dst + q * pl.bh * 32, &A.in[o][t], c0h, q * pl.bh, plane, fb, pol);
+          } else {
+            for (int q = 0; q < pl.nbh; ++q)
+              tma_load3(dst + q * pl.bh * 16, &A.in[o][t], s0, q * pl.bh, plane, fb, pol);
+          }
         }
       }
       if (++stage == pl.nstages) { stage = 0; phase ^= 1; }
@@ -469,7 +480,7 @@ __device__ __forceinline__ void fwd_tile_horiz(const Plan& pl, const Chain& ch, 
 template <typename T, int kMaxNWC>
 __global__ void __launch_bounds__((kMaxNWC + 1) * 32, 1) fwd_stream_kernel(const __grid_constant__ StreamArgs A) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared address space
   const Plan& pl = A.plan;
   uint8_t* ring = smem;
   uint8_t* outbuf = ring + static_cast<size_t>(pl.nstages) * pl.stage_bytes;
@@ -647,7 +658,10 @@ __device__ __forceinline__ void bwd_tile_horiz(const StreamArgs& A, const Chain&
   float* dwa_r = kGrouped ? p.dwa_r + ch.wplane * HW : nullptr;
   const int c0 = tile_start(ch, j, K);  // canonical column of kk = 0 (W % K == 0 on this path)
   bool valid[kNS], hl[kNS], hr[kNS];
-  uint4 X[kNS], LAM[kNS], DH[kNS], WL[kNS], WM[kNS], WR[kNS], HP[kNS];
+  uint4 X[kNS], LAM[kNS], DH[kNS], WL[kNS], WM[kNS], WR[kNS], HP0[kNS], HP1[kNS];
+  // h tile: rows of 2K steps (32 bytes) with the TMA 32-byte swizzle (16-byte chunk ^= row bit 2)
+  const uint8_t* hbase = st + B_H * pl.tile_bytes;
+  auto swz = [](int r, int c) { return static_cast<uint32_t>(r * 32 + ((c ^ ((r >> 2) & 1)) << 4)); };
   uint4 O0[kNS], O1[kNS], O2[kNS], O3[kNS];
   float DX[kNS][K];
 #pragma unroll
@@ -663,29 +677,31 @@ __device__ __forceinline__ void bwd_tile_horiz(const StreamArgs& A, const Chain&
     WL[q] = *reinterpret_cast<const uint4*>(st + B_WL * pl.tile_bytes + off);
     WM[q] = *reinterpret_cast<const uint4*>(st + B_WM * pl.tile_bytes + off);
     WR[q] = *reinterpret_cast<const uint4*>(st + B_WR * pl.tile_bytes + off);
-    HP[q] = *reinterpret_cast<const uint4*>(st + B_H * pl.tile_bytes + off);
+    HP0[q] = *reinterpret_cast<const uint4*>(hbase + swz(r, 0));
+    HP1[q] = *reinterpret_cast<const uint4*>(hbase + swz(r, 1));
     O0[q] = O1[q] = O2[q] = O3[q] = make_uint4(0, 0, 0, 0);
   }
   // rows just outside this warp's range (for h_{t-1}[r-1] of lane 0 / [r+1] of lane 31)
   const int row_lo = wi * kLanePos - 1, row_hi = wi * kLanePos + kLanePos;
-  const uint8_t* hb_lo = st + B_H * pl.tile_bytes + (row_lo >= 0 ? row_lo : 0) * 16;
-  const uint8_t* hb_hi = st + B_H * pl.tile_bytes + (row_hi < pl.ppad ? row_hi : pl.ppad - 1) * 16;
+  const int rlo = row_lo >= 0 ? row_lo : 0;
+  const int rhi = row_hi < pl.ppad ? row_hi : pl.ppad - 1;
 #pragma unroll
   for (int tt = K - 1; tt >= 0; --tt) {
     const int t = j * K + tt;
     const int kk = kRev ? (K - 1 - tt) : tt;
+    const int he = kRev ? (kk + 1) : (K + kk - 1);  // h_{t-1} element in the 2K-step h row
     if (t < ch.L) {
       float from_right[kNS], from_left[kNS], hv[kNS], hup[kNS], hdn[kNS];
 #pragma unroll
       for (int q = 0; q < kNS; ++q) {
         from_right[q] = shfl_idx(ea[q], (lane + 1) & 31);
         from_left[q] = shfl_idx(ec[q], (lane + 31) & 31);
-        hv[q] = Row<T>::get(HP[q], kk);
+        hv[q] = (he < K) ? Row<T>::get(HP0[q], he) : Row<T>::get(HP1[q], he - K);
         hup[q] = shfl_idx(hv[q], (lane + 31) & 31);
         hdn[q] = shfl_idx(hv[q], (lane + 1) & 31);
       }
-      const float h_lo = to_f(*reinterpret_cast<const T*>(hb_lo + kk * es));
-      const float h_hi = to_f(*reinterpret_cast<const T*>(hb_hi + kk * es));
+      const float h_lo = to_f(*reinterpret_cast<const T*>(hbase + swz(rlo, he / K) + (he % K) * es));
+      const float h_hi = to_f(*reinterpret_cast<const T*>(hbase + swz(rhi, he / K) + (he % K) * es));
       float fl, fr;
       halo_xchg(halo, par, wi, pl.nwc, lane, ea[0], ec[kNS - 1], fl, fr);
 #pragma unroll
@@ -800,7 +816,7 @@ __device__ void bwd_chain_epilogue(const StreamArgs& A, const Chain& ch, int* fl
 template <typename T, bool kGrouped, int kMaxNWC>
 __global__ void __launch_bounds__((kMaxNWC + 1) * 32, 1) bwd_stream_kernel(const __grid_constant__ StreamArgs A) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared address space
   const Plan& pl = A.plan;
   uint8_t* ring = smem;
   uint8_t* outbuf = ring + static_cast<size_t>(pl.nstages) * pl.stage_bytes;
@@ -884,7 +900,7 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 bool encode(CUtensorMap* m, const void* base, gspn_dtype_t dt, int64_t W, int64_t H, int64_t planes, int box0,
-            int box1, bool promote) {
+            int box1, bool promote, bool swizzle32 = false) {
   auto fn = get_encode();
   if (!fn) return false;
   const size_t s = dt == GSPN_BF16 ? 2 : 4;
@@ -894,7 +910,7 @@ bool encode(CUtensorMap* m, const void* base, gspn_dtype_t dt, int64_t W, int64_
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(m, dt == GSPN_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
                   const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  CU_TENSOR_MAP_SWIZZLE_NONE,
+                  swizzle32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE,
                   promote ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_NONE,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
@@ -955,10 +971,11 @@ bool make_plan(const ScanParams& p, gspn_dtype_t dt, int nin, int nout, int min_
   pl->nin = nin;
   pl->nout = nout;
   pl->tile_bytes = static_cast<uint32_t>(pl->K * pl->ppad * s);
-  pl->stage_bytes = nin * pl->tile_bytes;
+  pl->h_wide = (nin == B_NIN) ? 1 : 0;
+  pl->stage_bytes = (nin + pl->h_wide) * pl->tile_bytes;
   pl->out_bytes = nout * pl->tile_bytes;
   pl->tx_v = static_cast<uint32_t>(nin * pl->nbw * pl->bw * pl->K * s);
-  pl->tx_h = static_cast<uint32_t>(nin * pl->nbh * pl->bh * pl->K * s);
+  pl->tx_h = static_cast<uint32_t>((nin + pl->h_wide) * pl->nbh * pl->bh * pl->K * s);
   const int budget = smem_optin() - 1024 /*alignment*/ - 512 /*barriers, halo, flag*/;
   const int avail = budget - 2 * static_cast<int>(pl->out_bytes);
   int ns = avail / static_cast<int>(pl->stage_bytes);
@@ -976,7 +993,9 @@ bool fill_maps(StreamArgs* A, const void* const* ins, int nin, void* const* outs
   const ScanParams& p = A->p;
   for (int t = 0; t < nin; ++t) {
     if (!encode(&A->in[0][t], ins[t], dt, p.W, p.H, in_planes[t], pl.bw, pl.K, false)) return false;
-    if (!encode(&A->in[1][t], ins[t], dt, p.W, p.H, in_planes[t], pl.K, pl.bh, true)) return false;
+    const bool wide = pl.h_wide && t == nin - 1;  // bwd h_{t-1} view: 2K-step rows, 32-byte swizzle
+    if (!encode(&A->in[1][t], ins[t], dt, p.W, p.H, in_planes[t], wide ? 2 * pl.K : pl.K, pl.bh, true, wide))
+      return false;
   }
   for (int t = 0; t < nout; ++t) {
     if (!encode(&A->out[0][t], outs[t], dt, p.W, p.H, out_planes[t], pl.bw, pl.K, false)) return false;

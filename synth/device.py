@@ -76,43 +76,64 @@ def shard_for(cfg: Config, rank: int, world: int) -> Shard:
     raise ValueError(f"cannot shard {U} units over {world} ranks")
 
 
+def index_maps(cfg: Config, sh: Shard) -> dict:
+    """(index_base, inner, outer_stride) of every tensor of a shard: local flat index i maps to the
+    unsharded flat index index_base + (i // inner) * outer_stride + i % inner (inner 0 = identity)."""
+    HW = cfg.H * cfg.W
+    Cg = cfg.C // cfg.G
+    if sh.kind == "full":
+        m = {n: (0, 0, 0) for n in ("x", "lam", "dh", "w_l", "w_m", "w_r")}
+    elif sh.kind == "units":
+        base = sh.unit0 * Cg * HW
+        per_c = (base, sh.units * Cg * HW, cfg.B * cfg.C * HW)
+        per_w = (sh.unit0 * HW, sh.units * HW, cfg.B * cfg.G * HW)
+        m = {"x": (base, 0, 0), "lam": per_c, "dh": per_c, "w_l": per_w, "w_m": per_w, "w_r": per_w}
+    else:  # channels [chan0, chan0 + chans) of the single unit; w replicated
+        base = sh.chan0 * HW
+        per_c = (base, sh.chans * HW, cfg.C * HW)
+        m = {"x": (base, 0, 0), "lam": per_c, "dh": per_c, "w_l": (0, 0, 0), "w_m": (0, 0, 0), "w_r": (0, 0, 0)}
+    return m
+
+
+def shard_shapes(cfg: Config, sh: Shard) -> dict:
+    D, H, W = cfg.D, cfg.H, cfg.W
+    return {"x": (sh.B, sh.C, H, W), "lam": (D, sh.B, sh.C, H, W), "dh": (D, sh.B, sh.C, H, W),
+            "w_l": (D, sh.B, sh.G, H, W), "w_m": (D, sh.B, sh.G, H, W), "w_r": (D, sh.B, sh.G, H, W)}
+
+
+def full_shard(cfg: Config) -> Shard:
+    return Shard(cfg.B, cfg.C, cfg.G, 0, cfg.B * cfg.G, 0, cfg.C, "full")
+
+
+def host_shard_inputs(cfg: Config, sh: Shard | None = None) -> dict:
+    """Host (numpy) twin of make_inputs: I/O-dtype values of every tensor of the shard."""
+    from . import tensor
+
+    sh = sh or full_shard(cfg)
+    seed = seed_for(cfg.cfg_id)
+    maps, shapes = index_maps(cfg, sh), shard_shapes(cfg, sh)
+    out = {}
+    for n, shape in shapes.items():
+        base, inner, outer = maps[n]
+        out[n] = tensor(seed, n, shape, cfg.dtype, base, inner or None, outer or None)
+    return out
+
+
 def make_inputs(cfg: Config, device, shard: Shard | None = None, with_dh: bool = True):
     """Allocate and fill x, w_l, w_m, w_r, lam (and dh) for (a shard of) config `cfg` on `device`."""
     import torch
 
-    sh = shard or Shard(cfg.B, cfg.C, cfg.G, 0, cfg.B * cfg.G, 0, cfg.C, "full")
+    sh = shard or full_shard(cfg)
     seed = seed_for(cfg.cfg_id)
     dt = torch.bfloat16 if cfg.dtype == "bf16" else torch.float32
-    D, H, W = cfg.D, cfg.H, cfg.W
-    HW = H * W
-    Cg = cfg.C // cfg.G
+    maps, shapes = index_maps(cfg, sh), shard_shapes(cfg, sh)
     out = {}
-    x = torch.empty((sh.B, sh.C, H, W), dtype=dt, device=device)
-    lam = torch.empty((D, sh.B, sh.C, H, W), dtype=dt, device=device)
-    ws = [torch.empty((D, sh.B, sh.G, H, W), dtype=dt, device=device) for _ in range(3)]
-    dh = torch.empty((D, sh.B, sh.C, H, W), dtype=dt, device=device) if with_dh else None
-    if sh.kind == "full":
-        fill_(x, seed, "x")
-        fill_(lam, seed, "lam")
-        for w, n in zip(ws, ("w_l", "w_m", "w_r")):
-            fill_(w, seed, n)
-        if dh is not None:
-            fill_(dh, seed, "dh")
-    elif sh.kind == "units":
-        base = sh.unit0 * Cg * HW
-        fill_(x, seed, "x", base)
-        fill_(lam, seed, "lam", base, sh.units * Cg * HW, cfg.B * cfg.C * HW)
-        for w, n in zip(ws, ("w_l", "w_m", "w_r")):
-            fill_(w, seed, n, sh.unit0 * HW, sh.units * HW, cfg.B * cfg.G * HW)
-        if dh is not None:
-            fill_(dh, seed, "dh", base, sh.units * Cg * HW, cfg.B * cfg.C * HW)
-    else:  # channels of the single unit
-        base = sh.chan0 * HW
-        fill_(x, seed, "x", base)
-        fill_(lam, seed, "lam", base, sh.chans * HW, cfg.C * HW)
-        for w, n in zip(ws, ("w_l", "w_m", "w_r")):
-            fill_(w, seed, n)
-        if dh is not None:
-            fill_(dh, seed, "dh", base, sh.chans * HW, cfg.C * HW)
-    out["x"], out["lam"], out["w_l"], out["w_m"], out["w_r"], out["dh"] = x, lam, ws[0], ws[1], ws[2], dh
+    for n, shape in shapes.items():
+        if n == "dh" and not with_dh:
+            out[n] = None
+            continue
+        t = torch.empty(shape, dtype=dt, device=device)
+        base, inner, outer = maps[n]
+        fill_(t, seed, n, base, inner, outer)
+        out[n] = t
     return out
