@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--flags", type=int, default=0)
+    ap.add_argument("--dirs", type=lambda v: int(v, 0), default=None, help="override the direction mask (experiments)")
     return ap.parse_args()
 
 
@@ -217,6 +218,8 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=dev)
 
     base = get_config(args.config)
+    if args.dirs is not None:
+        base = base.with_(dirs=args.dirs)
     if args.scaling == "weak":
         gcfg = base.with_(B=base.B * world)  # each rank owns one configuration's worth of units
     else:

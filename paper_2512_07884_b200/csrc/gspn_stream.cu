@@ -1,31 +1,36 @@
 // gspn_stream.cu — the TMA-streaming fast path for sm_100a (B200).
 //
-// One persistent launch covers every requested direction (PAPER.md:122-123 "Kernel Fuse", :201 — the
-// paper's one-stream-per-direction concurrency becomes a direction dimension of the work queue).
+// One persistent launch covers every requested direction ("Kernel Fuse"; the paper's
+// one-stream-per-direction concurrency, becomes a direction dimension of the work queue).
 // Work item = one chain (direction k, batch b, channel c): a P-wide state marching L steps. A CTA owns
-// a chain at a time: warp NWC (the producer) streams K-step tiles of every input tensor into a
-// shared-memory ring with TMA (cp.async.bulk.tensor, mbarrier complete_tx), NWC consumer warps run
-// the recurrence with the carry in fp32 registers, exchange neighbours with warp shuffles and, across
-// warps, through a shared-memory halo (one named barrier per step), and stage outputs in shared
-// memory for TMA stores. Loads are 16-byte vectors from shared memory in both orientations:
-//   T2B/B2T (vertical):   a tile is K image rows x P columns ([box][K][BW] in SMEM); a lane owns
-//                         E = 4 consecutive positions and reads one 4-element vector per step.
-//   L2R/R2L (horizontal): a tile is P image rows x K columns ([P][K], 16-byte rows = K steps); a lane
-//                         owns NS = 4 interleaved rows and reads all K steps of a row in one vector.
-// The chain order puts the D directions of one (b, c) plane next to each other so the plane's x (and
-// in bwd the fp32 dx accumulator) is shared through L2 by co-scheduled CTAs.
+// one chain at a time:
+//  * warp NWC (the producer) streams K-step tiles (K * sizeof(T) = 16 bytes) of every input tensor
+//    into a shared-memory ring with TMA (cp.async.bulk.tensor.3d, mbarrier complete_tx);
+//  * NWC consumer warps run the recurrence with the carry in fp32 registers. A warp covers 128
+//    consecutive positions: it OWNS the middle 128 - 2K and recomputes K "ghost" positions on each
+//    side (temporal blocking): neighbours move by warp shuffles every step, and warps exchange their
+//    edge values through shared memory once per K-step tile instead of once per step;
+//  * outputs are staged in shared memory (double-buffered) and written back with TMA stores.
+// Lane mappings (both conflict-free on the shared-memory tiles):
+//   T2B/B2T (vertical):   tile = K image rows x P columns ([box][K][bw]); a lane owns 4 consecutive
+//                         positions and reads one 4-element vector per tensor per step.
+//   L2R/R2L (horizontal): tile = P image rows x 16 bytes ([P][K]); a lane owns 4 interleaved rows
+//                         (position A + 32 q + lane) and holds the K steps of a row in one vector.
+// Chains are ordered (b, c)-major with the D directions adjacent, so co-scheduled CTAs share a
+// plane's x (and in the backward its fp32 dx accumulator) through L2.
 //
-// Backward: tiles in reverse step order; g_t = dh_t + b_{t+1} g_{t+1}
-// + a_{t+1}[r+1] g_{t+1}[r+1] + c_{t+1}[r-1] g_{t+1}[r-1] exchanged as (a g, c g) products; h_{t-1}
-// comes from a second TMA view of h shifted by one step (its zero fill at t = 0 is h_{-1} = 0);
-// dx (sum over directions) accumulates with red.global.add.v4.f32 into an fp32 workspace plane and is
-// converted by the last of the plane's D chains; per-channel dw gets the normalisation Jacobian in
-// registers; grouped dw accumulates the normalised-tap gradients in fp32 and the group's last
-// channel applies the Jacobian.
+// Backward: tiles in reverse step order; the carried state is
+// (a g, b g, c g) of the previous step, so g_t = dh_t + (b g)[r] + (a g)[r+1] + (c g)[r-1];
+// h_{t-1} comes from a second TMA view of h shifted one step against the scan (its zero fill at
+// t = 0 is h_{-1} = 0); dx (sum over directions) accumulates with red.global.add into an fp32
+// workspace plane that the last of the plane's D chains converts and discards from L2; per-channel
+// dw gets the normalisation Jacobian in registers; grouped dw sums the normalised-tap gradients with
+// red and the group's last channel applies the Jacobian.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -35,27 +40,34 @@
 namespace gspn {
 namespace {
 
-constexpr int kE = 2;        // vertical: consecutive positions per lane
-constexpr int kNS = 2;       // horizontal: interleaved rows per lane
-constexpr int kLanePos = 32 * kE;  // positions per consumer warp (both orientations: 32*kNS == 32*kE)
-constexpr int kHaloW = 16;   // halo slots (>= consumer warps of any instantiation)
+constexpr int kWarpPos = 128;  // positions covered by one consumer warp (4 per lane)
 constexpr int kMaxIn = 7;
 constexpr int kMaxOut = 4;
-constexpr int kBarStep = 1;  // named barrier ids (0 is __syncthreads)
-constexpr int kBarTile = 2;
+constexpr int kEdgeW = 16;     // max consumer warps (edge-buffer slots)
+constexpr int kBarTile = 1;    // named barrier id (0 is __syncthreads)
+
+template <typename T>
+struct Cfg {
+  static constexpr int es = static_cast<int>(sizeof(T));
+  static constexpr int K = 16 / es;             // steps per tile (one 16-byte row chunk)
+  static constexpr int GH = K;                  // ghost positions on each side of a warp
+  static constexpr int OWN = kWarpPos - 2 * GH; // positions a warp owns
+  static constexpr int KS = 8 / es;             // bwd horizontal sub-tile (one 8-byte row chunk)
+};
 
 struct Plan {
-  int K;               // steps per tile: K * sizeof(T) == 16 bytes
+  int K;               // steps per tile
+  int own;             // owned positions per warp
   int nwc;             // consumer warps
-  int ppad;            // positions covered: kLanePos * nwc
+  int ppad;            // positions held by a tile (>= P, multiple of 64 and of bw)
   int es;              // element size in bytes
   int bw, nbw;         // vertical TMA box width (positions) and box count
   int bh, nbh;         // horizontal TMA box height (positions) and box count
   int nin, nout;       // input / output tensors per tile
+  int h_wide;          // bwd: the last input (h) holds 2K steps for horizontal chains
   int nstages;
-  uint32_t tile_bytes;   // one tensor's tile in SMEM: K * ppad * es (= 16 * ppad)
+  uint32_t tile_bytes;   // one tensor's tile: K * ppad * es (= 16 * ppad)
   uint32_t stage_bytes;  // (nin + h_wide) * tile_bytes
-  int h_wide;            // bwd: the h slot (last input) holds 2K steps for horizontal chains
   uint32_t out_bytes;    // nout * tile_bytes (one staging buffer; two are allocated)
   uint32_t tx_v, tx_h;   // TMA bytes landing per stage (vertical / horizontal chains)
   int64_t nchains;
@@ -93,6 +105,17 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       "WAIT%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
       "@!p bra WAIT%=;\n}" ::"r"(bar),
       "r"(parity)
+      : "memory");
+}
+
+// Wait with a suspend-time hint: the (single) producer thread sleeps in hardware instead of
+// re-issuing try_wait, leaving its SMSP's issue slots to the consumer warps.
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\n"
+      "WAITS%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAITS%=;\n}" ::"r"(bar),
+      "r"(parity), "r"(1000000u)
       : "memory");
 }
 
@@ -159,76 +182,97 @@ __device__ __forceinline__ float fast_rcp(float x) {
   return r;
 }
 
+
+__device__ __forceinline__ void discard_l2_line(const void* p) {
+  asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
+
+// Neighbour values inside a warp; the warp's outermost lanes get 0 (their positions are ghosts).
+__device__ __forceinline__ float from_lower_lane(float v, int lane) {
+  const float u = __shfl_up_sync(0xffffffffu, v, 1);
+  return lane == 0 ? 0.f : u;
+}
+__device__ __forceinline__ float from_upper_lane(float v, int lane) {
+  const float u = __shfl_down_sync(0xffffffffu, v, 1);
+  return lane == 31 ? 0.f : u;
+}
+
 // ------------------------------------------------------------------------------ element access
 
-// 2 consecutive elements of T at a shared-memory address <-> floats (4 B for bf16, 8 B for fp32).
-template <typename T> struct V2;
-template <> struct V2<__nv_bfloat16> {
-  static __device__ __forceinline__ void load(const uint8_t* p, float (&v)[2]) {
-    const uint32_t u = *reinterpret_cast<const uint32_t*>(p);
-    v[0] = __uint_as_float(u << 16);
-    v[1] = __uint_as_float(u & 0xFFFF0000u);
+// 4 consecutive elements of T in shared memory <-> floats (8 bytes for bf16, 16 for fp32).
+template <typename T> struct V4;
+template <> struct V4<__nv_bfloat16> {
+  static __device__ __forceinline__ void load(const uint8_t* p, float (&v)[4]) {
+    const uint2 u = *reinterpret_cast<const uint2*>(p);
+    v[0] = __uint_as_float(u.x << 16); v[1] = __uint_as_float(u.x & 0xFFFF0000u);
+    v[2] = __uint_as_float(u.y << 16); v[3] = __uint_as_float(u.y & 0xFFFF0000u);
   }
-  static __device__ __forceinline__ void store(uint8_t* p, const float (&v)[2]) {
+  static __device__ __forceinline__ uint2 pack(const float (&v)[4]) {
     __nv_bfloat162 a = __floats2bfloat162_rn(v[0], v[1]);
-    *reinterpret_cast<__nv_bfloat162*>(p) = a;
+    __nv_bfloat162 b = __floats2bfloat162_rn(v[2], v[3]);
+    return make_uint2(*reinterpret_cast<uint32_t*>(&a), *reinterpret_cast<uint32_t*>(&b));
+  }
+  static __device__ __forceinline__ void store(uint8_t* p, const float (&v)[4]) {
+    *reinterpret_cast<uint2*>(p) = pack(v);
   }
 };
-template <> struct V2<float> {
-  static __device__ __forceinline__ void load(const uint8_t* p, float (&v)[2]) {
-    const float2 u = *reinterpret_cast<const float2*>(p);
-    v[0] = u.x;
-    v[1] = u.y;
+template <> struct V4<float> {
+  static __device__ __forceinline__ void load(const uint8_t* p, float (&v)[4]) {
+    const float4 u = *reinterpret_cast<const float4*>(p);
+    v[0] = u.x; v[1] = u.y; v[2] = u.z; v[3] = u.w;
   }
-  static __device__ __forceinline__ void store(uint8_t* p, const float (&v)[2]) {
-    *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
+  static __device__ __forceinline__ void store(uint8_t* p, const float (&v)[4]) {
+    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
   }
 };
 
-// 4 consecutive elements from fp32 -> T in global memory (dx conversion).
-template <typename T> __device__ __forceinline__ void store4(T* p, float4 v);
-template <> __device__ __forceinline__ void store4<__nv_bfloat16>(__nv_bfloat16* p, float4 v) {
-  __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
-  uint2 u;
-  u.x = *reinterpret_cast<uint32_t*>(&a);
-  u.y = *reinterpret_cast<uint32_t*>(&b);
-  *reinterpret_cast<uint2*>(p) = u;
+// 4 consecutive fp32 values -> T in global memory (dx conversion).
+template <typename T> __device__ __forceinline__ void store4_global(T* p, float4 v);
+template <> __device__ __forceinline__ void store4_global<__nv_bfloat16>(__nv_bfloat16* p, float4 v) {
+  const float a[4] = {v.x, v.y, v.z, v.w};
+  *reinterpret_cast<uint2*>(p) = V4<__nv_bfloat16>::pack(a);
 }
-template <> __device__ __forceinline__ void store4<float>(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+template <> __device__ __forceinline__ void store4_global<float>(float* p, float4 v) {
+  *reinterpret_cast<float4*>(p) = v;
+}
 
-// One 16-byte row chunk = K steps of one position (horizontal tiles). Indices are compile-time
-// constants after unrolling, so the selects fold away.
-template <typename T> struct Row;
-template <> struct Row<__nv_bfloat16> {
-  static constexpr int K = 8;
+// Element i of a packed row chunk (uint4 = 16 bytes, uint2 = 8 bytes) of T. i is a compile-time
+// constant after unrolling, so the selects fold away.
+template <typename T> struct Pk;
+template <> struct Pk<__nv_bfloat16> {
+  static __device__ __forceinline__ uint32_t word4(const uint4& u, int w) { return w == 0 ? u.x : w == 1 ? u.y : w == 2 ? u.z : u.w; }
   static __device__ __forceinline__ float get(const uint4& u, int i) {
-    const uint32_t w = (i < 2) ? u.x : (i < 4) ? u.y : (i < 6) ? u.z : u.w;
+    const uint32_t w = word4(u, i >> 1);
     return (i & 1) ? __uint_as_float(w & 0xFFFF0000u) : __uint_as_float(w << 16);
   }
+  static __device__ __forceinline__ float get(const uint2& u, int i) {
+    const uint32_t w = (i >> 1) ? u.y : u.x;
+    return (i & 1) ? __uint_as_float(w & 0xFFFF0000u) : __uint_as_float(w << 16);
+  }
+  static __device__ __forceinline__ uint32_t bits(float v) {
+    return static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(v)));
+  }
   static __device__ __forceinline__ void set(uint4& u, int i, float v) {
-    const uint32_t b = static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(v)));
-    uint32_t& w = (i < 2) ? u.x : (i < 4) ? u.y : (i < 6) ? u.z : u.w;
-    w = (i & 1) ? ((w & 0x0000FFFFu) | (b << 16)) : ((w & 0xFFFF0000u) | b);
+    uint32_t& w = (i >> 1) == 0 ? u.x : (i >> 1) == 1 ? u.y : (i >> 1) == 2 ? u.z : u.w;
+    w = (i & 1) ? ((w & 0x0000FFFFu) | (bits(v) << 16)) : ((w & 0xFFFF0000u) | bits(v));
+  }
+  static __device__ __forceinline__ void set(uint2& u, int i, float v) {
+    uint32_t& w = (i >> 1) ? u.y : u.x;
+    w = (i & 1) ? ((w & 0x0000FFFFu) | (bits(v) << 16)) : ((w & 0xFFFF0000u) | bits(v));
   }
 };
-template <> struct Row<float> {
-  static constexpr int K = 4;
+template <> struct Pk<float> {
   static __device__ __forceinline__ float get(const uint4& u, int i) {
-    return __uint_as_float((i == 0) ? u.x : (i == 1) ? u.y : (i == 2) ? u.z : u.w);
+    return __uint_as_float(i == 0 ? u.x : i == 1 ? u.y : i == 2 ? u.z : u.w);
   }
+  static __device__ __forceinline__ float get(const uint2& u, int i) { return __uint_as_float(i ? u.y : u.x); }
   static __device__ __forceinline__ void set(uint4& u, int i, float v) {
-    uint32_t& w = (i == 0) ? u.x : (i == 1) ? u.y : (i == 2) ? u.z : u.w;
+    uint32_t& w = i == 0 ? u.x : i == 1 ? u.y : i == 2 ? u.z : u.w;
     w = __float_as_uint(v);
   }
-};
-
-// Shared-memory byte offset of (step-in-tile kk, position r) inside one vertical tensor tile
-// ([box][K][bw] as written by the TMA boxes). Horizontal tiles are [position][16 bytes].
-struct TileGeom {
-  int K, bw_log2, es;
-  __device__ __forceinline__ uint32_t vert(int kk, int r) const {
-    const int bw = 1 << bw_log2;
-    return static_cast<uint32_t>((((r >> bw_log2) * K + kk) * bw + (r & (bw - 1))) * es);
+  static __device__ __forceinline__ void set(uint2& u, int i, float v) {
+    uint32_t& w = i ? u.y : u.x;
+    w = __float_as_uint(v);
   }
 };
 
@@ -236,9 +280,8 @@ struct TileGeom {
 
 struct Chain {
   int k;            // direction slab
-  uint32_t dir;
   bool vert, rev;   // orientation; reversed step order in canonical coordinates (B2T, R2L)
-  int64_t bc, b, c, g, chain, wplane;
+  int64_t bc, chain, wplane;
   int L, P, ntiles;
 };
 
@@ -246,15 +289,13 @@ __device__ __forceinline__ Chain make_chain(const ScanParams& p, int K, int64_t 
   Chain ch;
   const int64_t bc = w / p.D;
   ch.k = static_cast<int>(w % p.D);
-  ch.dir = p.dirbit[ch.k];
-  ch.vert = (ch.dir == GSPN_DIR_T2B) || (ch.dir == GSPN_DIR_B2T);
-  ch.rev = (ch.dir == GSPN_DIR_B2T) || (ch.dir == GSPN_DIR_R2L);
+  const uint32_t dir = p.dirbit[ch.k];
+  ch.vert = (dir == GSPN_DIR_T2B) || (dir == GSPN_DIR_B2T);
+  ch.rev = (dir == GSPN_DIR_B2T) || (dir == GSPN_DIR_R2L);
   ch.bc = bc;
-  ch.b = bc / p.C;
-  ch.c = bc % p.C;
-  ch.g = ch.c / (p.C / p.G);
-  ch.chain = (ch.k * p.B + ch.b) * p.C + ch.c;
-  ch.wplane = (ch.k * p.B + ch.b) * p.G + ch.g;
+  const int64_t b = bc / p.C, c = bc % p.C, g = c / (p.C / p.G);
+  ch.chain = (ch.k * p.B + b) * p.C + c;
+  ch.wplane = (ch.k * p.B + b) * p.G + g;
   ch.L = static_cast<int>(ch.vert ? p.H : p.W);
   ch.P = static_cast<int>(ch.vert ? p.W : p.H);
   ch.ntiles = (ch.L + K - 1) / K;
@@ -285,7 +326,7 @@ __device__ void producer_loop(const StreamArgs& A, uint8_t* ring, uint64_t* full
   const Plan& pl = A.plan;
   const ScanParams& p = A.p;
   const uint64_t pol_stream = policy_evict_first();
-  const uint64_t pol_keep = policy_evict_normal();
+  const uint64_t pol_keep = policy_evict_last();
   int stage = 0;
   uint32_t phase = 0;
   for (int64_t w = blockIdx.x; w < pl.nchains; w += gridDim.x) {
@@ -293,7 +334,7 @@ __device__ void producer_loop(const StreamArgs& A, uint8_t* ring, uint64_t* full
     const int o = ch.vert ? 0 : 1;
     for (int jj = 0; jj < ch.ntiles; ++jj) {
       const int j = kBwd ? (ch.ntiles - 1 - jj) : jj;
-      mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+      mbar_wait_sleep(smem_u32(&empty[stage]), phase ^ 1);
       const uint32_t fb = smem_u32(&full[stage]);
       mbar_arrive_tx(fb, ch.vert ? pl.tx_v : pl.tx_h);
       const int s0 = tile_start(ch, j, pl.K);
@@ -302,26 +343,25 @@ __device__ void producer_loop(const StreamArgs& A, uint8_t* ring, uint64_t* full
         const int plane = static_cast<int>(plane_of<kBwd>(ch, t));
         // h_{t-1} view for the backward, one step against the scan direction (its zero fill is
         // h_{-1} = 0). Vertical: the row coordinate shifts by one. Horizontal: TMA needs a 16-byte
-        // aligned inner coordinate, so a 2K-step box [s0-K, s0+K) (L2R) / [s0, s0+2K) (R2L) is loaded
-        // with a 32-byte swizzle and the consumer picks element K+kk-1 / kk+1.
+        // aligned inner coordinate, so a 2K-step box [s0-K, s0+K) (L2R) / [s0, s0+2K) (R2L) is
+        // loaded with a 32-byte swizzle and the consumer picks element K+kk-1 / kk+1.
         const bool hview = kBwd && t == B_H;
-        const int shift = (hview && ch.vert) ? (ch.rev ? 1 : -1) : 0;
-        // x is re-read by the plane's other directions; horizontal 16-byte row chunks are re-read
-        // by the next tiles through the 128-byte L2 promotion: keep those at normal priority.
+        // x is re-read by the plane's other directions, and a horizontal 16-byte row chunk shares its
+        // 32-byte sector with the next tile's chunk: both are kept (evict_last) so the second access
+        // hits L2; vertical streams are read exactly once (evict_first).
         const uint64_t pol = (t == 0 || !ch.vert) ? pol_keep : pol_stream;
         const uint32_t dst = st + t * pl.tile_bytes;
         if (ch.vert) {
+          const int row = s0 + (hview ? (ch.rev ? 1 : -1) : 0);
           for (int q = 0; q < pl.nbw; ++q)
-            tma_load3(dst + q * pl.K * pl.bw * pl.es, &A.in[o][t], q * pl.bw, s0 + shift, plane, fb, pol);
+            tma_load3(dst + q * pl.K * pl.bw * pl.es, &A.in[o][t], q * pl.bw, row, plane, fb, pol);
+        } else if (hview) {
+          const int c0h = ch.rev ? s0 : s0 - pl.K;
+          for (int q = 0; q < pl.nbh; ++q)
+            tma_load3(dst + q * pl.bh * 32, &A.in[o][t], c0h, q * pl.bh, plane, fb, pol);
         } else {
-          if (hview) {
-            const int c0h = ch.rev ? s0 : s0 - pl.K;
-            for (int q = 0; q < pl.nbh; ++q)
-              tma_load3(dst + q * pl.bh * 32, &A.in[o][t], c0h, q * pl.bh, plane, fb, pol);
-          } else {
-            for (int q = 0; q < pl.nbh; ++q)
-              tma_load3(dst + q * pl.bh * 16, &A.in[o][t], s0, q * pl.bh, plane, fb, pol);
-          }
+          for (int q = 0; q < pl.nbh; ++q)
+            tma_load3(dst + q * pl.bh * 16, &A.in[o][t], s0, q * pl.bh, plane, fb, pol);
         }
       }
       if (++stage == pl.nstages) { stage = 0; phase ^= 1; }
@@ -348,145 +388,212 @@ __device__ __forceinline__ void store_tile(const StreamArgs& A, const Chain& ch,
   bulk_commit();
 }
 
-// Cross-warp neighbour values of one step: every warp publishes the value at its first and last
-// position; lane 0 receives the left neighbour's last, lane 31 the right neighbour's first.
-// Double-buffered by step parity, so one named barrier per step suffices.
-__device__ __forceinline__ void halo_xchg(float* halo, int& par, int wi, int nwc, int lane, float first, float last,
-                                          float& from_left, float& from_right) {
-  from_left = 0.f;
-  from_right = 0.f;
-  if (nwc > 1) {
-    float* hb = halo + par * (2 * kHaloW);
-    if (lane == 0) hb[wi] = first;
-    if (lane == 31) hb[kHaloW + wi] = last;
-    named_bar(kBarStep, nwc * 32);
-    if (lane == 0 && wi > 0) from_left = hb[kHaloW + wi - 1];
-    if (lane == 31 && wi < nwc - 1) from_right = hb[wi + 1];
-    par ^= 1;
+// ------------------------------------------------------------------------------ per-lane geometry
+
+// The 4 positions a lane computes, their masks, and where they live in a shared-memory tile.
+// Warp w covers positions [A, A + 128), A = w * OWN - GH; it owns [A + GH, A + 128 - GH).
+//   vertical:   lane owns positions A + 4 lane + e            (e = 0..3)
+//   horizontal: lane owns positions A + 32 e + lane           (e = slot 0..3)
+struct Lanes {
+  int A;
+  int pos[4];
+  bool valid[4], hl[4], hr[4], own[4];
+  uint32_t voff;      // vertical: byte offset of the lane's 4 positions at kk = 0
+  uint32_t vstep;     // vertical: bytes between consecutive kk
+  uint32_t row[4];    // horizontal: clamped row index of each slot
+};
+
+template <typename T>
+__device__ __forceinline__ Lanes make_lanes(const Plan& pl, const Chain& ch, int wi, int lane) {
+  using C = Cfg<T>;
+  Lanes ln;
+  ln.A = wi * C::OWN - C::GH;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const int off = ch.vert ? (4 * lane + e) : (32 * e + lane);
+    const int r = ln.A + off;
+    ln.pos[e] = r;
+    ln.valid[e] = (r >= 0) && (r < ch.P);
+    ln.hl[e] = r >= 1;
+    ln.hr[e] = r <= ch.P - 2;
+    // owned, and inside the tile (positions >= ppad are padding >= P: nothing to store)
+    ln.own[e] = (off >= C::GH) && (off < kWarpPos - C::GH) && (r < pl.ppad);
+    const int rc = r < 0 ? 0 : (r >= pl.ppad ? pl.ppad - 1 : r);
+    ln.row[e] = static_cast<uint32_t>(rc);
+  }
+  int r0 = ln.A + 4 * lane;
+  r0 = r0 < 0 ? 0 : (r0 > pl.ppad - 4 ? pl.ppad - 4 : r0);
+  const int bwl = 31 - __clz(pl.bw);
+  ln.voff = static_cast<uint32_t>((((r0 >> bwl) * C::K) * pl.bw + (r0 & (pl.bw - 1))) * C::es);
+  ln.vstep = static_cast<uint32_t>(pl.bw * C::es);
+  return ln;
+}
+
+// Ghost exchange at a tile boundary. Each warp publishes its first GH and last GH owned values
+// (edges) and reloads its ghost positions from the neighbouring warps' edges; warps outside
+// [0, nwc) contribute 0. Parity-double-buffered; the caller separates publish and reload by a barrier.
+template <typename T>
+__device__ __forceinline__ void edge_publish(float* edge, int par, int wi, int lane, bool vert, const float (&v)[4]) {
+  using C = Cfg<T>;
+  float* L = edge + ((par * kEdgeW + wi) * 2 + 0) * 8;
+  float* R = edge + ((par * kEdgeW + wi) * 2 + 1) * 8;
+  if (vert) {
+    const int o = 4 * lane;
+    if (o >= C::GH && o < 2 * C::GH) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) L[o - C::GH + e] = v[e];
+    }
+    if (o >= kWarpPos - 2 * C::GH && o < kWarpPos - C::GH) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) R[o - (kWarpPos - 2 * C::GH) + e] = v[e];
+    }
+  } else {
+    if (lane >= C::GH && lane < 2 * C::GH) L[lane - C::GH] = v[0];
+    if (lane >= 32 - 2 * C::GH && lane < 32 - C::GH) R[lane - (32 - 2 * C::GH)] = v[3];
   }
 }
 
-__device__ __forceinline__ float shfl_idx(float v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+template <typename T>
+__device__ __forceinline__ void edge_reload(const float* edge, int par, int wi, int nwc, int lane, bool vert,
+                                            float (&v)[4]) {
+  using C = Cfg<T>;
+  const float* Rl = edge + ((par * kEdgeW + (wi - 1)) * 2 + 1) * 8;  // left neighbour's right edge
+  const float* Lr = edge + ((par * kEdgeW + (wi + 1)) * 2 + 0) * 8;  // right neighbour's left edge
+  if (vert) {
+    const int o = 4 * lane;
+    if (o < C::GH) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) v[e] = wi > 0 ? Rl[o + e] : 0.f;
+    }
+    if (o >= kWarpPos - C::GH) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) v[e] = wi < nwc - 1 ? Lr[o - (kWarpPos - C::GH) + e] : 0.f;
+    }
+  } else {
+    if (lane < C::GH) v[0] = wi > 0 ? Rl[lane] : 0.f;
+    if (lane >= 32 - C::GH) v[3] = wi < nwc - 1 ? Lr[lane - (32 - C::GH)] : 0.f;
+  }
+}
 
 // ------------------------------------------------------------------------------ forward consumer
 
-// Vertical tile: up to K steps; lane owns positions r0, r0+1.
-template <typename T>
-__device__ __forceinline__ void fwd_tile_vert(const Plan& pl, const TileGeom& tg, const Chain& ch, int j,
-                                              const uint8_t* st, uint8_t* ob, float* halo, int& par, int wi, int lane,
-                                              float (&h)[2], bool prenorm) {
-  const int r0 = wi * kLanePos + lane * kE;
-  bool valid[2], hl[2], hr[2];
+// One step of Eq. 1 for the lane's 4 positions given the previous state's outer neighbours.
+__device__ __forceinline__ void fwd_update(const Lanes& ln, const float (&x)[4], const float (&lam)[4],
+                                           const float (&wl)[4], const float (&wm)[4], const float (&wr)[4],
+                                           const float (&hm1)[4], const float (&hp1)[4], float (&h)[4],
+                                           bool prenorm) {
+  float hn[4];
 #pragma unroll
-  for (int e = 0; e < 2; ++e) {
-    valid[e] = (r0 + e) < ch.P;
-    hl[e] = (r0 + e) >= 1;
-    hr[e] = (r0 + e) <= ch.P - 2;
+  for (int e = 0; e < 4; ++e) {
+    const float l = ln.hl[e] ? wl[e] : 0.f;
+    const float r = ln.hr[e] ? wr[e] : 0.f;
+    const float acc = fmaf(l, hm1[e], fmaf(wm[e], h[e], r * hp1[e]));
+    const float inv = prenorm ? 1.f : fast_rcp(wm[e] + l + r);
+    hn[e] = ln.valid[e] ? fmaf(acc, inv, lam[e] * x[e]) : 0.f;
   }
-  for (int tt = 0; tt < pl.K; ++tt) {
-    const int t = j * pl.K + tt;
-    if (t >= ch.L) break;
-    const int kk = ch.rev ? (pl.K - 1 - tt) : tt;
-    const uint32_t off = tg.vert(kk, r0);
-    float x[2], lam[2], wl[2], wm[2], wr[2];
-    V2<T>::load(st + F_X * pl.tile_bytes + off, x);
-    V2<T>::load(st + F_LAM * pl.tile_bytes + off, lam);
-    V2<T>::load(st + F_WL * pl.tile_bytes + off, wl);
-    V2<T>::load(st + F_WM * pl.tile_bytes + off, wm);
-    V2<T>::load(st + F_WR * pl.tile_bytes + off, wr);
-    float left = shfl_idx(h[1], (lane + 31) & 31);
-    float right = shfl_idx(h[0], (lane + 1) & 31);
-    float fl, fr;
-    halo_xchg(halo, par, wi, pl.nwc, lane, h[0], h[1], fl, fr);
-    if (lane == 0) left = fl;
-    if (lane == 31) right = fr;
-    float hn[2];
 #pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const float l = hl[e] ? wl[e] : 0.f;
-      const float r = hr[e] ? wr[e] : 0.f;
-      const float hm1 = (e == 0) ? left : h[0];
-      const float hp1 = (e == 1) ? right : h[1];
-      const float acc = fmaf(l, hm1, fmaf(wm[e], h[e], r * hp1));
-      const float inv = prenorm ? 1.f : fast_rcp(wm[e] + l + r);
-      hn[e] = valid[e] ? fmaf(acc, inv, lam[e] * x[e]) : 0.f;
-    }
-    h[0] = hn[0];
-    h[1] = hn[1];
-    V2<T>::store(ob + off, h);
+  for (int e = 0; e < 4; ++e) h[e] = hn[e];
+}
+
+// Element-order reversal of packed row chunks (runtime flag), so horizontal chains of both
+// directions see their steps in scan order: after it, element s of a row chunk is in-tile step s.
+__device__ __forceinline__ uint32_t swap16(uint32_t v) { return __byte_perm(v, 0, 0x1032); }
+template <typename T> struct Rev;
+template <> struct Rev<__nv_bfloat16> {
+  static __device__ __forceinline__ uint4 r(const uint4& u, bool rev) {
+    return rev ? make_uint4(swap16(u.w), swap16(u.z), swap16(u.y), swap16(u.x)) : u;
+  }
+  static __device__ __forceinline__ uint2 r(const uint2& u, bool rev) {
+    return rev ? make_uint2(swap16(u.y), swap16(u.x)) : u;
+  }
+};
+template <> struct Rev<float> {
+  static __device__ __forceinline__ uint4 r(const uint4& u, bool rev) { return rev ? make_uint4(u.w, u.z, u.y, u.x) : u; }
+  static __device__ __forceinline__ uint2 r(const uint2& u, bool rev) { return rev ? make_uint2(u.y, u.x) : u; }
+};
+
+// Vertical tile: the step loop stays rolled (code size); the in-tile row is a runtime offset.
+template <typename T>
+__device__ __forceinline__ void fwd_tile_vert(const Plan& pl, const Lanes& ln, const uint8_t* st, uint8_t* ob,
+                                              int lane, bool rev, float (&h)[4], bool prenorm) {
+  constexpr int K = Cfg<T>::K;
+  const int dk = rev ? -static_cast<int>(ln.vstep) : static_cast<int>(ln.vstep);
+  uint32_t off = ln.voff + (rev ? (K - 1) * ln.vstep : 0u);
+#pragma unroll 1
+  for (int s = 0; s < K; ++s, off += dk) {
+    float x[4], lam[4], wl[4], wm[4], wr[4];
+    V4<T>::load(st + F_X * pl.tile_bytes + off, x);
+    V4<T>::load(st + F_LAM * pl.tile_bytes + off, lam);
+    V4<T>::load(st + F_WL * pl.tile_bytes + off, wl);
+    V4<T>::load(st + F_WM * pl.tile_bytes + off, wm);
+    V4<T>::load(st + F_WR * pl.tile_bytes + off, wr);
+    const float left = from_lower_lane(h[3], lane);
+    const float right = from_upper_lane(h[0], lane);
+    const float hm1[4] = {left, h[0], h[1], h[2]};
+    const float hp1[4] = {h[1], h[2], h[3], right};
+    fwd_update(ln, x, lam, wl, wm, wr, hm1, hp1, h, prenorm);
+    if (ln.own[0]) V4<T>::store(ob + off, h);  // the lane's 4 positions are owned together
   }
 }
 
-// Horizontal tile: K steps (one 16-byte row chunk per tensor); lane owns rows wi*64 + q*32 + lane.
-template <typename T, bool kRev>
-__device__ __forceinline__ void fwd_tile_horiz(const Plan& pl, const Chain& ch, int j, const uint8_t* st, uint8_t* ob,
-                                               float* halo, int& par, int wi, int lane, float (&h)[2], bool prenorm) {
-  constexpr int K = Row<T>::K;
-  uint4 X[kNS], LAM[kNS], WL[kNS], WM[kNS], WR[kNS], OUT[kNS];
-  bool valid[kNS], hl[kNS], hr[kNS];
+// Horizontal tile: one 16-byte row chunk (K steps) per tensor per slot, put in scan order.
+template <typename T>
+__device__ __forceinline__ void fwd_tile_horiz(const Plan& pl, const Lanes& ln, const uint8_t* st, uint8_t* ob,
+                                               int lane, bool rev, float (&h)[4], bool prenorm) {
+  constexpr int K = Cfg<T>::K;
+  uint4 X[4], LAM[4], WL[4], WM[4], WR[4], OUT[4];
 #pragma unroll
-  for (int q = 0; q < kNS; ++q) {
-    const int r = wi * kLanePos + q * 32 + lane;
-    valid[q] = r < ch.P;
-    hl[q] = r >= 1;
-    hr[q] = r <= ch.P - 2;
-    const uint32_t off = static_cast<uint32_t>(r * 16);
-    X[q] = *reinterpret_cast<const uint4*>(st + F_X * pl.tile_bytes + off);
-    LAM[q] = *reinterpret_cast<const uint4*>(st + F_LAM * pl.tile_bytes + off);
-    WL[q] = *reinterpret_cast<const uint4*>(st + F_WL * pl.tile_bytes + off);
-    WM[q] = *reinterpret_cast<const uint4*>(st + F_WM * pl.tile_bytes + off);
-    WR[q] = *reinterpret_cast<const uint4*>(st + F_WR * pl.tile_bytes + off);
+  for (int q = 0; q < 4; ++q) {
+    const uint32_t off = ln.row[q] * 16;
+    X[q] = Rev<T>::r(*reinterpret_cast<const uint4*>(st + F_X * pl.tile_bytes + off), rev);
+    LAM[q] = Rev<T>::r(*reinterpret_cast<const uint4*>(st + F_LAM * pl.tile_bytes + off), rev);
+    WL[q] = Rev<T>::r(*reinterpret_cast<const uint4*>(st + F_WL * pl.tile_bytes + off), rev);
+    WM[q] = Rev<T>::r(*reinterpret_cast<const uint4*>(st + F_WM * pl.tile_bytes + off), rev);
+    WR[q] = Rev<T>::r(*reinterpret_cast<const uint4*>(st + F_WR * pl.tile_bytes + off), rev);
     OUT[q] = make_uint4(0, 0, 0, 0);
   }
 #pragma unroll
-  for (int tt = 0; tt < K; ++tt) {
-    const int t = j * K + tt;
-    if (t < ch.L) {
-      const int kk = kRev ? (K - 1 - tt) : tt;
-      float up[kNS], dn[kNS];
+  for (int s = 0; s < K; ++s) {
+    float up[4], dn[4], w_lo[4], w_hi[4];
 #pragma unroll
-      for (int q = 0; q < kNS; ++q) {
-        up[q] = shfl_idx(h[q], (lane + 31) & 31);
-        dn[q] = shfl_idx(h[q], (lane + 1) & 31);
-      }
-      float fl, fr;
-      halo_xchg(halo, par, wi, pl.nwc, lane, h[0], h[kNS - 1], fl, fr);
-      float hn[kNS];
-#pragma unroll
-      for (int q = 0; q < kNS; ++q) {
-        const float hm1 = (lane == 0) ? (q == 0 ? fl : up[q > 0 ? q - 1 : 0]) : up[q];
-        const float hp1 = (lane == 31) ? (q == kNS - 1 ? fr : dn[q + 1 < kNS ? q + 1 : q]) : dn[q];
-        const float wlv = hl[q] ? Row<T>::get(WL[q], kk) : 0.f;
-        const float wrv = hr[q] ? Row<T>::get(WR[q], kk) : 0.f;
-        const float wmv = Row<T>::get(WM[q], kk);
-        const float acc = fmaf(wlv, hm1, fmaf(wmv, h[q], wrv * hp1));
-        const float inv = prenorm ? 1.f : fast_rcp(wmv + wlv + wrv);
-        hn[q] = valid[q] ? fmaf(acc, inv, Row<T>::get(LAM[q], kk) * Row<T>::get(X[q], kk)) : 0.f;
-      }
-#pragma unroll
-      for (int q = 0; q < kNS; ++q) {
-        h[q] = hn[q];
-        Row<T>::set(OUT[q], kk, hn[q]);
-      }
+    for (int q = 0; q < 4; ++q) {
+      up[q] = __shfl_up_sync(0xffffffffu, h[q], 1);
+      dn[q] = __shfl_down_sync(0xffffffffu, h[q], 1);
+      w_lo[q] = __shfl_sync(0xffffffffu, h[q > 0 ? q - 1 : 0], 31);
+      w_hi[q] = __shfl_sync(0xffffffffu, h[q < 3 ? q + 1 : 3], 0);
     }
+    float hm1[4], hp1[4], x[4], lam[4], wl[4], wm[4], wr[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      // position A + 32 q + lane: its lower neighbour is lane-1 of slot q (lane 0: lane 31 of slot q-1)
+      hm1[q] = lane == 0 ? (q == 0 ? 0.f : w_lo[q]) : up[q];
+      hp1[q] = lane == 31 ? (q == 3 ? 0.f : w_hi[q]) : dn[q];
+      x[q] = Pk<T>::get(X[q], s);
+      lam[q] = Pk<T>::get(LAM[q], s);
+      wl[q] = Pk<T>::get(WL[q], s);
+      wm[q] = Pk<T>::get(WM[q], s);
+      wr[q] = Pk<T>::get(WR[q], s);
+    }
+    fwd_update(ln, x, lam, wl, wm, wr, hm1, hp1, h, prenorm);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) Pk<T>::set(OUT[q], s, h[q]);
   }
 #pragma unroll
-  for (int q = 0; q < kNS; ++q) {
-    const int r = wi * kLanePos + q * 32 + lane;
-    *reinterpret_cast<uint4*>(ob + r * 16) = OUT[q];
-  }
+  for (int q = 0; q < 4; ++q)
+    if (ln.own[q]) *reinterpret_cast<uint4*>(ob + ln.row[q] * 16) = Rev<T>::r(OUT[q], rev);
 }
 
 template <typename T, int kMaxNWC>
-__global__ void __launch_bounds__((kMaxNWC + 1) * 32, 1) fwd_stream_kernel(const __grid_constant__ StreamArgs A) {
+__global__ void __launch_bounds__((kMaxNWC + 1) * 32, kMaxNWC <= 6 ? 2 : 1)
+    fwd_stream_kernel(const __grid_constant__ StreamArgs A) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared address space
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared space
   const Plan& pl = A.plan;
   uint8_t* ring = smem;
   uint8_t* outbuf = ring + static_cast<size_t>(pl.nstages) * pl.stage_bytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(outbuf + 2 * static_cast<size_t>(pl.out_bytes));
   uint64_t* empty = full + pl.nstages;
-  float* halo = reinterpret_cast<float*>(empty + pl.nstages);
+  float* edge = reinterpret_cast<float*>(empty + pl.nstages);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < pl.nstages; ++s) {
@@ -506,38 +613,34 @@ __global__ void __launch_bounds__((kMaxNWC + 1) * 32, 1) fwd_stream_kernel(const
   }
   const bool prenorm = A.p.flags & GSPN_FLAG_PRENORMALIZED;
   const uint64_t pol_out = policy_evict_first();
-  TileGeom tg;
-  tg.K = pl.K;
-  tg.bw_log2 = 31 - __clz(pl.bw);
-  tg.es = pl.es;
+  const uint64_t pol_keep = policy_evict_last();  // horizontal outputs: the sector completes one tile later
   const int nthreads = pl.nwc * 32;
   int stage = 0, par = 0, ob_sel = 0;
   uint32_t phase = 0;
   for (int64_t w = blockIdx.x; w < pl.nchains; w += gridDim.x) {
     const Chain ch = make_chain(A.p, pl.K, w);
-    float h[2] = {0.f, 0.f};
+    const Lanes ln = make_lanes<T>(pl, ch, warp, lane);
+    float h[4] = {0.f, 0.f, 0.f, 0.f};
     for (int j = 0; j < ch.ntiles; ++j) {
       mbar_wait(smem_u32(&full[stage]), phase);
       const uint8_t* st = ring + static_cast<size_t>(stage) * pl.stage_bytes;
       uint8_t* ob = outbuf + static_cast<size_t>(ob_sel) * pl.out_bytes;
-      if (ch.vert) {
-        fwd_tile_vert<T>(pl, tg, ch, j, st, ob, halo, par, warp, lane, h, prenorm);
-      } else if (ch.rev) {
-        fwd_tile_horiz<T, true>(pl, ch, j, st, ob, halo, par, warp, lane, h, prenorm);
-      } else {
-        fwd_tile_horiz<T, false>(pl, ch, j, st, ob, halo, par, warp, lane, h, prenorm);
-      }
+      if (ch.vert) fwd_tile_vert<T>(pl, ln, st, ob, lane, ch.rev, h, prenorm);
+      else fwd_tile_horiz<T>(pl, ln, st, ob, lane, ch.rev, h, prenorm);
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&empty[stage]));
       if (++stage == pl.nstages) { stage = 0; phase ^= 1; }
+      edge_publish<T>(edge, par, warp, lane, ch.vert, h);
       fence_proxy_async();
       named_bar(kBarTile, nthreads);
       if (threadIdx.x == 0) {
         const int64_t planes[1] = {ch.chain};
-        store_tile(A, ch, j, ob, 1, planes, pol_out);
+        store_tile(A, ch, j, ob, 1, planes, ch.vert ? pol_out : pol_keep);
         bulk_wait_read1();
       }
+      edge_reload<T>(edge, par, warp, pl.nwc, lane, ch.vert, h);
       named_bar(kBarTile, nthreads);
+      par ^= 1;
       ob_sel ^= 1;
     }
   }
@@ -546,230 +649,246 @@ __global__ void __launch_bounds__((kMaxNWC + 1) * 32, 1) fwd_stream_kernel(const
 
 // ------------------------------------------------------------------------------ backward consumer
 
-// Vertical backward tile (reverse step order). ea/eb/ec carry a_{t+1} g_{t+1}, b_{t+1} g_{t+1},
-// c_{t+1} g_{t+1} of this lane's positions from the previously processed step.
+// State carried between steps (reverse order): ea = a_{t+1} g_{t+1}, eb = b_{t+1} g_{t+1},
+// ec = c_{t+1} g_{t+1} at the lane's 4 positions.
+struct BwdState {
+  float ea[4], eb[4], ec[4];
+};
+
+// One adjoint step for the lane's 4 positions. nr/nl: (a g) of the upper neighbour / (c g) of the
+// lower neighbour; hm1/h0/hp1: h_{t-1} at r-1, r, r+1. Outputs dlam, dw (or the tap gradients D
+// for the grouped path), dxv = g lam; the state is replaced by step t's products.
+template <bool kGrouped>
+__device__ __forceinline__ void bwd_update(const Lanes& ln, bool live, const float (&x)[4], const float (&lam)[4],
+                                           const float (&dh)[4], const float (&wl)[4], const float (&wm)[4],
+                                           const float (&wr)[4], const float (&hm1)[4], const float (&h0)[4],
+                                           const float (&hp1)[4], const float (&nr)[4], const float (&nl)[4],
+                                           BwdState& S, float (&dlam)[4], float (&o1)[4], float (&o2)[4],
+                                           float (&o3)[4], float (&dxv)[4], bool prenorm) {
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const bool ok = live && ln.valid[e];
+    const float g = ok ? (dh[e] + S.eb[e] + nr[e] + nl[e]) : 0.f;
+    const float l = ln.hl[e] ? wl[e] : 0.f;
+    const float r = ln.hr[e] ? wr[e] : 0.f;
+    const float inv = prenorm ? 1.f : fast_rcp(wm[e] + l + r);
+    dlam[e] = g * x[e];
+    dxv[e] = g * lam[e];
+    const float Da = ln.hl[e] ? g * hm1[e] : 0.f;
+    const float Db = g * h0[e];
+    const float Dc = ln.hr[e] ? g * hp1[e] : 0.f;
+    if (kGrouped || prenorm) {
+      o1[e] = Da; o2[e] = Db; o3[e] = Dc;
+    } else {  // normalisation Jacobian (gspn_common.cuh: jacobian): dw = (D - q)/S
+      const float inv2 = inv * inv;
+      o1[e] = ln.hl[e] ? fmaf(wm[e] + r, Da, -fmaf(wm[e], Db, r * Dc)) * inv2 : 0.f;
+      o2[e] = fmaf(l + r, Db, -fmaf(l, Da, r * Dc)) * inv2;
+      o3[e] = ln.hr[e] ? fmaf(l + wm[e], Dc, -fmaf(l, Da, wm[e] * Db)) * inv2 : 0.f;
+    }
+    S.ea[e] = ok ? l * inv * g : 0.f;
+    S.eb[e] = ok ? wm[e] * inv * g : 0.f;
+    S.ec[e] = ok ? r * inv * g : 0.f;
+  }
+}
+
 template <typename T, bool kGrouped>
-__device__ __forceinline__ void bwd_tile_vert(const StreamArgs& A, const TileGeom& tg, const Chain& ch, int j,
-                                              const uint8_t* st, uint8_t* ob, float* halo, int& par, int wi,
-                                              int lane, float (&ea)[2], float (&eb)[2], float (&ec)[2], bool prenorm,
+__device__ __forceinline__ void bwd_tile_vert(const StreamArgs& A, const Lanes& ln, const Chain& ch, int j,
+                                              const uint8_t* st, uint8_t* ob, int lane, BwdState& S, bool prenorm,
                                               uint64_t pol_acc) {
+  constexpr int K = Cfg<T>::K;
   const Plan& pl = A.plan;
   const ScanParams& p = A.p;
-  const int r0 = wi * kLanePos + lane * kE;
-  bool valid[2], hl[2], hr[2];
-#pragma unroll
-  for (int e = 0; e < 2; ++e) {
-    valid[e] = (r0 + e) < ch.P;
-    hl[e] = (r0 + e) >= 1;
-    hr[e] = (r0 + e) <= ch.P - 2;
-  }
   const int64_t HW = p.H * p.W;
   float* dxacc = p.dx_acc + ch.bc * HW;
-  float* dwa_l = kGrouped ? p.dwa_l + ch.wplane * HW : nullptr;
-  float* dwa_m = kGrouped ? p.dwa_m + ch.wplane * HW : nullptr;
-  float* dwa_r = kGrouped ? p.dwa_r + ch.wplane * HW : nullptr;
-  const int rl = (r0 >= 1) ? r0 - 1 : 0;  // clamped neighbour positions (masked by hl/hr)
-  const int rr = (r0 + 2 < pl.ppad) ? r0 + 2 : r0 + 1;
-  for (int tt = pl.K - 1; tt >= 0; --tt) {
-    const int t = j * pl.K + tt;
-    if (t >= ch.L) continue;
-    const int kk = ch.rev ? (pl.K - 1 - tt) : tt;
-    const uint32_t off = tg.vert(kk, r0);
-    float x[2], lam[2], dh[2], wl[2], wm[2], wr[2], hp[2];
-    V2<T>::load(st + B_X * pl.tile_bytes + off, x);
-    V2<T>::load(st + B_LAM * pl.tile_bytes + off, lam);
-    V2<T>::load(st + B_DH * pl.tile_bytes + off, dh);
-    V2<T>::load(st + B_WL * pl.tile_bytes + off, wl);
-    V2<T>::load(st + B_WM * pl.tile_bytes + off, wm);
-    V2<T>::load(st + B_WR * pl.tile_bytes + off, wr);
-    V2<T>::load(st + B_H * pl.tile_bytes + off, hp);
-    const uint8_t* hb = st + B_H * pl.tile_bytes;
-    const float hpl = to_f(*reinterpret_cast<const T*>(hb + tg.vert(kk, rl)));
-    const float hpr = to_f(*reinterpret_cast<const T*>(hb + tg.vert(kk, rr)));
-    // g_t = dh_t + b_{t+1} g_{t+1} + a_{t+1}[r+1] g_{t+1}[r+1] + c_{t+1}[r-1] g_{t+1}[r-1]
-    float from_right = shfl_idx(ea[0], (lane + 1) & 31);  // a g of position r0+2
-    float from_left = shfl_idx(ec[1], (lane + 31) & 31);  // c g of position r0-1
-    float fl, fr;
-    halo_xchg(halo, par, wi, pl.nwc, lane, ea[0], ec[1], fl, fr);
-    if (lane == 0) from_left = fl;
-    if (lane == 31) from_right = fr;
-    float g[2];
-    g[0] = valid[0] ? (dh[0] + eb[0] + ea[1] + from_left) : 0.f;
-    g[1] = valid[1] ? (dh[1] + eb[1] + from_right + ec[0]) : 0.f;
-    float dlam[2], dwl[2], dwm[2], dwr[2], Da[2], Db[2], Dc[2];
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const float l = hl[e] ? wl[e] : 0.f;
-      const float r = hr[e] ? wr[e] : 0.f;
-      const float inv = prenorm ? 1.f : fast_rcp(wm[e] + l + r);
-      const float a = l * inv, b = wm[e] * inv, c = r * inv;
-      dlam[e] = g[e] * x[e];
-      const float hm1 = (e == 0) ? hpl : hp[0];
-      const float hp1 = (e == 1) ? hpr : hp[1];
-      Da[e] = hl[e] ? g[e] * hm1 : 0.f;
-      Db[e] = g[e] * hp[e];
-      Dc[e] = hr[e] ? g[e] * hp1 : 0.f;
+  const int64_t wofs = ch.wplane * HW;
+  const bool lane_out = ln.own[0] && ln.valid[0];  // P % 4 == 0: a lane's 4 positions share validity
+  // steps s = K-1 .. 0 (reverse); in-tile row kk = rev ? K-1-s : s
+  const int dk = ch.rev ? static_cast<int>(ln.vstep) : -static_cast<int>(ln.vstep);
+  uint32_t off = ln.voff + (ch.rev ? 0u : (K - 1) * ln.vstep);
+#pragma unroll 1
+  for (int s = K - 1; s >= 0; --s, off += dk) {
+    const int t = j * K + s;
+    const bool live = t < ch.L;
+    float x[4], lam[4], dh[4], wl[4], wm[4], wr[4], hp[4];
+    V4<T>::load(st + B_X * pl.tile_bytes + off, x);
+    V4<T>::load(st + B_LAM * pl.tile_bytes + off, lam);
+    V4<T>::load(st + B_DH * pl.tile_bytes + off, dh);
+    V4<T>::load(st + B_WL * pl.tile_bytes + off, wl);
+    V4<T>::load(st + B_WM * pl.tile_bytes + off, wm);
+    V4<T>::load(st + B_WR * pl.tile_bytes + off, wr);
+    V4<T>::load(st + B_H * pl.tile_bytes + off, hp);
+    const float hpl = from_lower_lane(hp[3], lane);
+    const float hpr = from_upper_lane(hp[0], lane);
+    const float from_right = from_upper_lane(S.ea[0], lane);  // (a g) of position r0 + 4
+    const float from_left = from_lower_lane(S.ec[3], lane);   // (c g) of position r0 - 1
+    const float hm1[4] = {hpl, hp[0], hp[1], hp[2]};
+    const float hp1[4] = {hp[1], hp[2], hp[3], hpr};
+    const float nr[4] = {S.ea[1], S.ea[2], S.ea[3], from_right};
+    const float nl[4] = {from_left, S.ec[0], S.ec[1], S.ec[2]};
+    float dlam[4], o1[4], o2[4], o3[4], dxv[4];
+    bwd_update<kGrouped>(ln, live, x, lam, dh, wl, wm, wr, hm1, hp, hp1, nr, nl, S, dlam, o1, o2, o3, dxv, prenorm);
+    if (ln.own[0]) {
+      V4<T>::store(ob + O_DLAM * pl.tile_bytes + off, dlam);
       if (!kGrouped) {
-        if (prenorm) {
-          dwl[e] = Da[e]; dwm[e] = Db[e]; dwr[e] = Dc[e];
-        } else {  // normalisation Jacobian (gspn_common.cuh: jacobian), inv = 1/S
-          const float inv2 = inv * inv;
-          dwl[e] = hl[e] ? fmaf(wm[e] + r, Da[e], -fmaf(wm[e], Db[e], r * Dc[e])) * inv2 : 0.f;
-          dwm[e] = valid[e] ? fmaf(l + r, Db[e], -fmaf(l, Da[e], r * Dc[e])) * inv2 : 0.f;
-          dwr[e] = hr[e] ? fmaf(l + wm[e], Dc[e], -fmaf(l, Da[e], wm[e] * Db[e])) * inv2 : 0.f;
-        }
+        V4<T>::store(ob + O_DWL * pl.tile_bytes + off, o1);
+        V4<T>::store(ob + O_DWM * pl.tile_bytes + off, o2);
+        V4<T>::store(ob + O_DWR * pl.tile_bytes + off, o3);
       }
-      ea[e] = valid[e] ? a * g[e] : 0.f;
-      eb[e] = valid[e] ? b * g[e] : 0.f;
-      ec[e] = valid[e] ? c * g[e] : 0.f;
     }
-    V2<T>::store(ob + O_DLAM * pl.tile_bytes + off, dlam);
-    if (!kGrouped) {
-      V2<T>::store(ob + O_DWL * pl.tile_bytes + off, dwl);
-      V2<T>::store(ob + O_DWM * pl.tile_bytes + off, dwm);
-      V2<T>::store(ob + O_DWR * pl.tile_bytes + off, dwr);
-    }
-    if (valid[0]) {  // W % 2 == 0 on this path: both positions valid or both padding
+    if (lane_out && live) {
       const int row = ch.rev ? (ch.L - 1 - t) : t;
-      const int64_t o = static_cast<int64_t>(row) * p.W + r0;
-      red_add_v2(dxacc + o, g[0] * lam[0], g[1] * lam[1], pol_acc);
+      const int64_t o = static_cast<int64_t>(row) * p.W + ln.pos[0];
+      red_add_v4(dxacc + o, dxv[0], dxv[1], dxv[2], dxv[3], pol_acc);
       if (kGrouped && t >= 1) {
-        red_add_v2(dwa_l + o, Da[0], Da[1], pol_acc);
-        red_add_v2(dwa_m + o, Db[0], Db[1], pol_acc);
-        red_add_v2(dwa_r + o, Dc[0], Dc[1], pol_acc);
+        red_add_v4(p.dwa_l + wofs + o, o1[0], o1[1], o1[2], o1[3], pol_acc);
+        red_add_v4(p.dwa_m + wofs + o, o2[0], o2[1], o2[2], o2[3], pol_acc);
+        red_add_v4(p.dwa_r + wofs + o, o3[0], o3[1], o3[2], o3[3], pol_acc);
       }
     }
   }
 }
 
-// Horizontal backward tile (reverse step order); lane owns rows wi*64 + q*32 + lane.
-template <typename T, bool kRev, bool kGrouped>
-__device__ __forceinline__ void bwd_tile_horiz(const StreamArgs& A, const Chain& ch, int j, const uint8_t* st,
-                                               uint8_t* ob, float* halo, int& par, int wi, int lane, float (&ea)[2],
-                                               float (&eb)[2], float (&ec)[2], bool prenorm, uint64_t pol_acc) {
-  constexpr int K = Row<T>::K;
-  constexpr int es = static_cast<int>(sizeof(T));
+// Horizontal backward tile. Rows of x, lam, dh and the taps come in as 16-byte chunks (K steps,
+// put in scan order); they are processed as NSUB sub-tiles of KS steps (the upper half first: the
+// backward walks the steps downwards) with the working half selected at run time, which keeps one
+// copy of the unrolled step code. h_{t-1} is read per step from the 2K-step swizzled h row.
+template <typename T, bool kGrouped>
+__device__ __forceinline__ void bwd_tile_horiz(const StreamArgs& A, const Lanes& ln, const Chain& ch, int j,
+                                               const uint8_t* st, uint8_t* ob, int lane, BwdState& S, bool prenorm,
+                                               uint64_t pol_acc) {
+  using C = Cfg<T>;
+  constexpr int K = C::K, KS = C::KS, NSUB = K / KS;
+  static_assert(NSUB == 2, "sub-tiles are the two 8-byte halves of a 16-byte row chunk");
   const Plan& pl = A.plan;
   const ScanParams& p = A.p;
+  const bool rev = ch.rev;
   const int64_t HW = p.H * p.W;
   float* dxacc = p.dx_acc + ch.bc * HW;
-  float* dwa_l = kGrouped ? p.dwa_l + ch.wplane * HW : nullptr;
-  float* dwa_m = kGrouped ? p.dwa_m + ch.wplane * HW : nullptr;
-  float* dwa_r = kGrouped ? p.dwa_r + ch.wplane * HW : nullptr;
+  const int64_t wofs = ch.wplane * HW;
   const int c0 = tile_start(ch, j, K);  // canonical column of kk = 0 (W % K == 0 on this path)
-  bool valid[kNS], hl[kNS], hr[kNS];
-  uint4 X[kNS], LAM[kNS], DH[kNS], WL[kNS], WM[kNS], WR[kNS], HP0[kNS], HP1[kNS];
-  // h tile: rows of 2K steps (32 bytes) with the TMA 32-byte swizzle (16-byte chunk ^= row bit 2)
   const uint8_t* hbase = st + B_H * pl.tile_bytes;
-  auto swz = [](int r, int c) { return static_cast<uint32_t>(r * 32 + ((c ^ ((r >> 2) & 1)) << 4)); };
-  uint4 O0[kNS], O1[kNS], O2[kNS], O3[kNS];
-  float DX[kNS][K];
+  uint4 X[4], LAM[4], DH[4], WL[4], WM[4], WR[4];
 #pragma unroll
-  for (int q = 0; q < kNS; ++q) {
-    const int r = wi * kLanePos + q * 32 + lane;
-    valid[q] = r < ch.P;
-    hl[q] = r >= 1;
-    hr[q] = r <= ch.P - 2;
-    const uint32_t off = static_cast<uint32_t>(r * 16);
-    X[q] = *reinterpret_cast<const uint4*>(st + B_X * pl.tile_bytes + off);
-    LAM[q] = *reinterpret_cast<const uint4*>(st + B_LAM * pl.tile_bytes + off);
-    DH[q] = *reinterpret_cast<const uint4*>(st + B_DH * pl.tile_bytes + off);
-    WL[q] = *reinterpret_cast<const uint4*>(st + B_WL * pl.tile_bytes + off);
-    WM[q] = *reinterpret_cast<const uint4*>(st + B_WM * pl.tile_bytes + off);
-    WR[q] = *reinterpret_cast<const uint4*>(st + B_WR * pl.tile_bytes + off);
-    HP0[q] = *reinterpret_cast<const uint4*>(hbase + swz(r, 0));
-    HP1[q] = *reinterpret_cast<const uint4*>(hbase + swz(r, 1));
-    O0[q] = O1[q] = O2[q] = O3[q] = make_uint4(0, 0, 0, 0);
+  for (int q = 0; q < 4; ++q) {
+    const uint32_t off = ln.row[q] * 16;
+    X[q] = Rev<T>::r(*reinterpret_cast<const uint4*>(st + B_X * pl.tile_bytes + off), rev);
+    LAM[q] = Rev<T>::r(*reinterpret_cast<const uint4*>(st + B_LAM * pl.tile_bytes + off), rev);
+    DH[q] = Rev<T>::r(*reinterpret_cast<const uint4*>(st + B_DH * pl.tile_bytes + off), rev);
+    WL[q] = Rev<T>::r(*reinterpret_cast<const uint4*>(st + B_WL * pl.tile_bytes + off), rev);
+    WM[q] = Rev<T>::r(*reinterpret_cast<const uint4*>(st + B_WM * pl.tile_bytes + off), rev);
+    WR[q] = Rev<T>::r(*reinterpret_cast<const uint4*>(st + B_WR * pl.tile_bytes + off), rev);
   }
-  // rows just outside this warp's range (for h_{t-1}[r-1] of lane 0 / [r+1] of lane 31)
-  const int row_lo = wi * kLanePos - 1, row_hi = wi * kLanePos + kLanePos;
-  const int rlo = row_lo >= 0 ? row_lo : 0;
-  const int rhi = row_hi < pl.ppad ? row_hi : pl.ppad - 1;
+  // byte offset of h element e of row r in the 32-byte-swizzled h tile (16-byte chunk ^= row bit 2)
+  auto hoff = [](uint32_t r, int e) {
+    const int c16 = e / K;
+    return r * 32 + ((static_cast<uint32_t>(c16) ^ ((r >> 2) & 1)) << 4) + (e % K) * Cfg<T>::es;
+  };
+#pragma unroll 1
+  for (int sub = NSUB - 1; sub >= 0; --sub) {
+    uint2 x2[4], lam2[4], dh2[4], wl2[4], wm2[4], wr2[4];
 #pragma unroll
-  for (int tt = K - 1; tt >= 0; --tt) {
-    const int t = j * K + tt;
-    const int kk = kRev ? (K - 1 - tt) : tt;
-    const int he = kRev ? (kk + 1) : (K + kk - 1);  // h_{t-1} element in the 2K-step h row
-    if (t < ch.L) {
-      float from_right[kNS], from_left[kNS], hv[kNS], hup[kNS], hdn[kNS];
+    for (int q = 0; q < 4; ++q) {
+      x2[q] = sub ? make_uint2(X[q].z, X[q].w) : make_uint2(X[q].x, X[q].y);
+      lam2[q] = sub ? make_uint2(LAM[q].z, LAM[q].w) : make_uint2(LAM[q].x, LAM[q].y);
+      dh2[q] = sub ? make_uint2(DH[q].z, DH[q].w) : make_uint2(DH[q].x, DH[q].y);
+      wl2[q] = sub ? make_uint2(WL[q].z, WL[q].w) : make_uint2(WL[q].x, WL[q].y);
+      wm2[q] = sub ? make_uint2(WM[q].z, WM[q].w) : make_uint2(WM[q].x, WM[q].y);
+      wr2[q] = sub ? make_uint2(WR[q].z, WR[q].w) : make_uint2(WR[q].x, WR[q].y);
+    }
+    uint2 OL[4], O1[4], O2[4], O3[4];
+    float DXa[4][KS], DA[4][KS], DB[4][KS], DC[4][KS];
 #pragma unroll
-      for (int q = 0; q < kNS; ++q) {
-        from_right[q] = shfl_idx(ea[q], (lane + 1) & 31);
-        from_left[q] = shfl_idx(ec[q], (lane + 31) & 31);
-        hv[q] = (he < K) ? Row<T>::get(HP0[q], he) : Row<T>::get(HP1[q], he - K);
-        hup[q] = shfl_idx(hv[q], (lane + 31) & 31);
-        hdn[q] = shfl_idx(hv[q], (lane + 1) & 31);
+    for (int q = 0; q < 4; ++q) OL[q] = O1[q] = O2[q] = O3[q] = make_uint2(0, 0);
+#pragma unroll
+    for (int ss = KS - 1; ss >= 0; --ss) {
+      const int s = sub * KS + ss;  // in-tile step (scan order)
+      const int t = j * K + s;
+      // h_{t-1}: element K + s - 1 (L2R) / K - s (R2L) of the canonical 2K-step h row
+      const int he = rev ? (K - s) : (K + s - 1);
+      float x[4], lam[4], dh[4], wl[4], wm[4], wr[4], h0[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        x[q] = Pk<T>::get(x2[q], ss);
+        lam[q] = Pk<T>::get(lam2[q], ss);
+        dh[q] = Pk<T>::get(dh2[q], ss);
+        wl[q] = Pk<T>::get(wl2[q], ss);
+        wm[q] = Pk<T>::get(wm2[q], ss);
+        wr[q] = Pk<T>::get(wr2[q], ss);
+        h0[q] = to_f(*reinterpret_cast<const T*>(hbase + hoff(ln.row[q], he)));
       }
-      const float h_lo = to_f(*reinterpret_cast<const T*>(hbase + swz(rlo, he / K) + (he % K) * es));
-      const float h_hi = to_f(*reinterpret_cast<const T*>(hbase + swz(rhi, he / K) + (he % K) * es));
-      float fl, fr;
-      halo_xchg(halo, par, wi, pl.nwc, lane, ea[0], ec[kNS - 1], fl, fr);
+      float hm1[4], hp1[4], nr[4], nl[4];
 #pragma unroll
-      for (int q = 0; q < kNS; ++q) {
-        const float nr = (lane == 31) ? (q == kNS - 1 ? fr : from_right[q + 1 < kNS ? q + 1 : q]) : from_right[q];
-        const float nl = (lane == 0) ? (q == 0 ? fl : from_left[q > 0 ? q - 1 : 0]) : from_left[q];
-        const float hpl = (lane == 0) ? (q == 0 ? h_lo : hup[q > 0 ? q - 1 : 0]) : hup[q];
-        const float hpr = (lane == 31) ? (q == kNS - 1 ? h_hi : hdn[q + 1 < kNS ? q + 1 : q]) : hdn[q];
-        const float g = valid[q] ? (Row<T>::get(DH[q], kk) + eb[q] + nr + nl) : 0.f;
-        const float wl = Row<T>::get(WL[q], kk), wm = Row<T>::get(WM[q], kk), wr = Row<T>::get(WR[q], kk);
-        const float l = hl[q] ? wl : 0.f;
-        const float rr = hr[q] ? wr : 0.f;
-        const float inv = prenorm ? 1.f : fast_rcp(wm + l + rr);
-        const float a = l * inv, b = wm * inv, c = rr * inv;
-        const float Da = hl[q] ? g * hpl : 0.f;
-        const float Db = g * hv[q];
-        const float Dc = hr[q] ? g * hpr : 0.f;
-        Row<T>::set(O0[q], kk, g * Row<T>::get(X[q], kk));
+      for (int q = 0; q < 4; ++q) {
+        const float hu = __shfl_up_sync(0xffffffffu, h0[q], 1);
+        const float hd = __shfl_down_sync(0xffffffffu, h0[q], 1);
+        const float au = __shfl_down_sync(0xffffffffu, S.ea[q], 1);
+        const float cd = __shfl_up_sync(0xffffffffu, S.ec[q], 1);
+        const float hw_lo = __shfl_sync(0xffffffffu, h0[q > 0 ? q - 1 : 0], 31);
+        const float hw_hi = __shfl_sync(0xffffffffu, h0[q < 3 ? q + 1 : 3], 0);
+        const float aw_hi = __shfl_sync(0xffffffffu, S.ea[q < 3 ? q + 1 : 3], 0);
+        const float cw_lo = __shfl_sync(0xffffffffu, S.ec[q > 0 ? q - 1 : 0], 31);
+        hm1[q] = lane == 0 ? (q == 0 ? 0.f : hw_lo) : hu;
+        hp1[q] = lane == 31 ? (q == 3 ? 0.f : hw_hi) : hd;
+        nr[q] = lane == 31 ? (q == 3 ? 0.f : aw_hi) : au;
+        nl[q] = lane == 0 ? (q == 0 ? 0.f : cw_lo) : cd;
+      }
+      float dlam[4], o1[4], o2[4], o3[4], dxv[4];
+      bwd_update<kGrouped>(ln, true, x, lam, dh, wl, wm, wr, hm1, h0, hp1, nr, nl, S, dlam, o1, o2, o3, dxv, prenorm);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        Pk<T>::set(OL[q], ss, dlam[q]);
         if (!kGrouped) {
-          float dwl, dwm, dwr;
-          if (prenorm) {
-            dwl = Da; dwm = Db; dwr = Dc;
-          } else {  // normalisation Jacobian (gspn_common.cuh: jacobian), inv = 1/S
-            const float inv2 = inv * inv;
-            dwl = hl[q] ? fmaf(wm + rr, Da, -fmaf(wm, Db, rr * Dc)) * inv2 : 0.f;
-            dwm = valid[q] ? fmaf(l + rr, Db, -fmaf(l, Da, rr * Dc)) * inv2 : 0.f;
-            dwr = hr[q] ? fmaf(l + wm, Dc, -fmaf(l, Da, wm * Db)) * inv2 : 0.f;
-          }
-          Row<T>::set(O1[q], kk, dwl);
-          Row<T>::set(O2[q], kk, dwm);
-          Row<T>::set(O3[q], kk, dwr);
-        } else if (valid[q] && t >= 1) {
-          const int r = wi * kLanePos + q * 32 + lane;
-          const int64_t o = static_cast<int64_t>(r) * p.W + c0 + kk;
-          red_add_f32(dwa_l + o, Da, pol_acc);
-          red_add_f32(dwa_m + o, Db, pol_acc);
-          red_add_f32(dwa_r + o, Dc, pol_acc);
+          Pk<T>::set(O1[q], ss, o1[q]);
+          Pk<T>::set(O2[q], ss, o2[q]);
+          Pk<T>::set(O3[q], ss, o3[q]);
+        } else {
+          DA[q][ss] = t >= 1 ? o1[q] : 0.f;
+          DB[q][ss] = t >= 1 ? o2[q] : 0.f;
+          DC[q][ss] = t >= 1 ? o3[q] : 0.f;
         }
-        DX[q][kk] = g * Row<T>::get(LAM[q], kk);
-        ea[q] = valid[q] ? a * g : 0.f;
-        eb[q] = valid[q] ? b * g : 0.f;
-        ec[q] = valid[q] ? c * g : 0.f;
+        DXa[q][ss] = dxv[q];
       }
-    } else {
-#pragma unroll
-      for (int q = 0; q < kNS; ++q) DX[q][kk] = 0.f;
     }
-  }
+    // write back in canonical order: chunk c8 of the row, elements reversed for R2L
+    const int c8 = rev ? (NSUB - 1 - sub) : sub;
 #pragma unroll
-  for (int q = 0; q < kNS; ++q) {
-    const int r = wi * kLanePos + q * 32 + lane;
-    *reinterpret_cast<uint4*>(ob + O_DLAM * pl.tile_bytes + r * 16) = O0[q];
-    if (!kGrouped) {
-      *reinterpret_cast<uint4*>(ob + O_DWL * pl.tile_bytes + r * 16) = O1[q];
-      *reinterpret_cast<uint4*>(ob + O_DWM * pl.tile_bytes + r * 16) = O2[q];
-      *reinterpret_cast<uint4*>(ob + O_DWR * pl.tile_bytes + r * 16) = O3[q];
-    }
-    if (valid[q]) {
-      const int64_t o = static_cast<int64_t>(r) * p.W + c0;
+    for (int q = 0; q < 4; ++q) {
+      if (!ln.own[q]) continue;
+      const uint32_t off = ln.row[q] * 16 + c8 * 8;
+      *reinterpret_cast<uint2*>(ob + O_DLAM * pl.tile_bytes + off) = Rev<T>::r(OL[q], rev);
+      if (!kGrouped) {
+        *reinterpret_cast<uint2*>(ob + O_DWL * pl.tile_bytes + off) = Rev<T>::r(O1[q], rev);
+        *reinterpret_cast<uint2*>(ob + O_DWM * pl.tile_bytes + off) = Rev<T>::r(O2[q], rev);
+        *reinterpret_cast<uint2*>(ob + O_DWR * pl.tile_bytes + off) = Rev<T>::r(O3[q], rev);
+      }
+      if (ln.valid[q]) {
+        const int64_t o = static_cast<int64_t>(ln.pos[q]) * p.W + c0 + c8 * KS;
+        float d[KS];
 #pragma unroll
-      for (int v = 0; v < K; v += 4) red_add_v4(dxacc + o + v, DX[q][v], DX[q][v + 1], DX[q][v + 2], DX[q][v + 3], pol_acc);
+        for (int i = 0; i < KS; ++i) d[i] = rev ? DXa[q][KS - 1 - i] : DXa[q][i];
+        if (KS == 4) red_add_v4(dxacc + o, d[0], d[1 % KS], d[2 % KS], d[3 % KS], pol_acc);
+        else red_add_v2(dxacc + o, d[0], d[1 % KS], pol_acc);
+        if (kGrouped) {
+          float* dst[3] = {p.dwa_l + wofs + o, p.dwa_m + wofs + o, p.dwa_r + wofs + o};
+#pragma unroll
+          for (int m = 0; m < 3; ++m) {
+#pragma unroll
+            for (int i = 0; i < KS; ++i) {
+              const int si = rev ? KS - 1 - i : i;
+              d[i] = m == 0 ? DA[q][si] : (m == 1 ? DB[q][si] : DC[q][si]);
+            }
+            if (KS == 4) red_add_v4(dst[m], d[0], d[1 % KS], d[2 % KS], d[3 % KS], pol_acc);
+            else red_add_v2(dst[m], d[0], d[1 % KS], pol_acc);
+          }
+        }
+      }
     }
   }
 }
 
-// The last of a plane's D chains converts the fp32 dx accumulator; the last of a group's C/G channels
-// applies the normalisation Jacobian to the group-summed tap gradients:
-// q = a Da + b Db + c Dc; dw_l = [r>=1](Da - q)/S, dw_m = (Db - q)/S, dw_r = [r<=P-2](Dc - q)/S.
+// The last of a plane's D chains converts the fp32 dx accumulator and drops it from L2 (discard: no
+// write-back of dead lines); the last of a group's C/G channels applies the normalisation Jacobian
+// to the group-summed tap gradients.
 template <typename T, bool kGrouped>
 __device__ void bwd_chain_epilogue(const StreamArgs& A, const Chain& ch, int* flag, int nthreads) {
   const ScanParams& p = A.p;
@@ -790,7 +909,24 @@ __device__ void bwd_chain_epilogue(const StreamArgs& A, const Chain& ch, int* fl
   if (f & 1) {
     const float4* src = reinterpret_cast<const float4*>(p.dx_acc + ch.bc * HW);
     T* dst = static_cast<T*>(p.dx) + ch.bc * HW;
-    for (int64_t i = threadIdx.x; i < HW / 4; i += nthreads) store4<T>(dst + 4 * i, __ldcg(src + i));
+    const int64_t n4 = HW / 4;
+    constexpr int U = 8;  // independent L2 loads in flight per thread
+    for (int64_t i0 = threadIdx.x; i0 < n4; i0 += static_cast<int64_t>(U) * nthreads) {
+      float4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t i = i0 + static_cast<int64_t>(u) * nthreads;
+        v[u] = i < n4 ? __ldcg(src + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t i = i0 + static_cast<int64_t>(u) * nthreads;
+        if (i < n4) store4_global<T>(dst + 4 * i, v[u]);
+      }
+    }
+    named_bar(kBarTile, nthreads);
+    const char* base = reinterpret_cast<const char*>(p.dx_acc + ch.bc * HW);
+    for (int64_t l = threadIdx.x; l < (HW * 4) / 128; l += nthreads) discard_l2_line(base + l * 128);
   }
   if (kGrouped && (f & 2)) {
     const bool prenorm = p.flags & GSPN_FLAG_PRENORMALIZED;
@@ -816,14 +952,14 @@ __device__ void bwd_chain_epilogue(const StreamArgs& A, const Chain& ch, int* fl
 template <typename T, bool kGrouped, int kMaxNWC>
 __global__ void __launch_bounds__((kMaxNWC + 1) * 32, 1) bwd_stream_kernel(const __grid_constant__ StreamArgs A) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared address space
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared space
   const Plan& pl = A.plan;
   uint8_t* ring = smem;
   uint8_t* outbuf = ring + static_cast<size_t>(pl.nstages) * pl.stage_bytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(outbuf + 2 * static_cast<size_t>(pl.out_bytes));
   uint64_t* empty = full + pl.nstages;
-  float* halo = reinterpret_cast<float*>(empty + pl.nstages);
-  int* flag = reinterpret_cast<int*>(halo + 4 * kHaloW);
+  float* edge = reinterpret_cast<float*>(empty + pl.nstages);  // [3 state arrays][2 par][kEdgeW][2][8]
+  int* flag = reinterpret_cast<int*>(edge + 3 * 2 * kEdgeW * 2 * 8);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < pl.nstages; ++s) {
@@ -843,40 +979,43 @@ __global__ void __launch_bounds__((kMaxNWC + 1) * 32, 1) bwd_stream_kernel(const
   }
   const bool prenorm = A.p.flags & GSPN_FLAG_PRENORMALIZED;
   const uint64_t pol_out = policy_evict_first();
+  const uint64_t pol_keep = policy_evict_last();  // horizontal outputs: the sector completes one tile later
   const uint64_t pol_acc = policy_evict_last();
-  TileGeom tg;
-  tg.K = pl.K;
-  tg.bw_log2 = 31 - __clz(pl.bw);
-  tg.es = pl.es;
   const int nthreads = pl.nwc * 32;
+  constexpr int kEdgeArr = 2 * kEdgeW * 2 * 8;
   int stage = 0, par = 0, ob_sel = 0;
   uint32_t phase = 0;
   for (int64_t w = blockIdx.x; w < pl.nchains; w += gridDim.x) {
     const Chain ch = make_chain(A.p, pl.K, w);
-    float ea[2] = {0.f, 0.f}, eb[2] = {0.f, 0.f}, ec[2] = {0.f, 0.f};
+    const Lanes ln = make_lanes<T>(pl, ch, warp, lane);
+    BwdState S;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) S.ea[e] = S.eb[e] = S.ec[e] = 0.f;
     for (int jj = 0; jj < ch.ntiles; ++jj) {
       const int j = ch.ntiles - 1 - jj;
       mbar_wait(smem_u32(&full[stage]), phase);
       const uint8_t* st = ring + static_cast<size_t>(stage) * pl.stage_bytes;
       uint8_t* ob = outbuf + static_cast<size_t>(ob_sel) * pl.out_bytes;
-      if (ch.vert) {
-        bwd_tile_vert<T, kGrouped>(A, tg, ch, j, st, ob, halo, par, warp, lane, ea, eb, ec, prenorm, pol_acc);
-      } else if (ch.rev) {
-        bwd_tile_horiz<T, true, kGrouped>(A, ch, j, st, ob, halo, par, warp, lane, ea, eb, ec, prenorm, pol_acc);
-      } else {
-        bwd_tile_horiz<T, false, kGrouped>(A, ch, j, st, ob, halo, par, warp, lane, ea, eb, ec, prenorm, pol_acc);
-      }
+      if (ch.vert) bwd_tile_vert<T, kGrouped>(A, ln, ch, j, st, ob, lane, S, prenorm, pol_acc);
+      else bwd_tile_horiz<T, kGrouped>(A, ln, ch, j, st, ob, lane, S, prenorm, pol_acc);
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&empty[stage]));
       if (++stage == pl.nstages) { stage = 0; phase ^= 1; }
+      edge_publish<T>(edge + 0 * kEdgeArr, par, warp, lane, ch.vert, S.ea);
+      edge_publish<T>(edge + 1 * kEdgeArr, par, warp, lane, ch.vert, S.eb);
+      edge_publish<T>(edge + 2 * kEdgeArr, par, warp, lane, ch.vert, S.ec);
       fence_proxy_async();
       named_bar(kBarTile, nthreads);
       if (threadIdx.x == 0) {
         const int64_t planes[4] = {ch.chain, ch.wplane, ch.wplane, ch.wplane};
-        store_tile(A, ch, j, ob, kGrouped ? 1 : 4, planes, pol_out);
+        store_tile(A, ch, j, ob, kGrouped ? 1 : 4, planes, ch.vert ? pol_out : pol_keep);
         bulk_wait_read1();
       }
+      edge_reload<T>(edge + 0 * kEdgeArr, par, warp, pl.nwc, lane, ch.vert, S.ea);
+      edge_reload<T>(edge + 1 * kEdgeArr, par, warp, pl.nwc, lane, ch.vert, S.eb);
+      edge_reload<T>(edge + 2 * kEdgeArr, par, warp, pl.nwc, lane, ch.vert, S.ec);
       named_bar(kBarTile, nthreads);
+      par ^= 1;
       ob_sel ^= 1;
     }
     bwd_chain_epilogue<T, kGrouped>(A, ch, flag, nthreads);
@@ -900,7 +1039,7 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 bool encode(CUtensorMap* m, const void* base, gspn_dtype_t dt, int64_t W, int64_t H, int64_t planes, int box0,
-            int box1, bool promote, bool swizzle32 = false) {
+            int box1, CUtensorMapL2promotion promote, bool swizzle32 = false) {
   auto fn = get_encode();
   if (!fn) return false;
   const size_t s = dt == GSPN_BF16 ? 2 : 4;
@@ -911,7 +1050,7 @@ bool encode(CUtensorMap* m, const void* base, gspn_dtype_t dt, int64_t W, int64_
   CUresult r = fn(m, dt == GSPN_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
                   const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                   swizzle32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE,
-                  promote ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                  promote,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -938,15 +1077,26 @@ int smem_optin() {
   return n;
 }
 
-// Largest power-of-two box extent (<= 256, >= min_box) whose boxes tile n positions inside ppad.
-int pick_box(int64_t n, int ppad, int min_box) {
-  for (int b = 256; b >= min_box; b >>= 1)
-    if (((n + b - 1) / b) * b <= ppad) return b;
-  return 0;
+// L2 promotion of the horizontal (16-byte row chunk) TMA loads; GSPN_L2PROMO=0|64|128|256 overrides
+// (experiments only). Default: none — the next tile's chunk shares the 32-byte sector anyway.
+CUtensorMapL2promotion horiz_promotion() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("GSPN_L2PROMO");
+    v = e ? atoi(e) : 0;
+  }
+  switch (v) {
+    case 64: return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+    case 128: return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+    case 256: return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    default: return CU_TENSOR_MAP_L2_PROMOTION_NONE;
+  }
 }
 
+constexpr int kSmemTail = 8192;  // mbarriers, ghost-edge buffers, flags
+
 // Shape eligibility + plan. nin/nout: tensors per tile.
-bool make_plan(const ScanParams& p, gspn_dtype_t dt, int nin, int nout, int min_stages, Plan* pl) {
+bool make_plan(const ScanParams& p, gspn_dtype_t dt, int nin, int nout, int min_stages, bool two_ctas, Plan* pl) {
   const int s = dt == GSPN_BF16 ? 2 : 4;
   if ((p.W * s) % 16 != 0) return false;  // TMA global stride alignment; also K | W for horizontal tiles
   bool any_v = false, any_h = false;
@@ -954,18 +1104,27 @@ bool make_plan(const ScanParams& p, gspn_dtype_t dt, int nin, int nout, int min_
     if (p.dirbit[k] == GSPN_DIR_T2B || p.dirbit[k] == GSPN_DIR_B2T) any_v = true; else any_h = true;
   }
   const int64_t maxP = std::max<int64_t>(any_v ? p.W : 0, any_h ? p.H : 0);
-  if (maxP > static_cast<int64_t>(kLanePos) * kHaloW) return false;
   memset(pl, 0, sizeof *pl);
   pl->K = 16 / s;
   pl->es = s;
-  pl->nwc = static_cast<int>((maxP + kLanePos - 1) / kLanePos);
-  pl->ppad = kLanePos * pl->nwc;
-  pl->bw = pick_box(p.W, pl->ppad, 16 / s);
-  pl->bh = pick_box(p.H, pl->ppad, 1);
-  if (any_v && pl->bw == 0) return false;
-  if (any_h && pl->bh == 0) return false;
-  if (pl->bw == 0) pl->bw = 16 / s;
-  if (pl->bh == 0) pl->bh = 1;
+  pl->own = kWarpPos - 2 * pl->K;
+  pl->nwc = static_cast<int>((maxP + pl->own - 1) / pl->own);
+  if (pl->nwc > kEdgeW) return false;
+  // positions addressable in a tile: every owned position, a whole number of vertical boxes
+  int ppad = static_cast<int>((maxP + 63) / 64 * 64);
+  int bw = 0;
+  for (int b = 256; b >= 16 / s; b >>= 1)
+    if (ppad % b == 0 && (p.W + b - 1) / b * b <= ppad) { bw = b; break; }
+  if (bw == 0) {  // round ppad up to the widest box that tiles W
+    bw = 64;
+    ppad = (ppad + 63) / 64 * 64;
+  }
+  pl->ppad = ppad;
+  pl->bw = bw;
+  pl->bh = 0;
+  for (int b = 256; b >= 1; b >>= 1)
+    if ((p.H + b - 1) / b * b <= ppad) { pl->bh = b; break; }
+  if (pl->bh == 0) return false;
   pl->nbw = static_cast<int>((p.W + pl->bw - 1) / pl->bw);
   pl->nbh = static_cast<int>((p.H + pl->bh - 1) / pl->bh);
   pl->nin = nin;
@@ -976,14 +1135,19 @@ bool make_plan(const ScanParams& p, gspn_dtype_t dt, int nin, int nout, int min_
   pl->out_bytes = nout * pl->tile_bytes;
   pl->tx_v = static_cast<uint32_t>(nin * pl->nbw * pl->bw * pl->K * s);
   pl->tx_h = static_cast<uint32_t>((nin + pl->h_wide) * pl->nbh * pl->bh * pl->K * s);
-  const int budget = smem_optin() - 1024 /*alignment*/ - 512 /*barriers, halo, flag*/;
+  const int budget = smem_optin() - 1024 /*alignment*/ - kSmemTail;
   const int avail = budget - 2 * static_cast<int>(pl->out_bytes);
   int ns = avail / static_cast<int>(pl->stage_bytes);
+  // Two CTAs per SM when both fit with >= 2 stages each: the second chain hides the first's
+  // per-tile latencies. Otherwise one CTA with a deeper ring.
+  const int half = (smem_optin() / 2 - 1024 - kSmemTail - 2 * static_cast<int>(pl->out_bytes)) /
+                   static_cast<int>(pl->stage_bytes);
+  if (two_ctas && half >= 2 && pl->nwc <= 6) ns = std::min(half, 4);
   if (ns > 8) ns = 8;
   if (ns < min_stages) return false;
   pl->nstages = ns;
   pl->nchains = p.D * p.B * p.C;
-  pl->smem_bytes = 1024 + ns * pl->stage_bytes + 2 * pl->out_bytes + 512;
+  pl->smem_bytes = 1024 + ns * pl->stage_bytes + 2 * pl->out_bytes + kSmemTail;
   return true;
 }
 
@@ -992,14 +1156,18 @@ bool fill_maps(StreamArgs* A, const void* const* ins, int nin, void* const* outs
   const Plan& pl = A->plan;
   const ScanParams& p = A->p;
   for (int t = 0; t < nin; ++t) {
-    if (!encode(&A->in[0][t], ins[t], dt, p.W, p.H, in_planes[t], pl.bw, pl.K, false)) return false;
+    if (!encode(&A->in[0][t], ins[t], dt, p.W, p.H, in_planes[t], pl.bw, pl.K, CU_TENSOR_MAP_L2_PROMOTION_NONE))
+      return false;
     const bool wide = pl.h_wide && t == nin - 1;  // bwd h_{t-1} view: 2K-step rows, 32-byte swizzle
-    if (!encode(&A->in[1][t], ins[t], dt, p.W, p.H, in_planes[t], wide ? 2 * pl.K : pl.K, pl.bh, true, wide))
+    if (!encode(&A->in[1][t], ins[t], dt, p.W, p.H, in_planes[t], wide ? 2 * pl.K : pl.K, pl.bh, horiz_promotion(),
+                wide))
       return false;
   }
   for (int t = 0; t < nout; ++t) {
-    if (!encode(&A->out[0][t], outs[t], dt, p.W, p.H, out_planes[t], pl.bw, pl.K, false)) return false;
-    if (!encode(&A->out[1][t], outs[t], dt, p.W, p.H, out_planes[t], pl.K, pl.bh, false)) return false;
+    if (!encode(&A->out[0][t], outs[t], dt, p.W, p.H, out_planes[t], pl.bw, pl.K, CU_TENSOR_MAP_L2_PROMOTION_NONE))
+      return false;
+    if (!encode(&A->out[1][t], outs[t], dt, p.W, p.H, out_planes[t], pl.K, pl.bh, CU_TENSOR_MAP_L2_PROMOTION_NONE))
+      return false;
   }
   return true;
 }
@@ -1053,7 +1221,7 @@ cudaError_t launch_fwd_stream(const ScanParams& p, gspn_dtype_t dt, cudaStream_t
   std::lock_guard<std::mutex> lock(mu);
   memset(&A, 0, sizeof A);
   A.p = p;
-  if (!make_plan(p, dt, F_NIN, 1, 2, &A.plan)) return cudaSuccess;
+  if (!make_plan(p, dt, F_NIN, 1, 2, /*two_ctas=*/true, &A.plan)) return cudaSuccess;
   const void* ins[F_NIN] = {p.x, p.lam, p.wl, p.wm, p.wr};
   const int64_t in_planes[F_NIN] = {p.B * p.C, p.D * p.B * p.C, p.D * p.B * p.G, p.D * p.B * p.G, p.D * p.B * p.G};
   void* outs[1] = {p.hout};
@@ -1061,10 +1229,11 @@ cudaError_t launch_fwd_stream(const ScanParams& p, gspn_dtype_t dt, cudaStream_t
   if (!fill_maps(&A, ins, F_NIN, outs, in_planes, out_planes, 1, dt)) return cudaSuccess;
   *handled = true;
   cudaError_t e;
-  if (A.plan.nwc <= 8)
-    e = dt == GSPN_BF16 ? launch(fwd_stream_kernel<__nv_bfloat16, 8>, A, s) : launch(fwd_stream_kernel<float, 8>, A, s);
+  if (A.plan.nwc <= 6)
+    e = dt == GSPN_BF16 ? launch(fwd_stream_kernel<__nv_bfloat16, 6>, A, s) : launch(fwd_stream_kernel<float, 6>, A, s);
   else
-    e = dt == GSPN_BF16 ? launch(fwd_stream_kernel<__nv_bfloat16, 16>, A, s) : launch(fwd_stream_kernel<float, 16>, A, s);
+    e = dt == GSPN_BF16 ? launch(fwd_stream_kernel<__nv_bfloat16, kEdgeW>, A, s)
+                        : launch(fwd_stream_kernel<float, kEdgeW>, A, s);
   *launches += 1;
   return e;
 }
@@ -1079,7 +1248,7 @@ cudaError_t launch_bwd_stream(const ScanParams& p0, gspn_dtype_t dt, cudaStream_
   ScanParams& p = A.p;
   const bool grouped = p.G < p.C;
   const int nout = grouped ? 1 : 4;
-  if (!make_plan(p, dt, B_NIN, nout, 2, &A.plan)) return cudaSuccess;
+  if (!make_plan(p, dt, B_NIN, nout, 2, /*two_ctas=*/false, &A.plan)) return cudaSuccess;
   const WsLayout l = ws_layout(p.B, p.C, p.H, p.W, p.D, p.G);
   if (p.ws == nullptr || p.ws_bytes < l.total) return cudaSuccess;
   char* ws = static_cast<char*>(p.ws);
@@ -1100,17 +1269,17 @@ cudaError_t launch_bwd_stream(const ScanParams& p0, gspn_dtype_t dt, cudaStream_
   *handled = true;
   cudaError_t e = cudaMemsetAsync(p.ws, 0, l.zero_bytes, s);
   if (e != cudaSuccess) return e;
-  const bool small = A.plan.nwc <= 8;
+  const bool small = A.plan.nwc <= 6;
   if (dt == GSPN_BF16) {
     if (small)
-      e = grouped ? launch(bwd_stream_kernel<__nv_bfloat16, true, 8>, A, s) : launch(bwd_stream_kernel<__nv_bfloat16, false, 8>, A, s);
+      e = grouped ? launch(bwd_stream_kernel<__nv_bfloat16, true, 6>, A, s) : launch(bwd_stream_kernel<__nv_bfloat16, false, 6>, A, s);
     else
-      e = grouped ? launch(bwd_stream_kernel<__nv_bfloat16, true, 16>, A, s) : launch(bwd_stream_kernel<__nv_bfloat16, false, 16>, A, s);
+      e = grouped ? launch(bwd_stream_kernel<__nv_bfloat16, true, kEdgeW>, A, s) : launch(bwd_stream_kernel<__nv_bfloat16, false, kEdgeW>, A, s);
   } else {
     if (small)
-      e = grouped ? launch(bwd_stream_kernel<float, true, 8>, A, s) : launch(bwd_stream_kernel<float, false, 8>, A, s);
+      e = grouped ? launch(bwd_stream_kernel<float, true, 6>, A, s) : launch(bwd_stream_kernel<float, false, 6>, A, s);
     else
-      e = grouped ? launch(bwd_stream_kernel<float, true, 16>, A, s) : launch(bwd_stream_kernel<float, false, 16>, A, s);
+      e = grouped ? launch(bwd_stream_kernel<float, true, kEdgeW>, A, s) : launch(bwd_stream_kernel<float, false, kEdgeW>, A, s);
   }
   *launches += 1;
   return e;
