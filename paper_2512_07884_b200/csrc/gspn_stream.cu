@@ -31,6 +31,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <mutex>
 
@@ -40,10 +41,10 @@
 namespace gspn {
 namespace {
 
-constexpr int kWarpPos = 128;  // positions covered by one consumer warp (4 per lane)
 constexpr int kMaxIn = 7;
 constexpr int kMaxOut = 4;
 constexpr int kEdgeW = 16;     // max consumer warps (edge-buffer slots)
+constexpr int kBwdE2Warps = 12;  // consumer warps of the 2-positions-per-lane backward variant
 constexpr int kBarTile = 1;    // named barrier id (0 is __syncthreads)
 
 template <typename T>
@@ -51,7 +52,6 @@ struct Cfg {
   static constexpr int es = static_cast<int>(sizeof(T));
   static constexpr int K = 16 / es;             // steps per tile (one 16-byte row chunk)
   static constexpr int GH = K;                  // ghost positions on each side of a warp
-  static constexpr int OWN = kWarpPos - 2 * GH; // positions a warp owns
   static constexpr int KS = 8 / es;             // bwd horizontal sub-tile (one 8-byte row chunk)
 };
 
@@ -72,6 +72,9 @@ struct Plan {
   uint32_t tx_v, tx_h;   // TMA bytes landing per stage (vertical / horizontal chains)
   int64_t nchains;
   uint32_t smem_bytes;
+  // L2 eviction priority per access class (0 evict_first, 1 evict_normal, 2 evict_last):
+  // x loads, vertical loads, horizontal loads, vertical stores, horizontal stores, fp32 accumulators
+  int pol[6];
 };
 
 struct alignas(64) StreamArgs {
@@ -155,6 +158,10 @@ __device__ __forceinline__ uint64_t policy_evict_normal() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
   return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last();
+__device__ __forceinline__ uint64_t policy_of(int code) {
+  return code == 0 ? policy_evict_first() : (code == 1 ? policy_evict_normal() : policy_evict_last());
 }
 __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t p;
@@ -325,8 +332,9 @@ template <bool kBwd>
 __device__ void producer_loop(const StreamArgs& A, uint8_t* ring, uint64_t* full, uint64_t* empty) {
   const Plan& pl = A.plan;
   const ScanParams& p = A.p;
-  const uint64_t pol_stream = policy_evict_first();
-  const uint64_t pol_keep = policy_evict_last();
+  const uint64_t pol_xin = policy_of(pl.pol[0]);
+  const uint64_t pol_vin = policy_of(pl.pol[1]);
+  const uint64_t pol_hin = policy_of(pl.pol[2]);
   int stage = 0;
   uint32_t phase = 0;
   for (int64_t w = blockIdx.x; w < pl.nchains; w += gridDim.x) {
@@ -349,7 +357,7 @@ __device__ void producer_loop(const StreamArgs& A, uint8_t* ring, uint64_t* full
         // x is re-read by the plane's other directions, and a horizontal 16-byte row chunk shares its
         // 32-byte sector with the next tile's chunk: both are kept (evict_last) so the second access
         // hits L2; vertical streams are read exactly once (evict_first).
-        const uint64_t pol = (t == 0 || !ch.vert) ? pol_keep : pol_stream;
+        const uint64_t pol = t == 0 ? pol_xin : (ch.vert ? pol_vin : pol_hin);
         const uint32_t dst = st + t * pl.tile_bytes;
         if (ch.vert) {
           const int row = s0 + (hview ? (ch.rev ? 1 : -1) : 0);
@@ -390,39 +398,75 @@ __device__ __forceinline__ void store_tile(const StreamArgs& A, const Chain& ch,
 
 // ------------------------------------------------------------------------------ per-lane geometry
 
-// The 4 positions a lane computes, their masks, and where they live in a shared-memory tile.
-// Warp w covers positions [A, A + 128), A = w * OWN - GH; it owns [A + GH, A + 128 - GH).
-//   vertical:   lane owns positions A + 4 lane + e            (e = 0..3)
-//   horizontal: lane owns positions A + 32 e + lane           (e = slot 0..3)
-struct Lanes {
-  int A;
-  int pos[4];
-  bool valid[4], hl[4], hr[4], own[4];
-  uint32_t voff;      // vertical: byte offset of the lane's 4 positions at kk = 0
-  uint32_t vstep;     // vertical: bytes between consecutive kk
-  uint32_t row[4];    // horizontal: clamped row index of each slot
+// E consecutive elements of T in shared memory <-> floats (E = 2: 4/8 bytes, E = 4: 8/16 bytes).
+template <typename T, int E> struct VE;
+template <typename T> struct VE<T, 4> {
+  static __device__ __forceinline__ void load(const uint8_t* p, float (&v)[4]) { V4<T>::load(p, v); }
+  static __device__ __forceinline__ void store(uint8_t* p, const float (&v)[4]) { V4<T>::store(p, v); }
+};
+template <> struct VE<__nv_bfloat16, 2> {
+  static __device__ __forceinline__ void load(const uint8_t* p, float (&v)[2]) {
+    const uint32_t u = *reinterpret_cast<const uint32_t*>(p);
+    v[0] = __uint_as_float(u << 16);
+    v[1] = __uint_as_float(u & 0xFFFF0000u);
+  }
+  static __device__ __forceinline__ void store(uint8_t* p, const float (&v)[2]) {
+    *reinterpret_cast<__nv_bfloat162*>(p) = __floats2bfloat162_rn(v[0], v[1]);
+  }
+};
+template <> struct VE<float, 2> {
+  static __device__ __forceinline__ void load(const uint8_t* p, float (&v)[2]) {
+    const float2 u = *reinterpret_cast<const float2*>(p);
+    v[0] = u.x;
+    v[1] = u.y;
+  }
+  static __device__ __forceinline__ void store(uint8_t* p, const float (&v)[2]) {
+    *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
+  }
 };
 
-template <typename T>
-__device__ __forceinline__ Lanes make_lanes(const Plan& pl, const Chain& ch, int wi, int lane) {
+template <int E>
+__device__ __forceinline__ void red_add_vec(float* p, const float (&v)[E], uint64_t pol) {
+  if constexpr (E == 4) red_add_v4(p, v[0], v[1], v[2], v[3], pol);
+  else red_add_v2(p, v[0], v[1], pol);
+}
+
+// The E positions a lane computes, their masks, and where they live in a shared-memory tile.
+// Warp w covers positions [A, A + 32 E), A = w * OWN - GH, OWN = 32 E - 2 GH; it owns the middle
+// [A + GH, A + 32 E - GH) and recomputes GH ghost positions on each side.
+//   vertical:   lane owns positions A + E lane + e            (e = 0..E-1)
+//   horizontal: lane owns positions A + 32 e + lane           (e = slot 0..E-1)
+template <int E>
+struct Lanes {
+  int A;
+  int pos[E];
+  bool valid[E], hl[E], hr[E], own[E];
+  uint32_t voff;      // vertical: byte offset of the lane's E positions at kk = 0
+  uint32_t vstep;     // vertical: bytes between consecutive kk
+  uint32_t row[E];    // horizontal: clamped row index of each slot
+};
+
+template <typename T, int E>
+__device__ __forceinline__ Lanes<E> make_lanes(const Plan& pl, const Chain& ch, int wi, int lane) {
   using C = Cfg<T>;
-  Lanes ln;
-  ln.A = wi * C::OWN - C::GH;
+  constexpr int WARP = 32 * E, OWN = WARP - 2 * C::GH;
+  Lanes<E> ln;
+  ln.A = wi * OWN - C::GH;
 #pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    const int off = ch.vert ? (4 * lane + e) : (32 * e + lane);
+  for (int e = 0; e < E; ++e) {
+    const int off = ch.vert ? (E * lane + e) : (32 * e + lane);
     const int r = ln.A + off;
     ln.pos[e] = r;
     ln.valid[e] = (r >= 0) && (r < ch.P);
     ln.hl[e] = r >= 1;
     ln.hr[e] = r <= ch.P - 2;
     // owned, and inside the tile (positions >= ppad are padding >= P: nothing to store)
-    ln.own[e] = (off >= C::GH) && (off < kWarpPos - C::GH) && (r < pl.ppad);
+    ln.own[e] = (off >= C::GH) && (off < WARP - C::GH) && (r < pl.ppad);
     const int rc = r < 0 ? 0 : (r >= pl.ppad ? pl.ppad - 1 : r);
     ln.row[e] = static_cast<uint32_t>(rc);
   }
-  int r0 = ln.A + 4 * lane;
-  r0 = r0 < 0 ? 0 : (r0 > pl.ppad - 4 ? pl.ppad - 4 : r0);
+  int r0 = ln.A + E * lane;
+  r0 = r0 < 0 ? 0 : (r0 > pl.ppad - E ? pl.ppad - E : r0);
   const int bwl = 31 - __clz(pl.bw);
   ln.voff = static_cast<uint32_t>((((r0 >> bwl) * C::K) * pl.bw + (r0 & (pl.bw - 1))) * C::es);
   ln.vstep = static_cast<uint32_t>(pl.bw * C::es);
@@ -432,67 +476,79 @@ __device__ __forceinline__ Lanes make_lanes(const Plan& pl, const Chain& ch, int
 // Ghost exchange at a tile boundary. Each warp publishes its first GH and last GH owned values
 // (edges) and reloads its ghost positions from the neighbouring warps' edges; warps outside
 // [0, nwc) contribute 0. Parity-double-buffered; the caller separates publish and reload by a barrier.
-template <typename T>
-__device__ __forceinline__ void edge_publish(float* edge, int par, int wi, int lane, bool vert, const float (&v)[4]) {
+template <typename T, int E>
+__device__ __forceinline__ void edge_publish(float* edge, int par, int wi, int lane, bool vert, const float (&v)[E]) {
   using C = Cfg<T>;
+  constexpr int WARP = 32 * E;
   float* L = edge + ((par * kEdgeW + wi) * 2 + 0) * 8;
   float* R = edge + ((par * kEdgeW + wi) * 2 + 1) * 8;
   if (vert) {
-    const int o = 4 * lane;
+    const int o = E * lane;
     if (o >= C::GH && o < 2 * C::GH) {
 #pragma unroll
-      for (int e = 0; e < 4; ++e) L[o - C::GH + e] = v[e];
+      for (int e = 0; e < E; ++e) L[o - C::GH + e] = v[e];
     }
-    if (o >= kWarpPos - 2 * C::GH && o < kWarpPos - C::GH) {
+    if (o >= WARP - 2 * C::GH && o < WARP - C::GH) {
 #pragma unroll
-      for (int e = 0; e < 4; ++e) R[o - (kWarpPos - 2 * C::GH) + e] = v[e];
+      for (int e = 0; e < E; ++e) R[o - (WARP - 2 * C::GH) + e] = v[e];
     }
   } else {
     if (lane >= C::GH && lane < 2 * C::GH) L[lane - C::GH] = v[0];
-    if (lane >= 32 - 2 * C::GH && lane < 32 - C::GH) R[lane - (32 - 2 * C::GH)] = v[3];
+    if (lane >= 32 - 2 * C::GH && lane < 32 - C::GH) R[lane - (32 - 2 * C::GH)] = v[E - 1];
   }
 }
 
-template <typename T>
+template <typename T, int E>
 __device__ __forceinline__ void edge_reload(const float* edge, int par, int wi, int nwc, int lane, bool vert,
-                                            float (&v)[4]) {
+                                            float (&v)[E]) {
   using C = Cfg<T>;
+  constexpr int WARP = 32 * E;
   const float* Rl = edge + ((par * kEdgeW + (wi - 1)) * 2 + 1) * 8;  // left neighbour's right edge
   const float* Lr = edge + ((par * kEdgeW + (wi + 1)) * 2 + 0) * 8;  // right neighbour's left edge
   if (vert) {
-    const int o = 4 * lane;
+    const int o = E * lane;
     if (o < C::GH) {
 #pragma unroll
-      for (int e = 0; e < 4; ++e) v[e] = wi > 0 ? Rl[o + e] : 0.f;
+      for (int e = 0; e < E; ++e) v[e] = wi > 0 ? Rl[o + e] : 0.f;
     }
-    if (o >= kWarpPos - C::GH) {
+    if (o >= WARP - C::GH) {
 #pragma unroll
-      for (int e = 0; e < 4; ++e) v[e] = wi < nwc - 1 ? Lr[o - (kWarpPos - C::GH) + e] : 0.f;
+      for (int e = 0; e < E; ++e) v[e] = wi < nwc - 1 ? Lr[o - (WARP - C::GH) + e] : 0.f;
     }
   } else {
     if (lane < C::GH) v[0] = wi > 0 ? Rl[lane] : 0.f;
-    if (lane >= 32 - C::GH) v[3] = wi < nwc - 1 ? Lr[lane - (32 - C::GH)] : 0.f;
+    if (lane >= 32 - C::GH) v[E - 1] = wi < nwc - 1 ? Lr[lane - (32 - C::GH)] : 0.f;
   }
 }
 
-// ------------------------------------------------------------------------------ forward consumer
-
-// One step of Eq. 1 for the lane's 4 positions given the previous state's outer neighbours.
-__device__ __forceinline__ void fwd_update(const Lanes& ln, const float (&x)[4], const float (&lam)[4],
-                                           const float (&wl)[4], const float (&wm)[4], const float (&wr)[4],
-                                           const float (&hm1)[4], const float (&hp1)[4], float (&h)[4],
-                                           bool prenorm) {
-  float hn[4];
+// Neighbours inside a warp. Vertical (blocked): position e's lower neighbour is e-1 of the same lane
+// (lane-1's last for e = 0); horizontal (interleaved, position A + 32 q + lane): one rotating
+// shuffle per slot; lane 0 of slot q takes lane 31 of slot q-1, lane 31 takes lane 0 of slot q+1.
+// The warp's two outermost positions get 0 (they are ghosts).
+template <int E>
+__device__ __forceinline__ void vert_neighbours(const float (&v)[E], int lane, float (&lo)[E], float (&hi)[E]) {
+  const float left = from_lower_lane(v[E - 1], lane);
+  const float right = from_upper_lane(v[0], lane);
 #pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    const float l = ln.hl[e] ? wl[e] : 0.f;
-    const float r = ln.hr[e] ? wr[e] : 0.f;
-    const float acc = fmaf(l, hm1[e], fmaf(wm[e], h[e], r * hp1[e]));
-    const float inv = prenorm ? 1.f : fast_rcp(wm[e] + l + r);
-    hn[e] = ln.valid[e] ? fmaf(acc, inv, lam[e] * x[e]) : 0.f;
+  for (int e = 0; e < E; ++e) {
+    lo[e] = e == 0 ? left : v[e > 0 ? e - 1 : 0];
+    hi[e] = e == E - 1 ? right : v[e < E - 1 ? e + 1 : 0];
+  }
+}
+
+template <int E>
+__device__ __forceinline__ void slot_neighbours(const float (&v)[E], int lane, float (&lo)[E], float (&hi)[E]) {
+  float up[E], dn[E];
+#pragma unroll
+  for (int q = 0; q < E; ++q) {
+    up[q] = __shfl_sync(0xffffffffu, v[q], (lane + 31) & 31);
+    dn[q] = __shfl_sync(0xffffffffu, v[q], (lane + 1) & 31);
   }
 #pragma unroll
-  for (int e = 0; e < 4; ++e) h[e] = hn[e];
+  for (int q = 0; q < E; ++q) {
+    lo[q] = lane == 0 ? (q == 0 ? 0.f : up[q > 0 ? q - 1 : 0]) : up[q];
+    hi[q] = lane == 31 ? (q == E - 1 ? 0.f : dn[q < E - 1 ? q + 1 : 0]) : dn[q];
+  }
 }
 
 // Element-order reversal of packed row chunks (runtime flag), so horizontal chains of both
@@ -512,38 +568,56 @@ template <> struct Rev<float> {
   static __device__ __forceinline__ uint2 r(const uint2& u, bool rev) { return rev ? make_uint2(u.y, u.x) : u; }
 };
 
+// ------------------------------------------------------------------------------ forward consumer
+
+// One step of Eq. 1 for the lane's E positions given the previous state's neighbours.
+template <int E>
+__device__ __forceinline__ void fwd_update(const Lanes<E>& ln, const float (&x)[E], const float (&lam)[E],
+                                           const float (&wl)[E], const float (&wm)[E], const float (&wr)[E],
+                                           const float (&hm1)[E], const float (&hp1)[E], float (&h)[E],
+                                           bool prenorm) {
+  float hn[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const float l = ln.hl[e] ? wl[e] : 0.f;
+    const float r = ln.hr[e] ? wr[e] : 0.f;
+    const float acc = fmaf(l, hm1[e], fmaf(wm[e], h[e], r * hp1[e]));
+    const float inv = prenorm ? 1.f : fast_rcp(wm[e] + l + r);
+    hn[e] = ln.valid[e] ? fmaf(acc, inv, lam[e] * x[e]) : 0.f;
+  }
+#pragma unroll
+  for (int e = 0; e < E; ++e) h[e] = hn[e];
+}
+
 // Vertical tile: the step loop stays rolled (code size); the in-tile row is a runtime offset.
-template <typename T>
-__device__ __forceinline__ void fwd_tile_vert(const Plan& pl, const Lanes& ln, const uint8_t* st, uint8_t* ob,
-                                              int lane, bool rev, float (&h)[4], bool prenorm) {
+template <typename T, int E>
+__device__ __forceinline__ void fwd_tile_vert(const Plan& pl, const Lanes<E>& ln, const uint8_t* st, uint8_t* ob,
+                                              int lane, bool rev, float (&h)[E], bool prenorm) {
   constexpr int K = Cfg<T>::K;
   const int dk = rev ? -static_cast<int>(ln.vstep) : static_cast<int>(ln.vstep);
   uint32_t off = ln.voff + (rev ? (K - 1) * ln.vstep : 0u);
 #pragma unroll 1
   for (int s = 0; s < K; ++s, off += dk) {
-    float x[4], lam[4], wl[4], wm[4], wr[4];
-    V4<T>::load(st + F_X * pl.tile_bytes + off, x);
-    V4<T>::load(st + F_LAM * pl.tile_bytes + off, lam);
-    V4<T>::load(st + F_WL * pl.tile_bytes + off, wl);
-    V4<T>::load(st + F_WM * pl.tile_bytes + off, wm);
-    V4<T>::load(st + F_WR * pl.tile_bytes + off, wr);
-    const float left = from_lower_lane(h[3], lane);
-    const float right = from_upper_lane(h[0], lane);
-    const float hm1[4] = {left, h[0], h[1], h[2]};
-    const float hp1[4] = {h[1], h[2], h[3], right};
-    fwd_update(ln, x, lam, wl, wm, wr, hm1, hp1, h, prenorm);
-    if (ln.own[0]) V4<T>::store(ob + off, h);  // the lane's 4 positions are owned together
+    float x[E], lam[E], wl[E], wm[E], wr[E], hm1[E], hp1[E];
+    VE<T, E>::load(st + F_X * pl.tile_bytes + off, x);
+    VE<T, E>::load(st + F_LAM * pl.tile_bytes + off, lam);
+    VE<T, E>::load(st + F_WL * pl.tile_bytes + off, wl);
+    VE<T, E>::load(st + F_WM * pl.tile_bytes + off, wm);
+    VE<T, E>::load(st + F_WR * pl.tile_bytes + off, wr);
+    vert_neighbours<E>(h, lane, hm1, hp1);
+    fwd_update<E>(ln, x, lam, wl, wm, wr, hm1, hp1, h, prenorm);
+    if (ln.own[0]) VE<T, E>::store(ob + off, h);  // the lane's E positions are owned together
   }
 }
 
 // Horizontal tile: one 16-byte row chunk (K steps) per tensor per slot, put in scan order.
-template <typename T>
-__device__ __forceinline__ void fwd_tile_horiz(const Plan& pl, const Lanes& ln, const uint8_t* st, uint8_t* ob,
-                                               int lane, bool rev, float (&h)[4], bool prenorm) {
+template <typename T, int E>
+__device__ __forceinline__ void fwd_tile_horiz(const Plan& pl, const Lanes<E>& ln, const uint8_t* st, uint8_t* ob,
+                                               int lane, bool rev, float (&h)[E], bool prenorm) {
   constexpr int K = Cfg<T>::K;
-  uint4 X[4], LAM[4], WL[4], WM[4], WR[4], OUT[4];
+  uint4 X[E], LAM[E], WL[E], WM[E], WR[E], OUT[E];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
+  for (int q = 0; q < E; ++q) {
     const uint32_t off = ln.row[q] * 16;
     X[q] = Rev<T>::r(*reinterpret_cast<const uint4*>(st + F_X * pl.tile_bytes + off), rev);
     LAM[q] = Rev<T>::r(*reinterpret_cast<const uint4*>(st + F_LAM * pl.tile_bytes + off), rev);
@@ -554,36 +628,26 @@ __device__ __forceinline__ void fwd_tile_horiz(const Plan& pl, const Lanes& ln, 
   }
 #pragma unroll
   for (int s = 0; s < K; ++s) {
-    float up[4], dn[4], w_lo[4], w_hi[4];
+    float hm1[E], hp1[E], x[E], lam[E], wl[E], wm[E], wr[E];
+    slot_neighbours<E>(h, lane, hm1, hp1);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      up[q] = __shfl_up_sync(0xffffffffu, h[q], 1);
-      dn[q] = __shfl_down_sync(0xffffffffu, h[q], 1);
-      w_lo[q] = __shfl_sync(0xffffffffu, h[q > 0 ? q - 1 : 0], 31);
-      w_hi[q] = __shfl_sync(0xffffffffu, h[q < 3 ? q + 1 : 3], 0);
-    }
-    float hm1[4], hp1[4], x[4], lam[4], wl[4], wm[4], wr[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      // position A + 32 q + lane: its lower neighbour is lane-1 of slot q (lane 0: lane 31 of slot q-1)
-      hm1[q] = lane == 0 ? (q == 0 ? 0.f : w_lo[q]) : up[q];
-      hp1[q] = lane == 31 ? (q == 3 ? 0.f : w_hi[q]) : dn[q];
+    for (int q = 0; q < E; ++q) {
       x[q] = Pk<T>::get(X[q], s);
       lam[q] = Pk<T>::get(LAM[q], s);
       wl[q] = Pk<T>::get(WL[q], s);
       wm[q] = Pk<T>::get(WM[q], s);
       wr[q] = Pk<T>::get(WR[q], s);
     }
-    fwd_update(ln, x, lam, wl, wm, wr, hm1, hp1, h, prenorm);
+    fwd_update<E>(ln, x, lam, wl, wm, wr, hm1, hp1, h, prenorm);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) Pk<T>::set(OUT[q], s, h[q]);
+    for (int q = 0; q < E; ++q) Pk<T>::set(OUT[q], s, h[q]);
   }
 #pragma unroll
-  for (int q = 0; q < 4; ++q)
+  for (int q = 0; q < E; ++q)
     if (ln.own[q]) *reinterpret_cast<uint4*>(ob + ln.row[q] * 16) = Rev<T>::r(OUT[q], rev);
 }
 
-template <typename T, int kMaxNWC>
+template <typename T, int E, int kMaxNWC>
 __global__ void __launch_bounds__((kMaxNWC + 1) * 32, kMaxNWC <= 6 ? 2 : 1)
     fwd_stream_kernel(const __grid_constant__ StreamArgs A) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -612,25 +676,27 @@ __global__ void __launch_bounds__((kMaxNWC + 1) * 32, kMaxNWC <= 6 ? 2 : 1)
     return;
   }
   const bool prenorm = A.p.flags & GSPN_FLAG_PRENORMALIZED;
-  const uint64_t pol_out = policy_evict_first();
-  const uint64_t pol_keep = policy_evict_last();  // horizontal outputs: the sector completes one tile later
+  const uint64_t pol_out = policy_of(pl.pol[3]);
+  const uint64_t pol_keep = policy_of(pl.pol[4]);  // horizontal outputs: the sector completes one tile later
   const int nthreads = pl.nwc * 32;
   int stage = 0, par = 0, ob_sel = 0;
   uint32_t phase = 0;
   for (int64_t w = blockIdx.x; w < pl.nchains; w += gridDim.x) {
     const Chain ch = make_chain(A.p, pl.K, w);
-    const Lanes ln = make_lanes<T>(pl, ch, warp, lane);
-    float h[4] = {0.f, 0.f, 0.f, 0.f};
+    const Lanes<E> ln = make_lanes<T, E>(pl, ch, warp, lane);
+    float h[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) h[e] = 0.f;
     for (int j = 0; j < ch.ntiles; ++j) {
       mbar_wait(smem_u32(&full[stage]), phase);
       const uint8_t* st = ring + static_cast<size_t>(stage) * pl.stage_bytes;
       uint8_t* ob = outbuf + static_cast<size_t>(ob_sel) * pl.out_bytes;
-      if (ch.vert) fwd_tile_vert<T>(pl, ln, st, ob, lane, ch.rev, h, prenorm);
-      else fwd_tile_horiz<T>(pl, ln, st, ob, lane, ch.rev, h, prenorm);
+      if (ch.vert) fwd_tile_vert<T, E>(pl, ln, st, ob, lane, ch.rev, h, prenorm);
+      else fwd_tile_horiz<T, E>(pl, ln, st, ob, lane, ch.rev, h, prenorm);
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&empty[stage]));
       if (++stage == pl.nstages) { stage = 0; phase ^= 1; }
-      edge_publish<T>(edge, par, warp, lane, ch.vert, h);
+      edge_publish<T, E>(edge, par, warp, lane, ch.vert, h);
       fence_proxy_async();
       named_bar(kBarTile, nthreads);
       if (threadIdx.x == 0) {
@@ -638,7 +704,7 @@ __global__ void __launch_bounds__((kMaxNWC + 1) * 32, kMaxNWC <= 6 ? 2 : 1)
         store_tile(A, ch, j, ob, 1, planes, ch.vert ? pol_out : pol_keep);
         bulk_wait_read1();
       }
-      edge_reload<T>(edge, par, warp, pl.nwc, lane, ch.vert, h);
+      edge_reload<T, E>(edge, par, warp, pl.nwc, lane, ch.vert, h);
       named_bar(kBarTile, nthreads);
       par ^= 1;
       ob_sel ^= 1;
@@ -650,50 +716,56 @@ __global__ void __launch_bounds__((kMaxNWC + 1) * 32, kMaxNWC <= 6 ? 2 : 1)
 // ------------------------------------------------------------------------------ backward consumer
 
 // State carried between steps (reverse order): ea = a_{t+1} g_{t+1}, eb = b_{t+1} g_{t+1},
-// ec = c_{t+1} g_{t+1} at the lane's 4 positions.
+// ec = c_{t+1} g_{t+1} at the lane's E positions.
+template <int E>
 struct BwdState {
-  float ea[4], eb[4], ec[4];
+  float ea[E], eb[E], ec[E];
 };
 
-// One adjoint step for the lane's 4 positions. nr/nl: (a g) of the upper neighbour / (c g) of the
-// lower neighbour; hm1/h0/hp1: h_{t-1} at r-1, r, r+1. Outputs dlam, dw (or the tap gradients D
-// for the grouped path), dxv = g lam; the state is replaced by step t's products.
-template <bool kGrouped>
-__device__ __forceinline__ void bwd_update(const Lanes& ln, bool live, const float (&x)[4], const float (&lam)[4],
-                                           const float (&dh)[4], const float (&wl)[4], const float (&wm)[4],
-                                           const float (&wr)[4], const float (&hm1)[4], const float (&h0)[4],
-                                           const float (&hp1)[4], const float (&nr)[4], const float (&nl)[4],
-                                           BwdState& S, float (&dlam)[4], float (&o1)[4], float (&o2)[4],
-                                           float (&o3)[4], float (&dxv)[4], bool prenorm) {
+// One adjoint step for the lane's E positions. nr/nl: (a g) of the upper neighbour / (c g) of the
+// lower neighbour; hm1/h0/hp1: h_{t-1} at r-1, r, r+1. Outputs dlam, dw (or the tap gradients D for
+// the grouped path), dxv = g lam; the state is replaced by step t's products. Per-channel weights
+// get the normalisation Jacobian in the cancellation-free form (gspn_common.cuh: jacobian), written
+// with u = h[r-1] - h[r], v = h[r+1] - h[r]:
+//   dw_l = g ((m + r) u - r v) / S^2,  dw_m = -g (l u + r v) / S^2,  dw_r = g ((l + m) v - l u) / S^2.
+template <int E, bool kGrouped>
+__device__ __forceinline__ void bwd_update(const Lanes<E>& ln, bool live, const float (&x)[E], const float (&lam)[E],
+                                           const float (&dh)[E], const float (&wl)[E], const float (&wm)[E],
+                                           const float (&wr)[E], const float (&hm1)[E], const float (&h0)[E],
+                                           const float (&hp1)[E], const float (&nr)[E], const float (&nl)[E],
+                                           BwdState<E>& S, float (&dlam)[E], float (&o1)[E], float (&o2)[E],
+                                           float (&o3)[E], float (&dxv)[E], bool prenorm) {
 #pragma unroll
-  for (int e = 0; e < 4; ++e) {
+  for (int e = 0; e < E; ++e) {
     const bool ok = live && ln.valid[e];
     const float g = ok ? (dh[e] + S.eb[e] + nr[e] + nl[e]) : 0.f;
     const float l = ln.hl[e] ? wl[e] : 0.f;
     const float r = ln.hr[e] ? wr[e] : 0.f;
     const float inv = prenorm ? 1.f : fast_rcp(wm[e] + l + r);
+    const float ig = inv * g;
     dlam[e] = g * x[e];
     dxv[e] = g * lam[e];
-    const float Da = ln.hl[e] ? g * hm1[e] : 0.f;
-    const float Db = g * h0[e];
-    const float Dc = ln.hr[e] ? g * hp1[e] : 0.f;
     if (kGrouped || prenorm) {
-      o1[e] = Da; o2[e] = Db; o3[e] = Dc;
-    } else {  // normalisation Jacobian (gspn_common.cuh: jacobian): dw = (D - q)/S
-      const float inv2 = inv * inv;
-      o1[e] = ln.hl[e] ? fmaf(wm[e] + r, Da, -fmaf(wm[e], Db, r * Dc)) * inv2 : 0.f;
-      o2[e] = fmaf(l + r, Db, -fmaf(l, Da, r * Dc)) * inv2;
-      o3[e] = ln.hr[e] ? fmaf(l + wm[e], Dc, -fmaf(l, Da, wm[e] * Db)) * inv2 : 0.f;
+      o1[e] = ln.hl[e] ? g * hm1[e] : 0.f;
+      o2[e] = g * h0[e];
+      o3[e] = ln.hr[e] ? g * hp1[e] : 0.f;
+    } else {
+      const float q = ig * inv;
+      const float u = hm1[e] - h0[e], v = hp1[e] - h0[e];
+      const float rv = r * v, lu = l * u;
+      o1[e] = ln.hl[e] ? q * fmaf(wm[e] + r, u, -rv) : 0.f;
+      o2[e] = -q * (lu + rv);
+      o3[e] = ln.hr[e] ? q * fmaf(l + wm[e], v, -lu) : 0.f;
     }
-    S.ea[e] = ok ? l * inv * g : 0.f;
-    S.eb[e] = ok ? wm[e] * inv * g : 0.f;
-    S.ec[e] = ok ? r * inv * g : 0.f;
+    S.ea[e] = ok ? l * ig : 0.f;
+    S.eb[e] = ok ? wm[e] * ig : 0.f;
+    S.ec[e] = ok ? r * ig : 0.f;
   }
 }
 
-template <typename T, bool kGrouped>
-__device__ __forceinline__ void bwd_tile_vert(const StreamArgs& A, const Lanes& ln, const Chain& ch, int j,
-                                              const uint8_t* st, uint8_t* ob, int lane, BwdState& S, bool prenorm,
+template <typename T, int E, bool kGrouped>
+__device__ __forceinline__ void bwd_tile_vert(const StreamArgs& A, const Lanes<E>& ln, const Chain& ch, int j,
+                                              const uint8_t* st, uint8_t* ob, int lane, BwdState<E>& S, bool prenorm,
                                               uint64_t pol_acc) {
   constexpr int K = Cfg<T>::K;
   const Plan& pl = A.plan;
@@ -701,7 +773,7 @@ __device__ __forceinline__ void bwd_tile_vert(const StreamArgs& A, const Lanes& 
   const int64_t HW = p.H * p.W;
   float* dxacc = p.dx_acc + ch.bc * HW;
   const int64_t wofs = ch.wplane * HW;
-  const bool lane_out = ln.own[0] && ln.valid[0];  // P % 4 == 0: a lane's 4 positions share validity
+  const bool lane_out = ln.own[0] && ln.valid[0];  // P % E == 0: a lane's positions share validity
   // steps s = K-1 .. 0 (reverse); in-tile row kk = rev ? K-1-s : s
   const int dk = ch.rev ? static_cast<int>(ln.vstep) : -static_cast<int>(ln.vstep);
   uint32_t off = ln.voff + (ch.rev ? 0u : (K - 1) * ln.vstep);
@@ -709,40 +781,35 @@ __device__ __forceinline__ void bwd_tile_vert(const StreamArgs& A, const Lanes& 
   for (int s = K - 1; s >= 0; --s, off += dk) {
     const int t = j * K + s;
     const bool live = t < ch.L;
-    float x[4], lam[4], dh[4], wl[4], wm[4], wr[4], hp[4];
-    V4<T>::load(st + B_X * pl.tile_bytes + off, x);
-    V4<T>::load(st + B_LAM * pl.tile_bytes + off, lam);
-    V4<T>::load(st + B_DH * pl.tile_bytes + off, dh);
-    V4<T>::load(st + B_WL * pl.tile_bytes + off, wl);
-    V4<T>::load(st + B_WM * pl.tile_bytes + off, wm);
-    V4<T>::load(st + B_WR * pl.tile_bytes + off, wr);
-    V4<T>::load(st + B_H * pl.tile_bytes + off, hp);
-    const float hpl = from_lower_lane(hp[3], lane);
-    const float hpr = from_upper_lane(hp[0], lane);
-    const float from_right = from_upper_lane(S.ea[0], lane);  // (a g) of position r0 + 4
-    const float from_left = from_lower_lane(S.ec[3], lane);   // (c g) of position r0 - 1
-    const float hm1[4] = {hpl, hp[0], hp[1], hp[2]};
-    const float hp1[4] = {hp[1], hp[2], hp[3], hpr};
-    const float nr[4] = {S.ea[1], S.ea[2], S.ea[3], from_right};
-    const float nl[4] = {from_left, S.ec[0], S.ec[1], S.ec[2]};
-    float dlam[4], o1[4], o2[4], o3[4], dxv[4];
-    bwd_update<kGrouped>(ln, live, x, lam, dh, wl, wm, wr, hm1, hp, hp1, nr, nl, S, dlam, o1, o2, o3, dxv, prenorm);
+    float x[E], lam[E], dh[E], wl[E], wm[E], wr[E], hp[E], hm1[E], hp1[E], nr[E], nl[E], lo_a[E], hi_c[E];
+    VE<T, E>::load(st + B_X * pl.tile_bytes + off, x);
+    VE<T, E>::load(st + B_LAM * pl.tile_bytes + off, lam);
+    VE<T, E>::load(st + B_DH * pl.tile_bytes + off, dh);
+    VE<T, E>::load(st + B_WL * pl.tile_bytes + off, wl);
+    VE<T, E>::load(st + B_WM * pl.tile_bytes + off, wm);
+    VE<T, E>::load(st + B_WR * pl.tile_bytes + off, wr);
+    VE<T, E>::load(st + B_H * pl.tile_bytes + off, hp);
+    vert_neighbours<E>(hp, lane, hm1, hp1);
+    vert_neighbours<E>(S.ea, lane, lo_a, nr);   // nr[e] = (a g) of position e + 1
+    vert_neighbours<E>(S.ec, lane, nl, hi_c);   // nl[e] = (c g) of position e - 1
+    float dlam[E], o1[E], o2[E], o3[E], dxv[E];
+    bwd_update<E, kGrouped>(ln, live, x, lam, dh, wl, wm, wr, hm1, hp, hp1, nr, nl, S, dlam, o1, o2, o3, dxv, prenorm);
     if (ln.own[0]) {
-      V4<T>::store(ob + O_DLAM * pl.tile_bytes + off, dlam);
+      VE<T, E>::store(ob + O_DLAM * pl.tile_bytes + off, dlam);
       if (!kGrouped) {
-        V4<T>::store(ob + O_DWL * pl.tile_bytes + off, o1);
-        V4<T>::store(ob + O_DWM * pl.tile_bytes + off, o2);
-        V4<T>::store(ob + O_DWR * pl.tile_bytes + off, o3);
+        VE<T, E>::store(ob + O_DWL * pl.tile_bytes + off, o1);
+        VE<T, E>::store(ob + O_DWM * pl.tile_bytes + off, o2);
+        VE<T, E>::store(ob + O_DWR * pl.tile_bytes + off, o3);
       }
     }
     if (lane_out && live) {
       const int row = ch.rev ? (ch.L - 1 - t) : t;
       const int64_t o = static_cast<int64_t>(row) * p.W + ln.pos[0];
-      red_add_v4(dxacc + o, dxv[0], dxv[1], dxv[2], dxv[3], pol_acc);
+      red_add_vec<E>(dxacc + o, dxv, pol_acc);
       if (kGrouped && t >= 1) {
-        red_add_v4(p.dwa_l + wofs + o, o1[0], o1[1], o1[2], o1[3], pol_acc);
-        red_add_v4(p.dwa_m + wofs + o, o2[0], o2[1], o2[2], o2[3], pol_acc);
-        red_add_v4(p.dwa_r + wofs + o, o3[0], o3[1], o3[2], o3[3], pol_acc);
+        red_add_vec<E>(p.dwa_l + wofs + o, o1, pol_acc);
+        red_add_vec<E>(p.dwa_m + wofs + o, o2, pol_acc);
+        red_add_vec<E>(p.dwa_r + wofs + o, o3, pol_acc);
       }
     }
   }
@@ -752,10 +819,10 @@ __device__ __forceinline__ void bwd_tile_vert(const StreamArgs& A, const Lanes& 
 // put in scan order); they are processed as NSUB sub-tiles of KS steps (the upper half first: the
 // backward walks the steps downwards) with the working half selected at run time, which keeps one
 // copy of the unrolled step code. h_{t-1} is read per step from the 2K-step swizzled h row.
-template <typename T, bool kGrouped>
-__device__ __forceinline__ void bwd_tile_horiz(const StreamArgs& A, const Lanes& ln, const Chain& ch, int j,
-                                               const uint8_t* st, uint8_t* ob, int lane, BwdState& S, bool prenorm,
-                                               uint64_t pol_acc) {
+template <typename T, int E, bool kGrouped>
+__device__ __forceinline__ void bwd_tile_horiz(const StreamArgs& A, const Lanes<E>& ln, const Chain& ch, int j,
+                                               const uint8_t* st, uint8_t* ob, int lane, BwdState<E>& S,
+                                               bool prenorm, uint64_t pol_acc) {
   using C = Cfg<T>;
   constexpr int K = C::K, KS = C::KS, NSUB = K / KS;
   static_assert(NSUB == 2, "sub-tiles are the two 8-byte halves of a 16-byte row chunk");
@@ -767,9 +834,9 @@ __device__ __forceinline__ void bwd_tile_horiz(const StreamArgs& A, const Lanes&
   const int64_t wofs = ch.wplane * HW;
   const int c0 = tile_start(ch, j, K);  // canonical column of kk = 0 (W % K == 0 on this path)
   const uint8_t* hbase = st + B_H * pl.tile_bytes;
-  uint4 X[4], LAM[4], DH[4], WL[4], WM[4], WR[4];
+  uint4 X[E], LAM[E], DH[E], WL[E], WM[E], WR[E];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
+  for (int q = 0; q < E; ++q) {
     const uint32_t off = ln.row[q] * 16;
     X[q] = Rev<T>::r(*reinterpret_cast<const uint4*>(st + B_X * pl.tile_bytes + off), rev);
     LAM[q] = Rev<T>::r(*reinterpret_cast<const uint4*>(st + B_LAM * pl.tile_bytes + off), rev);
@@ -778,16 +845,11 @@ __device__ __forceinline__ void bwd_tile_horiz(const StreamArgs& A, const Lanes&
     WM[q] = Rev<T>::r(*reinterpret_cast<const uint4*>(st + B_WM * pl.tile_bytes + off), rev);
     WR[q] = Rev<T>::r(*reinterpret_cast<const uint4*>(st + B_WR * pl.tile_bytes + off), rev);
   }
-  // byte offset of h element e of row r in the 32-byte-swizzled h tile (16-byte chunk ^= row bit 2)
-  auto hoff = [](uint32_t r, int e) {
-    const int c16 = e / K;
-    return r * 32 + ((static_cast<uint32_t>(c16) ^ ((r >> 2) & 1)) << 4) + (e % K) * Cfg<T>::es;
-  };
 #pragma unroll 1
   for (int sub = NSUB - 1; sub >= 0; --sub) {
-    uint2 x2[4], lam2[4], dh2[4], wl2[4], wm2[4], wr2[4];
+    uint2 x2[E], lam2[E], dh2[E], wl2[E], wm2[E], wr2[E];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < E; ++q) {
       x2[q] = sub ? make_uint2(X[q].z, X[q].w) : make_uint2(X[q].x, X[q].y);
       lam2[q] = sub ? make_uint2(LAM[q].z, LAM[q].w) : make_uint2(LAM[q].x, LAM[q].y);
       dh2[q] = sub ? make_uint2(DH[q].z, DH[q].w) : make_uint2(DH[q].x, DH[q].y);
@@ -795,47 +857,39 @@ __device__ __forceinline__ void bwd_tile_horiz(const StreamArgs& A, const Lanes&
       wm2[q] = sub ? make_uint2(WM[q].z, WM[q].w) : make_uint2(WM[q].x, WM[q].y);
       wr2[q] = sub ? make_uint2(WR[q].z, WR[q].w) : make_uint2(WR[q].x, WR[q].y);
     }
-    uint2 OL[4], O1[4], O2[4], O3[4];
-    float DXa[4][KS], DA[4][KS], DB[4][KS], DC[4][KS];
+    uint2 OL[E], O1[E], O2[E], O3[E];
+    float DXa[E][KS], DA[E][KS], DB[E][KS], DC[E][KS];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) OL[q] = O1[q] = O2[q] = O3[q] = make_uint2(0, 0);
+    for (int q = 0; q < E; ++q) OL[q] = O1[q] = O2[q] = O3[q] = make_uint2(0, 0);
 #pragma unroll
     for (int ss = KS - 1; ss >= 0; --ss) {
       const int s = sub * KS + ss;  // in-tile step (scan order)
       const int t = j * K + s;
-      // h_{t-1}: element K + s - 1 (L2R) / K - s (R2L) of the canonical 2K-step h row
+      // h_{t-1}: element K + s - 1 (L2R) / K - s (R2L) of the canonical 2K-step h row, whose 16-byte
+      // chunks are swizzled by row bit 2 (TMA SWIZZLE_32B)
       const int he = rev ? (K - s) : (K + s - 1);
-      float x[4], lam[4], dh[4], wl[4], wm[4], wr[4], h0[4];
+      float x[E], lam[E], dh[E], wl[E], wm[E], wr[E], h0[E];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < E; ++q) {
         x[q] = Pk<T>::get(x2[q], ss);
         lam[q] = Pk<T>::get(lam2[q], ss);
         dh[q] = Pk<T>::get(dh2[q], ss);
         wl[q] = Pk<T>::get(wl2[q], ss);
         wm[q] = Pk<T>::get(wm2[q], ss);
         wr[q] = Pk<T>::get(wr2[q], ss);
-        h0[q] = to_f(*reinterpret_cast<const T*>(hbase + hoff(ln.row[q], he)));
+        const uint32_t r = ln.row[q];
+        const uint32_t c16 = static_cast<uint32_t>(he / K) ^ ((r >> 2) & 1);
+        h0[q] = to_f(*reinterpret_cast<const T*>(hbase + r * 32 + (c16 << 4) + (he % K) * C::es));
       }
-      float hm1[4], hp1[4], nr[4], nl[4];
+      float hm1[E], hp1[E], nr[E], nl[E], ea_lo[E], ec_hi[E];
+      slot_neighbours<E>(h0, lane, hm1, hp1);
+      slot_neighbours<E>(S.ea, lane, ea_lo, nr);
+      slot_neighbours<E>(S.ec, lane, nl, ec_hi);
+      float dlam[E], o1[E], o2[E], o3[E], dxv[E];
+      bwd_update<E, kGrouped>(ln, true, x, lam, dh, wl, wm, wr, hm1, h0, hp1, nr, nl, S, dlam, o1, o2, o3, dxv,
+                              prenorm);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float hu = __shfl_up_sync(0xffffffffu, h0[q], 1);
-        const float hd = __shfl_down_sync(0xffffffffu, h0[q], 1);
-        const float au = __shfl_down_sync(0xffffffffu, S.ea[q], 1);
-        const float cd = __shfl_up_sync(0xffffffffu, S.ec[q], 1);
-        const float hw_lo = __shfl_sync(0xffffffffu, h0[q > 0 ? q - 1 : 0], 31);
-        const float hw_hi = __shfl_sync(0xffffffffu, h0[q < 3 ? q + 1 : 3], 0);
-        const float aw_hi = __shfl_sync(0xffffffffu, S.ea[q < 3 ? q + 1 : 3], 0);
-        const float cw_lo = __shfl_sync(0xffffffffu, S.ec[q > 0 ? q - 1 : 0], 31);
-        hm1[q] = lane == 0 ? (q == 0 ? 0.f : hw_lo) : hu;
-        hp1[q] = lane == 31 ? (q == 3 ? 0.f : hw_hi) : hd;
-        nr[q] = lane == 31 ? (q == 3 ? 0.f : aw_hi) : au;
-        nl[q] = lane == 0 ? (q == 0 ? 0.f : cw_lo) : cd;
-      }
-      float dlam[4], o1[4], o2[4], o3[4], dxv[4];
-      bwd_update<kGrouped>(ln, true, x, lam, dh, wl, wm, wr, hm1, h0, hp1, nr, nl, S, dlam, o1, o2, o3, dxv, prenorm);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < E; ++q) {
         Pk<T>::set(OL[q], ss, dlam[q]);
         if (!kGrouped) {
           Pk<T>::set(O1[q], ss, o1[q]);
@@ -852,7 +906,7 @@ __device__ __forceinline__ void bwd_tile_horiz(const StreamArgs& A, const Lanes&
     // write back in canonical order: chunk c8 of the row, elements reversed for R2L
     const int c8 = rev ? (NSUB - 1 - sub) : sub;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < E; ++q) {
       if (!ln.own[q]) continue;
       const uint32_t off = ln.row[q] * 16 + c8 * 8;
       *reinterpret_cast<uint2*>(ob + O_DLAM * pl.tile_bytes + off) = Rev<T>::r(OL[q], rev);
@@ -866,8 +920,7 @@ __device__ __forceinline__ void bwd_tile_horiz(const StreamArgs& A, const Lanes&
         float d[KS];
 #pragma unroll
         for (int i = 0; i < KS; ++i) d[i] = rev ? DXa[q][KS - 1 - i] : DXa[q][i];
-        if (KS == 4) red_add_v4(dxacc + o, d[0], d[1 % KS], d[2 % KS], d[3 % KS], pol_acc);
-        else red_add_v2(dxacc + o, d[0], d[1 % KS], pol_acc);
+        red_add_vec<KS>(dxacc + o, d, pol_acc);
         if (kGrouped) {
           float* dst[3] = {p.dwa_l + wofs + o, p.dwa_m + wofs + o, p.dwa_r + wofs + o};
 #pragma unroll
@@ -877,8 +930,7 @@ __device__ __forceinline__ void bwd_tile_horiz(const StreamArgs& A, const Lanes&
               const int si = rev ? KS - 1 - i : i;
               d[i] = m == 0 ? DA[q][si] : (m == 1 ? DB[q][si] : DC[q][si]);
             }
-            if (KS == 4) red_add_v4(dst[m], d[0], d[1 % KS], d[2 % KS], d[3 % KS], pol_acc);
-            else red_add_v2(dst[m], d[0], d[1 % KS], pol_acc);
+            red_add_vec<KS>(dst[m], d, pol_acc);
           }
         }
       }
@@ -949,7 +1001,7 @@ __device__ void bwd_chain_epilogue(const StreamArgs& A, const Chain& ch, int* fl
   }
 }
 
-template <typename T, bool kGrouped, int kMaxNWC>
+template <typename T, int E, bool kGrouped, int kMaxNWC>
 __global__ void __launch_bounds__((kMaxNWC + 1) * 32, 1) bwd_stream_kernel(const __grid_constant__ StreamArgs A) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared space
@@ -978,32 +1030,32 @@ __global__ void __launch_bounds__((kMaxNWC + 1) * 32, 1) bwd_stream_kernel(const
     return;
   }
   const bool prenorm = A.p.flags & GSPN_FLAG_PRENORMALIZED;
-  const uint64_t pol_out = policy_evict_first();
-  const uint64_t pol_keep = policy_evict_last();  // horizontal outputs: the sector completes one tile later
-  const uint64_t pol_acc = policy_evict_last();
+  const uint64_t pol_out = policy_of(pl.pol[3]);
+  const uint64_t pol_keep = policy_of(pl.pol[4]);  // horizontal outputs: the sector completes one tile later
+  const uint64_t pol_acc = policy_of(pl.pol[5]);
   const int nthreads = pl.nwc * 32;
   constexpr int kEdgeArr = 2 * kEdgeW * 2 * 8;
   int stage = 0, par = 0, ob_sel = 0;
   uint32_t phase = 0;
   for (int64_t w = blockIdx.x; w < pl.nchains; w += gridDim.x) {
     const Chain ch = make_chain(A.p, pl.K, w);
-    const Lanes ln = make_lanes<T>(pl, ch, warp, lane);
-    BwdState S;
+    const Lanes<E> ln = make_lanes<T, E>(pl, ch, warp, lane);
+    BwdState<E> S;
 #pragma unroll
-    for (int e = 0; e < 4; ++e) S.ea[e] = S.eb[e] = S.ec[e] = 0.f;
+    for (int e = 0; e < E; ++e) S.ea[e] = S.eb[e] = S.ec[e] = 0.f;
     for (int jj = 0; jj < ch.ntiles; ++jj) {
       const int j = ch.ntiles - 1 - jj;
       mbar_wait(smem_u32(&full[stage]), phase);
       const uint8_t* st = ring + static_cast<size_t>(stage) * pl.stage_bytes;
       uint8_t* ob = outbuf + static_cast<size_t>(ob_sel) * pl.out_bytes;
-      if (ch.vert) bwd_tile_vert<T, kGrouped>(A, ln, ch, j, st, ob, lane, S, prenorm, pol_acc);
-      else bwd_tile_horiz<T, kGrouped>(A, ln, ch, j, st, ob, lane, S, prenorm, pol_acc);
+      if (ch.vert) bwd_tile_vert<T, E, kGrouped>(A, ln, ch, j, st, ob, lane, S, prenorm, pol_acc);
+      else bwd_tile_horiz<T, E, kGrouped>(A, ln, ch, j, st, ob, lane, S, prenorm, pol_acc);
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&empty[stage]));
       if (++stage == pl.nstages) { stage = 0; phase ^= 1; }
-      edge_publish<T>(edge + 0 * kEdgeArr, par, warp, lane, ch.vert, S.ea);
-      edge_publish<T>(edge + 1 * kEdgeArr, par, warp, lane, ch.vert, S.eb);
-      edge_publish<T>(edge + 2 * kEdgeArr, par, warp, lane, ch.vert, S.ec);
+      edge_publish<T, E>(edge + 0 * kEdgeArr, par, warp, lane, ch.vert, S.ea);
+      edge_publish<T, E>(edge + 1 * kEdgeArr, par, warp, lane, ch.vert, S.eb);
+      edge_publish<T, E>(edge + 2 * kEdgeArr, par, warp, lane, ch.vert, S.ec);
       fence_proxy_async();
       named_bar(kBarTile, nthreads);
       if (threadIdx.x == 0) {
@@ -1011,9 +1063,9 @@ __global__ void __launch_bounds__((kMaxNWC + 1) * 32, 1) bwd_stream_kernel(const
         store_tile(A, ch, j, ob, kGrouped ? 1 : 4, planes, ch.vert ? pol_out : pol_keep);
         bulk_wait_read1();
       }
-      edge_reload<T>(edge + 0 * kEdgeArr, par, warp, pl.nwc, lane, ch.vert, S.ea);
-      edge_reload<T>(edge + 1 * kEdgeArr, par, warp, pl.nwc, lane, ch.vert, S.eb);
-      edge_reload<T>(edge + 2 * kEdgeArr, par, warp, pl.nwc, lane, ch.vert, S.ec);
+      edge_reload<T, E>(edge + 0 * kEdgeArr, par, warp, pl.nwc, lane, ch.vert, S.ea);
+      edge_reload<T, E>(edge + 1 * kEdgeArr, par, warp, pl.nwc, lane, ch.vert, S.eb);
+      edge_reload<T, E>(edge + 2 * kEdgeArr, par, warp, pl.nwc, lane, ch.vert, S.ec);
       named_bar(kBarTile, nthreads);
       par ^= 1;
       ob_sel ^= 1;
@@ -1096,7 +1148,8 @@ CUtensorMapL2promotion horiz_promotion() {
 constexpr int kSmemTail = 8192;  // mbarriers, ghost-edge buffers, flags
 
 // Shape eligibility + plan. nin/nout: tensors per tile.
-bool make_plan(const ScanParams& p, gspn_dtype_t dt, int nin, int nout, int min_stages, bool two_ctas, Plan* pl) {
+bool make_plan(const ScanParams& p, gspn_dtype_t dt, int nin, int nout, int min_stages, bool two_ctas, int E,
+               Plan* pl) {
   const int s = dt == GSPN_BF16 ? 2 : 4;
   if ((p.W * s) % 16 != 0) return false;  // TMA global stride alignment; also K | W for horizontal tiles
   bool any_v = false, any_h = false;
@@ -1107,7 +1160,7 @@ bool make_plan(const ScanParams& p, gspn_dtype_t dt, int nin, int nout, int min_
   memset(pl, 0, sizeof *pl);
   pl->K = 16 / s;
   pl->es = s;
-  pl->own = kWarpPos - 2 * pl->K;
+  pl->own = 32 * E - 2 * pl->K;
   pl->nwc = static_cast<int>((maxP + pl->own - 1) / pl->own);
   if (pl->nwc > kEdgeW) return false;
   // positions addressable in a tile: every owned position, a whole number of vertical boxes
@@ -1147,6 +1200,13 @@ bool make_plan(const ScanParams& p, gspn_dtype_t dt, int nin, int nout, int min_
   if (ns < min_stages) return false;
   pl->nstages = ns;
   pl->nchains = p.D * p.B * p.C;
+  // L2 priorities (experiments: GSPN_POL="x,vin,hin,vout,hout,acc", each 0|1|2)
+  static const int def_pol[6] = {1, 0, 1, 0, 1, 2};
+  for (int i = 0; i < 6; ++i) pl->pol[i] = def_pol[i];
+  if (const char* e = getenv("GSPN_POL")) {
+    int v[6], n = sscanf(e, "%d,%d,%d,%d,%d,%d", &v[0], &v[1], &v[2], &v[3], &v[4], &v[5]);
+    for (int i = 0; i < n && i < 6; ++i) pl->pol[i] = v[i];
+  }
   pl->smem_bytes = 1024 + ns * pl->stage_bytes + 2 * pl->out_bytes + kSmemTail;
   return true;
 }
@@ -1183,6 +1243,10 @@ cudaError_t launch(KernelT kernel, const StreamArgs& A, cudaStream_t s) {
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   int64_t grid = static_cast<int64_t>(sm_count()) * per_sm;
+  if (const char* e = getenv("GSPN_GRID")) {  // experiments only: cap the persistent grid
+    const int64_t g = atoll(e);
+    if (g > 0 && g < grid) grid = g;
+  }
   if (grid > A.plan.nchains) grid = A.plan.nchains;
   kernel<<<static_cast<unsigned>(grid), threads, A.plan.smem_bytes, s>>>(A);
   return cudaGetLastError();
@@ -1221,7 +1285,7 @@ cudaError_t launch_fwd_stream(const ScanParams& p, gspn_dtype_t dt, cudaStream_t
   std::lock_guard<std::mutex> lock(mu);
   memset(&A, 0, sizeof A);
   A.p = p;
-  if (!make_plan(p, dt, F_NIN, 1, 2, /*two_ctas=*/true, &A.plan)) return cudaSuccess;
+  if (!make_plan(p, dt, F_NIN, 1, 2, /*two_ctas=*/true, /*E=*/4, &A.plan)) return cudaSuccess;
   const void* ins[F_NIN] = {p.x, p.lam, p.wl, p.wm, p.wr};
   const int64_t in_planes[F_NIN] = {p.B * p.C, p.D * p.B * p.C, p.D * p.B * p.G, p.D * p.B * p.G, p.D * p.B * p.G};
   void* outs[1] = {p.hout};
@@ -1230,10 +1294,10 @@ cudaError_t launch_fwd_stream(const ScanParams& p, gspn_dtype_t dt, cudaStream_t
   *handled = true;
   cudaError_t e;
   if (A.plan.nwc <= 6)
-    e = dt == GSPN_BF16 ? launch(fwd_stream_kernel<__nv_bfloat16, 6>, A, s) : launch(fwd_stream_kernel<float, 6>, A, s);
+    e = dt == GSPN_BF16 ? launch(fwd_stream_kernel<__nv_bfloat16, 4, 6>, A, s) : launch(fwd_stream_kernel<float, 4, 6>, A, s);
   else
-    e = dt == GSPN_BF16 ? launch(fwd_stream_kernel<__nv_bfloat16, kEdgeW>, A, s)
-                        : launch(fwd_stream_kernel<float, kEdgeW>, A, s);
+    e = dt == GSPN_BF16 ? launch(fwd_stream_kernel<__nv_bfloat16, 4, kEdgeW>, A, s)
+                        : launch(fwd_stream_kernel<float, 4, kEdgeW>, A, s);
   *launches += 1;
   return e;
 }
@@ -1248,7 +1312,14 @@ cudaError_t launch_bwd_stream(const ScanParams& p0, gspn_dtype_t dt, cudaStream_
   ScanParams& p = A.p;
   const bool grouped = p.G < p.C;
   const int nout = grouped ? 1 : 4;
-  if (!make_plan(p, dt, B_NIN, nout, 2, /*two_ctas=*/false, &A.plan)) return cudaSuccess;
+  // Positions per lane: 2 (more warps per chain, better latency hiding) while a chain fits in
+  // kBwdE2Warps warps, else 4. GSPN_BWD_E=2|4 overrides (experiments).
+  int E = 2;
+  if (const char* ev = getenv("GSPN_BWD_E")) E = atoi(ev) == 4 ? 4 : 2;
+  if (!make_plan(p, dt, B_NIN, nout, 2, /*two_ctas=*/false, E, &A.plan) || (E == 2 && A.plan.nwc > kBwdE2Warps)) {
+    E = 4;
+    if (!make_plan(p, dt, B_NIN, nout, 2, /*two_ctas=*/false, E, &A.plan)) return cudaSuccess;
+  }
   const WsLayout l = ws_layout(p.B, p.C, p.H, p.W, p.D, p.G);
   if (p.ws == nullptr || p.ws_bytes < l.total) return cudaSuccess;
   char* ws = static_cast<char*>(p.ws);
@@ -1269,17 +1340,20 @@ cudaError_t launch_bwd_stream(const ScanParams& p0, gspn_dtype_t dt, cudaStream_
   *handled = true;
   cudaError_t e = cudaMemsetAsync(p.ws, 0, l.zero_bytes, s);
   if (e != cudaSuccess) return e;
-  const bool small = A.plan.nwc <= 6;
+  using BF = __nv_bfloat16;
   if (dt == GSPN_BF16) {
-    if (small)
-      e = grouped ? launch(bwd_stream_kernel<__nv_bfloat16, true, 6>, A, s) : launch(bwd_stream_kernel<__nv_bfloat16, false, 6>, A, s);
+    if (E == 2)
+      e = grouped ? launch(bwd_stream_kernel<BF, 2, true, kBwdE2Warps>, A, s)
+                  : launch(bwd_stream_kernel<BF, 2, false, kBwdE2Warps>, A, s);
     else
-      e = grouped ? launch(bwd_stream_kernel<__nv_bfloat16, true, kEdgeW>, A, s) : launch(bwd_stream_kernel<__nv_bfloat16, false, kEdgeW>, A, s);
+      e = grouped ? launch(bwd_stream_kernel<BF, 4, true, kEdgeW>, A, s) : launch(bwd_stream_kernel<BF, 4, false, kEdgeW>, A, s);
   } else {
-    if (small)
-      e = grouped ? launch(bwd_stream_kernel<float, true, 6>, A, s) : launch(bwd_stream_kernel<float, false, 6>, A, s);
+    if (E == 2)
+      e = grouped ? launch(bwd_stream_kernel<float, 2, true, kBwdE2Warps>, A, s)
+                  : launch(bwd_stream_kernel<float, 2, false, kBwdE2Warps>, A, s);
     else
-      e = grouped ? launch(bwd_stream_kernel<float, true, kEdgeW>, A, s) : launch(bwd_stream_kernel<float, false, kEdgeW>, A, s);
+      e = grouped ? launch(bwd_stream_kernel<float, 4, true, kEdgeW>, A, s)
+                  : launch(bwd_stream_kernel<float, 4, false, kEdgeW>, A, s);
   }
   *launches += 1;
   return e;
