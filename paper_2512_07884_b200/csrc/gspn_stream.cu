@@ -45,7 +45,8 @@ constexpr int kMaxIn = 7;
 constexpr int kMaxOut = 4;
 constexpr int kEdgeW = 16;     // max consumer warps (edge-buffer slots)
 constexpr int kBwdE2Warps = 12;  // consumer warps of the 2-positions-per-lane backward variant
-constexpr int kBarTile = 1;    // named barrier id (0 is __syncthreads)
+constexpr int kBarTile = 1;    // named barrier ids (0 is __syncthreads): ghost exchange / epilogue
+constexpr int kBarRows = 2;    // horizontal tiles: every warp holds its rows in registers
 
 template <typename T>
 struct Cfg {
@@ -64,11 +65,11 @@ struct Plan {
   int bw, nbw;         // vertical TMA box width (positions) and box count
   int bh, nbh;         // horizontal TMA box height (positions) and box count
   int nin, nout;       // input / output tensors per tile
+  int pair;            // load horizontal tiles in back-to-back pairs (ring of >= 3 stages)
   int h_wide;          // bwd: the last input (h) holds 2K steps for horizontal chains
   int nstages;
   uint32_t tile_bytes;   // one tensor's tile: K * ppad * es (= 16 * ppad)
   uint32_t stage_bytes;  // (nin + h_wide) * tile_bytes
-  uint32_t out_bytes;    // nout * tile_bytes (one staging buffer; two are allocated)
   uint32_t tx_v, tx_h;   // TMA bytes landing per stage (vertical / horizontal chains)
   int64_t nchains;
   uint32_t smem_bytes;
@@ -141,7 +142,6 @@ __device__ __forceinline__ void tma_store3(const CUtensorMap* map, uint32_t src,
 }
 
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
@@ -179,9 +179,19 @@ __device__ __forceinline__ void red_add_v2(float* p, float a, float b, uint64_t 
   asm volatile("red.global.add.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(p), "f"(a), "f"(b), "l"(pol) : "memory");
 }
 
-__device__ __forceinline__ void red_add_f32(float* p, float a, uint64_t pol) {
-  asm volatile("red.global.add.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(a), "l"(pol) : "memory");
+
+__device__ __forceinline__ void st_global_b32(void* p, uint32_t a, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(a), "l"(pol) : "memory");
 }
+__device__ __forceinline__ void st_global_v2(void* p, uint32_t a, uint32_t b, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.b32 [%0], {%1, %2}, %3;" ::"l"(p), "r"(a), "r"(b), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_global_v4(void* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d),
+               "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 
 __device__ __forceinline__ float fast_rcp(float x) {
   float r;
@@ -329,6 +339,34 @@ __device__ __forceinline__ int64_t plane_of(const Chain& ch, int slot) {
 // ------------------------------------------------------------------------------ producer
 
 template <bool kBwd>
+__device__ __forceinline__ void issue_tile(const StreamArgs& A, const Chain& ch, int j, int t, uint32_t st,
+                                           uint32_t fb, uint64_t pol) {
+  const Plan& pl = A.plan;
+  const int o = ch.vert ? 0 : 1;
+  const int s0 = tile_start(ch, j, pl.K);
+  const int plane = static_cast<int>(plane_of<kBwd>(ch, t));
+  // h_{t-1} view for the backward, one step against the scan direction (its zero fill is
+  // h_{-1} = 0). Vertical: the row coordinate shifts by one. Horizontal: TMA needs a 16-byte
+  // aligned inner coordinate, so a 2K-step box [s0-K, s0+K) (L2R) / [s0, s0+2K) (R2L) is
+  // loaded with a 32-byte swizzle and the consumer picks element K+kk-1 / kk+1.
+  const bool hview = kBwd && t == B_H;
+  const uint32_t dst = st + t * pl.tile_bytes;
+  if (ch.vert) {
+    const int row = s0 + (hview ? (ch.rev ? 1 : -1) : 0);
+    for (int q = 0; q < pl.nbw; ++q)
+      tma_load3(dst + q * pl.K * pl.bw * pl.es, &A.in[o][t], q * pl.bw, row, plane, fb, pol);
+  } else if (hview) {
+    const int c0h = ch.rev ? s0 : s0 - pl.K;
+    for (int q = 0; q < pl.nbh; ++q) tma_load3(dst + q * pl.bh * 32, &A.in[o][t], c0h, q * pl.bh, plane, fb, pol);
+  } else {
+    for (int q = 0; q < pl.nbh; ++q) tma_load3(dst + q * pl.bh * 16, &A.in[o][t], s0, q * pl.bh, plane, fb, pol);
+  }
+}
+
+// The producer thread. Horizontal tiles are 16-byte row chunks: two consecutive tiles share every
+// 32-byte DRAM sector, so with a ring of >= 3 stages they are loaded as a pair, back to back, and
+// each sector is fetched from DRAM once (no reliance on L2 keeping it for a whole tile).
+template <bool kBwd>
 __device__ void producer_loop(const StreamArgs& A, uint8_t* ring, uint64_t* full, uint64_t* empty) {
   const Plan& pl = A.plan;
   const ScanParams& p = A.p;
@@ -339,61 +377,60 @@ __device__ void producer_loop(const StreamArgs& A, uint8_t* ring, uint64_t* full
   uint32_t phase = 0;
   for (int64_t w = blockIdx.x; w < pl.nchains; w += gridDim.x) {
     const Chain ch = make_chain(p, pl.K, w);
-    const int o = ch.vert ? 0 : 1;
-    for (int jj = 0; jj < ch.ntiles; ++jj) {
-      const int j = kBwd ? (ch.ntiles - 1 - jj) : jj;
-      mbar_wait_sleep(smem_u32(&empty[stage]), phase ^ 1);
-      const uint32_t fb = smem_u32(&full[stage]);
-      mbar_arrive_tx(fb, ch.vert ? pl.tx_v : pl.tx_h);
-      const int s0 = tile_start(ch, j, pl.K);
-      const uint32_t st = smem_u32(ring + static_cast<size_t>(stage) * pl.stage_bytes);
-      for (int t = 0; t < pl.nin; ++t) {
-        const int plane = static_cast<int>(plane_of<kBwd>(ch, t));
-        // h_{t-1} view for the backward, one step against the scan direction (its zero fill is
-        // h_{-1} = 0). Vertical: the row coordinate shifts by one. Horizontal: TMA needs a 16-byte
-        // aligned inner coordinate, so a 2K-step box [s0-K, s0+K) (L2R) / [s0, s0+2K) (R2L) is
-        // loaded with a 32-byte swizzle and the consumer picks element K+kk-1 / kk+1.
-        const bool hview = kBwd && t == B_H;
-        // x is re-read by the plane's other directions, and a horizontal 16-byte row chunk shares its
-        // 32-byte sector with the next tile's chunk: both are kept (evict_last) so the second access
-        // hits L2; vertical streams are read exactly once (evict_first).
-        const uint64_t pol = t == 0 ? pol_xin : (ch.vert ? pol_vin : pol_hin);
-        const uint32_t dst = st + t * pl.tile_bytes;
-        if (ch.vert) {
-          const int row = s0 + (hview ? (ch.rev ? 1 : -1) : 0);
-          for (int q = 0; q < pl.nbw; ++q)
-            tma_load3(dst + q * pl.K * pl.bw * pl.es, &A.in[o][t], q * pl.bw, row, plane, fb, pol);
-        } else if (hview) {
-          const int c0h = ch.rev ? s0 : s0 - pl.K;
-          for (int q = 0; q < pl.nbh; ++q)
-            tma_load3(dst + q * pl.bh * 32, &A.in[o][t], c0h, q * pl.bh, plane, fb, pol);
-        } else {
-          for (int q = 0; q < pl.nbh; ++q)
-            tma_load3(dst + q * pl.bh * 16, &A.in[o][t], s0, q * pl.bh, plane, fb, pol);
-        }
+    for (int jj = 0; jj < ch.ntiles;) {
+      const int ng = (!ch.vert && pl.pair && jj + 1 < ch.ntiles) ? 2 : 1;
+      int stg[2], jt[2];
+      for (int u = 0; u < ng; ++u) {
+        mbar_wait_sleep(smem_u32(&empty[stage]), phase ^ 1);
+        mbar_arrive_tx(smem_u32(&full[stage]), ch.vert ? pl.tx_v : pl.tx_h);
+        stg[u] = stage;
+        jt[u] = kBwd ? (ch.ntiles - 1 - (jj + u)) : (jj + u);
+        if (++stage == pl.nstages) { stage = 0; phase ^= 1; }
       }
-      if (++stage == pl.nstages) { stage = 0; phase ^= 1; }
+      for (int t = 0; t < pl.nin; ++t) {
+        // x is re-read by the plane's other directions; vertical streams are read exactly once
+        const uint64_t pol = t == 0 ? pol_xin : (ch.vert ? pol_vin : pol_hin);
+        for (int u = 0; u < ng; ++u)
+          issue_tile<kBwd>(A, ch, jt[u], t, smem_u32(ring + static_cast<size_t>(stg[u]) * pl.stage_bytes),
+                           smem_u32(&full[stg[u]]), pol);
+      }
+      jj += ng;
     }
   }
 }
 
-// Output tile store (issued by consumer thread 0 once the staging buffer is complete).
-__device__ __forceinline__ void store_tile(const StreamArgs& A, const Chain& ch, int j, const uint8_t* buf, int nout,
-                                           const int64_t* planes, uint64_t pol) {
+// The storer thread: once the consumer warps of a horizontal tile have written its outputs in place
+// (over the consumed input rows) it stores them with TMA, waits until the bulk copy has read shared
+// memory, and only then hands the stage back to the producer. Vertical tiles store from registers,
+// so their stage is released as soon as the consumers are done with it.
+__device__ void storer_loop(const StreamArgs& A, uint8_t* ring, uint64_t* done, uint64_t* empty, int nout,
+                            const int* slots, bool bwd) {
   const Plan& pl = A.plan;
-  const int o = ch.vert ? 0 : 1;
-  const int s0 = tile_start(ch, j, pl.K);
-  for (int t = 0; t < nout; ++t) {
-    const uint32_t src = smem_u32(buf + static_cast<size_t>(t) * pl.tile_bytes);
-    if (ch.vert) {
-      for (int q = 0; q < pl.nbw; ++q)
-        tma_store3(&A.out[o][t], src + q * pl.K * pl.bw * pl.es, q * pl.bw, s0, static_cast<int>(planes[t]), pol);
-    } else {
-      for (int q = 0; q < pl.nbh; ++q)
-        tma_store3(&A.out[o][t], src + q * pl.bh * 16, s0, q * pl.bh, static_cast<int>(planes[t]), pol);
+  const uint64_t pol = policy_of(pl.pol[4]);
+  int stage = 0;
+  uint32_t phase = 0;
+  for (int64_t w = blockIdx.x; w < pl.nchains; w += gridDim.x) {
+    const Chain ch = make_chain(A.p, pl.K, w);
+    for (int jj = 0; jj < ch.ntiles; ++jj) {
+      const int j = bwd ? (ch.ntiles - 1 - jj) : jj;
+      mbar_wait(smem_u32(&done[stage]), phase);
+      if (!ch.vert) {
+        const int s0 = tile_start(ch, j, pl.K);
+        const uint8_t* st = ring + static_cast<size_t>(stage) * pl.stage_bytes;
+        for (int t = 0; t < nout; ++t) {
+          const int64_t plane = t == 0 ? ch.chain : ch.wplane;
+          const uint32_t src = smem_u32(st + static_cast<size_t>(slots[t]) * pl.tile_bytes);
+          for (int q = 0; q < pl.nbh; ++q)
+            tma_store3(&A.out[1][t], src + q * pl.bh * 16, s0, q * pl.bh, static_cast<int>(plane), pol);
+        }
+        bulk_commit();
+        bulk_wait_read0();
+      }
+      mbar_arrive(smem_u32(&empty[stage]));
+      if (++stage == pl.nstages) { stage = 0; phase ^= 1; }
     }
   }
-  bulk_commit();
+  bulk_wait_all();
 }
 
 // ------------------------------------------------------------------------------ per-lane geometry
@@ -422,6 +459,32 @@ template <> struct VE<float, 2> {
   }
   static __device__ __forceinline__ void store(uint8_t* p, const float (&v)[2]) {
     *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
+  }
+};
+
+// E consecutive outputs (E = 2 or 4) from registers straight to global memory (vertical chains:
+// a warp's owned positions are contiguous, so these stores coalesce).
+template <typename T, int E> struct GStore;
+template <> struct GStore<__nv_bfloat16, 2> {
+  static __device__ __forceinline__ void st(__nv_bfloat16* p, const float (&v)[2], uint64_t pol) {
+    __nv_bfloat162 a = __floats2bfloat162_rn(v[0], v[1]);
+    st_global_b32(p, *reinterpret_cast<uint32_t*>(&a), pol);
+  }
+};
+template <> struct GStore<__nv_bfloat16, 4> {
+  static __device__ __forceinline__ void st(__nv_bfloat16* p, const float (&v)[4], uint64_t pol) {
+    const uint2 u = V4<__nv_bfloat16>::pack(v);
+    st_global_v2(p, u.x, u.y, pol);
+  }
+};
+template <> struct GStore<float, 2> {
+  static __device__ __forceinline__ void st(float* p, const float (&v)[2], uint64_t pol) {
+    st_global_v2(p, __float_as_uint(v[0]), __float_as_uint(v[1]), pol);
+  }
+};
+template <> struct GStore<float, 4> {
+  static __device__ __forceinline__ void st(float* p, const float (&v)[4], uint64_t pol) {
+    st_global_v4(p, __float_as_uint(v[0]), __float_as_uint(v[1]), __float_as_uint(v[2]), __float_as_uint(v[3]), pol);
   }
 };
 
@@ -589,13 +652,18 @@ __device__ __forceinline__ void fwd_update(const Lanes<E>& ln, const float (&x)[
   for (int e = 0; e < E; ++e) h[e] = hn[e];
 }
 
-// Vertical tile: the step loop stays rolled (code size); the in-tile row is a runtime offset.
+// Vertical tile: the step loop stays rolled (code size); the in-tile row is a runtime offset. The
+// new state goes from registers straight to global memory (coalesced: a warp's owned positions
+// are contiguous).
 template <typename T, int E>
-__device__ __forceinline__ void fwd_tile_vert(const Plan& pl, const Lanes<E>& ln, const uint8_t* st, uint8_t* ob,
-                                              int lane, bool rev, float (&h)[E], bool prenorm) {
+__device__ __forceinline__ void fwd_tile_vert(const Plan& pl, const Lanes<E>& ln, const Chain& ch, int j,
+                                              const uint8_t* st, T* hplane, int64_t W, int lane, float (&h)[E],
+                                              bool prenorm, uint64_t pol) {
   constexpr int K = Cfg<T>::K;
+  const bool rev = ch.rev;
   const int dk = rev ? -static_cast<int>(ln.vstep) : static_cast<int>(ln.vstep);
   uint32_t off = ln.voff + (rev ? (K - 1) * ln.vstep : 0u);
+  const bool lane_out = ln.own[0] && ln.valid[0];  // P % E == 0: a lane's positions share validity
 #pragma unroll 1
   for (int s = 0; s < K; ++s, off += dk) {
     float x[E], lam[E], wl[E], wm[E], wr[E], hm1[E], hp1[E];
@@ -606,14 +674,20 @@ __device__ __forceinline__ void fwd_tile_vert(const Plan& pl, const Lanes<E>& ln
     VE<T, E>::load(st + F_WR * pl.tile_bytes + off, wr);
     vert_neighbours<E>(h, lane, hm1, hp1);
     fwd_update<E>(ln, x, lam, wl, wm, wr, hm1, hp1, h, prenorm);
-    if (ln.own[0]) VE<T, E>::store(ob + off, h);  // the lane's E positions are owned together
+    const int t = j * K + s;
+    if (lane_out && t < ch.L) {
+      const int row = rev ? (ch.L - 1 - t) : t;
+      GStore<T, E>::st(hplane + static_cast<int64_t>(row) * W + ln.pos[0], h, pol);
+    }
   }
 }
 
-// Horizontal tile: one 16-byte row chunk (K steps) per tensor per slot, put in scan order.
+// Horizontal tile: one 16-byte row chunk (K steps) per tensor per slot, put in scan order. Once every
+// consumer warp holds its rows in registers (named barrier), the new state is written in place over
+// the consumed x rows, from where the storer warp sends the tile out with TMA.
 template <typename T, int E>
-__device__ __forceinline__ void fwd_tile_horiz(const Plan& pl, const Lanes<E>& ln, const uint8_t* st, uint8_t* ob,
-                                               int lane, bool rev, float (&h)[E], bool prenorm) {
+__device__ __forceinline__ void fwd_tile_horiz(const Plan& pl, const Lanes<E>& ln, uint8_t* st, int lane, bool rev,
+                                               float (&h)[E], bool prenorm, int nthreads) {
   constexpr int K = Cfg<T>::K;
   uint4 X[E], LAM[E], WL[E], WM[E], WR[E], OUT[E];
 #pragma unroll
@@ -626,6 +700,7 @@ __device__ __forceinline__ void fwd_tile_horiz(const Plan& pl, const Lanes<E>& l
     WR[q] = Rev<T>::r(*reinterpret_cast<const uint4*>(st + F_WR * pl.tile_bytes + off), rev);
     OUT[q] = make_uint4(0, 0, 0, 0);
   }
+  named_bar(kBarRows, nthreads);  // all rows (incl. other warps' ghost rows) are in registers now
 #pragma unroll
   for (int s = 0; s < K; ++s) {
     float hm1[E], hp1[E], x[E], lam[E], wl[E], wm[E], wr[E];
@@ -644,73 +719,91 @@ __device__ __forceinline__ void fwd_tile_horiz(const Plan& pl, const Lanes<E>& l
   }
 #pragma unroll
   for (int q = 0; q < E; ++q)
-    if (ln.own[q]) *reinterpret_cast<uint4*>(ob + ln.row[q] * 16) = Rev<T>::r(OUT[q], rev);
+    if (ln.own[q]) *reinterpret_cast<uint4*>(st + F_X * pl.tile_bytes + ln.row[q] * 16) = Rev<T>::r(OUT[q], rev);
 }
 
-template <typename T, int E, int kMaxNWC>
-__global__ void __launch_bounds__((kMaxNWC + 1) * 32, kMaxNWC <= 6 ? 2 : 1)
-    fwd_stream_kernel(const __grid_constant__ StreamArgs A) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared space
-  const Plan& pl = A.plan;
-  uint8_t* ring = smem;
-  uint8_t* outbuf = ring + static_cast<size_t>(pl.nstages) * pl.stage_bytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(outbuf + 2 * static_cast<size_t>(pl.out_bytes));
-  uint64_t* empty = full + pl.nstages;
-  float* edge = reinterpret_cast<float*>(empty + pl.nstages);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+// Shared-memory carve-up common to both kernels: ring | full | empty | done | edges | flag.
+struct Smem {
+  uint8_t* ring;
+  uint64_t *full, *empty, *done;
+  float* edge;
+  int* flag;
+};
+
+__device__ __forceinline__ Smem carve(uint8_t* smem_raw, const Plan& pl) {
+  Smem m;
+  m.ring = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared space
+  m.full = reinterpret_cast<uint64_t*>(m.ring + static_cast<size_t>(pl.nstages) * pl.stage_bytes);
+  m.empty = m.full + pl.nstages;
+  m.done = m.empty + pl.nstages;
+  m.edge = reinterpret_cast<float*>(m.done + pl.nstages);  // [3 state arrays][2 par][kEdgeW][2][8]
+  m.flag = reinterpret_cast<int*>(m.edge + 3 * 2 * kEdgeW * 2 * 8);
+  return m;
+}
+
+__device__ __forceinline__ void init_barriers(const Smem& m, const Plan& pl) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < pl.nstages; ++s) {
-      mbar_init(smem_u32(&full[s]), 1);
-      mbar_init(smem_u32(&empty[s]), pl.nwc);
+      mbar_init(smem_u32(&m.full[s]), 1);       // producer arrive + TMA bytes
+      mbar_init(smem_u32(&m.empty[s]), 1);      // storer
+      mbar_init(smem_u32(&m.done[s]), pl.nwc);  // one arrive per consumer warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+}
+
+template <typename T, int E, int kMaxNWC>
+__global__ void __launch_bounds__((kMaxNWC + 2) * 32, kMaxNWC <= 6 ? 2 : 1)
+    fwd_stream_kernel(const __grid_constant__ StreamArgs A) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const Plan& pl = A.plan;
+  const Smem m = carve(smem_raw, pl);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  init_barriers(m, pl);
   if (warp == pl.nwc) {  // producer warp
     if (lane == 0) {
       for (int o = 0; o < 2; ++o)
         for (int t = 0; t < F_NIN; ++t) asm volatile("prefetch.tensormap [%0];" ::"l"(&A.in[o][t]) : "memory");
-      producer_loop<false>(A, ring, full, empty);
+      producer_loop<false>(A, m.ring, m.full, m.empty);
+    }
+    return;
+  }
+  if (warp == pl.nwc + 1) {  // storer warp
+    if (lane == 0) {
+      const int slots[1] = {F_X};
+      storer_loop(A, m.ring, m.done, m.empty, 1, slots, false);
     }
     return;
   }
   const bool prenorm = A.p.flags & GSPN_FLAG_PRENORMALIZED;
-  const uint64_t pol_out = policy_of(pl.pol[3]);
-  const uint64_t pol_keep = policy_of(pl.pol[4]);  // horizontal outputs: the sector completes one tile later
+  const uint64_t pol_vout = policy_of(pl.pol[3]);
   const int nthreads = pl.nwc * 32;
-  int stage = 0, par = 0, ob_sel = 0;
+  const int64_t HW = A.p.H * A.p.W;
+  int stage = 0, par = 0;
   uint32_t phase = 0;
   for (int64_t w = blockIdx.x; w < pl.nchains; w += gridDim.x) {
     const Chain ch = make_chain(A.p, pl.K, w);
     const Lanes<E> ln = make_lanes<T, E>(pl, ch, warp, lane);
+    T* hplane = static_cast<T*>(A.p.hout) + ch.chain * HW;
     float h[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) h[e] = 0.f;
     for (int j = 0; j < ch.ntiles; ++j) {
-      mbar_wait(smem_u32(&full[stage]), phase);
-      const uint8_t* st = ring + static_cast<size_t>(stage) * pl.stage_bytes;
-      uint8_t* ob = outbuf + static_cast<size_t>(ob_sel) * pl.out_bytes;
-      if (ch.vert) fwd_tile_vert<T, E>(pl, ln, st, ob, lane, ch.rev, h, prenorm);
-      else fwd_tile_horiz<T, E>(pl, ln, st, ob, lane, ch.rev, h, prenorm);
+      mbar_wait(smem_u32(&m.full[stage]), phase);
+      uint8_t* st = m.ring + static_cast<size_t>(stage) * pl.stage_bytes;
+      if (ch.vert) fwd_tile_vert<T, E>(pl, ln, ch, j, st, hplane, A.p.W, lane, h, prenorm, pol_vout);
+      else fwd_tile_horiz<T, E>(pl, ln, st, lane, ch.rev, h, prenorm, nthreads);
+      fence_proxy_async();  // in-place outputs -> visible to the storer's TMA (async proxy)
       __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&empty[stage]));
+      if (lane == 0) mbar_arrive(smem_u32(&m.done[stage]));
       if (++stage == pl.nstages) { stage = 0; phase ^= 1; }
-      edge_publish<T, E>(edge, par, warp, lane, ch.vert, h);
-      fence_proxy_async();
+      edge_publish<T, E>(m.edge, par, warp, lane, ch.vert, h);
       named_bar(kBarTile, nthreads);
-      if (threadIdx.x == 0) {
-        const int64_t planes[1] = {ch.chain};
-        store_tile(A, ch, j, ob, 1, planes, ch.vert ? pol_out : pol_keep);
-        bulk_wait_read1();
-      }
-      edge_reload<T, E>(edge, par, warp, pl.nwc, lane, ch.vert, h);
-      named_bar(kBarTile, nthreads);
+      edge_reload<T, E>(m.edge, par, warp, pl.nwc, lane, ch.vert, h);
       par ^= 1;
-      ob_sel ^= 1;
     }
   }
-  if (threadIdx.x == 0) bulk_wait_all();
 }
 
 // ------------------------------------------------------------------------------ backward consumer
@@ -765,8 +858,8 @@ __device__ __forceinline__ void bwd_update(const Lanes<E>& ln, bool live, const 
 
 template <typename T, int E, bool kGrouped>
 __device__ __forceinline__ void bwd_tile_vert(const StreamArgs& A, const Lanes<E>& ln, const Chain& ch, int j,
-                                              const uint8_t* st, uint8_t* ob, int lane, BwdState<E>& S, bool prenorm,
-                                              uint64_t pol_acc) {
+                                              const uint8_t* st, int lane, BwdState<E>& S, bool prenorm,
+                                              uint64_t pol_acc, uint64_t pol_out) {
   constexpr int K = Cfg<T>::K;
   const Plan& pl = A.plan;
   const ScanParams& p = A.p;
@@ -794,17 +887,15 @@ __device__ __forceinline__ void bwd_tile_vert(const StreamArgs& A, const Lanes<E
     vert_neighbours<E>(S.ec, lane, nl, hi_c);   // nl[e] = (c g) of position e - 1
     float dlam[E], o1[E], o2[E], o3[E], dxv[E];
     bwd_update<E, kGrouped>(ln, live, x, lam, dh, wl, wm, wr, hm1, hp, hp1, nr, nl, S, dlam, o1, o2, o3, dxv, prenorm);
-    if (ln.own[0]) {
-      VE<T, E>::store(ob + O_DLAM * pl.tile_bytes + off, dlam);
-      if (!kGrouped) {
-        VE<T, E>::store(ob + O_DWL * pl.tile_bytes + off, o1);
-        VE<T, E>::store(ob + O_DWM * pl.tile_bytes + off, o2);
-        VE<T, E>::store(ob + O_DWR * pl.tile_bytes + off, o3);
-      }
-    }
     if (lane_out && live) {
       const int row = ch.rev ? (ch.L - 1 - t) : t;
       const int64_t o = static_cast<int64_t>(row) * p.W + ln.pos[0];
+      GStore<T, E>::st(static_cast<T*>(p.dlam) + ch.chain * HW + o, dlam, pol_out);
+      if (!kGrouped) {
+        GStore<T, E>::st(static_cast<T*>(p.dwl) + wofs + o, o1, pol_out);
+        GStore<T, E>::st(static_cast<T*>(p.dwm) + wofs + o, o2, pol_out);
+        GStore<T, E>::st(static_cast<T*>(p.dwr) + wofs + o, o3, pol_out);
+      }
       red_add_vec<E>(dxacc + o, dxv, pol_acc);
       if (kGrouped && t >= 1) {
         red_add_vec<E>(p.dwa_l + wofs + o, o1, pol_acc);
@@ -821,8 +912,8 @@ __device__ __forceinline__ void bwd_tile_vert(const StreamArgs& A, const Lanes<E
 // copy of the unrolled step code. h_{t-1} is read per step from the 2K-step swizzled h row.
 template <typename T, int E, bool kGrouped>
 __device__ __forceinline__ void bwd_tile_horiz(const StreamArgs& A, const Lanes<E>& ln, const Chain& ch, int j,
-                                               const uint8_t* st, uint8_t* ob, int lane, BwdState<E>& S,
-                                               bool prenorm, uint64_t pol_acc) {
+                                               uint8_t* st, int lane, BwdState<E>& S, bool prenorm,
+                                               uint64_t pol_acc, int nthreads) {
   using C = Cfg<T>;
   constexpr int K = C::K, KS = C::KS, NSUB = K / KS;
   static_assert(NSUB == 2, "sub-tiles are the two 8-byte halves of a 16-byte row chunk");
@@ -845,6 +936,9 @@ __device__ __forceinline__ void bwd_tile_horiz(const StreamArgs& A, const Lanes<
     WM[q] = Rev<T>::r(*reinterpret_cast<const uint4*>(st + B_WM * pl.tile_bytes + off), rev);
     WR[q] = Rev<T>::r(*reinterpret_cast<const uint4*>(st + B_WR * pl.tile_bytes + off), rev);
   }
+  // every consumer warp holds its rows in registers: outputs may now overwrite x and the taps in place
+  named_bar(kBarRows, nthreads);
+  uint8_t* ob = st;  // dlam -> x slot, dw_l/m/r -> w_l/m/r slots (O_* == B_* slot indices below)
 #pragma unroll 1
   for (int sub = NSUB - 1; sub >= 0; --sub) {
     uint2 x2[E], lam2[E], dh2[E], wl2[E], wm2[E], wr2[E];
@@ -909,11 +1003,11 @@ __device__ __forceinline__ void bwd_tile_horiz(const StreamArgs& A, const Lanes<
     for (int q = 0; q < E; ++q) {
       if (!ln.own[q]) continue;
       const uint32_t off = ln.row[q] * 16 + c8 * 8;
-      *reinterpret_cast<uint2*>(ob + O_DLAM * pl.tile_bytes + off) = Rev<T>::r(OL[q], rev);
+      *reinterpret_cast<uint2*>(ob + B_X * pl.tile_bytes + off) = Rev<T>::r(OL[q], rev);
       if (!kGrouped) {
-        *reinterpret_cast<uint2*>(ob + O_DWL * pl.tile_bytes + off) = Rev<T>::r(O1[q], rev);
-        *reinterpret_cast<uint2*>(ob + O_DWM * pl.tile_bytes + off) = Rev<T>::r(O2[q], rev);
-        *reinterpret_cast<uint2*>(ob + O_DWR * pl.tile_bytes + off) = Rev<T>::r(O3[q], rev);
+        *reinterpret_cast<uint2*>(ob + B_WL * pl.tile_bytes + off) = Rev<T>::r(O1[q], rev);
+        *reinterpret_cast<uint2*>(ob + B_WM * pl.tile_bytes + off) = Rev<T>::r(O2[q], rev);
+        *reinterpret_cast<uint2*>(ob + B_WR * pl.tile_bytes + off) = Rev<T>::r(O3[q], rev);
       }
       if (ln.valid[q]) {
         const int64_t o = static_cast<int64_t>(ln.pos[q]) * p.W + c0 + c8 * KS;
@@ -1002,40 +1096,33 @@ __device__ void bwd_chain_epilogue(const StreamArgs& A, const Chain& ch, int* fl
 }
 
 template <typename T, int E, bool kGrouped, int kMaxNWC>
-__global__ void __launch_bounds__((kMaxNWC + 1) * 32, 1) bwd_stream_kernel(const __grid_constant__ StreamArgs A) {
+__global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_stream_kernel(const __grid_constant__ StreamArgs A) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared space
   const Plan& pl = A.plan;
-  uint8_t* ring = smem;
-  uint8_t* outbuf = ring + static_cast<size_t>(pl.nstages) * pl.stage_bytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(outbuf + 2 * static_cast<size_t>(pl.out_bytes));
-  uint64_t* empty = full + pl.nstages;
-  float* edge = reinterpret_cast<float*>(empty + pl.nstages);  // [3 state arrays][2 par][kEdgeW][2][8]
-  int* flag = reinterpret_cast<int*>(edge + 3 * 2 * kEdgeW * 2 * 8);
+  const Smem m = carve(smem_raw, pl);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < pl.nstages; ++s) {
-      mbar_init(smem_u32(&full[s]), 1);
-      mbar_init(smem_u32(&empty[s]), pl.nwc);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
+  init_barriers(m, pl);
   if (warp == pl.nwc) {
     if (lane == 0) {
       for (int o = 0; o < 2; ++o)
         for (int t = 0; t < B_NIN; ++t) asm volatile("prefetch.tensormap [%0];" ::"l"(&A.in[o][t]) : "memory");
-      producer_loop<true>(A, ring, full, empty);
+      producer_loop<true>(A, m.ring, m.full, m.empty);
+    }
+    return;
+  }
+  if (warp == pl.nwc + 1) {  // storer warp (horizontal tiles' in-place outputs)
+    if (lane == 0) {
+      const int slots[4] = {B_X, B_WL, B_WM, B_WR};
+      storer_loop(A, m.ring, m.done, m.empty, kGrouped ? 1 : 4, slots, true);
     }
     return;
   }
   const bool prenorm = A.p.flags & GSPN_FLAG_PRENORMALIZED;
-  const uint64_t pol_out = policy_of(pl.pol[3]);
-  const uint64_t pol_keep = policy_of(pl.pol[4]);  // horizontal outputs: the sector completes one tile later
+  const uint64_t pol_vout = policy_of(pl.pol[3]);
   const uint64_t pol_acc = policy_of(pl.pol[5]);
   const int nthreads = pl.nwc * 32;
   constexpr int kEdgeArr = 2 * kEdgeW * 2 * 8;
-  int stage = 0, par = 0, ob_sel = 0;
+  int stage = 0, par = 0;
   uint32_t phase = 0;
   for (int64_t w = blockIdx.x; w < pl.nchains; w += gridDim.x) {
     const Chain ch = make_chain(A.p, pl.K, w);
@@ -1045,34 +1132,25 @@ __global__ void __launch_bounds__((kMaxNWC + 1) * 32, 1) bwd_stream_kernel(const
     for (int e = 0; e < E; ++e) S.ea[e] = S.eb[e] = S.ec[e] = 0.f;
     for (int jj = 0; jj < ch.ntiles; ++jj) {
       const int j = ch.ntiles - 1 - jj;
-      mbar_wait(smem_u32(&full[stage]), phase);
-      const uint8_t* st = ring + static_cast<size_t>(stage) * pl.stage_bytes;
-      uint8_t* ob = outbuf + static_cast<size_t>(ob_sel) * pl.out_bytes;
-      if (ch.vert) bwd_tile_vert<T, E, kGrouped>(A, ln, ch, j, st, ob, lane, S, prenorm, pol_acc);
-      else bwd_tile_horiz<T, E, kGrouped>(A, ln, ch, j, st, ob, lane, S, prenorm, pol_acc);
+      mbar_wait(smem_u32(&m.full[stage]), phase);
+      uint8_t* st = m.ring + static_cast<size_t>(stage) * pl.stage_bytes;
+      if (ch.vert) bwd_tile_vert<T, E, kGrouped>(A, ln, ch, j, st, lane, S, prenorm, pol_acc, pol_vout);
+      else bwd_tile_horiz<T, E, kGrouped>(A, ln, ch, j, st, lane, S, prenorm, pol_acc, nthreads);
+      fence_proxy_async();  // in-place outputs -> visible to the storer's TMA (async proxy)
       __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&empty[stage]));
+      if (lane == 0) mbar_arrive(smem_u32(&m.done[stage]));
       if (++stage == pl.nstages) { stage = 0; phase ^= 1; }
-      edge_publish<T, E>(edge + 0 * kEdgeArr, par, warp, lane, ch.vert, S.ea);
-      edge_publish<T, E>(edge + 1 * kEdgeArr, par, warp, lane, ch.vert, S.eb);
-      edge_publish<T, E>(edge + 2 * kEdgeArr, par, warp, lane, ch.vert, S.ec);
-      fence_proxy_async();
+      edge_publish<T, E>(m.edge + 0 * kEdgeArr, par, warp, lane, ch.vert, S.ea);
+      edge_publish<T, E>(m.edge + 1 * kEdgeArr, par, warp, lane, ch.vert, S.eb);
+      edge_publish<T, E>(m.edge + 2 * kEdgeArr, par, warp, lane, ch.vert, S.ec);
       named_bar(kBarTile, nthreads);
-      if (threadIdx.x == 0) {
-        const int64_t planes[4] = {ch.chain, ch.wplane, ch.wplane, ch.wplane};
-        store_tile(A, ch, j, ob, kGrouped ? 1 : 4, planes, ch.vert ? pol_out : pol_keep);
-        bulk_wait_read1();
-      }
-      edge_reload<T, E>(edge + 0 * kEdgeArr, par, warp, pl.nwc, lane, ch.vert, S.ea);
-      edge_reload<T, E>(edge + 1 * kEdgeArr, par, warp, pl.nwc, lane, ch.vert, S.eb);
-      edge_reload<T, E>(edge + 2 * kEdgeArr, par, warp, pl.nwc, lane, ch.vert, S.ec);
-      named_bar(kBarTile, nthreads);
+      edge_reload<T, E>(m.edge + 0 * kEdgeArr, par, warp, pl.nwc, lane, ch.vert, S.ea);
+      edge_reload<T, E>(m.edge + 1 * kEdgeArr, par, warp, pl.nwc, lane, ch.vert, S.eb);
+      edge_reload<T, E>(m.edge + 2 * kEdgeArr, par, warp, pl.nwc, lane, ch.vert, S.ec);
       par ^= 1;
-      ob_sel ^= 1;
     }
-    bwd_chain_epilogue<T, kGrouped>(A, ch, flag, nthreads);
+    bwd_chain_epilogue<T, kGrouped>(A, ch, m.flag, nthreads);
   }
-  if (threadIdx.x == 0) bulk_wait_all();
 }
 
 // ------------------------------------------------------------------------------------- host side
@@ -1145,7 +1223,7 @@ CUtensorMapL2promotion horiz_promotion() {
   }
 }
 
-constexpr int kSmemTail = 8192;  // mbarriers, ghost-edge buffers, flags
+constexpr int kSmemTail = 6656;  // mbarriers (3 per stage), ghost-edge buffers (6 KB), flag
 
 // Shape eligibility + plan. nin/nout: tensors per tile.
 bool make_plan(const ScanParams& p, gspn_dtype_t dt, int nin, int nout, int min_stages, bool two_ctas, int E,
@@ -1185,16 +1263,18 @@ bool make_plan(const ScanParams& p, gspn_dtype_t dt, int nin, int nout, int min_
   pl->tile_bytes = static_cast<uint32_t>(pl->K * pl->ppad * s);
   pl->h_wide = (nin == B_NIN) ? 1 : 0;
   pl->stage_bytes = (nin + pl->h_wide) * pl->tile_bytes;
-  pl->out_bytes = nout * pl->tile_bytes;
   pl->tx_v = static_cast<uint32_t>(nin * pl->nbw * pl->bw * pl->K * s);
   pl->tx_h = static_cast<uint32_t>((nin + pl->h_wide) * pl->nbh * pl->bh * pl->K * s);
   const int budget = smem_optin() - 1024 /*alignment*/ - kSmemTail;
-  const int avail = budget - 2 * static_cast<int>(pl->out_bytes);
+  const int avail = budget;
   int ns = avail / static_cast<int>(pl->stage_bytes);
   // Two CTAs per SM when both fit with >= 2 stages each: the second chain hides the first's
   // per-tile latencies. Otherwise one CTA with a deeper ring.
-  const int half = (smem_optin() / 2 - 1024 - kSmemTail - 2 * static_cast<int>(pl->out_bytes)) /
+  const int half = (smem_optin() / 2 - 1024 - kSmemTail) /
                    static_cast<int>(pl->stage_bytes);
+  if (const char* e = getenv("GSPN_FWD_CTAS")) {  // experiments: force the fwd to 1 or 2 CTAs per SM
+    if (two_ctas && atoi(e) == 1) two_ctas = false;
+  }
   if (two_ctas && half >= 2 && pl->nwc <= 6) ns = std::min(half, 4);
   if (ns > 8) ns = 8;
   if (ns < min_stages) return false;
@@ -1207,7 +1287,9 @@ bool make_plan(const ScanParams& p, gspn_dtype_t dt, int nin, int nout, int min_
     int v[6], n = sscanf(e, "%d,%d,%d,%d,%d,%d", &v[0], &v[1], &v[2], &v[3], &v[4], &v[5]);
     for (int i = 0; i < n && i < 6; ++i) pl->pol[i] = v[i];
   }
-  pl->smem_bytes = 1024 + ns * pl->stage_bytes + 2 * pl->out_bytes + kSmemTail;
+  pl->smem_bytes = 1024 + ns * pl->stage_bytes + kSmemTail;
+  pl->pair = ns >= 3 ? 1 : 0;
+  if (const char* e = getenv("GSPN_PAIR")) pl->pair = pl->pair && atoi(e) != 0;
   return true;
 }
 
@@ -1237,7 +1319,7 @@ cudaError_t launch(KernelT kernel, const StreamArgs& A, cudaStream_t s) {
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(A.plan.smem_bytes));
   if (e != cudaSuccess) return e;
-  const int threads = (A.plan.nwc + 1) * 32;
+  const int threads = (A.plan.nwc + 2) * 32;  // consumers + producer + storer
   int per_sm = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, A.plan.smem_bytes);
   if (e != cudaSuccess) return e;
