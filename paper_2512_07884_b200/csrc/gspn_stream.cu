@@ -66,6 +66,8 @@ struct Plan {
   int bh, nbh;         // horizontal TMA box height (positions) and box count
   int nin, nout;       // input / output tensors per tile
   int pair;            // load horizontal tiles in back-to-back pairs (ring of >= 3 stages)
+  int null_compute;    // experiments only (GSPN_NULL=1): consumers skip the arithmetic (pipeline ceiling)
+  int nosleep;         // experiments only (GSPN_NOSLEEP=1): producer polls instead of sleeping
   int h_wide;          // bwd: the last input (h) holds 2K steps for horizontal chains
   int nstages;
   uint32_t tile_bytes;   // one tensor's tile: K * ppad * es (= 16 * ppad)
@@ -381,7 +383,8 @@ __device__ void producer_loop(const StreamArgs& A, uint8_t* ring, uint64_t* full
       const int ng = (!ch.vert && pl.pair && jj + 1 < ch.ntiles) ? 2 : 1;
       int stg[2], jt[2];
       for (int u = 0; u < ng; ++u) {
-        mbar_wait_sleep(smem_u32(&empty[stage]), phase ^ 1);
+        if (pl.nosleep) mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+        else mbar_wait_sleep(smem_u32(&empty[stage]), phase ^ 1);
         mbar_arrive_tx(smem_u32(&full[stage]), ch.vert ? pl.tx_v : pl.tx_h);
         stg[u] = stage;
         jt[u] = kBwd ? (ch.ntiles - 1 - (jj + u)) : (jj + u);
@@ -792,8 +795,12 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, kMaxNWC <= 6 ? 2 : 1)
     for (int j = 0; j < ch.ntiles; ++j) {
       mbar_wait(smem_u32(&m.full[stage]), phase);
       uint8_t* st = m.ring + static_cast<size_t>(stage) * pl.stage_bytes;
-      if (ch.vert) fwd_tile_vert<T, E>(pl, ln, ch, j, st, hplane, A.p.W, lane, h, prenorm, pol_vout);
-      else fwd_tile_horiz<T, E>(pl, ln, st, lane, ch.rev, h, prenorm, nthreads);
+      if (pl.null_compute) {
+      } else if (ch.vert) {
+        fwd_tile_vert<T, E>(pl, ln, ch, j, st, hplane, A.p.W, lane, h, prenorm, pol_vout);
+      } else {
+        fwd_tile_horiz<T, E>(pl, ln, st, lane, ch.rev, h, prenorm, nthreads);
+      }
       fence_proxy_async();  // in-place outputs -> visible to the storer's TMA (async proxy)
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&m.done[stage]));
@@ -1134,8 +1141,12 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_stream_kernel(const
       const int j = ch.ntiles - 1 - jj;
       mbar_wait(smem_u32(&m.full[stage]), phase);
       uint8_t* st = m.ring + static_cast<size_t>(stage) * pl.stage_bytes;
-      if (ch.vert) bwd_tile_vert<T, E, kGrouped>(A, ln, ch, j, st, lane, S, prenorm, pol_acc, pol_vout);
-      else bwd_tile_horiz<T, E, kGrouped>(A, ln, ch, j, st, lane, S, prenorm, pol_acc, nthreads);
+      if (pl.null_compute) {
+      } else if (ch.vert) {
+        bwd_tile_vert<T, E, kGrouped>(A, ln, ch, j, st, lane, S, prenorm, pol_acc, pol_vout);
+      } else {
+        bwd_tile_horiz<T, E, kGrouped>(A, ln, ch, j, st, lane, S, prenorm, pol_acc, nthreads);
+      }
       fence_proxy_async();  // in-place outputs -> visible to the storer's TMA (async proxy)
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&m.done[stage]));
@@ -1281,7 +1292,7 @@ bool make_plan(const ScanParams& p, gspn_dtype_t dt, int nin, int nout, int min_
   pl->nstages = ns;
   pl->nchains = p.D * p.B * p.C;
   // L2 priorities (experiments: GSPN_POL="x,vin,hin,vout,hout,acc", each 0|1|2)
-  static const int def_pol[6] = {1, 0, 1, 0, 1, 2};
+  static const int def_pol[6] = {1, 0, 2, 0, 1, 1};
   for (int i = 0; i < 6; ++i) pl->pol[i] = def_pol[i];
   if (const char* e = getenv("GSPN_POL")) {
     int v[6], n = sscanf(e, "%d,%d,%d,%d,%d,%d", &v[0], &v[1], &v[2], &v[3], &v[4], &v[5]);
@@ -1290,6 +1301,8 @@ bool make_plan(const ScanParams& p, gspn_dtype_t dt, int nin, int nout, int min_
   pl->smem_bytes = 1024 + ns * pl->stage_bytes + kSmemTail;
   pl->pair = ns >= 3 ? 1 : 0;
   if (const char* e = getenv("GSPN_PAIR")) pl->pair = pl->pair && atoi(e) != 0;
+  if (const char* e = getenv("GSPN_NULL")) pl->null_compute = atoi(e) != 0;
+  if (const char* e = getenv("GSPN_NOSLEEP")) pl->nosleep = atoi(e) != 0;
   return true;
 }
 
