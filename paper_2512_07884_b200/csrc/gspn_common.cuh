@@ -91,6 +91,9 @@ __device__ __forceinline__ Taps make_taps(float wl, float wm, float wr, bool has
 //   dw_r = (Dc - q)/S = ((l + m) Dc - l Da - m Db) / S^2
 // The right-hand forms avoid the cancellation of q against D and are exactly 0 when only one tap is
 // in range (P = 1). With pre-normalised taps the map is the identity on the in-range taps.
+// kFastRcp: rcp.approx (<= 1 ulp) instead of the IEEE-rounded reciprocal (which carries a slow-path
+// branch); the streaming kernels use it, the generic path keeps __frcp_rn.
+template <bool kFastRcp = false>
 __device__ __forceinline__ void jacobian(float wl, float wm, float wr, bool has_l, bool has_r, bool prenorm,
                                          float Da, float Db, float Dc, float& dwl, float& dwm, float& dwr) {
   const float l = has_l ? wl : 0.f;
@@ -99,7 +102,9 @@ __device__ __forceinline__ void jacobian(float wl, float wm, float wr, bool has_
     dwl = has_l ? Da : 0.f; dwm = Db; dwr = has_r ? Dc : 0.f;
     return;
   }
-  const float inv = __frcp_rn(wm + l + r);
+  float inv;
+  if constexpr (kFastRcp) asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(wm + l + r));
+  else inv = __frcp_rn(wm + l + r);
   const float inv2 = inv * inv;
   dwl = has_l ? fmaf(wm + r, Da, -fmaf(wm, Db, r * Dc)) * inv2 : 0.f;
   dwm = fmaf(l + r, Db, -fmaf(l, Da, r * Dc)) * inv2;

@@ -56,7 +56,6 @@ constexpr int kMaxIn = 6;
 constexpr int kMaxOut = 2;
 constexpr int kEdgeW = 16;     // max consumer warps (edge-buffer slots)
 constexpr int kBarEdge = 1;    // named barrier ids (0 is __syncthreads)
-constexpr int kBarEpi = 2;
 
 template <typename T>
 struct Cfg {
@@ -213,7 +212,11 @@ struct Chain {
 __device__ __forceinline__ Chain make_chain(const ScanParams& p, int K, int64_t w) {
   Chain ch;
   const int64_t bc = w / p.D;
-  ch.k = static_cast<int>(w % p.D);
+  // Round i of the persistent grid covers slots [i G, (i+1) G): whole planes when D divides G. The
+  // direction is rotated by i so every CTA cycles through all D directions (vertical and horizontal
+  // chains run at different speeds; a fixed direction per CTA would leave the fast ones idle).
+  const int64_t G = gridDim.x;
+  ch.k = static_cast<int>(G % p.D == 0 ? (w + w / G) % p.D : w % p.D);
   const uint32_t dir = p.dirbit[ch.k];
   ch.vert = (dir == GSPN_DIR_T2B) || (dir == GSPN_DIR_B2T);
   ch.rev = (dir == GSPN_DIR_B2T) || (dir == GSPN_DIR_R2L);
@@ -244,12 +247,12 @@ __device__ __forceinline__ int tile_step0(const Chain& ch, int j, int K) {
 
 // Input tensor slots.
 enum FwdIn { F_X = 0, F_LAM, F_WL, F_WM, F_WR, F_NIN };
-enum BwdIn { B_X = 0, B_LAM, B_DH, B_WL, B_WM, B_WR, B_NIN };
+enum BwdIn { B_DH = 0, B_WL, B_WM, B_WR, B_NIN };
 
 template <bool kBwd>
 __device__ __forceinline__ int64_t plane_of(const Chain& ch, int slot) {
-  const bool is_x = slot == 0;
-  const bool is_w = kBwd ? (slot == B_WL || slot == B_WM || slot == B_WR) : (slot == F_WL || slot == F_WM || slot == F_WR);
+  const bool is_x = !kBwd && slot == F_X;
+  const bool is_w = kBwd ? slot >= B_WL : slot >= F_WL;
   return is_x ? ch.bc : (is_w ? ch.wplane : ch.chain);
 }
 
@@ -276,7 +279,7 @@ __device__ void producer_loop(const StreamArgs& A, uint8_t* ring, uint64_t* full
       for (int t = 0; t < pl.nin; ++t) {
         const int plane = static_cast<int>(plane_of<kBwd>(ch, t));
         // x is re-read by the plane's other directions; vertical streams are read exactly once
-        const uint64_t pol = t == 0 ? pol_xin : (ch.vert ? pol_vin : pol_hin);
+        const uint64_t pol = (!kBwd && t == F_X) ? pol_xin : (ch.vert ? pol_vin : pol_hin);
         const uint32_t dst = st + t * pl.tile_bytes;
         if (ch.vert) {
           for (int q = 0; q < pl.nbw; ++q)
@@ -660,14 +663,11 @@ __device__ __forceinline__ void bwd_update(const Lanes<E>& ln, bool live, const 
 template <typename T, int E>
 __device__ __forceinline__ void bwd_half_vert(const StreamArgs& A, const Lanes<E>& ln, const Chain& ch, int j,
                                               int half, const uint8_t* st, int lane, BwdState<E>& S, bool prenorm,
-                                              uint64_t pol_acc, uint64_t pol_out) {
+                                              uint64_t pol_out) {
   constexpr int K = Cfg<T>::K, KS = Cfg<T>::KS;
   const Plan& pl = A.plan;
   const ScanParams& p = A.p;
-  const int64_t HW = p.H * p.W;
-  float* dxacc = p.dx_acc + ch.bc * HW;
-  T* dlam = static_cast<T*>(p.dlam) + ch.chain * HW;
-  T* gout = static_cast<T*>(A.g) + ch.chain * HW;
+  T* gout = static_cast<T*>(A.g) + ch.chain * p.H * p.W;
   const bool lane_out = ln.own[0] && ln.valid[0];
 #pragma unroll 1
   for (int ss = KS - 1; ss >= 0; --ss) {
@@ -676,9 +676,7 @@ __device__ __forceinline__ void bwd_half_vert(const StreamArgs& A, const Lanes<E
     const bool live = t < ch.L;
     const int kk = ch.rev ? (K - 1 - s) : s;
     const uint32_t off = ln.voff + kk * ln.vstep;
-    float x[E], lam[E], dh[E], wl[E], wm[E], wr[E], nr[E], nl[E], lo_a[E], hi_c[E], g[E];
-    VE<T, E>::load(st + B_X * pl.tile_bytes + off, x);
-    VE<T, E>::load(st + B_LAM * pl.tile_bytes + off, lam);
+    float dh[E], wl[E], wm[E], wr[E], nr[E], nl[E], lo_a[E], hi_c[E], g[E];
     VE<T, E>::load(st + B_DH * pl.tile_bytes + off, dh);
     VE<T, E>::load(st + B_WL * pl.tile_bytes + off, wl);
     VE<T, E>::load(st + B_WM * pl.tile_bytes + off, wm);
@@ -688,45 +686,33 @@ __device__ __forceinline__ void bwd_half_vert(const StreamArgs& A, const Lanes<E
     bwd_update<E>(ln, live, dh, wl, wm, wr, nr, nl, S, g, prenorm);
     if (lane_out && live) {
       const int row = ch.rev ? (ch.L - 1 - t) : t;
-      const int64_t o = static_cast<int64_t>(row) * p.W + ln.pos[0];
-      float dl[E], dxv[E];
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        dl[e] = g[e] * x[e];
-        dxv[e] = g[e] * lam[e];
-      }
-      GStore<T, E>::st(dlam + o, dl, pol_out);
-      GStore<T, E>::st(gout + o, g, pol_out);
-      red_add_vec<E>(dxacc + o, dxv, pol_acc);
+      GStore<T, E>::st(gout + static_cast<int64_t>(row) * p.W + ln.pos[0], g, pol_out);
     }
   }
 }
 
-// Horizontal half-tile (KS steps, descending). dlam and g come back packed for the in-place write,
-// the per-step g lam in DX (canonical order) for the dx reduction.
+// Horizontal half-tile (KS steps, descending); g comes back packed for the in-place write.
 template <typename T, int E>
 __device__ __forceinline__ void bwd_half_horiz(const Lanes<E>& ln, const Chain& ch, int j, int half,
                                                const uint8_t* st, uint32_t tile_bytes, int lane, BwdState<E>& S,
-                                               bool prenorm, uint4 (&OL)[E], uint4 (&OG)[E],
-                                               float (&DX)[E][Cfg<T>::KS]) {
+                                               bool prenorm, uint4 (&OG)[E]) {
   constexpr int K = Cfg<T>::K, KS = Cfg<T>::KS;
   const bool rev = ch.rev;
   const int cm = rev ? 1 - half : half;
-  uint4 X[E], LAM[E], DH[E], WL[E], WM[E], WR[E];
+  uint4 DH[E], WL[E], WM[E], WR[E];
 #pragma unroll
   for (int q = 0; q < E; ++q) {
     const uint32_t off = hchunk(ln.row[q], cm);
-    X[q] = Rev<T>::r(*reinterpret_cast<const uint4*>(st + B_X * tile_bytes + off), rev);
-    LAM[q] = Rev<T>::r(*reinterpret_cast<const uint4*>(st + B_LAM * tile_bytes + off), rev);
     DH[q] = Rev<T>::r(*reinterpret_cast<const uint4*>(st + B_DH * tile_bytes + off), rev);
     WL[q] = Rev<T>::r(*reinterpret_cast<const uint4*>(st + B_WL * tile_bytes + off), rev);
     WM[q] = Rev<T>::r(*reinterpret_cast<const uint4*>(st + B_WM * tile_bytes + off), rev);
     WR[q] = Rev<T>::r(*reinterpret_cast<const uint4*>(st + B_WR * tile_bytes + off), rev);
   }
-  float L_[E][KS], G_[E][KS];
+  float G_[E][KS];
+  const int t0 = tile_step0(ch, j, K) + half * KS;
 #pragma unroll
   for (int ss = KS - 1; ss >= 0; --ss) {
-    const int t = tile_step0(ch, j, K) + half * KS + ss;
+    const int t = t0 + ss;
     float dh[E], wl[E], wm[E], wr[E], nr[E], nl[E], ea_lo[E], ec_hi[E], g[E];
 #pragma unroll
     for (int q = 0; q < E; ++q) {
@@ -739,61 +725,10 @@ __device__ __forceinline__ void bwd_half_horiz(const Lanes<E>& ln, const Chain& 
     slot_neighbours<E>(S.ec, lane, nl, ec_hi);
     bwd_update<E>(ln, t >= 0 && t < ch.L, dh, wl, wm, wr, nr, nl, S, g, prenorm);
 #pragma unroll
-    for (int q = 0; q < E; ++q) {
-      L_[q][ss] = g[q] * Pk<T>::get(X[q], ss);
-      G_[q][ss] = g[q];
-      // canonical order within the chunk: element ss for L2R, KS-1-ss for R2L
-      DX[q][rev ? KS - 1 - ss : ss] = g[q] * Pk<T>::get(LAM[q], ss);
-    }
+    for (int q = 0; q < E; ++q) G_[q][ss] = g[q];
   }
 #pragma unroll
-  for (int q = 0; q < E; ++q) {
-    OL[q] = Rev<T>::r(Pk<T>::pack(L_[q]), rev);
-    OG[q] = Rev<T>::r(Pk<T>::pack(G_[q]), rev);
-  }
-}
-
-// The last of a plane's D chains converts the fp32 dx accumulator and drops it from L2 (discard: no
-// write-back of dead lines).
-template <typename T>
-__device__ void bwd_chain_epilogue(const StreamArgs& A, const Chain& ch, int* flag, int nthreads) {
-  const ScanParams& p = A.p;
-  const int64_t HW = p.H * p.W;
-  __threadfence();
-  named_bar(kBarEpi, nthreads);
-  if (threadIdx.x == 0) *flag = atomicAdd(&p.counters[ch.bc], 1u) == static_cast<unsigned>(p.D - 1);
-  named_bar(kBarEpi, nthreads);
-  const int f = *flag;
-  named_bar(kBarEpi, nthreads);  // flag slot reusable by the next chain
-  if (!f) return;
-  __threadfence();
-  const float4* src = reinterpret_cast<const float4*>(p.dx_acc + ch.bc * HW);
-  T* dst = static_cast<T*>(p.dx) + ch.bc * HW;
-  const int64_t n4 = HW / 4;
-  constexpr int U = 8;  // independent L2 loads in flight per thread
-  for (int64_t i0 = threadIdx.x; i0 < n4; i0 += static_cast<int64_t>(U) * nthreads) {
-    float4 v[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t i = i0 + static_cast<int64_t>(u) * nthreads;
-      v[u] = i < n4 ? __ldcg(src + i) : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t i = i0 + static_cast<int64_t>(u) * nthreads;
-      if (i < n4) {
-        if constexpr (sizeof(T) == 2) {
-          *reinterpret_cast<uint2*>(dst + 4 * i) =
-              make_uint2(pack_bf16x2(v[u].x, v[u].y), pack_bf16x2(v[u].z, v[u].w));
-        } else {
-          *reinterpret_cast<float4*>(dst + 4 * i) = v[u];
-        }
-      }
-    }
-  }
-  named_bar(kBarEpi, nthreads);
-  const char* base = reinterpret_cast<const char*>(p.dx_acc + ch.bc * HW);
-  for (int64_t l = threadIdx.x; l < (HW * 4) / 128; l += nthreads) discard_l2_line(base + l * 128);
+  for (int q = 0; q < E; ++q) OG[q] = Rev<T>::r(Pk<T>::pack(G_[q]), rev);
 }
 
 template <typename T, int E, int kMaxNWC>
@@ -812,25 +747,22 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_stream_kernel(const
     }
     return;
   }
-  if (warp == pl.nwc + 1) {  // storer warp: horizontal tiles' dlam (x slot) and g (dh slot)
+  if (warp == pl.nwc + 1) {  // storer warp: horizontal tiles' g (written over the dh slot)
     if (lane == 0) {
-      const int slots[2] = {B_X, B_DH};
-      storer_loop(A, m.ring, m.done, m.empty, 2, slots, true);
+      const int slots[1] = {B_DH};
+      storer_loop(A, m.ring, m.done, m.empty, 1, slots, true);
     }
     return;
   }
   const bool prenorm = A.p.flags & GSPN_FLAG_PRENORMALIZED;
   const uint64_t pol_vout = policy_of(pl.pol[3]);
-  const uint64_t pol_acc = policy_of(pl.pol[5]);
   const int nthreads = pl.nwc * 32;
   constexpr int kEdgeArr = 2 * kEdgeW * 2 * 8;
-  const int64_t HW = A.p.H * A.p.W;
   int stage = 0, par = 0;
   uint32_t phase = 0;
   for (int64_t w = blockIdx.x; w < pl.nchains; w += gridDim.x) {
     const Chain ch = make_chain(A.p, pl.K, w);
     const Lanes<E> ln = make_lanes<T, E>(pl, ch, warp, lane);
-    float* dxacc = A.p.dx_acc + ch.bc * HW;
     BwdState<E> S;
 #pragma unroll
     for (int e = 0; e < E; ++e) S.ea[e] = S.eb[e] = S.ec[e] = 0.f;
@@ -838,17 +770,12 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_stream_kernel(const
       const int j = ch.ntiles - 1 - jj;
       mbar_wait(smem_u32(&m.full[stage]), phase);
       uint8_t* st = m.ring + static_cast<size_t>(stage) * pl.stage_bytes;
-      const int c0 = tile_start(ch, j, C::K);  // horizontal: canonical column of the tile's first step
 #pragma unroll 1
       for (int half = 1; half >= 0; --half) {
-        uint4 OL[E], OG[E];
-        float DX[E][C::KS];
+        uint4 OG[E];
         if (!pl.null_compute) {
-          if (ch.vert) {
-            bwd_half_vert<T, E>(A, ln, ch, j, half, st, lane, S, prenorm, pol_acc, pol_vout);
-          } else {
-            bwd_half_horiz<T, E>(ln, ch, j, half, st, pl.tile_bytes, lane, S, prenorm, OL, OG, DX);
-          }
+          if (ch.vert) bwd_half_vert<T, E>(A, ln, ch, j, half, st, lane, S, prenorm, pol_vout);
+          else bwd_half_horiz<T, E>(ln, ch, j, half, st, pl.tile_bytes, lane, S, prenorm, OG);
         }
         edge_publish<T, E>(m.edge + 0 * kEdgeArr, par, warp, lane, ch.vert, S.ea);
         edge_publish<T, E>(m.edge + 1 * kEdgeArr, par, warp, lane, ch.vert, S.eb);
@@ -860,22 +787,9 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_stream_kernel(const
         par ^= 1;
         if (!ch.vert && !pl.null_compute) {
           const int cm = ch.rev ? 1 - half : half;
-          const int col = c0 + cm * C::KS;  // canonical column of the chunk's first element
 #pragma unroll
-          for (int q = 0; q < E; ++q) {
-            if (!ln.own[q]) continue;
-            const uint32_t off = hchunk(ln.row[q], cm);
-            *reinterpret_cast<uint4*>(st + B_X * pl.tile_bytes + off) = OL[q];
-            *reinterpret_cast<uint4*>(st + B_DH * pl.tile_bytes + off) = OG[q];
-            if (ln.valid[q] && col >= 0 && col < ch.L) {  // W % KS == 0: chunks are all in or all out
-              const int64_t o = static_cast<int64_t>(ln.pos[q]) * A.p.W + col;
-#pragma unroll
-              for (int v = 0; v < C::KS; v += 4) {
-                const float d[4] = {DX[q][v], DX[q][v + 1], DX[q][v + 2], DX[q][v + 3]};
-                red_add_vec<4>(dxacc + o + v, d, pol_acc);
-              }
-            }
-          }
+          for (int q = 0; q < E; ++q)
+            if (ln.own[q]) *reinterpret_cast<uint4*>(st + B_DH * pl.tile_bytes + hchunk(ln.row[q], cm)) = OG[q];
         }
       }
       fence_proxy_async();  // in-place outputs -> visible to the storer's TMA (async proxy)
@@ -883,98 +797,402 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_stream_kernel(const
       if (lane == 0) mbar_arrive(smem_u32(&m.done[stage]));
       if (++stage == pl.nstages) { stage = 0; phase ^= 1; }
     }
-    bwd_chain_epilogue<T>(A, ch, m.flag, nthreads);
   }
 }
 
-// ------------------------------------------------------------------------------ tap gradients
+// ------------------------------------------------------------------------------ backward outputs
 
-// dw from g and the saved h, one thread per (direction, b, group, row, 4 columns): for every channel
-// of the group, Da += g h_{t-1}[r-1], Db += g h_{t-1}[r], Dc += g h_{t-1}[r+1] (h_{-1} = 0; the
-// neighbours along the scan-orthogonal axis; out-of-range taps dropped), then the normalisation
-// Jacobian (gspn_common.cuh: jacobian). Coalesced along columns; the 3 h values per element come from
-// a 6-wide window of one row (vertical scans) or three rows (horizontal scans).
+// Backward outputs from the adjoint state g and the saved h, one thread per
+// (b, group, R rows, V columns), all D directions: dlam_k = g_k x, dx = sum_k g_k lam_k, and for the
+// taps Da = g h_{t-1}[r-1], Db = g h_{t-1}[r], Dc = g h_{t-1}[r+1] (h_{-1} = 0, the neighbours along
+// the scan-orthogonal axis) summed over the group's channels, then the normalisation Jacobian
+// (gspn_common.cuh: jacobian). Coalesced along columns; the 3 h values per element come from a
+// (V+2)-wide window of one row (vertical scans) or from three rows (horizontal scans; the next row's
+// thread-iteration re-reads two of them from L1).
+// V consecutive elements <-> floats through one 8- or 16-byte global access (read-only path for loads).
+template <typename T, int V> struct GVec;
+template <> struct GVec<__nv_bfloat16, 8> {
+  static __device__ __forceinline__ void load(const __nv_bfloat16* p, float (&v)[8]) {
+    const uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) { v[2 * q] = __uint_as_float(w[q] << 16); v[2 * q + 1] = __uint_as_float(w[q] & 0xFFFF0000u); }
+  }
+  static __device__ __forceinline__ void store(__nv_bfloat16* p, const float (&v)[8]) {
+    *reinterpret_cast<uint4*>(p) = make_uint4(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]),
+                                              pack_bf16x2(v[4], v[5]), pack_bf16x2(v[6], v[7]));
+  }
+};
+template <> struct GVec<__nv_bfloat16, 4> {
+  static __device__ __forceinline__ void load(const __nv_bfloat16* p, float (&v)[4]) {
+    const uint2 u = __ldg(reinterpret_cast<const uint2*>(p));
+    v[0] = __uint_as_float(u.x << 16); v[1] = __uint_as_float(u.x & 0xFFFF0000u);
+    v[2] = __uint_as_float(u.y << 16); v[3] = __uint_as_float(u.y & 0xFFFF0000u);
+  }
+  static __device__ __forceinline__ void store(__nv_bfloat16* p, const float (&v)[4]) {
+    *reinterpret_cast<uint2*>(p) = make_uint2(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]));
+  }
+};
+template <> struct GVec<float, 4> {
+  static __device__ __forceinline__ void load(const float* p, float (&v)[4]) {
+    const float4 u = __ldg(reinterpret_cast<const float4*>(p));
+    v[0] = u.x; v[1] = u.y; v[2] = u.z; v[3] = u.w;
+  }
+  static __device__ __forceinline__ void store(float* p, const float (&v)[4]) {
+    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  }
+};
+
 template <typename T>
-__global__ void __launch_bounds__(256) dw_kernel(ScanParams p, const T* __restrict__ g) {
-  const int64_t W = p.W, H = p.H, HW = H * W, W4 = W / 4;
-  const int64_t n = p.D * p.B * p.G * H * W4;
+__device__ __forceinline__ float ldg_f(const T* p) { return to_f(__ldg(p)); }
+
+// g * h_{t-1}[r-1], [r], [r+1] for V columns of row i of one chain, added to Da, Db, Dc.
+template <typename T, int V>
+__device__ __forceinline__ void accum_taps(uint32_t dir, const T* hp, int64_t H, int64_t W, int64_t i, int64_t j0,
+                                           const float (&gv)[V], float (&Da)[V], float (&Db)[V], float (&Dc)[V]) {
+  if (dir == GSPN_DIR_T2B || dir == GSPN_DIR_B2T) {
+    // step t <-> row i; h_{t-1} is row i-1 (T2B) or i+1 (B2T); neighbours r+-1 = columns j+-1
+    const int64_t ip = dir == GSPN_DIR_T2B ? i - 1 : i + 1;
+    if (ip < 0 || ip >= H) return;
+    const T* row = hp + ip * W;
+    float v[V];
+    GVec<T, V>::load(row + j0, v);
+    const float lo = j0 > 0 ? ldg_f(row + j0 - 1) : 0.f;
+    const float hi = j0 + V < W ? ldg_f(row + j0 + V) : 0.f;
+#pragma unroll
+    for (int q = 0; q < V; ++q) {
+      Da[q] = fmaf(gv[q], q > 0 ? v[q - 1] : lo, Da[q]);
+      Db[q] = fmaf(gv[q], v[q], Db[q]);
+      Dc[q] = fmaf(gv[q], q + 1 < V ? v[q + 1] : hi, Dc[q]);
+    }
+  } else {
+    // step t <-> column j; h_{t-1} is column j-1 (L2R) or j+1 (R2L); neighbours r+-1 = rows i+-1
+    const bool l2r = dir == GSPN_DIR_L2R;
+#pragma unroll
+    for (int rr = 0; rr < 3; ++rr) {
+      const int64_t ii = i - 1 + rr;
+      if (ii < 0 || ii >= H) continue;
+      const T* row = hp + ii * W;
+      float v[V], sh[V];  // sh: h_{t-1} of row ii for the V columns
+      GVec<T, V>::load(row + j0, v);
+      if (l2r) {
+        sh[0] = j0 > 0 ? ldg_f(row + j0 - 1) : 0.f;
+#pragma unroll
+        for (int q = 1; q < V; ++q) sh[q] = v[q - 1];
+      } else {
+#pragma unroll
+        for (int q = 0; q + 1 < V; ++q) sh[q] = v[q + 1];
+        sh[V - 1] = j0 + V < W ? ldg_f(row + j0 + V) : 0.f;
+      }
+#pragma unroll
+      for (int q = 0; q < V; ++q) {
+        if (rr == 0) Da[q] = fmaf(gv[q], sh[q], Da[q]);
+        else if (rr == 1) Db[q] = fmaf(gv[q], sh[q], Db[q]);
+        else Dc[q] = fmaf(gv[q], sh[q], Dc[q]);
+      }
+    }
+  }
+}
+
+// dw_k for V columns of row i from the summed Da, Db, Dc.
+template <typename T, int V>
+__device__ __forceinline__ void finish_taps(const ScanParams& p, uint32_t dir, int64_t woff, int64_t i, int64_t j0,
+                                            bool prenorm, const float (&Da)[V], const float (&Db)[V],
+                                            const float (&Dc)[V]) {
+  const bool vert = dir == GSPN_DIR_T2B || dir == GSPN_DIR_B2T;
+  const int64_t P = vert ? p.W : p.H;
+  float wl[V], wm[V], wr[V], ol[V], om[V], orr[V];
+  GVec<T, V>::load(static_cast<const T*>(p.wl) + woff, wl);
+  GVec<T, V>::load(static_cast<const T*>(p.wm) + woff, wm);
+  GVec<T, V>::load(static_cast<const T*>(p.wr) + woff, wr);
+#pragma unroll
+  for (int q = 0; q < V; ++q) {
+    const int64_t r = vert ? j0 + q : i;
+    const bool hl = r >= 1, hr = r <= P - 2;
+    jacobian<true>(wl[q], wm[q], wr[q], hl, hr, prenorm, hl ? Da[q] : 0.f, Db[q], hr ? Dc[q] : 0.f, ol[q], om[q], orr[q]);
+  }
+  GVec<T, V>::store(static_cast<T*>(p.dwl) + woff, ol);
+  GVec<T, V>::store(static_cast<T*>(p.dwm) + woff, om);
+  GVec<T, V>::store(static_cast<T*>(p.dwr) + woff, orr);
+}
+
+template <typename T, int V, int R, bool kPerChannel>
+__global__ void __launch_bounds__(256) bwd_out_kernel(ScanParams p, const T* __restrict__ g) {
+  const int64_t W = p.W, H = p.H, HW = H * W;
+  const int64_t nchunk = W / V, nrb = (H + R - 1) / R;
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= p.B * p.G * nrb * nchunk) return;
+  const int64_t j0 = (idx % nchunk) * V;
+  const int64_t i0 = ((idx / nchunk) % nrb) * R;
+  const int64_t bg = idx / (nchunk * nrb);
+  const int64_t b = bg / p.G, grp = bg % p.G;
   const int64_t Cg = p.C / p.G;
   const bool prenorm = p.flags & GSPN_FLAG_PRENORMALIZED;
   const T* hbase = static_cast<const T*>(p.h);
-  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
-       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t j0 = (e % W4) * 4;
-    const int64_t i = (e / W4) % H;
-    const int64_t wplane = e / (W4 * H);  // (k * B + b) * G + grp
-    const int k = static_cast<int>(wplane / (p.B * p.G));
-    const int64_t bg = wplane % (p.B * p.G);
-    const int64_t b = bg / p.G, grp = bg % p.G;
-    const uint32_t dir = p.dirbit[k];
-    const bool vert = dir == GSPN_DIR_T2B || dir == GSPN_DIR_B2T;
-    float Da[4] = {0.f, 0.f, 0.f, 0.f}, Db[4] = {0.f, 0.f, 0.f, 0.f}, Dc[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int64_t cc = 0; cc < Cg; ++cc) {
-      const int64_t chain = (static_cast<int64_t>(k) * p.B + b) * p.C + grp * Cg + cc;
-      const T* gp = g + chain * HW + i * W + j0;
-      const T* hp = hbase + chain * HW;
-      float gv[4];
+  const T* xb = static_cast<const T*>(p.x);
+  const T* lamb = static_cast<const T*>(p.lam);
+  T* dlamb = static_cast<T*>(p.dlam);
+  T* dxb = static_cast<T*>(p.dx);
+  const int64_t iend = i0 + R < H ? i0 + R : H;
+  for (int64_t i = i0; i < iend; ++i) {
+    const int64_t rowoff = i * W + j0;
+    if constexpr (kPerChannel) {
+      const int64_t xoff = (b * p.C + grp) * HW + rowoff;
+      float xv[V], dx[V];
+      GVec<T, V>::load(xb + xoff, xv);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) gv[q] = to_f(gp[q]);
-      if (vert) {
-        // step t <-> row i; h_{t-1} is row i-1 (T2B) or i+1 (B2T); neighbours r+-1 = columns j+-1
-        const int64_t ip = dir == GSPN_DIR_T2B ? i - 1 : i + 1;
-        float win[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // h_{t-1}[j0-1 .. j0+4]
-        if (ip >= 0 && ip < H) {
-          const T* row = hp + ip * W;
+      for (int q = 0; q < V; ++q) dx[q] = 0.f;
+      for (int k = 0; k < p.D; ++k) {
+        const uint32_t dir = p.dirbit[k];
+        const int64_t chain = (static_cast<int64_t>(k) * p.B + b) * p.C + grp;  // == weight plane (G = C)
+        const int64_t off = chain * HW + rowoff;
+        float gv[V], lv[V], dl[V], Da[V], Db[V], Dc[V];
+        GVec<T, V>::load(g + off, gv);
+        GVec<T, V>::load(lamb + off, lv);
 #pragma unroll
-          for (int q = 0; q < 6; ++q) {
-            const int64_t jj = j0 - 1 + q;
-            win[q] = (jj >= 0 && jj < W) ? to_f(row[jj]) : 0.f;
+        for (int q = 0; q < V; ++q) {
+          dl[q] = gv[q] * xv[q];
+          dx[q] = fmaf(gv[q], lv[q], dx[q]);
+          Da[q] = Db[q] = Dc[q] = 0.f;
+        }
+        GVec<T, V>::store(dlamb + off, dl);
+        accum_taps<T, V>(dir, hbase + chain * HW, H, W, i, j0, gv, Da, Db, Dc);
+        finish_taps<T, V>(p, dir, off, i, j0, prenorm, Da, Db, Dc);
+      }
+      GVec<T, V>::store(dxb + xoff, dx);
+    } else {
+      float Da[4][V], Db[4][V], Dc[4][V];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int q = 0; q < V; ++q) Da[k][q] = Db[k][q] = Dc[k][q] = 0.f;
+      for (int64_t cc = 0; cc < Cg; ++cc) {
+        const int64_t c = grp * Cg + cc;
+        const int64_t xoff = (b * p.C + c) * HW + rowoff;
+        float xv[V], dx[V];
+        GVec<T, V>::load(xb + xoff, xv);
+#pragma unroll
+        for (int q = 0; q < V; ++q) dx[q] = 0.f;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (k >= p.D) break;
+          const int64_t chain = (static_cast<int64_t>(k) * p.B + b) * p.C + c;
+          const int64_t off = chain * HW + rowoff;
+          float gv[V], lv[V], dl[V];
+          GVec<T, V>::load(g + off, gv);
+          GVec<T, V>::load(lamb + off, lv);
+#pragma unroll
+          for (int q = 0; q < V; ++q) {
+            dl[q] = gv[q] * xv[q];
+            dx[q] = fmaf(gv[q], lv[q], dx[q]);
           }
+          GVec<T, V>::store(dlamb + off, dl);
+          accum_taps<T, V>(p.dirbit[k], hbase + chain * HW, H, W, i, j0, gv, Da[k], Db[k], Dc[k]);
         }
+        GVec<T, V>::store(dxb + xoff, dx);
+      }
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          Da[q] = fmaf(gv[q], win[q], Da[q]);
-          Db[q] = fmaf(gv[q], win[q + 1], Db[q]);
-          Dc[q] = fmaf(gv[q], win[q + 2], Dc[q]);
-        }
+      for (int k = 0; k < 4; ++k) {
+        if (k >= p.D) break;
+        const int64_t woff = ((static_cast<int64_t>(k) * p.B + b) * p.G + grp) * HW + rowoff;
+        finish_taps<T, V>(p, p.dirbit[k], woff, i, j0, prenorm, Da[k], Db[k], Dc[k]);
+      }
+    }
+  }
+}
+
+// V elements of T held packed in 32-bit words (loads issued early, unpacked at use).
+template <typename T, int V>
+struct PackedV {
+  static constexpr int kWords = V * static_cast<int>(sizeof(T)) / 4;
+  static_assert(kWords == 2 || kWords == 4, "8- or 16-byte vectors");
+  uint32_t w[kWords];
+  __device__ __forceinline__ void load(const T* p) {
+    if constexpr (kWords == 4) {
+      const uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
+      w[0] = u.x; w[1] = u.y; w[2] = u.z; w[3] = u.w;
+    } else {
+      const uint2 u = __ldg(reinterpret_cast<const uint2*>(p));
+      w[0] = u.x; w[1] = u.y;
+    }
+  }
+  __device__ __forceinline__ void unpack(float (&v)[V]) const {
+#pragma unroll
+    for (int i = 0; i < kWords; ++i) {
+      if constexpr (sizeof(T) == 2) {
+        v[2 * i] = __uint_as_float(w[i] << 16);
+        v[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
       } else {
-        // step t <-> column j; h_{t-1} is column j-1 (L2R) or j+1 (R2L); neighbours r+-1 = rows i+-1
-        const int64_t dj = dir == GSPN_DIR_L2R ? -1 : 1;
+        v[i] = __uint_as_float(w[i]);
+      }
+    }
+  }
+};
+
+template <> struct GVec<float, 2> {
+  static __device__ __forceinline__ void store(float* p, const float (&v)[2]) {
+    *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
+  }
+};
+
+// Per-channel weights (G = C): one thread = (b, c, R rows, V columns), all D directions. Each row
+// issues every load it needs (x; g, lam, w_l/m/r and the h_{t-1} window of every direction) before
+// any arithmetic, so a thread has a whole row's worth of bytes in flight (the loop-carried version
+// waited on ~4 dependent round trips per direction).
+template <typename T, int V, int R, int kGrp>
+__global__ void __launch_bounds__(256) bwd_out_pc_kernel(ScanParams p, const T* __restrict__ g) {
+  const int64_t W = p.W, H = p.H, HW = H * W;
+  const int64_t nchunk = W / V, nrb = (H + R - 1) / R;
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= p.B * p.C * nrb * nchunk) return;
+  const int64_t j0 = (idx % nchunk) * V;
+  const int64_t i0 = ((idx / nchunk) % nrb) * R;
+  const int64_t bc = idx / (nchunk * nrb);
+  const int64_t b = bc / p.C, c = bc % p.C;
+  const int D = p.D;
+  const bool prenorm = p.flags & GSPN_FLAG_PRENORMALIZED;
+  const T* hb = static_cast<const T*>(p.h);
+  const T* lamb = static_cast<const T*>(p.lam);
+  const T* wlb = static_cast<const T*>(p.wl);
+  const T* wmb = static_cast<const T*>(p.wm);
+  const T* wrb = static_cast<const T*>(p.wr);
+  const int64_t iend = i0 + R < H ? i0 + R : H;
+#pragma unroll 1
+  for (int64_t i = i0; i < iend; ++i) {
+    const int64_t rowoff = i * W + j0;
+    PackedV<T, V> X;
+    X.load(static_cast<const T*>(p.x) + bc * HW + rowoff);
+    float xv[V], dx[V];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int64_t jp = j0 + q + dj;
-          float hm = 0.f, h0 = 0.f, hq = 0.f;
-          if (jp >= 0 && jp < W) {
-            if (i >= 1) hm = to_f(hp[(i - 1) * W + jp]);
-            h0 = to_f(hp[i * W + jp]);
-            if (i + 1 < H) hq = to_f(hp[(i + 1) * W + jp]);
-          }
-          Da[q] = fmaf(gv[q], hm, Da[q]);
-          Db[q] = fmaf(gv[q], h0, Db[q]);
-          Dc[q] = fmaf(gv[q], hq, Dc[q]);
+    for (int q = 0; q < V; ++q) dx[q] = 0.f;
+#pragma unroll 1
+    for (int k0 = 0; k0 < D; k0 += kGrp) {
+    // ---- loads (kGrp directions)
+    PackedV<T, V> Gk[kGrp], Lk[kGrp], WLk[kGrp], WMk[kGrp], WRk[kGrp], Hk[kGrp][3];
+    float hs[kGrp][3];
+#pragma unroll
+    for (int kk = 0; kk < kGrp; ++kk) {
+      const int k = k0 + kk;
+      if (k >= D) break;
+      const int64_t chain = (static_cast<int64_t>(k) * p.B + b) * p.C + c;  // == weight plane (G = C)
+      const int64_t off = chain * HW + rowoff;
+      Gk[kk].load(g + off);
+      Lk[kk].load(lamb + off);
+      WLk[kk].load(wlb + off);
+      WMk[kk].load(wmb + off);
+      WRk[kk].load(wrb + off);
+      const uint32_t dir = p.dirbit[k];
+      const T* hp = hb + chain * HW;
+      if (dir == GSPN_DIR_T2B || dir == GSPN_DIR_B2T) {
+        // h_{t-1} = row i-1 (T2B) / i+1 (B2T); neighbours r+-1 = columns j+-1
+        int64_t ip = dir == GSPN_DIR_T2B ? i - 1 : i + 1;
+        ip = ip < 0 ? 0 : (ip >= H ? H - 1 : ip);
+        const T* row = hp + ip * W;
+        Hk[kk][0].load(row + j0);
+        hs[kk][0] = j0 > 0 ? ldg_f(row + j0 - 1) : 0.f;
+        hs[kk][1] = j0 + V < W ? ldg_f(row + j0 + V) : 0.f;
+      } else {
+        // h_{t-1} = column j-1 (L2R) / j+1 (R2L); neighbours r+-1 = rows i+-1
+        const int64_t col = dir == GSPN_DIR_L2R ? j0 - 1 : j0 + V;
+#pragma unroll
+        for (int rr = 0; rr < 3; ++rr) {
+          int64_t ii = i - 1 + rr;
+          ii = ii < 0 ? 0 : (ii >= H ? H - 1 : ii);
+          const T* row = hp + ii * W;
+          Hk[kk][rr].load(row + j0);
+          hs[kk][rr] = (col >= 0 && col < W) ? ldg_f(row + col) : 0.f;
         }
       }
     }
-    const int64_t woff = wplane * HW + i * W + j0;
-    const T* wl = static_cast<const T*>(p.wl) + woff;
-    const T* wm = static_cast<const T*>(p.wm) + woff;
-    const T* wr = static_cast<const T*>(p.wr) + woff;
-    T* dwl = static_cast<T*>(p.dwl) + woff;
-    T* dwm = static_cast<T*>(p.dwm) + woff;
-    T* dwr = static_cast<T*>(p.dwr) + woff;
-    const int64_t P = vert ? W : H;
+    // ---- arithmetic + stores
+    X.unpack(xv);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int64_t r = vert ? j0 + q : i;
-      const bool hl = r >= 1, hr = r <= P - 2;
-      float ol, om, orr;
-      jacobian(to_f(wl[q]), to_f(wm[q]), to_f(wr[q]), hl, hr, prenorm, hl ? Da[q] : 0.f, Db[q], hr ? Dc[q] : 0.f, ol,
-               om, orr);
-      dwl[q] = from_f<T>(ol);
-      dwm[q] = from_f<T>(om);
-      dwr[q] = from_f<T>(orr);
+    for (int kk = 0; kk < kGrp; ++kk) {
+      const int k = k0 + kk;
+      if (k >= D) break;
+      const int64_t chain = (static_cast<int64_t>(k) * p.B + b) * p.C + c;
+      const int64_t off = chain * HW + rowoff;
+      const uint32_t dir = p.dirbit[k];
+      const bool vert = dir == GSPN_DIR_T2B || dir == GSPN_DIR_B2T;
+      float gv[V], lv[V], dl[V], Da[V], Db[V], Dc[V];
+      Gk[kk].unpack(gv);
+      Lk[kk].unpack(lv);
+#pragma unroll
+      for (int q = 0; q < V; ++q) {
+        dl[q] = gv[q] * xv[q];
+        dx[q] = fmaf(gv[q], lv[q], dx[q]);
+      }
+      GVec<T, V>::store(static_cast<T*>(p.dlam) + off, dl);
+      if (vert) {
+        const int64_t ip = dir == GSPN_DIR_T2B ? i - 1 : i + 1;
+        const bool ok = ip >= 0 && ip < H;
+        float v[V];
+        Hk[kk][0].unpack(v);
+#pragma unroll
+        for (int q = 0; q < V; ++q) {
+          const float gq = ok ? gv[q] : 0.f;
+          Da[q] = gq * (q > 0 ? v[q - 1] : hs[kk][0]);
+          Db[q] = gq * v[q];
+          Dc[q] = gq * (q + 1 < V ? v[q + 1] : hs[kk][1]);
+        }
+      } else {
+        const bool l2r = dir == GSPN_DIR_L2R;
+        float* Dr[3] = {Da, Db, Dc};
+#pragma unroll
+        for (int rr = 0; rr < 3; ++rr) {
+          const int64_t ii = i - 1 + rr;
+          const bool ok = ii >= 0 && ii < H;
+          float v[V];
+          Hk[kk][rr].unpack(v);
+#pragma unroll
+          for (int q = 0; q < V; ++q) {
+            const float sh = l2r ? (q > 0 ? v[q - 1] : hs[kk][rr]) : (q + 1 < V ? v[q + 1] : hs[kk][rr]);
+            Dr[rr][q] = ok ? gv[q] * sh : 0.f;
+          }
+        }
+      }
+      float wl[V], wm[V], wr[V], ol[V], om[V], orr[V];
+      WLk[kk].unpack(wl);
+      WMk[kk].unpack(wm);
+      WRk[kk].unpack(wr);
+      const int64_t P = vert ? W : H;
+#pragma unroll
+      for (int q = 0; q < V; ++q) {
+        const int64_t r = vert ? j0 + q : i;
+        const bool hl = r >= 1, hr = r <= P - 2;
+        jacobian<true>(wl[q], wm[q], wr[q], hl, hr, prenorm, hl ? Da[q] : 0.f, Db[q], hr ? Dc[q] : 0.f, ol[q], om[q],
+                       orr[q]);
+      }
+      GVec<T, V>::store(static_cast<T*>(p.dwl) + off, ol);
+      GVec<T, V>::store(static_cast<T*>(p.dwm) + off, om);
+      GVec<T, V>::store(static_cast<T*>(p.dwr) + off, orr);
     }
+    }
+    GVec<T, V>::store(static_cast<T*>(p.dx) + bc * HW + rowoff, dx);
   }
+}
+
+template <typename T, int V>
+cudaError_t launch_out_pc(const ScanParams& p, const void* g, cudaStream_t s) {
+  constexpr int R = 4;
+  const int64_t n = p.B * p.C * ((p.H + R - 1) / R) * (p.W / V);
+  const unsigned blocks = static_cast<unsigned>((n + 255) / 256);
+  int grp = 2;  // directions whose loads are in flight together (experiments: GSPN_OUTK=1|2|4)
+  if (const char* e = getenv("GSPN_OUTK")) grp = atoi(e);
+  const T* gt = static_cast<const T*>(g);
+  if (grp == 1) bwd_out_pc_kernel<T, V, R, 1><<<blocks, 256, 0, s>>>(p, gt);
+  else if (grp == 4) bwd_out_pc_kernel<T, V, R, 4><<<blocks, 256, 0, s>>>(p, gt);
+  else bwd_out_pc_kernel<T, V, R, 2><<<blocks, 256, 0, s>>>(p, gt);
+  return cudaGetLastError();
+}
+
+template <typename T, int V, bool kPerChannel>
+cudaError_t launch_out(const ScanParams& p, const void* g, cudaStream_t s) {
+  constexpr int R = 8;
+  const int64_t n = p.B * p.G * ((p.H + R - 1) / R) * (p.W / V);
+  const int64_t blocks = (n + 255) / 256;
+  bwd_out_kernel<T, V, R, kPerChannel><<<static_cast<unsigned>(blocks), 256, 0, s>>>(p, static_cast<const T*>(g));
+  return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------------------------- host side
@@ -1122,20 +1340,15 @@ cudaError_t launch(KernelT kernel, const StreamArgs& A, cudaStream_t s) {
 constexpr size_t kAlign = 256;
 size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
 
+// Backward workspace: the adjoint state g [D, B, C, H, W] in the I/O dtype.
 struct WsLayout {
-  size_t dx, cnt, g, total, zero_bytes;
+  size_t g, total;
 };
 
 WsLayout ws_layout(int64_t B, int64_t C, int64_t H, int64_t W, int64_t D, gspn_dtype_t dt) {
   WsLayout l;
-  l.dx = 0;
-  size_t off = align_up(static_cast<size_t>(B * C * H * W) * sizeof(float));
-  l.cnt = off;
-  off += align_up(static_cast<size_t>(B * C) * sizeof(unsigned));
-  l.zero_bytes = off;  // dx accumulator + counters are zeroed by the call
-  l.g = off;
-  off += align_up(static_cast<size_t>(D * B * C * H * W) * (dt == GSPN_BF16 ? 2 : 4));
-  l.total = off;
+  l.g = 0;
+  l.total = align_up(static_cast<size_t>(D * B * C * H * W) * (dt == GSPN_BF16 ? 2 : 4));
   return l;
 }
 
@@ -1190,23 +1403,18 @@ cudaError_t launch_bwd_stream(const ScanParams& p0, gspn_dtype_t dt, cudaStream_
   memset(&A, 0, sizeof A);
   A.p = p0;
   ScanParams& p = A.p;
-  if (p.W % 4 != 0) return cudaSuccess;  // dw_kernel works on 4-column groups
-  const int E = pick_E(p, dt, B_NIN, &A.plan);
+  const int E = pick_E(p, dt, B_NIN, &A.plan);  // (W * sizeof(T)) % 16 == 0: V-column groups tile W
   if (E == 0) return cudaSuccess;
   const WsLayout l = ws_layout(p.B, p.C, p.H, p.W, p.D, dt);
   if (p.ws == nullptr || p.ws_bytes < l.total) return cudaSuccess;
-  char* ws = static_cast<char*>(p.ws);
-  p.dx_acc = reinterpret_cast<float*>(ws + l.dx);
-  p.counters = reinterpret_cast<unsigned*>(ws + l.cnt);
-  A.g = ws + l.g;
-  const void* ins[B_NIN] = {p.x, p.lam, p.dh, p.wl, p.wm, p.wr};
-  const int64_t nbc = p.B * p.C, nc = p.D * p.B * p.C, nw = p.D * p.B * p.G;
-  const int64_t in_planes[B_NIN] = {nbc, nc, nc, nw, nw, nw};
-  void* outs[2] = {p.dlam, A.g};
-  if (!fill_maps(&A, ins, B_NIN, outs, in_planes, nc, 2, dt)) return cudaSuccess;
+  A.g = static_cast<char*>(p.ws) + l.g;
+  const void* ins[B_NIN] = {p.dh, p.wl, p.wm, p.wr};
+  const int64_t nc = p.D * p.B * p.C, nw = p.D * p.B * p.G;
+  const int64_t in_planes[B_NIN] = {nc, nw, nw, nw};
+  void* outs[1] = {A.g};
+  if (!fill_maps(&A, ins, B_NIN, outs, in_planes, nc, 1, dt)) return cudaSuccess;
   *handled = true;
-  cudaError_t e = cudaMemsetAsync(p.ws, 0, l.zero_bytes, s);
-  if (e != cudaSuccess) return e;
+  cudaError_t e;
   using BF = __nv_bfloat16;
   if (E == 2)
     e = dt == GSPN_BF16 ? launch(bwd_stream_kernel<BF, 2, kE2Warps>, A, s) : launch(bwd_stream_kernel<float, 2, kE2Warps>, A, s);
@@ -1214,15 +1422,13 @@ cudaError_t launch_bwd_stream(const ScanParams& p0, gspn_dtype_t dt, cudaStream_
     e = dt == GSPN_BF16 ? launch(bwd_stream_kernel<BF, 4, kEdgeW>, A, s) : launch(bwd_stream_kernel<float, 4, kEdgeW>, A, s);
   *launches += 1;
   if (e != cudaSuccess) return e;
-  const int64_t n = p.D * p.B * p.G * p.H * (p.W / 4);
-  int64_t blocks = (n + 255) / 256;
-  if (blocks > static_cast<int64_t>(sm_count()) * 16) blocks = static_cast<int64_t>(sm_count()) * 16;
+  const bool per_channel = p.G == p.C;
   if (dt == GSPN_BF16)
-    dw_kernel<BF><<<static_cast<unsigned>(blocks), 256, 0, s>>>(p, static_cast<const BF*>(A.g));
+    e = per_channel ? launch_out_pc<BF, 4>(p, A.g, s) : launch_out<BF, 4, false>(p, A.g, s);
   else
-    dw_kernel<float><<<static_cast<unsigned>(blocks), 256, 0, s>>>(p, static_cast<const float*>(A.g));
+    e = per_channel ? launch_out_pc<float, 2>(p, A.g, s) : launch_out<float, 4, false>(p, A.g, s);
   *launches += 1;
-  return cudaGetLastError();
+  return e;
 }
 
 }  // namespace gspn

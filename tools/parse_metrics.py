@@ -13,7 +13,7 @@ def parse(path):
         if len(r) < 15 or not r[0].isdigit():
             continue
         name = r[4]
-        k = "fwd" if "fwd_stream" in name else ("bwd" if "bwd_stream" in name else name[:30])
+        k = "fwd" if "fwd_stream" in name else ("bwd" if "bwd_stream" in name else ("out" if "out_" in name else name[:30]))
         d.setdefault((int(r[0]), k), {})[r[12]] = (r[13], r[14])
     out = []
     for (i, k), m in sorted(d.items()):
