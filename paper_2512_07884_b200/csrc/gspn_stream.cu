@@ -54,7 +54,13 @@ using namespace ptx;
 
 constexpr int kMaxIn = 6;
 constexpr int kMaxOut = 2;
-constexpr int kEdgeW = 16;     // max consumer warps (edge-buffer slots)
+constexpr int kEdgeW = 16;     // edge-buffer slots (>= consumer warps + 1)
+// Fixed tile geometry (chains with P <= kPpad): one tensor's tile holds K steps x kPpad positions =
+// 32 kPpad bytes; vertical tiles are [box][K][kRowB bytes] (box = kRowB / s positions), horizontal
+// tiles [row][32 bytes]. Compile-time strides let every shared-memory read use an immediate offset.
+constexpr int kPpad = 512;
+constexpr uint32_t kTile = 32u * kPpad;
+constexpr int kRowB = 512;
 constexpr int kBarEdge = 1;    // named barrier ids (0 is __syncthreads)
 
 template <typename T>
@@ -97,35 +103,6 @@ struct alignas(64) StreamArgs {
 
 // ------------------------------------------------------------------------------ element access
 
-// E consecutive elements of T in shared memory -> floats.
-template <typename T, int E> struct VE;
-template <> struct VE<__nv_bfloat16, 2> {
-  static __device__ __forceinline__ void load(const uint8_t* p, float (&v)[2]) {
-    const uint32_t u = *reinterpret_cast<const uint32_t*>(p);
-    v[0] = __uint_as_float(u << 16);
-    v[1] = __uint_as_float(u & 0xFFFF0000u);
-  }
-};
-template <> struct VE<__nv_bfloat16, 4> {
-  static __device__ __forceinline__ void load(const uint8_t* p, float (&v)[4]) {
-    const uint2 u = *reinterpret_cast<const uint2*>(p);
-    v[0] = __uint_as_float(u.x << 16); v[1] = __uint_as_float(u.x & 0xFFFF0000u);
-    v[2] = __uint_as_float(u.y << 16); v[3] = __uint_as_float(u.y & 0xFFFF0000u);
-  }
-};
-template <> struct VE<float, 2> {
-  static __device__ __forceinline__ void load(const uint8_t* p, float (&v)[2]) {
-    const float2 u = *reinterpret_cast<const float2*>(p);
-    v[0] = u.x; v[1] = u.y;
-  }
-};
-template <> struct VE<float, 4> {
-  static __device__ __forceinline__ void load(const uint8_t* p, float (&v)[4]) {
-    const float4 u = *reinterpret_cast<const float4*>(p);
-    v[0] = u.x; v[1] = u.y; v[2] = u.z; v[3] = u.w;
-  }
-};
-
 __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
   __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&v);
@@ -138,27 +115,11 @@ template <> struct GStore<__nv_bfloat16, 2> {
     st_global_b32(p, pack_bf16x2(v[0], v[1]), pol);
   }
 };
-template <> struct GStore<__nv_bfloat16, 4> {
-  static __device__ __forceinline__ void st(__nv_bfloat16* p, const float (&v)[4], uint64_t pol) {
-    st_global_v2(p, pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]), pol);
-  }
-};
 template <> struct GStore<float, 2> {
   static __device__ __forceinline__ void st(float* p, const float (&v)[2], uint64_t pol) {
     st_global_v2(p, __float_as_uint(v[0]), __float_as_uint(v[1]), pol);
   }
 };
-template <> struct GStore<float, 4> {
-  static __device__ __forceinline__ void st(float* p, const float (&v)[4], uint64_t pol) {
-    st_global_v4(p, __float_as_uint(v[0]), __float_as_uint(v[1]), __float_as_uint(v[2]), __float_as_uint(v[3]), pol);
-  }
-};
-
-template <int E>
-__device__ __forceinline__ void red_add_vec(float* p, const float (&v)[E], uint64_t pol) {
-  if constexpr (E == 4) red_add_v4(p, v[0], v[1], v[2], v[3], pol);
-  else red_add_v2(p, v[0], v[1], pol);
-}
 
 // One 16-byte chunk = KS steps of one row (horizontal tiles). Element indices are compile-time
 // constants after unrolling, so the selects fold away.
@@ -181,24 +142,6 @@ template <> struct Pk<float> {
     return make_uint4(__float_as_uint(v[0]), __float_as_uint(v[1]), __float_as_uint(v[2]), __float_as_uint(v[3]));
   }
 };
-
-// Element-order reversal of a chunk (runtime flag), so horizontal chains of both directions see
-// their steps in scan order.
-__device__ __forceinline__ uint32_t swap16(uint32_t v) { return __byte_perm(v, 0, 0x1032); }
-template <typename T> struct Rev;
-template <> struct Rev<__nv_bfloat16> {
-  static __device__ __forceinline__ uint4 r(const uint4& u, bool rev) {
-    return rev ? make_uint4(swap16(u.w), swap16(u.z), swap16(u.y), swap16(u.x)) : u;
-  }
-};
-template <> struct Rev<float> {
-  static __device__ __forceinline__ uint4 r(const uint4& u, bool rev) { return rev ? make_uint4(u.w, u.z, u.y, u.x) : u; }
-};
-
-// Byte offset of 16-byte chunk c of row r in a 32-byte-swizzled horizontal tile.
-__device__ __forceinline__ uint32_t hchunk(uint32_t r, int c) {
-  return r * 32 + ((static_cast<uint32_t>(c) ^ ((r >> 2) & 1)) << 4);
-}
 
 // ------------------------------------------------------------------------------ chain bookkeeping
 
@@ -237,12 +180,6 @@ __device__ __forceinline__ Chain make_chain(const ScanParams& p, int K, int64_t 
 __device__ __forceinline__ int tile_start(const Chain& ch, int j, int K) {
   if (!ch.rev) return j * K;
   return ch.vert ? (ch.L - (j + 1) * K) : (ch.ntiles - 1 - j) * K;
-}
-
-// Scan step of the tile's first (scan-order) step: step t = tile_step0 + s for in-tile offset s.
-// Negative for the partial first tile of an R2L chain (those leading steps do not exist).
-__device__ __forceinline__ int tile_step0(const Chain& ch, int j, int K) {
-  return (ch.rev && !ch.vert) ? (ch.L - tile_start(ch, j, K) - K) : j * K;
 }
 
 // Input tensor slots.
@@ -328,131 +265,182 @@ __device__ void storer_loop(const StreamArgs& A, uint8_t* ring, uint64_t* done, 
 
 // ------------------------------------------------------------------------------ per-lane geometry
 
-// The E positions a lane computes, their masks, and where they live in a shared-memory tile.
-// Warp w covers positions [A, A + 32 E), A = w * OWN - GH; it owns [A + GH, A + 32 E - GH).
-//   vertical:   lane owns positions A + E lane + e            (e = 0..E-1)
-//   horizontal: lane owns positions A + 32 e + lane           (e = slot 0..E-1)
-template <int E>
+// A warp covers 32 E = 64 consecutive positions starting at A = w * OWN - GH (OWN = 64 - 2 GH) and
+// owns offsets [GH, 64 - GH); warp 0's left ghosts are the invalid positions -GH..-1. Vertical: lane
+// holds positions A + 2 lane + e; horizontal: A + 32 q + lane (slot q), conflict-free on the tiles.
+//
+// Boundary handling without per-step masks: each lane gets byte-permute selectors (bf16) or
+// and/or masks (fp32) that unpack its tap values already masked -- w_l -> 0 at r = 0, w_r -> 0 at
+// r = P-1 (out-of-range taps, also dropped from S), and for positions outside [0, P) (TMA zero fill
+// or clamped rows) w_l, w_r -> 0 and w_m -> 1, so those positions never couple into [0, P) -- in the
+// forward through the masked taps of 0 and P-1, in the adjoint because their a g and c g are 0 --
+// and stay finite. Steps outside [0, L) (partial first/last tiles) read TMA zero fill; the reciprocal is
+// clamped so that S = 0 gives a zero update instead of 0 * inf.
+constexpr int kE = 2;
+constexpr int kMaxNWC = 11;                // consumer warps: 11 * 48 >= kPpad (bf16)
+constexpr float kRcpMax = 1e30f;
+
+__device__ __forceinline__ float bsel(uint32_t w, uint32_t sel) {
+  return __uint_as_float(__byte_perm(w, 0x00003F80u, sel));  // bytes 4..7 = {0x80, 0x3F, 0, 0}
+}
+constexpr uint32_t kSelLo = 0x1066u, kSelHi = 0x3266u, kSelZero = 0x6666u, kSelOne = 0x5466u;
+
+template <typename T>
 struct Lanes {
   int A;
-  int pos[E];
-  bool valid[E], hl[E], hr[E], own[E];
-  uint32_t voff;      // vertical: byte offset of the lane's E positions at kk = 0
-  uint32_t vstep;     // vertical: bytes between consecutive kk
-  uint32_t row[E];    // horizontal: clamped row index of each slot
+  bool own_v;            // vertical: both positions owned and < P
+  bool own_h[kE];        // horizontal: slot owned and inside the tile
+  uint32_t voff;         // vertical: byte offset of the lane's positions at kk = 0
+  uint32_t hoff[kE];     // horizontal: slot row's byte offset, chunk 0 (chunk c: hoff ^ (c << 4))
+  int pos0;              // vertical: first position
+  // tap unpack masks [tap l/m/r][element e | slot q][half / (and, or)]
+  uint32_t s[3][kE][2];
 };
 
-template <typename T, int E>
-__device__ __forceinline__ Lanes<E> make_lanes(const Plan& pl, const Chain& ch, int wi, int lane) {
-  using C = Cfg<T>;
-  constexpr int WARP = 32 * E, OWN = WARP - 2 * C::GH;
-  Lanes<E> ln;
-  ln.A = wi * OWN - C::GH;
-#pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int off = ch.vert ? (E * lane + e) : (32 * e + lane);
-    const int r = ln.A + off;
-    ln.pos[e] = r;
-    ln.valid[e] = (r >= 0) && (r < ch.P);
-    ln.hl[e] = r >= 1;
-    ln.hr[e] = r <= ch.P - 2;
-    // owned, and inside the tile (positions >= ppad are padding >= P: nothing to store)
-    ln.own[e] = (off >= C::GH) && (off < WARP - C::GH) && (r < pl.ppad);
-    const int rc = r < 0 ? 0 : (r >= pl.ppad ? pl.ppad - 1 : r);
-    ln.row[e] = static_cast<uint32_t>(rc);
+template <typename T>
+__device__ __forceinline__ void tap_masks(int r, int P, uint32_t (&sl)[2], uint32_t (&sm)[2], uint32_t (&sr)[2],
+                                          int half_for_bf16) {
+  const bool valid = r >= 0 && r < P, kl = valid && r >= 1, kr = valid && r <= P - 2;
+  if constexpr (sizeof(T) == 2) {
+    // half_for_bf16: -1 -> fill both halves (horizontal slot), 0/1 -> element in the low/high half
+    for (int hh = 0; hh < 2; ++hh) {
+      const int hf = half_for_bf16 < 0 ? hh : half_for_bf16;
+      const uint32_t keep = hf ? kSelHi : kSelLo;
+      sl[hh] = kl ? keep : kSelZero;
+      sr[hh] = kr ? keep : kSelZero;
+      sm[hh] = valid ? keep : kSelOne;
+    }
+  } else {
+    sl[0] = kl ? 0xFFFFFFFFu : 0u; sl[1] = 0u;
+    sr[0] = kr ? 0xFFFFFFFFu : 0u; sr[1] = 0u;
+    sm[0] = valid ? 0xFFFFFFFFu : 0u; sm[1] = valid ? 0u : 0x3F800000u;
   }
-  int r0 = ln.A + E * lane;
-  r0 = r0 < 0 ? 0 : (r0 > pl.ppad - E ? pl.ppad - E : r0);
-  const int bwl = 31 - __clz(pl.bw);
-  ln.voff = static_cast<uint32_t>((((r0 >> bwl) * C::K) * pl.bw + (r0 & (pl.bw - 1))) * C::es);
-  ln.vstep = static_cast<uint32_t>(pl.bw * C::es);
+}
+
+template <typename T>
+__device__ __forceinline__ Lanes<T> make_lanes(const Plan& pl, const Chain& ch, int wi, int lane) {
+  using C = Cfg<T>;
+  constexpr int WARP = 32 * kE, OWN = WARP - 2 * C::GH;
+  Lanes<T> ln;
+  ln.A = wi * OWN - C::GH;
+  constexpr int lo = C::GH;
+  // vertical
+  {
+    const int off = kE * lane;
+    const int r0 = ln.A + off;
+    ln.pos0 = r0;
+    ln.own_v = off >= lo && off < WARP - C::GH && r0 < ch.P;
+    const int rc = r0 < 0 ? 0 : (r0 > kPpad - kE ? kPpad - kE : r0);
+    const int bw = kRowB / C::es;
+    ln.voff = static_cast<uint32_t>((rc / bw) * (C::K * kRowB) + (rc % bw) * C::es);
+  }
+  // horizontal
+#pragma unroll
+  for (int q = 0; q < kE; ++q) {
+    const int off = 32 * q + lane;
+    const int r = ln.A + off;
+    ln.own_h[q] = off >= lo && off < WARP - C::GH && r < kPpad;
+    const uint32_t rc = static_cast<uint32_t>(r < 0 ? 0 : (r >= kPpad ? kPpad - 1 : r));
+    ln.hoff[q] = rc * 32 + (((rc >> 2) & 1u) << 4);
+  }
+  if (ch.vert) {
+#pragma unroll
+    for (int e = 0; e < kE; ++e) tap_masks<T>(ln.A + kE * lane + e, ch.P, ln.s[0][e], ln.s[1][e], ln.s[2][e], e);
+  } else {
+#pragma unroll
+    for (int q = 0; q < kE; ++q) tap_masks<T>(ln.A + 32 * q + lane, ch.P, ln.s[0][q], ln.s[1][q], ln.s[2][q], -1);
+  }
   return ln;
 }
 
-// Ghost exchange. Each warp publishes its first GH and last GH owned values (edges) and reloads its
-// ghost positions from the neighbouring warps' edges; warps outside [0, nwc) contribute 0.
+// Vertical step operands: 2 consecutive positions per tensor from one 4- (bf16) or 8-byte (fp32) read.
+template <typename T>
+__device__ __forceinline__ void vload(const uint8_t* p, float (&v)[2]) {
+  if constexpr (sizeof(T) == 2) {
+    const uint32_t u = *reinterpret_cast<const uint32_t*>(p);
+    v[0] = __uint_as_float(u << 16);
+    v[1] = __uint_as_float(u & 0xFFFF0000u);
+  } else {
+    const float2 u = *reinterpret_cast<const float2*>(p);
+    v[0] = u.x; v[1] = u.y;
+  }
+}
+template <typename T>
+__device__ __forceinline__ void vload_tap(const uint8_t* p, const uint32_t (&m)[kE][2], float (&v)[2]) {
+  if constexpr (sizeof(T) == 2) {
+    const uint32_t u = *reinterpret_cast<const uint32_t*>(p);
+    v[0] = bsel(u, m[0][0]);
+    v[1] = bsel(u, m[1][0]);
+  } else {
+    const uint2 u = *reinterpret_cast<const uint2*>(p);
+    v[0] = __uint_as_float((u.x & m[0][0]) | m[0][1]);
+    v[1] = __uint_as_float((u.y & m[1][0]) | m[1][1]);
+  }
+}
+
+// Horizontal chunk element i (memory order) of a 16-byte vector; tap version applies the slot masks.
+template <typename T>
+__device__ __forceinline__ float hget(const uint4& u, int i) {
+  if constexpr (sizeof(T) == 2) {
+    const uint32_t w = (i >> 1) == 0 ? u.x : (i >> 1) == 1 ? u.y : (i >> 1) == 2 ? u.z : u.w;
+    return (i & 1) ? __uint_as_float(w & 0xFFFF0000u) : __uint_as_float(w << 16);
+  } else {
+    return __uint_as_float(i == 0 ? u.x : i == 1 ? u.y : i == 2 ? u.z : u.w);
+  }
+}
+template <typename T>
+__device__ __forceinline__ float hget_tap(const uint4& u, int i, const uint32_t (&m)[2]) {
+  if constexpr (sizeof(T) == 2) {
+    const uint32_t w = (i >> 1) == 0 ? u.x : (i >> 1) == 1 ? u.y : (i >> 1) == 2 ? u.z : u.w;
+    return bsel(w, m[i & 1]);
+  } else {
+    const uint32_t w = i == 0 ? u.x : i == 1 ? u.y : i == 2 ? u.z : u.w;
+    return __uint_as_float((w & m[0]) | m[1]);
+  }
+}
+
+// Ghost exchange through shared memory: every warp publishes its first and last GH owned values;
+// warps w >= 1 reload their left ghosts from warp w-1, warps w < nwc-1 their right ghosts from w+1.
 // Parity-double-buffered; the caller separates publish and reload by one named barrier.
-template <typename T, int E>
-__device__ __forceinline__ void edge_publish(float* edge, int par, int wi, int lane, bool vert, const float (&v)[E]) {
+template <typename T>
+__device__ __forceinline__ void edge_publish(float* edge, int par, int wi, int lane, bool vert, const float (&v)[kE]) {
   using C = Cfg<T>;
-  constexpr int WARP = 32 * E;
+  constexpr int WARP = 32 * kE;
   float* L = edge + ((par * kEdgeW + wi) * 2 + 0) * 8;
   float* R = edge + ((par * kEdgeW + wi) * 2 + 1) * 8;
   if (vert) {
-    const int o = E * lane;
-    if (o >= C::GH && o < 2 * C::GH) {
-#pragma unroll
-      for (int e = 0; e < E; ++e) L[o - C::GH + e] = v[e];
-    }
-    if (o >= WARP - 2 * C::GH && o < WARP - C::GH) {
-#pragma unroll
-      for (int e = 0; e < E; ++e) R[o - (WARP - 2 * C::GH) + e] = v[e];
-    }
+    const int o = kE * lane;
+    if (o >= C::GH && o < 2 * C::GH) { L[o - C::GH] = v[0]; L[o - C::GH + 1] = v[1]; }
+    if (o >= WARP - 2 * C::GH && o < WARP - C::GH) { R[o - (WARP - 2 * C::GH)] = v[0]; R[o - (WARP - 2 * C::GH) + 1] = v[1]; }
   } else {
     if (lane >= C::GH && lane < 2 * C::GH) L[lane - C::GH] = v[0];
-    if (lane >= 32 - 2 * C::GH && lane < 32 - C::GH) R[lane - (32 - 2 * C::GH)] = v[E - 1];
+    if (lane >= 32 - 2 * C::GH && lane < 32 - C::GH) R[lane - (32 - 2 * C::GH)] = v[kE - 1];
   }
 }
 
-template <typename T, int E>
+template <typename T>
 __device__ __forceinline__ void edge_reload(const float* edge, int par, int wi, int nwc, int lane, bool vert,
-                                            float (&v)[E]) {
+                                            float (&v)[kE]) {
   using C = Cfg<T>;
-  constexpr int WARP = 32 * E;
+  constexpr int WARP = 32 * kE;
   const float* Rl = edge + ((par * kEdgeW + (wi - 1)) * 2 + 1) * 8;  // left neighbour's right edge
   const float* Lr = edge + ((par * kEdgeW + (wi + 1)) * 2 + 0) * 8;  // right neighbour's left edge
+  const bool has_l = wi > 0, has_r = wi < nwc - 1;
   if (vert) {
-    const int o = E * lane;
-    if (o < C::GH) {
-#pragma unroll
-      for (int e = 0; e < E; ++e) v[e] = wi > 0 ? Rl[o + e] : 0.f;
-    }
-    if (o >= WARP - C::GH) {
-#pragma unroll
-      for (int e = 0; e < E; ++e) v[e] = wi < nwc - 1 ? Lr[o - (WARP - C::GH) + e] : 0.f;
-    }
+    const int o = kE * lane;
+    if (has_l && o < C::GH) { v[0] = Rl[o]; v[1] = Rl[o + 1]; }
+    if (has_r && o >= WARP - C::GH) { v[0] = Lr[o - (WARP - C::GH)]; v[1] = Lr[o - (WARP - C::GH) + 1]; }
   } else {
-    if (lane < C::GH) v[0] = wi > 0 ? Rl[lane] : 0.f;
-    if (lane >= 32 - C::GH) v[E - 1] = wi < nwc - 1 ? Lr[lane - (32 - C::GH)] : 0.f;
+    if (has_l && lane < C::GH) v[0] = Rl[lane];
+    if (has_r && lane >= 32 - C::GH) v[kE - 1] = Lr[lane - (32 - C::GH)];
   }
 }
 
-// Neighbours inside a warp. Vertical (blocked): position e's lower neighbour is e-1 of the same lane
-// (lane-1's last for e = 0); horizontal (interleaved, position A + 32 q + lane): one rotating
-// shuffle per slot; lane 0 of slot q takes lane 31 of slot q-1, lane 31 takes lane 0 of slot q+1.
-// The warp's two outermost positions get 0 (they are ghosts).
-template <int E>
-__device__ __forceinline__ void vert_neighbours(const float (&v)[E], int lane, float (&lo)[E], float (&hi)[E]) {
-  const float left = from_lower_lane(v[E - 1], lane);
-  const float right = from_upper_lane(v[0], lane);
-#pragma unroll
-  for (int e = 0; e < E; ++e) {
-    lo[e] = e == 0 ? left : v[e > 0 ? e - 1 : 0];
-    hi[e] = e == E - 1 ? right : v[e < E - 1 ? e + 1 : 0];
-  }
-}
-
-template <int E>
-__device__ __forceinline__ void slot_neighbours(const float (&v)[E], int lane, float (&lo)[E], float (&hi)[E]) {
-  float up[E], dn[E];
-#pragma unroll
-  for (int q = 0; q < E; ++q) {
-    up[q] = __shfl_sync(0xffffffffu, v[q], (lane + 31) & 31);
-    dn[q] = __shfl_sync(0xffffffffu, v[q], (lane + 1) & 31);
-  }
-#pragma unroll
-  for (int q = 0; q < E; ++q) {
-    lo[q] = lane == 0 ? (q == 0 ? 0.f : up[q > 0 ? q - 1 : 0]) : up[q];
-    hi[q] = lane == 31 ? (q == E - 1 ? 0.f : dn[q < E - 1 ? q + 1 : 0]) : dn[q];
-  }
-}
-
-// Shared-memory carve-up common to both kernels: ring | full | empty | done | edges | flag.
+// Shared-memory carve-up common to both kernels: ring | full | empty | done | edges.
 struct Smem {
   uint8_t* ring;
   uint64_t *full, *empty, *done;
   float* edge;
-  int* flag;
 };
 
 __device__ __forceinline__ Smem carve(uint8_t* smem_raw, const Plan& pl) {
@@ -462,7 +450,6 @@ __device__ __forceinline__ Smem carve(uint8_t* smem_raw, const Plan& pl) {
   m.empty = m.full + pl.nstages;
   m.done = m.empty + pl.nstages;
   m.edge = reinterpret_cast<float*>(m.done + pl.nstages);  // [3 state arrays][2 par][kEdgeW][2][8]
-  m.flag = reinterpret_cast<int*>(m.edge + 3 * 2 * kEdgeW * 2 * 8);
   return m;
 }
 
@@ -478,97 +465,97 @@ __device__ __forceinline__ void init_barriers(const Smem& m, const Plan& pl) {
   __syncthreads();
 }
 
+__device__ __forceinline__ float clamped_rcp(float s) { return fminf(fast_rcp(s), kRcpMax); }
+
 // ------------------------------------------------------------------------------ forward
 
-// One step of Eq. 1 for the lane's E positions given the previous state's neighbours.
-template <int E>
-__device__ __forceinline__ void fwd_update(const Lanes<E>& ln, const float (&x)[E], const float (&lam)[E],
-                                           const float (&wl)[E], const float (&wm)[E], const float (&wr)[E],
-                                           const float (&hm1)[E], const float (&hp1)[E], float (&h)[E],
-                                           bool prenorm, bool live = true) {
-  float hn[E];
-#pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const float l = ln.hl[e] ? wl[e] : 0.f;
-    const float r = ln.hr[e] ? wr[e] : 0.f;
-    const float acc = fmaf(l, hm1[e], fmaf(wm[e], h[e], r * hp1[e]));
-    const float inv = prenorm ? 1.f : fast_rcp(wm[e] + l + r);
-    hn[e] = (ln.valid[e] && live) ? fmaf(acc, inv, lam[e] * x[e]) : 0.f;
-  }
-#pragma unroll
-  for (int e = 0; e < E; ++e) h[e] = hn[e];
+// One step of Eq. 1 at one position (taps already masked, see Lanes).
+template <bool kPre>
+__device__ __forceinline__ float fwd_math(float x, float lam, float l, float m, float r, float hm1, float h,
+                                          float hp1) {
+  const float acc = fmaf(l, hm1, fmaf(m, h, r * hp1));
+  const float inv = kPre ? 1.f : clamped_rcp((l + r) + m);
+  return fmaf(acc, inv, lam * x);
 }
 
-// Vertical half-tile (KS steps, rolled loop). The new state goes straight to global memory.
-template <typename T, int E>
-__device__ __forceinline__ void fwd_half_vert(const Plan& pl, const Lanes<E>& ln, const Chain& ch, int j, int half,
-                                              const uint8_t* st, T* hplane, int64_t W, int lane, float (&h)[E],
-                                              bool prenorm, uint64_t pol) {
-  constexpr int K = Cfg<T>::K, KS = Cfg<T>::KS;
-  const bool lane_out = ln.own[0] && ln.valid[0];  // P % E == 0: a lane's positions share validity
-#pragma unroll 1
-  for (int ss = 0; ss < KS; ++ss) {
-    const int s = half * KS + ss;
-    const int kk = ch.rev ? (K - 1 - s) : s;
-    const uint32_t off = ln.voff + kk * ln.vstep;
-    float x[E], lam[E], wl[E], wm[E], wr[E], hm1[E], hp1[E];
-    VE<T, E>::load(st + F_X * pl.tile_bytes + off, x);
-    VE<T, E>::load(st + F_LAM * pl.tile_bytes + off, lam);
-    VE<T, E>::load(st + F_WL * pl.tile_bytes + off, wl);
-    VE<T, E>::load(st + F_WM * pl.tile_bytes + off, wm);
-    VE<T, E>::load(st + F_WR * pl.tile_bytes + off, wr);
-    vert_neighbours<E>(h, lane, hm1, hp1);
-    fwd_update<E>(ln, x, lam, wl, wm, wr, hm1, hp1, h, prenorm);
-    const int t = j * K + s;
-    if (lane_out && t < ch.L) {
-      const int row = ch.rev ? (ch.L - 1 - t) : t;
-      GStore<T, E>::st(hplane + static_cast<int64_t>(row) * W + ln.pos[0], h, pol);
-    }
-  }
-}
-
-// Horizontal half-tile: one 16-byte chunk (KS steps) per tensor per slot, in scan order; the new
-// states are returned packed (written in place by the caller after the edge barrier).
-template <typename T, int E>
-__device__ __forceinline__ void fwd_half_horiz(const Plan& pl, const Lanes<E>& ln, bool rev, int half, int t0,
-                                               const uint8_t* st, int lane, float (&h)[E], bool prenorm,
-                                               uint4 (&OUT)[E]) {
+// Vertical half-tile: KS steps; p0 = the lane's operands at the half's first step, stepb = +-kRowB.
+// New states go straight to global memory (gp advances by gstep rows per step).
+template <typename T, bool kPre>
+__device__ __forceinline__ void fwd_half_vert(const Lanes<T>& ln, const uint8_t* p0, int stepb, T* gp,
+                                              int64_t gstep, int t0, int L, float (&h)[kE], uint64_t pol) {
   constexpr int KS = Cfg<T>::KS;
-  const int cm = rev ? 1 - half : half;  // memory chunk of this half
-  uint4 X[E], LAM[E], WL[E], WM[E], WR[E];
-#pragma unroll
-  for (int q = 0; q < E; ++q) {
-    const uint32_t off = hchunk(ln.row[q], cm);
-    X[q] = Rev<T>::r(*reinterpret_cast<const uint4*>(st + F_X * pl.tile_bytes + off), rev);
-    LAM[q] = Rev<T>::r(*reinterpret_cast<const uint4*>(st + F_LAM * pl.tile_bytes + off), rev);
-    WL[q] = Rev<T>::r(*reinterpret_cast<const uint4*>(st + F_WL * pl.tile_bytes + off), rev);
-    WM[q] = Rev<T>::r(*reinterpret_cast<const uint4*>(st + F_WM * pl.tile_bytes + off), rev);
-    WR[q] = Rev<T>::r(*reinterpret_cast<const uint4*>(st + F_WR * pl.tile_bytes + off), rev);
-  }
-  float O[E][KS];
 #pragma unroll
   for (int ss = 0; ss < KS; ++ss) {
-    float hm1[E], hp1[E], x[E], lam[E], wl[E], wm[E], wr[E];
-    slot_neighbours<E>(h, lane, hm1, hp1);
-#pragma unroll
-    for (int q = 0; q < E; ++q) {
-      x[q] = Pk<T>::get(X[q], ss);
-      lam[q] = Pk<T>::get(LAM[q], ss);
-      wl[q] = Pk<T>::get(WL[q], ss);
-      wm[q] = Pk<T>::get(WM[q], ss);
-      wr[q] = Pk<T>::get(WR[q], ss);
-    }
-    // steps before t = 0 (partial first R2L tile) keep h = h_{-1} = 0
-    fwd_update<E>(ln, x, lam, wl, wm, wr, hm1, hp1, h, prenorm, t0 + half * KS + ss >= 0);
-#pragma unroll
-    for (int q = 0; q < E; ++q) O[q][ss] = h[q];
+    const uint8_t* q = p0 + ss * stepb;
+    float x[2], lam[2], l[2], m[2], r[2];
+    vload<T>(q + F_X * kTile, x);
+    vload<T>(q + F_LAM * kTile, lam);
+    vload_tap<T>(q + F_WL * kTile, ln.s[0], l);
+    vload_tap<T>(q + F_WM * kTile, ln.s[1], m);
+    vload_tap<T>(q + F_WR * kTile, ln.s[2], r);
+    const float left = __shfl_up_sync(0xffffffffu, h[1], 1);    // lane 0: own value (ghost or masked)
+    const float right = __shfl_down_sync(0xffffffffu, h[0], 1);  // lane 31: own value
+    const float h0 = fwd_math<kPre>(x[0], lam[0], l[0], m[0], r[0], left, h[0], h[1]);
+    const float h1 = fwd_math<kPre>(x[1], lam[1], l[1], m[1], r[1], h[0], h[1], right);
+    h[0] = h0;
+    h[1] = h1;
+    if (ln.own_v && t0 + ss < L) GStore<T, 2>::st(gp, h, pol);
+    gp += gstep;
   }
-#pragma unroll
-  for (int q = 0; q < E; ++q) OUT[q] = Rev<T>::r(Pk<T>::pack(O[q]), rev);
 }
 
-template <typename T, int E, int kMaxNWC>
+// Horizontal neighbours: position A + 32 q + lane; lane 0 of slot 1 takes lane 31 of slot 0 and
+// lane 31 of slot 0 takes lane 0 of slot 1 (the warp's outermost positions are ghosts or masked).
+__device__ __forceinline__ void slot_lo(const float (&v)[kE], int lane, float (&lo)[kE]) {
+  const float u0 = __shfl_sync(0xffffffffu, v[0], (lane + 31) & 31);
+  const float u1 = __shfl_sync(0xffffffffu, v[1], (lane + 31) & 31);
+  lo[0] = u0;
+  lo[1] = lane == 0 ? u0 : u1;
+}
+__device__ __forceinline__ void slot_hi(const float (&v)[kE], int lane, float (&hi)[kE]) {
+  const float d0 = __shfl_sync(0xffffffffu, v[0], (lane + 1) & 31);
+  const float d1 = __shfl_sync(0xffffffffu, v[1], (lane + 1) & 31);
+  hi[0] = lane == 31 ? d1 : d0;
+  hi[1] = d1;
+}
+
+// Horizontal half-tile: one 16-byte chunk (KS steps) per tensor per slot; kRev walks the chunk
+// backwards (R2L). The new states come back packed in memory order for the in-place write.
+template <typename T, bool kPre, bool kRev>
+__device__ __forceinline__ void fwd_half_horiz(const Lanes<T>& ln, const uint8_t* st, int cm, int lane,
+                                               float (&h)[kE], uint4 (&OUT)[kE]) {
+  constexpr int KS = Cfg<T>::KS;
+  uint4 X[kE], LAM[kE], WL[kE], WM[kE], WR[kE];
+#pragma unroll
+  for (int q = 0; q < kE; ++q) {
+    const uint32_t off = ln.hoff[q] ^ (static_cast<uint32_t>(cm) << 4);
+    X[q] = *reinterpret_cast<const uint4*>(st + F_X * kTile + off);
+    LAM[q] = *reinterpret_cast<const uint4*>(st + F_LAM * kTile + off);
+    WL[q] = *reinterpret_cast<const uint4*>(st + F_WL * kTile + off);
+    WM[q] = *reinterpret_cast<const uint4*>(st + F_WM * kTile + off);
+    WR[q] = *reinterpret_cast<const uint4*>(st + F_WR * kTile + off);
+  }
+  float O[kE][KS];
+#pragma unroll
+  for (int ss = 0; ss < KS; ++ss) {
+    const int i = kRev ? KS - 1 - ss : ss;  // element of the chunk (memory order)
+    float lo[kE], hi[kE];
+    slot_lo(h, lane, lo);
+    slot_hi(h, lane, hi);
+#pragma unroll
+    for (int q = 0; q < kE; ++q) {
+      h[q] = fwd_math<kPre>(hget<T>(X[q], i), hget<T>(LAM[q], i), hget_tap<T>(WL[q], i, ln.s[0][q]),
+                            hget_tap<T>(WM[q], i, ln.s[1][q]), hget_tap<T>(WR[q], i, ln.s[2][q]), lo[q], h[q], hi[q]);
+      O[q][i] = h[q];
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < kE; ++q) OUT[q] = Pk<T>::pack(O[q]);
+}
+
+template <typename T, bool kPre>
 __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) fwd_stream_kernel(const __grid_constant__ StreamArgs A) {
+  using C = Cfg<T>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const Plan& pl = A.plan;
   const Smem m = carve(smem_raw, pl);
@@ -589,38 +576,47 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) fwd_stream_kernel(const
     }
     return;
   }
-  const bool prenorm = A.p.flags & GSPN_FLAG_PRENORMALIZED;
   const uint64_t pol_vout = policy_of(pl.pol[3]);
   const int nthreads = pl.nwc * 32;
-  const int64_t HW = A.p.H * A.p.W;
+  const int64_t HW = A.p.H * A.p.W, W = A.p.W;
   int stage = 0, par = 0;
   uint32_t phase = 0;
   for (int64_t w = blockIdx.x; w < pl.nchains; w += gridDim.x) {
-    const Chain ch = make_chain(A.p, pl.K, w);
-    const Lanes<E> ln = make_lanes<T, E>(pl, ch, warp, lane);
+    const Chain ch = make_chain(A.p, C::K, w);
+    const Lanes<T> ln = make_lanes<T>(pl, ch, warp, lane);
     T* hplane = static_cast<T*>(A.p.hout) + ch.chain * HW;
-    float h[E];
-#pragma unroll
-    for (int e = 0; e < E; ++e) h[e] = 0.f;
+    float h[kE] = {0.f, 0.f};
     for (int j = 0; j < ch.ntiles; ++j) {
       mbar_wait(smem_u32(&m.full[stage]), phase);
+      __syncwarp();  // reconverge after the per-thread spin: the shuffles below need no collective fallback
       uint8_t* st = m.ring + static_cast<size_t>(stage) * pl.stage_bytes;
 #pragma unroll 1
       for (int half = 0; half < 2; ++half) {
-        uint4 OUT[E];
+        uint4 OUT[kE];
+        const int cm = ch.rev ? 1 - half : half;  // horizontal: memory chunk of this half
         if (!pl.null_compute) {
-          if (ch.vert) fwd_half_vert<T, E>(pl, ln, ch, j, half, st, hplane, A.p.W, lane, h, prenorm, pol_vout);
-          else fwd_half_horiz<T, E>(pl, ln, ch.rev, half, tile_step0(ch, j, pl.K), st, lane, h, prenorm, OUT);
+          if (ch.vert) {
+            const int t0 = j * C::K + half * C::KS;
+            const int kk0 = ch.rev ? C::K - 1 - half * C::KS : half * C::KS;
+            const int row0 = ch.rev ? ch.L - 1 - t0 : t0;
+            fwd_half_vert<T, kPre>(ln, st + ln.voff + kk0 * kRowB, ch.rev ? -kRowB : kRowB,
+                                   hplane + static_cast<int64_t>(row0) * W + ln.pos0, ch.rev ? -W : W, t0, ch.L, h,
+                                   pol_vout);
+          } else if (ch.rev) {
+            fwd_half_horiz<T, kPre, true>(ln, st, cm, lane, h, OUT);
+          } else {
+            fwd_half_horiz<T, kPre, false>(ln, st, cm, lane, h, OUT);
+          }
         }
-        edge_publish<T, E>(m.edge, par, warp, lane, ch.vert, h);
+        edge_publish<T>(m.edge, par, warp, lane, ch.vert, h);
         named_bar(kBarEdge, nthreads);  // edges published; every warp has read this half's input rows
-        edge_reload<T, E>(m.edge, par, warp, pl.nwc, lane, ch.vert, h);
+        edge_reload<T>(m.edge, par, warp, pl.nwc, lane, ch.vert, h);
         par ^= 1;
         if (!ch.vert && !pl.null_compute) {  // new states in place over the x chunk of this half
-          const int cm = ch.rev ? 1 - half : half;
 #pragma unroll
-          for (int q = 0; q < E; ++q)
-            if (ln.own[q]) *reinterpret_cast<uint4*>(st + F_X * pl.tile_bytes + hchunk(ln.row[q], cm)) = OUT[q];
+          for (int q = 0; q < kE; ++q)
+            if (ln.own_h[q])
+              *reinterpret_cast<uint4*>(st + F_X * kTile + (ln.hoff[q] ^ (static_cast<uint32_t>(cm) << 4))) = OUT[q];
         }
       }
       fence_proxy_async();  // in-place outputs -> visible to the storer's TMA (async proxy)
@@ -633,108 +629,81 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) fwd_stream_kernel(const
 
 // ------------------------------------------------------------------------------ backward recurrence
 
-// State carried between steps (reverse order): ea = a_{t+1} g_{t+1}, eb = b_{t+1} g_{t+1},
-// ec = c_{t+1} g_{t+1} at the lane's E positions.
-template <int E>
+// State carried between steps (reverse order): ea = a g, eb = b g, ec = c g of step t+1 at the lane's
+// positions. g_t = dh_t + (b g)[r] + (a g)[r+1] + (c g)[r-1].
 struct BwdState {
-  float ea[E], eb[E], ec[E];
+  float ea[kE], eb[kE], ec[kE];
 };
 
-// One adjoint step: g_t = dh_t + (b g)[r] + (a g)[r+1] + (c g)[r-1] of step t+1 (nr, nl carry the
-// neighbours' products), then the state becomes step t's products.
-template <int E>
-__device__ __forceinline__ void bwd_update(const Lanes<E>& ln, bool live, const float (&dh)[E], const float (&wl)[E],
-                                           const float (&wm)[E], const float (&wr)[E], const float (&nr)[E],
-                                           const float (&nl)[E], BwdState<E>& S, float (&g)[E], bool prenorm) {
+template <bool kPre>
+__device__ __forceinline__ float bwd_math(float dh, float l, float m, float r, float nr, float nl, float& ea,
+                                          float& eb, float& ec) {
+  const float ge = (dh + eb) + (nr + nl);
+  const float ig = kPre ? ge : clamped_rcp((l + r) + m) * ge;
+  ea = l * ig;
+  eb = m * ig;
+  ec = r * ig;
+  return ge;
+}
+
+template <typename T, bool kPre>
+__device__ __forceinline__ void bwd_half_vert(const Lanes<T>& ln, const uint8_t* p0, int stepb, T* gp,
+                                              int64_t gstep, int t0, int L, BwdState& S, uint64_t pol) {
+  constexpr int KS = Cfg<T>::KS;
+  // steps t0 + KS - 1 down to t0; p0 / gp address step t0 + KS - 1
 #pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const bool ok = live && ln.valid[e];
-    const float ge = ok ? (dh[e] + S.eb[e] + nr[e] + nl[e]) : 0.f;
-    const float l = ln.hl[e] ? wl[e] : 0.f;
-    const float r = ln.hr[e] ? wr[e] : 0.f;
-    const float ig = (prenorm ? 1.f : fast_rcp(wm[e] + l + r)) * ge;
-    g[e] = ge;
-    S.ea[e] = ok ? l * ig : 0.f;
-    S.eb[e] = ok ? wm[e] * ig : 0.f;
-    S.ec[e] = ok ? r * ig : 0.f;
+  for (int i = 0; i < KS; ++i) {
+    const uint8_t* q = p0 + i * stepb;
+    float dh[2], l[2], m[2], r[2];
+    vload<T>(q + B_DH * kTile, dh);
+    vload_tap<T>(q + B_WL * kTile, ln.s[0], l);
+    vload_tap<T>(q + B_WM * kTile, ln.s[1], m);
+    vload_tap<T>(q + B_WR * kTile, ln.s[2], r);
+    const float nr1 = __shfl_down_sync(0xffffffffu, S.ea[0], 1);  // (a g) of the position above
+    const float nl0 = __shfl_up_sync(0xffffffffu, S.ec[1], 1);    // (c g) of the position below
+    const float ea0 = S.ea[1], ec1 = S.ec[0];
+    float g[2];
+    g[0] = bwd_math<kPre>(dh[0], l[0], m[0], r[0], ea0, nl0, S.ea[0], S.eb[0], S.ec[0]);
+    g[1] = bwd_math<kPre>(dh[1], l[1], m[1], r[1], nr1, ec1, S.ea[1], S.eb[1], S.ec[1]);
+    if (ln.own_v && t0 + KS - 1 - i < L) GStore<T, 2>::st(gp, g, pol);
+    gp += gstep;
   }
 }
 
-template <typename T, int E>
-__device__ __forceinline__ void bwd_half_vert(const StreamArgs& A, const Lanes<E>& ln, const Chain& ch, int j,
-                                              int half, const uint8_t* st, int lane, BwdState<E>& S, bool prenorm,
-                                              uint64_t pol_out) {
-  constexpr int K = Cfg<T>::K, KS = Cfg<T>::KS;
-  const Plan& pl = A.plan;
-  const ScanParams& p = A.p;
-  T* gout = static_cast<T*>(A.g) + ch.chain * p.H * p.W;
-  const bool lane_out = ln.own[0] && ln.valid[0];
-#pragma unroll 1
-  for (int ss = KS - 1; ss >= 0; --ss) {
-    const int s = half * KS + ss;
-    const int t = j * K + s;
-    const bool live = t < ch.L;
-    const int kk = ch.rev ? (K - 1 - s) : s;
-    const uint32_t off = ln.voff + kk * ln.vstep;
-    float dh[E], wl[E], wm[E], wr[E], nr[E], nl[E], lo_a[E], hi_c[E], g[E];
-    VE<T, E>::load(st + B_DH * pl.tile_bytes + off, dh);
-    VE<T, E>::load(st + B_WL * pl.tile_bytes + off, wl);
-    VE<T, E>::load(st + B_WM * pl.tile_bytes + off, wm);
-    VE<T, E>::load(st + B_WR * pl.tile_bytes + off, wr);
-    vert_neighbours<E>(S.ea, lane, lo_a, nr);  // nr[e] = (a g) of position e + 1
-    vert_neighbours<E>(S.ec, lane, nl, hi_c);  // nl[e] = (c g) of position e - 1
-    bwd_update<E>(ln, live, dh, wl, wm, wr, nr, nl, S, g, prenorm);
-    if (lane_out && live) {
-      const int row = ch.rev ? (ch.L - 1 - t) : t;
-      GStore<T, E>::st(gout + static_cast<int64_t>(row) * p.W + ln.pos[0], g, pol_out);
-    }
+template <typename T, bool kPre, bool kRev>
+__device__ __forceinline__ void bwd_half_horiz(const Lanes<T>& ln, const uint8_t* st, int cm, int lane, BwdState& S,
+                                               uint4 (&OG)[kE]) {
+  constexpr int KS = Cfg<T>::KS;
+  uint4 DH[kE], WL[kE], WM[kE], WR[kE];
+#pragma unroll
+  for (int q = 0; q < kE; ++q) {
+    const uint32_t off = ln.hoff[q] ^ (static_cast<uint32_t>(cm) << 4);
+    DH[q] = *reinterpret_cast<const uint4*>(st + B_DH * kTile + off);
+    WL[q] = *reinterpret_cast<const uint4*>(st + B_WL * kTile + off);
+    WM[q] = *reinterpret_cast<const uint4*>(st + B_WM * kTile + off);
+    WR[q] = *reinterpret_cast<const uint4*>(st + B_WR * kTile + off);
   }
+  float G_[kE][KS];
+#pragma unroll
+  for (int ss = KS - 1; ss >= 0; --ss) {  // scan order descending
+    const int i = kRev ? KS - 1 - ss : ss;
+    float nr[kE], nl[kE];
+    slot_hi(S.ea, lane, nr);
+    slot_lo(S.ec, lane, nl);
+#pragma unroll
+    for (int q = 0; q < kE; ++q)
+      G_[q][i] = bwd_math<kPre>(hget<T>(DH[q], i), hget_tap<T>(WL[q], i, ln.s[0][q]),
+                                hget_tap<T>(WM[q], i, ln.s[1][q]), hget_tap<T>(WR[q], i, ln.s[2][q]), nr[q], nl[q],
+                                S.ea[q], S.eb[q], S.ec[q]);
+  }
+#pragma unroll
+  for (int q = 0; q < kE; ++q) OG[q] = Pk<T>::pack(G_[q]);
 }
 
-// Horizontal half-tile (KS steps, descending); g comes back packed for the in-place write.
-template <typename T, int E>
-__device__ __forceinline__ void bwd_half_horiz(const Lanes<E>& ln, const Chain& ch, int j, int half,
-                                               const uint8_t* st, uint32_t tile_bytes, int lane, BwdState<E>& S,
-                                               bool prenorm, uint4 (&OG)[E]) {
-  constexpr int K = Cfg<T>::K, KS = Cfg<T>::KS;
-  const bool rev = ch.rev;
-  const int cm = rev ? 1 - half : half;
-  uint4 DH[E], WL[E], WM[E], WR[E];
-#pragma unroll
-  for (int q = 0; q < E; ++q) {
-    const uint32_t off = hchunk(ln.row[q], cm);
-    DH[q] = Rev<T>::r(*reinterpret_cast<const uint4*>(st + B_DH * tile_bytes + off), rev);
-    WL[q] = Rev<T>::r(*reinterpret_cast<const uint4*>(st + B_WL * tile_bytes + off), rev);
-    WM[q] = Rev<T>::r(*reinterpret_cast<const uint4*>(st + B_WM * tile_bytes + off), rev);
-    WR[q] = Rev<T>::r(*reinterpret_cast<const uint4*>(st + B_WR * tile_bytes + off), rev);
-  }
-  float G_[E][KS];
-  const int t0 = tile_step0(ch, j, K) + half * KS;
-#pragma unroll
-  for (int ss = KS - 1; ss >= 0; --ss) {
-    const int t = t0 + ss;
-    float dh[E], wl[E], wm[E], wr[E], nr[E], nl[E], ea_lo[E], ec_hi[E], g[E];
-#pragma unroll
-    for (int q = 0; q < E; ++q) {
-      dh[q] = Pk<T>::get(DH[q], ss);
-      wl[q] = Pk<T>::get(WL[q], ss);
-      wm[q] = Pk<T>::get(WM[q], ss);
-      wr[q] = Pk<T>::get(WR[q], ss);
-    }
-    slot_neighbours<E>(S.ea, lane, ea_lo, nr);
-    slot_neighbours<E>(S.ec, lane, nl, ec_hi);
-    bwd_update<E>(ln, t >= 0 && t < ch.L, dh, wl, wm, wr, nr, nl, S, g, prenorm);
-#pragma unroll
-    for (int q = 0; q < E; ++q) G_[q][ss] = g[q];
-  }
-#pragma unroll
-  for (int q = 0; q < E; ++q) OG[q] = Rev<T>::r(Pk<T>::pack(G_[q]), rev);
-}
-
-template <typename T, int E, int kMaxNWC>
+template <typename T, bool kPre>
 __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_stream_kernel(const __grid_constant__ StreamArgs A) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
   using C = Cfg<T>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
   const Plan& pl = A.plan;
   const Smem m = carve(smem_raw, pl);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -754,42 +723,56 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_stream_kernel(const
     }
     return;
   }
-  const bool prenorm = A.p.flags & GSPN_FLAG_PRENORMALIZED;
   const uint64_t pol_vout = policy_of(pl.pol[3]);
   const int nthreads = pl.nwc * 32;
   constexpr int kEdgeArr = 2 * kEdgeW * 2 * 8;
+  const int64_t HW = A.p.H * A.p.W, W = A.p.W;
   int stage = 0, par = 0;
   uint32_t phase = 0;
   for (int64_t w = blockIdx.x; w < pl.nchains; w += gridDim.x) {
-    const Chain ch = make_chain(A.p, pl.K, w);
-    const Lanes<E> ln = make_lanes<T, E>(pl, ch, warp, lane);
-    BwdState<E> S;
+    const Chain ch = make_chain(A.p, C::K, w);
+    const Lanes<T> ln = make_lanes<T>(pl, ch, warp, lane);
+    T* gplane = static_cast<T*>(A.g) + ch.chain * HW;
+    BwdState S;
 #pragma unroll
-    for (int e = 0; e < E; ++e) S.ea[e] = S.eb[e] = S.ec[e] = 0.f;
+    for (int e = 0; e < kE; ++e) S.ea[e] = S.eb[e] = S.ec[e] = 0.f;
     for (int jj = 0; jj < ch.ntiles; ++jj) {
       const int j = ch.ntiles - 1 - jj;
       mbar_wait(smem_u32(&m.full[stage]), phase);
+      __syncwarp();  // reconverge after the per-thread spin: the shuffles below need no collective fallback
       uint8_t* st = m.ring + static_cast<size_t>(stage) * pl.stage_bytes;
 #pragma unroll 1
       for (int half = 1; half >= 0; --half) {
-        uint4 OG[E];
+        uint4 OG[kE];
+        const int cm = ch.rev ? 1 - half : half;
         if (!pl.null_compute) {
-          if (ch.vert) bwd_half_vert<T, E>(A, ln, ch, j, half, st, lane, S, prenorm, pol_vout);
-          else bwd_half_horiz<T, E>(ln, ch, j, half, st, pl.tile_bytes, lane, S, prenorm, OG);
+          if (ch.vert) {
+            const int t0 = j * C::K + half * C::KS;          // first (lowest) step of the half
+            const int tl = t0 + C::KS - 1;                     // processed first
+            const int kkl = ch.rev ? C::K - 1 - (half * C::KS + C::KS - 1) : half * C::KS + C::KS - 1;
+            const int rowl = ch.rev ? ch.L - 1 - tl : tl;
+            bwd_half_vert<T, kPre>(ln, st + ln.voff + kkl * kRowB, ch.rev ? kRowB : -kRowB,
+                                   gplane + static_cast<int64_t>(rowl) * W + ln.pos0, ch.rev ? W : -W, t0, ch.L, S,
+                                   pol_vout);
+          } else if (ch.rev) {
+            bwd_half_horiz<T, kPre, true>(ln, st, cm, lane, S, OG);
+          } else {
+            bwd_half_horiz<T, kPre, false>(ln, st, cm, lane, S, OG);
+          }
         }
-        edge_publish<T, E>(m.edge + 0 * kEdgeArr, par, warp, lane, ch.vert, S.ea);
-        edge_publish<T, E>(m.edge + 1 * kEdgeArr, par, warp, lane, ch.vert, S.eb);
-        edge_publish<T, E>(m.edge + 2 * kEdgeArr, par, warp, lane, ch.vert, S.ec);
+        edge_publish<T>(m.edge + 0 * kEdgeArr, par, warp, lane, ch.vert, S.ea);
+        edge_publish<T>(m.edge + 1 * kEdgeArr, par, warp, lane, ch.vert, S.eb);
+        edge_publish<T>(m.edge + 2 * kEdgeArr, par, warp, lane, ch.vert, S.ec);
         named_bar(kBarEdge, nthreads);  // edges published; every warp has read this half's input rows
-        edge_reload<T, E>(m.edge + 0 * kEdgeArr, par, warp, pl.nwc, lane, ch.vert, S.ea);
-        edge_reload<T, E>(m.edge + 1 * kEdgeArr, par, warp, pl.nwc, lane, ch.vert, S.eb);
-        edge_reload<T, E>(m.edge + 2 * kEdgeArr, par, warp, pl.nwc, lane, ch.vert, S.ec);
+        edge_reload<T>(m.edge + 0 * kEdgeArr, par, warp, pl.nwc, lane, ch.vert, S.ea);
+        edge_reload<T>(m.edge + 1 * kEdgeArr, par, warp, pl.nwc, lane, ch.vert, S.eb);
+        edge_reload<T>(m.edge + 2 * kEdgeArr, par, warp, pl.nwc, lane, ch.vert, S.ec);
         par ^= 1;
         if (!ch.vert && !pl.null_compute) {
-          const int cm = ch.rev ? 1 - half : half;
 #pragma unroll
-          for (int q = 0; q < E; ++q)
-            if (ln.own[q]) *reinterpret_cast<uint4*>(st + B_DH * pl.tile_bytes + hchunk(ln.row[q], cm)) = OG[q];
+          for (int q = 0; q < kE; ++q)
+            if (ln.own_h[q])
+              *reinterpret_cast<uint4*>(st + B_DH * kTile + (ln.hoff[q] ^ (static_cast<uint32_t>(cm) << 4))) = OG[q];
         }
       }
       fence_proxy_async();  // in-place outputs -> visible to the storer's TMA (async proxy)
@@ -811,18 +794,6 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_stream_kernel(const
 // thread-iteration re-reads two of them from L1).
 // V consecutive elements <-> floats through one 8- or 16-byte global access (read-only path for loads).
 template <typename T, int V> struct GVec;
-template <> struct GVec<__nv_bfloat16, 8> {
-  static __device__ __forceinline__ void load(const __nv_bfloat16* p, float (&v)[8]) {
-    const uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
-    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-    for (int q = 0; q < 4; ++q) { v[2 * q] = __uint_as_float(w[q] << 16); v[2 * q + 1] = __uint_as_float(w[q] & 0xFFFF0000u); }
-  }
-  static __device__ __forceinline__ void store(__nv_bfloat16* p, const float (&v)[8]) {
-    *reinterpret_cast<uint4*>(p) = make_uint4(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]),
-                                              pack_bf16x2(v[4], v[5]), pack_bf16x2(v[6], v[7]));
-  }
-};
 template <> struct GVec<__nv_bfloat16, 4> {
   static __device__ __forceinline__ void load(const __nv_bfloat16* p, float (&v)[4]) {
     const uint2 u = __ldg(reinterpret_cast<const uint2*>(p));
@@ -1250,8 +1221,8 @@ int smem_optin() {
 
 constexpr int kSmemTail = 6656;  // mbarriers (3 per stage), ghost-edge buffers (6 KB), flag
 
-// Shape eligibility + plan (nin: tensors per tile, E: positions per lane).
-bool make_plan(const ScanParams& p, gspn_dtype_t dt, int nin, int E, Plan* pl) {
+// Shape eligibility + plan (nin: tensors per tile).
+bool make_plan(const ScanParams& p, gspn_dtype_t dt, int nin, Plan* pl) {
   const int s = dt == GSPN_BF16 ? 2 : 4;
   // TMA: 16-byte aligned row stride; the horizontal 16-byte chunks tile W exactly
   if ((p.W * s) % 16 != 0) return false;
@@ -1260,31 +1231,29 @@ bool make_plan(const ScanParams& p, gspn_dtype_t dt, int nin, int E, Plan* pl) {
     if (p.dirbit[k] == GSPN_DIR_T2B || p.dirbit[k] == GSPN_DIR_B2T) any_v = true; else any_h = true;
   }
   const int64_t maxP = std::max<int64_t>(any_v ? p.W : 0, any_h ? p.H : 0);
+  if (maxP > kPpad) return false;
   memset(pl, 0, sizeof *pl);
   pl->K = 32 / s;
-  pl->E = E;
+  const int GH = pl->K / 2;
+  pl->E = 2;
   pl->es = s;
-  pl->own = 32 * E - pl->K;  // 32 E - 2 GH, GH = K/2
-  pl->nwc = static_cast<int>((maxP + pl->own - 1) / pl->own);
-  if (pl->nwc > kEdgeW) return false;
-  int ppad = static_cast<int>((maxP + 63) / 64 * 64);
-  int bw = 0;
-  for (int b = 256; b >= 16 / s; b >>= 1)
-    if (ppad % b == 0 && (p.W + b - 1) / b * b <= ppad) { bw = b; break; }
-  if (bw == 0) return false;
-  pl->ppad = ppad;
-  pl->bw = bw;
-  pl->bh = 0;
-  for (int b = 256; b >= 8; b >>= 1)
-    if ((p.H + b - 1) / b * b <= ppad) { pl->bh = b; break; }
-  if (pl->bh == 0) return false;
-  pl->nbw = static_cast<int>((p.W + pl->bw - 1) / pl->bw);
-  pl->nbh = static_cast<int>((p.H + pl->bh - 1) / pl->bh);
+  pl->own = 64 - 2 * GH;
+  pl->nwc = static_cast<int>((maxP + pl->own - 1) / pl->own);  // warp w owns [w own, (w+1) own)
+  if (pl->nwc > 11) return false;
+  // positions any lane reads (clamped to the tile); the TMA boxes cover them so no lane reads stale rows
+  const int cover = static_cast<int>(std::min<int64_t>(kPpad, (pl->nwc - 1) * pl->own - GH + 64));
+  pl->ppad = kPpad;
+  pl->bw = kRowB / s;
+  pl->nbw = (cover + pl->bw - 1) / pl->bw;
+  int bh = 8;
+  while (bh < cover && bh < 256) bh <<= 1;
+  pl->bh = bh;
+  pl->nbh = (cover + bh - 1) / bh;
   pl->nin = nin;
-  pl->tile_bytes = static_cast<uint32_t>(pl->K * pl->ppad * s);
-  pl->stage_bytes = nin * pl->tile_bytes;
+  pl->tile_bytes = kTile;
+  pl->stage_bytes = nin * kTile;
   pl->tx_v = static_cast<uint32_t>(nin * pl->nbw * pl->bw * pl->K * s);
-  pl->tx_h = static_cast<uint32_t>(nin * pl->nbh * pl->bh * pl->K * s);
+  pl->tx_h = static_cast<uint32_t>(nin * pl->nbh * pl->bh * 32);
   const int budget = smem_optin() - 1024 /*alignment*/ - kSmemTail;
   int ns = budget / static_cast<int>(pl->stage_bytes);
   if (ns > 6) ns = 6;
@@ -1352,18 +1321,6 @@ WsLayout ws_layout(int64_t B, int64_t C, int64_t H, int64_t W, int64_t D, gspn_d
   return l;
 }
 
-// Positions per lane: 2 (more warps per chain, better latency hiding) while a chain fits in
-// kE2Warps warps, else 4. GSPN_E=2|4 overrides (experiments).
-constexpr int kE2Warps = 12;
-
-int pick_E(const ScanParams& p, gspn_dtype_t dt, int nin, Plan* pl) {
-  int E = 2;
-  if (const char* ev = getenv("GSPN_E")) E = atoi(ev) == 4 ? 4 : 2;
-  if (E == 2 && (!make_plan(p, dt, nin, 2, pl) || pl->nwc > kE2Warps)) E = 4;
-  if (E == 4 && !make_plan(p, dt, nin, 4, pl)) return 0;
-  return E;
-}
-
 }  // namespace
 
 size_t stream_bwd_workspace_bytes(int64_t B, int64_t C, int64_t H, int64_t W, int64_t D, int64_t, gspn_dtype_t dt) {
@@ -1377,20 +1334,19 @@ cudaError_t launch_fwd_stream(const ScanParams& p, gspn_dtype_t dt, cudaStream_t
   std::lock_guard<std::mutex> lock(mu);
   memset(&A, 0, sizeof A);
   A.p = p;
-  const int E = pick_E(p, dt, F_NIN, &A.plan);
-  if (E == 0) return cudaSuccess;
+  if (!make_plan(p, dt, F_NIN, &A.plan)) return cudaSuccess;
   const void* ins[F_NIN] = {p.x, p.lam, p.wl, p.wm, p.wr};
   const int64_t in_planes[F_NIN] = {p.B * p.C, p.D * p.B * p.C, p.D * p.B * p.G, p.D * p.B * p.G, p.D * p.B * p.G};
   void* outs[1] = {p.hout};
   if (!fill_maps(&A, ins, F_NIN, outs, in_planes, p.D * p.B * p.C, 1, dt)) return cudaSuccess;
   *handled = true;
+  using BF = __nv_bfloat16;
+  const bool pre = p.flags & GSPN_FLAG_PRENORMALIZED;
   cudaError_t e;
-  if (E == 2)
-    e = dt == GSPN_BF16 ? launch(fwd_stream_kernel<__nv_bfloat16, 2, kE2Warps>, A, s)
-                        : launch(fwd_stream_kernel<float, 2, kE2Warps>, A, s);
+  if (dt == GSPN_BF16)
+    e = pre ? launch(fwd_stream_kernel<BF, true>, A, s) : launch(fwd_stream_kernel<BF, false>, A, s);
   else
-    e = dt == GSPN_BF16 ? launch(fwd_stream_kernel<__nv_bfloat16, 4, kEdgeW>, A, s)
-                        : launch(fwd_stream_kernel<float, 4, kEdgeW>, A, s);
+    e = pre ? launch(fwd_stream_kernel<float, true>, A, s) : launch(fwd_stream_kernel<float, false>, A, s);
   *launches += 1;
   return e;
 }
@@ -1403,8 +1359,7 @@ cudaError_t launch_bwd_stream(const ScanParams& p0, gspn_dtype_t dt, cudaStream_
   memset(&A, 0, sizeof A);
   A.p = p0;
   ScanParams& p = A.p;
-  const int E = pick_E(p, dt, B_NIN, &A.plan);  // (W * sizeof(T)) % 16 == 0: V-column groups tile W
-  if (E == 0) return cudaSuccess;
+  if (!make_plan(p, dt, B_NIN, &A.plan)) return cudaSuccess;  // (W s) % 16 == 0: V-column groups tile W
   const WsLayout l = ws_layout(p.B, p.C, p.H, p.W, p.D, dt);
   if (p.ws == nullptr || p.ws_bytes < l.total) return cudaSuccess;
   A.g = static_cast<char*>(p.ws) + l.g;
@@ -1416,10 +1371,11 @@ cudaError_t launch_bwd_stream(const ScanParams& p0, gspn_dtype_t dt, cudaStream_
   *handled = true;
   cudaError_t e;
   using BF = __nv_bfloat16;
-  if (E == 2)
-    e = dt == GSPN_BF16 ? launch(bwd_stream_kernel<BF, 2, kE2Warps>, A, s) : launch(bwd_stream_kernel<float, 2, kE2Warps>, A, s);
+  const bool pre = p.flags & GSPN_FLAG_PRENORMALIZED;
+  if (dt == GSPN_BF16)
+    e = pre ? launch(bwd_stream_kernel<BF, true>, A, s) : launch(bwd_stream_kernel<BF, false>, A, s);
   else
-    e = dt == GSPN_BF16 ? launch(bwd_stream_kernel<BF, 4, kEdgeW>, A, s) : launch(bwd_stream_kernel<float, 4, kEdgeW>, A, s);
+    e = pre ? launch(bwd_stream_kernel<float, true>, A, s) : launch(bwd_stream_kernel<float, false>, A, s);
   *launches += 1;
   if (e != cudaSuccess) return e;
   const bool per_channel = p.G == p.C;

@@ -37,6 +37,15 @@ SHAPES = [
     (1, 2, 2, 256, 256, 0xF, "bf16"),
     (1, 3, 3, 512, 512, 0xF, "bf16"),
     (1, 2, 1, 200, 136, 0xF, "bf16"),
+    # stream-path ragged cases: partial first/last tiles, P not a multiple of a warp's span,
+    # P near the 512-position tile, tiny P against large L
+    (2, 3, 3, 100, 72, 0xF, "bf16"),
+    (1, 4, 2, 37, 24, 0xF, "bf16"),
+    (2, 2, 2, 19, 12, 0xF, "f32"),
+    (1, 2, 2, 512, 8, 0xF, "bf16"),
+    (1, 2, 1, 8, 512, 0xF, "f32"),
+    (1, 2, 2, 500, 504, 0xF, "bf16"),
+    (1, 1, 1, 250, 248, 0xF, "bf16"),
 ]
 FLAGS = [0, gspn.FLAG_FORCE_GENERIC]
 
@@ -105,7 +114,9 @@ def test_bwd_parity_given_h(shape, flags, cuda_device, oracle_cache):
 @pytest.mark.parametrize("shape", SHAPES, ids=_ids)
 def test_fwd_bwd_end_to_end(shape, cuda_device, oracle_cache):
     B, C, G, H, W, dirs, dtype = shape
-    cfg, inp, _, _, _, g_ref = _oracle(shape, oracle_cache)
+    # reference: the oracle backward on the oracle forward state rounded to the I/O dtype (DESIGN R18:
+    # h is stored in the I/O dtype, the backward is defined on the stored h)
+    cfg, inp, _, _, g_ref, _ = _oracle(shape, oracle_cache)
     t = _upload(inp, dtype, cuda_device)
     h = gspn.fwd(t["x"], t["w_l"], t["w_m"], t["w_r"], t["lam"], dirs, G)
     outs = gspn.bwd(t["x"], t["w_l"], t["w_m"], t["w_r"], t["lam"], h, t["dh"], dirs, G)
