@@ -1157,6 +1157,185 @@ cudaError_t launch_out_pc(const ScanParams& p, const void* g, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// ---- TMA-staged output kernel (G = C): a work unit is (b, c, RB image rows); the producer warp loads
+// the unit's x, and per direction g, lam, w_l, w_m, w_r (RB rows) and h (RB + 2 rows: the halo rows
+// i0-1 and i0+RB come from TMA, out-of-range rows as zero fill = h_{-1} = 0) into a shared-memory
+// ring; 8 consumer warps compute from shared memory and store straight to global memory. Loads in
+// flight no longer cost registers (the register-staged kernel was latency-bound at 2 CTAs/SM).
+struct OutArgs {
+  CUtensorMap x, g, lam, wl, wm, wr, h;
+  ScanParams p;
+  int RB, BX, nbx, nstages, nrb;
+  uint32_t box_rb, box_h;                            // bytes per TMA box (padded to 128)
+  uint32_t tile_rb, tile_h, per_k, stage_bytes, tx;  // bytes
+  int64_t nunits;
+};
+
+constexpr int kOutConsumers = 16;
+
+// element (r, c) of a [box][rows][BX] tile whose boxes are bstride bytes apart
+template <typename T>
+__device__ __forceinline__ float sm_ld(const uint8_t* tile, uint32_t bstride, int BX, int r, int c) {
+  const int b = c / BX;
+  return to_f(*reinterpret_cast<const T*>(tile + b * bstride + (r * BX + (c - b * BX)) * sizeof(T)));
+}
+
+template <typename T>
+__device__ __forceinline__ void sm_ld4(const uint8_t* tile, uint32_t bstride, int BX, int r, int c, float (&v)[4]) {
+  const int b = c / BX;  // 4 | BX and c % 4 == 0: the 4 elements sit in one box row
+  const uint8_t* p = tile + b * bstride + (r * BX + (c - b * BX)) * sizeof(T);
+  if constexpr (sizeof(T) == 2) {
+    const uint2 u = *reinterpret_cast<const uint2*>(p);
+    v[0] = __uint_as_float(u.x << 16); v[1] = __uint_as_float(u.x & 0xFFFF0000u);
+    v[2] = __uint_as_float(u.y << 16); v[3] = __uint_as_float(u.y & 0xFFFF0000u);
+  } else {
+    const float4 u = *reinterpret_cast<const float4*>(p);
+    v[0] = u.x; v[1] = u.y; v[2] = u.z; v[3] = u.w;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__((kOutConsumers + 1) * 32, 1) bwd_out_tma_kernel(const __grid_constant__ OutArgs A) {
+  constexpr int V = 4;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* ring = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + static_cast<size_t>(A.nstages) * A.stage_bytes);
+  uint64_t* empty = full + A.nstages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const ScanParams& p = A.p;
+  const int D = p.D, RB = A.RB, BX = A.BX;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < A.nstages; ++s) {
+      mbar_init(smem_u32(&full[s]), 1);
+      mbar_init(smem_u32(&empty[s]), kOutConsumers);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == kOutConsumers) {  // producer
+    if (lane == 0) {
+      const uint64_t pol = policy_of(0);  // every input is read once
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t u = blockIdx.x; u < A.nunits; u += gridDim.x) {
+        const int64_t bc = u / A.nrb;
+        const int i0 = static_cast<int>(u % A.nrb) * RB;
+        const int64_t b = bc / p.C, c = bc % p.C;
+        mbar_wait_sleep(smem_u32(&empty[stage]), phase ^ 1);
+        const uint32_t fb = smem_u32(&full[stage]);
+        mbar_arrive_tx(fb, A.tx);
+        const uint32_t st = smem_u32(ring + static_cast<size_t>(stage) * A.stage_bytes);
+        const uint32_t box_rb = A.box_rb, box_h = A.box_h;
+        for (int bx = 0; bx < A.nbx; ++bx) tma_load3(st + bx * box_rb, &A.x, bx * BX, i0, static_cast<int>(bc), fb, pol);
+        for (int k = 0; k < D; ++k) {
+          const int chain = static_cast<int>((static_cast<int64_t>(k) * p.B + b) * p.C + c);
+          const uint32_t base = st + A.tile_rb + k * A.per_k;
+          for (int bx = 0; bx < A.nbx; ++bx) {
+            tma_load3(base + 0 * A.tile_rb + bx * box_rb, &A.g, bx * BX, i0, chain, fb, pol);
+            tma_load3(base + 1 * A.tile_rb + bx * box_rb, &A.lam, bx * BX, i0, chain, fb, pol);
+            tma_load3(base + 2 * A.tile_rb + bx * box_rb, &A.wl, bx * BX, i0, chain, fb, pol);
+            tma_load3(base + 3 * A.tile_rb + bx * box_rb, &A.wm, bx * BX, i0, chain, fb, pol);
+            tma_load3(base + 4 * A.tile_rb + bx * box_rb, &A.wr, bx * BX, i0, chain, fb, pol);
+            tma_load3(base + 5 * A.tile_rb + bx * box_h, &A.h, bx * BX, i0 - 1, chain, fb, policy_of(1));
+          }
+        }
+        if (++stage == A.nstages) { stage = 0; phase ^= 1; }
+      }
+    }
+    return;
+  }
+  const bool prenorm = p.flags & GSPN_FLAG_PRENORMALIZED;
+  const int64_t H = p.H, W = p.W, HW = H * W;
+  const int nchunk = static_cast<int>(W / V);
+  const int nthreads = kOutConsumers * 32;
+  int stage = 0;
+  uint32_t phase = 0;
+  for (int64_t u = blockIdx.x; u < A.nunits; u += gridDim.x) {
+    const int64_t bc = u / A.nrb;
+    const int i0 = static_cast<int>(u % A.nrb) * RB;
+    const int64_t b = bc / p.C, c = bc % p.C;
+    mbar_wait(smem_u32(&full[stage]), phase);
+    const uint8_t* st = ring + static_cast<size_t>(stage) * A.stage_bytes;
+    for (int idx = threadIdx.x; idx < RB * nchunk; idx += nthreads) {
+      const int r = idx / nchunk;
+      const int j0 = (idx - r * nchunk) * V;
+      const int64_t i = i0 + r;
+      if (i >= H) continue;
+      const int64_t rowoff = i * W + j0;
+      float xv[V], dx[V];
+      sm_ld4<T>(st, A.box_rb, BX, r, j0, xv);
+#pragma unroll
+      for (int q = 0; q < V; ++q) dx[q] = 0.f;
+      for (int k = 0; k < D; ++k) {
+        const uint8_t* base = st + A.tile_rb + k * A.per_k;
+        const uint8_t* ht = base + 5 * A.tile_rb;
+        const uint32_t dir = p.dirbit[k];
+        const bool vert = dir == GSPN_DIR_T2B || dir == GSPN_DIR_B2T;
+        const int64_t off = ((static_cast<int64_t>(k) * p.B + b) * p.C + c) * HW + rowoff;
+        float gv[V], lv[V], dl[V], Da[V], Db[V], Dc[V];
+        sm_ld4<T>(base, A.box_rb, BX, r, j0, gv);
+        sm_ld4<T>(base + A.tile_rb, A.box_rb, BX, r, j0, lv);
+#pragma unroll
+        for (int q = 0; q < V; ++q) {
+          dl[q] = gv[q] * xv[q];
+          dx[q] = fmaf(gv[q], lv[q], dx[q]);
+        }
+        GVec<T, V>::store(static_cast<T*>(p.dlam) + off, dl);
+        if (vert) {
+          // h_{t-1}: row i-1 (T2B) / i+1 (B2T) = halo-tile row r / r+2; neighbours = columns j+-1
+          const int rr = dir == GSPN_DIR_T2B ? r : r + 2;
+          float v[V];
+          sm_ld4<T>(ht, A.box_h, BX, rr, j0, v);
+          const float lo = j0 > 0 ? sm_ld<T>(ht, A.box_h, BX, rr, j0 - 1) : 0.f;
+          const float hi = j0 + V < W ? sm_ld<T>(ht, A.box_h, BX, rr, j0 + V) : 0.f;
+#pragma unroll
+          for (int q = 0; q < V; ++q) {
+            Da[q] = gv[q] * (q > 0 ? v[q - 1] : lo);
+            Db[q] = gv[q] * v[q];
+            Dc[q] = gv[q] * (q + 1 < V ? v[q + 1] : hi);
+          }
+        } else {
+          // h_{t-1}: column j-1 (L2R) / j+1 (R2L); neighbours = rows i-1, i, i+1 = halo rows r..r+2
+          const bool l2r = dir == GSPN_DIR_L2R;
+          const int col = l2r ? j0 - 1 : j0 + V;
+          const bool col_ok = col >= 0 && col < W;
+          float* Dr[3] = {Da, Db, Dc};
+#pragma unroll
+          for (int rr = 0; rr < 3; ++rr) {
+            float v[V];
+            sm_ld4<T>(ht, A.box_h, BX, r + rr, j0, v);
+            const float e = col_ok ? sm_ld<T>(ht, A.box_h, BX, r + rr, col) : 0.f;
+#pragma unroll
+            for (int q = 0; q < V; ++q) {
+              const float sh = l2r ? (q > 0 ? v[q - 1] : e) : (q + 1 < V ? v[q + 1] : e);
+              Dr[rr][q] = gv[q] * sh;
+            }
+          }
+        }
+        float wl[V], wm[V], wr[V], ol[V], om[V], orr[V];
+        sm_ld4<T>(base + 2 * A.tile_rb, A.box_rb, BX, r, j0, wl);
+        sm_ld4<T>(base + 3 * A.tile_rb, A.box_rb, BX, r, j0, wm);
+        sm_ld4<T>(base + 4 * A.tile_rb, A.box_rb, BX, r, j0, wr);
+        const int64_t P = vert ? W : H;
+#pragma unroll
+        for (int q = 0; q < V; ++q) {
+          const int64_t rp = vert ? j0 + q : i;
+          const bool hl = rp >= 1, hr = rp <= P - 2;
+          jacobian<true>(wl[q], wm[q], wr[q], hl, hr, prenorm, hl ? Da[q] : 0.f, Db[q], hr ? Dc[q] : 0.f, ol[q], om[q],
+                         orr[q]);
+        }
+        GVec<T, V>::store(static_cast<T*>(p.dwl) + off, ol);
+        GVec<T, V>::store(static_cast<T*>(p.dwm) + off, om);
+        GVec<T, V>::store(static_cast<T*>(p.dwr) + off, orr);
+      }
+      GVec<T, V>::store(static_cast<T*>(p.dx) + bc * HW + rowoff, dx);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(smem_u32(&empty[stage]));
+    if (++stage == A.nstages) { stage = 0; phase ^= 1; }
+  }
+}
+
 template <typename T, int V, bool kPerChannel>
 cudaError_t launch_out(const ScanParams& p, const void* g, cudaStream_t s) {
   constexpr int R = 8;
@@ -1351,6 +1530,65 @@ cudaError_t launch_fwd_stream(const ScanParams& p, gspn_dtype_t dt, cudaStream_t
   return e;
 }
 
+// TMA-staged output kernel (G = C). Returns false if the shape does not fit (caller falls back).
+bool launch_out_tma(const ScanParams& p, const void* g, gspn_dtype_t dt, cudaStream_t s, cudaError_t* err) {
+  static OutArgs A;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  if (getenv("GSPN_OUT_REG")) return false;  // experiments: register-staged kernel
+  memset(&A, 0, sizeof A);
+  A.p = p;
+  const int es = dt == GSPN_BF16 ? 2 : 4;
+  A.BX = static_cast<int>(std::min<int64_t>(p.W, 256));
+  A.nbx = static_cast<int>((p.W + A.BX - 1) / A.BX);
+  const int D = static_cast<int>(p.D);
+  const int budget = smem_optin() - 1024 - 256;
+  auto pad = [](int64_t v) { return (v + 127) / 128 * 128; };
+  auto stage_of = [&](int rb) {
+    return A.nbx * (pad(es * A.BX * rb) * (1 + 5 * D) + pad(es * A.BX * (rb + 2)) * D);
+  };
+  // enough rows per unit to give every consumer thread a 4-column chunk, 2+ stages
+  int RB = 1;
+  while (RB < 16 && RB * (p.W / 4) < kOutConsumers * 32) RB <<= 1;
+  while (RB > 1 && 2 * stage_of(RB) > budget) RB >>= 1;
+  if (2 * stage_of(RB) > budget) return false;
+  A.RB = RB;
+  A.box_rb = static_cast<uint32_t>(pad(es * A.BX * RB));
+  A.box_h = static_cast<uint32_t>(pad(es * A.BX * (RB + 2)));
+  A.tile_rb = A.nbx * A.box_rb;
+  A.tile_h = A.nbx * A.box_h;
+  A.per_k = 5 * A.tile_rb + A.tile_h;
+  A.stage_bytes = A.tile_rb + D * A.per_k;
+  A.tx = static_cast<uint32_t>(A.nbx * (es * A.BX * RB * (1 + 5 * D) + es * A.BX * (RB + 2) * D));  // TMA payload
+  A.nstages = static_cast<int>(std::min<int64_t>(6, budget / A.stage_bytes));
+  A.nrb = static_cast<int>((p.H + RB - 1) / RB);
+  A.nunits = p.B * p.C * A.nrb;
+  const int64_t nc = p.D * p.B * p.C;
+  bool ok = encode(&A.x, p.x, dt, p.W, p.H, p.B * p.C, A.BX, RB, false) &&
+            encode(&A.g, g, dt, p.W, p.H, nc, A.BX, RB, false) &&
+            encode(&A.lam, p.lam, dt, p.W, p.H, nc, A.BX, RB, false) &&
+            encode(&A.wl, p.wl, dt, p.W, p.H, nc, A.BX, RB, false) &&
+            encode(&A.wm, p.wm, dt, p.W, p.H, nc, A.BX, RB, false) &&
+            encode(&A.wr, p.wr, dt, p.W, p.H, nc, A.BX, RB, false) &&
+            encode(&A.h, p.h, dt, p.W, p.H, nc, A.BX, RB + 2, false);
+  if (!ok) return false;
+  const uint32_t smem = 1024 + A.nstages * A.stage_bytes + 2 * 8 * A.nstages;
+  auto kern = dt == GSPN_BF16 ? bwd_out_tma_kernel<__nv_bfloat16> : bwd_out_tma_kernel<float>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e == cudaSuccess) {
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (kOutConsumers + 1) * 32, smem);
+    if (e == cudaSuccess) {
+      int64_t grid = static_cast<int64_t>(sm_count()) * std::max(per_sm, 1);
+      if (grid > A.nunits) grid = A.nunits;
+      kern<<<static_cast<unsigned>(grid), (kOutConsumers + 1) * 32, smem, s>>>(A);
+      e = cudaGetLastError();
+    }
+  }
+  *err = e;
+  return true;
+}
+
 cudaError_t launch_bwd_stream(const ScanParams& p0, gspn_dtype_t dt, cudaStream_t s, int* launches, bool* handled) {
   *handled = false;
   static StreamArgs A;
@@ -1379,6 +1617,10 @@ cudaError_t launch_bwd_stream(const ScanParams& p0, gspn_dtype_t dt, cudaStream_
   *launches += 1;
   if (e != cudaSuccess) return e;
   const bool per_channel = p.G == p.C;
+  if (per_channel && launch_out_tma(p, A.g, dt, s, &e)) {
+    *launches += 1;
+    return e;
+  }
   if (dt == GSPN_BF16)
     e = per_channel ? launch_out_pc<BF, 4>(p, A.g, s) : launch_out<BF, 4, false>(p, A.g, s);
   else
