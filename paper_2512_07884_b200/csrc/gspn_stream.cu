@@ -1173,17 +1173,9 @@ struct OutArgs {
 
 constexpr int kOutConsumers = 16;
 
-// element (r, c) of a [box][rows][BX] tile whose boxes are bstride bytes apart
+// 4 consecutive elements at a shared-memory address (8- or 16-byte aligned).
 template <typename T>
-__device__ __forceinline__ float sm_ld(const uint8_t* tile, uint32_t bstride, int BX, int r, int c) {
-  const int b = c / BX;
-  return to_f(*reinterpret_cast<const T*>(tile + b * bstride + (r * BX + (c - b * BX)) * sizeof(T)));
-}
-
-template <typename T>
-__device__ __forceinline__ void sm_ld4(const uint8_t* tile, uint32_t bstride, int BX, int r, int c, float (&v)[4]) {
-  const int b = c / BX;  // 4 | BX and c % 4 == 0: the 4 elements sit in one box row
-  const uint8_t* p = tile + b * bstride + (r * BX + (c - b * BX)) * sizeof(T);
+__device__ __forceinline__ void sm_ld4v(const uint8_t* p, float (&v)[4]) {
   if constexpr (sizeof(T) == 2) {
     const uint2 u = *reinterpret_cast<const uint2*>(p);
     v[0] = __uint_as_float(u.x << 16); v[1] = __uint_as_float(u.x & 0xFFFF0000u);
@@ -1246,14 +1238,16 @@ __global__ void __launch_bounds__((kOutConsumers + 1) * 32, 1) bwd_out_tma_kerne
   }
   const bool prenorm = p.flags & GSPN_FLAG_PRENORMALIZED;
   const int64_t H = p.H, W = p.W, HW = H * W;
+  const int64_t kstride = p.B * p.C * HW;  // between direction slabs of lam / g / h / w (G = C) / outputs
   const int nchunk = static_cast<int>(W / V);
   const int nthreads = kOutConsumers * 32;
+  constexpr int es = static_cast<int>(sizeof(T));
+  const uint32_t rowb = static_cast<uint32_t>(BX * es);  // bytes per box row
   int stage = 0;
   uint32_t phase = 0;
   for (int64_t u = blockIdx.x; u < A.nunits; u += gridDim.x) {
     const int64_t bc = u / A.nrb;
     const int i0 = static_cast<int>(u % A.nrb) * RB;
-    const int64_t b = bc / p.C, c = bc % p.C;
     mbar_wait(smem_u32(&full[stage]), phase);
     const uint8_t* st = ring + static_cast<size_t>(stage) * A.stage_bytes;
     for (int idx = threadIdx.x; idx < RB * nchunk; idx += nthreads) {
@@ -1261,9 +1255,17 @@ __global__ void __launch_bounds__((kOutConsumers + 1) * 32, 1) bwd_out_tma_kerne
       const int j0 = (idx - r * nchunk) * V;
       const int64_t i = i0 + r;
       if (i >= H) continue;
-      const int64_t rowoff = i * W + j0;
+      // byte offsets of this chunk inside a [box][rows][BX] tile (computed once per chunk)
+      const int bx = j0 >= BX ? j0 / BX : 0;
+      const uint32_t col = static_cast<uint32_t>((j0 - bx * BX) * es);
+      const uint32_t orb = bx * A.box_rb + r * rowb + col;     // RB-row tiles, row r
+      const uint32_t oh = bx * A.box_h + r * rowb + col;       // halo tile, halo row r (= image row i-1)
+      const bool has_lo = j0 > 0, has_hi = j0 + V < W;
+      const uint32_t ohl = (j0 - bx * BX) > 0 ? oh - es : (bx - 1) * A.box_h + r * rowb + (BX - 1) * es;  // column j0-1
+      const uint32_t ohh = (j0 - bx * BX) + V < BX ? oh + V * es : (bx + 1) * A.box_h + r * rowb;          // column j0+V
+      const int64_t off0 = bc * HW + i * W + j0;  // x / dx; direction k adds k * kstride (chain k, b, c)
       float xv[V], dx[V];
-      sm_ld4<T>(st, A.box_rb, BX, r, j0, xv);
+      sm_ld4v<T>(st + orb, xv);
 #pragma unroll
       for (int q = 0; q < V; ++q) dx[q] = 0.f;
       for (int k = 0; k < D; ++k) {
@@ -1271,10 +1273,10 @@ __global__ void __launch_bounds__((kOutConsumers + 1) * 32, 1) bwd_out_tma_kerne
         const uint8_t* ht = base + 5 * A.tile_rb;
         const uint32_t dir = p.dirbit[k];
         const bool vert = dir == GSPN_DIR_T2B || dir == GSPN_DIR_B2T;
-        const int64_t off = ((static_cast<int64_t>(k) * p.B + b) * p.C + c) * HW + rowoff;
+        const int64_t off = off0 + k * kstride;
         float gv[V], lv[V], dl[V], Da[V], Db[V], Dc[V];
-        sm_ld4<T>(base, A.box_rb, BX, r, j0, gv);
-        sm_ld4<T>(base + A.tile_rb, A.box_rb, BX, r, j0, lv);
+        sm_ld4v<T>(base + orb, gv);
+        sm_ld4v<T>(base + A.tile_rb + orb, lv);
 #pragma unroll
         for (int q = 0; q < V; ++q) {
           dl[q] = gv[q] * xv[q];
@@ -1282,12 +1284,12 @@ __global__ void __launch_bounds__((kOutConsumers + 1) * 32, 1) bwd_out_tma_kerne
         }
         GVec<T, V>::store(static_cast<T*>(p.dlam) + off, dl);
         if (vert) {
-          // h_{t-1}: row i-1 (T2B) / i+1 (B2T) = halo-tile row r / r+2; neighbours = columns j+-1
-          const int rr = dir == GSPN_DIR_T2B ? r : r + 2;
+          // h_{t-1}: image row i-1 (T2B) / i+1 (B2T) = halo row r / r+2; neighbours = columns j+-1
+          const uint32_t ro = dir == GSPN_DIR_T2B ? 0u : 2u * rowb;
           float v[V];
-          sm_ld4<T>(ht, A.box_h, BX, rr, j0, v);
-          const float lo = j0 > 0 ? sm_ld<T>(ht, A.box_h, BX, rr, j0 - 1) : 0.f;
-          const float hi = j0 + V < W ? sm_ld<T>(ht, A.box_h, BX, rr, j0 + V) : 0.f;
+          sm_ld4v<T>(ht + oh + ro, v);
+          const float lo = has_lo ? to_f(*reinterpret_cast<const T*>(ht + ohl + ro)) : 0.f;
+          const float hi = has_hi ? to_f(*reinterpret_cast<const T*>(ht + ohh + ro)) : 0.f;
 #pragma unroll
           for (int q = 0; q < V; ++q) {
             Da[q] = gv[q] * (q > 0 ? v[q - 1] : lo);
@@ -1295,16 +1297,16 @@ __global__ void __launch_bounds__((kOutConsumers + 1) * 32, 1) bwd_out_tma_kerne
             Dc[q] = gv[q] * (q + 1 < V ? v[q + 1] : hi);
           }
         } else {
-          // h_{t-1}: column j-1 (L2R) / j+1 (R2L); neighbours = rows i-1, i, i+1 = halo rows r..r+2
+          // h_{t-1}: column j-1 (L2R) / j+1 (R2L); neighbours = image rows i-1, i, i+1 = halo rows r..r+2
           const bool l2r = dir == GSPN_DIR_L2R;
-          const int col = l2r ? j0 - 1 : j0 + V;
-          const bool col_ok = col >= 0 && col < W;
+          const bool e_ok = l2r ? has_lo : has_hi;
+          const uint32_t oe = l2r ? ohl : ohh;
           float* Dr[3] = {Da, Db, Dc};
 #pragma unroll
           for (int rr = 0; rr < 3; ++rr) {
             float v[V];
-            sm_ld4<T>(ht, A.box_h, BX, r + rr, j0, v);
-            const float e = col_ok ? sm_ld<T>(ht, A.box_h, BX, r + rr, col) : 0.f;
+            sm_ld4v<T>(ht + oh + rr * rowb, v);
+            const float e = e_ok ? to_f(*reinterpret_cast<const T*>(ht + oe + rr * rowb)) : 0.f;
 #pragma unroll
             for (int q = 0; q < V; ++q) {
               const float sh = l2r ? (q > 0 ? v[q - 1] : e) : (q + 1 < V ? v[q + 1] : e);
@@ -1313,22 +1315,26 @@ __global__ void __launch_bounds__((kOutConsumers + 1) * 32, 1) bwd_out_tma_kerne
           }
         }
         float wl[V], wm[V], wr[V], ol[V], om[V], orr[V];
-        sm_ld4<T>(base + 2 * A.tile_rb, A.box_rb, BX, r, j0, wl);
-        sm_ld4<T>(base + 3 * A.tile_rb, A.box_rb, BX, r, j0, wm);
-        sm_ld4<T>(base + 4 * A.tile_rb, A.box_rb, BX, r, j0, wr);
-        const int64_t P = vert ? W : H;
+        sm_ld4v<T>(base + 2 * A.tile_rb + orb, wl);
+        sm_ld4v<T>(base + 3 * A.tile_rb + orb, wm);
+        sm_ld4v<T>(base + 4 * A.tile_rb + orb, wr);
+        if (vert) {
 #pragma unroll
-        for (int q = 0; q < V; ++q) {
-          const int64_t rp = vert ? j0 + q : i;
-          const bool hl = rp >= 1, hr = rp <= P - 2;
-          jacobian<true>(wl[q], wm[q], wr[q], hl, hr, prenorm, hl ? Da[q] : 0.f, Db[q], hr ? Dc[q] : 0.f, ol[q], om[q],
-                         orr[q]);
+          for (int q = 0; q < V; ++q) {
+            const bool hl = j0 + q >= 1, hr = j0 + q <= W - 2;
+            jacobian<true>(wl[q], wm[q], wr[q], hl, hr, prenorm, Da[q], Db[q], Dc[q], ol[q], om[q], orr[q]);
+          }
+        } else {
+          const bool hl = i >= 1, hr = i <= H - 2;
+#pragma unroll
+          for (int q = 0; q < V; ++q)
+            jacobian<true>(wl[q], wm[q], wr[q], hl, hr, prenorm, Da[q], Db[q], Dc[q], ol[q], om[q], orr[q]);
         }
         GVec<T, V>::store(static_cast<T*>(p.dwl) + off, ol);
         GVec<T, V>::store(static_cast<T*>(p.dwm) + off, om);
         GVec<T, V>::store(static_cast<T*>(p.dwr) + off, orr);
       }
-      GVec<T, V>::store(static_cast<T*>(p.dx) + bc * HW + rowoff, dx);
+      GVec<T, V>::store(static_cast<T*>(p.dx) + off0, dx);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(smem_u32(&empty[stage]));
