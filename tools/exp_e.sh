@@ -1,0 +1,10 @@
+#!/bin/bash
+bash tools/gpu_check.sh
+M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum
+for E in 2 4; do
+  GSPN_E=$E timeout 300 ncu --metrics $M --clock-control none -k regex:"stream_kernel|out_" -s 3 -c 3 --csv \
+    python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline 2>/dev/null | grep -E "stream_kernel|out_" > gpurun_out/exp_e$E.csv
+done
+GSPN_NULL=1 timeout 300 ncu --metrics $M --clock-control none -k regex:"stream_kernel|out_" -s 3 -c 3 --csv \
+    python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline 2>/dev/null | grep -E "stream_kernel|out_" > gpurun_out/exp_e4null.csv
+bash tools/profile.sh
