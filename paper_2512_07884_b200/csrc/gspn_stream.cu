@@ -81,6 +81,12 @@ struct Plan {
   int bw, nbw;         // vertical TMA box width (positions) and box count
   int bh, nbh;         // horizontal TMA box height (rows) and box count
   int nin;             // input tensors per tile
+  // chain packing (G = C, max(H, W) <= kPpad / 2): npack chains of one direction side by side in a
+  // tile, positions c * psub + r; vertical packed tiles are [K][npack][W] (one 3D box), horizontal
+  // [npack][H][32 B]. Unpacked: npack = 1, vertical tiles [box][K][kRowB].
+  int npack;
+  int64_t nbc;         // B * C planes
+  uint32_t vstep;      // bytes between consecutive steps of a vertical tile (kRowB, or npack W s)
   int nstages;
   uint32_t tile_bytes;   // one tensor's tile: K * ppad * es (= 32 * ppad)
   uint32_t stage_bytes;  // nin * tile_bytes
@@ -148,13 +154,14 @@ template <> struct Pk<float> {
 struct Chain {
   int k;            // direction slab
   bool vert, rev;   // orientation; reversed step order in canonical coordinates (B2T, R2L)
-  int64_t bc, chain, wplane;
+  int64_t bc, chain, wplane;  // first plane of the (pack of) chain(s): x, lam/h/dh, w
   int L, P, ntiles;
+  int psub, nvalid;           // positions per chain; chains of the pack that exist
 };
 
-__device__ __forceinline__ Chain make_chain(const ScanParams& p, int K, int64_t w) {
+__device__ __forceinline__ Chain make_chain(const ScanParams& p, const Plan& pl, int64_t w) {
   Chain ch;
-  const int64_t bc = w / p.D;
+  const int64_t bc = (w / p.D) * pl.npack;
   // Round i of the persistent grid covers slots [i G, (i+1) G): whole planes when D divides G. The
   // direction is rotated by i so every CTA cycles through all D directions (vertical and horizontal
   // chains run at different speeds; a fixed direction per CTA would leave the fast ones idle).
@@ -168,8 +175,10 @@ __device__ __forceinline__ Chain make_chain(const ScanParams& p, int K, int64_t 
   ch.chain = (ch.k * p.B + b) * p.C + c;
   ch.wplane = (ch.k * p.B + b) * p.G + g;
   ch.L = static_cast<int>(ch.vert ? p.H : p.W);
-  ch.P = static_cast<int>(ch.vert ? p.W : p.H);
-  ch.ntiles = (ch.L + K - 1) / K;
+  ch.psub = static_cast<int>(ch.vert ? p.W : p.H);
+  ch.P = ch.psub * pl.npack;
+  ch.nvalid = static_cast<int>(pl.nbc - bc < pl.npack ? pl.nbc - bc : pl.npack);
+  ch.ntiles = (ch.L + pl.K - 1) / pl.K;
   return ch;
 }
 
@@ -204,7 +213,7 @@ __device__ void producer_loop(const StreamArgs& A, uint8_t* ring, uint64_t* full
   int stage = 0;
   uint32_t phase = 0;
   for (int64_t w = blockIdx.x; w < pl.nchains; w += gridDim.x) {
-    const Chain ch = make_chain(A.p, pl.K, w);
+    const Chain ch = make_chain(A.p, pl, w);
     const int o = ch.vert ? 0 : 1;
     for (int jj = 0; jj < ch.ntiles; ++jj) {
       const int j = kBwd ? (ch.ntiles - 1 - jj) : jj;
@@ -218,7 +227,10 @@ __device__ void producer_loop(const StreamArgs& A, uint8_t* ring, uint64_t* full
         // x is re-read by the plane's other directions; vertical streams are read exactly once
         const uint64_t pol = (!kBwd && t == F_X) ? pol_xin : (ch.vert ? pol_vin : pol_hin);
         const uint32_t dst = st + t * pl.tile_bytes;
-        if (ch.vert) {
+        if (pl.npack > 1) {  // one 3D box: vertical (W, planes, rows), horizontal (cols, H, planes)
+          if (ch.vert) tma_load3(dst, &A.in[0][t], 0, plane, s0, fb, pol);
+          else tma_load3(dst, &A.in[1][t], s0, 0, plane, fb, pol);
+        } else if (ch.vert) {
           for (int q = 0; q < pl.nbw; ++q)
             tma_load3(dst + q * pl.K * pl.bw * pl.es, &A.in[o][t], q * pl.bw, s0, plane, fb, pol);
         } else {
@@ -241,7 +253,7 @@ __device__ void storer_loop(const StreamArgs& A, uint8_t* ring, uint64_t* done, 
   int stage = 0;
   uint32_t phase = 0;
   for (int64_t w = blockIdx.x; w < pl.nchains; w += gridDim.x) {
-    const Chain ch = make_chain(A.p, pl.K, w);
+    const Chain ch = make_chain(A.p, pl, w);
     for (int jj = 0; jj < ch.ntiles; ++jj) {
       const int j = bwd ? (ch.ntiles - 1 - jj) : jj;
       mbar_wait(smem_u32(&done[stage]), phase);
@@ -250,8 +262,12 @@ __device__ void storer_loop(const StreamArgs& A, uint8_t* ring, uint64_t* done, 
         const uint8_t* st = ring + static_cast<size_t>(stage) * pl.stage_bytes;
         for (int t = 0; t < nout; ++t) {
           const uint32_t src = smem_u32(st + static_cast<size_t>(slots[t]) * pl.tile_bytes);
-          for (int q = 0; q < pl.nbh; ++q)
-            tma_store3(&A.out[1][t], src + q * pl.bh * 32, s0, q * pl.bh, static_cast<int>(ch.chain), pol);
+          if (pl.npack > 1) {
+            tma_store3(&A.out[1][t], src, s0, 0, static_cast<int>(ch.chain), pol);
+          } else {
+            for (int q = 0; q < pl.nbh; ++q)
+              tma_store3(&A.out[1][t], src + q * pl.bh * 32, s0, q * pl.bh, static_cast<int>(ch.chain), pol);
+          }
         }
         bulk_commit();
         bulk_wait_read0();
@@ -292,15 +308,19 @@ struct Lanes {
   bool own_h[kE];        // horizontal: slot owned and inside the tile
   uint32_t voff;         // vertical: byte offset of the lane's positions at kk = 0
   uint32_t hoff[kE];     // horizontal: slot row's byte offset, chunk 0 (chunk c: hoff ^ (c << 4))
-  int pos0;              // vertical: first position
+  int64_t vout;          // vertical: element offset of the lane's first position in row 0 of its plane
   // tap unpack masks [tap l/m/r][element e | slot q][half / (and, or)]
   uint32_t s[3][kE][2];
 };
 
+// r: tile position; psub: positions per chain; nvalid: chains present (packing). A chain's taps at its
+// own first / last position are dropped, which also decouples packed neighbours.
 template <typename T>
-__device__ __forceinline__ void tap_masks(int r, int P, uint32_t (&sl)[2], uint32_t (&sm)[2], uint32_t (&sr)[2],
-                                          int half_for_bf16) {
-  const bool valid = r >= 0 && r < P, kl = valid && r >= 1, kr = valid && r <= P - 2;
+__device__ __forceinline__ void tap_masks(int r, int psub, int nvalid, uint32_t (&sl)[2], uint32_t (&sm)[2],
+                                          uint32_t (&sr)[2], int half_for_bf16) {
+  const bool valid = r >= 0 && r < psub * nvalid;
+  const int rl = valid ? r % psub : 0;
+  const bool kl = valid && rl >= 1, kr = valid && rl <= psub - 2;
   if constexpr (sizeof(T) == 2) {
     // half_for_bf16: -1 -> fill both halves (horizontal slot), 0/1 -> element in the low/high half
     for (int hh = 0; hh < 2; ++hh) {
@@ -318,37 +338,46 @@ __device__ __forceinline__ void tap_masks(int r, int P, uint32_t (&sl)[2], uint3
 }
 
 template <typename T>
-__device__ __forceinline__ Lanes<T> make_lanes(const Plan& pl, const Chain& ch, int wi, int lane) {
+__device__ __forceinline__ Lanes<T> make_lanes(const Plan& pl, const ScanParams& p, const Chain& ch, int wi,
+                                               int lane) {
   using C = Cfg<T>;
   constexpr int WARP = 32 * kE, OWN = WARP - 2 * C::GH;
   Lanes<T> ln;
   ln.A = wi * OWN - C::GH;
   constexpr int lo = C::GH;
+  const int nval = ch.psub * ch.nvalid;
   // vertical
   {
     const int off = kE * lane;
     const int r0 = ln.A + off;
-    ln.pos0 = r0;
-    ln.own_v = off >= lo && off < WARP - C::GH && r0 < ch.P;
+    ln.own_v = off >= lo && off < WARP - C::GH && r0 >= 0 && r0 < nval;
     const int rc = r0 < 0 ? 0 : (r0 > kPpad - kE ? kPpad - kE : r0);
-    const int bw = kRowB / C::es;
-    ln.voff = static_cast<uint32_t>((rc / bw) * (C::K * kRowB) + (rc % bw) * C::es);
+    if (pl.npack > 1) {
+      ln.voff = static_cast<uint32_t>(rc * C::es);
+    } else {
+      const int bw = kRowB / C::es;
+      ln.voff = static_cast<uint32_t>((rc / bw) * (C::K * kRowB) + (rc % bw) * C::es);
+    }
+    const int rv = r0 < 0 ? 0 : r0;
+    ln.vout = (ch.chain + rv / ch.psub) * (p.H * p.W) + rv % ch.psub;  // P % kE == 0: both positions in one chain
   }
   // horizontal
 #pragma unroll
   for (int q = 0; q < kE; ++q) {
     const int off = 32 * q + lane;
     const int r = ln.A + off;
-    ln.own_h[q] = off >= lo && off < WARP - C::GH && r < kPpad;
+    ln.own_h[q] = off >= lo && off < WARP - C::GH && r < kPpad;  // rows >= P: outside the store box
     const uint32_t rc = static_cast<uint32_t>(r < 0 ? 0 : (r >= kPpad ? kPpad - 1 : r));
     ln.hoff[q] = rc * 32 + (((rc >> 2) & 1u) << 4);
   }
   if (ch.vert) {
 #pragma unroll
-    for (int e = 0; e < kE; ++e) tap_masks<T>(ln.A + kE * lane + e, ch.P, ln.s[0][e], ln.s[1][e], ln.s[2][e], e);
+    for (int e = 0; e < kE; ++e)
+      tap_masks<T>(ln.A + kE * lane + e, ch.psub, ch.nvalid, ln.s[0][e], ln.s[1][e], ln.s[2][e], e);
   } else {
 #pragma unroll
-    for (int q = 0; q < kE; ++q) tap_masks<T>(ln.A + 32 * q + lane, ch.P, ln.s[0][q], ln.s[1][q], ln.s[2][q], -1);
+    for (int q = 0; q < kE; ++q)
+      tap_masks<T>(ln.A + 32 * q + lane, ch.psub, ch.nvalid, ln.s[0][q], ln.s[1][q], ln.s[2][q], -1);
   }
   return ln;
 }
@@ -454,6 +483,14 @@ __device__ __forceinline__ Smem carve(uint8_t* smem_raw, const Plan& pl) {
 }
 
 __device__ __forceinline__ void init_barriers(const Smem& m, const Plan& pl) {
+  // Zero the ring once: lanes may read tile rows no TMA box of the chain writes (clamped or packed
+  // tails); those rows must hold finite values (zero, or earlier tiles' data).
+  {
+    uint4* r = reinterpret_cast<uint4*>(m.ring);
+    const uint32_t n = pl.nstages * pl.stage_bytes / 16;
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) r[i] = make_uint4(0u, 0u, 0u, 0u);
+    fence_proxy_async();  // generic-proxy zeros ordered before the TMA (async-proxy) writes
+  }
   if (threadIdx.x == 0) {
     for (int s = 0; s < pl.nstages; ++s) {
       mbar_init(smem_u32(&m.full[s]), 1);       // producer arrive + TMA bytes
@@ -578,13 +615,13 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) fwd_stream_kernel(const
   }
   const uint64_t pol_vout = policy_of(pl.pol[3]);
   const int nthreads = pl.nwc * 32;
-  const int64_t HW = A.p.H * A.p.W, W = A.p.W;
+  const int64_t W = A.p.W;
   int stage = 0, par = 0;
   uint32_t phase = 0;
   for (int64_t w = blockIdx.x; w < pl.nchains; w += gridDim.x) {
-    const Chain ch = make_chain(A.p, C::K, w);
-    const Lanes<T> ln = make_lanes<T>(pl, ch, warp, lane);
-    T* hplane = static_cast<T*>(A.p.hout) + ch.chain * HW;
+    const Chain ch = make_chain(A.p, pl, w);
+    const Lanes<T> ln = make_lanes<T>(pl, A.p, ch, warp, lane);
+    T* hout = static_cast<T*>(A.p.hout) + ln.vout;
     float h[kE] = {0.f, 0.f};
     for (int j = 0; j < ch.ntiles; ++j) {
       mbar_wait(smem_u32(&m.full[stage]), phase);
@@ -599,9 +636,9 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) fwd_stream_kernel(const
             const int t0 = j * C::K + half * C::KS;
             const int kk0 = ch.rev ? C::K - 1 - half * C::KS : half * C::KS;
             const int row0 = ch.rev ? ch.L - 1 - t0 : t0;
-            fwd_half_vert<T, kPre>(ln, st + ln.voff + kk0 * kRowB, ch.rev ? -kRowB : kRowB,
-                                   hplane + static_cast<int64_t>(row0) * W + ln.pos0, ch.rev ? -W : W, t0, ch.L, h,
-                                   pol_vout);
+            const int vs = static_cast<int>(pl.vstep);
+            fwd_half_vert<T, kPre>(ln, st + ln.voff + kk0 * vs, ch.rev ? -vs : vs,
+                                   hout + static_cast<int64_t>(row0) * W, ch.rev ? -W : W, t0, ch.L, h, pol_vout);
           } else if (ch.rev) {
             fwd_half_horiz<T, kPre, true>(ln, st, cm, lane, h, OUT);
           } else {
@@ -726,13 +763,13 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_stream_kernel(const
   const uint64_t pol_vout = policy_of(pl.pol[3]);
   const int nthreads = pl.nwc * 32;
   constexpr int kEdgeArr = 2 * kEdgeW * 2 * 8;
-  const int64_t HW = A.p.H * A.p.W, W = A.p.W;
+  const int64_t W = A.p.W;
   int stage = 0, par = 0;
   uint32_t phase = 0;
   for (int64_t w = blockIdx.x; w < pl.nchains; w += gridDim.x) {
-    const Chain ch = make_chain(A.p, C::K, w);
-    const Lanes<T> ln = make_lanes<T>(pl, ch, warp, lane);
-    T* gplane = static_cast<T*>(A.g) + ch.chain * HW;
+    const Chain ch = make_chain(A.p, pl, w);
+    const Lanes<T> ln = make_lanes<T>(pl, A.p, ch, warp, lane);
+    T* gout = static_cast<T*>(A.g) + ln.vout;
     BwdState S;
 #pragma unroll
     for (int e = 0; e < kE; ++e) S.ea[e] = S.eb[e] = S.ec[e] = 0.f;
@@ -751,9 +788,9 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_stream_kernel(const
             const int tl = t0 + C::KS - 1;                     // processed first
             const int kkl = ch.rev ? C::K - 1 - (half * C::KS + C::KS - 1) : half * C::KS + C::KS - 1;
             const int rowl = ch.rev ? ch.L - 1 - tl : tl;
-            bwd_half_vert<T, kPre>(ln, st + ln.voff + kkl * kRowB, ch.rev ? kRowB : -kRowB,
-                                   gplane + static_cast<int64_t>(rowl) * W + ln.pos0, ch.rev ? W : -W, t0, ch.L, S,
-                                   pol_vout);
+            const int vs = static_cast<int>(pl.vstep);
+            bwd_half_vert<T, kPre>(ln, st + ln.voff + kkl * vs, ch.rev ? vs : -vs,
+                                   gout + static_cast<int64_t>(rowl) * W, ch.rev ? W : -W, t0, ch.L, S, pol_vout);
           } else if (ch.rev) {
             bwd_half_horiz<T, kPre, true>(ln, st, cm, lane, S, OG);
           } else {
@@ -1366,14 +1403,22 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
+// 3D map over a [planes][H][W] tensor. plane_mid: dims ordered (W, planes, H) instead of (W, H, planes)
+// (packed vertical tiles: one box = K rows of npack consecutive planes, step-major in shared memory).
 bool encode(CUtensorMap* m, const void* base, gspn_dtype_t dt, int64_t W, int64_t H, int64_t planes, int box0,
-            int box1, bool swizzle32) {
+            int box1, bool swizzle32, int box2 = 1, bool plane_mid = false) {
   auto fn = get_encode();
   if (!fn) return false;
   const size_t s = dt == GSPN_BF16 ? 2 : 4;
   cuuint64_t dims[3] = {static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H), static_cast<cuuint64_t>(planes)};
   cuuint64_t strides[2] = {static_cast<cuuint64_t>(W * s), static_cast<cuuint64_t>(W * H * s)};
-  cuuint32_t box[3] = {static_cast<cuuint32_t>(box0), static_cast<cuuint32_t>(box1), 1};
+  if (plane_mid) {
+    dims[1] = static_cast<cuuint64_t>(planes);
+    dims[2] = static_cast<cuuint64_t>(H);
+    strides[0] = static_cast<cuuint64_t>(W * H * s);
+    strides[1] = static_cast<cuuint64_t>(W * s);
+  }
+  cuuint32_t box[3] = {static_cast<cuuint32_t>(box0), static_cast<cuuint32_t>(box1), static_cast<cuuint32_t>(box2)};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(m, dt == GSPN_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
                   const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -1439,12 +1484,29 @@ bool make_plan(const ScanParams& p, gspn_dtype_t dt, int nin, Plan* pl) {
   pl->stage_bytes = nin * kTile;
   pl->tx_v = static_cast<uint32_t>(nin * pl->nbw * pl->bw * pl->K * s);
   pl->tx_h = static_cast<uint32_t>(nin * pl->nbh * pl->bh * 32);
+  pl->npack = 1;
+  pl->nbc = p.B * p.C;
+  pl->vstep = kRowB;
+  const int64_t PH = std::max<int64_t>(p.H, p.W);  // packing needs both orientations to fit
+  if (p.G == p.C && PH <= kPpad / 2 && pl->nbc > 1 && !getenv("GSPN_NOPACK")) {
+    // a divisor of B C: no partial pack, so a packed TMA store never spills into the next direction
+    int np = static_cast<int>(std::min<int64_t>({kPpad / PH, 256, pl->nbc}));
+    while (pl->nbc % np != 0) --np;
+    if (np >= 2) {
+      pl->npack = np;
+      pl->vstep = static_cast<uint32_t>(np * p.W * s);
+      pl->nwc = static_cast<int>((np * PH + pl->own - 1) / pl->own);
+      if (pl->nwc > 11) return false;
+      pl->tx_v = static_cast<uint32_t>(nin * np * p.W * pl->K * s);
+      pl->tx_h = static_cast<uint32_t>(nin * np * p.H * 32);
+    }
+  }
   const int budget = smem_optin() - 1024 /*alignment*/ - kSmemTail;
   int ns = budget / static_cast<int>(pl->stage_bytes);
   if (ns > 6) ns = 6;
   if (ns < 2) return false;
   pl->nstages = ns;
-  pl->nchains = p.D * p.B * p.C;
+  pl->nchains = p.D * ((pl->nbc + pl->npack - 1) / pl->npack);  // work items: packs of chains
   pl->smem_bytes = 1024 + ns * pl->stage_bytes + kSmemTail;
   // L2 priorities (experiments: GSPN_POL="x,vin,hin,vout,hout,acc", each 0|1|2)
   static const int def_pol[6] = {1, 0, 1, 0, 1, 1};
@@ -1462,6 +1524,15 @@ bool fill_maps(StreamArgs* A, const void* const* ins, int nin, void* const* outs
                int64_t out_planes, int nout, gspn_dtype_t dt) {
   const Plan& pl = A->plan;
   const ScanParams& p = A->p;
+  if (pl.npack > 1) {
+    for (int t = 0; t < nin; ++t) {
+      if (!encode(&A->in[0][t], ins[t], dt, p.W, p.H, in_planes[t], p.W, pl.npack, false, pl.K, true)) return false;
+      if (!encode(&A->in[1][t], ins[t], dt, p.W, p.H, in_planes[t], pl.K, p.H, true, pl.npack)) return false;
+    }
+    for (int t = 0; t < nout; ++t)
+      if (!encode(&A->out[1][t], outs[t], dt, p.W, p.H, out_planes, pl.K, p.H, true, pl.npack)) return false;
+    return true;
+  }
   for (int t = 0; t < nin; ++t) {
     if (!encode(&A->in[0][t], ins[t], dt, p.W, p.H, in_planes[t], pl.bw, pl.K, false)) return false;
     if (!encode(&A->in[1][t], ins[t], dt, p.W, p.H, in_planes[t], pl.K, pl.bh, true)) return false;
