@@ -87,6 +87,11 @@ struct Plan {
   int npack;
   int64_t nbc;         // B * C planes
   uint32_t vstep;      // bytes between consecutive steps of a vertical tile (kRowB, or npack W s)
+  // P-split (P > one tile): a cluster of cl CTAs runs one chain, CTA s holds positions
+  // [s ownc - GH, s ownc - GH + kPpad) and owns [s ownc, (s+1) ownc); slice-edge ghosts travel
+  // through distributed shared memory. cl = 1: no cluster.
+  int cl, ownc;
+  int bhs, nbhs;       // cluster mode: horizontal TMA store boxes over the owned rows
   int nstages;
   uint32_t tile_bytes;   // one tensor's tile: K * ppad * es (= 32 * ppad)
   uint32_t stage_bytes;  // nin * tile_bytes
@@ -159,13 +164,25 @@ struct Chain {
   int psub, nvalid;           // positions per chain; chains of the pack that exist
 };
 
+// Work items are handed out round-robin over the persistent grid (CTAs, or clusters in P-split mode).
+__device__ __forceinline__ int64_t work_first(const Plan& pl) {
+  return pl.cl > 1 ? static_cast<int64_t>(cluster_id_x()) : static_cast<int64_t>(blockIdx.x);
+}
+__device__ __forceinline__ int64_t work_stride(const Plan& pl) {
+  return pl.cl > 1 ? static_cast<int64_t>(nclusters_x()) : static_cast<int64_t>(gridDim.x);
+}
+// First tile position held by this CTA (P-split: slice start minus the left ghosts).
+__device__ __forceinline__ int tile_base(const Plan& pl) {
+  return pl.cl > 1 ? static_cast<int>(cluster_ctarank()) * pl.ownc - pl.K / 2 : 0;
+}
+
 __device__ __forceinline__ Chain make_chain(const ScanParams& p, const Plan& pl, int64_t w) {
   Chain ch;
   const int64_t bc = (w / p.D) * pl.npack;
   // Round i of the persistent grid covers slots [i G, (i+1) G): whole planes when D divides G. The
   // direction is rotated by i so every CTA cycles through all D directions (vertical and horizontal
   // chains run at different speeds; a fixed direction per CTA would leave the fast ones idle).
-  const int64_t G = gridDim.x;
+  const int64_t G = work_stride(pl);
   ch.k = static_cast<int>(G % p.D == 0 ? (w + w / G) % p.D : w % p.D);
   const uint32_t dir = p.dirbit[ch.k];
   ch.vert = (dir == GSPN_DIR_T2B) || (dir == GSPN_DIR_B2T);
@@ -212,7 +229,8 @@ __device__ void producer_loop(const StreamArgs& A, uint8_t* ring, uint64_t* full
   const uint64_t pol_hin = policy_of(pl.pol[2]);
   int stage = 0;
   uint32_t phase = 0;
-  for (int64_t w = blockIdx.x; w < pl.nchains; w += gridDim.x) {
+  const int base = tile_base(pl);
+  for (int64_t w = work_first(pl); w < pl.nchains; w += work_stride(pl)) {
     const Chain ch = make_chain(A.p, pl, w);
     const int o = ch.vert ? 0 : 1;
     for (int jj = 0; jj < ch.ntiles; ++jj) {
@@ -232,9 +250,10 @@ __device__ void producer_loop(const StreamArgs& A, uint8_t* ring, uint64_t* full
           else tma_load3(dst, &A.in[1][t], s0, 0, plane, fb, pol);
         } else if (ch.vert) {
           for (int q = 0; q < pl.nbw; ++q)
-            tma_load3(dst + q * pl.K * pl.bw * pl.es, &A.in[o][t], q * pl.bw, s0, plane, fb, pol);
+            tma_load3(dst + q * pl.K * pl.bw * pl.es, &A.in[o][t], base + q * pl.bw, s0, plane, fb, pol);
         } else {
-          for (int q = 0; q < pl.nbh; ++q) tma_load3(dst + q * pl.bh * 32, &A.in[o][t], s0, q * pl.bh, plane, fb, pol);
+          for (int q = 0; q < pl.nbh; ++q)
+            tma_load3(dst + q * pl.bh * 32, &A.in[o][t], s0, base + q * pl.bh, plane, fb, pol);
         }
       }
       if (++stage == pl.nstages) { stage = 0; phase ^= 1; }
@@ -252,7 +271,7 @@ __device__ void storer_loop(const StreamArgs& A, uint8_t* ring, uint64_t* done, 
   const uint64_t pol = policy_of(pl.pol[4]);
   int stage = 0;
   uint32_t phase = 0;
-  for (int64_t w = blockIdx.x; w < pl.nchains; w += gridDim.x) {
+  for (int64_t w = work_first(pl); w < pl.nchains; w += work_stride(pl)) {
     const Chain ch = make_chain(A.p, pl, w);
     for (int jj = 0; jj < ch.ntiles; ++jj) {
       const int j = bwd ? (ch.ntiles - 1 - jj) : jj;
@@ -264,6 +283,11 @@ __device__ void storer_loop(const StreamArgs& A, uint8_t* ring, uint64_t* done, 
           const uint32_t src = smem_u32(st + static_cast<size_t>(slots[t]) * pl.tile_bytes);
           if (pl.npack > 1) {
             tma_store3(&A.out[1][t], src, s0, 0, static_cast<int>(ch.chain), pol);
+          } else if (pl.cl > 1) {  // only the owned rows: the ghost rows belong to the neighbour CTAs
+            const int gh = pl.K / 2;
+            for (int q = 0; q < pl.nbhs; ++q)
+              tma_store3(&A.out[1][t], src + (gh + q * pl.bhs) * 32, s0, tile_base(pl) + gh + q * pl.bhs,
+                         static_cast<int>(ch.chain), pol);
           } else {
             for (int q = 0; q < pl.nbh; ++q)
               tma_store3(&A.out[1][t], src + q * pl.bh * 32, s0, q * pl.bh, static_cast<int>(ch.chain), pol);
@@ -343,7 +367,8 @@ __device__ __forceinline__ Lanes<T> make_lanes(const Plan& pl, const ScanParams&
   using C = Cfg<T>;
   constexpr int WARP = 32 * kE, OWN = WARP - 2 * C::GH;
   Lanes<T> ln;
-  ln.A = wi * OWN - C::GH;
+  const int base = tile_base(pl);  // tile row = position - base
+  ln.A = (pl.cl > 1 ? base : -C::GH) + wi * OWN;
   constexpr int lo = C::GH;
   const int nval = ch.psub * ch.nvalid;
   // vertical
@@ -351,7 +376,8 @@ __device__ __forceinline__ Lanes<T> make_lanes(const Plan& pl, const ScanParams&
     const int off = kE * lane;
     const int r0 = ln.A + off;
     ln.own_v = off >= lo && off < WARP - C::GH && r0 >= 0 && r0 < nval;
-    const int rc = r0 < 0 ? 0 : (r0 > kPpad - kE ? kPpad - kE : r0);
+    const int rt = r0 - base;
+    const int rc = rt < 0 ? 0 : (rt > kPpad - kE ? kPpad - kE : rt);
     if (pl.npack > 1) {
       ln.voff = static_cast<uint32_t>(rc * C::es);
     } else {
@@ -366,8 +392,9 @@ __device__ __forceinline__ Lanes<T> make_lanes(const Plan& pl, const ScanParams&
   for (int q = 0; q < kE; ++q) {
     const int off = 32 * q + lane;
     const int r = ln.A + off;
-    ln.own_h[q] = off >= lo && off < WARP - C::GH && r < kPpad;  // rows >= P: outside the store box
-    const uint32_t rc = static_cast<uint32_t>(r < 0 ? 0 : (r >= kPpad ? kPpad - 1 : r));
+    const int rt = r - base;
+    ln.own_h[q] = off >= lo && off < WARP - C::GH && rt < kPpad;  // rows >= P: outside the store box
+    const uint32_t rc = static_cast<uint32_t>(rt < 0 ? 0 : (rt >= kPpad ? kPpad - 1 : rt));
     ln.hoff[q] = rc * 32 + (((rc >> 2) & 1u) << 4);
   }
   if (ch.vert) {
@@ -465,11 +492,13 @@ __device__ __forceinline__ void edge_reload(const float* edge, int par, int wi, 
   }
 }
 
-// Shared-memory carve-up common to both kernels: ring | full | empty | done | edges.
+// Shared-memory carve-up common to both kernels: ring | full | empty | done | edges | cluster edges.
 struct Smem {
   uint8_t* ring;
   uint64_t *full, *empty, *done;
   float* edge;
+  float *xl, *xr;   // P-split: ghost values from the left / right neighbour CTA [3 arrays][2 par][8]
+  uint64_t* xb;     // P-split: [0..1] left-neighbour data landed (par), [2..3] right-neighbour data landed
 };
 
 __device__ __forceinline__ Smem carve(uint8_t* smem_raw, const Plan& pl) {
@@ -479,6 +508,9 @@ __device__ __forceinline__ Smem carve(uint8_t* smem_raw, const Plan& pl) {
   m.empty = m.full + pl.nstages;
   m.done = m.empty + pl.nstages;
   m.edge = reinterpret_cast<float*>(m.done + pl.nstages);  // [3 state arrays][2 par][kEdgeW][2][8]
+  m.xl = m.edge + 3 * 2 * kEdgeW * 2 * 8;
+  m.xr = m.xl + 3 * 2 * 8;
+  m.xb = reinterpret_cast<uint64_t*>(m.xr + 3 * 2 * 8);
   return m;
 }
 
@@ -497,9 +529,77 @@ __device__ __forceinline__ void init_barriers(const Smem& m, const Plan& pl) {
       mbar_init(smem_u32(&m.empty[s]), 1);      // storer
       mbar_init(smem_u32(&m.done[s]), pl.nwc);  // one arrive per consumer warp
     }
+    for (int i = 0; i < 4; ++i) mbar_init(smem_u32(&m.xb[i]), 32);  // one arrive per lane of the sending warp
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  if (pl.cl > 1) cluster_sync_all();  // neighbours' barriers initialised before any remote access
+}
+
+// ---- P-split ghost exchange between the CTAs of a cluster (after the intra-CTA publish).
+// Warp 0 of CTA s sends its first GH owned values to CTA s-1 (they are that CTA's right ghosts), the
+// last warp sends its last GH owned values to CTA s+1; every lane of a sending warp then arrives on
+// the receiver's barrier (release at cluster scope). Parity-double-buffered like the local edges;
+// a sender cannot run two halves ahead because it needs the receiver's edges of the half between.
+// side 0: towards rank - 1, side 1: towards rank + 1.
+__device__ __forceinline__ bool xgo(int side, int wi, int nwc, int rank, int cl) {
+  return side == 0 ? (wi == 0 && rank > 0) : (wi == nwc - 1 && rank < cl - 1);
+}
+
+template <typename T>
+__device__ __forceinline__ void xput(const Smem& m, int par, int side, uint32_t tr, int a, int lane, bool vert,
+                                     const float (&v)[kE]) {
+  using C = Cfg<T>;
+  constexpr int WARP = 32 * kE;
+  float* dst = (side == 0 ? m.xr : m.xl) + (a * 2 + par) * 8;  // left-going data = receiver's right ghosts
+  if (vert) {
+    const int o = kE * lane;
+    const int lo = side == 0 ? C::GH : WARP - 2 * C::GH;
+    if (o >= lo && o < lo + C::GH) {
+#pragma unroll
+      for (int e = 0; e < kE; ++e) st_cluster_f32(mapa(smem_u32(dst + o - lo + e), tr), v[e]);
+    }
+  } else {
+    const int lo = side == 0 ? C::GH : 32 - 2 * C::GH;
+    if (lane >= lo && lane < lo + C::GH) st_cluster_f32(mapa(smem_u32(dst + lane - lo), tr), side == 0 ? v[0] : v[kE - 1]);
+  }
+}
+
+__device__ __forceinline__ void xarrive(const Smem& m, int par, int side, uint32_t tr) {
+  __syncwarp();
+  mbar_arrive_remote(mapa(smem_u32(&m.xb[(side == 0 ? 2 : 0) + par]), tr));
+}
+
+__device__ __forceinline__ void xwait(const Smem& m, int par, int side, uint32_t xphase) {
+  mbar_wait_cluster(smem_u32(&m.xb[(side == 0 ? 0 : 2) + par]), xphase);
+}
+
+template <typename T>
+__device__ __forceinline__ void xget(const Smem& m, int par, int side, int a, int lane, bool vert, float (&v)[kE]) {
+  using C = Cfg<T>;
+  constexpr int WARP = 32 * kE;
+  const float* src = (side == 0 ? m.xl : m.xr) + (a * 2 + par) * 8;
+  if (vert) {
+    const int o = kE * lane;
+    const int lo = side == 0 ? 0 : WARP - C::GH;
+    if (o >= lo && o < lo + C::GH) {
+#pragma unroll
+      for (int e = 0; e < kE; ++e) v[e] = src[o - lo + e];
+    }
+  } else {
+    const int lo = side == 0 ? 0 : 32 - C::GH;
+    if (lane >= lo && lane < lo + C::GH) {
+      if (side == 0) v[0] = src[lane - lo];
+      else v[kE - 1] = src[lane - lo];
+    }
+  }
+}
+
+// Every thread of every role passes one final cluster barrier: no CTA leaves while a neighbour may
+// still address its shared memory.
+__device__ __forceinline__ void cluster_exit(const Plan& pl) {
+  __syncwarp();
+  if (pl.cl > 1) cluster_sync_all();
 }
 
 __device__ __forceinline__ float clamped_rcp(float s) { return fminf(fast_rcp(s), kRcpMax); }
@@ -604,6 +704,7 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) fwd_stream_kernel(const
         for (int t = 0; t < F_NIN; ++t) asm volatile("prefetch.tensormap [%0];" ::"l"(&A.in[o][t]) : "memory");
       producer_loop<false>(A, m.ring, m.full, m.empty);
     }
+    cluster_exit(pl);
     return;
   }
   if (warp == pl.nwc + 1) {  // storer warp
@@ -611,14 +712,17 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) fwd_stream_kernel(const
       const int slots[1] = {F_X};
       storer_loop(A, m.ring, m.done, m.empty, 1, slots, false);
     }
+    cluster_exit(pl);
     return;
   }
   const uint64_t pol_vout = policy_of(pl.pol[3]);
   const int nthreads = pl.nwc * 32;
   const int64_t W = A.p.W;
+  const int rank = pl.cl > 1 ? static_cast<int>(cluster_ctarank()) : 0;
+  uint32_t xphase = 0;  // P-split: phase bit of the cluster edge barriers, per parity
   int stage = 0, par = 0;
   uint32_t phase = 0;
-  for (int64_t w = blockIdx.x; w < pl.nchains; w += gridDim.x) {
+  for (int64_t w = work_first(pl); w < pl.nchains; w += work_stride(pl)) {
     const Chain ch = make_chain(A.p, pl, w);
     const Lanes<T> ln = make_lanes<T>(pl, A.p, ch, warp, lane);
     T* hout = static_cast<T*>(A.p.hout) + ln.vout;
@@ -646,8 +750,26 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) fwd_stream_kernel(const
           }
         }
         edge_publish<T>(m.edge, par, warp, lane, ch.vert, h);
+        if (pl.cl > 1) {
+#pragma unroll
+          for (int side = 0; side < 2; ++side) {
+            if (!xgo(side, warp, pl.nwc, rank, pl.cl)) continue;
+            const uint32_t tr = static_cast<uint32_t>(side == 0 ? rank - 1 : rank + 1);
+            xput<T>(m, par, side, tr, 0, lane, ch.vert, h);
+            xarrive(m, par, side, tr);
+          }
+        }
         named_bar(kBarEdge, nthreads);  // edges published; every warp has read this half's input rows
         edge_reload<T>(m.edge, par, warp, pl.nwc, lane, ch.vert, h);
+        if (pl.cl > 1) {
+#pragma unroll
+          for (int side = 0; side < 2; ++side) {
+            if (!xgo(side, warp, pl.nwc, rank, pl.cl)) continue;
+            xwait(m, par, side, (xphase >> par) & 1u);
+            xget<T>(m, par, side, 0, lane, ch.vert, h);
+          }
+          xphase ^= 1u << par;
+        }
         par ^= 1;
         if (!ch.vert && !pl.null_compute) {  // new states in place over the x chunk of this half
 #pragma unroll
@@ -662,6 +784,7 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) fwd_stream_kernel(const
       if (++stage == pl.nstages) { stage = 0; phase ^= 1; }
     }
   }
+  cluster_exit(pl);
 }
 
 // ------------------------------------------------------------------------------ backward recurrence
@@ -751,6 +874,7 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_stream_kernel(const
         for (int t = 0; t < B_NIN; ++t) asm volatile("prefetch.tensormap [%0];" ::"l"(&A.in[o][t]) : "memory");
       producer_loop<true>(A, m.ring, m.full, m.empty);
     }
+    cluster_exit(pl);
     return;
   }
   if (warp == pl.nwc + 1) {  // storer warp: horizontal tiles' g (written over the dh slot)
@@ -758,15 +882,18 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_stream_kernel(const
       const int slots[1] = {B_DH};
       storer_loop(A, m.ring, m.done, m.empty, 1, slots, true);
     }
+    cluster_exit(pl);
     return;
   }
   const uint64_t pol_vout = policy_of(pl.pol[3]);
   const int nthreads = pl.nwc * 32;
   constexpr int kEdgeArr = 2 * kEdgeW * 2 * 8;
   const int64_t W = A.p.W;
+  const int rank = pl.cl > 1 ? static_cast<int>(cluster_ctarank()) : 0;
+  uint32_t xphase = 0;
   int stage = 0, par = 0;
   uint32_t phase = 0;
-  for (int64_t w = blockIdx.x; w < pl.nchains; w += gridDim.x) {
+  for (int64_t w = work_first(pl); w < pl.nchains; w += work_stride(pl)) {
     const Chain ch = make_chain(A.p, pl, w);
     const Lanes<T> ln = make_lanes<T>(pl, A.p, ch, warp, lane);
     T* gout = static_cast<T*>(A.g) + ln.vout;
@@ -800,10 +927,32 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_stream_kernel(const
         edge_publish<T>(m.edge + 0 * kEdgeArr, par, warp, lane, ch.vert, S.ea);
         edge_publish<T>(m.edge + 1 * kEdgeArr, par, warp, lane, ch.vert, S.eb);
         edge_publish<T>(m.edge + 2 * kEdgeArr, par, warp, lane, ch.vert, S.ec);
+        if (pl.cl > 1) {
+#pragma unroll
+          for (int side = 0; side < 2; ++side) {
+            if (!xgo(side, warp, pl.nwc, rank, pl.cl)) continue;
+            const uint32_t tr = static_cast<uint32_t>(side == 0 ? rank - 1 : rank + 1);
+            xput<T>(m, par, side, tr, 0, lane, ch.vert, S.ea);
+            xput<T>(m, par, side, tr, 1, lane, ch.vert, S.eb);
+            xput<T>(m, par, side, tr, 2, lane, ch.vert, S.ec);
+            xarrive(m, par, side, tr);
+          }
+        }
         named_bar(kBarEdge, nthreads);  // edges published; every warp has read this half's input rows
         edge_reload<T>(m.edge + 0 * kEdgeArr, par, warp, pl.nwc, lane, ch.vert, S.ea);
         edge_reload<T>(m.edge + 1 * kEdgeArr, par, warp, pl.nwc, lane, ch.vert, S.eb);
         edge_reload<T>(m.edge + 2 * kEdgeArr, par, warp, pl.nwc, lane, ch.vert, S.ec);
+        if (pl.cl > 1) {
+#pragma unroll
+          for (int side = 0; side < 2; ++side) {
+            if (!xgo(side, warp, pl.nwc, rank, pl.cl)) continue;
+            xwait(m, par, side, (xphase >> par) & 1u);
+            xget<T>(m, par, side, 0, lane, ch.vert, S.ea);
+            xget<T>(m, par, side, 1, lane, ch.vert, S.eb);
+            xget<T>(m, par, side, 2, lane, ch.vert, S.ec);
+          }
+          xphase ^= 1u << par;
+        }
         par ^= 1;
         if (!ch.vert && !pl.null_compute) {
 #pragma unroll
@@ -818,6 +967,7 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_stream_kernel(const
       if (++stage == pl.nstages) { stage = 0; phase ^= 1; }
     }
   }
+  cluster_exit(pl);
 }
 
 // ------------------------------------------------------------------------------ backward outputs
@@ -1449,7 +1599,7 @@ int smem_optin() {
   return n;
 }
 
-constexpr int kSmemTail = 6656;  // mbarriers (3 per stage), ghost-edge buffers (6 KB), flag
+constexpr int kSmemTail = 7168;  // mbarriers (3 per stage), ghost-edge buffers (6 KB), cluster edges + barriers
 
 // Shape eligibility + plan (nin: tensors per tile).
 bool make_plan(const ScanParams& p, gspn_dtype_t dt, int nin, Plan* pl) {
@@ -1461,17 +1611,28 @@ bool make_plan(const ScanParams& p, gspn_dtype_t dt, int nin, Plan* pl) {
     if (p.dirbit[k] == GSPN_DIR_T2B || p.dirbit[k] == GSPN_DIR_B2T) any_v = true; else any_h = true;
   }
   const int64_t maxP = std::max<int64_t>(any_v ? p.W : 0, any_h ? p.H : 0);
-  if (maxP > kPpad) return false;
   memset(pl, 0, sizeof *pl);
   pl->K = 32 / s;
   const int GH = pl->K / 2;
   pl->E = 2;
   pl->es = s;
   pl->own = 64 - 2 * GH;
+  pl->cl = 1;
   pl->nwc = static_cast<int>((maxP + pl->own - 1) / pl->own);  // warp w owns [w own, (w+1) own)
-  if (pl->nwc > 11) return false;
   // positions any lane reads (clamped to the tile); the TMA boxes cover them so no lane reads stale rows
-  const int cover = static_cast<int>(std::min<int64_t>(kPpad, (pl->nwc - 1) * pl->own - GH + 64));
+  int cover = static_cast<int>(std::min<int64_t>(kPpad, (pl->nwc - 1) * pl->own - GH + 64));
+  if (pl->nwc > 11) {
+    // P-split over a cluster: each CTA owns the positions its warps own while their ghosts stay
+    // inside its 512-position tile (10 x 48 bf16 / 9 x 56 fp32)
+    const int nwc_c = (kPpad - 2 * GH) / pl->own;
+    pl->ownc = nwc_c * pl->own;
+    pl->cl = static_cast<int>((maxP + pl->ownc - 1) / pl->ownc);
+    if (pl->cl > 8 || getenv("GSPN_NOCLUSTER")) return false;
+    pl->nwc = nwc_c;
+    cover = kPpad;
+    pl->bhs = pl->ownc / 2;  // <= 256 rows per TMA store box
+    pl->nbhs = 2;
+  }
   pl->ppad = kPpad;
   pl->bw = kRowB / s;
   pl->nbw = (cover + pl->bw - 1) / pl->bw;
@@ -1488,7 +1649,7 @@ bool make_plan(const ScanParams& p, gspn_dtype_t dt, int nin, Plan* pl) {
   pl->nbc = p.B * p.C;
   pl->vstep = kRowB;
   const int64_t PH = std::max<int64_t>(p.H, p.W);  // packing needs both orientations to fit
-  if (p.G == p.C && PH <= kPpad / 2 && pl->nbc > 1 && !getenv("GSPN_NOPACK")) {
+  if (pl->cl == 1 && p.G == p.C && PH <= kPpad / 2 && pl->nbc > 1 && !getenv("GSPN_NOPACK")) {
     // a divisor of B C: no partial pack, so a packed TMA store never spills into the next direction
     int np = static_cast<int>(std::min<int64_t>({kPpad / PH, 256, pl->nbc}));
     while (pl->nbc % np != 0) --np;
@@ -1538,7 +1699,8 @@ bool fill_maps(StreamArgs* A, const void* const* ins, int nin, void* const* outs
     if (!encode(&A->in[1][t], ins[t], dt, p.W, p.H, in_planes[t], pl.K, pl.bh, true)) return false;
   }
   for (int t = 0; t < nout; ++t)
-    if (!encode(&A->out[1][t], outs[t], dt, p.W, p.H, out_planes, pl.K, pl.bh, true)) return false;
+    if (!encode(&A->out[1][t], outs[t], dt, p.W, p.H, out_planes, pl.K, pl.cl > 1 ? pl.bhs : pl.bh, true))
+      return false;
   return true;
 }
 
@@ -1556,6 +1718,29 @@ cudaError_t launch(KernelT kernel, const StreamArgs& A, cudaStream_t s) {
   if (const char* ev = getenv("GSPN_GRID")) {  // experiments only: cap the persistent grid
     const int64_t g = atoll(ev);
     if (g > 0 && g < grid) grid = g;
+  }
+  if (A.plan.cl > 1) {  // P-split: clusters of cl CTAs, one chain per cluster at a time
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = A.plan.cl;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.blockDim = dim3(threads, 1, 1);
+    cfg.dynamicSmemBytes = A.plan.smem_bytes;
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cfg.gridDim = dim3(static_cast<unsigned>(A.plan.cl * 148), 1, 1);
+    int ncl = 0;
+    e = cudaOccupancyMaxActiveClusters(&ncl, kernel, &cfg);
+    if (e != cudaSuccess) return e;
+    if (ncl < 1) return cudaErrorInvalidConfiguration;
+    if (ncl > A.plan.nchains) ncl = static_cast<int>(A.plan.nchains);
+    cfg.gridDim = dim3(static_cast<unsigned>(ncl * A.plan.cl), 1, 1);
+    e = cudaLaunchKernelEx(&cfg, kernel, A);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
   }
   if (grid > A.plan.nchains) grid = A.plan.nchains;
   kernel<<<static_cast<unsigned>(grid), threads, A.plan.smem_bytes, s>>>(A);

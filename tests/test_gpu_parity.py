@@ -46,6 +46,10 @@ SHAPES = [
     (1, 2, 1, 8, 512, 0xF, "f32"),
     (1, 2, 2, 500, 504, 0xF, "bf16"),
     (1, 1, 1, 250, 248, 0xF, "bf16"),
+    # P-split over a thread-block cluster (P > 512: 2-3 CTAs per chain, ghosts through DSMEM)
+    (1, 2, 2, 24, 1000, 0xF, "bf16"),
+    (1, 1, 1, 700, 48, 0xF, "bf16"),
+    (1, 2, 2, 20, 1040, 0xF, "f32"),
 ]
 FLAGS = [0, gspn.FLAG_FORCE_GENERIC]
 
