@@ -1529,6 +1529,180 @@ __global__ void __launch_bounds__((kOutConsumers + 1) * 32, 1) bwd_out_tma_kerne
   }
 }
 
+// ---- Grouped weights (G < C): a unit is (b, group, RB rows); the ring streams one channel of the
+// group per stage (x, and per direction g, lam and the h halo tile), every thread keeps the group sums
+// Da/Db/Dc of its 4-column chunk for all directions in registers, and after the group's last channel
+// reads w from global memory once and writes dw. One chunk per consumer thread (RB W / 4 <= 512).
+template <typename T>
+__global__ void __launch_bounds__((kOutConsumers + 1) * 32, 1) bwd_out_grp_tma_kernel(const __grid_constant__ OutArgs A) {
+  constexpr int V = 4;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* ring = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + static_cast<size_t>(A.nstages) * A.stage_bytes);
+  uint64_t* empty = full + A.nstages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const ScanParams& p = A.p;
+  const int D = p.D, RB = A.RB, BX = A.BX;
+  const int64_t Cg = p.C / p.G;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < A.nstages; ++s) {
+      mbar_init(smem_u32(&full[s]), 1);
+      mbar_init(smem_u32(&empty[s]), kOutConsumers);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == kOutConsumers) {  // producer
+    if (lane == 0) {
+      const uint64_t pol = policy_of(0);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t u = blockIdx.x; u < A.nunits; u += gridDim.x) {
+        const int64_t bg = u / A.nrb;
+        const int i0 = static_cast<int>(u % A.nrb) * RB;
+        const int64_t b = bg / p.G, grp = bg % p.G;
+        for (int64_t cc = 0; cc < Cg; ++cc) {
+          const int64_t bc = b * p.C + grp * Cg + cc;
+          mbar_wait_sleep(smem_u32(&empty[stage]), phase ^ 1);
+          const uint32_t fb = smem_u32(&full[stage]);
+          mbar_arrive_tx(fb, A.tx);
+          const uint32_t st = smem_u32(ring + static_cast<size_t>(stage) * A.stage_bytes);
+          for (int bx = 0; bx < A.nbx; ++bx) tma_load3(st + bx * A.box_rb, &A.x, bx * BX, i0, static_cast<int>(bc), fb, pol);
+          for (int k = 0; k < D; ++k) {
+            const int chain = static_cast<int>(static_cast<int64_t>(k) * p.B * p.C + bc);
+            const uint32_t base = st + A.tile_rb + k * A.per_k;
+            for (int bx = 0; bx < A.nbx; ++bx) {
+              tma_load3(base + bx * A.box_rb, &A.g, bx * BX, i0, chain, fb, pol);
+              tma_load3(base + A.tile_rb + bx * A.box_rb, &A.lam, bx * BX, i0, chain, fb, pol);
+              tma_load3(base + 2 * A.tile_rb + bx * A.box_h, &A.h, bx * BX, i0 - 1, chain, fb, policy_of(1));
+            }
+          }
+          if (++stage == A.nstages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+    return;
+  }
+  const bool prenorm = p.flags & GSPN_FLAG_PRENORMALIZED;
+  const int64_t H = p.H, W = p.W, HW = H * W;
+  const int64_t kstride = p.B * p.C * HW;   // direction slabs of lam / g / h / dlam
+  const int64_t kwstride = p.B * p.G * HW;  // direction slabs of w / dw
+  const int nchunk = static_cast<int>(W / V);
+  constexpr int es = static_cast<int>(sizeof(T));
+  const uint32_t rowb = static_cast<uint32_t>(BX * es);
+  const int idx = threadIdx.x;  // this thread's chunk (one per thread)
+  const int r = idx / nchunk;
+  const int j0 = (idx - r * nchunk) * V;
+  const int bx = j0 >= BX ? j0 / BX : 0;
+  const uint32_t col = static_cast<uint32_t>((j0 - bx * BX) * es);
+  const uint32_t orb = bx * A.box_rb + r * rowb + col;
+  const uint32_t oh = bx * A.box_h + r * rowb + col;
+  const bool has_lo = j0 > 0, has_hi = j0 + V < W;
+  const uint32_t ohl = (j0 - bx * BX) > 0 ? oh - es : (bx - 1) * A.box_h + r * rowb + (BX - 1) * es;
+  const uint32_t ohh = (j0 - bx * BX) + V < BX ? oh + V * es : (bx + 1) * A.box_h + r * rowb;
+  int stage = 0;
+  uint32_t phase = 0;
+  for (int64_t u = blockIdx.x; u < A.nunits; u += gridDim.x) {
+    const int64_t bg = u / A.nrb;
+    const int i0 = static_cast<int>(u % A.nrb) * RB;
+    const int64_t b = bg / p.G, grp = bg % p.G;
+    const int64_t i = i0 + r;
+    const bool valid = r < RB && i < H;
+    float Da[4][V], Db[4][V], Dc[4][V];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int q = 0; q < V; ++q) Da[k][q] = Db[k][q] = Dc[k][q] = 0.f;
+    for (int64_t cc = 0; cc < Cg; ++cc) {
+      mbar_wait(smem_u32(&full[stage]), phase);
+      const uint8_t* st = ring + static_cast<size_t>(stage) * A.stage_bytes;
+      if (valid) {
+        const int64_t bc = b * p.C + grp * Cg + cc;
+        const int64_t off0 = bc * HW + i * W + j0;
+        float xv[V], dx[V];
+        sm_ld4v<T>(st + orb, xv);
+#pragma unroll
+        for (int q = 0; q < V; ++q) dx[q] = 0.f;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (k >= D) break;
+          const uint8_t* base = st + A.tile_rb + k * A.per_k;
+          const uint8_t* ht = base + 2 * A.tile_rb;
+          const uint32_t dir = p.dirbit[k];
+          const int64_t off = off0 + k * kstride;
+          float gv[V], lv[V], dl[V];
+          sm_ld4v<T>(base + orb, gv);
+          sm_ld4v<T>(base + A.tile_rb + orb, lv);
+#pragma unroll
+          for (int q = 0; q < V; ++q) {
+            dl[q] = gv[q] * xv[q];
+            dx[q] = fmaf(gv[q], lv[q], dx[q]);
+          }
+          GVec<T, V>::store(static_cast<T*>(p.dlam) + off, dl);
+          if (dir == GSPN_DIR_T2B || dir == GSPN_DIR_B2T) {
+            const uint32_t ro = dir == GSPN_DIR_T2B ? 0u : 2u * rowb;
+            float v[V];
+            sm_ld4v<T>(ht + oh + ro, v);
+            const float lo = has_lo ? to_f(*reinterpret_cast<const T*>(ht + ohl + ro)) : 0.f;
+            const float hi = has_hi ? to_f(*reinterpret_cast<const T*>(ht + ohh + ro)) : 0.f;
+#pragma unroll
+            for (int q = 0; q < V; ++q) {
+              Da[k][q] = fmaf(gv[q], q > 0 ? v[q - 1] : lo, Da[k][q]);
+              Db[k][q] = fmaf(gv[q], v[q], Db[k][q]);
+              Dc[k][q] = fmaf(gv[q], q + 1 < V ? v[q + 1] : hi, Dc[k][q]);
+            }
+          } else {
+            const bool l2r = dir == GSPN_DIR_L2R;
+            const bool e_ok = l2r ? has_lo : has_hi;
+            const uint32_t oe = l2r ? ohl : ohh;
+#pragma unroll
+            for (int rr = 0; rr < 3; ++rr) {
+              float v[V];
+              sm_ld4v<T>(ht + oh + rr * rowb, v);
+              const float e = e_ok ? to_f(*reinterpret_cast<const T*>(ht + oe + rr * rowb)) : 0.f;
+#pragma unroll
+              for (int q = 0; q < V; ++q) {
+                const float sh = l2r ? (q > 0 ? v[q - 1] : e) : (q + 1 < V ? v[q + 1] : e);
+                if (rr == 0) Da[k][q] = fmaf(gv[q], sh, Da[k][q]);
+                else if (rr == 1) Db[k][q] = fmaf(gv[q], sh, Db[k][q]);
+                else Dc[k][q] = fmaf(gv[q], sh, Dc[k][q]);
+              }
+            }
+          }
+        }
+        GVec<T, V>::store(static_cast<T*>(p.dx) + off0, dx);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&empty[stage]));
+      if (++stage == A.nstages) { stage = 0; phase ^= 1; }
+    }
+    if (valid) {
+      const int64_t woff0 = (b * p.G + grp) * HW + i * W + j0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (k >= D) break;
+        const uint32_t dir = p.dirbit[k];
+        const bool vert = dir == GSPN_DIR_T2B || dir == GSPN_DIR_B2T;
+        const int64_t woff = woff0 + k * kwstride;
+        float wl[V], wm[V], wr[V], ol[V], om[V], orr[V];
+        GVec<T, V>::load(static_cast<const T*>(p.wl) + woff, wl);
+        GVec<T, V>::load(static_cast<const T*>(p.wm) + woff, wm);
+        GVec<T, V>::load(static_cast<const T*>(p.wr) + woff, wr);
+#pragma unroll
+        for (int q = 0; q < V; ++q) {
+          const int64_t rp = vert ? j0 + q : i;
+          const int64_t P = vert ? W : H;
+          jacobian<true>(wl[q], wm[q], wr[q], rp >= 1, rp <= P - 2, prenorm, Da[k][q], Db[k][q], Dc[k][q], ol[q],
+                         om[q], orr[q]);
+        }
+        GVec<T, V>::store(static_cast<T*>(p.dwl) + woff, ol);
+        GVec<T, V>::store(static_cast<T*>(p.dwm) + woff, om);
+        GVec<T, V>::store(static_cast<T*>(p.dwr) + woff, orr);
+      }
+    }
+  }
+}
+
 template <typename T, int V, bool kPerChannel>
 cudaError_t launch_out(const ScanParams& p, const void* g, cudaStream_t s) {
   constexpr int R = 8;
@@ -1794,6 +1968,7 @@ cudaError_t launch_fwd_stream(const ScanParams& p, gspn_dtype_t dt, cudaStream_t
 
 // TMA-staged output kernel (G = C). Returns false if the shape does not fit (caller falls back).
 bool launch_out_tma(const ScanParams& p, const void* g, gspn_dtype_t dt, cudaStream_t s, cudaError_t* err) {
+  const bool grouped = p.G != p.C;
   static OutArgs A;
   static std::mutex mu;
   std::lock_guard<std::mutex> lock(mu);
@@ -1806,12 +1981,17 @@ bool launch_out_tma(const ScanParams& p, const void* g, gspn_dtype_t dt, cudaStr
   const int D = static_cast<int>(p.D);
   const int budget = smem_optin() - 1024 - 256;
   auto pad = [](int64_t v) { return (v + 127) / 128 * 128; };
+  const int nrb_t = grouped ? 2 : 5;  // RB-row tiles per direction: g, lam (+ w_l, w_m, w_r)
   auto stage_of = [&](int rb) {
-    return A.nbx * (pad(es * A.BX * rb) * (1 + 5 * D) + pad(es * A.BX * (rb + 2)) * D);
+    return A.nbx * (pad(es * A.BX * rb) * (1 + nrb_t * D) + pad(es * A.BX * (rb + 2)) * D);
   };
   // enough rows per unit to give every consumer thread a 4-column chunk, 2+ stages
   int RB = 1;
   while (RB < 16 && RB * (p.W / 4) < kOutConsumers * 32) RB <<= 1;
+  if (grouped) {  // exactly one chunk per thread: the group sums live in its registers
+    while (RB > 1 && RB * (p.W / 4) > kOutConsumers * 32) RB >>= 1;
+    if (p.W / 4 > kOutConsumers * 32) return false;
+  }
   while (RB > 1 && 2 * stage_of(RB) > budget) RB >>= 1;
   if (2 * stage_of(RB) > budget) return false;
   A.RB = RB;
@@ -1819,12 +1999,12 @@ bool launch_out_tma(const ScanParams& p, const void* g, gspn_dtype_t dt, cudaStr
   A.box_h = static_cast<uint32_t>(pad(es * A.BX * (RB + 2)));
   A.tile_rb = A.nbx * A.box_rb;
   A.tile_h = A.nbx * A.box_h;
-  A.per_k = 5 * A.tile_rb + A.tile_h;
+  A.per_k = nrb_t * A.tile_rb + A.tile_h;
   A.stage_bytes = A.tile_rb + D * A.per_k;
-  A.tx = static_cast<uint32_t>(A.nbx * (es * A.BX * RB * (1 + 5 * D) + es * A.BX * (RB + 2) * D));  // TMA payload
+  A.tx = static_cast<uint32_t>(A.nbx * (es * A.BX * RB * (1 + nrb_t * D) + es * A.BX * (RB + 2) * D));  // payload
   A.nstages = static_cast<int>(std::min<int64_t>(6, budget / A.stage_bytes));
   A.nrb = static_cast<int>((p.H + RB - 1) / RB);
-  A.nunits = p.B * p.C * A.nrb;
+  A.nunits = (grouped ? p.B * p.G : p.B * p.C) * A.nrb;
   const int64_t nc = p.D * p.B * p.C;
   bool ok = encode(&A.x, p.x, dt, p.W, p.H, p.B * p.C, A.BX, RB, false) &&
             encode(&A.g, g, dt, p.W, p.H, nc, A.BX, RB, false) &&
@@ -1835,7 +2015,8 @@ bool launch_out_tma(const ScanParams& p, const void* g, gspn_dtype_t dt, cudaStr
             encode(&A.h, p.h, dt, p.W, p.H, nc, A.BX, RB + 2, false);
   if (!ok) return false;
   const uint32_t smem = 1024 + A.nstages * A.stage_bytes + 2 * 8 * A.nstages;
-  auto kern = dt == GSPN_BF16 ? bwd_out_tma_kernel<__nv_bfloat16> : bwd_out_tma_kernel<float>;
+  auto kern = grouped ? (dt == GSPN_BF16 ? bwd_out_grp_tma_kernel<__nv_bfloat16> : bwd_out_grp_tma_kernel<float>)
+                      : (dt == GSPN_BF16 ? bwd_out_tma_kernel<__nv_bfloat16> : bwd_out_tma_kernel<float>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e == cudaSuccess) {
     int per_sm = 0;
@@ -1879,7 +2060,7 @@ cudaError_t launch_bwd_stream(const ScanParams& p0, gspn_dtype_t dt, cudaStream_
   *launches += 1;
   if (e != cudaSuccess) return e;
   const bool per_channel = p.G == p.C;
-  if (per_channel && launch_out_tma(p, A.g, dt, s, &e)) {
+  if (launch_out_tma(p, A.g, dt, s, &e)) {
     *launches += 1;
     return e;
   }
