@@ -81,17 +81,6 @@ struct Plan {
   int bw, nbw;         // vertical TMA box width (positions) and box count
   int bh, nbh;         // horizontal TMA box height (rows) and box count
   int nin;             // input tensors per tile
-  // chain packing (G = C, max(H, W) <= kPpad / 2): npack chains of one direction side by side in a
-  // tile, positions c * psub + r; vertical packed tiles are [K][npack][W] (one 3D box), horizontal
-  // [npack][H][32 B]. Unpacked: npack = 1, vertical tiles [box][K][kRowB].
-  int npack;
-  int64_t nbc;         // B * C planes
-  uint32_t vstep;      // bytes between consecutive steps of a vertical tile (kRowB, or npack W s)
-  // P-split (P > one tile): a cluster of cl CTAs runs one chain, CTA s holds positions
-  // [s ownc - GH, s ownc - GH + kPpad) and owns [s ownc, (s+1) ownc); slice-edge ghosts travel
-  // through distributed shared memory. cl = 1: no cluster.
-  int cl, ownc;
-  int bhs, nbhs;       // cluster mode: horizontal TMA store boxes over the owned rows
   int nstages;
   uint32_t tile_bytes;   // one tensor's tile: K * ppad * es (= 32 * ppad)
   uint32_t stage_bytes;  // nin * tile_bytes
@@ -159,38 +148,17 @@ template <> struct Pk<float> {
 struct Chain {
   int k;            // direction slab
   bool vert, rev;   // orientation; reversed step order in canonical coordinates (B2T, R2L)
-  int64_t bc, chain, wplane;  // first plane of the (pack of) chain(s): x, lam/h/dh, w
+  int64_t bc, chain, wplane;
   int L, P, ntiles;
-  int psub, nvalid;           // positions per chain; chains of the pack that exist
 };
 
-// Work items are handed out round-robin over the persistent grid (CTAs, or clusters in P-split mode).
-// kCl: P-split kernels (launched in clusters); the plain kernels carry none of the cluster logic.
-template <bool kCl>
-__device__ __forceinline__ int64_t work_first(const Plan&) {
-  if constexpr (kCl) return static_cast<int64_t>(cluster_id_x());
-  else return static_cast<int64_t>(blockIdx.x);
-}
-template <bool kCl>
-__device__ __forceinline__ int64_t work_stride(const Plan&) {
-  if constexpr (kCl) return static_cast<int64_t>(nclusters_x());
-  else return static_cast<int64_t>(gridDim.x);
-}
-// First tile position held by this CTA (P-split: slice start minus the left ghosts).
-template <bool kCl>
-__device__ __forceinline__ int tile_base(const Plan& pl) {
-  if constexpr (kCl) return static_cast<int>(cluster_ctarank()) * pl.ownc - pl.K / 2;
-  else return 0;
-}
-
-template <bool kCl>
-__device__ __forceinline__ Chain make_chain(const ScanParams& p, const Plan& pl, int64_t w) {
+__device__ __forceinline__ Chain make_chain(const ScanParams& p, int K, int64_t w) {
   Chain ch;
-  const int64_t bc = (w / p.D) * pl.npack;
+  const int64_t bc = w / p.D;
   // Round i of the persistent grid covers slots [i G, (i+1) G): whole planes when D divides G. The
   // direction is rotated by i so every CTA cycles through all D directions (vertical and horizontal
   // chains run at different speeds; a fixed direction per CTA would leave the fast ones idle).
-  const int64_t G = work_stride<kCl>(pl);
+  const int64_t G = gridDim.x;
   ch.k = static_cast<int>(G % p.D == 0 ? (w + w / G) % p.D : w % p.D);
   const uint32_t dir = p.dirbit[ch.k];
   ch.vert = (dir == GSPN_DIR_T2B) || (dir == GSPN_DIR_B2T);
@@ -200,10 +168,8 @@ __device__ __forceinline__ Chain make_chain(const ScanParams& p, const Plan& pl,
   ch.chain = (ch.k * p.B + b) * p.C + c;
   ch.wplane = (ch.k * p.B + b) * p.G + g;
   ch.L = static_cast<int>(ch.vert ? p.H : p.W);
-  ch.psub = static_cast<int>(ch.vert ? p.W : p.H);
-  ch.P = ch.psub * pl.npack;
-  ch.nvalid = static_cast<int>(pl.nbc - bc < pl.npack ? pl.nbc - bc : pl.npack);
-  ch.ntiles = (ch.L + pl.K - 1) / pl.K;
+  ch.P = static_cast<int>(ch.vert ? p.W : p.H);
+  ch.ntiles = (ch.L + K - 1) / K;
   return ch;
 }
 
@@ -229,7 +195,7 @@ __device__ __forceinline__ int64_t plane_of(const Chain& ch, int slot) {
 
 // ------------------------------------------------------------------------------ producer / storer
 
-template <bool kBwd, bool kCl>
+template <bool kBwd>
 __device__ void producer_loop(const StreamArgs& A, uint8_t* ring, uint64_t* full, uint64_t* empty) {
   const Plan& pl = A.plan;
   const uint64_t pol_xin = policy_of(pl.pol[0]);
@@ -237,9 +203,8 @@ __device__ void producer_loop(const StreamArgs& A, uint8_t* ring, uint64_t* full
   const uint64_t pol_hin = policy_of(pl.pol[2]);
   int stage = 0;
   uint32_t phase = 0;
-  const int base = tile_base<kCl>(pl);
-  for (int64_t w = work_first<kCl>(pl); w < pl.nchains; w += work_stride<kCl>(pl)) {
-    const Chain ch = make_chain<kCl>(A.p, pl, w);
+  for (int64_t w = blockIdx.x; w < pl.nchains; w += gridDim.x) {
+    const Chain ch = make_chain(A.p, pl.K, w);
     const int o = ch.vert ? 0 : 1;
     for (int jj = 0; jj < ch.ntiles; ++jj) {
       const int j = kBwd ? (ch.ntiles - 1 - jj) : jj;
@@ -253,15 +218,11 @@ __device__ void producer_loop(const StreamArgs& A, uint8_t* ring, uint64_t* full
         // x is re-read by the plane's other directions; vertical streams are read exactly once
         const uint64_t pol = (!kBwd && t == F_X) ? pol_xin : (ch.vert ? pol_vin : pol_hin);
         const uint32_t dst = st + t * pl.tile_bytes;
-        if (pl.npack > 1) {  // one 3D box: vertical (W, planes, rows), horizontal (cols, H, planes)
-          if (ch.vert) tma_load3(dst, &A.in[0][t], 0, plane, s0, fb, pol);
-          else tma_load3(dst, &A.in[1][t], s0, 0, plane, fb, pol);
-        } else if (ch.vert) {
+        if (ch.vert) {
           for (int q = 0; q < pl.nbw; ++q)
-            tma_load3(dst + q * pl.K * pl.bw * pl.es, &A.in[o][t], base + q * pl.bw, s0, plane, fb, pol);
+            tma_load3(dst + q * pl.K * pl.bw * pl.es, &A.in[o][t], q * pl.bw, s0, plane, fb, pol);
         } else {
-          for (int q = 0; q < pl.nbh; ++q)
-            tma_load3(dst + q * pl.bh * 32, &A.in[o][t], s0, base + q * pl.bh, plane, fb, pol);
+          for (int q = 0; q < pl.nbh; ++q) tma_load3(dst + q * pl.bh * 32, &A.in[o][t], s0, q * pl.bh, plane, fb, pol);
         }
       }
       if (++stage == pl.nstages) { stage = 0; phase ^= 1; }
@@ -273,15 +234,14 @@ __device__ void producer_loop(const StreamArgs& A, uint8_t* ring, uint64_t* full
 // input rows) the storer sends them out with TMA, waits until the bulk copy has read shared memory,
 // and only then hands the stage back to the producer. Vertical tiles store from registers, so their
 // stage is released as soon as the consumers are done with it.
-template <bool kCl>
 __device__ void storer_loop(const StreamArgs& A, uint8_t* ring, uint64_t* done, uint64_t* empty, int nout,
                             const int* slots, bool bwd) {
   const Plan& pl = A.plan;
   const uint64_t pol = policy_of(pl.pol[4]);
   int stage = 0;
   uint32_t phase = 0;
-  for (int64_t w = work_first<kCl>(pl); w < pl.nchains; w += work_stride<kCl>(pl)) {
-    const Chain ch = make_chain<kCl>(A.p, pl, w);
+  for (int64_t w = blockIdx.x; w < pl.nchains; w += gridDim.x) {
+    const Chain ch = make_chain(A.p, pl.K, w);
     for (int jj = 0; jj < ch.ntiles; ++jj) {
       const int j = bwd ? (ch.ntiles - 1 - jj) : jj;
       mbar_wait(smem_u32(&done[stage]), phase);
@@ -290,17 +250,8 @@ __device__ void storer_loop(const StreamArgs& A, uint8_t* ring, uint64_t* done, 
         const uint8_t* st = ring + static_cast<size_t>(stage) * pl.stage_bytes;
         for (int t = 0; t < nout; ++t) {
           const uint32_t src = smem_u32(st + static_cast<size_t>(slots[t]) * pl.tile_bytes);
-          if (pl.npack > 1) {
-            tma_store3(&A.out[1][t], src, s0, 0, static_cast<int>(ch.chain), pol);
-          } else if (kCl) {  // only the owned rows: the ghost rows belong to the neighbour CTAs
-            const int gh = pl.K / 2;
-            for (int q = 0; q < pl.nbhs; ++q)
-              tma_store3(&A.out[1][t], src + (gh + q * pl.bhs) * 32, s0, tile_base<kCl>(pl) + gh + q * pl.bhs,
-                         static_cast<int>(ch.chain), pol);
-          } else {
-            for (int q = 0; q < pl.nbh; ++q)
-              tma_store3(&A.out[1][t], src + q * pl.bh * 32, s0, q * pl.bh, static_cast<int>(ch.chain), pol);
-          }
+          for (int q = 0; q < pl.nbh; ++q)
+            tma_store3(&A.out[1][t], src + q * pl.bh * 32, s0, q * pl.bh, static_cast<int>(ch.chain), pol);
         }
         bulk_commit();
         bulk_wait_read0();
@@ -341,19 +292,15 @@ struct Lanes {
   bool own_h[kE];        // horizontal: slot owned and inside the tile
   uint32_t voff;         // vertical: byte offset of the lane's positions at kk = 0
   uint32_t hoff[kE];     // horizontal: slot row's byte offset, chunk 0 (chunk c: hoff ^ (c << 4))
-  int64_t vout;          // vertical: element offset of the lane's first position in row 0 of its plane
+  int pos0;              // vertical: first position
   // tap unpack masks [tap l/m/r][element e | slot q][half / (and, or)]
   uint32_t s[3][kE][2];
 };
 
-// r: tile position; psub: positions per chain; nvalid: chains present (packing). A chain's taps at its
-// own first / last position are dropped, which also decouples packed neighbours.
 template <typename T>
-__device__ __forceinline__ void tap_masks(int r, int psub, int nvalid, uint32_t (&sl)[2], uint32_t (&sm)[2],
-                                          uint32_t (&sr)[2], int half_for_bf16) {
-  const bool valid = r >= 0 && r < psub * nvalid;
-  const int rl = valid ? r % psub : 0;
-  const bool kl = valid && rl >= 1, kr = valid && rl <= psub - 2;
+__device__ __forceinline__ void tap_masks(int r, int P, uint32_t (&sl)[2], uint32_t (&sm)[2], uint32_t (&sr)[2],
+                                          int half_for_bf16) {
+  const bool valid = r >= 0 && r < P, kl = valid && r >= 1, kr = valid && r <= P - 2;
   if constexpr (sizeof(T) == 2) {
     // half_for_bf16: -1 -> fill both halves (horizontal slot), 0/1 -> element in the low/high half
     for (int hh = 0; hh < 2; ++hh) {
@@ -370,50 +317,38 @@ __device__ __forceinline__ void tap_masks(int r, int psub, int nvalid, uint32_t 
   }
 }
 
-template <typename T, bool kCl>
-__device__ __forceinline__ Lanes<T> make_lanes(const Plan& pl, const ScanParams& p, const Chain& ch, int wi,
-                                               int lane) {
+template <typename T>
+__device__ __forceinline__ Lanes<T> make_lanes(const Plan& pl, const Chain& ch, int wi, int lane) {
   using C = Cfg<T>;
   constexpr int WARP = 32 * kE, OWN = WARP - 2 * C::GH;
   Lanes<T> ln;
-  const int base = tile_base<kCl>(pl);  // tile row = position - base
-  ln.A = (kCl ? base : -C::GH) + wi * OWN;
+  ln.A = wi * OWN - C::GH;
   constexpr int lo = C::GH;
-  const int nval = ch.psub * ch.nvalid;
   // vertical
   {
     const int off = kE * lane;
     const int r0 = ln.A + off;
-    ln.own_v = off >= lo && off < WARP - C::GH && r0 >= 0 && r0 < nval;
-    const int rt = r0 - base;
-    const int rc = rt < 0 ? 0 : (rt > kPpad - kE ? kPpad - kE : rt);
-    if (pl.npack > 1) {
-      ln.voff = static_cast<uint32_t>(rc * C::es);
-    } else {
-      const int bw = kRowB / C::es;
-      ln.voff = static_cast<uint32_t>((rc / bw) * (C::K * kRowB) + (rc % bw) * C::es);
-    }
-    const int rv = r0 < 0 ? 0 : r0;
-    ln.vout = (ch.chain + rv / ch.psub) * (p.H * p.W) + rv % ch.psub;  // P % kE == 0: both positions in one chain
+    ln.pos0 = r0;
+    ln.own_v = off >= lo && off < WARP - C::GH && r0 < ch.P;
+    const int rc = r0 < 0 ? 0 : (r0 > kPpad - kE ? kPpad - kE : r0);
+    const int bw = kRowB / C::es;
+    ln.voff = static_cast<uint32_t>((rc / bw) * (C::K * kRowB) + (rc % bw) * C::es);
   }
   // horizontal
 #pragma unroll
   for (int q = 0; q < kE; ++q) {
     const int off = 32 * q + lane;
     const int r = ln.A + off;
-    const int rt = r - base;
-    ln.own_h[q] = off >= lo && off < WARP - C::GH && rt < kPpad;  // rows >= P: outside the store box
-    const uint32_t rc = static_cast<uint32_t>(rt < 0 ? 0 : (rt >= kPpad ? kPpad - 1 : rt));
+    ln.own_h[q] = off >= lo && off < WARP - C::GH && r < kPpad;
+    const uint32_t rc = static_cast<uint32_t>(r < 0 ? 0 : (r >= kPpad ? kPpad - 1 : r));
     ln.hoff[q] = rc * 32 + (((rc >> 2) & 1u) << 4);
   }
   if (ch.vert) {
 #pragma unroll
-    for (int e = 0; e < kE; ++e)
-      tap_masks<T>(ln.A + kE * lane + e, ch.psub, ch.nvalid, ln.s[0][e], ln.s[1][e], ln.s[2][e], e);
+    for (int e = 0; e < kE; ++e) tap_masks<T>(ln.A + kE * lane + e, ch.P, ln.s[0][e], ln.s[1][e], ln.s[2][e], e);
   } else {
 #pragma unroll
-    for (int q = 0; q < kE; ++q)
-      tap_masks<T>(ln.A + 32 * q + lane, ch.psub, ch.nvalid, ln.s[0][q], ln.s[1][q], ln.s[2][q], -1);
+    for (int q = 0; q < kE; ++q) tap_masks<T>(ln.A + 32 * q + lane, ch.P, ln.s[0][q], ln.s[1][q], ln.s[2][q], -1);
   }
   return ln;
 }
@@ -501,13 +436,11 @@ __device__ __forceinline__ void edge_reload(const float* edge, int par, int wi, 
   }
 }
 
-// Shared-memory carve-up common to both kernels: ring | full | empty | done | edges | cluster edges.
+// Shared-memory carve-up common to both kernels: ring | full | empty | done | edges.
 struct Smem {
   uint8_t* ring;
   uint64_t *full, *empty, *done;
   float* edge;
-  float *xl, *xr;   // P-split: ghost values from the left / right neighbour CTA [3 arrays][2 par][8]
-  uint64_t* xb;     // P-split: [0..1] left-neighbour data landed (par), [2..3] right-neighbour data landed
 };
 
 __device__ __forceinline__ Smem carve(uint8_t* smem_raw, const Plan& pl) {
@@ -517,101 +450,19 @@ __device__ __forceinline__ Smem carve(uint8_t* smem_raw, const Plan& pl) {
   m.empty = m.full + pl.nstages;
   m.done = m.empty + pl.nstages;
   m.edge = reinterpret_cast<float*>(m.done + pl.nstages);  // [3 state arrays][2 par][kEdgeW][2][8]
-  m.xl = m.edge + 3 * 2 * kEdgeW * 2 * 8;
-  m.xr = m.xl + 3 * 2 * 8;
-  m.xb = reinterpret_cast<uint64_t*>(m.xr + 3 * 2 * 8);
   return m;
 }
 
-template <bool kCl>
 __device__ __forceinline__ void init_barriers(const Smem& m, const Plan& pl) {
-  // Packed tiles: zero the ring once; lanes may read tile rows past the packed chains that no TMA box
-  // writes, and those rows must hold finite values (zero, or earlier tiles' data). Unpacked plans
-  // size their boxes to cover every row a lane reads.
-  if (pl.npack > 1) {
-    uint4* r = reinterpret_cast<uint4*>(m.ring);
-    const uint32_t n = pl.nstages * pl.stage_bytes / 16;
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) r[i] = make_uint4(0u, 0u, 0u, 0u);
-    fence_proxy_async();  // generic-proxy zeros ordered before the TMA (async-proxy) writes
-  }
   if (threadIdx.x == 0) {
     for (int s = 0; s < pl.nstages; ++s) {
       mbar_init(smem_u32(&m.full[s]), 1);       // producer arrive + TMA bytes
       mbar_init(smem_u32(&m.empty[s]), 1);      // storer
       mbar_init(smem_u32(&m.done[s]), pl.nwc);  // one arrive per consumer warp
     }
-    for (int i = 0; i < 4; ++i) mbar_init(smem_u32(&m.xb[i]), 32);  // one arrive per lane of the sending warp
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  if constexpr (kCl) cluster_sync_all();  // neighbours' barriers initialised before any remote access
-}
-
-// ---- P-split ghost exchange between the CTAs of a cluster (after the intra-CTA publish).
-// Warp 0 of CTA s sends its first GH owned values to CTA s-1 (they are that CTA's right ghosts), the
-// last warp sends its last GH owned values to CTA s+1; every lane of a sending warp then arrives on
-// the receiver's barrier (release at cluster scope). Parity-double-buffered like the local edges;
-// a sender cannot run two halves ahead because it needs the receiver's edges of the half between.
-// side 0: towards rank - 1, side 1: towards rank + 1.
-__device__ __forceinline__ bool xgo(int side, int wi, int nwc, int rank, int cl) {
-  return side == 0 ? (wi == 0 && rank > 0) : (wi == nwc - 1 && rank < cl - 1);
-}
-
-template <typename T>
-__device__ __forceinline__ void xput(const Smem& m, int par, int side, uint32_t tr, int a, int lane, bool vert,
-                                     const float (&v)[kE]) {
-  using C = Cfg<T>;
-  constexpr int WARP = 32 * kE;
-  float* dst = (side == 0 ? m.xr : m.xl) + (a * 2 + par) * 8;  // left-going data = receiver's right ghosts
-  if (vert) {
-    const int o = kE * lane;
-    const int lo = side == 0 ? C::GH : WARP - 2 * C::GH;
-    if (o >= lo && o < lo + C::GH) {
-#pragma unroll
-      for (int e = 0; e < kE; ++e) st_cluster_f32(mapa(smem_u32(dst + o - lo + e), tr), v[e]);
-    }
-  } else {
-    const int lo = side == 0 ? C::GH : 32 - 2 * C::GH;
-    if (lane >= lo && lane < lo + C::GH) st_cluster_f32(mapa(smem_u32(dst + lane - lo), tr), side == 0 ? v[0] : v[kE - 1]);
-  }
-}
-
-__device__ __forceinline__ void xarrive(const Smem& m, int par, int side, uint32_t tr) {
-  __syncwarp();
-  mbar_arrive_remote(mapa(smem_u32(&m.xb[(side == 0 ? 2 : 0) + par]), tr));
-}
-
-__device__ __forceinline__ void xwait(const Smem& m, int par, int side, uint32_t xphase) {
-  mbar_wait_cluster(smem_u32(&m.xb[(side == 0 ? 0 : 2) + par]), xphase);
-}
-
-template <typename T>
-__device__ __forceinline__ void xget(const Smem& m, int par, int side, int a, int lane, bool vert, float (&v)[kE]) {
-  using C = Cfg<T>;
-  constexpr int WARP = 32 * kE;
-  const float* src = (side == 0 ? m.xl : m.xr) + (a * 2 + par) * 8;
-  if (vert) {
-    const int o = kE * lane;
-    const int lo = side == 0 ? 0 : WARP - C::GH;
-    if (o >= lo && o < lo + C::GH) {
-#pragma unroll
-      for (int e = 0; e < kE; ++e) v[e] = src[o - lo + e];
-    }
-  } else {
-    const int lo = side == 0 ? 0 : 32 - C::GH;
-    if (lane >= lo && lane < lo + C::GH) {
-      if (side == 0) v[0] = src[lane - lo];
-      else v[kE - 1] = src[lane - lo];
-    }
-  }
-}
-
-// Every thread of every role passes one final cluster barrier: no CTA leaves while a neighbour may
-// still address its shared memory.
-template <bool kCl>
-__device__ __forceinline__ void cluster_exit() {
-  __syncwarp();
-  if constexpr (kCl) cluster_sync_all();
 }
 
 __device__ __forceinline__ float clamped_rcp(float s) { return fminf(fast_rcp(s), kRcpMax); }
@@ -702,42 +553,38 @@ __device__ __forceinline__ void fwd_half_horiz(const Lanes<T>& ln, const uint8_t
   for (int q = 0; q < kE; ++q) OUT[q] = Pk<T>::pack(O[q]);
 }
 
-template <typename T, bool kPre, bool kCl>
+template <typename T, bool kPre>
 __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) fwd_stream_kernel(const __grid_constant__ StreamArgs A) {
   using C = Cfg<T>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const Plan& pl = A.plan;
   const Smem m = carve(smem_raw, pl);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  init_barriers<kCl>(m, pl);
+  init_barriers(m, pl);
   if (warp == pl.nwc) {  // producer warp
     if (lane == 0) {
       for (int o = 0; o < 2; ++o)
         for (int t = 0; t < F_NIN; ++t) asm volatile("prefetch.tensormap [%0];" ::"l"(&A.in[o][t]) : "memory");
-      producer_loop<false, kCl>(A, m.ring, m.full, m.empty);
+      producer_loop<false>(A, m.ring, m.full, m.empty);
     }
-    cluster_exit<kCl>();
     return;
   }
   if (warp == pl.nwc + 1) {  // storer warp
     if (lane == 0) {
       const int slots[1] = {F_X};
-      storer_loop<kCl>(A, m.ring, m.done, m.empty, 1, slots, false);
+      storer_loop(A, m.ring, m.done, m.empty, 1, slots, false);
     }
-    cluster_exit<kCl>();
     return;
   }
   const uint64_t pol_vout = policy_of(pl.pol[3]);
   const int nthreads = pl.nwc * 32;
-  const int64_t W = A.p.W;
-  const int rank = kCl ? static_cast<int>(cluster_ctarank()) : 0;
-  uint32_t xphase = 0;  // P-split: phase bit of the cluster edge barriers, per parity
+  const int64_t HW = A.p.H * A.p.W, W = A.p.W;
   int stage = 0, par = 0;
   uint32_t phase = 0;
-  for (int64_t w = work_first<kCl>(pl); w < pl.nchains; w += work_stride<kCl>(pl)) {
-    const Chain ch = make_chain<kCl>(A.p, pl, w);
-    const Lanes<T> ln = make_lanes<T, kCl>(pl, A.p, ch, warp, lane);
-    T* hout = static_cast<T*>(A.p.hout) + ln.vout;
+  for (int64_t w = blockIdx.x; w < pl.nchains; w += gridDim.x) {
+    const Chain ch = make_chain(A.p, C::K, w);
+    const Lanes<T> ln = make_lanes<T>(pl, ch, warp, lane);
+    T* hplane = static_cast<T*>(A.p.hout) + ch.chain * HW;
     float h[kE] = {0.f, 0.f};
     for (int j = 0; j < ch.ntiles; ++j) {
       mbar_wait(smem_u32(&m.full[stage]), phase);
@@ -752,9 +599,9 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) fwd_stream_kernel(const
             const int t0 = j * C::K + half * C::KS;
             const int kk0 = ch.rev ? C::K - 1 - half * C::KS : half * C::KS;
             const int row0 = ch.rev ? ch.L - 1 - t0 : t0;
-            const int vs = static_cast<int>(pl.vstep);
-            fwd_half_vert<T, kPre>(ln, st + ln.voff + kk0 * vs, ch.rev ? -vs : vs,
-                                   hout + static_cast<int64_t>(row0) * W, ch.rev ? -W : W, t0, ch.L, h, pol_vout);
+            fwd_half_vert<T, kPre>(ln, st + ln.voff + kk0 * kRowB, ch.rev ? -kRowB : kRowB,
+                                   hplane + static_cast<int64_t>(row0) * W + ln.pos0, ch.rev ? -W : W, t0, ch.L, h,
+                                   pol_vout);
           } else if (ch.rev) {
             fwd_half_horiz<T, kPre, true>(ln, st, cm, lane, h, OUT);
           } else {
@@ -762,26 +609,8 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) fwd_stream_kernel(const
           }
         }
         edge_publish<T>(m.edge, par, warp, lane, ch.vert, h);
-        if constexpr (kCl) {
-#pragma unroll
-          for (int side = 0; side < 2; ++side) {
-            if (!xgo(side, warp, pl.nwc, rank, pl.cl)) continue;
-            const uint32_t tr = static_cast<uint32_t>(side == 0 ? rank - 1 : rank + 1);
-            xput<T>(m, par, side, tr, 0, lane, ch.vert, h);
-            xarrive(m, par, side, tr);
-          }
-        }
         named_bar(kBarEdge, nthreads);  // edges published; every warp has read this half's input rows
         edge_reload<T>(m.edge, par, warp, pl.nwc, lane, ch.vert, h);
-        if constexpr (kCl) {
-#pragma unroll
-          for (int side = 0; side < 2; ++side) {
-            if (!xgo(side, warp, pl.nwc, rank, pl.cl)) continue;
-            xwait(m, par, side, (xphase >> par) & 1u);
-            xget<T>(m, par, side, 0, lane, ch.vert, h);
-          }
-          xphase ^= 1u << par;
-        }
         par ^= 1;
         if (!ch.vert && !pl.null_compute) {  // new states in place over the x chunk of this half
 #pragma unroll
@@ -796,7 +625,6 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) fwd_stream_kernel(const
       if (++stage == pl.nstages) { stage = 0; phase ^= 1; }
     }
   }
-  cluster_exit<kCl>();
 }
 
 // ------------------------------------------------------------------------------ backward recurrence
@@ -872,43 +700,39 @@ __device__ __forceinline__ void bwd_half_horiz(const Lanes<T>& ln, const uint8_t
   for (int q = 0; q < kE; ++q) OG[q] = Pk<T>::pack(G_[q]);
 }
 
-template <typename T, bool kPre, bool kCl>
+template <typename T, bool kPre>
 __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_stream_kernel(const __grid_constant__ StreamArgs A) {
   using C = Cfg<T>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const Plan& pl = A.plan;
   const Smem m = carve(smem_raw, pl);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  init_barriers<kCl>(m, pl);
+  init_barriers(m, pl);
   if (warp == pl.nwc) {
     if (lane == 0) {
       for (int o = 0; o < 2; ++o)
         for (int t = 0; t < B_NIN; ++t) asm volatile("prefetch.tensormap [%0];" ::"l"(&A.in[o][t]) : "memory");
-      producer_loop<true, kCl>(A, m.ring, m.full, m.empty);
+      producer_loop<true>(A, m.ring, m.full, m.empty);
     }
-    cluster_exit<kCl>();
     return;
   }
   if (warp == pl.nwc + 1) {  // storer warp: horizontal tiles' g (written over the dh slot)
     if (lane == 0) {
       const int slots[1] = {B_DH};
-      storer_loop<kCl>(A, m.ring, m.done, m.empty, 1, slots, true);
+      storer_loop(A, m.ring, m.done, m.empty, 1, slots, true);
     }
-    cluster_exit<kCl>();
     return;
   }
   const uint64_t pol_vout = policy_of(pl.pol[3]);
   const int nthreads = pl.nwc * 32;
   constexpr int kEdgeArr = 2 * kEdgeW * 2 * 8;
-  const int64_t W = A.p.W;
-  const int rank = kCl ? static_cast<int>(cluster_ctarank()) : 0;
-  uint32_t xphase = 0;
+  const int64_t HW = A.p.H * A.p.W, W = A.p.W;
   int stage = 0, par = 0;
   uint32_t phase = 0;
-  for (int64_t w = work_first<kCl>(pl); w < pl.nchains; w += work_stride<kCl>(pl)) {
-    const Chain ch = make_chain<kCl>(A.p, pl, w);
-    const Lanes<T> ln = make_lanes<T, kCl>(pl, A.p, ch, warp, lane);
-    T* gout = static_cast<T*>(A.g) + ln.vout;
+  for (int64_t w = blockIdx.x; w < pl.nchains; w += gridDim.x) {
+    const Chain ch = make_chain(A.p, C::K, w);
+    const Lanes<T> ln = make_lanes<T>(pl, ch, warp, lane);
+    T* gplane = static_cast<T*>(A.g) + ch.chain * HW;
     BwdState S;
 #pragma unroll
     for (int e = 0; e < kE; ++e) S.ea[e] = S.eb[e] = S.ec[e] = 0.f;
@@ -927,9 +751,9 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_stream_kernel(const
             const int tl = t0 + C::KS - 1;                     // processed first
             const int kkl = ch.rev ? C::K - 1 - (half * C::KS + C::KS - 1) : half * C::KS + C::KS - 1;
             const int rowl = ch.rev ? ch.L - 1 - tl : tl;
-            const int vs = static_cast<int>(pl.vstep);
-            bwd_half_vert<T, kPre>(ln, st + ln.voff + kkl * vs, ch.rev ? vs : -vs,
-                                   gout + static_cast<int64_t>(rowl) * W, ch.rev ? W : -W, t0, ch.L, S, pol_vout);
+            bwd_half_vert<T, kPre>(ln, st + ln.voff + kkl * kRowB, ch.rev ? kRowB : -kRowB,
+                                   gplane + static_cast<int64_t>(rowl) * W + ln.pos0, ch.rev ? W : -W, t0, ch.L, S,
+                                   pol_vout);
           } else if (ch.rev) {
             bwd_half_horiz<T, kPre, true>(ln, st, cm, lane, S, OG);
           } else {
@@ -939,32 +763,10 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_stream_kernel(const
         edge_publish<T>(m.edge + 0 * kEdgeArr, par, warp, lane, ch.vert, S.ea);
         edge_publish<T>(m.edge + 1 * kEdgeArr, par, warp, lane, ch.vert, S.eb);
         edge_publish<T>(m.edge + 2 * kEdgeArr, par, warp, lane, ch.vert, S.ec);
-        if constexpr (kCl) {
-#pragma unroll
-          for (int side = 0; side < 2; ++side) {
-            if (!xgo(side, warp, pl.nwc, rank, pl.cl)) continue;
-            const uint32_t tr = static_cast<uint32_t>(side == 0 ? rank - 1 : rank + 1);
-            xput<T>(m, par, side, tr, 0, lane, ch.vert, S.ea);
-            xput<T>(m, par, side, tr, 1, lane, ch.vert, S.eb);
-            xput<T>(m, par, side, tr, 2, lane, ch.vert, S.ec);
-            xarrive(m, par, side, tr);
-          }
-        }
         named_bar(kBarEdge, nthreads);  // edges published; every warp has read this half's input rows
         edge_reload<T>(m.edge + 0 * kEdgeArr, par, warp, pl.nwc, lane, ch.vert, S.ea);
         edge_reload<T>(m.edge + 1 * kEdgeArr, par, warp, pl.nwc, lane, ch.vert, S.eb);
         edge_reload<T>(m.edge + 2 * kEdgeArr, par, warp, pl.nwc, lane, ch.vert, S.ec);
-        if constexpr (kCl) {
-#pragma unroll
-          for (int side = 0; side < 2; ++side) {
-            if (!xgo(side, warp, pl.nwc, rank, pl.cl)) continue;
-            xwait(m, par, side, (xphase >> par) & 1u);
-            xget<T>(m, par, side, 0, lane, ch.vert, S.ea);
-            xget<T>(m, par, side, 1, lane, ch.vert, S.eb);
-            xget<T>(m, par, side, 2, lane, ch.vert, S.ec);
-          }
-          xphase ^= 1u << par;
-        }
         par ^= 1;
         if (!ch.vert && !pl.null_compute) {
 #pragma unroll
@@ -979,7 +781,6 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_stream_kernel(const
       if (++stage == pl.nstages) { stage = 0; phase ^= 1; }
     }
   }
-  cluster_exit<kCl>();
 }
 
 // ------------------------------------------------------------------------------ backward outputs
@@ -1541,180 +1342,6 @@ __global__ void __launch_bounds__((kOutConsumers + 1) * 32, 1) bwd_out_tma_kerne
   }
 }
 
-// ---- Grouped weights (G < C): a unit is (b, group, RB rows); the ring streams one channel of the
-// group per stage (x, and per direction g, lam and the h halo tile), every thread keeps the group sums
-// Da/Db/Dc of its 4-column chunk for all directions in registers, and after the group's last channel
-// reads w from global memory once and writes dw. One chunk per consumer thread (RB W / 4 <= 512).
-template <typename T>
-__global__ void __launch_bounds__((kOutConsumers + 1) * 32, 1) bwd_out_grp_tma_kernel(const __grid_constant__ OutArgs A) {
-  constexpr int V = 4;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* ring = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t* full = reinterpret_cast<uint64_t*>(ring + static_cast<size_t>(A.nstages) * A.stage_bytes);
-  uint64_t* empty = full + A.nstages;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const ScanParams& p = A.p;
-  const int D = p.D, RB = A.RB, BX = A.BX;
-  const int64_t Cg = p.C / p.G;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < A.nstages; ++s) {
-      mbar_init(smem_u32(&full[s]), 1);
-      mbar_init(smem_u32(&empty[s]), kOutConsumers);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  if (warp == kOutConsumers) {  // producer
-    if (lane == 0) {
-      const uint64_t pol = policy_of(0);
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int64_t u = blockIdx.x; u < A.nunits; u += gridDim.x) {
-        const int64_t bg = u / A.nrb;
-        const int i0 = static_cast<int>(u % A.nrb) * RB;
-        const int64_t b = bg / p.G, grp = bg % p.G;
-        for (int64_t cc = 0; cc < Cg; ++cc) {
-          const int64_t bc = b * p.C + grp * Cg + cc;
-          mbar_wait_sleep(smem_u32(&empty[stage]), phase ^ 1);
-          const uint32_t fb = smem_u32(&full[stage]);
-          mbar_arrive_tx(fb, A.tx);
-          const uint32_t st = smem_u32(ring + static_cast<size_t>(stage) * A.stage_bytes);
-          for (int bx = 0; bx < A.nbx; ++bx) tma_load3(st + bx * A.box_rb, &A.x, bx * BX, i0, static_cast<int>(bc), fb, pol);
-          for (int k = 0; k < D; ++k) {
-            const int chain = static_cast<int>(static_cast<int64_t>(k) * p.B * p.C + bc);
-            const uint32_t base = st + A.tile_rb + k * A.per_k;
-            for (int bx = 0; bx < A.nbx; ++bx) {
-              tma_load3(base + bx * A.box_rb, &A.g, bx * BX, i0, chain, fb, pol);
-              tma_load3(base + A.tile_rb + bx * A.box_rb, &A.lam, bx * BX, i0, chain, fb, pol);
-              tma_load3(base + 2 * A.tile_rb + bx * A.box_h, &A.h, bx * BX, i0 - 1, chain, fb, policy_of(1));
-            }
-          }
-          if (++stage == A.nstages) { stage = 0; phase ^= 1; }
-        }
-      }
-    }
-    return;
-  }
-  const bool prenorm = p.flags & GSPN_FLAG_PRENORMALIZED;
-  const int64_t H = p.H, W = p.W, HW = H * W;
-  const int64_t kstride = p.B * p.C * HW;   // direction slabs of lam / g / h / dlam
-  const int64_t kwstride = p.B * p.G * HW;  // direction slabs of w / dw
-  const int nchunk = static_cast<int>(W / V);
-  constexpr int es = static_cast<int>(sizeof(T));
-  const uint32_t rowb = static_cast<uint32_t>(BX * es);
-  const int idx = threadIdx.x;  // this thread's chunk (one per thread)
-  const int r = idx / nchunk;
-  const int j0 = (idx - r * nchunk) * V;
-  const int bx = j0 >= BX ? j0 / BX : 0;
-  const uint32_t col = static_cast<uint32_t>((j0 - bx * BX) * es);
-  const uint32_t orb = bx * A.box_rb + r * rowb + col;
-  const uint32_t oh = bx * A.box_h + r * rowb + col;
-  const bool has_lo = j0 > 0, has_hi = j0 + V < W;
-  const uint32_t ohl = (j0 - bx * BX) > 0 ? oh - es : (bx - 1) * A.box_h + r * rowb + (BX - 1) * es;
-  const uint32_t ohh = (j0 - bx * BX) + V < BX ? oh + V * es : (bx + 1) * A.box_h + r * rowb;
-  int stage = 0;
-  uint32_t phase = 0;
-  for (int64_t u = blockIdx.x; u < A.nunits; u += gridDim.x) {
-    const int64_t bg = u / A.nrb;
-    const int i0 = static_cast<int>(u % A.nrb) * RB;
-    const int64_t b = bg / p.G, grp = bg % p.G;
-    const int64_t i = i0 + r;
-    const bool valid = r < RB && i < H;
-    float Da[4][V], Db[4][V], Dc[4][V];
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-#pragma unroll
-      for (int q = 0; q < V; ++q) Da[k][q] = Db[k][q] = Dc[k][q] = 0.f;
-    for (int64_t cc = 0; cc < Cg; ++cc) {
-      mbar_wait(smem_u32(&full[stage]), phase);
-      const uint8_t* st = ring + static_cast<size_t>(stage) * A.stage_bytes;
-      if (valid) {
-        const int64_t bc = b * p.C + grp * Cg + cc;
-        const int64_t off0 = bc * HW + i * W + j0;
-        float xv[V], dx[V];
-        sm_ld4v<T>(st + orb, xv);
-#pragma unroll
-        for (int q = 0; q < V; ++q) dx[q] = 0.f;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          if (k >= D) break;
-          const uint8_t* base = st + A.tile_rb + k * A.per_k;
-          const uint8_t* ht = base + 2 * A.tile_rb;
-          const uint32_t dir = p.dirbit[k];
-          const int64_t off = off0 + k * kstride;
-          float gv[V], lv[V], dl[V];
-          sm_ld4v<T>(base + orb, gv);
-          sm_ld4v<T>(base + A.tile_rb + orb, lv);
-#pragma unroll
-          for (int q = 0; q < V; ++q) {
-            dl[q] = gv[q] * xv[q];
-            dx[q] = fmaf(gv[q], lv[q], dx[q]);
-          }
-          GVec<T, V>::store(static_cast<T*>(p.dlam) + off, dl);
-          if (dir == GSPN_DIR_T2B || dir == GSPN_DIR_B2T) {
-            const uint32_t ro = dir == GSPN_DIR_T2B ? 0u : 2u * rowb;
-            float v[V];
-            sm_ld4v<T>(ht + oh + ro, v);
-            const float lo = has_lo ? to_f(*reinterpret_cast<const T*>(ht + ohl + ro)) : 0.f;
-            const float hi = has_hi ? to_f(*reinterpret_cast<const T*>(ht + ohh + ro)) : 0.f;
-#pragma unroll
-            for (int q = 0; q < V; ++q) {
-              Da[k][q] = fmaf(gv[q], q > 0 ? v[q - 1] : lo, Da[k][q]);
-              Db[k][q] = fmaf(gv[q], v[q], Db[k][q]);
-              Dc[k][q] = fmaf(gv[q], q + 1 < V ? v[q + 1] : hi, Dc[k][q]);
-            }
-          } else {
-            const bool l2r = dir == GSPN_DIR_L2R;
-            const bool e_ok = l2r ? has_lo : has_hi;
-            const uint32_t oe = l2r ? ohl : ohh;
-#pragma unroll
-            for (int rr = 0; rr < 3; ++rr) {
-              float v[V];
-              sm_ld4v<T>(ht + oh + rr * rowb, v);
-              const float e = e_ok ? to_f(*reinterpret_cast<const T*>(ht + oe + rr * rowb)) : 0.f;
-#pragma unroll
-              for (int q = 0; q < V; ++q) {
-                const float sh = l2r ? (q > 0 ? v[q - 1] : e) : (q + 1 < V ? v[q + 1] : e);
-                if (rr == 0) Da[k][q] = fmaf(gv[q], sh, Da[k][q]);
-                else if (rr == 1) Db[k][q] = fmaf(gv[q], sh, Db[k][q]);
-                else Dc[k][q] = fmaf(gv[q], sh, Dc[k][q]);
-              }
-            }
-          }
-        }
-        GVec<T, V>::store(static_cast<T*>(p.dx) + off0, dx);
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&empty[stage]));
-      if (++stage == A.nstages) { stage = 0; phase ^= 1; }
-    }
-    if (valid) {
-      const int64_t woff0 = (b * p.G + grp) * HW + i * W + j0;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        if (k >= D) break;
-        const uint32_t dir = p.dirbit[k];
-        const bool vert = dir == GSPN_DIR_T2B || dir == GSPN_DIR_B2T;
-        const int64_t woff = woff0 + k * kwstride;
-        float wl[V], wm[V], wr[V], ol[V], om[V], orr[V];
-        GVec<T, V>::load(static_cast<const T*>(p.wl) + woff, wl);
-        GVec<T, V>::load(static_cast<const T*>(p.wm) + woff, wm);
-        GVec<T, V>::load(static_cast<const T*>(p.wr) + woff, wr);
-#pragma unroll
-        for (int q = 0; q < V; ++q) {
-          const int64_t rp = vert ? j0 + q : i;
-          const int64_t P = vert ? W : H;
-          jacobian<true>(wl[q], wm[q], wr[q], rp >= 1, rp <= P - 2, prenorm, Da[k][q], Db[k][q], Dc[k][q], ol[q],
-                         om[q], orr[q]);
-        }
-        GVec<T, V>::store(static_cast<T*>(p.dwl) + woff, ol);
-        GVec<T, V>::store(static_cast<T*>(p.dwm) + woff, om);
-        GVec<T, V>::store(static_cast<T*>(p.dwr) + woff, orr);
-      }
-    }
-  }
-}
-
 template <typename T, int V, bool kPerChannel>
 cudaError_t launch_out(const ScanParams& p, const void* g, cudaStream_t s) {
   constexpr int R = 8;
@@ -1739,22 +1366,14 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-// 3D map over a [planes][H][W] tensor. plane_mid: dims ordered (W, planes, H) instead of (W, H, planes)
-// (packed vertical tiles: one box = K rows of npack consecutive planes, step-major in shared memory).
 bool encode(CUtensorMap* m, const void* base, gspn_dtype_t dt, int64_t W, int64_t H, int64_t planes, int box0,
-            int box1, bool swizzle32, int box2 = 1, bool plane_mid = false) {
+            int box1, bool swizzle32) {
   auto fn = get_encode();
   if (!fn) return false;
   const size_t s = dt == GSPN_BF16 ? 2 : 4;
   cuuint64_t dims[3] = {static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H), static_cast<cuuint64_t>(planes)};
   cuuint64_t strides[2] = {static_cast<cuuint64_t>(W * s), static_cast<cuuint64_t>(W * H * s)};
-  if (plane_mid) {
-    dims[1] = static_cast<cuuint64_t>(planes);
-    dims[2] = static_cast<cuuint64_t>(H);
-    strides[0] = static_cast<cuuint64_t>(W * H * s);
-    strides[1] = static_cast<cuuint64_t>(W * s);
-  }
-  cuuint32_t box[3] = {static_cast<cuuint32_t>(box0), static_cast<cuuint32_t>(box1), static_cast<cuuint32_t>(box2)};
+  cuuint32_t box[3] = {static_cast<cuuint32_t>(box0), static_cast<cuuint32_t>(box1), 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(m, dt == GSPN_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
                   const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -1785,7 +1404,7 @@ int smem_optin() {
   return n;
 }
 
-constexpr int kSmemTail = 7168;  // mbarriers (3 per stage), ghost-edge buffers (6 KB), cluster edges + barriers
+constexpr int kSmemTail = 6656;  // mbarriers (3 per stage), ghost-edge buffers (6 KB), flag
 
 // Shape eligibility + plan (nin: tensors per tile).
 bool make_plan(const ScanParams& p, gspn_dtype_t dt, int nin, Plan* pl) {
@@ -1797,28 +1416,17 @@ bool make_plan(const ScanParams& p, gspn_dtype_t dt, int nin, Plan* pl) {
     if (p.dirbit[k] == GSPN_DIR_T2B || p.dirbit[k] == GSPN_DIR_B2T) any_v = true; else any_h = true;
   }
   const int64_t maxP = std::max<int64_t>(any_v ? p.W : 0, any_h ? p.H : 0);
+  if (maxP > kPpad) return false;
   memset(pl, 0, sizeof *pl);
   pl->K = 32 / s;
   const int GH = pl->K / 2;
   pl->E = 2;
   pl->es = s;
   pl->own = 64 - 2 * GH;
-  pl->cl = 1;
   pl->nwc = static_cast<int>((maxP + pl->own - 1) / pl->own);  // warp w owns [w own, (w+1) own)
+  if (pl->nwc > 11) return false;
   // positions any lane reads (clamped to the tile); the TMA boxes cover them so no lane reads stale rows
-  int cover = static_cast<int>(std::min<int64_t>(kPpad, (pl->nwc - 1) * pl->own - GH + 64));
-  if (pl->nwc > 11) {
-    // P-split over a cluster: each CTA owns the positions its warps own while their ghosts stay
-    // inside its 512-position tile (10 x 48 bf16 / 9 x 56 fp32)
-    const int nwc_c = (kPpad - 2 * GH) / pl->own;
-    pl->ownc = nwc_c * pl->own;
-    pl->cl = static_cast<int>((maxP + pl->ownc - 1) / pl->ownc);
-    if (pl->cl > 8 || getenv("GSPN_NOCLUSTER")) return false;
-    pl->nwc = nwc_c;
-    cover = kPpad;
-    pl->bhs = pl->ownc / 2;  // <= 256 rows per TMA store box
-    pl->nbhs = 2;
-  }
+  const int cover = static_cast<int>(std::min<int64_t>(kPpad, (pl->nwc - 1) * pl->own - GH + 64));
   pl->ppad = kPpad;
   pl->bw = kRowB / s;
   pl->nbw = (cover + pl->bw - 1) / pl->bw;
@@ -1831,29 +1439,12 @@ bool make_plan(const ScanParams& p, gspn_dtype_t dt, int nin, Plan* pl) {
   pl->stage_bytes = nin * kTile;
   pl->tx_v = static_cast<uint32_t>(nin * pl->nbw * pl->bw * pl->K * s);
   pl->tx_h = static_cast<uint32_t>(nin * pl->nbh * pl->bh * 32);
-  pl->npack = 1;
-  pl->nbc = p.B * p.C;
-  pl->vstep = kRowB;
-  const int64_t PH = std::max<int64_t>(p.H, p.W);  // packing needs both orientations to fit
-  if (pl->cl == 1 && p.G == p.C && PH <= kPpad / 2 && pl->nbc > 1 && !getenv("GSPN_NOPACK")) {
-    // a divisor of B C: no partial pack, so a packed TMA store never spills into the next direction
-    int np = static_cast<int>(std::min<int64_t>({kPpad / PH, 256, pl->nbc}));
-    while (pl->nbc % np != 0) --np;
-    if (np >= 2) {
-      pl->npack = np;
-      pl->vstep = static_cast<uint32_t>(np * p.W * s);
-      pl->nwc = static_cast<int>((np * PH + pl->own - 1) / pl->own);
-      if (pl->nwc > 11) return false;
-      pl->tx_v = static_cast<uint32_t>(nin * np * p.W * pl->K * s);
-      pl->tx_h = static_cast<uint32_t>(nin * np * p.H * 32);
-    }
-  }
   const int budget = smem_optin() - 1024 /*alignment*/ - kSmemTail;
   int ns = budget / static_cast<int>(pl->stage_bytes);
   if (ns > 6) ns = 6;
   if (ns < 2) return false;
   pl->nstages = ns;
-  pl->nchains = p.D * ((pl->nbc + pl->npack - 1) / pl->npack);  // work items: packs of chains
+  pl->nchains = p.D * p.B * p.C;
   pl->smem_bytes = 1024 + ns * pl->stage_bytes + kSmemTail;
   // L2 priorities (experiments: GSPN_POL="x,vin,hin,vout,hout,acc", each 0|1|2)
   static const int def_pol[6] = {1, 0, 1, 0, 1, 1};
@@ -1871,22 +1462,12 @@ bool fill_maps(StreamArgs* A, const void* const* ins, int nin, void* const* outs
                int64_t out_planes, int nout, gspn_dtype_t dt) {
   const Plan& pl = A->plan;
   const ScanParams& p = A->p;
-  if (pl.npack > 1) {
-    for (int t = 0; t < nin; ++t) {
-      if (!encode(&A->in[0][t], ins[t], dt, p.W, p.H, in_planes[t], p.W, pl.npack, false, pl.K, true)) return false;
-      if (!encode(&A->in[1][t], ins[t], dt, p.W, p.H, in_planes[t], pl.K, p.H, true, pl.npack)) return false;
-    }
-    for (int t = 0; t < nout; ++t)
-      if (!encode(&A->out[1][t], outs[t], dt, p.W, p.H, out_planes, pl.K, p.H, true, pl.npack)) return false;
-    return true;
-  }
   for (int t = 0; t < nin; ++t) {
     if (!encode(&A->in[0][t], ins[t], dt, p.W, p.H, in_planes[t], pl.bw, pl.K, false)) return false;
     if (!encode(&A->in[1][t], ins[t], dt, p.W, p.H, in_planes[t], pl.K, pl.bh, true)) return false;
   }
   for (int t = 0; t < nout; ++t)
-    if (!encode(&A->out[1][t], outs[t], dt, p.W, p.H, out_planes, pl.K, pl.cl > 1 ? pl.bhs : pl.bh, true))
-      return false;
+    if (!encode(&A->out[1][t], outs[t], dt, p.W, p.H, out_planes, pl.K, pl.bh, true)) return false;
   return true;
 }
 
@@ -1904,29 +1485,6 @@ cudaError_t launch(KernelT kernel, const StreamArgs& A, cudaStream_t s) {
   if (const char* ev = getenv("GSPN_GRID")) {  // experiments only: cap the persistent grid
     const int64_t g = atoll(ev);
     if (g > 0 && g < grid) grid = g;
-  }
-  if (A.plan.cl > 1) {  // P-split: clusters of cl CTAs, one chain per cluster at a time
-    cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = A.plan.cl;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.blockDim = dim3(threads, 1, 1);
-    cfg.dynamicSmemBytes = A.plan.smem_bytes;
-    cfg.stream = s;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cfg.gridDim = dim3(static_cast<unsigned>(A.plan.cl * 148), 1, 1);
-    int ncl = 0;
-    e = cudaOccupancyMaxActiveClusters(&ncl, kernel, &cfg);
-    if (e != cudaSuccess) return e;
-    if (ncl < 1) return cudaErrorInvalidConfiguration;
-    if (ncl > A.plan.nchains) ncl = static_cast<int>(A.plan.nchains);
-    cfg.gridDim = dim3(static_cast<unsigned>(ncl * A.plan.cl), 1, 1);
-    e = cudaLaunchKernelEx(&cfg, kernel, A);
-    if (e != cudaSuccess) return e;
-    return cudaGetLastError();
   }
   if (grid > A.plan.nchains) grid = A.plan.nchains;
   kernel<<<static_cast<unsigned>(grid), threads, A.plan.smem_bytes, s>>>(A);
@@ -1970,21 +1528,16 @@ cudaError_t launch_fwd_stream(const ScanParams& p, gspn_dtype_t dt, cudaStream_t
   using BF = __nv_bfloat16;
   const bool pre = p.flags & GSPN_FLAG_PRENORMALIZED;
   cudaError_t e;
-  const bool cl = A.plan.cl > 1;
-  if (dt == GSPN_BF16) {
-    if (cl) e = pre ? launch(fwd_stream_kernel<BF, true, true>, A, s) : launch(fwd_stream_kernel<BF, false, true>, A, s);
-    else e = pre ? launch(fwd_stream_kernel<BF, true, false>, A, s) : launch(fwd_stream_kernel<BF, false, false>, A, s);
-  } else {
-    if (cl) e = pre ? launch(fwd_stream_kernel<float, true, true>, A, s) : launch(fwd_stream_kernel<float, false, true>, A, s);
-    else e = pre ? launch(fwd_stream_kernel<float, true, false>, A, s) : launch(fwd_stream_kernel<float, false, false>, A, s);
-  }
+  if (dt == GSPN_BF16)
+    e = pre ? launch(fwd_stream_kernel<BF, true>, A, s) : launch(fwd_stream_kernel<BF, false>, A, s);
+  else
+    e = pre ? launch(fwd_stream_kernel<float, true>, A, s) : launch(fwd_stream_kernel<float, false>, A, s);
   *launches += 1;
   return e;
 }
 
 // TMA-staged output kernel (G = C). Returns false if the shape does not fit (caller falls back).
 bool launch_out_tma(const ScanParams& p, const void* g, gspn_dtype_t dt, cudaStream_t s, cudaError_t* err) {
-  const bool grouped = p.G != p.C;
   static OutArgs A;
   static std::mutex mu;
   std::lock_guard<std::mutex> lock(mu);
@@ -1997,17 +1550,12 @@ bool launch_out_tma(const ScanParams& p, const void* g, gspn_dtype_t dt, cudaStr
   const int D = static_cast<int>(p.D);
   const int budget = smem_optin() - 1024 - 256;
   auto pad = [](int64_t v) { return (v + 127) / 128 * 128; };
-  const int nrb_t = grouped ? 2 : 5;  // RB-row tiles per direction: g, lam (+ w_l, w_m, w_r)
   auto stage_of = [&](int rb) {
-    return A.nbx * (pad(es * A.BX * rb) * (1 + nrb_t * D) + pad(es * A.BX * (rb + 2)) * D);
+    return A.nbx * (pad(es * A.BX * rb) * (1 + 5 * D) + pad(es * A.BX * (rb + 2)) * D);
   };
   // enough rows per unit to give every consumer thread a 4-column chunk, 2+ stages
   int RB = 1;
   while (RB < 16 && RB * (p.W / 4) < kOutConsumers * 32) RB <<= 1;
-  if (grouped) {  // exactly one chunk per thread: the group sums live in its registers
-    while (RB > 1 && RB * (p.W / 4) > kOutConsumers * 32) RB >>= 1;
-    if (p.W / 4 > kOutConsumers * 32) return false;
-  }
   while (RB > 1 && 2 * stage_of(RB) > budget) RB >>= 1;
   if (2 * stage_of(RB) > budget) return false;
   A.RB = RB;
@@ -2015,12 +1563,12 @@ bool launch_out_tma(const ScanParams& p, const void* g, gspn_dtype_t dt, cudaStr
   A.box_h = static_cast<uint32_t>(pad(es * A.BX * (RB + 2)));
   A.tile_rb = A.nbx * A.box_rb;
   A.tile_h = A.nbx * A.box_h;
-  A.per_k = nrb_t * A.tile_rb + A.tile_h;
+  A.per_k = 5 * A.tile_rb + A.tile_h;
   A.stage_bytes = A.tile_rb + D * A.per_k;
-  A.tx = static_cast<uint32_t>(A.nbx * (es * A.BX * RB * (1 + nrb_t * D) + es * A.BX * (RB + 2) * D));  // payload
+  A.tx = static_cast<uint32_t>(A.nbx * (es * A.BX * RB * (1 + 5 * D) + es * A.BX * (RB + 2) * D));  // TMA payload
   A.nstages = static_cast<int>(std::min<int64_t>(6, budget / A.stage_bytes));
   A.nrb = static_cast<int>((p.H + RB - 1) / RB);
-  A.nunits = (grouped ? p.B * p.G : p.B * p.C) * A.nrb;
+  A.nunits = p.B * p.C * A.nrb;
   const int64_t nc = p.D * p.B * p.C;
   bool ok = encode(&A.x, p.x, dt, p.W, p.H, p.B * p.C, A.BX, RB, false) &&
             encode(&A.g, g, dt, p.W, p.H, nc, A.BX, RB, false) &&
@@ -2031,8 +1579,7 @@ bool launch_out_tma(const ScanParams& p, const void* g, gspn_dtype_t dt, cudaStr
             encode(&A.h, p.h, dt, p.W, p.H, nc, A.BX, RB + 2, false);
   if (!ok) return false;
   const uint32_t smem = 1024 + A.nstages * A.stage_bytes + 2 * 8 * A.nstages;
-  auto kern = grouped ? (dt == GSPN_BF16 ? bwd_out_grp_tma_kernel<__nv_bfloat16> : bwd_out_grp_tma_kernel<float>)
-                      : (dt == GSPN_BF16 ? bwd_out_tma_kernel<__nv_bfloat16> : bwd_out_tma_kernel<float>);
+  auto kern = dt == GSPN_BF16 ? bwd_out_tma_kernel<__nv_bfloat16> : bwd_out_tma_kernel<float>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e == cudaSuccess) {
     int per_sm = 0;
@@ -2069,18 +1616,14 @@ cudaError_t launch_bwd_stream(const ScanParams& p0, gspn_dtype_t dt, cudaStream_
   cudaError_t e;
   using BF = __nv_bfloat16;
   const bool pre = p.flags & GSPN_FLAG_PRENORMALIZED;
-  const bool cl = A.plan.cl > 1;
-  if (dt == GSPN_BF16) {
-    if (cl) e = pre ? launch(bwd_stream_kernel<BF, true, true>, A, s) : launch(bwd_stream_kernel<BF, false, true>, A, s);
-    else e = pre ? launch(bwd_stream_kernel<BF, true, false>, A, s) : launch(bwd_stream_kernel<BF, false, false>, A, s);
-  } else {
-    if (cl) e = pre ? launch(bwd_stream_kernel<float, true, true>, A, s) : launch(bwd_stream_kernel<float, false, true>, A, s);
-    else e = pre ? launch(bwd_stream_kernel<float, true, false>, A, s) : launch(bwd_stream_kernel<float, false, false>, A, s);
-  }
+  if (dt == GSPN_BF16)
+    e = pre ? launch(bwd_stream_kernel<BF, true>, A, s) : launch(bwd_stream_kernel<BF, false>, A, s);
+  else
+    e = pre ? launch(bwd_stream_kernel<float, true>, A, s) : launch(bwd_stream_kernel<float, false>, A, s);
   *launches += 1;
   if (e != cudaSuccess) return e;
   const bool per_channel = p.G == p.C;
-  if (launch_out_tma(p, A.g, dt, s, &e)) {
+  if (per_channel && launch_out_tma(p, A.g, dt, s, &e)) {
     *launches += 1;
     return e;
   }
