@@ -616,20 +616,31 @@ __device__ __forceinline__ void cluster_exit() {
 
 __device__ __forceinline__ float clamped_rcp(float s) { return fminf(fast_rcp(s), kRcpMax); }
 
+// Normaliser modes (kernel template parameter): pre-normalised taps (1 / S = 1); raw taps with the
+// clamped reciprocal (chains with partial tiles read zero-filled steps, S = 0); raw taps when every
+// L is a multiple of K (no zero-filled steps: S > 0 at valid positions, S = 1 at masked ones).
+enum NormMode { kNormPre = 0, kNormClamp = 1, kNormFull = 2 };
+template <int kMode>
+__device__ __forceinline__ float norm_inv(float s) {
+  if constexpr (kMode == kNormPre) return 1.f;
+  else if constexpr (kMode == kNormClamp) return clamped_rcp(s);
+  else return fast_rcp(s);
+}
+
 // ------------------------------------------------------------------------------ forward
 
 // One step of Eq. 1 at one position (taps already masked, see Lanes).
-template <bool kPre>
+template <int kPre>
 __device__ __forceinline__ float fwd_math(float x, float lam, float l, float m, float r, float hm1, float h,
                                           float hp1) {
   const float acc = fmaf(l, hm1, fmaf(m, h, r * hp1));
-  const float inv = kPre ? 1.f : clamped_rcp((l + r) + m);
+  const float inv = norm_inv<kPre>((l + r) + m);
   return fmaf(acc, inv, lam * x);
 }
 
 // Vertical half-tile: KS steps; p0 = the lane's operands at the half's first step, stepb = +-kRowB.
 // New states go straight to global memory (gp advances by gstep rows per step).
-template <typename T, bool kPre>
+template <typename T, int kPre>
 __device__ __forceinline__ void fwd_half_vert(const Lanes<T>& ln, const uint8_t* p0, int stepb, T* gp,
                                               int64_t gstep, int t0, int L, float (&h)[kE], uint64_t pol) {
   constexpr int KS = Cfg<T>::KS;
@@ -670,7 +681,7 @@ __device__ __forceinline__ void slot_hi(const float (&v)[kE], int lane, float (&
 
 // Horizontal half-tile: one 16-byte chunk (KS steps) per tensor per slot; kRev walks the chunk
 // backwards (R2L). The new states come back packed in memory order for the in-place write.
-template <typename T, bool kPre, bool kRev>
+template <typename T, int kPre, bool kRev>
 __device__ __forceinline__ void fwd_half_horiz(const Lanes<T>& ln, const uint8_t* st, int cm, int lane,
                                                float (&h)[kE], uint4 (&OUT)[kE]) {
   constexpr int KS = Cfg<T>::KS;
@@ -702,7 +713,7 @@ __device__ __forceinline__ void fwd_half_horiz(const Lanes<T>& ln, const uint8_t
   for (int q = 0; q < kE; ++q) OUT[q] = Pk<T>::pack(O[q]);
 }
 
-template <typename T, bool kPre, bool kCl>
+template <typename T, int kPre, bool kCl>
 __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) fwd_stream_kernel(const __grid_constant__ StreamArgs A) {
   using C = Cfg<T>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -807,18 +818,18 @@ struct BwdState {
   float ea[kE], eb[kE], ec[kE];
 };
 
-template <bool kPre>
+template <int kPre>
 __device__ __forceinline__ float bwd_math(float dh, float l, float m, float r, float nr, float nl, float& ea,
                                           float& eb, float& ec) {
   const float ge = (dh + eb) + (nr + nl);
-  const float ig = kPre ? ge : clamped_rcp((l + r) + m) * ge;
+  const float ig = kPre == kNormPre ? ge : norm_inv<kPre>((l + r) + m) * ge;
   ea = l * ig;
   eb = m * ig;
   ec = r * ig;
   return ge;
 }
 
-template <typename T, bool kPre>
+template <typename T, int kPre>
 __device__ __forceinline__ void bwd_half_vert(const Lanes<T>& ln, const uint8_t* p0, int stepb, T* gp,
                                               int64_t gstep, int t0, int L, BwdState& S, uint64_t pol) {
   constexpr int KS = Cfg<T>::KS;
@@ -842,7 +853,7 @@ __device__ __forceinline__ void bwd_half_vert(const Lanes<T>& ln, const uint8_t*
   }
 }
 
-template <typename T, bool kPre, bool kRev>
+template <typename T, int kPre, bool kRev>
 __device__ __forceinline__ void bwd_half_horiz(const Lanes<T>& ln, const uint8_t* st, int cm, int lane, BwdState& S,
                                                uint4 (&OG)[kE]) {
   constexpr int KS = Cfg<T>::KS;
@@ -872,7 +883,7 @@ __device__ __forceinline__ void bwd_half_horiz(const Lanes<T>& ln, const uint8_t
   for (int q = 0; q < kE; ++q) OG[q] = Pk<T>::pack(G_[q]);
 }
 
-template <typename T, bool kPre, bool kCl>
+template <typename T, int kPre, bool kCl>
 __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_stream_kernel(const __grid_constant__ StreamArgs A) {
   using C = Cfg<T>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -1933,6 +1944,24 @@ cudaError_t launch(KernelT kernel, const StreamArgs& A, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+template <typename T, bool kCl>
+cudaError_t launch_fwd(int mode, const StreamArgs& A, cudaStream_t s) {
+  if (mode == kNormPre) return launch(fwd_stream_kernel<T, kNormPre, kCl>, A, s);
+  if (mode == kNormClamp) return launch(fwd_stream_kernel<T, kNormClamp, kCl>, A, s);
+  return launch(fwd_stream_kernel<T, kNormFull, kCl>, A, s);
+}
+template <typename T, bool kCl>
+cudaError_t launch_bwd(int mode, const StreamArgs& A, cudaStream_t s) {
+  if (mode == kNormPre) return launch(bwd_stream_kernel<T, kNormPre, kCl>, A, s);
+  if (mode == kNormClamp) return launch(bwd_stream_kernel<T, kNormClamp, kCl>, A, s);
+  return launch(bwd_stream_kernel<T, kNormFull, kCl>, A, s);
+}
+
+int norm_mode(const ScanParams& p, const Plan& pl) {
+  if (p.flags & GSPN_FLAG_PRENORMALIZED) return kNormPre;
+  return (p.H % pl.K == 0 && p.W % pl.K == 0) ? kNormFull : kNormClamp;
+}
+
 constexpr size_t kAlign = 256;
 size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
 
@@ -1968,16 +1997,11 @@ cudaError_t launch_fwd_stream(const ScanParams& p, gspn_dtype_t dt, cudaStream_t
   if (!fill_maps(&A, ins, F_NIN, outs, in_planes, p.D * p.B * p.C, 1, dt)) return cudaSuccess;
   *handled = true;
   using BF = __nv_bfloat16;
-  const bool pre = p.flags & GSPN_FLAG_PRENORMALIZED;
+  const int mode = norm_mode(p, A.plan);
   cudaError_t e;
   const bool cl = A.plan.cl > 1;
-  if (dt == GSPN_BF16) {
-    if (cl) e = pre ? launch(fwd_stream_kernel<BF, true, true>, A, s) : launch(fwd_stream_kernel<BF, false, true>, A, s);
-    else e = pre ? launch(fwd_stream_kernel<BF, true, false>, A, s) : launch(fwd_stream_kernel<BF, false, false>, A, s);
-  } else {
-    if (cl) e = pre ? launch(fwd_stream_kernel<float, true, true>, A, s) : launch(fwd_stream_kernel<float, false, true>, A, s);
-    else e = pre ? launch(fwd_stream_kernel<float, true, false>, A, s) : launch(fwd_stream_kernel<float, false, false>, A, s);
-  }
+  if (dt == GSPN_BF16) e = cl ? launch_fwd<BF, true>(mode, A, s) : launch_fwd<BF, false>(mode, A, s);
+  else e = cl ? launch_fwd<float, true>(mode, A, s) : launch_fwd<float, false>(mode, A, s);
   *launches += 1;
   return e;
 }
@@ -2068,15 +2092,10 @@ cudaError_t launch_bwd_stream(const ScanParams& p0, gspn_dtype_t dt, cudaStream_
   *handled = true;
   cudaError_t e;
   using BF = __nv_bfloat16;
-  const bool pre = p.flags & GSPN_FLAG_PRENORMALIZED;
+  const int mode = norm_mode(p, A.plan);
   const bool cl = A.plan.cl > 1;
-  if (dt == GSPN_BF16) {
-    if (cl) e = pre ? launch(bwd_stream_kernel<BF, true, true>, A, s) : launch(bwd_stream_kernel<BF, false, true>, A, s);
-    else e = pre ? launch(bwd_stream_kernel<BF, true, false>, A, s) : launch(bwd_stream_kernel<BF, false, false>, A, s);
-  } else {
-    if (cl) e = pre ? launch(bwd_stream_kernel<float, true, true>, A, s) : launch(bwd_stream_kernel<float, false, true>, A, s);
-    else e = pre ? launch(bwd_stream_kernel<float, true, false>, A, s) : launch(bwd_stream_kernel<float, false, false>, A, s);
-  }
+  if (dt == GSPN_BF16) e = cl ? launch_bwd<BF, true>(mode, A, s) : launch_bwd<BF, false>(mode, A, s);
+  else e = cl ? launch_bwd<float, true>(mode, A, s) : launch_bwd<float, false>(mode, A, s);
   *launches += 1;
   if (e != cudaSuccess) return e;
   const bool per_channel = p.G == p.C;
