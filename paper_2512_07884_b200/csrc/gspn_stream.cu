@@ -1,39 +1,40 @@
-// gspn_stream.cu — the TMA-streaming fast path for sm_100a (B200).
+// gspn_stream.cu — the TMA-streaming fast path for sm_100a (B200). DESIGN.md §6 has the measured
+// numbers behind each choice below.
 //
 // Forward: one persistent launch covers every requested direction ("Kernel Fuse";
 // the paper's one-stream-per-direction concurrency, becomes a direction dimension of the
-// work queue). Backward: one persistent launch for the adjoint recurrence (dlam, dx, and g, the
-// adjoint state) plus one elementwise launch for the tap gradients (dw), which need g and h only.
+// work queue). Backward: one persistent launch for the adjoint recurrence (writes g, the adjoint
+// state, to workspace) plus one TMA-staged launch for the outputs (dlam, dx, dw), which are
+// elementwise in g, h, x, lam and w.
 //
-// Work item = one chain (direction k, batch b, channel c): a P-wide state marching L steps. A CTA owns
-// one chain at a time:
+// Work item = one chain (direction k, batch b, channel c): a P-wide state marching L steps -- or a
+// pack of npack chains side by side (small planes), or, for P > 512, a slice of a chain held by one
+// CTA of a thread-block cluster. A CTA owns one work item at a time:
 //  * warp NWC (producer) streams K-step tiles of every input tensor into a shared-memory ring with
 //    TMA (cp.async.bulk.tensor.3d + mbarrier complete_tx). K * sizeof(T) = 32 bytes: a horizontal
 //    tile reads one full 32-byte DRAM sector of every row (narrower chunks measured at half the TMA
-//    rate and needed L2 to keep the rest of the sector between tiles — tools/tma_probe.cu,
-//    profiles/r1_notes.md);
-//  * NWC consumer warps run the recurrence with the carry in fp32 registers. A warp covers 32 E
-//    consecutive positions (E per lane): it owns the middle 32 E - 2 GH and recomputes GH ghost
-//    positions on each side (temporal blocking), so neighbours move by warp shuffles every step
-//    and warps exchange edge values through shared memory once per GH = K/2 steps;
+//    rate -- tools/tma_probe.cu, profiles/r1_notes.md);
+//  * NWC consumer warps run the recurrence with the carry in fp32 registers. A warp covers 64
+//    consecutive positions (2 per lane): it owns the middle 64 - 2 GH and recomputes GH ghost
+//    positions on each side (temporal blocking), so neighbours move by warp shuffles every step and
+//    warps exchange edge values through shared memory once per GH = K/2 steps (across the CTAs of a
+//    cluster through distributed shared memory);
 //  * warp NWC+1 (storer) writes horizontal tiles' outputs with TMA stores once the consumers have
 //    written them in place over the consumed input rows; vertical chains store straight from
 //    registers (a warp's owned positions are contiguous, so these stores coalesce).
 // Lane mappings (both conflict-free on the shared-memory tiles):
-//   T2B/B2T (vertical):   tile = K image rows x P columns ([box][K][bw]); a lane owns E consecutive
-//                         positions and reads one E-element vector per tensor per step.
-//   L2R/R2L (horizontal): tile = P image rows x 32 bytes (TMA SWIZZLE_32B: 16-byte chunk ^= row bit
-//                         2); a lane owns E interleaved rows and reads each half-tile (K/2 steps) of
-//                         a row as one 16-byte vector.
-// Chains are ordered (b, c)-major with the D directions adjacent, so co-scheduled CTAs share a
-// plane's x (and in the backward its fp32 dx accumulator) through L2.
+//   T2B/B2T (vertical):   tile = K image rows x 512 positions ([box][K][512 B], packed: [K][npack][W]);
+//                         a lane reads one 2-element vector per tensor per step.
+//   L2R/R2L (horizontal): tile = up to 512 image rows x 32 bytes (TMA SWIZZLE_32B: 16-byte chunk ^=
+//                         row bit 2); a lane owns 2 interleaved rows and reads each half-tile (K/2
+//                         steps) of a row as one 16-byte vector.
+// Work items are ordered (b, c)-major with the D directions adjacent and rotated per grid round, so
+// co-scheduled CTAs share a plane's x through L2 and every CTA mixes vertical and horizontal chains.
 //
 // Backward recurrence: tiles in reverse step order; the carried state is
-// (a g, b g, c g) of the previous step, so g_t = dh_t + (b g)[r] + (a g)[r+1] + (c g)[r-1].
-// dlam = g x; dx (sum over directions) accumulates with red.global.add into an fp32 workspace plane
-// that the last of the plane's D chains converts and discards from L2. g is written to workspace in
-// the I/O dtype; dw_kernel then forms Da = g h_{t-1}[r-1], Db = g h_{t-1}[r], Dc = g h_{t-1}[r+1],
-// sums them over the group's channels and applies the normalisation Jacobian (a7).
+// (a g, b g, c g) of the previous step, so g_t = dh_t + (b g)[r] + (a g)[r+1] + (c g)[r-1]. The output
+// kernels (a7) form dlam = g x, dx = sum_k g lam, and Da = g h_{t-1}[r-1], Db = g h_{t-1}[r],
+// Dc = g h_{t-1}[r+1] summed over the group's channels, then apply the normalisation Jacobian.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
