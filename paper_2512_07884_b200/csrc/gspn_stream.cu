@@ -285,7 +285,7 @@ __device__ void storer_loop(const StreamArgs& A, uint8_t* ring, uint64_t* done, 
     const Chain ch = make_chain<kCl>(A.p, pl, w);
     for (int jj = 0; jj < ch.ntiles; ++jj) {
       const int j = bwd ? (ch.ntiles - 1 - jj) : jj;
-      mbar_wait(smem_u32(&done[stage]), phase);
+      mbar_wait_sleep(smem_u32(&done[stage]), phase);
       if (!ch.vert) {
         const int s0 = tile_start(ch, j, pl.K);
         const uint8_t* st = ring + static_cast<size_t>(stage) * pl.stage_bytes;
@@ -752,7 +752,7 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) fwd_stream_kernel(const
     T* hout = static_cast<T*>(A.p.hout) + ln.vout;
     float h[kE] = {0.f, 0.f};
     for (int j = 0; j < ch.ntiles; ++j) {
-      mbar_wait(smem_u32(&m.full[stage]), phase);
+      mbar_wait_sleep(smem_u32(&m.full[stage]), phase);
       __syncwarp();  // reconverge after the per-thread spin: the shuffles below need no collective fallback
       uint8_t* st = m.ring + static_cast<size_t>(stage) * pl.stage_bytes;
 #pragma unroll 1
@@ -926,7 +926,7 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_stream_kernel(const
     for (int e = 0; e < kE; ++e) S.ea[e] = S.eb[e] = S.ec[e] = 0.f;
     for (int jj = 0; jj < ch.ntiles; ++jj) {
       const int j = ch.ntiles - 1 - jj;
-      mbar_wait(smem_u32(&m.full[stage]), phase);
+      mbar_wait_sleep(smem_u32(&m.full[stage]), phase);
       __syncwarp();  // reconverge after the per-thread spin: the shuffles below need no collective fallback
       uint8_t* st = m.ring + static_cast<size_t>(stage) * pl.stage_bytes;
 #pragma unroll 1
@@ -1459,7 +1459,7 @@ __global__ void __launch_bounds__((kOutConsumers + 1) * 32, 1) bwd_out_tma_kerne
   for (int64_t u = blockIdx.x; u < A.nunits; u += gridDim.x) {
     const int64_t bc = u / A.nrb;
     const int i0 = static_cast<int>(u % A.nrb) * RB;
-    mbar_wait(smem_u32(&full[stage]), phase);
+    mbar_wait_sleep(smem_u32(&full[stage]), phase);
     const uint8_t* st = ring + static_cast<size_t>(stage) * A.stage_bytes;
     for (int idx = threadIdx.x; idx < RB * nchunk; idx += nthreads) {
       const int r = idx / nchunk;
@@ -1638,7 +1638,7 @@ __global__ void __launch_bounds__((kOutConsumers + 1) * 32, 1) bwd_out_grp_tma_k
 #pragma unroll
       for (int q = 0; q < V; ++q) Da[k][q] = Db[k][q] = Dc[k][q] = 0.f;
     for (int64_t cc = 0; cc < Cg; ++cc) {
-      mbar_wait(smem_u32(&full[stage]), phase);
+      mbar_wait_sleep(smem_u32(&full[stage]), phase);
       const uint8_t* st = ring + static_cast<size_t>(stage) * A.stage_bytes;
       if (valid) {
         const int64_t bc = b * p.C + grp * Cg + cc;
