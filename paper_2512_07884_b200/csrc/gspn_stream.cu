@@ -465,40 +465,62 @@ __device__ __forceinline__ float hget_tap(const uint4& u, int i, const uint32_t 
   }
 }
 
-// Ghost exchange through shared memory: every warp publishes its first and last GH owned values;
-// warps w >= 1 reload their left ghosts from warp w-1, warps w < nwc-1 their right ghosts from w+1.
-// Parity-double-buffered; the caller separates publish and reload by one named barrier.
+// Ghost exchange through shared memory, without divergent branches: every lane stores all of its
+// values into its warp's 64-slot row of the exchange buffer [array][par][warp][64]; after the named
+// barrier every lane reads back one value per slot from a per-lane precomputed source -- a ghost
+// slot from the neighbouring warp's owned edge (offset +-(64 - 2 GH)), any other slot from itself.
+// Warp 0's left and the last warp's right ghosts keep their own (outside-the-chain) values.
+constexpr int kXRow = 64;  // floats per warp row of the exchange buffer
+constexpr int kXArr = 2 * kEdgeW * kXRow;  // floats per state array (2 parities)
+
+struct XSrc {
+  uint32_t v;      // vertical: byte offset (within one parity plane) of the lane's 2 source values
+  uint32_t h[kE];  // horizontal: byte offset of each slot's source value
+};
+
 template <typename T>
-__device__ __forceinline__ void edge_publish(float* edge, int par, int wi, int lane, bool vert, const float (&v)[kE]) {
+__device__ __forceinline__ XSrc make_xsrc(int wi, int nwc, int lane) {
   using C = Cfg<T>;
-  constexpr int WARP = 32 * kE;
-  float* L = edge + ((par * kEdgeW + wi) * 2 + 0) * 8;
-  float* R = edge + ((par * kEdgeW + wi) * 2 + 1) * 8;
-  if (vert) {
+  constexpr int WARP = 32 * kE, SH = WARP - 2 * C::GH;  // ghost <-> neighbour's owned edge distance
+  XSrc x;
+  {
     const int o = kE * lane;
-    if (o >= C::GH && o < 2 * C::GH) { L[o - C::GH] = v[0]; L[o - C::GH + 1] = v[1]; }
-    if (o >= WARP - 2 * C::GH && o < WARP - C::GH) { R[o - (WARP - 2 * C::GH)] = v[0]; R[o - (WARP - 2 * C::GH) + 1] = v[1]; }
+    int sw = wi, so = o;
+    if (o < C::GH && wi > 0) { sw = wi - 1; so = o + SH; }
+    else if (o >= WARP - C::GH && wi < nwc - 1) { sw = wi + 1; so = o - SH; }
+    x.v = static_cast<uint32_t>((sw * kXRow + so) * 4);
+  }
+#pragma unroll
+  for (int q = 0; q < kE; ++q) {
+    const int o = 32 * q + lane;
+    int sw = wi, so = o;
+    if (o < C::GH && wi > 0) { sw = wi - 1; so = o + SH; }
+    else if (o >= WARP - C::GH && wi < nwc - 1) { sw = wi + 1; so = o - SH; }
+    x.h[q] = static_cast<uint32_t>((sw * kXRow + so) * 4);
+  }
+  return x;
+}
+
+// buf: exchange buffer of one state array at parity par.
+__device__ __forceinline__ void edge_publish(float* buf, int wi, int lane, bool vert, const float (&v)[kE]) {
+  float* row = buf + wi * kXRow;
+  if (vert) {
+    *reinterpret_cast<float2*>(row + kE * lane) = make_float2(v[0], v[1]);
   } else {
-    if (lane >= C::GH && lane < 2 * C::GH) L[lane - C::GH] = v[0];
-    if (lane >= 32 - 2 * C::GH && lane < 32 - C::GH) R[lane - (32 - 2 * C::GH)] = v[kE - 1];
+    row[lane] = v[0];
+    row[32 + lane] = v[1];
   }
 }
 
-template <typename T>
-__device__ __forceinline__ void edge_reload(const float* edge, int par, int wi, int nwc, int lane, bool vert,
-                                            float (&v)[kE]) {
-  using C = Cfg<T>;
-  constexpr int WARP = 32 * kE;
-  const float* Rl = edge + ((par * kEdgeW + (wi - 1)) * 2 + 1) * 8;  // left neighbour's right edge
-  const float* Lr = edge + ((par * kEdgeW + (wi + 1)) * 2 + 0) * 8;  // right neighbour's left edge
-  const bool has_l = wi > 0, has_r = wi < nwc - 1;
+__device__ __forceinline__ void edge_reload(const float* buf, const XSrc& x, bool vert, float (&v)[kE]) {
+  const char* b = reinterpret_cast<const char*>(buf);
   if (vert) {
-    const int o = kE * lane;
-    if (has_l && o < C::GH) { v[0] = Rl[o]; v[1] = Rl[o + 1]; }
-    if (has_r && o >= WARP - C::GH) { v[0] = Lr[o - (WARP - C::GH)]; v[1] = Lr[o - (WARP - C::GH) + 1]; }
+    const float2 u = *reinterpret_cast<const float2*>(b + x.v);
+    v[0] = u.x;
+    v[1] = u.y;
   } else {
-    if (has_l && lane < C::GH) v[0] = Rl[lane];
-    if (has_r && lane >= 32 - C::GH) v[kE - 1] = Lr[lane - (32 - C::GH)];
+    v[0] = *reinterpret_cast<const float*>(b + x.h[0]);
+    v[1] = *reinterpret_cast<const float*>(b + x.h[1]);
   }
 }
 
@@ -517,8 +539,8 @@ __device__ __forceinline__ Smem carve(uint8_t* smem_raw, const Plan& pl) {
   m.full = reinterpret_cast<uint64_t*>(m.ring + static_cast<size_t>(pl.nstages) * pl.stage_bytes);
   m.empty = m.full + pl.nstages;
   m.done = m.empty + pl.nstages;
-  m.edge = reinterpret_cast<float*>(m.done + pl.nstages);  // [3 state arrays][2 par][kEdgeW][2][8]
-  m.xl = m.edge + 3 * 2 * kEdgeW * 2 * 8;
+  m.edge = reinterpret_cast<float*>(m.done + pl.nstages);  // [3 state arrays][2 par][kEdgeW][64]
+  m.xl = m.edge + 3 * kXArr;
   m.xr = m.xl + 3 * 2 * 8;
   m.xb = reinterpret_cast<uint64_t*>(m.xr + 3 * 2 * 8);
   return m;
@@ -743,6 +765,7 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) fwd_stream_kernel(const
   const int nthreads = pl.nwc * 32;
   const int64_t W = A.p.W;
   const int rank = kCl ? static_cast<int>(cluster_ctarank()) : 0;
+  const XSrc xs = make_xsrc<T>(warp, pl.nwc, lane);
   uint32_t xphase = 0;  // P-split: phase bit of the cluster edge barriers, per parity
   int stage = 0, par = 0;
   uint32_t phase = 0;
@@ -773,7 +796,7 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) fwd_stream_kernel(const
             fwd_half_horiz<T, kPre, false>(ln, st, cm, lane, h, OUT);
           }
         }
-        edge_publish<T>(m.edge, par, warp, lane, ch.vert, h);
+        edge_publish(m.edge + par * kEdgeW * kXRow, warp, lane, ch.vert, h);
         if constexpr (kCl) {
 #pragma unroll
           for (int side = 0; side < 2; ++side) {
@@ -784,7 +807,7 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) fwd_stream_kernel(const
           }
         }
         named_bar(kBarEdge, nthreads);  // edges published; every warp has read this half's input rows
-        edge_reload<T>(m.edge, par, warp, pl.nwc, lane, ch.vert, h);
+        edge_reload(m.edge + par * kEdgeW * kXRow, xs, ch.vert, h);
         if constexpr (kCl) {
 #pragma unroll
           for (int side = 0; side < 2; ++side) {
@@ -911,9 +934,9 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_stream_kernel(const
   }
   const uint64_t pol_vout = policy_of(pl.pol[3]);
   const int nthreads = pl.nwc * 32;
-  constexpr int kEdgeArr = 2 * kEdgeW * 2 * 8;
   const int64_t W = A.p.W;
   const int rank = kCl ? static_cast<int>(cluster_ctarank()) : 0;
+  const XSrc xs = make_xsrc<T>(warp, pl.nwc, lane);
   uint32_t xphase = 0;
   int stage = 0, par = 0;
   uint32_t phase = 0;
@@ -948,9 +971,9 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_stream_kernel(const
             bwd_half_horiz<T, kPre, false>(ln, st, cm, lane, S, OG);
           }
         }
-        edge_publish<T>(m.edge + 0 * kEdgeArr, par, warp, lane, ch.vert, S.ea);
-        edge_publish<T>(m.edge + 1 * kEdgeArr, par, warp, lane, ch.vert, S.eb);
-        edge_publish<T>(m.edge + 2 * kEdgeArr, par, warp, lane, ch.vert, S.ec);
+        edge_publish(m.edge + 0 * kXArr + par * kEdgeW * kXRow, warp, lane, ch.vert, S.ea);
+        edge_publish(m.edge + 1 * kXArr + par * kEdgeW * kXRow, warp, lane, ch.vert, S.eb);
+        edge_publish(m.edge + 2 * kXArr + par * kEdgeW * kXRow, warp, lane, ch.vert, S.ec);
         if constexpr (kCl) {
 #pragma unroll
           for (int side = 0; side < 2; ++side) {
@@ -963,9 +986,9 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_stream_kernel(const
           }
         }
         named_bar(kBarEdge, nthreads);  // edges published; every warp has read this half's input rows
-        edge_reload<T>(m.edge + 0 * kEdgeArr, par, warp, pl.nwc, lane, ch.vert, S.ea);
-        edge_reload<T>(m.edge + 1 * kEdgeArr, par, warp, pl.nwc, lane, ch.vert, S.eb);
-        edge_reload<T>(m.edge + 2 * kEdgeArr, par, warp, pl.nwc, lane, ch.vert, S.ec);
+        edge_reload(m.edge + 0 * kXArr + par * kEdgeW * kXRow, xs, ch.vert, S.ea);
+        edge_reload(m.edge + 1 * kXArr + par * kEdgeW * kXRow, xs, ch.vert, S.eb);
+        edge_reload(m.edge + 2 * kXArr + par * kEdgeW * kXRow, xs, ch.vert, S.ec);
         if constexpr (kCl) {
 #pragma unroll
           for (int side = 0; side < 2; ++side) {
@@ -1797,7 +1820,7 @@ int smem_optin() {
   return n;
 }
 
-constexpr int kSmemTail = 7168;  // mbarriers (3 per stage), ghost-edge buffers (6 KB), cluster edges + barriers
+constexpr int kSmemTail = 26624;  // mbarriers (3 per stage), exchange rows (3 x 2 x 16 x 64 floats = 24 KB), cluster edges
 
 // Shape eligibility + plan (nin: tensors per tile).
 bool make_plan(const ScanParams& p, gspn_dtype_t dt, int nin, Plan* pl) {
