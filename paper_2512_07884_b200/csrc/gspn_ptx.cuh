@@ -154,6 +154,20 @@ __device__ __forceinline__ void st_global_b32(void* p, uint32_t a, uint64_t pol)
 __device__ __forceinline__ void st_global_v2(void* p, uint32_t a, uint32_t b, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.v2.b32 [%0], {%1, %2}, %3;" ::"l"(p), "r"(a), "r"(b), "l"(pol) : "memory");
 }
+// Predicated forms: the predicate lives inside the asm, so the compiler emits @P STG instead of a
+// branch around an opaque asm block.
+__device__ __forceinline__ void st_global_b32_if(bool pred, void* p, uint32_t a, uint64_t pol) {
+  asm volatile(
+      "{\n.reg .pred q;\nsetp.ne.u32 q, %3, 0;\n@q st.global.L2::cache_hint.b32 [%0], %1, %2;\n}" ::"l"(p), "r"(a),
+      "l"(pol), "r"(static_cast<uint32_t>(pred))
+      : "memory");
+}
+__device__ __forceinline__ void st_global_v2_if(bool pred, void* p, uint32_t a, uint32_t b, uint64_t pol) {
+  asm volatile(
+      "{\n.reg .pred q;\nsetp.ne.u32 q, %4, 0;\n@q st.global.L2::cache_hint.v2.b32 [%0], {%1, %2}, %3;\n}" ::"l"(p),
+      "r"(a), "r"(b), "l"(pol), "r"(static_cast<uint32_t>(pred))
+      : "memory");
+}
 __device__ __forceinline__ void st_global_v4(void* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d),
                "l"(pol)

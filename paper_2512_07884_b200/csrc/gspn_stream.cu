@@ -126,10 +126,16 @@ template <> struct GStore<__nv_bfloat16, 2> {
   static __device__ __forceinline__ void st(__nv_bfloat16* p, const float (&v)[2], uint64_t pol) {
     st_global_b32(p, pack_bf16x2(v[0], v[1]), pol);
   }
+  static __device__ __forceinline__ void st_if(bool pred, __nv_bfloat16* p, const float (&v)[2], uint64_t pol) {
+    st_global_b32_if(pred, p, pack_bf16x2(v[0], v[1]), pol);
+  }
 };
 template <> struct GStore<float, 2> {
   static __device__ __forceinline__ void st(float* p, const float (&v)[2], uint64_t pol) {
     st_global_v2(p, __float_as_uint(v[0]), __float_as_uint(v[1]), pol);
+  }
+  static __device__ __forceinline__ void st_if(bool pred, float* p, const float (&v)[2], uint64_t pol) {
+    st_global_v2_if(pred, p, __float_as_uint(v[0]), __float_as_uint(v[1]), pol);
   }
 };
 
@@ -682,7 +688,7 @@ __device__ __forceinline__ void fwd_half_vert(const Lanes<T>& ln, const uint8_t*
     const float h1 = fwd_math<kPre>(x[1], lam[1], l[1], m[1], r[1], h[0], h[1], right);
     h[0] = h0;
     h[1] = h1;
-    if (ln.own_v && t0 + ss < L) GStore<T, 2>::st(gp, h, pol);
+    GStore<T, 2>::st_if(ln.own_v && t0 + ss < L, gp, h, pol);
     gp += gstep;
   }
 }
@@ -872,7 +878,7 @@ __device__ __forceinline__ void bwd_half_vert(const Lanes<T>& ln, const uint8_t*
     float g[2];
     g[0] = bwd_math<kPre>(dh[0], l[0], m[0], r[0], ea0, nl0, S.ea[0], S.eb[0], S.ec[0]);
     g[1] = bwd_math<kPre>(dh[1], l[1], m[1], r[1], nr1, ec1, S.ea[1], S.eb[1], S.ec[1]);
-    if (ln.own_v && t0 + KS - 1 - i < L) GStore<T, 2>::st(gp, g, pol);
+    GStore<T, 2>::st_if(ln.own_v && t0 + KS - 1 - i < L, gp, g, pol);
     gp += gstep;
   }
 }
