@@ -38,11 +38,15 @@ def _load():
         lib = ctypes.CDLL(build())
         d = ctypes.POINTER(ctypes.c_double)
         i64 = ctypes.c_int64
-        lib.gspn_oracle_fwd.argtypes = [d] * 6 + [i64] * 4 + [ctypes.c_uint, i64, ctypes.c_uint, ctypes.c_int]
+        lib.gspn_oracle_fwd.argtypes = [d] * 6 + [i64] * 4 + [ctypes.c_uint, i64, ctypes.c_uint, i64, ctypes.c_int]
         lib.gspn_oracle_fwd.restype = ctypes.c_int
-        lib.gspn_oracle_bwd.argtypes = [d] * 12 + [i64] * 4 + [ctypes.c_uint, i64, ctypes.c_uint, ctypes.c_int]
+        lib.gspn_oracle_bwd.argtypes = [d] * 12 + [i64] * 4 + [ctypes.c_uint, i64, ctypes.c_uint, i64, ctypes.c_int]
         lib.gspn_oracle_bwd.restype = ctypes.c_int
         lib.gspn_oracle_detail.restype = ctypes.c_char_p
+        lib.gspn_oracle_merge_fwd.argtypes = [d] * 3 + [i64, i64, ctypes.c_int]
+        lib.gspn_oracle_merge_fwd.restype = None
+        lib.gspn_oracle_merge_bwd.argtypes = [d] * 5 + [i64, i64, ctypes.c_int]
+        lib.gspn_oracle_merge_bwd.restype = None
         _lib = lib
     return _lib
 
@@ -63,19 +67,20 @@ def default_threads() -> int:
     return len(os.sched_getaffinity(0))
 
 
-def fwd(x, wl, wm, wr, lam, dirs: int, groups: int, flags: int = 0, threads: int = 1) -> np.ndarray:
-    """h [D,B,C,H,W] from x [B,C,H,W], w_* [D,B,G,H,W], lam [D,B,C,H,W] (float64)."""
+def fwd(x, wl, wm, wr, lam, dirs: int, groups: int, flags: int = 0, threads: int = 1, kchunk: int = 0) -> np.ndarray:
+    """h [D,B,C,H,W] from x [B,C,H,W], w_* [D,B,G,H,W], lam [D,B,C,H,W] (float64).
+    kchunk > 0: GSPN-local, h reset at every segment start."""
     x, wl, wm, wr, lam = map(_f64, (x, wl, wm, wr, lam))
     B, C, H, W = x.shape
     h = np.empty(lam.shape, dtype=np.float64)
     st = _load().gspn_oracle_fwd(_p(x), _p(wl), _p(wm), _p(wr), _p(lam), _p(h), B, C, H, W, dirs, groups,
-                                 flags, threads)
+                                 flags, kchunk, threads)
     if st:
         raise OracleError(f"oracle fwd status {st}: {_load().gspn_oracle_detail().decode()}")
     return h
 
 
-def bwd(x, wl, wm, wr, lam, h, dh, dirs: int, groups: int, flags: int = 0, threads: int = 1):
+def bwd(x, wl, wm, wr, lam, h, dh, dirs: int, groups: int, flags: int = 0, threads: int = 1, kchunk: int = 0):
     """(dx, dw_l, dw_m, dw_r, dlam) given saved h and upstream dh (float64)."""
     x, wl, wm, wr, lam, h, dh = map(_f64, (x, wl, wm, wr, lam, h, dh))
     B, C, H, W = x.shape
@@ -83,7 +88,25 @@ def bwd(x, wl, wm, wr, lam, h, dh, dirs: int, groups: int, flags: int = 0, threa
     dwl, dwm, dwr = np.empty(wl.shape), np.empty(wl.shape), np.empty(wl.shape)
     dlam = np.empty(lam.shape)
     st = _load().gspn_oracle_bwd(_p(x), _p(wl), _p(wm), _p(wr), _p(lam), _p(h), _p(dh), _p(dx), _p(dwl), _p(dwm),
-                                 _p(dwr), _p(dlam), B, C, H, W, dirs, groups, flags, threads)
+                                 _p(dwr), _p(dlam), B, C, H, W, dirs, groups, flags, kchunk, threads)
     if st:
         raise OracleError(f"oracle bwd status {st}: {_load().gspn_oracle_detail().decode()}")
     return dx, dwl, dwm, dwr, dlam
+
+
+def merge_fwd(h, u, mean: bool = False) -> np.ndarray:
+    """y [B,C,H,W] = s * sum_d u_d * h_d (Eq. 2, four passes combined; s = 1 or 1/D)."""
+    h, u = _f64(h), _f64(u)
+    D, N = h.shape[0], h[0].size
+    y = np.empty(h.shape[1:])
+    _load().gspn_oracle_merge_fwd(_p(h), _p(u), _p(y), D, N, int(mean))
+    return y
+
+
+def merge_bwd(h, u, dy, mean: bool = False):
+    """(dh, du) [D,B,C,H,W] of merge_fwd given dy [B,C,H,W]."""
+    h, u, dy = _f64(h), _f64(u), _f64(dy)
+    D, N = h.shape[0], h[0].size
+    dh, du = np.empty(h.shape), np.empty(h.shape)
+    _load().gspn_oracle_merge_bwd(_p(h), _p(u), _p(dy), _p(dh), _p(du), D, N, int(mean))
+    return dh, du

@@ -11,6 +11,8 @@
  *   PAPER.md:89 (§3.2)                w_i tridiagonal (3 neighbours of the previous row), row-stochastic,
  *                                     four directional passes T2B, B2T, L2R, R2L
  *   PAPER.md:155 (§4.2, Eq. 4)        first block row is Lambda_1, i.e. h_{-1} = 0
+ *   PAPER.md:91-92 (§3.2)             GSPN-local: h resets at every kchunk segment start
+ *   PAPER.md:84-88 (§3.2, Eq. 2)      output gate y = u (.) h, four passes combined (NEXT-1, merge_*)
  *   Backward: the adjoint (reverse-order) recurrence of the same linear map; the paper gives no
  *   formula, so this is the chain rule written out step by step.
  * Readings of silent points (R1-R16): row-stochastic = divide the in-range raw taps by
@@ -78,6 +80,7 @@ typedef struct {
   const double *x, *wl, *wm, *wr, *lam, *h, *dh;
   double *hout, *dx, *dwl, *dwm, *dwr, *dlam;
   int64_t B, C, H, W, G;
+  int64_t kchunk; /* GSPN-local segment length along the scan axis; 0 = global scan */
   unsigned dirs, flags;
   int backward;
   int64_t next_unit; /* guarded by mu */
@@ -90,6 +93,20 @@ static int dir_list(unsigned dirs, unsigned* out) {
   const unsigned all[4] = {T2B, B2T, L2R, R2L};
   for (int k = 0; k < 4; ++k) if (dirs & all[k]) out[n++] = all[k];
   return n;
+}
+
+/* GSPN-local (§3.2: "splits each row or column into fixed-length segments of size
+ * kchunk and confines propagation to within those segments"; "At each kchunk segment
+ * start, h resets to 0"). Segments are fixed on the canonical image grid -- canonical scan-axis index
+ * s (row i for T2B/B2T, column j for L2R/R2L) lies in segment s / kchunk, the last one may be short
+ * -- so all four directions confine propagation to the same image strips (DESIGN.md
+ * R19). Returns 1 when scan step t of direction dir is the first step of its segment in scan order,
+ * i.e. h_{t-1} does not reach h_t. kchunk = 0: the global scan, only t = 0 starts. */
+static int seg_start(unsigned dir, int64_t t, int64_t L, int64_t kchunk) {
+  if (t == 0) return 1;
+  if (kchunk <= 0) return 0;
+  if (dir == T2B || dir == L2R) return t % kchunk == 0;  /* canonical s = t */
+  return (L - t) % kchunk == 0;                          /* canonical s = L-1-t: s + 1 multiple of kchunk */
 }
 
 /* Forward of unit (b, g): every channel of the group, every direction. Eq. 1 / Eq. 3 step by step. */
@@ -117,7 +134,7 @@ static int forward_unit(job_t* J, int64_t b, int64_t g) {
             return ORACLE_NONPOSITIVE_SUM;
           }
           double acc = 0.0; /* w_i h_{i-1}: zero at t = 0 because h_{-1} = 0 */
-          if (t > 0) {
+          if (!seg_start(dl[k], t, L, J->kchunk)) { /* and at GSPN-local segment starts (h resets) */
             if (r >= 1) acc += a * h[pixel(dl[k], J->H, J->W, t - 1, r - 1)];
             acc += bb * h[pixel(dl[k], J->H, J->W, t - 1, r)];
             if (r <= P - 2) acc += cc * h[pixel(dl[k], J->H, J->W, t - 1, r + 1)];
@@ -164,7 +181,7 @@ static int backward_unit(job_t* J, int64_t b, int64_t g) {
         /* g_t = dh_t + w_{t+1}^T g_{t+1}  (adjoint of h_{t+1} = w_{t+1} h_t + ...) */
         for (int64_t r = 0; r < P; ++r) {
           double gt = dh[pixel(dl[k], J->H, J->W, t, r)];
-          if (t + 1 < L) {
+          if (t + 1 < L && !seg_start(dl[k], t + 1, L, J->kchunk)) { /* h_{t+1} depends on h_t */
             double a, bb, cc, S;
             /* row r of w_{t+1} reaches h_t[r] through its centre tap */
             taps(wl[pixel(dl[k], J->H, J->W, t + 1, r)], wm[pixel(dl[k], J->H, J->W, t + 1, r)],
@@ -187,7 +204,7 @@ static int backward_unit(job_t* J, int64_t b, int64_t g) {
           const int64_t p = pixel(dl[k], J->H, J->W, t, r);
           dlam[p] = gcur[r] * x[p]; /* d/dlambda of lambda_t x_t */
           dx[p] += gcur[r] * lam[p]; /* d/dx, summed over directions (R6) */
-          if (t >= 1) {               /* d/d(normalised taps); h_{-1} = 0 gives zero at t = 0 */
+          if (!seg_start(dl[k], t, L, J->kchunk)) { /* d/d(normalised taps); zero where h_{t-1} is reset */
             if (r >= 1) Da[p] += gcur[r] * h[pixel(dl[k], J->H, J->W, t - 1, r - 1)];
             Db[p] += gcur[r] * h[pixel(dl[k], J->H, J->W, t - 1, r)];
             if (r <= P - 2) Dc[p] += gcur[r] * h[pixel(dl[k], J->H, J->W, t - 1, r + 1)];
@@ -248,7 +265,7 @@ static void* worker(void* arg) {
 
 static int run(job_t* J, int threads) {
   if (J->B < 1 || J->C < 1 || J->H < 1 || J->W < 1 || J->G < 1 || J->C % J->G != 0 || J->dirs == 0 ||
-      J->dirs > 15 || (J->flags & ~PRENORMALIZED)) {
+      J->dirs > 15 || (J->flags & ~PRENORMALIZED) || J->kchunk < 0) {
     snprintf(g_detail, sizeof g_detail, "invalid argument");
     return ORACLE_BAD_ARG;
   }
@@ -269,24 +286,50 @@ static int run(job_t* J, int threads) {
 
 int gspn_oracle_fwd(const double* x, const double* wl, const double* wm, const double* wr, const double* lam,
                     double* h, int64_t B, int64_t C, int64_t H, int64_t W, unsigned dirs, int64_t G,
-                    unsigned flags, int threads) {
+                    unsigned flags, int64_t kchunk, int threads) {
   if (!x || !wl || !wm || !wr || !lam || !h) return ORACLE_BAD_ARG;
   job_t J;
   memset(&J, 0, sizeof J);
   J.x = x; J.wl = wl; J.wm = wm; J.wr = wr; J.lam = lam; J.hout = h;
   J.B = B; J.C = C; J.H = H; J.W = W; J.G = G; J.dirs = dirs; J.flags = flags; J.backward = 0;
+  J.kchunk = kchunk;
   return run(&J, threads);
 }
 
 int gspn_oracle_bwd(const double* x, const double* wl, const double* wm, const double* wr, const double* lam,
                     const double* h, const double* dh, double* dx, double* dwl, double* dwm, double* dwr,
                     double* dlam, int64_t B, int64_t C, int64_t H, int64_t W, unsigned dirs, int64_t G,
-                    unsigned flags, int threads) {
+                    unsigned flags, int64_t kchunk, int threads) {
   if (!x || !wl || !wm || !wr || !lam || !h || !dh || !dx || !dwl || !dwm || !dwr || !dlam) return ORACLE_BAD_ARG;
   job_t J;
   memset(&J, 0, sizeof J);
   J.x = x; J.wl = wl; J.wm = wm; J.wr = wr; J.lam = lam; J.h = h; J.dh = dh;
   J.dx = dx; J.dwl = dwl; J.dwm = dwm; J.dwr = dwr; J.dlam = dlam;
   J.B = B; J.C = C; J.H = H; J.W = W; J.G = G; J.dirs = dirs; J.flags = flags; J.backward = 1;
+  J.kchunk = kchunk;
   return run(&J, threads);
+}
+
+/* Output gate and direction merge (§3.2 Eq. 2 "y = u (.) h", per direction; the four
+ * directional passes are "combined" -- by Sum, or Mean on request, SPEC.md:203/263,
+ * DESIGN.md R7):  y = s * sum_d u_d (.) h_d,  s = 1 (Sum) or 1/D (Mean).
+ * h, u: [D, N] (N = B*C*H*W, direction slabs in bit order); y: [N]. */
+void gspn_oracle_merge_fwd(const double* h, const double* u, double* y, int64_t D, int64_t N, int mean) {
+  const double s = mean ? 1.0 / (double)D : 1.0;
+  for (int64_t n = 0; n < N; ++n) {
+    double acc = 0.0;
+    for (int64_t d = 0; d < D; ++d) acc += u[d * N + n] * h[d * N + n];
+    y[n] = s * acc;
+  }
+}
+
+/* Its adjoint: dh_d = s * u_d (.) dy,  du_d = s * h_d (.) dy  (y is bilinear in (u, h)). */
+void gspn_oracle_merge_bwd(const double* h, const double* u, const double* dy, double* dh, double* du, int64_t D,
+                           int64_t N, int mean) {
+  const double s = mean ? 1.0 / (double)D : 1.0;
+  for (int64_t d = 0; d < D; ++d)
+    for (int64_t n = 0; n < N; ++n) {
+      dh[d * N + n] = s * (u[d * N + n] * dy[n]);
+      du[d * N + n] = s * (h[d * N + n] * dy[n]);
+    }
 }
