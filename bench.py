@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-next", action="store_true", help="skip the SURVEY §8(f) rows (merge, GSPN-local)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--flags", type=int, default=0)
@@ -300,6 +301,11 @@ def run_ours(args):
     if args.scaling == "strong":
         total_bytes = gcfg.fwd_bytes() + gcfg.bwd_bytes()
 
+    # ---- SURVEY §8(f) rows on the same workload (after the headline region; not part of `value`)
+    nxt = None
+    if not args.no_next:
+        nxt = measure_next(args, gspn, gcfg, sh, t, h, outs, ws, dev, stream)
+
     # ---- end to end through the public API with host buffers (pinned), copies inside the timed region
     e2e = None
     if not args.no_e2e:
@@ -360,9 +366,61 @@ def run_ours(args):
         "gpu_launches": args.steps * (launches["fwd"] + launches["bwd"]),
         "e2e": e2e,
         "cpu_baseline": cpu,
+        "next": nxt,
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def measure_next(args, gspn, cfg, sh, t, h, outs, ws, dev, stream):
+    """SURVEY §8(f) rows on the bench workload, each timed alone with CUDA events after warm-up:
+    NEXT-1 output gate + direction merge (gspn_merge_fwd / _bwd; algorithmic bytes s N (2D+1) and
+    s N (4D+1), one launch each) and NEXT-2 GSPN-local fwd + bwd (kchunk = L/4; same bytes as the
+    global scan)."""
+    import torch
+
+    from synth import seed_for
+    from synth.device import fill_
+
+    peak, _ = peaks()
+    D, s = cfg.D, (2 if cfg.dtype == "bf16" else 4)
+    N = sh.B * sh.C * cfg.H * cfg.W
+    seed = seed_for(cfg.cfg_id)
+    u = fill_(torch.empty_like(h), seed, "u")
+    dy = fill_(torch.empty_like(t["x"]), seed, "dy")
+    y = torch.empty_like(t["x"])
+    dh2, du = torch.empty_like(h), torch.empty_like(h)
+
+    def timed(fn, reps):
+        for _ in range(3):
+            fn()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        return e0.elapsed_time(e1) / reps
+
+    reps = max(3, args.steps)
+    out = {}
+    mf = timed(lambda: gspn.merge_fwd(h, u, cfg.dirs, out=y), reps)
+    mb = timed(lambda: gspn.merge_bwd(h, u, dy, cfg.dirs, outs=(dh2, du)), reps)
+    for name, ms, nbytes in (("merge_fwd", mf, s * N * (2 * D + 1)), ("merge_bwd", mb, s * N * (4 * D + 1))):
+        gbs = nbytes / (ms * 1e-3) / 1e9
+        out[name] = {"ms": ms, "gbs": gbs, "frac": gbs / peak, "bytes": nbytes, "launches": 1}
+    del u, dy, y, dh2, du
+    k = max(1, min(cfg.H, cfg.W) // 4)
+    lf = timed(lambda: gspn.fwd(t["x"], t["w_l"], t["w_m"], t["w_r"], t["lam"], cfg.dirs, sh.G, out=h, kchunk=k), reps)
+    lpath = gspn.last_path()
+    lb = timed(lambda: gspn.bwd(t["x"], t["w_l"], t["w_m"], t["w_r"], t["lam"], h, t["dh"], cfg.dirs, sh.G,
+                                outs=outs, workspace=ws, kchunk=k), reps)
+    bf = gspn.algorithmic_bytes(sh.B, sh.C, cfg.H, cfg.W, cfg.dirs, sh.G,
+                                gspn.DTYPE_BF16 if cfg.dtype == "bf16" else gspn.DTYPE_F32, False)
+    out["local"] = {"kchunk": k, "fwd_ms": lf, "bwd_ms": lb, "gbs": 3 * bf / ((lf + lb) * 1e-3) / 1e9,
+                    "path": lpath}
+    out["local"]["frac"] = out["local"]["gbs"] / peak
+    return out
 
 
 def run_e2e(args, gspn, cfg, sh, t, h, outs, ws, dev, world, dist):

@@ -67,6 +67,7 @@ typedef enum { GSPN_F32 = 0, GSPN_BF16 = 1 } gspn_dtype_t;
 
 #define GSPN_FLAG_PRENORMALIZED 0x1u /* taps already row-normalised: no division (out-of-range taps still dropped) */
 #define GSPN_FLAG_FORCE_GENERIC 0x2u /* testing: force the generic (non-TMA) kernels */
+#define GSPN_FLAG_MERGE_MEAN 0x4u    /* gspn_merge_*: combine the directions by Mean instead of Sum */
 
 /* cudaStream_t without including CUDA headers (ABI-identical: an opaque pointer). */
 typedef struct CUstream_st* gspn_stream_t;
@@ -96,6 +97,25 @@ gspn_status_t gspn_bwd(const void* x, const void* w_l, const void* w_m, const vo
                        gspn_dtype_t dtype, uint32_t flags, void* workspace, size_t workspace_bytes,
                        gspn_stream_t stream);
 
+/*
+ * GSPN-local variant (§3.2: "splits each row or column into fixed-length segments of size
+ * kchunk and confines propagation to within those segments"). The scan axis of
+ * every direction is cut into segments of kchunk steps fixed on the canonical image grid (canonical
+ * row i for T2B/B2T, column j for L2R/R2L, in segment i / kchunk resp. j / kchunk; the last segment may
+ * be short), and h restarts from 0 at each segment's first step in scan order (
+ * DESIGN.md R19). kchunk = 0 (or >= the scan length) is the global scan: gspn_fwd / gspn_bwd are
+ * exactly these calls with kchunk = 0. kchunk < 0 is GSPN_ERR_INVALID_ARG. In the backward, the taps of a
+ * segment's first step get dw = 0. Everything else as gspn_fwd / gspn_bwd (same workspace size).
+ */
+gspn_status_t gspn_fwd_local(const void* x, const void* w_l, const void* w_m, const void* w_r, const void* lam,
+                             void* h, int64_t B, int64_t C, int64_t H, int64_t W, uint32_t dirs, int64_t groups,
+                             int64_t kchunk, gspn_dtype_t dtype, uint32_t flags, gspn_stream_t stream);
+gspn_status_t gspn_bwd_local(const void* x, const void* w_l, const void* w_m, const void* w_r, const void* lam,
+                             const void* h, const void* dh, void* dx, void* dw_l, void* dw_m, void* dw_r, void* dlam,
+                             int64_t B, int64_t C, int64_t H, int64_t W, uint32_t dirs, int64_t groups,
+                             int64_t kchunk, gspn_dtype_t dtype, uint32_t flags, void* workspace,
+                             size_t workspace_bytes, gspn_stream_t stream);
+
 /* Workspace bytes gspn_bwd needs for this problem (0 on invalid arguments). */
 size_t gspn_bwd_workspace_bytes(int64_t B, int64_t C, int64_t H, int64_t W, uint32_t dirs, int64_t groups,
                                 gspn_dtype_t dtype);
@@ -104,6 +124,27 @@ size_t gspn_bwd_workspace_bytes(int64_t B, int64_t C, int64_t H, int64_t W, uint
  *   fwd = s * (N (1 + 2D) + 3 D N_w),  bwd = 2 * fwd,  N = B C H W,  N_w = B G H W. */
 double gspn_algorithmic_bytes(int64_t B, int64_t C, int64_t H, int64_t W, uint32_t dirs, int64_t groups,
                               gspn_dtype_t dtype, int backward);
+
+/*
+ * Output gate + direction merge. PAPER.md:84-88 (§3.2, Eq. 2) gates each
+ * pass's state, y = u (.) h; the four directional passes are "combined" -- by Sum, or by
+ * Mean with GSPN_FLAG_MERGE_MEAN (R7):
+ *     y = s * sum_d u_d (.) h_d,      s = 1 (Sum) or 1/D (Mean)
+ *   h, u [D,B,C,H,W] (slabs in bit order, as gspn_fwd's h)  ->  y [B,C,H,W]
+ * Arithmetic in fp32, y rounded once to dtype. flags: 0 or GSPN_FLAG_MERGE_MEAN. Pointers non-null,
+ * 16-byte aligned; y must not overlap h or u. One launch; HBM-bound (s N (2D + 1) bytes).
+ */
+gspn_status_t gspn_merge_fwd(const void* h, const void* u, void* y, int64_t B, int64_t C, int64_t H, int64_t W,
+                             uint32_t dirs, gspn_dtype_t dtype, uint32_t flags, gspn_stream_t stream);
+
+/*
+ * Adjoint of gspn_merge_fwd given dy [B,C,H,W]:  dh_d = s * u_d (.) dy,  du_d = s * h_d (.) dy
+ * (dh, du [D,B,C,H,W]; dh is what gspn_bwd takes as its upstream gradient). No output may overlap an
+ * input or the other output. One launch; s N (4D + 1) bytes.
+ */
+gspn_status_t gspn_merge_bwd(const void* h, const void* u, const void* dy, void* dh, void* du, int64_t B, int64_t C,
+                             int64_t H, int64_t W, uint32_t dirs, gspn_dtype_t dtype, uint32_t flags,
+                             gspn_stream_t stream);
 
 const char* gspn_status_string(gspn_status_t s);
 /* Thread-local detail string of the last failing call on this thread (names the offending argument). */

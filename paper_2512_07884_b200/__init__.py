@@ -5,6 +5,9 @@ stream; every step of the scan runs in the CUDA kernels of libgspn.so. No CPU fa
 
   fwd(x, w_l, w_m, w_r, lam, dirs, groups, flags=0) -> h
   bwd(x, w_l, w_m, w_r, lam, h, dh, dirs, groups, flags=0) -> (dx, dw_l, dw_m, dw_r, dlam)
+  fwd(..., kchunk=k) / bwd(..., kchunk=k)                (GSPN-local, P:91-92)
+  merge_fwd(h, u, dirs, mean=False) -> y               (output gate + direction merge, Eq. 2)
+  merge_bwd(h, u, dy, dirs, mean=False) -> (dh, du)
 
 Shapes (gspn.h): x [B,C,H,W]; w_* [D,B,G,H,W]; lam, h, dh, dlam [D,B,C,H,W]; dx [B,C,H,W].
 """
@@ -17,6 +20,7 @@ from ._lib import GspnError, check, last_launch_count, last_path, lib  # noqa: F
 DIR_T2B, DIR_B2T, DIR_L2R, DIR_R2L, DIR_ALL = 0x1, 0x2, 0x4, 0x8, 0xF
 FLAG_PRENORMALIZED = 0x1
 FLAG_FORCE_GENERIC = 0x2
+FLAG_MERGE_MEAN = 0x4
 DTYPE_F32, DTYPE_BF16 = 0, 1
 
 
@@ -58,8 +62,8 @@ def popcount(d: int) -> int:
 
 
 def fwd(x, w_l, w_m, w_r, lam, dirs: int = DIR_ALL, groups: int | None = None, flags: int = 0, out=None,
-        stream=None):
-    """Forward scan. groups defaults to C (per-channel weights)."""
+        stream=None, kchunk: int = 0):
+    """Forward scan. groups defaults to C (per-channel weights); kchunk > 0: GSPN-local (gspn_fwd_local)."""
     torch = _torch()
     B, C, H, W = x.shape
     G = C if groups is None else int(groups)
@@ -71,8 +75,12 @@ def fwd(x, w_l, w_m, w_r, lam, dirs: int = DIR_ALL, groups: int | None = None, f
             raise ValueError(f"{n} shape {tuple(w.shape)} != {(D, B, G, H, W)}")
     h = torch.empty_like(lam) if out is None else out
     _check_tensors([("x", x), ("w_l", w_l), ("w_m", w_m), ("w_r", w_r), ("lam", lam), ("h", h)], x.dtype, x.device)
-    check(lib().gspn_fwd(x.data_ptr(), w_l.data_ptr(), w_m.data_ptr(), w_r.data_ptr(), lam.data_ptr(), h.data_ptr(),
-                         B, C, H, W, dirs, G, _dtype_code(x), flags, _stream_ptr(stream, x.device)))
+    ptrs = (x.data_ptr(), w_l.data_ptr(), w_m.data_ptr(), w_r.data_ptr(), lam.data_ptr(), h.data_ptr())
+    if kchunk:
+        check(lib().gspn_fwd_local(*ptrs, B, C, H, W, dirs, G, int(kchunk), _dtype_code(x), flags,
+                                   _stream_ptr(stream, x.device)))
+    else:
+        check(lib().gspn_fwd(*ptrs, B, C, H, W, dirs, G, _dtype_code(x), flags, _stream_ptr(stream, x.device)))
     return h
 
 
@@ -85,7 +93,7 @@ def algorithmic_bytes(B, C, H, W, dirs, groups, dtype_code, backward: bool) -> f
 
 
 def bwd(x, w_l, w_m, w_r, lam, h, dh, dirs: int = DIR_ALL, groups: int | None = None, flags: int = 0,
-        outs=None, workspace=None, stream=None):
+        outs=None, workspace=None, stream=None, kchunk: int = 0):
     """Backward scan: returns (dx, dw_l, dw_m, dw_r, dlam)."""
     torch = _torch()
     B, C, H, W = x.shape
@@ -100,9 +108,37 @@ def bwd(x, w_l, w_m, w_r, lam, h, dh, dirs: int = DIR_ALL, groups: int | None = 
     need = workspace_bytes(B, C, H, W, dirs, G, dt)
     if workspace is None or workspace.numel() < need:
         workspace = torch.empty(max(need, 16), dtype=torch.uint8, device=x.device)
-    check(lib().gspn_bwd(x.data_ptr(), w_l.data_ptr(), w_m.data_ptr(), w_r.data_ptr(), lam.data_ptr(), h.data_ptr(),
-                         dh.data_ptr(), dx.data_ptr(), dwl.data_ptr(), dwm.data_ptr(), dwr.data_ptr(),
-                         dlam.data_ptr(), B, C, H, W, dirs, G, dt, flags,
-                         workspace.data_ptr() if need > 0 else None, workspace.numel(),
-                         _stream_ptr(stream, x.device)))
+    ptrs = (x.data_ptr(), w_l.data_ptr(), w_m.data_ptr(), w_r.data_ptr(), lam.data_ptr(), h.data_ptr(),
+            dh.data_ptr(), dx.data_ptr(), dwl.data_ptr(), dwm.data_ptr(), dwr.data_ptr(), dlam.data_ptr())
+    ws = (workspace.data_ptr() if need > 0 else None, workspace.numel(), _stream_ptr(stream, x.device))
+    if kchunk:
+        check(lib().gspn_bwd_local(*ptrs, B, C, H, W, dirs, G, int(kchunk), dt, flags, *ws))
+    else:
+        check(lib().gspn_bwd(*ptrs, B, C, H, W, dirs, G, dt, flags, *ws))
     return dx, dwl, dwm, dwr, dlam
+
+
+def merge_fwd(h, u, dirs: int = DIR_ALL, mean: bool = False, out=None, stream=None):
+    """y [B,C,H,W] = s * sum_d u_d * h_d (s = 1, or 1/D with mean=True)."""
+    torch = _torch()
+    D, B, C, H, W = h.shape
+    if D != popcount(dirs) or tuple(u.shape) != tuple(h.shape):
+        raise ValueError(f"h {tuple(h.shape)} / u {tuple(u.shape)} do not match dirs=0x{dirs:x}")
+    y = torch.empty(h.shape[1:], dtype=h.dtype, device=h.device) if out is None else out
+    _check_tensors([("h", h), ("u", u), ("y", y)], h.dtype, h.device)
+    check(lib().gspn_merge_fwd(h.data_ptr(), u.data_ptr(), y.data_ptr(), B, C, H, W, dirs, _dtype_code(h),
+                               FLAG_MERGE_MEAN if mean else 0, _stream_ptr(stream, h.device)))
+    return y
+
+
+def merge_bwd(h, u, dy, dirs: int = DIR_ALL, mean: bool = False, outs=None, stream=None):
+    """(dh, du) [D,B,C,H,W] of merge_fwd given dy [B,C,H,W]."""
+    torch = _torch()
+    D, B, C, H, W = h.shape
+    if D != popcount(dirs) or tuple(u.shape) != tuple(h.shape) or tuple(dy.shape) != tuple(h.shape[1:]):
+        raise ValueError("h / u / dy shapes do not match")
+    dh, du = (torch.empty_like(h), torch.empty_like(h)) if outs is None else outs
+    _check_tensors([("h", h), ("u", u), ("dy", dy), ("dh", dh), ("du", du)], h.dtype, h.device)
+    check(lib().gspn_merge_bwd(h.data_ptr(), u.data_ptr(), dy.data_ptr(), dh.data_ptr(), du.data_ptr(), B, C, H, W,
+                               dirs, _dtype_code(h), FLAG_MERGE_MEAN if mean else 0, _stream_ptr(stream, h.device)))
+    return dh, du

@@ -138,8 +138,15 @@ size_t gspn_bwd_workspace_bytes(int64_t B, int64_t C, int64_t H, int64_t W, uint
 gspn_status_t gspn_fwd(const void* x, const void* w_l, const void* w_m, const void* w_r, const void* lam, void* h,
                        int64_t B, int64_t C, int64_t H, int64_t W, uint32_t dirs, int64_t groups,
                        gspn_dtype_t dtype, uint32_t flags, gspn_stream_t stream) {
+  return gspn_fwd_local(x, w_l, w_m, w_r, lam, h, B, C, H, W, dirs, groups, 0, dtype, flags, stream);
+}
+
+gspn_status_t gspn_fwd_local(const void* x, const void* w_l, const void* w_m, const void* w_r, const void* lam,
+                             void* h, int64_t B, int64_t C, int64_t H, int64_t W, uint32_t dirs, int64_t groups,
+                             int64_t kchunk, gspn_dtype_t dtype, uint32_t flags, gspn_stream_t stream) {
   try {
     gspn_status_t st;
+    if (kchunk < 0) return fail(GSPN_ERR_INVALID_ARG, "%s must be >= 0 (got %lld)", "kchunk", kchunk);
     if ((st = check_ptr(x, "x")) || (st = check_ptr(w_l, "w_l")) || (st = check_ptr(w_m, "w_m")) ||
         (st = check_ptr(w_r, "w_r")) || (st = check_ptr(lam, "lam")) || (st = check_ptr(h, "h")))
       return st;
@@ -160,6 +167,7 @@ gspn_status_t gspn_fwd(const void* x, const void* w_l, const void* w_m, const vo
     memset(&p, 0, sizeof p);
     p.x = x; p.wl = w_l; p.wm = w_m; p.wr = w_r; p.lam = lam; p.hout = h;
     p.B = B; p.C = C; p.H = H; p.W = W; p.G = groups; p.D = D; p.flags = flags;
+    p.kchunk = kchunk >= (H > W ? H : W) ? 0 : kchunk;  // a segment covering every scan is the global scan
     fill_dirs(p, dirs);
     cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
     int launches = 0;
@@ -188,8 +196,18 @@ gspn_status_t gspn_bwd(const void* x, const void* w_l, const void* w_m, const vo
                        int64_t B, int64_t C, int64_t H, int64_t W, uint32_t dirs, int64_t groups,
                        gspn_dtype_t dtype, uint32_t flags, void* workspace, size_t workspace_bytes,
                        gspn_stream_t stream) {
+  return gspn_bwd_local(x, w_l, w_m, w_r, lam, h, dh, dx, dw_l, dw_m, dw_r, dlam, B, C, H, W, dirs, groups, 0, dtype,
+                        flags, workspace, workspace_bytes, stream);
+}
+
+gspn_status_t gspn_bwd_local(const void* x, const void* w_l, const void* w_m, const void* w_r, const void* lam,
+                             const void* h, const void* dh, void* dx, void* dw_l, void* dw_m, void* dw_r, void* dlam,
+                             int64_t B, int64_t C, int64_t H, int64_t W, uint32_t dirs, int64_t groups,
+                             int64_t kchunk, gspn_dtype_t dtype, uint32_t flags, void* workspace,
+                             size_t workspace_bytes, gspn_stream_t stream) {
   try {
     gspn_status_t st;
+    if (kchunk < 0) return fail(GSPN_ERR_INVALID_ARG, "%s must be >= 0 (got %lld)", "kchunk", kchunk);
     if ((st = check_ptr(x, "x")) || (st = check_ptr(w_l, "w_l")) || (st = check_ptr(w_m, "w_m")) ||
         (st = check_ptr(w_r, "w_r")) || (st = check_ptr(lam, "lam")) || (st = check_ptr(h, "h")) ||
         (st = check_ptr(dh, "dh")) || (st = check_ptr(dx, "dx")) || (st = check_ptr(dw_l, "dw_l")) ||
@@ -222,6 +240,7 @@ gspn_status_t gspn_bwd(const void* x, const void* w_l, const void* w_m, const vo
     p.x = x; p.wl = w_l; p.wm = w_m; p.wr = w_r; p.lam = lam; p.h = h; p.dh = dh;
     p.dx = dx; p.dwl = dw_l; p.dwm = dw_m; p.dwr = dw_r; p.dlam = dlam;
     p.B = B; p.C = C; p.H = H; p.W = W; p.G = groups; p.D = D; p.flags = flags;
+    p.kchunk = kchunk >= (H > W ? H : W) ? 0 : kchunk;
     fill_dirs(p, dirs);
     cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
     int launches = 0;
@@ -261,6 +280,85 @@ gspn_status_t gspn_bwd(const void* x, const void* w_l, const void* w_m, const vo
     snprintf(t_detail, sizeof t_detail, "internal error");
     return GSPN_ERR_INTERNAL;
   }
+}
+
+}  // extern "C"
+
+namespace {
+
+// Shared validation of the merge entry points (dims, dirs, dtype, flags).
+gspn_status_t check_merge(int64_t B, int64_t C, int64_t H, int64_t W, uint32_t dirs, gspn_dtype_t dt, uint32_t flags) {
+  if (flags & ~GSPN_FLAG_MERGE_MEAN) return fail(GSPN_ERR_INVALID_ARG, "%s has unknown bits (0x%llx)", "flags", flags);
+  return check_dims(B, C, H, W, dirs, 1, dt, 0);
+}
+
+template <typename F>
+gspn_status_t guarded(F&& f) {
+  try {
+    return f();
+  } catch (const std::exception& ex) {
+    snprintf(t_detail, sizeof t_detail, "internal: %s", ex.what());
+    return GSPN_ERR_INTERNAL;
+  } catch (...) {
+    snprintf(t_detail, sizeof t_detail, "internal error");
+    return GSPN_ERR_INTERNAL;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+gspn_status_t gspn_merge_fwd(const void* h, const void* u, void* y, int64_t B, int64_t C, int64_t H, int64_t W,
+                             uint32_t dirs, gspn_dtype_t dtype, uint32_t flags, gspn_stream_t stream) {
+  return guarded([&]() -> gspn_status_t {
+    gspn_status_t st;
+    if ((st = check_ptr(h, "h")) || (st = check_ptr(u, "u")) || (st = check_ptr(y, "y"))) return st;
+    if ((st = check_merge(B, C, H, W, dirs, dtype, flags))) return st;
+    const int D = popcount4(dirs);
+    const size_t s = dtype == GSPN_BF16 ? 2 : 4;
+    const int64_t N = B * C * H * W;
+    const Span ins[2] = {span("h", h, (size_t)D * N * s), span("u", u, (size_t)D * N * s)};
+    const Span outs[1] = {span("y", y, (size_t)N * s)};
+    if ((st = check_aliasing(outs, 1, ins, 2))) return st;
+    const cudaError_t e = gspn::launch_merge_fwd(h, u, y, N, D, flags & GSPN_FLAG_MERGE_MEAN, dtype,
+                                                 reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) {
+      snprintf(t_detail, sizeof t_detail, "CUDA error: %s", cudaGetErrorString(e));
+      return GSPN_ERR_CUDA;
+    }
+    t_path = "merge";
+    t_launches = 1;
+    return GSPN_OK;
+  });
+}
+
+gspn_status_t gspn_merge_bwd(const void* h, const void* u, const void* dy, void* dh, void* du, int64_t B, int64_t C,
+                             int64_t H, int64_t W, uint32_t dirs, gspn_dtype_t dtype, uint32_t flags,
+                             gspn_stream_t stream) {
+  return guarded([&]() -> gspn_status_t {
+    gspn_status_t st;
+    if ((st = check_ptr(h, "h")) || (st = check_ptr(u, "u")) || (st = check_ptr(dy, "dy")) ||
+        (st = check_ptr(dh, "dh")) || (st = check_ptr(du, "du")))
+      return st;
+    if ((st = check_merge(B, C, H, W, dirs, dtype, flags))) return st;
+    const int D = popcount4(dirs);
+    const size_t s = dtype == GSPN_BF16 ? 2 : 4;
+    const int64_t N = B * C * H * W;
+    const Span ins[3] = {span("h", h, (size_t)D * N * s), span("u", u, (size_t)D * N * s),
+                         span("dy", dy, (size_t)N * s)};
+    const Span outs[2] = {span("dh", dh, (size_t)D * N * s), span("du", du, (size_t)D * N * s)};
+    if ((st = check_aliasing(outs, 2, ins, 3))) return st;
+    const cudaError_t e = gspn::launch_merge_bwd(h, u, dy, dh, du, N, D, flags & GSPN_FLAG_MERGE_MEAN, dtype,
+                                                 reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) {
+      snprintf(t_detail, sizeof t_detail, "CUDA error: %s", cudaGetErrorString(e));
+      return GSPN_ERR_CUDA;
+    }
+    t_path = "merge";
+    t_launches = 1;
+    return GSPN_OK;
+  });
 }
 
 }  // extern "C"

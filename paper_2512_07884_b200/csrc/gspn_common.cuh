@@ -32,6 +32,7 @@ struct ScanParams {
   void* ws;                // bwd: caller workspace (carved by the launcher of the chosen path)
   size_t ws_bytes;
   int64_t B, C, H, W, G, D;
+  int64_t kchunk;          // GSPN-local segment length along the scan axis (0: global scan)
   uint32_t dirbit[4];      // direction bit (GSPN_DIR_*) of slab k
   uint32_t flags;
 };
@@ -55,6 +56,27 @@ __host__ __device__ __forceinline__ DirGeom dir_geom(uint32_t dirbit, int64_t H,
 
 __device__ __forceinline__ bool is_vertical(uint32_t dirbit) {
   return dirbit == GSPN_DIR_T2B || dirbit == GSPN_DIR_B2T;
+}
+
+// GSPN-local (R19): segments of kchunk steps fixed on the canonical image grid
+// (canonical scan-axis index s in segment s / kchunk, the last one short). A pixel starts its segment
+// in scan order -- its h_{t-1} is not propagated -- when s % kchunk == 0 (T2B, L2R) or
+// (s + 1) % kchunk == 0 or s is the last index (B2T, R2L). kchunk > 0.
+__host__ __device__ __forceinline__ bool seg_start_px(uint32_t dirbit, int64_t i, int64_t j, int64_t H, int64_t W,
+                                                      int64_t kchunk) {
+  switch (dirbit) {
+    case GSPN_DIR_T2B: return i % kchunk == 0;
+    case GSPN_DIR_B2T: return (i + 1) % kchunk == 0 || i == H - 1;
+    case GSPN_DIR_L2R: return j % kchunk == 0;
+    default:           return (j + 1) % kchunk == 0 || j == W - 1;  // R2L
+  }
+}
+// The same in scan coordinates: step t of a direction with scan length L (t = 0 always starts).
+__host__ __device__ __forceinline__ bool seg_start_step(uint32_t dirbit, int64_t t, int64_t L, int64_t kchunk) {
+  if (t == 0) return true;
+  if (kchunk <= 0) return false;
+  const bool fwd_dir = dirbit == GSPN_DIR_T2B || dirbit == GSPN_DIR_L2R;
+  return fwd_dir ? t % kchunk == 0 : (L - t) % kchunk == 0;  // reversed: canonical s = L-1-t
 }
 
 template <typename T> __device__ __forceinline__ float to_f(T v);

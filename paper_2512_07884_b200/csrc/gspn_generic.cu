@@ -31,7 +31,7 @@ __device__ __forceinline__ ChainIdx chain_idx(const ScanParams& p, int64_t chain
 
 // Forward, Eq. 1 / Eq. 3, h_{-1} = 0.
 template <typename T>
-__global__ void fwd_generic_kernel(ScanParams p) {
+__global__ void __launch_bounds__(1024) fwd_generic_kernel(ScanParams p) {
   extern __shared__ float smem[];
   const ChainIdx ci = chain_idx(p, blockIdx.x);
   const DirGeom gm = dir_geom(p.dirbit[ci.k], p.H, p.W);
@@ -51,7 +51,7 @@ __global__ void fwd_generic_kernel(ScanParams p) {
       const int64_t off = gm.base + t * gm.ts + r * gm.rs;
       const Taps tp = make_taps(to_f(wl[off]), to_f(wm[off]), to_f(wr[off]), r >= 1, r <= gm.P - 2, prenorm);
       float acc = 0.f;
-      if (t > 0) {
+      if (!seg_start_step(p.dirbit[ci.k], t, gm.L, p.kchunk)) {  // h_{-1} = 0; GSPN-local resets
         acc = tp.b * hp[r];
         if (r >= 1) acc = fmaf(tp.a, hp[r - 1], acc);
         if (r <= gm.P - 2) acc = fmaf(tp.c, hp[r + 1], acc);
@@ -70,7 +70,7 @@ __global__ void fwd_generic_kernel(ScanParams p) {
 // otherwise the normalised-tap gradients are summed over the group's channels into fp32 workspace
 // and finish_dw_kernel applies the Jacobian.
 template <typename T, bool kPerChannel>
-__global__ void bwd_generic_kernel(ScanParams p) {
+__global__ void __launch_bounds__(1024) bwd_generic_kernel(ScanParams p) {
   extern __shared__ float smem[];
   const ChainIdx ci = chain_idx(p, blockIdx.x);
   const DirGeom gm = dir_geom(p.dirbit[ci.k], p.H, p.W);
@@ -93,7 +93,7 @@ __global__ void bwd_generic_kernel(ScanParams p) {
     for (int64_t r = threadIdx.x; r < P; r += blockDim.x) {
       const int64_t off = gm.base + t * gm.ts + r * gm.rs;
       float g = to_f(dh[off]);
-      if (t + 1 < gm.L) {
+      if (t + 1 < gm.L && !seg_start_step(p.dirbit[ci.k], t + 1, gm.L, p.kchunk)) {
         const int64_t on = off + gm.ts;  // pixel (t+1, r)
         const Taps tm = make_taps(to_f(wl[on]), to_f(wm[on]), to_f(wr[on]), r >= 1, r <= P - 2, prenorm);
         g = fmaf(tm.b, gn[r], g);
@@ -112,7 +112,8 @@ __global__ void bwd_generic_kernel(ScanParams p) {
       dlam[off] = from_f<T>(g * to_f(x[off]));
       atomicAdd(dx_acc + off, g * to_f(lam[off]));
       float Da = 0.f, Db = 0.f, Dc = 0.f;
-      if (t >= 1) {
+      const bool has_prev = !seg_start_step(p.dirbit[ci.k], t, gm.L, p.kchunk);
+      if (has_prev) {
         const int64_t op = off - gm.ts;  // pixel (t-1, r)
         Db = g * to_f(h[op]);
         if (r >= 1) Da = g * to_f(h[op - gm.rs]);
@@ -125,7 +126,7 @@ __global__ void bwd_generic_kernel(ScanParams p) {
         static_cast<T*>(p.dwm)[wplane * HW + off] = from_f<T>(om);
         static_cast<T*>(p.dwr)[wplane * HW + off] = from_f<T>(r <= P - 2 ? orr : 0.f);
       } else {
-        if (t >= 1) {
+        if (has_prev) {
           if (r >= 1) atomicAdd(p.dwa_l + wplane * HW + off, Da);
           atomicAdd(p.dwa_m + wplane * HW + off, Db);
           if (r <= P - 2) atomicAdd(p.dwa_r + wplane * HW + off, Dc);

@@ -16,4 +16,10 @@ cudaError_t launch_fwd_stream(const ScanParams& p, gspn_dtype_t dt, cudaStream_t
 cudaError_t launch_bwd_stream(const ScanParams& p, gspn_dtype_t dt, cudaStream_t s, int* launches, bool* handled);
 size_t stream_bwd_workspace_bytes(int64_t B, int64_t C, int64_t H, int64_t W, int64_t D, int64_t G, gspn_dtype_t dt);
 
+// Output gate + direction merge (gspn_merge.cu). N = B*C*H*W elements per direction slab.
+cudaError_t launch_merge_fwd(const void* h, const void* u, void* y, int64_t N, int D, bool mean, gspn_dtype_t dt,
+                             cudaStream_t st);
+cudaError_t launch_merge_bwd(const void* h, const void* u, const void* dy, void* dh, void* du, int64_t N, int D,
+                             bool mean, gspn_dtype_t dt, cudaStream_t st);
+
 }  // namespace gspn

@@ -656,6 +656,19 @@ __device__ __forceinline__ float norm_inv(float s) {
   else return fast_rcp(s);
 }
 
+// GSPN-local (R19): bit p of the result is set when the p-th step a half
+// processes starts a kchunk segment in scan order. c_first: canonical scan-axis index (row / column) of
+// that half's first processed step; cstep = +-1: canonical index change per processed step; scan_fwd:
+// T2B / L2R (segment start s % k == 0) vs B2T / R2L ((s + 1) % k == 0). One modulo per half.
+__device__ __forceinline__ uint32_t reset_bits(int c_first, int cstep, bool scan_fwd, int k, int n) {
+  const int target = scan_fwd ? 0 : k - 1;  // residue of a segment's first scan step
+  int o = (cstep * (target - c_first)) % k;
+  if (o < 0) o += k;
+  uint32_t m = 0;
+  for (; o < n; o += k) m |= 1u << o;
+  return m;
+}
+
 // ------------------------------------------------------------------------------ forward
 
 // One step of Eq. 1 at one position (taps already masked, see Lanes).
@@ -669,12 +682,16 @@ __device__ __forceinline__ float fwd_math(float x, float lam, float l, float m, 
 
 // Vertical half-tile: KS steps; p0 = the lane's operands at the half's first step, stepb = +-kRowB.
 // New states go straight to global memory (gp advances by gstep rows per step).
-template <typename T, int kPre>
+template <typename T, int kPre, bool kLocal>
 __device__ __forceinline__ void fwd_half_vert(const Lanes<T>& ln, const uint8_t* p0, int stepb, T* gp,
-                                              int64_t gstep, int t0, int L, float (&h)[kE], uint64_t pol) {
+                                              int64_t gstep, int t0, int L, float (&h)[kE], uint64_t pol,
+                                              uint32_t rm) {
   constexpr int KS = Cfg<T>::KS;
 #pragma unroll
   for (int ss = 0; ss < KS; ++ss) {
+    if constexpr (kLocal) {  // segment start: h_{t-1} does not propagate (warp-uniform)
+      if ((rm >> ss) & 1u) h[0] = h[1] = 0.f;
+    }
     const uint8_t* q = p0 + ss * stepb;
     float x[2], lam[2], l[2], m[2], r[2];
     vload<T>(q + F_X * kTile, x);
@@ -710,9 +727,9 @@ __device__ __forceinline__ void slot_hi(const float (&v)[kE], int lane, float (&
 
 // Horizontal half-tile: one 16-byte chunk (KS steps) per tensor per slot; kRev walks the chunk
 // backwards (R2L). The new states come back packed in memory order for the in-place write.
-template <typename T, int kPre, bool kRev>
+template <typename T, int kPre, bool kRev, bool kLocal>
 __device__ __forceinline__ void fwd_half_horiz(const Lanes<T>& ln, const uint8_t* st, int cm, int lane,
-                                               float (&h)[kE], uint4 (&OUT)[kE]) {
+                                               float (&h)[kE], uint4 (&OUT)[kE], uint32_t rm) {
   constexpr int KS = Cfg<T>::KS;
   uint4 X[kE], LAM[kE], WL[kE], WM[kE], WR[kE];
 #pragma unroll
@@ -728,6 +745,9 @@ __device__ __forceinline__ void fwd_half_horiz(const Lanes<T>& ln, const uint8_t
 #pragma unroll
   for (int ss = 0; ss < KS; ++ss) {
     const int i = kRev ? KS - 1 - ss : ss;  // element of the chunk (memory order)
+    if constexpr (kLocal) {
+      if ((rm >> ss) & 1u) h[0] = h[1] = 0.f;
+    }
     float lo[kE], hi[kE];
     slot_lo(h, lane, lo);
     slot_hi(h, lane, hi);
@@ -742,7 +762,7 @@ __device__ __forceinline__ void fwd_half_horiz(const Lanes<T>& ln, const uint8_t
   for (int q = 0; q < kE; ++q) OUT[q] = Pk<T>::pack(O[q]);
 }
 
-template <typename T, int kPre, bool kCl>
+template <typename T, int kPre, bool kCl, bool kLocal>
 __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) fwd_stream_kernel(const __grid_constant__ StreamArgs A) {
   using C = Cfg<T>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -770,6 +790,7 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) fwd_stream_kernel(const
   const uint64_t pol_vout = policy_of(pl.pol[3]);
   const int nthreads = pl.nwc * 32;
   const int64_t W = A.p.W;
+  const int kchunk = static_cast<int>(A.p.kchunk);
   const int rank = kCl ? static_cast<int>(cluster_ctarank()) : 0;
   const XSrc xs = make_xsrc<T>(warp, pl.nwc, lane);
   uint32_t xphase = 0;  // P-split: phase bit of the cluster edge barriers, per parity
@@ -789,17 +810,22 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) fwd_stream_kernel(const
         uint4 OUT[kE];
         const int cm = ch.rev ? 1 - half : half;  // horizontal: memory chunk of this half
         if (!pl.null_compute) {
+          uint32_t rm = 0;
           if (ch.vert) {
             const int t0 = j * C::K + half * C::KS;
             const int kk0 = ch.rev ? C::K - 1 - half * C::KS : half * C::KS;
             const int row0 = ch.rev ? ch.L - 1 - t0 : t0;
             const int vs = static_cast<int>(pl.vstep);
-            fwd_half_vert<T, kPre>(ln, st + ln.voff + kk0 * vs, ch.rev ? -vs : vs,
-                                   hout + static_cast<int64_t>(row0) * W, ch.rev ? -W : W, t0, ch.L, h, pol_vout);
-          } else if (ch.rev) {
-            fwd_half_horiz<T, kPre, true>(ln, st, cm, lane, h, OUT);
+            if constexpr (kLocal) rm = reset_bits(row0, ch.rev ? -1 : 1, !ch.rev, kchunk, C::KS);
+            fwd_half_vert<T, kPre, kLocal>(ln, st + ln.voff + kk0 * vs, ch.rev ? -vs : vs,
+                                           hout + static_cast<int64_t>(row0) * W, ch.rev ? -W : W, t0, ch.L, h,
+                                           pol_vout, rm);
           } else {
-            fwd_half_horiz<T, kPre, false>(ln, st, cm, lane, h, OUT);
+            if constexpr (kLocal)
+              rm = reset_bits(tile_start(ch, j, C::K) + cm * C::KS + (ch.rev ? C::KS - 1 : 0), ch.rev ? -1 : 1,
+                              !ch.rev, kchunk, C::KS);
+            if (ch.rev) fwd_half_horiz<T, kPre, true, kLocal>(ln, st, cm, lane, h, OUT, rm);
+            else fwd_half_horiz<T, kPre, false, kLocal>(ln, st, cm, lane, h, OUT, rm);
           }
         }
         edge_publish(m.edge + par * kEdgeW * kXRow, warp, lane, ch.vert, h);
@@ -859,9 +885,9 @@ __device__ __forceinline__ float bwd_math(float dh, float l, float m, float r, f
   return ge;
 }
 
-template <typename T, int kPre>
+template <typename T, int kPre, bool kLocal>
 __device__ __forceinline__ void bwd_half_vert(const Lanes<T>& ln, const uint8_t* p0, int stepb, T* gp,
-                                              int64_t gstep, int t0, int L, BwdState& S, uint64_t pol) {
+                                              int64_t gstep, int t0, int L, BwdState& S, uint64_t pol, uint32_t rm) {
   constexpr int KS = Cfg<T>::KS;
   // steps t0 + KS - 1 down to t0; p0 / gp address step t0 + KS - 1
 #pragma unroll
@@ -880,12 +906,15 @@ __device__ __forceinline__ void bwd_half_vert(const Lanes<T>& ln, const uint8_t*
     g[1] = bwd_math<kPre>(dh[1], l[1], m[1], r[1], nr1, ec1, S.ea[1], S.eb[1], S.ec[1]);
     GStore<T, 2>::st_if(ln.own_v && t0 + KS - 1 - i < L, gp, g, pol);
     gp += gstep;
+    if constexpr (kLocal) {  // segment start: g_{t-1} receives nothing from step t
+      if ((rm >> i) & 1u) S.ea[0] = S.ea[1] = S.eb[0] = S.eb[1] = S.ec[0] = S.ec[1] = 0.f;
+    }
   }
 }
 
-template <typename T, int kPre, bool kRev>
+template <typename T, int kPre, bool kRev, bool kLocal>
 __device__ __forceinline__ void bwd_half_horiz(const Lanes<T>& ln, const uint8_t* st, int cm, int lane, BwdState& S,
-                                               uint4 (&OG)[kE]) {
+                                               uint4 (&OG)[kE], uint32_t rm) {
   constexpr int KS = Cfg<T>::KS;
   uint4 DH[kE], WL[kE], WM[kE], WR[kE];
 #pragma unroll
@@ -908,12 +937,15 @@ __device__ __forceinline__ void bwd_half_horiz(const Lanes<T>& ln, const uint8_t
       G_[q][i] = bwd_math<kPre>(hget<T>(DH[q], i), hget_tap<T>(WL[q], i, ln.s[0][q]),
                                 hget_tap<T>(WM[q], i, ln.s[1][q]), hget_tap<T>(WR[q], i, ln.s[2][q]), nr[q], nl[q],
                                 S.ea[q], S.eb[q], S.ec[q]);
+    if constexpr (kLocal) {
+      if ((rm >> (KS - 1 - ss)) & 1u) S.ea[0] = S.ea[1] = S.eb[0] = S.eb[1] = S.ec[0] = S.ec[1] = 0.f;
+    }
   }
 #pragma unroll
   for (int q = 0; q < kE; ++q) OG[q] = Pk<T>::pack(G_[q]);
 }
 
-template <typename T, int kPre, bool kCl>
+template <typename T, int kPre, bool kCl, bool kLocal>
 __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_stream_kernel(const __grid_constant__ StreamArgs A) {
   using C = Cfg<T>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -941,6 +973,7 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_stream_kernel(const
   const uint64_t pol_vout = policy_of(pl.pol[3]);
   const int nthreads = pl.nwc * 32;
   const int64_t W = A.p.W;
+  const int kchunk = static_cast<int>(A.p.kchunk);
   const int rank = kCl ? static_cast<int>(cluster_ctarank()) : 0;
   const XSrc xs = make_xsrc<T>(warp, pl.nwc, lane);
   uint32_t xphase = 0;
@@ -963,18 +996,23 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_stream_kernel(const
         uint4 OG[kE];
         const int cm = ch.rev ? 1 - half : half;
         if (!pl.null_compute) {
+          uint32_t rm = 0;
           if (ch.vert) {
             const int t0 = j * C::K + half * C::KS;          // first (lowest) step of the half
             const int tl = t0 + C::KS - 1;                     // processed first
             const int kkl = ch.rev ? C::K - 1 - (half * C::KS + C::KS - 1) : half * C::KS + C::KS - 1;
             const int rowl = ch.rev ? ch.L - 1 - tl : tl;
             const int vs = static_cast<int>(pl.vstep);
-            bwd_half_vert<T, kPre>(ln, st + ln.voff + kkl * vs, ch.rev ? vs : -vs,
-                                   gout + static_cast<int64_t>(rowl) * W, ch.rev ? W : -W, t0, ch.L, S, pol_vout);
-          } else if (ch.rev) {
-            bwd_half_horiz<T, kPre, true>(ln, st, cm, lane, S, OG);
+            if constexpr (kLocal) rm = reset_bits(rowl, ch.rev ? 1 : -1, !ch.rev, kchunk, C::KS);
+            bwd_half_vert<T, kPre, kLocal>(ln, st + ln.voff + kkl * vs, ch.rev ? vs : -vs,
+                                           gout + static_cast<int64_t>(rowl) * W, ch.rev ? W : -W, t0, ch.L, S,
+                                           pol_vout, rm);
           } else {
-            bwd_half_horiz<T, kPre, false>(ln, st, cm, lane, S, OG);
+            if constexpr (kLocal)
+              rm = reset_bits(tile_start(ch, j, C::K) + cm * C::KS + (ch.rev ? 0 : C::KS - 1), ch.rev ? 1 : -1,
+                              !ch.rev, kchunk, C::KS);
+            if (ch.rev) bwd_half_horiz<T, kPre, true, kLocal>(ln, st, cm, lane, S, OG, rm);
+            else bwd_half_horiz<T, kPre, false, kLocal>(ln, st, cm, lane, S, OG, rm);
           }
         }
         edge_publish(m.edge + 0 * kXArr + par * kEdgeW * kXRow, warp, lane, ch.vert, S.ea);
@@ -1105,6 +1143,17 @@ __device__ __forceinline__ void accum_taps(uint32_t dir, const T* hp, int64_t H,
   }
 }
 
+// GSPN-local: the taps of a segment's first step act on a reset h_{t-1}, so their gradient is 0
+// (the D terms of a7 vanish). Uniform branch, no cost for the global scan (kchunk = 0).
+template <int V>
+__device__ __forceinline__ void local_dw_mask(const ScanParams& p, uint32_t dir, int64_t i, int64_t j0, float (&ol)[V],
+                                              float (&om)[V], float (&orr)[V]) {
+  if (p.kchunk <= 0) return;
+#pragma unroll
+  for (int q = 0; q < V; ++q)
+    if (seg_start_px(dir, i, j0 + q, p.H, p.W, p.kchunk)) ol[q] = om[q] = orr[q] = 0.f;
+}
+
 // dw_k for V columns of row i from the summed Da, Db, Dc.
 template <typename T, int V>
 __device__ __forceinline__ void finish_taps(const ScanParams& p, uint32_t dir, int64_t woff, int64_t i, int64_t j0,
@@ -1122,6 +1171,7 @@ __device__ __forceinline__ void finish_taps(const ScanParams& p, uint32_t dir, i
     const bool hl = r >= 1, hr = r <= P - 2;
     jacobian<true>(wl[q], wm[q], wr[q], hl, hr, prenorm, hl ? Da[q] : 0.f, Db[q], hr ? Dc[q] : 0.f, ol[q], om[q], orr[q]);
   }
+  local_dw_mask<V>(p, dir, i, j0, ol, om, orr);
   GVec<T, V>::store(static_cast<T*>(p.dwl) + woff, ol);
   GVec<T, V>::store(static_cast<T*>(p.dwm) + woff, om);
   GVec<T, V>::store(static_cast<T*>(p.dwr) + woff, orr);
@@ -1374,6 +1424,7 @@ __global__ void __launch_bounds__(256) bwd_out_pc_kernel(ScanParams p, const T* 
         jacobian<true>(wl[q], wm[q], wr[q], hl, hr, prenorm, hl ? Da[q] : 0.f, Db[q], hr ? Dc[q] : 0.f, ol[q], om[q],
                        orr[q]);
       }
+      local_dw_mask<V>(p, dir, i, j0, ol, om, orr);
       GVec<T, V>::store(static_cast<T*>(p.dwl) + off, ol);
       GVec<T, V>::store(static_cast<T*>(p.dwm) + off, om);
       GVec<T, V>::store(static_cast<T*>(p.dwr) + off, orr);
@@ -1570,6 +1621,7 @@ __global__ void __launch_bounds__((kOutConsumers + 1) * 32, 1) bwd_out_tma_kerne
           for (int q = 0; q < V; ++q)
             jacobian<true>(wl[q], wm[q], wr[q], hl, hr, prenorm, Da[q], Db[q], Dc[q], ol[q], om[q], orr[q]);
         }
+        local_dw_mask<V>(p, dir, i, j0, ol, om, orr);
         GVec<T, V>::store(static_cast<T*>(p.dwl) + off, ol);
         GVec<T, V>::store(static_cast<T*>(p.dwm) + off, om);
         GVec<T, V>::store(static_cast<T*>(p.dwr) + off, orr);
@@ -1748,6 +1800,7 @@ __global__ void __launch_bounds__((kOutConsumers + 1) * 32, 1) bwd_out_grp_tma_k
           jacobian<true>(wl[q], wm[q], wr[q], rp >= 1, rp <= P - 2, prenorm, Da[k][q], Db[k][q], Dc[k][q], ol[q],
                          om[q], orr[q]);
         }
+        local_dw_mask<V>(p, dir, i, j0, ol, om, orr);
         GVec<T, V>::store(static_cast<T*>(p.dwl) + woff, ol);
         GVec<T, V>::store(static_cast<T*>(p.dwm) + woff, om);
         GVec<T, V>::store(static_cast<T*>(p.dwr) + woff, orr);
@@ -1974,17 +2027,27 @@ cudaError_t launch(KernelT kernel, const StreamArgs& A, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// GSPN-local chains (kchunk > 0) run the kLocal instantiations, with the pre-normalised or the clamped
+// normaliser only (fewer instantiations; the clamped reciprocal is exact wherever S > 0).
 template <typename T, bool kCl>
-cudaError_t launch_fwd(int mode, const StreamArgs& A, cudaStream_t s) {
-  if (mode == kNormPre) return launch(fwd_stream_kernel<T, kNormPre, kCl>, A, s);
-  if (mode == kNormClamp) return launch(fwd_stream_kernel<T, kNormClamp, kCl>, A, s);
-  return launch(fwd_stream_kernel<T, kNormFull, kCl>, A, s);
+cudaError_t launch_fwd(int mode, bool local, const StreamArgs& A, cudaStream_t s) {
+  if (local) {
+    if (mode == kNormPre) return launch(fwd_stream_kernel<T, kNormPre, kCl, true>, A, s);
+    return launch(fwd_stream_kernel<T, kNormClamp, kCl, true>, A, s);
+  }
+  if (mode == kNormPre) return launch(fwd_stream_kernel<T, kNormPre, kCl, false>, A, s);
+  if (mode == kNormClamp) return launch(fwd_stream_kernel<T, kNormClamp, kCl, false>, A, s);
+  return launch(fwd_stream_kernel<T, kNormFull, kCl, false>, A, s);
 }
 template <typename T, bool kCl>
-cudaError_t launch_bwd(int mode, const StreamArgs& A, cudaStream_t s) {
-  if (mode == kNormPre) return launch(bwd_stream_kernel<T, kNormPre, kCl>, A, s);
-  if (mode == kNormClamp) return launch(bwd_stream_kernel<T, kNormClamp, kCl>, A, s);
-  return launch(bwd_stream_kernel<T, kNormFull, kCl>, A, s);
+cudaError_t launch_bwd(int mode, bool local, const StreamArgs& A, cudaStream_t s) {
+  if (local) {
+    if (mode == kNormPre) return launch(bwd_stream_kernel<T, kNormPre, kCl, true>, A, s);
+    return launch(bwd_stream_kernel<T, kNormClamp, kCl, true>, A, s);
+  }
+  if (mode == kNormPre) return launch(bwd_stream_kernel<T, kNormPre, kCl, false>, A, s);
+  if (mode == kNormClamp) return launch(bwd_stream_kernel<T, kNormClamp, kCl, false>, A, s);
+  return launch(bwd_stream_kernel<T, kNormFull, kCl, false>, A, s);
 }
 
 int norm_mode(const ScanParams& p, const Plan& pl) {
@@ -2030,8 +2093,9 @@ cudaError_t launch_fwd_stream(const ScanParams& p, gspn_dtype_t dt, cudaStream_t
   const int mode = norm_mode(p, A.plan);
   cudaError_t e;
   const bool cl = A.plan.cl > 1;
-  if (dt == GSPN_BF16) e = cl ? launch_fwd<BF, true>(mode, A, s) : launch_fwd<BF, false>(mode, A, s);
-  else e = cl ? launch_fwd<float, true>(mode, A, s) : launch_fwd<float, false>(mode, A, s);
+  const bool local = p.kchunk > 0;
+  if (dt == GSPN_BF16) e = cl ? launch_fwd<BF, true>(mode, local, A, s) : launch_fwd<BF, false>(mode, local, A, s);
+  else e = cl ? launch_fwd<float, true>(mode, local, A, s) : launch_fwd<float, false>(mode, local, A, s);
   *launches += 1;
   return e;
 }
@@ -2124,8 +2188,9 @@ cudaError_t launch_bwd_stream(const ScanParams& p0, gspn_dtype_t dt, cudaStream_
   using BF = __nv_bfloat16;
   const int mode = norm_mode(p, A.plan);
   const bool cl = A.plan.cl > 1;
-  if (dt == GSPN_BF16) e = cl ? launch_bwd<BF, true>(mode, A, s) : launch_bwd<BF, false>(mode, A, s);
-  else e = cl ? launch_bwd<float, true>(mode, A, s) : launch_bwd<float, false>(mode, A, s);
+  const bool local = p.kchunk > 0;
+  if (dt == GSPN_BF16) e = cl ? launch_bwd<BF, true>(mode, local, A, s) : launch_bwd<BF, false>(mode, local, A, s);
+  else e = cl ? launch_bwd<float, true>(mode, local, A, s) : launch_bwd<float, false>(mode, local, A, s);
   *launches += 1;
   if (e != cudaSuccess) return e;
   const bool per_channel = p.G == p.C;

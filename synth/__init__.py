@@ -12,7 +12,7 @@ Recipe (DESIGN.md "Input recipe"):
         -> fp32 (round-to-nearest-even) -> bf16 (RNE) for bf16 tensors
 Distributions mirror the paper's post-sigmoid affinities and gates and zero-mean
 activations: x, dh ~ U[-1, 1); lam ~ U[0, 1); w_l, w_m, w_r ~ U[0.05, 1) (strictly positive, so the
-row sum S > 0 everywhere and connectivity is dense).
+row sum S > 0 everywhere and connectivity is dense); the merge's gate u ~ U[0, 1), dy, hs ~ U[-1, 1).
 """
 from __future__ import annotations
 
@@ -33,6 +33,11 @@ STREAMS = {
     "w_r": (4, 0.05, 1.0),
     "lam": (5, 0.0, 1.0),
     "dh": (6, -1.0, 1.0),
+    # SURVEY §8(f) NEXT-1 (output gate + merge): u is a post-sigmoid-like gate,
+    # dy a zero-mean upstream gradient, hs a zero-mean stand-in state for merge-only tests
+    "u": (7, 0.0, 1.0),
+    "dy": (8, -1.0, 1.0),
+    "hs": (9, -1.0, 1.0),
 }
 
 

@@ -118,3 +118,36 @@ def test_python_binding_refuses_cpu_tensors():
     lam = torch.ones(1, 1, 2, 4, 4)
     with pytest.raises(ValueError, match="CUDA tensor"):
         gspn.fwd(x, w, w, w, lam, dirs=1, groups=2)
+
+
+def test_local_validation():
+    """gspn_fwd_local / gspn_bwd_local (GSPN-local) reject a negative kchunk before any CUDA call
+    and otherwise validate exactly like gspn_fwd / gspn_bwd."""
+    L = gspn.lib()
+    base = 1 << 30
+    assert L.gspn_fwd_local(A, A, A, A, A, A + base, 1, 4, 8, 8, 0xF, 4, -1, 1, 0, None) == 1
+    assert "kchunk" in detail()
+    assert L.gspn_fwd_local(None, A, A, A, A, A + base, 1, 4, 8, 8, 0xF, 4, 2, 1, 0, None) == 1
+    assert "x is NULL" in detail()
+    p = [A + k * base for k in range(12)]
+    assert L.gspn_bwd_local(*p, 2, 4, 16, 16, 0xF, 2, -3, 1, 0, A + (40 << 30), 1 << 40, None) == 1
+    assert "kchunk" in detail()
+    assert L.gspn_bwd_local(*p[:6], None, *p[7:], 2, 4, 16, 16, 0xF, 2, 4, 1, 0, A + (40 << 30), 1 << 40, None) == 1
+    assert "dh is NULL" in detail()
+
+
+def test_merge_validation():
+    """gspn_merge_fwd / gspn_merge_bwd (output gate + direction merge, Eq. 2)."""
+    L = gspn.lib()
+    base = 1 << 30
+    h, u, y = A, A + base, A + 2 * base
+    assert L.gspn_merge_fwd(None, u, y, 1, 4, 8, 8, 0xF, 1, 0, None) == 1 and "h is NULL" in detail()
+    assert L.gspn_merge_fwd(h, u + 2, y, 1, 4, 8, 8, 0xF, 1, 0, None) == 1 and "u is not 16-byte" in detail()
+    assert L.gspn_merge_fwd(h, u, y, 1, 4, 8, 8, 0x0, 1, 0, None) == 1 and "dirs" in detail()
+    assert L.gspn_merge_fwd(h, u, y, 1, 4, 8, 8, 0xF, 1, 0x1, None) == 1 and "flags" in detail()
+    assert L.gspn_merge_fwd(h, u, y, 0, 4, 8, 8, 0xF, 1, 0, None) == 1 and "B must be" in detail()
+    assert L.gspn_merge_fwd(h, u, h + 64, 1, 4, 8, 8, 0xF, 1, 0, None) == 1 and "overlaps" in detail()
+    dy, dh, du = A + 3 * base, A + 4 * base, A + 5 * base
+    assert L.gspn_merge_bwd(h, u, None, dh, du, 1, 4, 8, 8, 0xF, 1, 0, None) == 1 and "dy is NULL" in detail()
+    assert L.gspn_merge_bwd(h, u, dy, dh, dh + 16, 1, 4, 8, 8, 0xF, 1, 4, None) == 1 and "overlaps" in detail()
+    assert L.gspn_merge_bwd(h, u, dy, u, du, 1, 4, 8, 8, 0xF, 1, 4, None) == 1 and "overlaps" in detail()

@@ -1,0 +1,193 @@
+"""GPU parity of the SURVEY §8(f) rows against the fp64 oracle (through the C ABI):
+
+NEXT-1  gspn_merge_fwd / gspn_merge_bwd (output gate + direction merge, Eq. 2);
+        standalone, composed with the scan (fwd -> merge, merge adjoint -> bwd), and at BASELINE config 4's
+        full size on sampled outputs.
+
+Inputs come from synth on the host (never from the CUDA path); tolerances are north_star's normwise
+1e-5 (fp32) / 2e-2 (bf16) (R16), with the stored-dtype intermediates of DESIGN.md R18.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2512_07884_b200 as gspn
+import synth
+from tests.parity_utils import TOL, from_torch, host_inputs, host_tensor, normwise, round_io, small_config, to_torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _dev():
+    import torch
+
+    return torch.device("cuda:0")
+
+
+# (B, C, H, W, dirs, dtype): N % 8 == 0 (vector kernels) and N % 8 != 0 (scalar kernels), D = 1..4
+MERGE_SHAPES = [
+    (2, 4, 16, 16, 0xF, "bf16"),
+    (2, 4, 16, 16, 0xF, "f32"),
+    (1, 3, 5, 7, 0xF, "bf16"),
+    (1, 3, 5, 7, 0x5, "f32"),
+    (3, 2, 9, 11, 0x1, "bf16"),
+    (1, 8, 56, 56, 0x7, "bf16"),
+    (1, 1, 1, 1, 0xF, "f32"),
+]
+
+
+@pytest.mark.parametrize("mean", [False, True])
+@pytest.mark.parametrize("shape", MERGE_SHAPES, ids=lambda s: "B{}C{}H{}W{}d{:x}{}".format(*s))
+def test_merge_parity(shape, mean):
+    B, C, H, W, dirs, dt = shape
+    cfg = small_config(B, C, C, H, W, dirs, dt, cfg_id=601)
+    D = cfg.D
+    seed = synth.seed_for(cfg.cfg_id)
+    hv, hf = host_tensor(cfg, "hs", (D, B, C, H, W))
+    uv, uf = host_tensor(cfg, "u", (D, B, C, H, W))
+    gv, gf = host_tensor(cfg, "dy", (B, C, H, W))
+    assert seed == synth.seed_for(601)
+    dev = _dev()
+    h, u, dy = to_torch(hv, dt, dev), to_torch(uv, dt, dev), to_torch(gv, dt, dev)
+    y = gspn.merge_fwd(h, u, dirs, mean)
+    assert gspn.last_path() == "merge" and gspn.last_launch_count() == 1
+    dh, du = gspn.merge_bwd(h, u, dy, dirs, mean)
+    y_ref = oracle.merge_fwd(hf, uf, mean)
+    dh_ref, du_ref = oracle.merge_bwd(hf, uf, gf, mean)
+    tol = TOL[dt]
+    assert normwise(from_torch(y), y_ref) <= tol
+    for k in range(D):
+        assert normwise(from_torch(dh)[k], dh_ref[k]) <= tol
+        assert normwise(from_torch(du)[k], du_ref[k]) <= tol
+
+
+@pytest.mark.parametrize("shape", [(2, 4, 2, 40, 56, 0xF, "bf16"), (1, 3, 3, 17, 33, 0xF, "f32"),
+                                   (1, 4, 1, 64, 64, 0xF, "bf16")], ids=str)
+def test_scan_then_merge_end_to_end(shape):
+    """y = merge(fwd(...)); the adjoint chain dy -> (dh, du) -> gspn_bwd -> (dx, dw, dlam), against the
+    oracle chain evaluated on the stored-dtype intermediates (h and dh as the API stores them, R18)."""
+    B, C, G, H, W, dirs, dt = shape
+    cfg = small_config(B, C, G, H, W, dirs, dt, cfg_id=602)
+    inp = host_inputs(cfg)
+    f = {k: v[1] for k, v in inp.items()}
+    uv, uf = host_tensor(cfg, "u", (cfg.D, B, C, H, W))
+    gv, gf = host_tensor(cfg, "dy", (B, C, H, W))
+    dev = _dev()
+    t = {k: to_torch(v[0], dt, dev) for k, v in inp.items()}
+    u, dy = to_torch(uv, dt, dev), to_torch(gv, dt, dev)
+    h = gspn.fwd(t["x"], t["w_l"], t["w_m"], t["w_r"], t["lam"], dirs, G)
+    y = gspn.merge_fwd(h, u, dirs)
+    dh, du = gspn.merge_bwd(h, u, dy, dirs)
+    grads = gspn.bwd(t["x"], t["w_l"], t["w_m"], t["w_r"], t["lam"], h, dh, dirs, G)
+
+    h_ref = round_io(oracle.fwd(f["x"], f["w_l"], f["w_m"], f["w_r"], f["lam"], dirs, G), dt)
+    y_ref = oracle.merge_fwd(h_ref, uf)
+    dh_ref, du_ref = oracle.merge_bwd(h_ref, uf, gf)
+    g_ref = oracle.bwd(f["x"], f["w_l"], f["w_m"], f["w_r"], f["lam"], h_ref, round_io(dh_ref, dt), dirs, G)
+    tol = TOL[dt]
+    assert normwise(from_torch(y), y_ref) <= tol
+    assert normwise(from_torch(du), du_ref) <= tol
+    for name, a, r in zip(("dx", "dw_l", "dw_m", "dw_r", "dlam"), grads, g_ref):
+        assert normwise(from_torch(a), r) <= tol, name
+
+
+def test_merge_fullsize_config4_sampled():
+    """BASELINE configs[3] shape (B=4, C=320, 512 x 512, 4 directions, bf16) on device-generated inputs;
+    4096 sampled outputs of y, dh and du recomputed by the oracle from host-regenerated values."""
+    import torch
+
+    cfg = synth.get_config("4")
+    D, B, C, H, W = cfg.D, cfg.B, cfg.C, cfg.H, cfg.W
+    N = B * C * H * W
+    seed = synth.seed_for(cfg.cfg_id)
+    from synth.device import fill_
+
+    dev = _dev()
+    h = fill_(torch.empty((D, B, C, H, W), dtype=torch.bfloat16, device=dev), seed, "hs")
+    u = fill_(torch.empty((D, B, C, H, W), dtype=torch.bfloat16, device=dev), seed, "u")
+    dy = fill_(torch.empty((B, C, H, W), dtype=torch.bfloat16, device=dev), seed, "dy")
+    y = gspn.merge_fwd(h, u, 0xF)
+    dh, du = gspn.merge_bwd(h, u, dy, 0xF)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(4)
+    n = np.concatenate([rng.integers(0, N, 4090), [0, 1, N - 3, N - 2, N - 1, N // 2]]).astype(np.uint64)
+    idx = torch.from_numpy(n.astype(np.int64)).to(dev)
+    hs = np.stack([synth.as_f64(synth.values(seed, "hs", n + np.uint64(k * N), "bf16"), "bf16") for k in range(D)])
+    us = np.stack([synth.as_f64(synth.values(seed, "u", n + np.uint64(k * N), "bf16"), "bf16") for k in range(D)])
+    gs = synth.as_f64(synth.values(seed, "dy", n, "bf16"), "bf16")
+    y_ref = oracle.merge_fwd(hs, us)
+    dh_ref, du_ref = oracle.merge_bwd(hs, us, gs)
+    got_y = from_torch(y.reshape(-1)[idx])
+    got_dh = from_torch(dh.reshape(D, -1)[:, idx])
+    got_du = from_torch(du.reshape(D, -1)[:, idx])
+    assert normwise(got_y, y_ref) <= TOL["bf16"]
+    assert normwise(got_dh, dh_ref) <= TOL["bf16"]
+    assert normwise(got_du, du_ref) <= TOL["bf16"]
+
+
+# ------------------------------------------------------------------------------------ NEXT-2 kchunk
+
+# (B, C, G, H, W, dirs, dtype, kchunk): stream path (vertical/horizontal, reversed, partial first/last
+# tiles, packed small planes, grouped weights, P-split clusters) and segments shorter than, equal to and
+# longer than a 16-step tile, with a short last segment; kchunk = 1 (every step isolated).
+LOCAL_CASES = [
+    (1, 4, 4, 64, 64, 0xF, "bf16", 16),
+    (1, 4, 4, 64, 64, 0xF, "bf16", 5),
+    (2, 3, 3, 100, 72, 0xF, "bf16", 24),
+    (1, 4, 2, 37, 24, 0xF, "bf16", 7),
+    (2, 2, 2, 19, 12, 0xF, "f32", 3),
+    (1, 2, 2, 40, 56, 0xF, "f32", 8),
+    (2, 4, 4, 56, 56, 0xF, "bf16", 14),
+    (1, 4, 1, 64, 64, 0xF, "bf16", 32),
+    (1, 2, 2, 24, 1000, 0xF, "bf16", 100),
+    (1, 1, 1, 700, 48, 0xF, "bf16", 50),
+    (1, 2, 2, 33, 17, 0xF, "f32", 4),
+    (1, 2, 2, 48, 40, 0xF, "bf16", 1),
+    (1, 3, 3, 512, 512, 0xF, "bf16", 64),
+]
+
+
+@pytest.mark.parametrize("flags", [0, gspn.FLAG_FORCE_GENERIC], ids=["auto", "generic"])
+@pytest.mark.parametrize("case", LOCAL_CASES, ids=lambda c: "B{}C{}G{}H{}W{}d{:x}{}k{}".format(*c))
+def test_local_parity(case, flags):
+    B, C, G, H, W, dirs, dt, k = case
+    if flags and H * W > 64 * 64 and max(H, W) > 512:
+        pytest.skip("generic path on P-split shapes is covered by test_gpu_parity")
+    cfg = small_config(B, C, G, H, W, dirs, dt, cfg_id=603)
+    inp = host_inputs(cfg)
+    f = {n: v[1] for n, v in inp.items()}
+    dev = _dev()
+    t = {n: to_torch(v[0], dt, dev) for n, v in inp.items()}
+    h = gspn.fwd(t["x"], t["w_l"], t["w_m"], t["w_r"], t["lam"], dirs, G, flags=flags, kchunk=k)
+    path = gspn.last_path()
+    grads = gspn.bwd(t["x"], t["w_l"], t["w_m"], t["w_r"], t["lam"], h, t["dh"], dirs, G, flags=flags, kchunk=k)
+    h_ref = oracle.fwd(f["x"], f["w_l"], f["w_m"], f["w_r"], f["lam"], dirs, G, kchunk=k)
+    g_ref = oracle.bwd(f["x"], f["w_l"], f["w_m"], f["w_r"], f["lam"], round_io(h_ref, dt), f["dh"], dirs, G,
+                       kchunk=k)
+    tol = TOL[dt]
+    hg = from_torch(h)
+    for s in range(cfg.D):
+        assert normwise(hg[s], h_ref[s]) <= tol, f"h slab {s} ({path})"
+    for name, a, r in zip(("dx", "dw_l", "dw_m", "dw_r", "dlam"), grads, g_ref):
+        a = from_torch(a)
+        if a.ndim == 5:
+            for s in range(a.shape[0]):
+                assert normwise(a[s], r[s]) <= tol, f"{name} slab {s} ({path})"
+        else:
+            assert normwise(a, r) <= tol, f"{name} ({path})"
+    if not flags and (W * (2 if dt == "bf16" else 4)) % 16 == 0:
+        assert path == "stream"
+
+
+def test_local_kchunk_one_is_lambda_x():
+    """kchunk = 1 isolates every step: h = lam x exactly up to the I/O rounding of one product."""
+    import torch
+
+    cfg = small_config(2, 4, 4, 64, 64, 0xF, "f32", cfg_id=604)
+    inp = host_inputs(cfg)
+    dev = _dev()
+    t = {n: to_torch(v[0], "f32", dev) for n, v in inp.items()}
+    h = gspn.fwd(t["x"], t["w_l"], t["w_m"], t["w_r"], t["lam"], 0xF, 4, kchunk=1)
+    torch.testing.assert_close(h, t["lam"] * t["x"].unsqueeze(0), rtol=0, atol=0)
