@@ -35,18 +35,22 @@ def lib() -> ctypes.CDLL:
         L.gspn_fwd.restype = ctypes.c_int
         L.gspn_bwd.argtypes = [vp] * 12 + [i64] * 4 + [u32, i64, ctypes.c_int, u32, vp, sz, vp]
         L.gspn_bwd.restype = ctypes.c_int
-        L.gspn_fwd_local.argtypes = [vp] * 6 + [i64] * 4 + [u32, i64, i64, ctypes.c_int, u32, vp]
-        L.gspn_fwd_local.restype = ctypes.c_int
-        L.gspn_bwd_local.argtypes = [vp] * 12 + [i64] * 4 + [u32, i64, i64, ctypes.c_int, u32, vp, sz, vp]
-        L.gspn_bwd_local.restype = ctypes.c_int
+        # SURVEY §8(f) entry points (bound when present, so an older library still serves the core calls in
+        # A/B timing runs; calling a missing one raises AttributeError)
+        if hasattr(L, "gspn_fwd_local"):
+            L.gspn_fwd_local.argtypes = [vp] * 6 + [i64] * 4 + [u32, i64, i64, ctypes.c_int, u32, vp]
+            L.gspn_fwd_local.restype = ctypes.c_int
+            L.gspn_bwd_local.argtypes = [vp] * 12 + [i64] * 4 + [u32, i64, i64, ctypes.c_int, u32, vp, sz, vp]
+            L.gspn_bwd_local.restype = ctypes.c_int
         L.gspn_bwd_workspace_bytes.argtypes = [i64] * 4 + [u32, i64, ctypes.c_int]
         L.gspn_bwd_workspace_bytes.restype = sz
         L.gspn_algorithmic_bytes.argtypes = [i64] * 4 + [u32, i64, ctypes.c_int, ctypes.c_int]
         L.gspn_algorithmic_bytes.restype = ctypes.c_double
-        L.gspn_merge_fwd.argtypes = [vp] * 3 + [i64] * 4 + [u32, ctypes.c_int, u32, vp]
-        L.gspn_merge_fwd.restype = ctypes.c_int
-        L.gspn_merge_bwd.argtypes = [vp] * 5 + [i64] * 4 + [u32, ctypes.c_int, u32, vp]
-        L.gspn_merge_bwd.restype = ctypes.c_int
+        if hasattr(L, "gspn_merge_fwd"):
+            L.gspn_merge_fwd.argtypes = [vp] * 3 + [i64] * 4 + [u32, ctypes.c_int, u32, vp]
+            L.gspn_merge_fwd.restype = ctypes.c_int
+            L.gspn_merge_bwd.argtypes = [vp] * 5 + [i64] * 4 + [u32, ctypes.c_int, u32, vp]
+            L.gspn_merge_bwd.restype = ctypes.c_int
         L.gspn_status_string.argtypes = [ctypes.c_int]
         L.gspn_status_string.restype = ctypes.c_char_p
         L.gspn_last_error_detail.restype = ctypes.c_char_p

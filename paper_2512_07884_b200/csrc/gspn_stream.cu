@@ -1145,13 +1145,26 @@ __device__ __forceinline__ void accum_taps(uint32_t dir, const T* hp, int64_t H,
 
 // GSPN-local: the taps of a segment's first step act on a reset h_{t-1}, so their gradient is 0
 // (the D terms of a7 vanish). Uniform branch, no cost for the global scan (kchunk = 0).
+// One 32-bit modulo per call: a vertical direction's segment start depends on the row only, a horizontal
+// one's on the column (bit q of reset_bits(j0, +1, ...) = column j0 + q starts a segment).
 template <int V>
 __device__ __forceinline__ void local_dw_mask(const ScanParams& p, uint32_t dir, int64_t i, int64_t j0, float (&ol)[V],
                                               float (&om)[V], float (&orr)[V]) {
   if (p.kchunk <= 0) return;
+  const int k = static_cast<int>(p.kchunk);
+  uint32_t m;
+  if (dir == GSPN_DIR_T2B || dir == GSPN_DIR_B2T) {
+    const int ii = static_cast<int>(i);
+    const bool st = dir == GSPN_DIR_T2B ? ii % k == 0 : ((ii + 1) % k == 0 || ii == static_cast<int>(p.H) - 1);
+    m = st ? 0xFFFFFFFFu : 0u;
+  } else {
+    const int jj = static_cast<int>(j0);
+    m = reset_bits(jj, 1, dir == GSPN_DIR_L2R, k, V);
+    if (dir == GSPN_DIR_R2L && static_cast<int>(p.W) - 1 - jj < V) m |= 1u << (static_cast<int>(p.W) - 1 - jj);
+  }
 #pragma unroll
   for (int q = 0; q < V; ++q)
-    if (seg_start_px(dir, i, j0 + q, p.H, p.W, p.kchunk)) ol[q] = om[q] = orr[q] = 0.f;
+    if ((m >> q) & 1u) ol[q] = om[q] = orr[q] = 0.f;
 }
 
 // dw_k for V columns of row i from the summed Da, Db, Dc.
@@ -1477,7 +1490,7 @@ __device__ __forceinline__ void sm_ld4v(const uint8_t* p, float (&v)[4]) {
   }
 }
 
-template <typename T>
+template <typename T, bool kLocal>
 __global__ void __launch_bounds__((kOutConsumers + 1) * 32, 1) bwd_out_tma_kernel(const __grid_constant__ OutArgs A) {
   constexpr int V = 4;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -1621,7 +1634,7 @@ __global__ void __launch_bounds__((kOutConsumers + 1) * 32, 1) bwd_out_tma_kerne
           for (int q = 0; q < V; ++q)
             jacobian<true>(wl[q], wm[q], wr[q], hl, hr, prenorm, Da[q], Db[q], Dc[q], ol[q], om[q], orr[q]);
         }
-        local_dw_mask<V>(p, dir, i, j0, ol, om, orr);
+        if constexpr (kLocal) local_dw_mask<V>(p, dir, i, j0, ol, om, orr);
         GVec<T, V>::store(static_cast<T*>(p.dwl) + off, ol);
         GVec<T, V>::store(static_cast<T*>(p.dwm) + off, om);
         GVec<T, V>::store(static_cast<T*>(p.dwr) + off, orr);
@@ -1638,7 +1651,7 @@ __global__ void __launch_bounds__((kOutConsumers + 1) * 32, 1) bwd_out_tma_kerne
 // group per stage (x, and per direction g, lam and the h halo tile), every thread keeps the group sums
 // Da/Db/Dc of its 4-column chunk for all directions in registers, and after the group's last channel
 // reads w from global memory once and writes dw. One chunk per consumer thread (RB W / 4 <= 512).
-template <typename T>
+template <typename T, bool kLocal>
 __global__ void __launch_bounds__((kOutConsumers + 1) * 32, 1) bwd_out_grp_tma_kernel(const __grid_constant__ OutArgs A) {
   constexpr int V = 4;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -1800,7 +1813,7 @@ __global__ void __launch_bounds__((kOutConsumers + 1) * 32, 1) bwd_out_grp_tma_k
           jacobian<true>(wl[q], wm[q], wr[q], rp >= 1, rp <= P - 2, prenorm, Da[k][q], Db[k][q], Dc[k][q], ol[q],
                          om[q], orr[q]);
         }
-        local_dw_mask<V>(p, dir, i, j0, ol, om, orr);
+        if constexpr (kLocal) local_dw_mask<V>(p, dir, i, j0, ol, om, orr);
         GVec<T, V>::store(static_cast<T*>(p.dwl) + woff, ol);
         GVec<T, V>::store(static_cast<T*>(p.dwm) + woff, om);
         GVec<T, V>::store(static_cast<T*>(p.dwr) + woff, orr);
@@ -2149,8 +2162,12 @@ bool launch_out_tma(const ScanParams& p, const void* g, gspn_dtype_t dt, cudaStr
             encode(&A.h, p.h, dt, p.W, p.H, nc, A.BX, RB + 2, false);
   if (!ok) return false;
   const uint32_t smem = 1024 + A.nstages * A.stage_bytes + 2 * 8 * A.nstages;
-  auto kern = grouped ? (dt == GSPN_BF16 ? bwd_out_grp_tma_kernel<__nv_bfloat16> : bwd_out_grp_tma_kernel<float>)
-                      : (dt == GSPN_BF16 ? bwd_out_tma_kernel<__nv_bfloat16> : bwd_out_tma_kernel<float>);
+  using BF = __nv_bfloat16;
+  auto kern = p.kchunk > 0
+      ? (grouped ? (dt == GSPN_BF16 ? bwd_out_grp_tma_kernel<BF, true> : bwd_out_grp_tma_kernel<float, true>)
+                 : (dt == GSPN_BF16 ? bwd_out_tma_kernel<BF, true> : bwd_out_tma_kernel<float, true>))
+      : (grouped ? (dt == GSPN_BF16 ? bwd_out_grp_tma_kernel<BF, false> : bwd_out_grp_tma_kernel<float, false>)
+                 : (dt == GSPN_BF16 ? bwd_out_tma_kernel<BF, false> : bwd_out_tma_kernel<float, false>));
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e == cudaSuccess) {
     int per_sm = 0;
