@@ -246,11 +246,12 @@ gspn_status_t gspn_bwd_local(const void* x, const void* w_l, const void* w_m, co
     int launches = 0;
     bool handled = false;
     cudaError_t e = cudaSuccess;
+    const char* stream_path = "stream";
     if (!(flags & GSPN_FLAG_FORCE_GENERIC)) {
       // the streaming path carves the workspace itself
       p.ws = workspace;
       p.ws_bytes = workspace_bytes;
-      e = gspn::launch_bwd_stream(p, dtype, cs, &launches, &handled);
+      e = gspn::launch_bwd_stream(p, dtype, cs, &launches, &handled, &stream_path);
     }
     if (e == cudaSuccess && !handled) {
       char* ws = static_cast<char*>(workspace);
@@ -270,7 +271,7 @@ gspn_status_t gspn_bwd_local(const void* x, const void* w_l, const void* w_m, co
       snprintf(t_detail, sizeof t_detail, "CUDA error: %s", cudaGetErrorString(e));
       return GSPN_ERR_CUDA;
     }
-    t_path = handled ? "stream" : "generic";
+    t_path = handled ? stream_path : "generic";
     t_launches = launches;
     return GSPN_OK;
   } catch (const std::exception& ex) {

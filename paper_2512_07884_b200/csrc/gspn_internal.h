@@ -13,7 +13,9 @@ cudaError_t launch_bwd_generic(const ScanParams& p, gspn_dtype_t dt, cudaStream_
 
 // Fast TMA-streaming path (gspn_stream.cu). *handled = false when the shape is not eligible.
 cudaError_t launch_fwd_stream(const ScanParams& p, gspn_dtype_t dt, cudaStream_t s, int* launches, bool* handled);
-cudaError_t launch_bwd_stream(const ScanParams& p, gspn_dtype_t dt, cudaStream_t s, int* launches, bool* handled);
+// Backward: *path = "stream-fused" (recurrence + tap gradients in one pass, G = C) or "stream" (split).
+cudaError_t launch_bwd_stream(const ScanParams& p, gspn_dtype_t dt, cudaStream_t s, int* launches, bool* handled,
+                              const char** path);
 size_t stream_bwd_workspace_bytes(int64_t B, int64_t C, int64_t H, int64_t W, int64_t D, int64_t G, gspn_dtype_t dt);
 
 // Output gate + direction merge (gspn_merge.cu). N = B*C*H*W elements per direction slab.

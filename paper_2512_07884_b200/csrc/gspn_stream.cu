@@ -54,7 +54,7 @@ namespace {
 using namespace ptx;
 
 constexpr int kMaxIn = 6;
-constexpr int kMaxOut = 2;
+constexpr int kMaxOut = 4;
 constexpr int kEdgeW = 16;     // edge-buffer slots (>= consumer warps + 1)
 // Fixed tile geometry (chains with P <= kPpad): one tensor's tile holds K steps x kPpad positions =
 // 32 kPpad bytes; vertical tiles are [box][K][kRowB bytes] (box = kRowB / s positions), horizontal
@@ -103,6 +103,7 @@ struct Plan {
   // x loads, vertical loads, horizontal loads, vertical stores, horizontal stores, fp32 accumulators
   int pol[6];
   int null_compute;    // experiments only (GSPN_NULL=1): consumers skip the arithmetic
+  int fuse_h;          // fused backward: horizontal chains also form dw in the recurrence (else g only)
 };
 
 struct alignas(64) StreamArgs {
@@ -226,6 +227,10 @@ __device__ __forceinline__ int tile_start(const Chain& ch, int j, int K) {
 // Input tensor slots.
 enum FwdIn { F_X = 0, F_LAM, F_WL, F_WM, F_WR, F_NIN };
 enum BwdIn { B_DH = 0, B_WL, B_WM, B_WR, B_NIN };
+// Fused backward (G = C): + h_{t-1} tiles. Vertical: B_H0 = the h rows one step earlier (box shifted by
+// one row). Horizontal: B_H0 = h on the tile's own (K-aligned) columns, B_H1 = the neighbouring aligned
+// tile on the side of step t-1 (its edge column is h_{t-1} of the tile's first step).
+enum BwdFusedIn { B_H0 = B_NIN, B_H1, B_NINF };
 
 template <bool kBwd>
 __device__ __forceinline__ int64_t plane_of(const Chain& ch, int slot) {
@@ -1061,6 +1066,316 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_stream_kernel(const
   cluster_exit<kCl>();
 }
 
+
+// ------------------------------------------------------------------------------ fused backward (G = C)
+//
+// The adjoint recurrence above plus the tap gradients of a7 in the same pass: with g_t, the step's raw
+// taps (l, m, r) and 1/S already in registers, and h_{t-1}[r-1..r+1] streamed in as one more tile,
+//   u = g / S^2;  d1 = h[r-1] - h[r], d2 = h[r-1] - h[r+1], d3 = h[r] - h[r+1]   (h = h_{t-1})
+//   dw_l = u (m d1 + r d2),  dw_m = u (r d3 - l d1),  dw_r = -u (l d2 + m d3)
+// which is the Jacobian of SURVEY.md §8(a) a7 ((m + r) Da - m Db - r Dc) / S^2 etc. with Da = g h[r-1],
+// Db = g h[r], Dc = g h[r+1], regrouped (pre-normalised taps: dw = (Da, Db, Dc)). Out-of-range taps get
+// dw = 0. This removes the second read of w and the g round trip's w half that the split backward
+// pays; dlam and dx (which sum over directions) follow in one elementwise pass (bwd_dx_kernel).
+
+// Per-lane tap-range flags from the unpack selectors (an out-of-range tap unpacks to 0).
+template <typename T>
+__device__ __forceinline__ bool tap_on(const uint32_t (&m)[2]) {
+  if constexpr (sizeof(T) == 2) return m[0] != kSelZero;
+  else return m[0] != 0u;
+}
+
+template <int kPre>
+__device__ __forceinline__ void dw_math(float g, float l, float m, float r, float hm1, float h0, float hp1, float& ol,
+                                        float& om, float& orr) {
+  if constexpr (kPre == kNormPre) {
+    ol = g * hm1; om = g * h0; orr = g * hp1;
+  } else {
+    const float inv = norm_inv<kPre>((l + r) + m);
+    const float u = g * inv * inv;
+    const float d1 = hm1 - h0, d2 = hm1 - hp1, d3 = h0 - hp1;
+    ol = u * fmaf(m, d1, r * d2);
+    om = u * fmaf(r, d3, -l * d1);
+    orr = -u * fmaf(l, d2, m * d3);
+  }
+}
+
+template <typename T, int kPre>
+__device__ __forceinline__ void bwd_half_vert_fused(const Lanes<T>& ln, const uint8_t* p0, int stepb, int64_t gofs,
+                                                    int64_t gstep, int t0, int L, BwdState& S, uint64_t pol, T* gbase,
+                                                    T* dwl, T* dwm, T* dwr, bool hl0, bool hr1) {
+  constexpr int KS = Cfg<T>::KS;
+#pragma unroll
+  for (int i = 0; i < KS; ++i) {
+    const uint8_t* q = p0 + i * stepb;
+    float dh[2], l[2], m[2], r[2], hp[2];
+    vload<T>(q + B_DH * kTile, dh);
+    vload_tap<T>(q + B_WL * kTile, ln.s[0], l);
+    vload_tap<T>(q + B_WM * kTile, ln.s[1], m);
+    vload_tap<T>(q + B_WR * kTile, ln.s[2], r);
+    vload<T>(q + B_H0 * kTile, hp);  // h_{t-1} at the lane's two positions
+    const float nr1 = __shfl_down_sync(0xffffffffu, S.ea[0], 1);
+    const float nl0 = __shfl_up_sync(0xffffffffu, S.ec[1], 1);
+    const float hleft = __shfl_up_sync(0xffffffffu, hp[1], 1);    // h_{t-1}[r0 - 1] (lane 0: a ghost)
+    const float hright = __shfl_down_sync(0xffffffffu, hp[0], 1);  // h_{t-1}[r0 + 2] (lane 31: a ghost)
+    const float ea0 = S.ea[1], ec1 = S.ec[0];
+    float g[2], ol[2], om[2], orr[2];
+    g[0] = bwd_math<kPre>(dh[0], l[0], m[0], r[0], ea0, nl0, S.ea[0], S.eb[0], S.ec[0]);
+    g[1] = bwd_math<kPre>(dh[1], l[1], m[1], r[1], nr1, ec1, S.ea[1], S.eb[1], S.ec[1]);
+    dw_math<kPre>(g[0], l[0], m[0], r[0], hleft, hp[0], hp[1], ol[0], om[0], orr[0]);
+    dw_math<kPre>(g[1], l[1], m[1], r[1], hp[0], hp[1], hright, ol[1], om[1], orr[1]);
+    ol[0] = hl0 ? ol[0] : 0.f;    // position r0 may be the chain's first (no left tap)
+    orr[1] = hr1 ? orr[1] : 0.f;  // position r0 + 1 may be its last (no right tap)
+    const bool st = ln.own_v && t0 + KS - 1 - i < L;
+    GStore<T, 2>::st_if(st, gbase + gofs, g, pol);
+    GStore<T, 2>::st_if(st, dwl + gofs, ol, pol);
+    GStore<T, 2>::st_if(st, dwm + gofs, om, pol);
+    GStore<T, 2>::st_if(st, dwr + gofs, orr, pol);
+    gofs += gstep;
+  }
+}
+
+// Horizontal tap gradients of one half, after the edge barrier (every warp has read this half's input
+// chunks, so each lane may overwrite its OWNED rows in place): g of the half (OG, already rounded to the
+// I/O dtype like the split path's workspace g), the raw taps re-read from shared memory, and h_{t-1} =
+// the chunk shifted by one column towards step t-1 -- elements of the same chunk plus one edge element of
+// the spill chunk (the other chunk of this tile, or the neighbouring tile B_H1) -- for rows r-1, r, r+1.
+template <typename T, int kPre, bool kRev>
+__device__ __forceinline__ void dw_half_horiz(const Lanes<T>& ln, uint8_t* st, int cm, const uint4 (&OG)[kE],
+                                              const uint32_t (&hrow)[kE][3], const bool (&hl)[kE],
+                                              const bool (&hr)[kE]) {
+  constexpr int KS = Cfg<T>::KS;
+  // L2R (h_{t-1} = column c-1): cm 1 -> this tile's chunk 0; cm 0 -> tile B_H1 chunk 1.
+  // R2L (column c+1):           cm 0 -> this tile's chunk 1; cm 1 -> tile B_H1 chunk 0.
+  const bool own_tile = kRev ? cm == 0 : cm == 1;
+  const uint32_t sp_slot = own_tile ? B_H0 * kTile : B_H1 * kTile;
+  const uint32_t sp_chunk = static_cast<uint32_t>(cm ^ 1) << 4;
+  const uint32_t cmx = static_cast<uint32_t>(cm) << 4;
+#pragma unroll
+  for (int q = 0; q < kE; ++q) {
+    if (!ln.own_h[q]) continue;
+    const uint32_t off = ln.hoff[q] ^ cmx;
+    const uint4 WL = *reinterpret_cast<const uint4*>(st + B_WL * kTile + off);
+    const uint4 WM = *reinterpret_cast<const uint4*>(st + B_WM * kTile + off);
+    const uint4 WR = *reinterpret_cast<const uint4*>(st + B_WR * kTile + off);
+    uint4 Hc[3], Hs[3];  // rows r-1, r, r+1: this chunk of B_H0, and the spill chunk
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      Hc[a] = *reinterpret_cast<const uint4*>(st + B_H0 * kTile + (hrow[q][a] ^ cmx));
+      Hs[a] = *reinterpret_cast<const uint4*>(st + sp_slot + (hrow[q][a] ^ sp_chunk));
+    }
+    float ol[KS], om[KS], orr[KS];
+#pragma unroll
+    for (int i = 0; i < KS; ++i) {
+      float hv[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        if constexpr (!kRev) hv[a] = i > 0 ? hget<T>(Hc[a], i - 1) : hget<T>(Hs[a], KS - 1);
+        else hv[a] = i < KS - 1 ? hget<T>(Hc[a], i + 1) : hget<T>(Hs[a], 0);
+      }
+      dw_math<kPre>(hget<T>(OG[q], i), hget_tap<T>(WL, i, ln.s[0][q]), hget_tap<T>(WM, i, ln.s[1][q]),
+                    hget_tap<T>(WR, i, ln.s[2][q]), hv[0], hv[1], hv[2], ol[i], om[i], orr[i]);
+      ol[i] = hl[q] ? ol[i] : 0.f;
+      orr[i] = hr[q] ? orr[i] : 0.f;
+    }
+    *reinterpret_cast<uint4*>(st + B_DH * kTile + off) = OG[q];
+    *reinterpret_cast<uint4*>(st + B_WL * kTile + off) = Pk<T>::pack(ol);
+    *reinterpret_cast<uint4*>(st + B_WM * kTile + off) = Pk<T>::pack(om);
+    *reinterpret_cast<uint4*>(st + B_WR * kTile + off) = Pk<T>::pack(orr);
+  }
+}
+
+template <typename T, int kPre>
+__device__ void producer_fused(const StreamArgs& A, uint8_t* ring, uint64_t* full, uint64_t* empty) {
+  const Plan& pl = A.plan;
+  const uint64_t pol_vin = policy_of(pl.pol[1]);
+  const uint64_t pol_hin = policy_of(pl.pol[2]);
+  int stage = 0;
+  uint32_t phase = 0;
+  for (int64_t w = blockIdx.x; w < pl.nchains; w += gridDim.x) {
+    const Chain ch = make_chain<false>(A.p, pl, w);
+    const int o = ch.vert ? 0 : 1;
+    const int chain = static_cast<int>(ch.chain);
+    for (int jj = 0; jj < ch.ntiles; ++jj) {
+      const int j = ch.ntiles - 1 - jj;
+      mbar_wait_sleep(smem_u32(&empty[stage]), phase ^ 1);
+      const uint32_t fb = smem_u32(&full[stage]);
+      mbar_arrive_tx(fb, ch.vert ? pl.tx_v : pl.tx_h);
+      const int s0 = tile_start(ch, j, pl.K);
+      const uint32_t st = smem_u32(ring + static_cast<size_t>(stage) * pl.stage_bytes);
+      const uint64_t pol = ch.vert ? pol_vin : pol_hin;
+      for (int t = 0; t < B_NIN; ++t) {
+        const uint32_t dst = st + t * pl.tile_bytes;
+        if (ch.vert) {
+          for (int q = 0; q < pl.nbw; ++q)
+            tma_load3(dst + q * pl.K * pl.bw * pl.es, &A.in[0][t], q * pl.bw, s0, chain, fb, pol);
+        } else {
+          for (int q = 0; q < pl.nbh; ++q)
+            tma_load3(dst + q * pl.bh * 32, &A.in[1][t], s0, q * pl.bh, chain, fb, pol);
+        }
+      }
+      if (ch.vert) {  // h rows one step earlier: T2B row - 1, B2T row + 1 (out of range: zero = h_{-1})
+        const int sh = ch.rev ? s0 + 1 : s0 - 1;
+        const uint32_t dst = st + B_H0 * pl.tile_bytes;
+        for (int q = 0; q < pl.nbw; ++q)
+          tma_load3(dst + q * pl.K * pl.bw * pl.es, &A.in[0][B_H0], q * pl.bw, sh, chain, fb, pol);
+      } else if (pl.fuse_h) {  // this tile's columns and the neighbouring tile towards step t-1 (zero fill)
+        const int sn = ch.rev ? s0 + pl.K : s0 - pl.K;
+        for (int q = 0; q < pl.nbh; ++q) {
+          tma_load3(st + B_H0 * pl.tile_bytes + q * pl.bh * 32, &A.in[1][B_H0], s0, q * pl.bh, chain, fb, pol);
+          tma_load3(st + B_H1 * pl.tile_bytes + q * pl.bh * 32, &A.in[1][B_H0], sn, q * pl.bh, chain, fb, pol);
+        }
+      }
+      if (++stage == pl.nstages) { stage = 0; phase ^= 1; }
+    }
+  }
+}
+
+template <typename T, int kPre>
+__global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_fused_kernel(const __grid_constant__ StreamArgs A) {
+  using C = Cfg<T>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const Plan& pl = A.plan;
+  const Smem m = carve(smem_raw, pl);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  init_barriers<false>(m, pl);
+  if (warp == pl.nwc) {
+    if (lane == 0) {
+      for (int o = 0; o < 2; ++o)
+        for (int t = 0; t < B_H1; ++t) asm volatile("prefetch.tensormap [%0];" ::"l"(&A.in[o][t]) : "memory");
+      producer_fused<T, kPre>(A, m.ring, m.full, m.empty);
+    }
+    return;
+  }
+  if (warp == pl.nwc + 1) {  // storer: horizontal tiles' g and dw_l/m/r (written over dh, w_l, w_m, w_r)
+    if (lane == 0) {
+      const int slots[4] = {B_DH, B_WL, B_WM, B_WR};
+      storer_loop<false>(A, m.ring, m.done, m.empty, pl.fuse_h ? 4 : 1, slots, true);
+    }
+    return;
+  }
+  const uint64_t pol_vout = policy_of(pl.pol[3]);
+  const int nthreads = pl.nwc * 32;
+  const int64_t W = A.p.W;
+  const XSrc xs = make_xsrc<T>(warp, pl.nwc, lane);
+  T* const gbase = static_cast<T*>(A.g);
+  T* const dwl = static_cast<T*>(A.p.dwl);
+  T* const dwm = static_cast<T*>(A.p.dwm);
+  T* const dwr = static_cast<T*>(A.p.dwr);
+  int stage = 0, par = 0;
+  uint32_t phase = 0;
+  for (int64_t w = blockIdx.x; w < pl.nchains; w += gridDim.x) {
+    const Chain ch = make_chain<false>(A.p, pl, w);
+    const Lanes<T> ln = make_lanes<T, false>(pl, A.p, ch, warp, lane);
+    // tap-range flags and the swizzled offsets of rows r-1, r, r+1 (horizontal slots)
+    const bool hl0 = tap_on<T>(ln.s[0][0]), hr1 = tap_on<T>(ln.s[2][1]);
+    bool hl[kE], hr[kE];
+    uint32_t hrow[kE][3];
+#pragma unroll
+    for (int q = 0; q < kE; ++q) {
+      hl[q] = tap_on<T>(ln.s[0][q]);
+      hr[q] = tap_on<T>(ln.s[2][q]);
+      const int rt = ln.A + 32 * q + lane;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        int rr = rt - 1 + a;
+        rr = rr < 0 ? 0 : (rr >= kPpad ? kPpad - 1 : rr);
+        const uint32_t rc = static_cast<uint32_t>(rr);
+        hrow[q][a] = rc * 32 + (((rc >> 2) & 1u) << 4);
+      }
+    }
+    BwdState S;
+#pragma unroll
+    for (int e = 0; e < kE; ++e) S.ea[e] = S.eb[e] = S.ec[e] = 0.f;
+    for (int jj = 0; jj < ch.ntiles; ++jj) {
+      const int j = ch.ntiles - 1 - jj;
+      mbar_wait_sleep(smem_u32(&m.full[stage]), phase);
+      __syncwarp();
+      uint8_t* st = m.ring + static_cast<size_t>(stage) * pl.stage_bytes;
+#pragma unroll 1
+      for (int half = 1; half >= 0; --half) {
+        uint4 OG[kE];
+        const int cm = ch.rev ? 1 - half : half;
+        if (!pl.null_compute) {
+          if (ch.vert) {
+            const int t0 = j * C::K + half * C::KS;
+            const int tl = t0 + C::KS - 1;
+            const int kkl = ch.rev ? C::K - 1 - (half * C::KS + C::KS - 1) : half * C::KS + C::KS - 1;
+            const int rowl = ch.rev ? ch.L - 1 - tl : tl;
+            const int vs = static_cast<int>(pl.vstep);
+            bwd_half_vert_fused<T, kPre>(ln, st + ln.voff + kkl * vs, ch.rev ? vs : -vs,
+                                         ln.vout + static_cast<int64_t>(rowl) * W, ch.rev ? W : -W, t0, ch.L, S,
+                                         pol_vout, gbase, dwl, dwm, dwr, hl0, hr1);
+          } else if (ch.rev) {
+            bwd_half_horiz<T, kPre, true, false>(ln, st, cm, lane, S, OG, 0u);
+          } else {
+            bwd_half_horiz<T, kPre, false, false>(ln, st, cm, lane, S, OG, 0u);
+          }
+        }
+        edge_publish(m.edge + 0 * kXArr + par * kEdgeW * kXRow, warp, lane, ch.vert, S.ea);
+        edge_publish(m.edge + 1 * kXArr + par * kEdgeW * kXRow, warp, lane, ch.vert, S.eb);
+        edge_publish(m.edge + 2 * kXArr + par * kEdgeW * kXRow, warp, lane, ch.vert, S.ec);
+        named_bar(kBarEdge, nthreads);  // edges published; every warp has read this half's input rows
+        edge_reload(m.edge + 0 * kXArr + par * kEdgeW * kXRow, xs, ch.vert, S.ea);
+        edge_reload(m.edge + 1 * kXArr + par * kEdgeW * kXRow, xs, ch.vert, S.eb);
+        edge_reload(m.edge + 2 * kXArr + par * kEdgeW * kXRow, xs, ch.vert, S.ec);
+        par ^= 1;
+        if (!ch.vert && !pl.null_compute) {
+          if (pl.fuse_h) {  // tap gradients; g and dw in place over this half's dh / w chunks
+            if (ch.rev) dw_half_horiz<T, kPre, true>(ln, st, cm, OG, hrow, hl, hr);
+            else dw_half_horiz<T, kPre, false>(ln, st, cm, OG, hrow, hl, hr);
+          } else {  // g only (the output kernel forms these chains' dw): in place over the dh chunk
+#pragma unroll
+            for (int q = 0; q < kE; ++q)
+              if (ln.own_h[q])
+                *reinterpret_cast<uint4*>(st + B_DH * kTile + (ln.hoff[q] ^ (static_cast<uint32_t>(cm) << 4))) = OG[q];
+          }
+        }
+      }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&m.done[stage]));
+      if (++stage == pl.nstages) { stage = 0; phase ^= 1; }
+    }
+  }
+}
+
+// dlam_k = g_k x and dx = sum_k g_k lam_k (a7), elementwise over [B, C, H, W] with all D directions per
+// thread; 16-byte vectors, streaming loads / stores (HBM-bound: s (1 + 4D) reads + s (D + 1) writes).
+template <typename T, int D>
+__global__ void __launch_bounds__(256) bwd_dx_kernel(const T* __restrict__ x, const T* __restrict__ lam,
+                                                     const T* __restrict__ g, T* __restrict__ dlam,
+                                                     T* __restrict__ dx, int64_t N, int64_t nv) {
+  constexpr int V = 16 / sizeof(T);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x) {
+    uint4 gq[D], lq[D];
+    const uint4 xq = ld_nc_v4(x + i * V);
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      gq[k] = ld_nc_v4(g + k * N + i * V);
+      lq[k] = ld_nc_v4(lam + k * N + i * V);
+    }
+    float xv[V], acc[V];
+#pragma unroll
+    for (int e = 0; e < V; ++e) {
+      xv[e] = hget<T>(xq, e);
+      acc[e] = 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      float dl[V];
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        const float gv = hget<T>(gq[k], e);
+        dl[e] = gv * xv[e];
+        acc[e] = fmaf(gv, hget<T>(lq[k], e), acc[e]);
+      }
+      st_cs_v4(dlam + k * N + i * V, Pk<T>::pack(dl));
+    }
+    st_cs_v4(dx + i * V, Pk<T>::pack(acc));
+  }
+}
+
 // ------------------------------------------------------------------------------ backward outputs
 
 // Backward outputs from the adjoint state g and the saved h, one thread per
@@ -1472,6 +1787,7 @@ struct OutArgs {
   int RB, BX, nbx, nstages, nrb;
   uint32_t box_rb, box_h;                            // bytes per TMA box (padded to 128)
   uint32_t tile_rb, tile_h, per_k, stage_bytes, tx;  // bytes
+  uint32_t koff[4];                                  // byte offset of direction k's tiles in a stage
   int64_t nunits;
 };
 
@@ -1490,7 +1806,9 @@ __device__ __forceinline__ void sm_ld4v(const uint8_t* p, float (&v)[4]) {
   }
 }
 
-template <typename T, bool kLocal>
+// kVertDone: the fused recurrence already wrote dw of the vertical directions (hybrid backward): their
+// w and h tiles are neither loaded nor used, only dlam and dx are formed for them.
+template <typename T, bool kLocal, bool kVertDone>
 __global__ void __launch_bounds__((kOutConsumers + 1) * 32, 1) bwd_out_tma_kernel(const __grid_constant__ OutArgs A) {
   constexpr int V = 4;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -1525,10 +1843,12 @@ __global__ void __launch_bounds__((kOutConsumers + 1) * 32, 1) bwd_out_tma_kerne
         for (int bx = 0; bx < A.nbx; ++bx) tma_load3(st + bx * box_rb, &A.x, bx * BX, i0, static_cast<int>(bc), fb, pol);
         for (int k = 0; k < D; ++k) {
           const int chain = static_cast<int>((static_cast<int64_t>(k) * p.B + b) * p.C + c);
-          const uint32_t base = st + A.tile_rb + k * A.per_k;
+          const uint32_t base = st + A.koff[k];
+          const bool skip_w = kVertDone && (p.dirbit[k] == GSPN_DIR_T2B || p.dirbit[k] == GSPN_DIR_B2T);
           for (int bx = 0; bx < A.nbx; ++bx) {
             tma_load3(base + 0 * A.tile_rb + bx * box_rb, &A.g, bx * BX, i0, chain, fb, pol);
             tma_load3(base + 1 * A.tile_rb + bx * box_rb, &A.lam, bx * BX, i0, chain, fb, pol);
+            if (skip_w) continue;
             tma_load3(base + 2 * A.tile_rb + bx * box_rb, &A.wl, bx * BX, i0, chain, fb, pol);
             tma_load3(base + 3 * A.tile_rb + bx * box_rb, &A.wm, bx * BX, i0, chain, fb, pol);
             tma_load3(base + 4 * A.tile_rb + bx * box_rb, &A.wr, bx * BX, i0, chain, fb, pol);
@@ -1573,7 +1893,7 @@ __global__ void __launch_bounds__((kOutConsumers + 1) * 32, 1) bwd_out_tma_kerne
 #pragma unroll
       for (int q = 0; q < V; ++q) dx[q] = 0.f;
       for (int k = 0; k < D; ++k) {
-        const uint8_t* base = st + A.tile_rb + k * A.per_k;
+        const uint8_t* base = st + A.koff[k];
         const uint8_t* ht = base + 5 * A.tile_rb;
         const uint32_t dir = p.dirbit[k];
         const bool vert = dir == GSPN_DIR_T2B || dir == GSPN_DIR_B2T;
@@ -1587,6 +1907,7 @@ __global__ void __launch_bounds__((kOutConsumers + 1) * 32, 1) bwd_out_tma_kerne
           dx[q] = fmaf(gv[q], lv[q], dx[q]);
         }
         GVec<T, V>::store(static_cast<T*>(p.dlam) + off, dl);
+        if (kVertDone && vert) continue;
         if (vert) {
           // h_{t-1}: image row i-1 (T2B) / i+1 (B2T) = halo row r / r+2; neighbours = columns j+-1
           const uint32_t ro = dir == GSPN_DIR_T2B ? 0u : 2u * rowb;
@@ -2114,7 +2435,8 @@ cudaError_t launch_fwd_stream(const ScanParams& p, gspn_dtype_t dt, cudaStream_t
 }
 
 // TMA-staged output kernel (G = C). Returns false if the shape does not fit (caller falls back).
-bool launch_out_tma(const ScanParams& p, const void* g, gspn_dtype_t dt, cudaStream_t s, cudaError_t* err) {
+bool launch_out_tma(const ScanParams& p, const void* g, gspn_dtype_t dt, cudaStream_t s, cudaError_t* err,
+                    bool vert_done = false, bool dry_run = false) {
   const bool grouped = p.G != p.C;
   static OutArgs A;
   static std::mutex mu;
@@ -2148,7 +2470,21 @@ bool launch_out_tma(const ScanParams& p, const void* g, gspn_dtype_t dt, cudaStr
   A.tile_h = A.nbx * A.box_h;
   A.per_k = nrb_t * A.tile_rb + A.tile_h;
   A.stage_bytes = A.tile_rb + D * A.per_k;
+  {  // direction k's tiles; a vertical direction of the hybrid backward holds only g and lam
+    uint32_t o = A.tile_rb;
+    for (int k = 0; k < D; ++k) {
+      A.koff[k] = o;
+      const bool vd = vert_done && (p.dirbit[k] == GSPN_DIR_T2B || p.dirbit[k] == GSPN_DIR_B2T);
+      o += vd ? 2 * A.tile_rb : A.per_k;
+    }
+    A.stage_bytes = o;
+  }
   A.tx = static_cast<uint32_t>(A.nbx * (es * A.BX * RB * (1 + nrb_t * D) + es * A.BX * (RB + 2) * D));  // payload
+  if (vert_done) {  // vertical directions load g and lam only
+    int nv = 0;
+    for (int k = 0; k < D; ++k) nv += (p.dirbit[k] == GSPN_DIR_T2B || p.dirbit[k] == GSPN_DIR_B2T) ? 1 : 0;
+    A.tx -= static_cast<uint32_t>(A.nbx * nv * (es * A.BX * RB * (nrb_t - 2) + es * A.BX * (RB + 2)));
+  }
   A.nstages = static_cast<int>(std::min<int64_t>(6, budget / A.stage_bytes));
   A.nrb = static_cast<int>((p.H + RB - 1) / RB);
   A.nunits = (grouped ? p.B * p.G : p.B * p.C) * A.nrb;
@@ -2161,13 +2497,17 @@ bool launch_out_tma(const ScanParams& p, const void* g, gspn_dtype_t dt, cudaStr
             encode(&A.wr, p.wr, dt, p.W, p.H, nc, A.BX, RB, false) &&
             encode(&A.h, p.h, dt, p.W, p.H, nc, A.BX, RB + 2, false);
   if (!ok) return false;
+  if (dry_run) return true;
   const uint32_t smem = 1024 + A.nstages * A.stage_bytes + 2 * 8 * A.nstages;
   using BF = __nv_bfloat16;
   auto kern = p.kchunk > 0
       ? (grouped ? (dt == GSPN_BF16 ? bwd_out_grp_tma_kernel<BF, true> : bwd_out_grp_tma_kernel<float, true>)
-                 : (dt == GSPN_BF16 ? bwd_out_tma_kernel<BF, true> : bwd_out_tma_kernel<float, true>))
+                 : (dt == GSPN_BF16 ? bwd_out_tma_kernel<BF, true, false> : bwd_out_tma_kernel<float, true, false>))
       : (grouped ? (dt == GSPN_BF16 ? bwd_out_grp_tma_kernel<BF, false> : bwd_out_grp_tma_kernel<float, false>)
-                 : (dt == GSPN_BF16 ? bwd_out_tma_kernel<BF, false> : bwd_out_tma_kernel<float, false>));
+                 : vert_done ? (dt == GSPN_BF16 ? bwd_out_tma_kernel<BF, false, true>
+                                                : bwd_out_tma_kernel<float, false, true>)
+                             : (dt == GSPN_BF16 ? bwd_out_tma_kernel<BF, false, false>
+                                                : bwd_out_tma_kernel<float, false, false>));
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e == cudaSuccess) {
     int per_sm = 0;
@@ -2183,8 +2523,96 @@ bool launch_out_tma(const ScanParams& p, const void* g, gspn_dtype_t dt, cudaStr
   return true;
 }
 
-cudaError_t launch_bwd_stream(const ScanParams& p0, gspn_dtype_t dt, cudaStream_t s, int* launches, bool* handled) {
+// dlam and dx of the fused backward (one elementwise launch over [B, C, H, W]).
+template <typename T>
+cudaError_t launch_dx(const ScanParams& p, const void* g, cudaStream_t s) {
+  constexpr int V = 16 / sizeof(T);
+  const int64_t N = p.B * p.C * p.H * p.W;
+  const int64_t nv = N / V;
+  int64_t blocks = (nv + 255) / 256;
+  if (blocks > static_cast<int64_t>(sm_count()) * 8) blocks = static_cast<int64_t>(sm_count()) * 8;
+  const T *x = static_cast<const T*>(p.x), *lam = static_cast<const T*>(p.lam), *gt = static_cast<const T*>(g);
+  T *dl = static_cast<T*>(p.dlam), *dx = static_cast<T*>(p.dx);
+  const unsigned b = static_cast<unsigned>(blocks < 1 ? 1 : blocks);
+  switch (p.D) {
+    case 1: bwd_dx_kernel<T, 1><<<b, 256, 0, s>>>(x, lam, gt, dl, dx, N, nv); break;
+    case 2: bwd_dx_kernel<T, 2><<<b, 256, 0, s>>>(x, lam, gt, dl, dx, N, nv); break;
+    case 3: bwd_dx_kernel<T, 3><<<b, 256, 0, s>>>(x, lam, gt, dl, dx, N, nv); break;
+    default: bwd_dx_kernel<T, 4><<<b, 256, 0, s>>>(x, lam, gt, dl, dx, N, nv); break;
+  }
+  return cudaGetLastError();
+}
+
+// Fused backward for per-channel weights on unpacked, unsplit chains (the bench's config 4 shape):
+// one persistent launch for the recurrence + tap gradients, one elementwise launch for dlam / dx.
+// Returns false (nothing launched) when the shape takes the split path.
+bool launch_bwd_fused(const ScanParams& p0, gspn_dtype_t dt, cudaStream_t s, int* launches, cudaError_t* err) {
+  static StreamArgs A;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  if (p0.G != p0.C || p0.kchunk > 0 || getenv("GSPN_NOFUSE")) return false;
+  const int es = dt == GSPN_BF16 ? 2 : 4;
+  if ((p0.B * p0.C * p0.H * p0.W * es) % 16 != 0) return false;  // dx kernel: 16-byte vectors per slab
+  memset(&A, 0, sizeof A);
+  A.p = p0;
+  ScanParams& p = A.p;
+  // Horizontal chains' dw in the recurrence measured slower than the split (6.45 vs 3.98 ms bwd on
+  // config 4's horizontal directions; profiles/r1_notes.md): by default only vertical chains are fused
+  // and the output kernel forms the horizontal chains' dw (GSPN_FUSE_H=1: fuse both, experiments).
+  const bool fuse_h = getenv("GSPN_FUSE_H") != nullptr;
+  if (!make_plan(p, dt, fuse_h ? B_NINF : B_NIN + 1, &A.plan)) return false;
+  Plan& pl = A.plan;
+  if (pl.npack > 1 || pl.cl > 1) return false;
+  pl.fuse_h = fuse_h ? 1 : 0;
+  pl.tx_v = static_cast<uint32_t>((B_NIN + 1) * pl.nbw * pl.bw * pl.K * es);  // vertical: no B_H1 tile
+  if (!fuse_h) pl.tx_h = static_cast<uint32_t>(B_NIN * pl.nbh * pl.bh * 32);  // horizontal: dh and w only
+  const WsLayout l = ws_layout(p.B, p.C, p.H, p.W, p.D, dt);
+  if (p.ws == nullptr || p.ws_bytes < l.total) return false;
+  A.g = static_cast<char*>(p.ws) + l.g;
+  const void* ins[B_NINF] = {p.dh, p.wl, p.wm, p.wr, p.h, p.h};
+  const int64_t nc = p.D * p.B * p.C;
+  const int64_t in_planes[B_NINF] = {nc, nc, nc, nc, nc, nc};
+  void* outs[4] = {A.g, p.dwl, p.dwm, p.dwr};
+  if (!fill_maps(&A, ins, pl.nin, outs, in_planes, nc, pl.fuse_h ? 4 : 1, dt)) return false;
+  cudaError_t e0 = cudaSuccess;
+  if (!pl.fuse_h && !launch_out_tma(p, A.g, dt, s, &e0, true, true)) return false;  // output kernel must fit
+  const int mode = norm_mode(p, pl);
+  cudaError_t e;
+  if (dt == GSPN_BF16) {
+    using BF = __nv_bfloat16;
+    e = mode == kNormPre ? launch(bwd_fused_kernel<BF, kNormPre>, A, s)
+        : mode == kNormClamp ? launch(bwd_fused_kernel<BF, kNormClamp>, A, s)
+                             : launch(bwd_fused_kernel<BF, kNormFull>, A, s);
+  } else {
+    e = mode == kNormPre ? launch(bwd_fused_kernel<float, kNormPre>, A, s)
+        : mode == kNormClamp ? launch(bwd_fused_kernel<float, kNormClamp>, A, s)
+                             : launch(bwd_fused_kernel<float, kNormFull>, A, s);
+  }
+  *launches += 1;
+  if (e == cudaSuccess) {
+    if (pl.fuse_h) {
+      e = dt == GSPN_BF16 ? launch_dx<__nv_bfloat16>(p, A.g, s) : launch_dx<float>(p, A.g, s);
+    } else if (!launch_out_tma(p, A.g, dt, s, &e, true)) {
+      e = cudaErrorNotSupported;  // cannot happen for shapes make_plan accepted (checked below)
+    }
+    *launches += 1;
+  }
+  *err = e;
+  return true;
+}
+
+cudaError_t launch_bwd_stream(const ScanParams& p0, gspn_dtype_t dt, cudaStream_t s, int* launches, bool* handled,
+                              const char** path) {
   *handled = false;
+  {
+    cudaError_t e = cudaSuccess;
+    if (launch_bwd_fused(p0, dt, s, launches, &e)) {
+      *handled = true;
+      *path = "stream-fused";
+      return e;
+    }
+  }
+  *path = "stream";
   static StreamArgs A;
   static std::mutex mu;
   std::lock_guard<std::mutex> lock(mu);

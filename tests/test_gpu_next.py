@@ -191,3 +191,53 @@ def test_local_kchunk_one_is_lambda_x():
     t = {n: to_torch(v[0], "f32", dev) for n, v in inp.items()}
     h = gspn.fwd(t["x"], t["w_l"], t["w_m"], t["w_r"], t["lam"], 0xF, 4, kchunk=1)
     torch.testing.assert_close(h, t["lam"] * t["x"].unsqueeze(0), rtol=0, atol=0)
+
+
+# ------------------------------------------------------------------- fused backward (G = C, stream path)
+
+# Unpacked, unsplit per-channel shapes (max(H, W) > 256 or a single plane): the adjoint recurrence and
+# the tap gradients run in one pass; ragged tiles on both axes, reversed directions, single directions.
+FUSED_SHAPES = [
+    (1, 2, 2, 300, 264, 0xF, "bf16"),
+    (2, 2, 2, 264, 300, 0xF, "f32"),
+    (1, 3, 3, 272, 288, 0x5, "bf16"),
+    (1, 2, 2, 280, 264, 0xA, "bf16"),
+    (1, 1, 1, 100, 72, 0xF, "bf16"),
+    (1, 1, 1, 37, 24, 0xF, "f32"),
+    (1, 2, 2, 512, 512, 0xF, "bf16"),
+    (1, 2, 2, 257, 512, 0xC, "bf16"),
+    (1, 2, 2, 512, 8, 0xF, "bf16"),
+]
+
+
+@pytest.mark.parametrize("pre", [False, True], ids=["raw", "prenorm"])
+@pytest.mark.parametrize("shape", FUSED_SHAPES, ids=lambda s: "B{}C{}G{}H{}W{}d{:x}{}".format(*s))
+def test_fused_bwd_parity(shape, pre):
+    """gspn_bwd on the fused path vs the oracle backward given the same (stored-dtype) h."""
+    B, C, G, H, W, dirs, dt = shape
+    cfg = small_config(B, C, G, H, W, dirs, dt, cfg_id=605)
+    inp = host_inputs(cfg)
+    f = {n: v[1] for n, v in inp.items()}
+    dev = _dev()
+    t = {n: to_torch(v[0], dt, dev) for n, v in inp.items()}
+    flags = gspn.FLAG_PRENORMALIZED if pre else 0
+    if pre:  # pre-normalised taps: use the oracle's normalisation of the generated taps as the input
+        import torch
+
+        S = t["w_l"].float() + t["w_m"].float() + t["w_r"].float()
+        for n in ("w_l", "w_m", "w_r"):
+            t[n] = (t[n].float() / S).to(t[n].dtype)
+            f[n] = from_torch(t[n])
+    h = gspn.fwd(t["x"], t["w_l"], t["w_m"], t["w_r"], t["lam"], dirs, G, flags=flags)
+    grads = gspn.bwd(t["x"], t["w_l"], t["w_m"], t["w_r"], t["lam"], h, t["dh"], dirs, G, flags=flags)
+    assert gspn.last_path() == "stream-fused"
+    g_ref = oracle.bwd(f["x"], f["w_l"], f["w_m"], f["w_r"], f["lam"], from_torch(h), f["dh"], dirs, G,
+                       flags=oracle.PRENORMALIZED if pre else 0)
+    tol = TOL[dt]
+    for name, a, r in zip(("dx", "dw_l", "dw_m", "dw_r", "dlam"), grads, g_ref):
+        a = from_torch(a)
+        if a.ndim == 5:
+            for s in range(a.shape[0]):
+                assert normwise(a[s], r[s]) <= tol, f"{name} slab {s}"
+        else:
+            assert normwise(a, r) <= tol, name
