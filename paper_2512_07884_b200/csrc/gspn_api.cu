@@ -173,13 +173,22 @@ gspn_status_t gspn_fwd_local(const void* x, const void* w_l, const void* w_m, co
     int launches = 0;
     bool handled = false;
     cudaError_t e = cudaSuccess;
-    if (!(flags & GSPN_FLAG_FORCE_GENERIC)) e = gspn::launch_fwd_stream(p, dtype, cs, &launches, &handled);
+    const char* path = "generic";
+    if (!(flags & GSPN_FLAG_FORCE_GENERIC)) {
+      e = gspn::launch_fwd_stream(p, dtype, cs, &launches, &handled);
+      if (handled) path = "stream";
+      if (e == cudaSuccess && !handled && gspn::small_eligible(p)) {
+        e = gspn::launch_fwd_small(p, dtype, cs, &launches);
+        handled = true;
+        path = "small";
+      }
+    }
     if (e == cudaSuccess && !handled) e = gspn::launch_fwd_generic(p, dtype, cs, &launches);
     if (e != cudaSuccess) {
       snprintf(t_detail, sizeof t_detail, "CUDA error: %s", cudaGetErrorString(e));
       return GSPN_ERR_CUDA;
     }
-    t_path = handled ? "stream" : "generic";
+    t_path = path;
     t_launches = launches;
     return GSPN_OK;
   } catch (const std::exception& ex) {
@@ -256,7 +265,8 @@ gspn_status_t gspn_bwd_local(const void* x, const void* w_l, const void* w_m, co
     if (e == cudaSuccess && !handled) {
       char* ws = static_cast<char*>(workspace);
       p.dx_acc = reinterpret_cast<float*>(ws);
-      size_t off = align_up((size_t)(B * C * H * W) * sizeof(float));
+      const size_t dx_bytes = align_up((size_t)(B * C * H * W) * sizeof(float));
+      size_t off = dx_bytes;
       const size_t zero_bytes = generic_workspace(B, C, H, W, D, groups);
       if (groups < C) {
         const size_t nwb = align_up((size_t)(D * B * groups * H * W) * sizeof(float));
@@ -264,8 +274,17 @@ gspn_status_t gspn_bwd_local(const void* x, const void* w_l, const void* w_m, co
         p.dwa_m = reinterpret_cast<float*>(ws + off); off += nwb;
         p.dwa_r = reinterpret_cast<float*>(ws + off); off += nwb;
       }
-      e = cudaMemsetAsync(workspace, 0, zero_bytes, cs);
-      if (e == cudaSuccess) e = gspn::launch_bwd_generic(p, dtype, cs, &launches);
+      if (!(flags & GSPN_FLAG_FORCE_GENERIC) && gspn::small_eligible(p)) {
+        // small-plane path: dx summed inside the CTA; only the group sums (G < C) use the workspace
+        stream_path = "small";
+        handled = true;
+        if (groups < C) e = cudaMemsetAsync(ws + dx_bytes, 0, zero_bytes - dx_bytes, cs);
+        if (e == cudaSuccess) e = gspn::launch_bwd_small(p, dtype, cs, &launches);
+        if (e == cudaSuccess && groups < C) e = gspn::launch_finish_dw(p, dtype, cs, &launches);
+      } else {
+        e = cudaMemsetAsync(workspace, 0, zero_bytes, cs);
+        if (e == cudaSuccess) e = gspn::launch_bwd_generic(p, dtype, cs, &launches);
+      }
     }
     if (e != cudaSuccess) {
       snprintf(t_detail, sizeof t_detail, "CUDA error: %s", cudaGetErrorString(e));

@@ -72,7 +72,8 @@ __host__ __device__ __forceinline__ bool seg_start_px(uint32_t dirbit, int64_t i
   }
 }
 // The same in scan coordinates: step t of a direction with scan length L (t = 0 always starts).
-__host__ __device__ __forceinline__ bool seg_start_step(uint32_t dirbit, int64_t t, int64_t L, int64_t kchunk) {
+template <typename I>  // int64_t (generic path) or int (small planes: 32-bit modulo)
+__host__ __device__ __forceinline__ bool seg_start_step(uint32_t dirbit, I t, I L, I kchunk) {
   if (t == 0) return true;
   if (kchunk <= 0) return false;
   const bool fwd_dir = dirbit == GSPN_DIR_T2B || dirbit == GSPN_DIR_L2R;

@@ -237,6 +237,14 @@ static cudaError_t bwd_generic_t(const ScanParams& p, cudaStream_t s, int* launc
   return cudaSuccess;
 }
 
+cudaError_t launch_finish_dw(const ScanParams& p, gspn_dtype_t dt, cudaStream_t s, int* launches) {
+  const unsigned blocks = grid_stride_blocks(p.D * p.B * p.G * p.H * p.W);
+  if (dt == GSPN_BF16) finish_dw_kernel<__nv_bfloat16><<<blocks, 256, 0, s>>>(p);
+  else finish_dw_kernel<float><<<blocks, 256, 0, s>>>(p);
+  *launches += 1;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_bwd_generic(const ScanParams& p, gspn_dtype_t dt, cudaStream_t s, int* launches) {
   return dt == GSPN_BF16 ? bwd_generic_t<__nv_bfloat16>(p, s, launches) : bwd_generic_t<float>(p, s, launches);
 }

@@ -11,6 +11,14 @@ int64_t generic_max_P();
 cudaError_t launch_fwd_generic(const ScanParams& p, gspn_dtype_t dt, cudaStream_t s, int* launches);
 cudaError_t launch_bwd_generic(const ScanParams& p, gspn_dtype_t dt, cudaStream_t s, int* launches);
 
+// Group-summed tap gradients (fp32 workspace dwa_*) -> dw through the normalisation Jacobian (G < C).
+cudaError_t launch_finish_dw(const ScanParams& p, gspn_dtype_t dt, cudaStream_t s, int* launches);
+
+// Small-plane path (gspn_small.cu): max(H, W) <= 32, whole planes in shared memory, one CTA per (b, c).
+bool small_eligible(const ScanParams& p);
+cudaError_t launch_fwd_small(const ScanParams& p, gspn_dtype_t dt, cudaStream_t s, int* launches);
+cudaError_t launch_bwd_small(const ScanParams& p, gspn_dtype_t dt, cudaStream_t s, int* launches);
+
 // Fast TMA-streaming path (gspn_stream.cu). *handled = false when the shape is not eligible.
 cudaError_t launch_fwd_stream(const ScanParams& p, gspn_dtype_t dt, cudaStream_t s, int* launches, bool* handled);
 // Backward: *path = "stream-fused" (recurrence + tap gradients in one pass, G = C) or "stream" (split).

@@ -1,0 +1,262 @@
+// gspn_small.cu — small-plane path (max(H, W) <= 32): the compact-channel and proxy-space shapes of the
+// paper (28 x 28 stages with C_proxy channels) whose rows are too short for TMA's
+// 16-byte row strides (W s % 16 != 0, e.g. 28 x 2 bytes). SURVEY.md §8(a) a2 "small-plane path".
+//
+// One CTA per (b, c) plane, one warp per direction (D <= 4 warps). Every plane the chain set needs is
+// staged whole in shared memory with coalesced vector loads (a plane is at most 32 x 32 elements); then
+// each warp runs its direction's L-step recurrence with lane = position (P <= 32), neighbours by warp
+// shuffle, no block barriers inside the scan; outputs leave shared memory with coalesced stores.
+// Forward: h_t[r] = a h_{t-1}[r-1] + b h_{t-1}[r] + c h_{t-1}[r+1] + lam x (Eq. 1/3).
+// Backward: each warp runs the adjoint recurrence of its direction into an fp32
+// g plane; then all threads form, per pixel, dlam_d = g_d x, dx = sum_d g_d lam_d (fixed order, no
+// atomics), Da/Db/Dc from h_{t-1} and the normalisation Jacobian -- written directly for per-channel
+// weights (G = C), or summed over the group's channels with fp32 red.global.add into the workspace and
+// finished by the generic path's finish_dw kernel (G < C).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "gspn_common.cuh"
+#include "gspn_internal.h"
+
+namespace gspn {
+namespace {
+
+constexpr int kSmallMax = 32;
+
+// Copy n elements (one plane) global -> shared; 16-byte vectors when both sides allow it.
+template <typename T>
+__device__ __forceinline__ void plane_in(T* dst, const T* src, int n) {
+  const bool vec = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15u) == 0 &&
+                   (n * static_cast<int>(sizeof(T))) % 16 == 0;
+  if (vec) {
+    const int nv = n * static_cast<int>(sizeof(T)) / 16;
+    const uint4* s = reinterpret_cast<const uint4*>(src);
+    uint4* d = reinterpret_cast<uint4*>(dst);
+    for (int i = threadIdx.x; i < nv; i += blockDim.x) d[i] = __ldg(s + i);
+  } else {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void plane_out(T* dst, const T* src, int n) {
+  const bool vec = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15u) == 0 &&
+                   (n * static_cast<int>(sizeof(T))) % 16 == 0;
+  if (vec) {
+    const int nv = n * static_cast<int>(sizeof(T)) / 16;
+    const uint4* s = reinterpret_cast<const uint4*>(src);
+    uint4* d = reinterpret_cast<uint4*>(dst);
+    for (int i = threadIdx.x; i < nv; i += blockDim.x) d[i] = s[i];
+  } else {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+  }
+}
+
+// Row-normalised taps with the hardware reciprocal (rcp.approx, <= 1 ulp; R15) -- the scan is
+// a serial chain per warp, so the IEEE reciprocal's slow-path branch would sit on its critical path.
+__device__ __forceinline__ Taps fast_taps(float wl, float wm, float wr, bool has_l, bool has_r, bool prenorm) {
+  Taps t;
+  const float l = has_l ? wl : 0.f, r = has_r ? wr : 0.f;
+  if (prenorm) {
+    t.a = l; t.b = wm; t.c = r; t.inv = 1.f;
+  } else {
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t.inv) : "f"(wm + l + r));
+    t.a = l * t.inv; t.b = wm * t.inv; t.c = r * t.inv;
+  }
+  return t;
+}
+
+// Shared-memory planes are padded to 16 bytes so every plane starts aligned.
+__host__ __device__ __forceinline__ int padded(int n, int es) { return (n * es + 15) / 16 * 16 / es; }
+
+// Forward. smem: x | per direction: lam, w_l, w_m, w_r, h.
+template <typename T>
+__global__ void __launch_bounds__(128) fwd_small_kernel(ScanParams p) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const int H = static_cast<int>(p.H), W = static_cast<int>(p.W), HW = H * W, D = static_cast<int>(p.D);
+  const int np = padded(HW, sizeof(T));
+  const int64_t bc = blockIdx.x;  // b * C + c
+  const int64_t b = bc / p.C, c = bc % p.C, g = c / (p.C / p.G);
+  T* xs = reinterpret_cast<T*>(sm);
+  plane_in(xs, static_cast<const T*>(p.x) + bc * HW, HW);
+  for (int k = 0; k < D; ++k) {
+    T* base = xs + np * (1 + 5 * k);
+    const int64_t chain = (k * p.B + b) * p.C + c, wpl = (k * p.B + b) * p.G + g;
+    plane_in(base, static_cast<const T*>(p.lam) + chain * HW, HW);
+    plane_in(base + np, static_cast<const T*>(p.wl) + wpl * HW, HW);
+    plane_in(base + 2 * np, static_cast<const T*>(p.wm) + wpl * HW, HW);
+    plane_in(base + 3 * np, static_cast<const T*>(p.wr) + wpl * HW, HW);
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, r = threadIdx.x & 31;
+  const bool prenorm = p.flags & GSPN_FLAG_PRENORMALIZED;
+  if (warp < D) {
+    const uint32_t dir = p.dirbit[warp];
+    const DirGeom gm = dir_geom(dir, H, W);
+    const int L = static_cast<int>(gm.L), P = static_cast<int>(gm.P);
+    const int gbase = static_cast<int>(gm.base), gts = static_cast<int>(gm.ts), grs = static_cast<int>(gm.rs);
+    const int kc = static_cast<int>(p.kchunk);
+    const T* lam = xs + np * (1 + 5 * warp);
+    const T *wl = lam + np, *wm = lam + 2 * np, *wr = lam + 3 * np;
+    T* h = xs + np * (1 + 5 * warp) + 4 * np;
+    const bool in = r < P, hl = r >= 1, hr = r <= P - 2;
+    float hv = 0.f;
+    for (int t = 0; t < L; ++t) {
+      const int off = gbase + t * gts + (in ? r : 0) * grs;
+      const float up = __shfl_up_sync(0xffffffffu, hv, 1);
+      const float dn = __shfl_down_sync(0xffffffffu, hv, 1);
+      float v = 0.f;
+      if (in) {
+        const Taps tp = fast_taps(to_f(wl[off]), to_f(wm[off]), to_f(wr[off]), hl, hr, prenorm);
+        float acc = 0.f;
+        if (!seg_start_step(dir, t, L, kc)) {
+          acc = tp.b * hv;
+          if (hl) acc = fmaf(tp.a, up, acc);
+          if (hr) acc = fmaf(tp.c, dn, acc);
+        }
+        v = fmaf(to_f(lam[off]), to_f(xs[off]), acc);
+        h[off] = from_f<T>(v);
+      }
+      hv = v;
+    }
+  }
+  __syncthreads();
+  for (int k = 0; k < D; ++k) {
+    const int64_t chain = (k * p.B + b) * p.C + c;
+    plane_out(static_cast<T*>(p.hout) + chain * HW, xs + np * (1 + 5 * k + 4), HW);
+  }
+}
+
+// Backward. smem: x | per direction: lam, w_l, w_m, w_r, h, dh | fp32 g planes [D][HW].
+template <typename T, bool kPerChannel>
+__global__ void __launch_bounds__(128) bwd_small_kernel(ScanParams p) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const int H = static_cast<int>(p.H), W = static_cast<int>(p.W), HW = H * W, D = static_cast<int>(p.D);
+  const int np = padded(HW, sizeof(T));
+  const int64_t bc = blockIdx.x;
+  const int64_t b = bc / p.C, c = bc % p.C, g = c / (p.C / p.G);
+  T* xs = reinterpret_cast<T*>(sm);
+  float* gs = reinterpret_cast<float*>(sm + static_cast<size_t>(np) * (1 + 6 * D) * sizeof(T));
+  plane_in(xs, static_cast<const T*>(p.x) + bc * HW, HW);
+  for (int k = 0; k < D; ++k) {
+    T* base = xs + np * (1 + 6 * k);
+    const int64_t chain = (k * p.B + b) * p.C + c, wpl = (k * p.B + b) * p.G + g;
+    plane_in(base, static_cast<const T*>(p.lam) + chain * HW, HW);
+    plane_in(base + np, static_cast<const T*>(p.wl) + wpl * HW, HW);
+    plane_in(base + 2 * np, static_cast<const T*>(p.wm) + wpl * HW, HW);
+    plane_in(base + 3 * np, static_cast<const T*>(p.wr) + wpl * HW, HW);
+    plane_in(base + 4 * np, static_cast<const T*>(p.h) + chain * HW, HW);
+    plane_in(base + 5 * np, static_cast<const T*>(p.dh) + chain * HW, HW);
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, r = threadIdx.x & 31;
+  const bool prenorm = p.flags & GSPN_FLAG_PRENORMALIZED;
+  if (warp < D) {  // adjoint recurrence, reverse step order: g_t = dh_t + (b g)[r] + (a g)[r+1] + (c g)[r-1]
+    const uint32_t dir = p.dirbit[warp];
+    const DirGeom gm = dir_geom(dir, H, W);
+    const int L = static_cast<int>(gm.L), P = static_cast<int>(gm.P);
+    const int gbase = static_cast<int>(gm.base), gts = static_cast<int>(gm.ts), grs = static_cast<int>(gm.rs);
+    const int kc = static_cast<int>(p.kchunk);
+    const T* lam = xs + np * (1 + 6 * warp);
+    const T *wl = lam + np, *wm = lam + 2 * np, *wr = lam + 3 * np, *dh = lam + 5 * np;
+    float* gp = gs + warp * HW;
+    const bool in = r < P, hl = r >= 1, hr = r <= P - 2;
+    float ea = 0.f, eb = 0.f, ec = 0.f;  // (a g, b g, c g) of step t+1 at this position
+    for (int t = L - 1; t >= 0; --t) {
+      const float from_r = __shfl_down_sync(0xffffffffu, ea, 1);  // a_{t+1}[r+1] g_{t+1}[r+1]
+      const float from_l = __shfl_up_sync(0xffffffffu, ec, 1);    // c_{t+1}[r-1] g_{t+1}[r-1]
+      float na = 0.f, nb = 0.f, nc = 0.f;
+      if (in) {
+        const int off = gbase + t * gts + r * grs;
+        const float gt = to_f(dh[off]) + eb + (hr ? from_r : 0.f) + (hl ? from_l : 0.f);
+        gp[off] = gt;
+        if (!seg_start_step(dir, t, L, kc)) {  // h_t depends on h_{t-1}: pass g back through w_t
+          const Taps tp = fast_taps(to_f(wl[off]), to_f(wm[off]), to_f(wr[off]), hl, hr, prenorm);
+          na = tp.a * gt; nb = tp.b * gt; nc = tp.c * gt;
+        }
+      }
+      ea = na; eb = nb; ec = nc;
+    }
+  }
+  __syncthreads();
+  // per pixel: dlam_d, dx, and the tap gradients of every direction
+  for (int px = threadIdx.x; px < HW; px += blockDim.x) {
+    const int i = px / W, j = px - (px / W) * W;
+    const float xv = to_f(xs[px]);
+    float dx = 0.f;
+    for (int k = 0; k < D; ++k) {
+      const T* lam = xs + np * (1 + 6 * k);
+      const T *wl = lam + np, *wm = lam + 2 * np, *wr = lam + 3 * np, *h = lam + 4 * np;
+      const float gt = gs[k * HW + px];
+      const int64_t chain = (k * p.B + b) * p.C + c;
+      static_cast<T*>(p.dlam)[chain * HW + px] = from_f<T>(gt * xv);
+      dx = fmaf(gt, to_f(lam[px]), dx);
+      const uint32_t dir = p.dirbit[k];
+      const bool vert = is_vertical(dir);
+      const int t = dir == GSPN_DIR_T2B ? i : dir == GSPN_DIR_B2T ? H - 1 - i : dir == GSPN_DIR_L2R ? j : W - 1 - j;
+      const int L = vert ? H : W, P = vert ? W : H, rr = vert ? j : i;
+      const bool hl = rr >= 1, hr = rr <= P - 2;
+      float Da = 0.f, Db = 0.f, Dc = 0.f;
+      if (!seg_start_step(dir, t, L, static_cast<int>(p.kchunk))) {  // h_{t-1} and its neighbours along the parallel axis
+        const int prev = dir == GSPN_DIR_T2B ? px - W : dir == GSPN_DIR_B2T ? px + W : dir == GSPN_DIR_L2R ? px - 1 : px + 1;
+        const int rs = vert ? 1 : W;
+        Db = gt * to_f(h[prev]);
+        if (hl) Da = gt * to_f(h[prev - rs]);
+        if (hr) Dc = gt * to_f(h[prev + rs]);
+      }
+      const int64_t wofs = ((k * p.B + b) * p.G + g) * HW + px;
+      if constexpr (kPerChannel) {
+        float ol, om, orr;
+        jacobian<true>(to_f(wl[px]), to_f(wm[px]), to_f(wr[px]), hl, hr, prenorm, Da, Db, Dc, ol, om, orr);
+        static_cast<T*>(p.dwl)[wofs] = from_f<T>(hl ? ol : 0.f);
+        static_cast<T*>(p.dwm)[wofs] = from_f<T>(om);
+        static_cast<T*>(p.dwr)[wofs] = from_f<T>(hr ? orr : 0.f);
+      } else {
+        if (hl) atomicAdd(p.dwa_l + wofs, Da);
+        atomicAdd(p.dwa_m + wofs, Db);
+        if (hr) atomicAdd(p.dwa_r + wofs, Dc);
+      }
+    }
+    static_cast<T*>(p.dx)[bc * HW + px] = from_f<T>(dx);
+  }
+}
+
+size_t fwd_smem(const ScanParams& p, int es) {
+  const int np = padded(static_cast<int>(p.H * p.W), es);
+  return static_cast<size_t>(np) * (1 + 5 * p.D) * es;
+}
+size_t bwd_smem(const ScanParams& p, int es) {
+  const int np = padded(static_cast<int>(p.H * p.W), es);
+  return static_cast<size_t>(np) * (1 + 6 * p.D) * es + static_cast<size_t>(p.D * p.H * p.W) * 4;
+}
+
+template <typename K>
+cudaError_t launch_small(K kern, const ScanParams& p, size_t smem, cudaStream_t s) {
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  kern<<<static_cast<unsigned>(p.B * p.C), 128, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool small_eligible(const ScanParams& p) { return p.H <= kSmallMax && p.W <= kSmallMax && p.D <= 4; }
+
+cudaError_t launch_fwd_small(const ScanParams& p, gspn_dtype_t dt, cudaStream_t s, int* launches) {
+  *launches += 1;
+  if (dt == GSPN_BF16) return launch_small(fwd_small_kernel<__nv_bfloat16>, p, fwd_smem(p, 2), s);
+  return launch_small(fwd_small_kernel<float>, p, fwd_smem(p, 4), s);
+}
+
+// G < C: p.dwa_* must point at zeroed fp32 workspace; the caller then runs the generic finish_dw.
+cudaError_t launch_bwd_small(const ScanParams& p, gspn_dtype_t dt, cudaStream_t s, int* launches) {
+  *launches += 1;
+  const bool pc = p.G == p.C;
+  if (dt == GSPN_BF16)
+    return pc ? launch_small(bwd_small_kernel<__nv_bfloat16, true>, p, bwd_smem(p, 2), s)
+              : launch_small(bwd_small_kernel<__nv_bfloat16, false>, p, bwd_smem(p, 2), s);
+  return pc ? launch_small(bwd_small_kernel<float, true>, p, bwd_smem(p, 4), s)
+            : launch_small(bwd_small_kernel<float, false>, p, bwd_smem(p, 4), s);
+}
+
+}  // namespace gspn

@@ -241,3 +241,46 @@ def test_fused_bwd_parity(shape, pre):
                 assert normwise(a[s], r[s]) <= tol, f"{name} slab {s}"
         else:
             assert normwise(a, r) <= tol, name
+
+
+# ------------------------------------------------------------------- small-plane path (max(H, W) <= 32)
+
+# Rows too short for TMA (W s % 16 != 0): BASELINE configs[2]'s 28 x 28 proxy planes, grouped and per
+# channel, odd sizes, single directions, GSPN-local.
+SMALL_CASES = [
+    (2, 8, 1, 28, 28, 0xF, "bf16", 0),
+    (2, 12, 4, 28, 28, 0xF, "bf16", 0),
+    (1, 6, 6, 28, 26, 0xF, "f32", 0),
+    (3, 4, 2, 13, 27, 0xF, "bf16", 0),
+    (1, 3, 3, 31, 5, 0x9, "f32", 0),
+    (1, 2, 1, 1, 19, 0xF, "bf16", 0),
+    (2, 8, 1, 28, 28, 0xF, "bf16", 7),
+    (1, 4, 4, 21, 30, 0xF, "f32", 4),
+]
+
+
+@pytest.mark.parametrize("case", SMALL_CASES, ids=lambda c: "B{}C{}G{}H{}W{}d{:x}{}k{}".format(*c))
+def test_small_plane_parity(case):
+    B, C, G, H, W, dirs, dt, k = case
+    cfg = small_config(B, C, G, H, W, dirs, dt, cfg_id=606)
+    inp = host_inputs(cfg)
+    f = {n: v[1] for n, v in inp.items()}
+    dev = _dev()
+    t = {n: to_torch(v[0], dt, dev) for n, v in inp.items()}
+    h = gspn.fwd(t["x"], t["w_l"], t["w_m"], t["w_r"], t["lam"], dirs, G, kchunk=k)
+    assert gspn.last_path() == "small"
+    grads = gspn.bwd(t["x"], t["w_l"], t["w_m"], t["w_r"], t["lam"], h, t["dh"], dirs, G, kchunk=k)
+    assert gspn.last_path() == "small"
+    h_ref = oracle.fwd(f["x"], f["w_l"], f["w_m"], f["w_r"], f["lam"], dirs, G, kchunk=k)
+    g_ref = oracle.bwd(f["x"], f["w_l"], f["w_m"], f["w_r"], f["lam"], from_torch(h), f["dh"], dirs, G, kchunk=k)
+    tol = TOL[dt]
+    hg = from_torch(h)
+    for s in range(cfg.D):
+        assert normwise(hg[s], h_ref[s]) <= tol, f"h slab {s}"
+    for name, a, r in zip(("dx", "dw_l", "dw_m", "dw_r", "dlam"), grads, g_ref):
+        a = from_torch(a)
+        if a.ndim == 5:
+            for s in range(a.shape[0]):
+                assert normwise(a[s], r[s]) <= tol, f"{name} slab {s}"
+        else:
+            assert normwise(a, r) <= tol, name
