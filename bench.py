@@ -127,32 +127,19 @@ def traffic_for(config_name: str, kernel: str):
 
 # ------------------------------------------------------------------------------------------ oracle arm
 
-def oracle_sample(cfg, seconds: float):
-    """Time the fp64 oracle (as it stands) on consecutive units of `cfg` until ~`seconds` of CPU work.
-    Returns (algorithmic bytes processed, wall seconds, threads, description)."""
-    import numpy as np
-
+def oracle_prepare(cfg, max_elems: int = 1 << 27):
+    """A bounded sample of `cfg` for the CPU oracle: consecutive units (b, g) as one (B'=n, C=C/G, G=1)
+    problem whose largest tensor has at most `max_elems` elements, inputs regenerated on the host (fp64).
+    Generated once (untimed); `oracle_time` then times passes over it."""
     import oracle
     import synth
-    from tests.parity_utils import unit_inputs
 
-    threads = oracle.default_threads()
     U = cfg.B * cfg.G
     Cg = cfg.C // cfg.G
-    unit_cfg = cfg.with_(B=1, C=Cg, G=1)
-    per_unit = unit_cfg.fwd_bytes() + unit_cfg.bwd_bytes()
-    # probe one unit single-threaded to size the batch
-    inp = unit_inputs(cfg, 0, 0)
-    f = {k: v[1] for k, v in inp.items()}
-    t0 = time.perf_counter()
-    h = oracle.fwd(f["x"], f["w_l"], f["w_m"], f["w_r"], f["lam"], cfg.dirs, 1, threads=1)
-    oracle.bwd(f["x"], f["w_l"], f["w_m"], f["w_r"], f["lam"], h, f["dh"], cfg.dirs, 1, threads=1)
-    t_unit = max(time.perf_counter() - t0, 1e-6)
-    n_units = int(max(1, min(U, round(seconds * threads / t_unit))))
-    # batch of consecutive units as one (B'=n, C=Cg, G=1) problem; inputs regenerated on the host
-    seed = synth.seed_for(cfg.cfg_id)
     HW = cfg.H * cfg.W
     D = cfg.D
+    n_units = int(max(1, min(U, max_elems // max(1, D * Cg * HW))))
+    seed = synth.seed_for(cfg.cfg_id)
     x = synth.as_f64(synth.tensor(seed, "x", (n_units, Cg, cfg.H, cfg.W), cfg.dtype), cfg.dtype)
     ws = [synth.as_f64(synth.tensor(seed, n, (D, n_units, 1, cfg.H, cfg.W), cfg.dtype, 0, n_units * HW,
                                     U * HW), cfg.dtype) for n in ("w_l", "w_m", "w_r")]
@@ -160,14 +147,33 @@ def oracle_sample(cfg, seconds: float):
                                     n_units * Cg * HW, cfg.B * cfg.C * HW), cfg.dtype)
     dh = synth.as_f64(synth.tensor(seed, "dh", (D, n_units, Cg, cfg.H, cfg.W), cfg.dtype, 0,
                                    n_units * Cg * HW, cfg.B * cfg.C * HW), cfg.dtype)
-    t0 = time.perf_counter()
-    h = oracle.fwd(x, ws[0], ws[1], ws[2], lam, cfg.dirs, 1, threads=threads)
-    oracle.bwd(x, ws[0], ws[1], ws[2], lam, h, dh, cfg.dirs, 1, threads=threads)
-    wall = time.perf_counter() - t0
-    del np
+    unit_cfg = cfg.with_(B=1, C=Cg, G=1)
+    per_unit = unit_cfg.fwd_bytes() + unit_cfg.bwd_bytes()
+    threads = oracle.default_threads()
     desc = (f"{n_units} of {U} units (b,g) of config {cfg.name} (fwd+bwd, all {D} directions, fp64 oracle, "
             f"{threads} threads); bytes counted at the I/O dtype")
-    return n_units * per_unit, wall, threads, desc
+    return {"x": x, "ws": ws, "lam": lam, "dh": dh, "dirs": cfg.dirs, "bytes": n_units * per_unit,
+            "threads": threads, "desc": desc}
+
+
+def oracle_time(sm, seconds: float):
+    """Time whole fwd+bwd passes of the oracle (as it stands) over a prepared sample until ~`seconds`
+    (at least one pass). Returns (algorithmic bytes processed, wall seconds, threads, description)."""
+    import oracle
+
+    passes, t0 = 0, time.perf_counter()
+    while True:
+        h = oracle.fwd(sm["x"], *sm["ws"], sm["lam"], sm["dirs"], 1, threads=sm["threads"])
+        oracle.bwd(sm["x"], *sm["ws"], sm["lam"], h, sm["dh"], sm["dirs"], 1, threads=sm["threads"])
+        passes += 1
+        wall = time.perf_counter() - t0
+        if wall >= seconds:
+            break
+    return passes * sm["bytes"], wall, sm["threads"], f"{sm['desc']}; {passes} pass(es)"
+
+
+def oracle_sample(cfg, seconds: float):
+    return oracle_time(oracle_prepare(cfg), seconds)
 
 
 def run_reference(args):
@@ -178,11 +184,12 @@ def run_reference(args):
 
     cfg = get_config(args.config)
     per_step = max(2.0, min(args.cpu_seconds, 60.0 / max(1, args.steps + args.warmup)))
+    sm = oracle_prepare(cfg)
     for _ in range(args.warmup):
-        oracle_sample(cfg, per_step / 2)
+        oracle_time(sm, per_step / 2)
     vals, walls, desc, threads = [], [], "", 1
     for _ in range(args.steps):
-        b, w, threads, desc = oracle_sample(cfg, per_step)
+        b, w, threads, desc = oracle_time(sm, per_step)
         vals.append(b / w / 1e9)
         walls.append(w)
     value = statistics.median(vals)
@@ -424,49 +431,96 @@ def measure_next(args, gspn, cfg, sh, t, h, outs, ws, dev, stream):
 
 
 def run_e2e(args, gspn, cfg, sh, t, h, outs, ws, dev, world, dist):
-    """Same metric through the public API with pinned HOST buffers: every step copies its inputs
-    host->device, runs fwd + bwd, and copies every output device->host (CUDA events on the stream)."""
+    """Same metric through the public API with pinned HOST buffers: every step copies all of its inputs
+    host->device, runs fwd + bwd, and copies every output device->host, inside the CUDA-event timed
+    region. The batch is streamed in per-b chunks (units are independent) through two
+    device buffer sets on three streams, so H2D of chunk k+1, compute of chunk k and D2H of chunk k-1
+    overlap (PCIe is full duplex) -- the way a caller with host-resident data uses the API."""
     import torch
 
-    stream = torch.cuda.current_stream(dev)
     names = ["x", "w_l", "w_m", "w_r", "lam", "dh"]
+    onames = ["h", "dx", "dw_l", "dw_m", "dw_r", "dlam"]
     host_in = {}
     for n in names:
         host_in[n] = torch.empty(t[n].shape, dtype=t[n].dtype, pin_memory=True)
         host_in[n].copy_(t[n])
-    host_out = [torch.empty(o.shape, dtype=o.dtype, pin_memory=True) for o in (h, *outs)]
+    full_out = {"h": h, "dx": outs[0], "dw_l": outs[1], "dw_m": outs[2], "dw_r": outs[3], "dlam": outs[4]}
+    host_out = {n: torch.empty(full_out[n].shape, dtype=full_out[n].dtype, pin_memory=True) for n in onames}
     h2d = sum(v.numel() * v.element_size() for v in host_in.values())
-    d2h = sum(v.numel() * v.element_size() for v in host_out)
+    d2h = sum(v.numel() * v.element_size() for v in host_out.values())
+    B = sh.B
+    dt_code = gspn.DTYPE_BF16 if cfg.dtype == "bf16" else gspn.DTYPE_F32
+
+    def chunk_shape(x):  # [B, ...] -> [1, ...]; [D, B, ...] -> [D, 1, ...]
+        return (1,) + tuple(x.shape[1:]) if x.dim() == 4 else (x.shape[0], 1) + tuple(x.shape[2:])
+
+    def piece(x, b):  # contiguous pieces of batch b: one for [B,...], D for [D,B,...]
+        return [x[b]] if x.dim() == 4 else [x[d, b] for d in range(x.shape[0])]
+
+    bufs = []
+    for _ in range(2):
+        bi = {n: torch.empty(chunk_shape(t[n]), dtype=t[n].dtype, device=dev) for n in names}
+        bo = {n: torch.empty(chunk_shape(full_out[n]), dtype=full_out[n].dtype, device=dev) for n in onames}
+        wsb = gspn.workspace_bytes(1, sh.C, cfg.H, cfg.W, cfg.dirs, sh.G, dt_code)
+        bufs.append((bi, bo, torch.empty(max(wsb, 16), dtype=torch.uint8, device=dev)))
+    s_in, s_cmp, s_out = (torch.cuda.Stream(dev) for _ in range(3))
+    ev = {k: [torch.cuda.Event() for _ in range(2)] for k in ("in", "cmp", "out")}
+    for k in ev:  # nothing pending on either buffer set at the start
+        for e in ev[k]:
+            e.record(torch.cuda.current_stream(dev))
 
     def step():
-        for n in names:
-            t[n].copy_(host_in[n], non_blocking=True)
-        gspn.fwd(t["x"], t["w_l"], t["w_m"], t["w_r"], t["lam"], cfg.dirs, sh.G, out=h)
-        gspn.bwd(t["x"], t["w_l"], t["w_m"], t["w_r"], t["lam"], h, t["dh"], cfg.dirs, sh.G, outs=outs, workspace=ws)
-        for ho, o in zip(host_out, (h, *outs)):
-            ho.copy_(o, non_blocking=True)
+        for b in range(B):
+            j = b % 2
+            bi, bo, wsj = bufs[j]
+            s_in.wait_event(ev["cmp"][j])  # compute of chunk b-2 has finished reading these inputs
+            with torch.cuda.stream(s_in):
+                for n in names:
+                    for dst, src in zip(piece(bi[n], 0), piece(host_in[n], b)):
+                        dst.copy_(src, non_blocking=True)
+            ev["in"][j].record(s_in)
+            s_cmp.wait_event(ev["in"][j])
+            s_cmp.wait_event(ev["out"][j])  # D2H of chunk b-2 has finished reading these outputs
+            with torch.cuda.stream(s_cmp):
+                gspn.fwd(bi["x"], bi["w_l"], bi["w_m"], bi["w_r"], bi["lam"], cfg.dirs, sh.G, out=bo["h"],
+                         stream=s_cmp)
+                gspn.bwd(bi["x"], bi["w_l"], bi["w_m"], bi["w_r"], bi["lam"], bo["h"], bi["dh"], cfg.dirs, sh.G,
+                         outs=(bo["dx"], bo["dw_l"], bo["dw_m"], bo["dw_r"], bo["dlam"]), workspace=wsj,
+                         stream=s_cmp)
+            ev["cmp"][j].record(s_cmp)
+            s_out.wait_event(ev["cmp"][j])
+            with torch.cuda.stream(s_out):
+                for n in onames:
+                    for dst, src in zip(piece(host_out[n], b), piece(bo[n], 0)):
+                        dst.copy_(src, non_blocking=True)
+            ev["out"][j].record(s_out)
 
+    main = torch.cuda.current_stream(dev)
     step()
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     n = max(1, args.e2e_steps)
-    e0.record(stream)
+    e0.record(main)
+    for s_ in (s_in, s_cmp, s_out):
+        s_.wait_event(e0)
     for _ in range(n):
         step()
-    e1.record(stream)
+    for s_ in (s_in, s_cmp, s_out):
+        main.wait_stream(s_)
+    e1.record(main)
     torch.cuda.synchronize(dev)
     ms = torch.tensor([e0.elapsed_time(e1) / n], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     ms = float(ms.item())
     total = (cfg.fwd_bytes() + cfg.bwd_bytes()) if args.scaling == "strong" else \
-        (gspn.algorithmic_bytes(sh.B, sh.C, cfg.H, cfg.W, cfg.dirs, sh.G,
-                                gspn.DTYPE_BF16 if cfg.dtype == "bf16" else gspn.DTYPE_F32, False) * 3 * world)
+        (gspn.algorithmic_bytes(sh.B, sh.C, cfg.H, cfg.W, cfg.dirs, sh.G, dt_code, False) * 3 * world)
     return {"value": total / (ms * 1e-3) / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d * world,
-            "d2h_bytes_per_step": d2h * world, "ms_per_step": ms, "steps": n,
-            "note": "pinned host buffers; H2D of x,w,lam,dh + fwd + bwd + D2H of h,dx,dw,dlam on one stream"}
+            "d2h_bytes_per_step": d2h * world, "ms_per_step": ms, "steps": n, "chunks": B,
+            "note": "pinned host buffers; per-b chunks through 2 device buffer sets on 3 streams: H2D of "
+                    "x,w,lam,dh | fwd + bwd | D2H of h,dx,dw,dlam overlap across chunks"}
 
 
 def main():
