@@ -70,13 +70,14 @@ __device__ __forceinline__ Taps fast_taps(float wl, float wm, float wr, bool has
 __host__ __device__ __forceinline__ int padded(int n, int es) { return (n * es + 15) / 16 * 16 / es; }
 
 // Forward. smem: x | per direction: lam, w_l, w_m, w_r, h.
-template <typename T>
+template <typename T, bool kLocal>
 __global__ void __launch_bounds__(128) fwd_small_kernel(ScanParams p) {
   extern __shared__ __align__(16) uint8_t sm[];
   const int H = static_cast<int>(p.H), W = static_cast<int>(p.W), HW = H * W, D = static_cast<int>(p.D);
   const int np = padded(HW, sizeof(T));
-  const int64_t bc = blockIdx.x;  // b * C + c
-  const int64_t b = bc / p.C, c = bc % p.C, g = c / (p.C / p.G);
+  const int C32 = static_cast<int>(p.C), Cg32 = static_cast<int>(p.C / p.G);
+  const int bc32 = blockIdx.x, b32 = bc32 / C32, c32 = bc32 - b32 * C32;  // 32-bit: B C < 2^31
+  const int64_t bc = bc32, b = b32, c = c32, g = c32 / Cg32;
   T* xs = reinterpret_cast<T*>(sm);
   plane_in(xs, static_cast<const T*>(p.x) + bc * HW, HW);
   for (int k = 0; k < D; ++k) {
@@ -101,23 +102,18 @@ __global__ void __launch_bounds__(128) fwd_small_kernel(ScanParams p) {
     T* h = xs + np * (1 + 5 * warp) + 4 * np;
     const bool in = r < P, hl = r >= 1, hr = r <= P - 2;
     float hv = 0.f;
-    for (int t = 0; t < L; ++t) {
-      const int off = gbase + t * gts + (in ? r : 0) * grs;
+    int off = gbase + (in ? r : 0) * grs;
+    for (int t = 0; t < L; ++t, off += gts) {
+      if constexpr (kLocal) {
+        if (seg_start_step(dir, t, L, kc)) hv = 0.f;  // warp-uniform: h_{t-1} does not propagate
+      }
       const float up = __shfl_up_sync(0xffffffffu, hv, 1);
       const float dn = __shfl_down_sync(0xffffffffu, hv, 1);
-      float v = 0.f;
-      if (in) {
-        const Taps tp = fast_taps(to_f(wl[off]), to_f(wm[off]), to_f(wr[off]), hl, hr, prenorm);
-        float acc = 0.f;
-        if (!seg_start_step(dir, t, L, kc)) {
-          acc = tp.b * hv;
-          if (hl) acc = fmaf(tp.a, up, acc);
-          if (hr) acc = fmaf(tp.c, dn, acc);
-        }
-        v = fmaf(to_f(lam[off]), to_f(xs[off]), acc);
-        h[off] = from_f<T>(v);
-      }
-      hv = v;
+      // masked taps are 0: lanes outside [0, P) (hv = 0) and the shuffle wrap never couple in
+      const Taps tp = fast_taps(to_f(wl[off]), to_f(wm[off]), to_f(wr[off]), hl, hr, prenorm);
+      const float v = fmaf(tp.a, up, fmaf(tp.b, hv, fmaf(tp.c, dn, to_f(lam[off]) * to_f(xs[off]))));
+      if (in) h[off] = from_f<T>(v);
+      hv = in ? v : 0.f;
     }
   }
   __syncthreads();
@@ -128,13 +124,14 @@ __global__ void __launch_bounds__(128) fwd_small_kernel(ScanParams p) {
 }
 
 // Backward. smem: x | per direction: lam, w_l, w_m, w_r, h, dh | fp32 g planes [D][HW].
-template <typename T, bool kPerChannel>
+template <typename T, bool kPerChannel, bool kLocal>
 __global__ void __launch_bounds__(128) bwd_small_kernel(ScanParams p) {
   extern __shared__ __align__(16) uint8_t sm[];
   const int H = static_cast<int>(p.H), W = static_cast<int>(p.W), HW = H * W, D = static_cast<int>(p.D);
   const int np = padded(HW, sizeof(T));
-  const int64_t bc = blockIdx.x;
-  const int64_t b = bc / p.C, c = bc % p.C, g = c / (p.C / p.G);
+  const int C32 = static_cast<int>(p.C), Cg32 = static_cast<int>(p.C / p.G);
+  const int bc32 = blockIdx.x, b32 = bc32 / C32, c32 = bc32 - b32 * C32;
+  const int64_t bc = bc32, b = b32, c = c32, g = c32 / Cg32;
   T* xs = reinterpret_cast<T*>(sm);
   float* gs = reinterpret_cast<float*>(sm + static_cast<size_t>(np) * (1 + 6 * D) * sizeof(T));
   plane_in(xs, static_cast<const T*>(p.x) + bc * HW, HW);
@@ -162,20 +159,19 @@ __global__ void __launch_bounds__(128) bwd_small_kernel(ScanParams p) {
     float* gp = gs + warp * HW;
     const bool in = r < P, hl = r >= 1, hr = r <= P - 2;
     float ea = 0.f, eb = 0.f, ec = 0.f;  // (a g, b g, c g) of step t+1 at this position
-    for (int t = L - 1; t >= 0; --t) {
+    int off = gbase + (L - 1) * gts + (in ? r : 0) * grs;
+    for (int t = L - 1; t >= 0; --t, off -= gts) {
       const float from_r = __shfl_down_sync(0xffffffffu, ea, 1);  // a_{t+1}[r+1] g_{t+1}[r+1]
       const float from_l = __shfl_up_sync(0xffffffffu, ec, 1);    // c_{t+1}[r-1] g_{t+1}[r-1]
-      float na = 0.f, nb = 0.f, nc = 0.f;
-      if (in) {
-        const int off = gbase + t * gts + r * grs;
-        const float gt = to_f(dh[off]) + eb + (hr ? from_r : 0.f) + (hl ? from_l : 0.f);
-        gp[off] = gt;
-        if (!seg_start_step(dir, t, L, kc)) {  // h_t depends on h_{t-1}: pass g back through w_t
-          const Taps tp = fast_taps(to_f(wl[off]), to_f(wm[off]), to_f(wr[off]), hl, hr, prenorm);
-          na = tp.a * gt; nb = tp.b * gt; nc = tp.c * gt;
-        }
+      // lanes outside [0, P) carry 0; the masks stop the shuffle wrap at lanes 0 / 31
+      const float gt = to_f(dh[off]) + eb + ((hr ? from_r : 0.f) + (hl ? from_l : 0.f));
+      if (in) gp[off] = gt;
+      const Taps tp = fast_taps(to_f(wl[off]), to_f(wm[off]), to_f(wr[off]), hl, hr, prenorm);
+      const float gi = in ? gt : 0.f;
+      ea = tp.a * gi; eb = tp.b * gi; ec = tp.c * gi;
+      if constexpr (kLocal) {
+        if (seg_start_step(dir, t, L, kc)) ea = eb = ec = 0.f;  // h_t did not depend on h_{t-1}
       }
-      ea = na; eb = nb; ec = nc;
     }
   }
   __syncthreads();
@@ -244,19 +240,29 @@ bool small_eligible(const ScanParams& p) { return p.H <= kSmallMax && p.W <= kSm
 
 cudaError_t launch_fwd_small(const ScanParams& p, gspn_dtype_t dt, cudaStream_t s, int* launches) {
   *launches += 1;
-  if (dt == GSPN_BF16) return launch_small(fwd_small_kernel<__nv_bfloat16>, p, fwd_smem(p, 2), s);
-  return launch_small(fwd_small_kernel<float>, p, fwd_smem(p, 4), s);
+  const bool local = p.kchunk > 0;
+  if (dt == GSPN_BF16)
+    return local ? launch_small(fwd_small_kernel<__nv_bfloat16, true>, p, fwd_smem(p, 2), s)
+                 : launch_small(fwd_small_kernel<__nv_bfloat16, false>, p, fwd_smem(p, 2), s);
+  return local ? launch_small(fwd_small_kernel<float, true>, p, fwd_smem(p, 4), s)
+               : launch_small(fwd_small_kernel<float, false>, p, fwd_smem(p, 4), s);
 }
 
 // G < C: p.dwa_* must point at zeroed fp32 workspace; the caller then runs the generic finish_dw.
 cudaError_t launch_bwd_small(const ScanParams& p, gspn_dtype_t dt, cudaStream_t s, int* launches) {
   *launches += 1;
-  const bool pc = p.G == p.C;
-  if (dt == GSPN_BF16)
-    return pc ? launch_small(bwd_small_kernel<__nv_bfloat16, true>, p, bwd_smem(p, 2), s)
-              : launch_small(bwd_small_kernel<__nv_bfloat16, false>, p, bwd_smem(p, 2), s);
-  return pc ? launch_small(bwd_small_kernel<float, true>, p, bwd_smem(p, 4), s)
-            : launch_small(bwd_small_kernel<float, false>, p, bwd_smem(p, 4), s);
+  const bool pc = p.G == p.C, lo = p.kchunk > 0;
+  using BF = __nv_bfloat16;
+  if (dt == GSPN_BF16) {
+    if (pc) return lo ? launch_small(bwd_small_kernel<BF, true, true>, p, bwd_smem(p, 2), s)
+                      : launch_small(bwd_small_kernel<BF, true, false>, p, bwd_smem(p, 2), s);
+    return lo ? launch_small(bwd_small_kernel<BF, false, true>, p, bwd_smem(p, 2), s)
+              : launch_small(bwd_small_kernel<BF, false, false>, p, bwd_smem(p, 2), s);
+  }
+  if (pc) return lo ? launch_small(bwd_small_kernel<float, true, true>, p, bwd_smem(p, 4), s)
+                    : launch_small(bwd_small_kernel<float, true, false>, p, bwd_smem(p, 4), s);
+  return lo ? launch_small(bwd_small_kernel<float, false, true>, p, bwd_smem(p, 4), s)
+            : launch_small(bwd_small_kernel<float, false, false>, p, bwd_smem(p, 4), s);
 }
 
 }  // namespace gspn
