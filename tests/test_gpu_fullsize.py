@@ -22,10 +22,10 @@ pytestmark = pytest.mark.gpu
 NTHREADS = oracle.default_threads()
 
 
-def _run(cfg, device):
+def _run(cfg, device, kchunk=0):
     t = make_inputs(cfg, device)
-    h = gspn.fwd(t["x"], t["w_l"], t["w_m"], t["w_r"], t["lam"], cfg.dirs, cfg.G)
-    g = gspn.bwd(t["x"], t["w_l"], t["w_m"], t["w_r"], t["lam"], h, t["dh"], cfg.dirs, cfg.G)
+    h = gspn.fwd(t["x"], t["w_l"], t["w_m"], t["w_r"], t["lam"], cfg.dirs, cfg.G, kchunk=kchunk)
+    g = gspn.bwd(t["x"], t["w_l"], t["w_m"], t["w_r"], t["lam"], h, t["dh"], cfg.dirs, cfg.G, kchunk=kchunk)
     return t, h, g
 
 
@@ -38,7 +38,7 @@ def _sample_units(cfg, n):
     return sorted(picks)
 
 
-def _check_unit(cfg, t, h, grads, u):
+def _check_unit(cfg, t, h, grads, u, kchunk=0):
     b, g = divmod(u, cfg.G)
     Cg = cfg.C // cfg.G
     c0 = g * Cg
@@ -51,8 +51,9 @@ def _check_unit(cfg, t, h, grads, u):
     else:
         assert np.array_equal(x_dev.numpy(), x_host)
     f = {k: v[1] for k, v in inp.items()}
-    h_ref = oracle.fwd(f["x"], f["w_l"], f["w_m"], f["w_r"], f["lam"], cfg.dirs, 1, threads=1)
-    gr = oracle.bwd(f["x"], f["w_l"], f["w_m"], f["w_r"], f["lam"], h_ref, f["dh"], cfg.dirs, 1, threads=1)
+    h_ref = oracle.fwd(f["x"], f["w_l"], f["w_m"], f["w_r"], f["lam"], cfg.dirs, 1, threads=1, kchunk=kchunk)
+    gr = oracle.bwd(f["x"], f["w_l"], f["w_m"], f["w_r"], f["lam"], h_ref, f["dh"], cfg.dirs, 1, threads=1,
+                    kchunk=kchunk)
     tol = TOL[cfg.dtype]
     got_h = from_torch(h[:, b:b + 1, c0:c0 + Cg])
     for k in range(cfg.D):
@@ -99,6 +100,16 @@ def test_config_sampled_parity(name, nunits, cuda_device):
     t, h, grads = _run(cfg, cuda_device)
     for u in _sample_units(cfg, nunits):
         _check_unit(cfg, t, h, grads, u)
+    _check_identities(cfg, t, h, grads)
+
+
+@pytest.mark.parametrize("name,nunits,kchunk", [("2", 3, 14), ("3b", 2, 7), ("4", 2, 128)])
+def test_config_sampled_parity_local(name, nunits, kchunk, cuda_device):
+    """GSPN-local at full size in the bench's launch configuration (bench `next.local`)."""
+    cfg = get_config(name)
+    t, h, grads = _run(cfg, cuda_device, kchunk)
+    for u in _sample_units(cfg, nunits):
+        _check_unit(cfg, t, h, grads, u, kchunk)
     _check_identities(cfg, t, h, grads)
 
 
