@@ -47,6 +47,10 @@ def _load():
         lib.gspn_oracle_merge_fwd.restype = None
         lib.gspn_oracle_merge_bwd.argtypes = [d] * 5 + [i64, i64, ctypes.c_int]
         lib.gspn_oracle_merge_bwd.restype = None
+        lib.gspn_oracle_proxy_mix.argtypes = [d] * 3 + [i64] * 4
+        lib.gspn_oracle_proxy_mix.restype = None
+        lib.gspn_oracle_proxy_wgrad.argtypes = [d] * 3 + [i64] * 4
+        lib.gspn_oracle_proxy_wgrad.restype = None
         _lib = lib
     return _lib
 
@@ -110,3 +114,25 @@ def merge_bwd(h, u, dy, mean: bool = False):
     dh, du = np.empty(h.shape), np.empty(h.shape)
     _load().gspn_oracle_merge_bwd(_p(h), _p(u), _p(dy), _p(dh), _p(du), D, N, int(mean))
     return dh, du
+
+
+def proxy_mix(inp, M) -> np.ndarray:
+    """out [B,Co,H,W] = sum_i M[o,i] inp[b,i] (1x1 projection); M [Co, Ci]."""
+    inp, M = _f64(inp), _f64(M)
+    B, Ci = inp.shape[:2]
+    Co = M.shape[0]
+    HW = int(np.prod(inp.shape[2:]))
+    out = np.empty((B, Co) + inp.shape[2:])
+    _load().gspn_oracle_proxy_mix(_p(inp), _p(M), _p(out), B, Ci, Co, HW)
+    return out
+
+
+def proxy_wgrad(dout, inp) -> np.ndarray:
+    """dM [Co, Ci] = sum_{b,n} dout[b,o,n] inp[b,i,n] (weight gradient of proxy_mix)."""
+    dout, inp = _f64(dout), _f64(inp)
+    B, Co = dout.shape[:2]
+    Ci = inp.shape[1]
+    HW = int(np.prod(inp.shape[2:]))
+    dM = np.empty((Co, Ci))
+    _load().gspn_oracle_proxy_wgrad(_p(dout), _p(inp), _p(dM), B, Ci, Co, HW)
+    return dM

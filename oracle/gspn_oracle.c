@@ -333,3 +333,31 @@ void gspn_oracle_merge_bwd(const double* h, const double* u, const double* dy, d
       du[d * N + n] = s * (h[d * N + n] * dy[n]);
     }
 }
+
+/* Compact-channel proxy projections (§4.2 "project the input tensor x in R^{N x C x H x W}
+ * into a lower-dimensional proxy subspace x_proxy in R^{N x C_proxy x H x W}"; "expand back
+ * to C with a learned 1x1 projection"). A 1x1 convolution is a channel mix at every
+ * pixel:  out[b, o, n] = sum_i M[o, i] in[b, i, n]   (n over the H W pixels; M [Co, Ci] row-major).
+ * Down-projection: M = P_down [C_proxy, C]; up-projection: M = P_up [C, C_proxy]. Its adjoints are the
+ * same mix with M^T (d in) and the weight gradient dM[o, i] = sum_{b, n} d out[b, o, n] in[b, i, n]. */
+void gspn_oracle_proxy_mix(const double* in, const double* M, double* out, int64_t B, int64_t Ci, int64_t Co,
+                           int64_t HW) {
+  for (int64_t b = 0; b < B; ++b)
+    for (int64_t o = 0; o < Co; ++o)
+      for (int64_t n = 0; n < HW; ++n) {
+        double acc = 0.0;
+        for (int64_t i = 0; i < Ci; ++i) acc += M[o * Ci + i] * in[(b * Ci + i) * HW + n];
+        out[(b * Co + o) * HW + n] = acc;
+      }
+}
+
+void gspn_oracle_proxy_wgrad(const double* dout, const double* in, double* dM, int64_t B, int64_t Ci, int64_t Co,
+                             int64_t HW) {
+  for (int64_t o = 0; o < Co; ++o)
+    for (int64_t i = 0; i < Ci; ++i) {
+      double acc = 0.0;
+      for (int64_t b = 0; b < B; ++b)
+        for (int64_t n = 0; n < HW; ++n) acc += dout[(b * Co + o) * HW + n] * in[(b * Ci + i) * HW + n];
+      dM[o * Ci + i] = acc;
+    }
+}

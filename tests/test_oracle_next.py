@@ -189,3 +189,76 @@ def test_merge_backward_matches_finite_differences():
             flat[i] = old
             fd.reshape(-1)[i] = (lp - lm) / (2 * eps)
         assert np.abs(fd - grad).max() < 1e-8
+
+
+# ------------------------------------------------------------------------------------ NEXT-4 proxy
+
+def test_proxy_identity_and_permutation():
+    """M = I copies the channels; a permutation matrix permutes them (exact)."""
+    rng = np.random.default_rng(13)
+    x = rng.uniform(-1, 1, (2, 5, 3, 4))
+    assert np.array_equal(oracle.proxy_mix(x, np.eye(5)), x)
+    perm = [3, 0, 4, 1, 2]
+    assert np.array_equal(oracle.proxy_mix(x, np.eye(5)[perm]), x[:, perm])
+
+
+def test_proxy_matches_einsum_and_roundtrip():
+    """Against numpy's einsum (a library primitive), and down-then-up with P_up = pinv(P_down) is the
+    orthogonal projection onto the proxy subspace (idempotent; identity when C_proxy = C)."""
+    rng = np.random.default_rng(14)
+    x = rng.uniform(-1, 1, (3, 12, 5, 7))
+    P = rng.normal(size=(4, 12))
+    xp = oracle.proxy_mix(x, P)
+    assert np.allclose(xp, np.einsum("pc,bchw->bphw", P, x), atol=1e-12)
+    Q = np.linalg.pinv(P)
+    y = oracle.proxy_mix(xp, Q)
+    assert np.allclose(oracle.proxy_mix(oracle.proxy_mix(y, P), Q), y, atol=1e-10)
+    Pf = rng.normal(size=(12, 12))
+    assert np.allclose(oracle.proxy_mix(oracle.proxy_mix(x, Pf), np.linalg.inv(Pf)), x, atol=1e-9)
+
+
+def test_proxy_adjoint_and_weight_gradient():
+    """<dout, M x> = <M^T dout, x> = <dM, M> with dM = wgrad(dout, x); finite differences on M."""
+    rng = np.random.default_rng(15)
+    x = rng.uniform(-1, 1, (2, 6, 3, 5))
+    M = rng.normal(size=(3, 6))
+    dout = rng.uniform(-1, 1, (2, 3, 3, 5))
+    ref = float(np.sum(dout * oracle.proxy_mix(x, M)))
+    assert abs(float(np.sum(oracle.proxy_mix(dout, M.T) * x)) - ref) < 1e-12
+    dM = oracle.proxy_wgrad(dout, x)
+    assert abs(float(np.sum(dM * M)) - ref) < 1e-12
+    eps = 1e-6
+    fd = np.zeros_like(M)
+    for idx in np.ndindex(M.shape):
+        Mp, Mm = M.copy(), M.copy()
+        Mp[idx] += eps
+        Mm[idx] -= eps
+        fd[idx] = (np.sum(dout * oracle.proxy_mix(x, Mp)) - np.sum(dout * oracle.proxy_mix(x, Mm))) / (2 * eps)
+    assert np.abs(fd - dM).max() < 1e-8
+
+
+def test_compact_block_linear_attention_rank():
+    """The compact block: down-project, scan with one shared affinity (G = 1), up-project.
+    With lam = 1 it is linear in x with rank <= C_proxy per pixel pair -- the low-rank structure of
+    PAPER.md:644 ('analogous to low-rank matrix factorization')."""
+    rng = np.random.default_rng(16)
+    B, C, Cp, H, W = 1, 6, 2, 3, 3
+    P = rng.normal(size=(Cp, C))
+    Q = rng.normal(size=(C, Cp))
+    wl, wm, wr = (rng.uniform(0.05, 1, (4, B, 1, H, W)) for _ in range(3))
+    lam = np.ones((4, B, Cp, H, W))
+
+    def block(x):
+        h = oracle.fwd(oracle.proxy_mix(x, P), wl, wm, wr, lam, 0xF, 1)
+        return oracle.proxy_mix(h.sum(axis=0), Q)
+
+    # Jacobian block between input pixel q and output pixel p is C x C of rank <= Cp
+    cols = []
+    for k in range(C * H * W):
+        e = np.zeros(C * H * W)
+        e[k] = 1.0
+        cols.append(block(e.reshape(B, C, H, W)).reshape(-1))
+    J = np.array(cols).T.reshape(C, H * W, C, H * W)
+    for p_ in range(H * W):
+        for q in range(H * W):
+            assert np.linalg.matrix_rank(J[:, p_, :, q], tol=1e-9) <= Cp
