@@ -146,6 +146,29 @@ gspn_status_t gspn_merge_bwd(const void* h, const void* u, const void* dy, void*
                              int64_t H, int64_t W, uint32_t dirs, gspn_dtype_t dtype, uint32_t flags,
                              gspn_stream_t stream);
 
+/*
+ * Compact-channel proxy projections (§4.2 "project the input tensor
+ * x in R^{N x C x H x W} into a lower-dimensional proxy subspace x_proxy in R^{N x C_proxy x H x W}",
+ * PAPER.md:172 "expand back to C with a learned 1x1 projection"). A 1x1 projection mixes channels at
+ * every pixel:
+ *     out[b, o, :] = sum_i M[o, i] in[b, i, :]      in [B, Ci, H, W] -> out [B, Co, H, W]
+ *   M [Co, Ci] row-major in dtype, or, with GSPN_FLAG_PROXY_TRANSPOSE, M stored [Ci, Co] (its transpose
+ *   is used): the data gradient of a projection by M is the projection of the upstream gradient by M^T.
+ *   Down-projection: M = P_down [C_proxy, C]; up-projection: M = P_up [C, C_proxy]. fp32 accumulation.
+ *   H*W must be even; Co*Ci <= 49152 (M staged in shared memory). One launch.
+ */
+#define GSPN_FLAG_PROXY_TRANSPOSE 0x8u
+gspn_status_t gspn_proxy_mix(const void* in, const void* M, void* out, int64_t B, int64_t Ci, int64_t Co, int64_t H,
+                             int64_t W, gspn_dtype_t dtype, uint32_t flags, gspn_stream_t stream);
+/*
+ * Weight gradient of gspn_proxy_mix:  dM[o, i] = sum_{b, pixels} dout[b, o, :] . in[b, i, :]
+ *   dout [B, Co, H, W], in [B, Ci, H, W] (dtype) -> dM [Co, Ci] in FP32 (overwritten; a reduction over
+ *   B H W terms). (Co + Ci) * 32 + Co * Ci <= 49152. A memset and one launch (fp32 atomics across CTAs,
+ *   so the summation order -- not the result beyond fp32 rounding -- varies between runs).
+ */
+gspn_status_t gspn_proxy_wgrad(const void* dout, const void* in, float* dM, int64_t B, int64_t Ci, int64_t Co,
+                               int64_t H, int64_t W, gspn_dtype_t dtype, gspn_stream_t stream);
+
 const char* gspn_status_string(gspn_status_t s);
 /* Thread-local detail string of the last failing call on this thread (names the offending argument). */
 const char* gspn_last_error_detail(void);

@@ -8,6 +8,8 @@ stream; every step of the scan runs in the CUDA kernels of libgspn.so. No CPU fa
   fwd(..., kchunk=k) / bwd(..., kchunk=k)                (GSPN-local, P:91-92)
   merge_fwd(h, u, dirs, mean=False) -> y               (output gate + direction merge, Eq. 2)
   merge_bwd(h, u, dy, dirs, mean=False) -> (dh, du)
+  proxy_mix(inp, M, transpose=False) -> out             (1x1 proxy projection)
+  proxy_wgrad(dout, inp) -> dM (fp32)
 
 Shapes (gspn.h): x [B,C,H,W]; w_* [D,B,G,H,W]; lam, h, dh, dlam [D,B,C,H,W]; dx [B,C,H,W].
 """
@@ -21,6 +23,7 @@ DIR_T2B, DIR_B2T, DIR_L2R, DIR_R2L, DIR_ALL = 0x1, 0x2, 0x4, 0x8, 0xF
 FLAG_PRENORMALIZED = 0x1
 FLAG_FORCE_GENERIC = 0x2
 FLAG_MERGE_MEAN = 0x4
+FLAG_PROXY_TRANSPOSE = 0x8
 DTYPE_F32, DTYPE_BF16 = 0, 1
 
 
@@ -142,3 +145,35 @@ def merge_bwd(h, u, dy, dirs: int = DIR_ALL, mean: bool = False, outs=None, stre
     check(lib().gspn_merge_bwd(h.data_ptr(), u.data_ptr(), dy.data_ptr(), dh.data_ptr(), du.data_ptr(), B, C, H, W,
                                dirs, _dtype_code(h), FLAG_MERGE_MEAN if mean else 0, _stream_ptr(stream, h.device)))
     return dh, du
+
+
+def proxy_mix(inp, M, transpose: bool = False, out=None, stream=None):
+    """out [B,Co,H,W] = sum_i M[o,i] inp[b,i]; M [Co, Ci] (or [Ci, Co] used transposed)."""
+    torch = _torch()
+    B, Ci, H, W = inp.shape
+    if transpose:
+        if M.shape[0] != Ci:
+            raise ValueError(f"M {tuple(M.shape)} (transposed) does not match Ci={Ci}")
+        Co = M.shape[1]
+    else:
+        if M.shape[1] != Ci:
+            raise ValueError(f"M {tuple(M.shape)} does not match Ci={Ci}")
+        Co = M.shape[0]
+    out = torch.empty((B, Co, H, W), dtype=inp.dtype, device=inp.device) if out is None else out
+    _check_tensors([("in", inp), ("M", M), ("out", out)], inp.dtype, inp.device)
+    check(lib().gspn_proxy_mix(inp.data_ptr(), M.data_ptr(), out.data_ptr(), B, Ci, Co, H, W, _dtype_code(inp),
+                               FLAG_PROXY_TRANSPOSE if transpose else 0, _stream_ptr(stream, inp.device)))
+    return out
+
+
+def proxy_wgrad(dout, inp, out=None, stream=None):
+    """dM [Co, Ci] (float32) = sum_{b,pixels} dout[b,o] . inp[b,i]."""
+    torch = _torch()
+    B, Co, H, W = dout.shape
+    Ci = inp.shape[1]
+    dM = torch.empty((Co, Ci), dtype=torch.float32, device=dout.device) if out is None else out
+    _check_tensors([("dout", dout), ("in", inp)], dout.dtype, dout.device)
+    _check_tensors([("dM", dM)], torch.float32, dout.device)
+    check(lib().gspn_proxy_wgrad(dout.data_ptr(), inp.data_ptr(), dM.data_ptr(), B, Ci, Co, H, W, _dtype_code(dout),
+                                 _stream_ptr(stream, dout.device)))
+    return dM

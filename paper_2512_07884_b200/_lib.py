@@ -51,6 +51,11 @@ def lib() -> ctypes.CDLL:
             L.gspn_merge_fwd.restype = ctypes.c_int
             L.gspn_merge_bwd.argtypes = [vp] * 5 + [i64] * 4 + [u32, ctypes.c_int, u32, vp]
             L.gspn_merge_bwd.restype = ctypes.c_int
+        if hasattr(L, "gspn_proxy_mix"):
+            L.gspn_proxy_mix.argtypes = [vp] * 3 + [i64] * 5 + [ctypes.c_int, u32, vp]
+            L.gspn_proxy_mix.restype = ctypes.c_int
+            L.gspn_proxy_wgrad.argtypes = [vp] * 3 + [i64] * 5 + [ctypes.c_int, vp]
+            L.gspn_proxy_wgrad.restype = ctypes.c_int
         L.gspn_status_string.argtypes = [ctypes.c_int]
         L.gspn_status_string.restype = ctypes.c_char_p
         L.gspn_last_error_detail.restype = ctypes.c_char_p

@@ -381,4 +381,56 @@ gspn_status_t gspn_merge_bwd(const void* h, const void* u, const void* dy, void*
   });
 }
 
+
+gspn_status_t gspn_proxy_mix(const void* in, const void* M, void* out, int64_t B, int64_t Ci, int64_t Co, int64_t H,
+                             int64_t W, gspn_dtype_t dtype, uint32_t flags, gspn_stream_t stream) {
+  return guarded([&]() -> gspn_status_t {
+    gspn_status_t st;
+    if ((st = check_ptr(in, "in")) || (st = check_ptr(M, "M")) || (st = check_ptr(out, "out"))) return st;
+    if (flags & ~GSPN_FLAG_PROXY_TRANSPOSE) return fail(GSPN_ERR_INVALID_ARG, "%s has unknown bits (0x%llx)", "flags", flags);
+    if ((st = check_dims(B, Ci, H, W, 1, 1, dtype, 0))) return st;
+    if (Co < 1) return fail(GSPN_ERR_INVALID_ARG, "%s must be >= 1 (got %lld)", "Co", Co);
+    if ((H * W) % 2 != 0) return fail(GSPN_ERR_UNSUPPORTED, "%s: H*W must be even (got %lld)", "shape", H * W);
+    if (Ci * Co > 49152) return fail(GSPN_ERR_UNSUPPORTED, "%s: Co*Ci above 49152 (%lld)", "M", Ci * Co);
+    const size_t s = dtype == GSPN_BF16 ? 2 : 4;
+    const Span ins[2] = {span("in", in, (size_t)(B * Ci * H * W) * s), span("M", M, (size_t)(Ci * Co) * s)};
+    const Span outs[1] = {span("out", out, (size_t)(B * Co * H * W) * s)};
+    if ((st = check_aliasing(outs, 1, ins, 2))) return st;
+    const cudaError_t e = gspn::launch_proxy_mix(in, M, out, B, Ci, Co, H * W, flags & GSPN_FLAG_PROXY_TRANSPOSE, dtype,
+                                                 reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) {
+      snprintf(t_detail, sizeof t_detail, "CUDA error: %s", cudaGetErrorString(e));
+      return GSPN_ERR_CUDA;
+    }
+    t_path = "proxy";
+    t_launches = 1;
+    return GSPN_OK;
+  });
+}
+
+gspn_status_t gspn_proxy_wgrad(const void* dout, const void* in, float* dM, int64_t B, int64_t Ci, int64_t Co,
+                               int64_t H, int64_t W, gspn_dtype_t dtype, gspn_stream_t stream) {
+  return guarded([&]() -> gspn_status_t {
+    gspn_status_t st;
+    if ((st = check_ptr(dout, "dout")) || (st = check_ptr(in, "in")) || (st = check_ptr(dM, "dM"))) return st;
+    if ((st = check_dims(B, Ci, H, W, 1, 1, dtype, 0))) return st;
+    if (Co < 1) return fail(GSPN_ERR_INVALID_ARG, "%s must be >= 1 (got %lld)", "Co", Co);
+    if ((Co + Ci) * 32 + Co * Ci > 49152)
+      return fail(GSPN_ERR_UNSUPPORTED, "%s: (Co+Ci)*32 + Co*Ci above 49152 (Co*Ci = %lld)", "shape", Ci * Co);
+    const size_t s = dtype == GSPN_BF16 ? 2 : 4;
+    const Span ins[2] = {span("dout", dout, (size_t)(B * Co * H * W) * s), span("in", in, (size_t)(B * Ci * H * W) * s)};
+    const Span outs[1] = {span("dM", dM, (size_t)(Ci * Co) * sizeof(float))};
+    if ((st = check_aliasing(outs, 1, ins, 2))) return st;
+    const cudaError_t e = gspn::launch_proxy_wgrad(dout, in, dM, B, Ci, Co, H * W, dtype,
+                                                   reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) {
+      snprintf(t_detail, sizeof t_detail, "CUDA error: %s", cudaGetErrorString(e));
+      return GSPN_ERR_CUDA;
+    }
+    t_path = "proxy";
+    t_launches = 1;
+    return GSPN_OK;
+  });
+}
+
 }  // extern "C"

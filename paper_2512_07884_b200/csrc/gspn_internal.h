@@ -32,4 +32,12 @@ cudaError_t launch_merge_fwd(const void* h, const void* u, void* y, int64_t N, i
 cudaError_t launch_merge_bwd(const void* h, const void* u, const void* dy, void* dh, void* du, int64_t N, int D,
                              bool mean, gspn_dtype_t dt, cudaStream_t st);
 
+// Proxy projections (gspn_proxy.cu).
+size_t proxy_mix_smem(int64_t Ci, int64_t Co);
+size_t proxy_wgrad_smem(int64_t Ci, int64_t Co);
+cudaError_t launch_proxy_mix(const void* in, const void* M, void* out, int64_t B, int64_t Ci, int64_t Co, int64_t HW,
+                             bool trans, gspn_dtype_t dt, cudaStream_t s);
+cudaError_t launch_proxy_wgrad(const void* dout, const void* in, float* dM, int64_t B, int64_t Ci, int64_t Co,
+                               int64_t HW, gspn_dtype_t dt, cudaStream_t s);
+
 }  // namespace gspn

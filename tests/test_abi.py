@@ -151,3 +151,18 @@ def test_merge_validation():
     assert L.gspn_merge_bwd(h, u, None, dh, du, 1, 4, 8, 8, 0xF, 1, 0, None) == 1 and "dy is NULL" in detail()
     assert L.gspn_merge_bwd(h, u, dy, dh, dh + 16, 1, 4, 8, 8, 0xF, 1, 4, None) == 1 and "overlaps" in detail()
     assert L.gspn_merge_bwd(h, u, dy, u, du, 1, 4, 8, 8, 0xF, 1, 4, None) == 1 and "overlaps" in detail()
+
+
+def test_proxy_validation():
+    """gspn_proxy_mix / gspn_proxy_wgrad (1x1 proxy projections) validate before any CUDA call."""
+    L = gspn.lib()
+    base = 1 << 30
+    i, m, o = A, A + base, A + 2 * base
+    assert L.gspn_proxy_mix(None, m, o, 2, 384, 8, 28, 28, 1, 0, None) == 1 and "in is NULL" in detail()
+    assert L.gspn_proxy_mix(i, m + 4, o, 2, 384, 8, 28, 28, 1, 0, None) == 1 and "M is not 16-byte" in detail()
+    assert L.gspn_proxy_mix(i, m, o, 2, 384, 0, 28, 28, 1, 0, None) == 1 and "Co must be" in detail()
+    assert L.gspn_proxy_mix(i, m, o, 2, 384, 8, 28, 28, 1, 0x1, None) == 1 and "flags" in detail()
+    assert L.gspn_proxy_mix(i, m, o, 2, 384, 8, 5, 5, 1, 0, None) == 2 and "even" in detail()
+    assert L.gspn_proxy_mix(i, m, i + 32, 2, 384, 8, 28, 28, 1, 0, None) == 1 and "overlaps" in detail()
+    assert L.gspn_proxy_wgrad(i, m, None, 2, 384, 8, 28, 28, 1, None) == 1 and "dM is NULL" in detail()
+    assert L.gspn_proxy_wgrad(i, m, o, 2, 4096, 64, 28, 28, 1, None) == 2

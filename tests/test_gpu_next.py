@@ -284,3 +284,53 @@ def test_small_plane_parity(case):
                 assert normwise(a[s], r[s]) <= tol, f"{name} slab {s}"
         else:
             assert normwise(a, r) <= tol, name
+
+
+# ------------------------------------------------------------------- NEXT-4 proxy projections
+
+# (B, C, C_proxy, H, W, dtype): BASELINE configs[2] (384 -> 8, 28 x 28) and a configs[4]-like 320 -> 40
+PROXY_CASES = [
+    (64, 384, 8, 28, 28, "bf16"),
+    (2, 320, 40, 16, 24, "bf16"),
+    (3, 24, 5, 7, 6, "f32"),
+    (1, 8, 8, 4, 4, "f32"),
+]
+
+
+@pytest.mark.parametrize("case", PROXY_CASES, ids=lambda c: "B{}C{}Cp{}H{}W{}{}".format(*c))
+def test_proxy_parity(case):
+    """down (P [Cp, C]), up (Q [C, Cp]), the data gradients (transposed mixes) and both weight gradients
+    against the fp64 oracle on host-generated inputs and weights."""
+    import torch
+
+    B, C, Cp, H, W, dt = case
+    rng = np.random.default_rng(C + Cp)
+    dtype = torch.bfloat16 if dt == "bf16" else torch.float32
+    dev = _dev()
+
+    def mk(shape, scale=1.0):
+        a = torch.from_numpy(rng.uniform(-scale, scale, shape)).to(dtype)
+        return a.to(dev), a.double().numpy()
+
+    x, xf = mk((B, C, H, W))
+    P, Pf = mk((Cp, C), 1.0 / np.sqrt(C))
+    Q, Qf = mk((C, Cp), 1.0 / np.sqrt(Cp))
+    dy, dyf = mk((B, C, H, W))
+    xp = gspn.proxy_mix(x, P)
+    assert gspn.last_path() == "proxy"
+    y = gspn.proxy_mix(xp, Q)
+    dxp = gspn.proxy_mix(dy, Q, transpose=True)           # d(up)/d(input) = Q^T dy
+    dx = gspn.proxy_mix(dxp, P, transpose=True)           # d(down)/d(input) = P^T dxp
+    dQ = gspn.proxy_wgrad(dy, xp)
+    dP = gspn.proxy_wgrad(dxp, x)
+    torch.cuda.synchronize()
+    tol = TOL[dt]
+    xp_ref = oracle.proxy_mix(xf, Pf)
+    xp_st = from_torch(xp)                                # downstream refs on the stored-dtype values (R18)
+    assert normwise(xp_st, xp_ref) <= tol
+    assert normwise(from_torch(y), oracle.proxy_mix(xp_st, Qf)) <= tol
+    dxp_st = from_torch(dxp)
+    assert normwise(dxp_st, oracle.proxy_mix(dyf, Qf.T)) <= tol
+    assert normwise(from_torch(dx), oracle.proxy_mix(dxp_st, Pf.T)) <= tol
+    assert normwise(from_torch(dQ), oracle.proxy_wgrad(dyf, xp_st)) <= tol
+    assert normwise(from_torch(dP), oracle.proxy_wgrad(dxp_st, xf)) <= tol
