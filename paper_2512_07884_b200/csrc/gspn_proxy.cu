@@ -87,6 +87,65 @@ __global__ void __launch_bounds__(256) mix_kernel(const T* __restrict__ in, cons
   }
 }
 
+// Down-projection shape (Co <= kOB, Ci >= 64): the Ci reduction is split over kKS thread slices of a
+// CTA (each slice sums Ci / kKS channels for the same 32 pixel pairs), partial sums meet in shared
+// memory -- 8x the threads of mix_kernel, whose per-thread Ci loop was latency-bound at 98 CTAs.
+constexpr int kKS = 8;
+template <typename T, bool kTrans>
+__global__ void __launch_bounds__(256) mix_splitk_kernel(const T* __restrict__ in, const T* __restrict__ M,
+                                                         T* __restrict__ out, int B, int Ci, int Co, int HW) {
+  extern __shared__ float Ms[];  // [Co][Ci] fp32, then partials [kKS][kOB][64]
+  float* part = Ms + Co * Ci;
+  for (int e = threadIdx.x; e < Co * Ci; e += blockDim.x) {
+    const int o = e / Ci, i = e - o * Ci;
+    Ms[e] = to_f(kTrans ? M[i * Co + o] : M[e]);
+  }
+  const int npair = HW / 2;
+  const int nblk = (npair + 31) / 32;  // 32 pixel pairs per CTA iteration
+  const int ks = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cs = (Ci + kKS - 1) / kKS, i0 = ks * cs, i1 = min(Ci, i0 + cs);
+  for (int64_t blk = blockIdx.x; blk < static_cast<int64_t>(B) * nblk; blk += gridDim.x) {
+    const int b = static_cast<int>(blk / nblk), pb = static_cast<int>(blk % nblk);
+    const int pp = pb * 32 + lane;
+    float acc[kOB][2];
+#pragma unroll
+    for (int q = 0; q < kOB; ++q) acc[q][0] = acc[q][1] = 0.f;
+    __syncthreads();  // Ms staged / previous iteration's partials consumed
+    if (pp < npair) {
+      const T* src = in + static_cast<int64_t>(b) * Ci * HW + 2 * pp;
+#pragma unroll 4
+      for (int i = i0; i < i1; ++i) {
+        float a0, a1;
+        Pair<T>::ld(src + static_cast<int64_t>(i) * HW, a0, a1);
+#pragma unroll
+        for (int q = 0; q < kOB; ++q) {
+          const float m = q < Co ? Ms[q * Ci + i] : 0.f;
+          acc[q][0] = fmaf(m, a0, acc[q][0]);
+          acc[q][1] = fmaf(m, a1, acc[q][1]);
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kOB; ++q) {
+      part[(ks * kOB + q) * 64 + 2 * lane] = acc[q][0];
+      part[(ks * kOB + q) * 64 + 2 * lane + 1] = acc[q][1];
+    }
+    __syncthreads();
+    // 256 threads finish kOB x 64 outputs: thread -> (q, pixel pair)
+    for (int e = threadIdx.x; e < kOB * 32; e += blockDim.x) {
+      const int q = e >> 5, l = e & 31, p2 = pb * 32 + l;
+      if (q >= Co || p2 >= npair) continue;
+      float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+      for (int k = 0; k < kKS; ++k) {
+        s0 += part[(k * kOB + q) * 64 + 2 * l];
+        s1 += part[(k * kOB + q) * 64 + 2 * l + 1];
+      }
+      Pair<T>::st(out + (static_cast<int64_t>(b) * Co + q) * HW + 2 * p2, s0, s1);
+    }
+  }
+}
+
 constexpr int kPT = 32;  // pixels per wgrad tile
 
 template <typename T>
@@ -102,17 +161,23 @@ __global__ void __launch_bounds__(256) wgrad_kernel(const T* __restrict__ dout, 
   const int64_t npx = static_cast<int64_t>(B) * HW;
   const int64_t p0 = blockIdx.x * px_per_cta;
   const int64_t p1 = p0 + px_per_cta < npx ? p0 + px_per_cta : npx;
+  __shared__ int64_t offo[kPT], offi[kPT];  // per tile slot: element offset of channel 0 in dout / in
   for (int64_t base = p0; base < p1; base += kPT) {
     const int n = static_cast<int>(p1 - base < kPT ? p1 - base : kPT);
     __syncthreads();
+    if (threadIdx.x < kPT) {
+      const int64_t gp = base + threadIdx.x;  // flat (b, pixel): one division per slot, not per element
+      const int64_t b = gp / HW, px = gp - b * HW;
+      offo[threadIdx.x] = b * Co * HW + px;
+      offi[threadIdx.x] = b * Ci * HW + px;
+    }
+    __syncthreads();
     for (int e = threadIdx.x; e < (Co + Ci) * kPT; e += blockDim.x) {
-      const int ch = e / kPT, k = e - ch * kPT;
+      const int ch = e >> 5, k = e & (kPT - 1);  // kPT = 32
       float v = 0.f;
-      if (k < n) {
-        const int64_t gp = base + k;  // flat (b, pixel)
-        const int64_t b = gp / HW, px = gp - b * HW;
-        v = ch < Co ? to_f(dout[(b * Co + ch) * HW + px]) : to_f(in[(b * Ci + (ch - Co)) * HW + px]);
-      }
+      if (k < n)
+        v = ch < Co ? to_f(dout[offo[k] + static_cast<int64_t>(ch) * HW])
+                    : to_f(in[offi[k] + static_cast<int64_t>(ch - Co) * HW]);
       sm[e] = v;  // so and si are contiguous: channel ch of the stacked [Co + Ci][kPT] tile
     }
     __syncthreads();
@@ -143,6 +208,17 @@ int sms() {
 
 template <typename T>
 cudaError_t mix_t(const void* in, const void* M, void* out, int B, int Ci, int Co, int HW, bool trans, cudaStream_t s) {
+  if (Co <= kOB && Ci >= 64) {
+    const size_t smem = (static_cast<size_t>(Co) * Ci + kKS * kOB * 64) * sizeof(float);
+    auto k = trans ? mix_splitk_kernel<T, true> : mix_splitk_kernel<T, false>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    const int64_t nblk = static_cast<int64_t>(B) * ((HW / 2 + 31) / 32);
+    const int64_t cap = static_cast<int64_t>(sms()) * 8;
+    k<<<static_cast<unsigned>(nblk < cap ? nblk : cap), 256, smem, s>>>(
+        static_cast<const T*>(in), static_cast<const T*>(M), static_cast<T*>(out), B, Ci, Co, HW);
+    return cudaGetLastError();
+  }
   const size_t smem = static_cast<size_t>(Co) * Ci * sizeof(float);
   auto k = trans ? mix_kernel<T, true> : mix_kernel<T, false>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -175,7 +251,7 @@ cudaError_t wgrad_t(const void* dout, const void* in, float* dM, int B, int Ci, 
 
 }  // namespace
 
-size_t proxy_mix_smem(int64_t Ci, int64_t Co) { return static_cast<size_t>(Ci * Co) * sizeof(float); }
+size_t proxy_mix_smem(int64_t Ci, int64_t Co) { return static_cast<size_t>(Ci * Co + kKS * kOB * 64) * sizeof(float); }
 size_t proxy_wgrad_smem(int64_t Ci, int64_t Co) {
   return (static_cast<size_t>(Co + Ci) * kPT + static_cast<size_t>(Co * Ci)) * sizeof(float);
 }
