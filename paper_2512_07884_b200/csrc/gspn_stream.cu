@@ -1194,7 +1194,6 @@ __device__ void producer_fused(const StreamArgs& A, uint8_t* ring, uint64_t* ful
   uint32_t phase = 0;
   for (int64_t w = blockIdx.x; w < pl.nchains; w += gridDim.x) {
     const Chain ch = make_chain<false>(A.p, pl, w);
-    const int o = ch.vert ? 0 : 1;
     const int chain = static_cast<int>(ch.chain);
     for (int jj = 0; jj < ch.ntiles; ++jj) {
       const int j = ch.ntiles - 1 - jj;
@@ -1206,7 +1205,10 @@ __device__ void producer_fused(const StreamArgs& A, uint8_t* ring, uint64_t* ful
       const uint64_t pol = ch.vert ? pol_vin : pol_hin;
       for (int t = 0; t < B_NIN; ++t) {
         const uint32_t dst = st + t * pl.tile_bytes;
-        if (ch.vert) {
+        if (pl.npack > 1) {  // packed chains: one 3D box, vertical (W, planes, rows), horizontal (cols, H, planes)
+          if (ch.vert) tma_load3(dst, &A.in[0][t], 0, chain, s0, fb, pol);
+          else tma_load3(dst, &A.in[1][t], s0, 0, chain, fb, pol);
+        } else if (ch.vert) {
           for (int q = 0; q < pl.nbw; ++q)
             tma_load3(dst + q * pl.K * pl.bw * pl.es, &A.in[0][t], q * pl.bw, s0, chain, fb, pol);
         } else {
@@ -1217,8 +1219,12 @@ __device__ void producer_fused(const StreamArgs& A, uint8_t* ring, uint64_t* ful
       if (ch.vert) {  // h rows one step earlier: T2B row - 1, B2T row + 1 (out of range: zero = h_{-1})
         const int sh = ch.rev ? s0 + 1 : s0 - 1;
         const uint32_t dst = st + B_H0 * pl.tile_bytes;
-        for (int q = 0; q < pl.nbw; ++q)
-          tma_load3(dst + q * pl.K * pl.bw * pl.es, &A.in[0][B_H0], q * pl.bw, sh, chain, fb, pol);
+        if (pl.npack > 1) {
+          tma_load3(dst, &A.in[0][B_H0], 0, chain, sh, fb, pol);
+        } else {
+          for (int q = 0; q < pl.nbw; ++q)
+            tma_load3(dst + q * pl.K * pl.bw * pl.es, &A.in[0][B_H0], q * pl.bw, sh, chain, fb, pol);
+        }
       } else if (pl.fuse_h) {  // this tile's columns and the neighbouring tile towards step t-1 (zero fill)
         const int sn = ch.rev ? s0 + pl.K : s0 - pl.K;
         for (int q = 0; q < pl.nbh; ++q) {
@@ -2562,10 +2568,12 @@ bool launch_bwd_fused(const ScanParams& p0, gspn_dtype_t dt, cudaStream_t s, int
   const bool fuse_h = getenv("GSPN_FUSE_H") != nullptr;
   if (!make_plan(p, dt, fuse_h ? B_NINF : B_NIN + 1, &A.plan)) return false;
   Plan& pl = A.plan;
-  if (pl.npack > 1 || pl.cl > 1) return false;
+  if (pl.cl > 1 || (fuse_h && pl.npack > 1) || (getenv("GSPN_NOFUSE_PACKED") && pl.npack > 1)) return false;
   pl.fuse_h = fuse_h ? 1 : 0;
-  pl.tx_v = static_cast<uint32_t>((B_NIN + 1) * pl.nbw * pl.bw * pl.K * es);  // vertical: no B_H1 tile
-  if (!fuse_h) pl.tx_h = static_cast<uint32_t>(B_NIN * pl.nbh * pl.bh * 32);  // horizontal: dh and w only
+  // make_plan counted pl.nin tiles per stage for both orientations: vertical loads B_NIN + 1 (no B_H1),
+  // horizontal B_NIN (dh, w) unless fully fused
+  pl.tx_v = pl.tx_v / pl.nin * (B_NIN + 1);
+  if (!fuse_h) pl.tx_h = pl.tx_h / pl.nin * B_NIN;
   const WsLayout l = ws_layout(p.B, p.C, p.H, p.W, p.D, dt);
   if (p.ws == nullptr || p.ws_bytes < l.total) return false;
   A.g = static_cast<char*>(p.ws) + l.g;
