@@ -207,6 +207,10 @@ FUSED_SHAPES = [
     (1, 2, 2, 512, 512, 0xF, "bf16"),
     (1, 2, 2, 257, 512, 0xC, "bf16"),
     (1, 2, 2, 512, 8, 0xF, "bf16"),
+    (1, 2, 2, 300, 264, 0x3, "bf16"),   # vertical directions only (the output kernel forms dlam, dx only)
+    (1, 2, 2, 264, 272, 0x1, "f32"),
+    (2, 4, 4, 56, 56, 0xF, "bf16"),     # packed small planes
+    (1, 6, 6, 40, 48, 0x6, "f32"),
 ]
 
 
