@@ -163,7 +163,7 @@ gspn_status_t gspn_proxy_mix(const void* in, const void* M, void* out, int64_t B
 /*
  * Weight gradient of gspn_proxy_mix:  dM[o, i] = sum_{b, pixels} dout[b, o, :] . in[b, i, :]
  *   dout [B, Co, H, W], in [B, Ci, H, W] (dtype) -> dM [Co, Ci] in FP32 (overwritten; a reduction over
- *   B H W terms). (Co + Ci) * 32 + Co * Ci <= 49152. A memset and one launch (fp32 atomics across CTAs,
+ *   B H W terms). (Co + Ci) * 33 + Co * Ci <= 49152. A memset and one launch (fp32 atomics across CTAs,
  *   so the summation order -- not the result beyond fp32 rounding -- varies between runs).
  */
 gspn_status_t gspn_proxy_wgrad(const void* dout, const void* in, float* dM, int64_t B, int64_t Ci, int64_t Co,

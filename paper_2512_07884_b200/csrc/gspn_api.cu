@@ -415,8 +415,8 @@ gspn_status_t gspn_proxy_wgrad(const void* dout, const void* in, float* dM, int6
     if ((st = check_ptr(dout, "dout")) || (st = check_ptr(in, "in")) || (st = check_ptr(dM, "dM"))) return st;
     if ((st = check_dims(B, Ci, H, W, 1, 1, dtype, 0))) return st;
     if (Co < 1) return fail(GSPN_ERR_INVALID_ARG, "%s must be >= 1 (got %lld)", "Co", Co);
-    if ((Co + Ci) * 32 + Co * Ci > 49152)
-      return fail(GSPN_ERR_UNSUPPORTED, "%s: (Co+Ci)*32 + Co*Ci above 49152 (Co*Ci = %lld)", "shape", Ci * Co);
+    if ((Co + Ci) * 33 + Co * Ci > 49152)
+      return fail(GSPN_ERR_UNSUPPORTED, "%s: (Co+Ci)*33 + Co*Ci above 49152 (Co*Ci = %lld)", "shape", Ci * Co);
     const size_t s = dtype == GSPN_BF16 ? 2 : 4;
     const Span ins[2] = {span("dout", dout, (size_t)(B * Co * H * W) * s), span("in", in, (size_t)(B * Ci * H * W) * s)};
     const Span outs[1] = {span("dM", dM, (size_t)(Ci * Co) * sizeof(float))};

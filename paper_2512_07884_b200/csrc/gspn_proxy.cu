@@ -146,16 +146,25 @@ __global__ void __launch_bounds__(256) mix_splitk_kernel(const T* __restrict__ i
   }
 }
 
-constexpr int kPT = 32;  // pixels per wgrad tile
+constexpr int kPT = 32;        // pixels per wgrad tile
+constexpr int kPTS = kPT + 1;  // staged row stride: odd, so threads on consecutive channels hit distinct banks
 
-template <typename T>
+// kSmall: 0 generic pair loop (shared accumulators); 1 Co <= 8 (down-projection weights); 2 Ci <= 8
+// (up-projection weights). kSlots: large-side channels per thread (large side <= kSlots * 256).
+constexpr int kSlots = 2;
+template <typename T, int kSmall>
 __global__ void __launch_bounds__(256) wgrad_kernel(const T* __restrict__ dout, const T* __restrict__ in,
                                                     float* __restrict__ dM, int B, int Ci, int Co, int HW,
                                                     int64_t px_per_cta) {
   extern __shared__ float sm[];
-  float* so = sm;                       // [Co][kPT]
-  float* si = so + Co * kPT;            // [Ci][kPT]
-  float* acc = si + Ci * kPT;           // [Co * Ci]
+  float racc[kSlots][8];
+#pragma unroll
+  for (int sl = 0; sl < kSlots; ++sl)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) racc[sl][q] = 0.f;
+  float* so = sm;                       // [Co][kPTS]
+  float* si = so + Co * kPTS;           // [Ci][kPTS]
+  float* acc = si + Ci * kPTS;          // [Co * Ci]
   const int npairs = Co * Ci;
   for (int e = threadIdx.x; e < npairs; e += blockDim.x) acc[e] = 0.f;
   const int64_t npx = static_cast<int64_t>(B) * HW;
@@ -178,18 +187,50 @@ __global__ void __launch_bounds__(256) wgrad_kernel(const T* __restrict__ dout, 
       if (k < n)
         v = ch < Co ? to_f(dout[offo[k] + static_cast<int64_t>(ch) * HW])
                     : to_f(in[offi[k] + static_cast<int64_t>(ch - Co) * HW]);
-      sm[e] = v;  // so and si are contiguous: channel ch of the stacked [Co + Ci][kPT] tile
+      sm[ch * kPTS + k] = v;  // so and si are contiguous: channel ch of the stacked [Co + Ci][kPTS] tile
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < npairs; e += blockDim.x) {
-      const int o = e / Ci, i = e - o * Ci;
-      const float* a = so + o * kPT;
-      const float* c = si + i * kPT;
-      float s = 0.f;
+    if (kSmall == 0) {
+      for (int e = threadIdx.x; e < npairs; e += blockDim.x) {
+        const int o = e / Ci, i = e - o * Ci;
+        const float* a = so + o * kPTS;
+        const float* c = si + i * kPTS;
+        float s = 0.f;
 #pragma unroll 8
-      for (int k = 0; k < kPT; ++k) s = fmaf(a[k], c[k], s);
-      acc[e] += s;
+        for (int k = 0; k < kPT; ++k) s = fmaf(a[k], c[k], s);
+        acc[e] += s;
+      }
+    } else {
+      // register-blocked: the small side (<= 8 channels) is read as broadcasts, each thread owns up to
+      // kSlots channels of the large side and all small-side partners, sums stay in registers
+      const int nsm = kSmall == 1 ? Co : Ci, nlg = kSmall == 1 ? Ci : Co;
+      const float* sml = kSmall == 1 ? so : si;
+      const float* lrg = kSmall == 1 ? si : so;
+#pragma unroll
+      for (int sl = 0; sl < kSlots; ++sl) {
+        const int l = threadIdx.x + sl * blockDim.x;
+        if (l >= nlg) break;
+#pragma unroll 4
+        for (int k = 0; k < kPT; ++k) {
+          const float c = lrg[l * kPTS + k];
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (q < nsm) racc[sl][q] = fmaf(sml[q * kPTS + k], c, racc[sl][q]);
+        }
+      }
     }
+  }
+  if (kSmall != 0) {
+    const int nsm = kSmall == 1 ? Co : Ci, nlg = kSmall == 1 ? Ci : Co;
+#pragma unroll
+    for (int sl = 0; sl < kSlots; ++sl) {
+      const int l = threadIdx.x + sl * blockDim.x;
+      if (l >= nlg) break;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (q < nsm) atomicAdd(dM + (kSmall == 1 ? q * Ci + l : l * Ci + q), racc[sl][q]);
+    }
+    return;
   }
   __syncthreads();
   for (int e = threadIdx.x; e < npairs; e += blockDim.x) atomicAdd(dM + e, acc[e]);
@@ -234,8 +275,10 @@ cudaError_t mix_t(const void* in, const void* M, void* out, int B, int Ci, int C
 
 template <typename T>
 cudaError_t wgrad_t(const void* dout, const void* in, float* dM, int B, int Ci, int Co, int HW, cudaStream_t s) {
-  const size_t smem = (static_cast<size_t>(Co + Ci) * kPT + static_cast<size_t>(Co) * Ci) * sizeof(float);
-  cudaError_t e = cudaFuncSetAttribute(wgrad_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  const size_t smem = (static_cast<size_t>(Co + Ci) * kPTS + static_cast<size_t>(Co) * Ci) * sizeof(float);
+  const int mode = (Co <= 8 && Ci <= kSlots * 256) ? 1 : (Ci <= 8 && Co <= kSlots * 256) ? 2 : 0;
+  auto kern = mode == 1 ? wgrad_kernel<T, 1> : mode == 2 ? wgrad_kernel<T, 2> : wgrad_kernel<T, 0>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   e = cudaMemsetAsync(dM, 0, static_cast<size_t>(Co) * Ci * sizeof(float), s);
   if (e != cudaSuccess) return e;
@@ -244,8 +287,8 @@ cudaError_t wgrad_t(const void* dout, const void* in, float* dM, int B, int Ci, 
   int64_t per = (npx + ctas - 1) / ctas;
   per = (per + kPT - 1) / kPT * kPT;
   ctas = (npx + per - 1) / per;
-  wgrad_kernel<T><<<static_cast<unsigned>(ctas), 256, smem, s>>>(static_cast<const T*>(dout), static_cast<const T*>(in),
-                                                                 dM, B, Ci, Co, HW, per);
+  kern<<<static_cast<unsigned>(ctas), 256, smem, s>>>(static_cast<const T*>(dout), static_cast<const T*>(in), dM, B, Ci,
+                                                      Co, HW, per);
   return cudaGetLastError();
 }
 
@@ -253,7 +296,7 @@ cudaError_t wgrad_t(const void* dout, const void* in, float* dM, int B, int Ci, 
 
 size_t proxy_mix_smem(int64_t Ci, int64_t Co) { return static_cast<size_t>(Ci * Co + kKS * kOB * 64) * sizeof(float); }
 size_t proxy_wgrad_smem(int64_t Ci, int64_t Co) {
-  return (static_cast<size_t>(Co + Ci) * kPT + static_cast<size_t>(Co * Ci)) * sizeof(float);
+  return (static_cast<size_t>(Co + Ci) * kPTS + static_cast<size_t>(Co * Ci)) * sizeof(float);
 }
 
 cudaError_t launch_proxy_mix(const void* in, const void* M, void* out, int64_t B, int64_t Ci, int64_t Co, int64_t HW,
