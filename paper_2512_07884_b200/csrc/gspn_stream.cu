@@ -224,6 +224,16 @@ __device__ __forceinline__ int tile_start(const Chain& ch, int j, int K) {
   return ch.vert ? (ch.L - (j + 1) * K) : (ch.ntiles - 1 - j) * K;
 }
 
+// A half-tile whose steps all lie outside [0, L) (the second half of a last partial tile, or for R2L the
+// zero-filled columns past W of the first tile) changes nothing: skip its arithmetic (uniform across the
+// CTA, so the edge exchange still runs). Vertical tiles start at the scan start; horizontal tiles sit on
+// the K-aligned column grid, and for both L2R and R2L a half is outside iff its first column is >= W.
+template <int K>
+__device__ __forceinline__ bool half_outside_k(const Chain& ch, int j, int half, int cm) {
+  if (ch.vert) return j * K + half * (K / 2) >= ch.L;
+  return tile_start(ch, j, K) + cm * (K / 2) >= ch.L;
+}
+
 // Input tensor slots.
 enum FwdIn { F_X = 0, F_LAM, F_WL, F_WM, F_WR, F_NIN };
 enum BwdIn { B_DH = 0, B_WL, B_WM, B_WR, B_NIN };
@@ -814,7 +824,8 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) fwd_stream_kernel(const
       for (int half = 0; half < 2; ++half) {
         uint4 OUT[kE];
         const int cm = ch.rev ? 1 - half : half;  // horizontal: memory chunk of this half
-        if (!pl.null_compute) {
+        const bool live = !pl.null_compute && !half_outside_k<C::K>(ch, j, half, cm);
+        if (live) {
           uint32_t rm = 0;
           if (ch.vert) {
             const int t0 = j * C::K + half * C::KS;
@@ -855,7 +866,7 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) fwd_stream_kernel(const
           xphase ^= 1u << par;
         }
         par ^= 1;
-        if (!ch.vert && !pl.null_compute) {  // new states in place over the x chunk of this half
+        if (!ch.vert && live) {  // new states in place over the x chunk of this half
 #pragma unroll
           for (int q = 0; q < kE; ++q)
             if (ln.own_h[q])
@@ -1000,7 +1011,8 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_stream_kernel(const
       for (int half = 1; half >= 0; --half) {
         uint4 OG[kE];
         const int cm = ch.rev ? 1 - half : half;
-        if (!pl.null_compute) {
+        const bool live = !pl.null_compute && !half_outside_k<C::K>(ch, j, half, cm);
+        if (live) {
           uint32_t rm = 0;
           if (ch.vert) {
             const int t0 = j * C::K + half * C::KS;          // first (lowest) step of the half
@@ -1050,7 +1062,7 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_stream_kernel(const
           xphase ^= 1u << par;
         }
         par ^= 1;
-        if (!ch.vert && !pl.null_compute) {
+        if (!ch.vert && live) {
 #pragma unroll
           for (int q = 0; q < kE; ++q)
             if (ln.own_h[q])
@@ -1302,7 +1314,8 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_fused_kernel(const 
       for (int half = 1; half >= 0; --half) {
         uint4 OG[kE];
         const int cm = ch.rev ? 1 - half : half;
-        if (!pl.null_compute) {
+        const bool live = !pl.null_compute && !half_outside_k<C::K>(ch, j, half, cm);
+        if (live) {
           if (ch.vert) {
             const int t0 = j * C::K + half * C::KS;
             const int tl = t0 + C::KS - 1;
@@ -1326,7 +1339,7 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_fused_kernel(const 
         edge_reload(m.edge + 1 * kXArr + par * kEdgeW * kXRow, xs, ch.vert, S.eb);
         edge_reload(m.edge + 2 * kXArr + par * kEdgeW * kXRow, xs, ch.vert, S.ec);
         par ^= 1;
-        if (!ch.vert && !pl.null_compute) {
+        if (!ch.vert && live) {
           if (pl.fuse_h) {  // tap gradients; g and dw in place over this half's dh / w chunks
             if (ch.rev) dw_half_horiz<T, kPre, true>(ln, st, cm, OG, hrow, hl, hr);
             else dw_half_horiz<T, kPre, false>(ln, st, cm, OG, hrow, hl, hr);
