@@ -450,7 +450,7 @@ def measure_next(args, gspn, cfg, sh, t, h, outs, ws, dev, stream):
 def run_e2e(args, gspn, cfg, sh, t, h, outs, ws, dev, world, dist):
     """Same metric through the public API with pinned HOST buffers: every step copies all of its inputs
     host->device, runs fwd + bwd, and copies every output device->host, inside the CUDA-event timed
-    region. The batch is streamed in per-b chunks (units are independent) through two
+    region. The batch is streamed in (b, group-block) chunks (units are independent) through two
     device buffer sets on three streams, so H2D of chunk k+1, compute of chunk k and D2H of chunk k-1
     overlap (PCIe is full duplex) -- the way a caller with host-resident data uses the API."""
     import torch
@@ -465,20 +465,31 @@ def run_e2e(args, gspn, cfg, sh, t, h, outs, ws, dev, world, dist):
     host_out = {n: torch.empty(full_out[n].shape, dtype=full_out[n].dtype, pin_memory=True) for n in onames}
     h2d = sum(v.numel() * v.element_size() for v in host_in.values())
     d2h = sum(v.numel() * v.element_size() for v in host_out.values())
-    B = sh.B
+    B, G = sh.B, sh.G
+    Cg = sh.C // sh.G
     dt_code = gspn.DTYPE_BF16 if cfg.dtype == "bf16" else gspn.DTYPE_F32
+    # chunks = (b, block of consecutive groups): ~16 per step, so the pipeline fill / drain is short
+    nsub = max(1, 16 // max(1, B))
+    while G % nsub:
+        nsub -= 1
+    gb = G // nsub
+    chunks = [(b, k * gb) for b in range(B) for k in range(nsub)]
 
-    def chunk_shape(x):  # [B, ...] -> [1, ...]; [D, B, ...] -> [D, 1, ...]
-        return (1,) + tuple(x.shape[1:]) if x.dim() == 4 else (x.shape[0], 1) + tuple(x.shape[2:])
+    wnames = {"w_l", "w_m", "w_r", "dw_l", "dw_m", "dw_r"}
 
-    def piece(x, b):  # contiguous pieces of batch b: one for [B,...], D for [D,B,...]
-        return [x[b]] if x.dim() == 4 else [x[d, b] for d in range(x.shape[0])]
+    def piece(x, b, g0, is_w):  # contiguous pieces of chunk (b, groups g0..g0+gb)
+        lo, hi = (g0, g0 + gb) if is_w else (g0 * Cg, (g0 + gb) * Cg)
+        return [x[b, lo:hi]] if x.dim() == 4 else [x[d, b, lo:hi] for d in range(x.shape[0])]
+
+    def dshape(x, is_w):
+        n = gb if is_w else gb * Cg
+        return (1, n) + tuple(x.shape[2:]) if x.dim() == 4 else (x.shape[0], 1, n) + tuple(x.shape[3:])
 
     bufs = []
     for _ in range(2):
-        bi = {n: torch.empty(chunk_shape(t[n]), dtype=t[n].dtype, device=dev) for n in names}
-        bo = {n: torch.empty(chunk_shape(full_out[n]), dtype=full_out[n].dtype, device=dev) for n in onames}
-        wsb = gspn.workspace_bytes(1, sh.C, cfg.H, cfg.W, cfg.dirs, sh.G, dt_code)
+        bi = {n: torch.empty(dshape(t[n], n in wnames), dtype=t[n].dtype, device=dev) for n in names}
+        bo = {n: torch.empty(dshape(full_out[n], n in wnames), dtype=full_out[n].dtype, device=dev) for n in onames}
+        wsb = gspn.workspace_bytes(1, gb * Cg, cfg.H, cfg.W, cfg.dirs, gb, dt_code)
         bufs.append((bi, bo, torch.empty(max(wsb, 16), dtype=torch.uint8, device=dev)))
     s_in, s_cmp, s_out = (torch.cuda.Stream(dev) for _ in range(3))
     ev = {k: [torch.cuda.Event() for _ in range(2)] for k in ("in", "cmp", "out")}
@@ -487,28 +498,28 @@ def run_e2e(args, gspn, cfg, sh, t, h, outs, ws, dev, world, dist):
             e.record(torch.cuda.current_stream(dev))
 
     def step():
-        for b in range(B):
-            j = b % 2
+        for ci, (b, g0) in enumerate(chunks):
+            j = ci % 2
             bi, bo, wsj = bufs[j]
-            s_in.wait_event(ev["cmp"][j])  # compute of chunk b-2 has finished reading these inputs
+            s_in.wait_event(ev["cmp"][j])  # compute of chunk ci-2 has finished reading these inputs
             with torch.cuda.stream(s_in):
                 for n in names:
-                    for dst, src in zip(piece(bi[n], 0), piece(host_in[n], b)):
+                    for dst, src in zip(piece(bi[n], 0, 0, n in wnames), piece(host_in[n], b, g0, n in wnames)):
                         dst.copy_(src, non_blocking=True)
             ev["in"][j].record(s_in)
             s_cmp.wait_event(ev["in"][j])
-            s_cmp.wait_event(ev["out"][j])  # D2H of chunk b-2 has finished reading these outputs
+            s_cmp.wait_event(ev["out"][j])  # D2H of chunk ci-2 has finished reading these outputs
             with torch.cuda.stream(s_cmp):
-                gspn.fwd(bi["x"], bi["w_l"], bi["w_m"], bi["w_r"], bi["lam"], cfg.dirs, sh.G, out=bo["h"],
+                gspn.fwd(bi["x"], bi["w_l"], bi["w_m"], bi["w_r"], bi["lam"], cfg.dirs, gb, out=bo["h"],
                          stream=s_cmp)
-                gspn.bwd(bi["x"], bi["w_l"], bi["w_m"], bi["w_r"], bi["lam"], bo["h"], bi["dh"], cfg.dirs, sh.G,
+                gspn.bwd(bi["x"], bi["w_l"], bi["w_m"], bi["w_r"], bi["lam"], bo["h"], bi["dh"], cfg.dirs, gb,
                          outs=(bo["dx"], bo["dw_l"], bo["dw_m"], bo["dw_r"], bo["dlam"]), workspace=wsj,
                          stream=s_cmp)
             ev["cmp"][j].record(s_cmp)
             s_out.wait_event(ev["cmp"][j])
             with torch.cuda.stream(s_out):
                 for n in onames:
-                    for dst, src in zip(piece(host_out[n], b), piece(bo[n], 0)):
+                    for dst, src in zip(piece(host_out[n], b, g0, n in wnames), piece(bo[n], 0, 0, n in wnames)):
                         dst.copy_(src, non_blocking=True)
             ev["out"][j].record(s_out)
 
@@ -535,9 +546,9 @@ def run_e2e(args, gspn, cfg, sh, t, h, outs, ws, dev, world, dist):
     total = (cfg.fwd_bytes() + cfg.bwd_bytes()) if args.scaling == "strong" else \
         (gspn.algorithmic_bytes(sh.B, sh.C, cfg.H, cfg.W, cfg.dirs, sh.G, dt_code, False) * 3 * world)
     return {"value": total / (ms * 1e-3) / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d * world,
-            "d2h_bytes_per_step": d2h * world, "ms_per_step": ms, "steps": n, "chunks": B,
-            "note": "pinned host buffers; per-b chunks through 2 device buffer sets on 3 streams: H2D of "
-                    "x,w,lam,dh | fwd + bwd | D2H of h,dx,dw,dlam overlap across chunks"}
+            "d2h_bytes_per_step": d2h * world, "ms_per_step": ms, "steps": n, "chunks": len(chunks),
+            "note": "pinned host buffers; (b, group-block) chunks through 2 device buffer sets on 3 streams: "
+                    "H2D of x,w,lam,dh | fwd + bwd | D2H of h,dx,dw,dlam overlap across chunks"}
 
 
 def main():
