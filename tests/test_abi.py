@@ -166,3 +166,13 @@ def test_proxy_validation():
     assert L.gspn_proxy_mix(i, m, i + 32, 2, 384, 8, 28, 28, 1, 0, None) == 1 and "overlaps" in detail()
     assert L.gspn_proxy_wgrad(i, m, None, 2, 384, 8, 28, 28, 1, None) == 1 and "dM is NULL" in detail()
     assert L.gspn_proxy_wgrad(i, m, o, 2, 4096, 64, 28, 28, 1, None) == 2
+
+
+def test_missing_library_fails_loudly(monkeypatch):
+    """No CPU fallback: without the built CUDA library the binding raises instead of computing anything."""
+    from paper_2512_07884_b200 import _lib
+
+    monkeypatch.setattr(_lib, "_lib", None)
+    monkeypatch.setattr(_lib, "LIBGSPN", "/nonexistent/libgspn.so")
+    with pytest.raises(ImportError, match="not built"):
+        _lib.lib()
