@@ -1112,10 +1112,10 @@ __device__ __forceinline__ void dw_math(float g, float l, float m, float r, floa
   }
 }
 
-template <typename T, int kPre>
+template <typename T, int kPre, bool kLocal>
 __device__ __forceinline__ void bwd_half_vert_fused(const Lanes<T>& ln, const uint8_t* p0, int stepb, int64_t gofs,
                                                     int64_t gstep, int t0, int L, BwdState& S, uint64_t pol, T* gbase,
-                                                    T* dwl, T* dwm, T* dwr, bool hl0, bool hr1) {
+                                                    T* dwl, T* dwm, T* dwr, bool hl0, bool hr1, uint32_t rm) {
   constexpr int KS = Cfg<T>::KS;
 #pragma unroll
   for (int i = 0; i < KS; ++i) {
@@ -1138,6 +1138,12 @@ __device__ __forceinline__ void bwd_half_vert_fused(const Lanes<T>& ln, const ui
     dw_math<kPre>(g[1], l[1], m[1], r[1], hp[0], hp[1], hright, ol[1], om[1], orr[1]);
     ol[0] = hl0 ? ol[0] : 0.f;    // position r0 may be the chain's first (no left tap)
     orr[1] = hr1 ? orr[1] : 0.f;  // position r0 + 1 may be its last (no right tap)
+    if constexpr (kLocal) {  // GSPN-local segment start: h_{t-1} was not propagated -> dw = 0, carry reset
+      if ((rm >> i) & 1u) {
+        ol[0] = ol[1] = om[0] = om[1] = orr[0] = orr[1] = 0.f;
+        S.ea[0] = S.ea[1] = S.eb[0] = S.eb[1] = S.ec[0] = S.ec[1] = 0.f;
+      }
+    }
     const bool st = ln.own_v && t0 + KS - 1 - i < L;
     GStore<T, 2>::st_if(st, gbase + gofs, g, pol);
     GStore<T, 2>::st_if(st, dwl + gofs, ol, pol);
@@ -1249,7 +1255,7 @@ __device__ void producer_fused(const StreamArgs& A, uint8_t* ring, uint64_t* ful
   }
 }
 
-template <typename T, int kPre>
+template <typename T, int kPre, bool kLocal>
 __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_fused_kernel(const __grid_constant__ StreamArgs A) {
   using C = Cfg<T>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -1280,6 +1286,7 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_fused_kernel(const 
   T* const dwl = static_cast<T*>(A.p.dwl);
   T* const dwm = static_cast<T*>(A.p.dwm);
   T* const dwr = static_cast<T*>(A.p.dwr);
+  const int kchunk = static_cast<int>(A.p.kchunk);
   int stage = 0, par = 0;
   uint32_t phase = 0;
   for (int64_t w = blockIdx.x; w < pl.nchains; w += gridDim.x) {
@@ -1316,19 +1323,23 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_fused_kernel(const 
         const int cm = ch.rev ? 1 - half : half;
         const bool live = !pl.null_compute && !half_outside_k<C::K>(ch, j, half, cm);
         if (live) {
+          uint32_t rm = 0;
           if (ch.vert) {
             const int t0 = j * C::K + half * C::KS;
             const int tl = t0 + C::KS - 1;
             const int kkl = ch.rev ? C::K - 1 - (half * C::KS + C::KS - 1) : half * C::KS + C::KS - 1;
             const int rowl = ch.rev ? ch.L - 1 - tl : tl;
             const int vs = static_cast<int>(pl.vstep);
-            bwd_half_vert_fused<T, kPre>(ln, st + ln.voff + kkl * vs, ch.rev ? vs : -vs,
-                                         ln.vout + static_cast<int64_t>(rowl) * W, ch.rev ? W : -W, t0, ch.L, S,
-                                         pol_vout, gbase, dwl, dwm, dwr, hl0, hr1);
-          } else if (ch.rev) {
-            bwd_half_horiz<T, kPre, true, false>(ln, st, cm, lane, S, OG, 0u);
+            if constexpr (kLocal) rm = reset_bits(rowl, ch.rev ? 1 : -1, !ch.rev, kchunk, C::KS);
+            bwd_half_vert_fused<T, kPre, kLocal>(ln, st + ln.voff + kkl * vs, ch.rev ? vs : -vs,
+                                                 ln.vout + static_cast<int64_t>(rowl) * W, ch.rev ? W : -W, t0, ch.L,
+                                                 S, pol_vout, gbase, dwl, dwm, dwr, hl0, hr1, rm);
           } else {
-            bwd_half_horiz<T, kPre, false, false>(ln, st, cm, lane, S, OG, 0u);
+            if constexpr (kLocal)
+              rm = reset_bits(tile_start(ch, j, C::K) + cm * C::KS + (ch.rev ? 0 : C::KS - 1), ch.rev ? 1 : -1,
+                              !ch.rev, kchunk, C::KS);
+            if (ch.rev) bwd_half_horiz<T, kPre, true, kLocal>(ln, st, cm, lane, S, OG, rm);
+            else bwd_half_horiz<T, kPre, false, kLocal>(ln, st, cm, lane, S, OG, rm);
           }
         }
         edge_publish(m.edge + 0 * kXArr + par * kEdgeW * kXRow, warp, lane, ch.vert, S.ea);
@@ -2521,7 +2532,10 @@ bool launch_out_tma(const ScanParams& p, const void* g, gspn_dtype_t dt, cudaStr
   using BF = __nv_bfloat16;
   auto kern = p.kchunk > 0
       ? (grouped ? (dt == GSPN_BF16 ? bwd_out_grp_tma_kernel<BF, true> : bwd_out_grp_tma_kernel<float, true>)
-                 : (dt == GSPN_BF16 ? bwd_out_tma_kernel<BF, true, false> : bwd_out_tma_kernel<float, true, false>))
+                 : vert_done ? (dt == GSPN_BF16 ? bwd_out_tma_kernel<BF, true, true>
+                                                : bwd_out_tma_kernel<float, true, true>)
+                             : (dt == GSPN_BF16 ? bwd_out_tma_kernel<BF, true, false>
+                                                : bwd_out_tma_kernel<float, true, false>))
       : (grouped ? (dt == GSPN_BF16 ? bwd_out_grp_tma_kernel<BF, false> : bwd_out_grp_tma_kernel<float, false>)
                  : vert_done ? (dt == GSPN_BF16 ? bwd_out_tma_kernel<BF, false, true>
                                                 : bwd_out_tma_kernel<float, false, true>)
@@ -2569,7 +2583,7 @@ bool launch_bwd_fused(const ScanParams& p0, gspn_dtype_t dt, cudaStream_t s, int
   static StreamArgs A;
   static std::mutex mu;
   std::lock_guard<std::mutex> lock(mu);
-  if (p0.G != p0.C || p0.kchunk > 0 || getenv("GSPN_NOFUSE")) return false;
+  if (p0.G != p0.C || getenv("GSPN_NOFUSE")) return false;
   const int es = dt == GSPN_BF16 ? 2 : 4;
   if ((p0.B * p0.C * p0.H * p0.W * es) % 16 != 0) return false;  // dx kernel: 16-byte vectors per slab
   memset(&A, 0, sizeof A);
@@ -2581,7 +2595,8 @@ bool launch_bwd_fused(const ScanParams& p0, gspn_dtype_t dt, cudaStream_t s, int
   const bool fuse_h = getenv("GSPN_FUSE_H") != nullptr;
   if (!make_plan(p, dt, fuse_h ? B_NINF : B_NIN + 1, &A.plan)) return false;
   Plan& pl = A.plan;
-  if (pl.cl > 1 || (fuse_h && pl.npack > 1) || (getenv("GSPN_NOFUSE_PACKED") && pl.npack > 1)) return false;
+  const bool local = p.kchunk > 0;
+  if (pl.cl > 1 || (fuse_h && (pl.npack > 1 || local)) || (getenv("GSPN_NOFUSE_PACKED") && pl.npack > 1)) return false;
   pl.fuse_h = fuse_h ? 1 : 0;
   // make_plan counted pl.nin tiles per stage for both orientations: vertical loads B_NIN + 1 (no B_H1),
   // horizontal B_NIN (dh, w) unless fully fused
@@ -2601,13 +2616,17 @@ bool launch_bwd_fused(const ScanParams& p0, gspn_dtype_t dt, cudaStream_t s, int
   cudaError_t e;
   if (dt == GSPN_BF16) {
     using BF = __nv_bfloat16;
-    e = mode == kNormPre ? launch(bwd_fused_kernel<BF, kNormPre>, A, s)
-        : mode == kNormClamp ? launch(bwd_fused_kernel<BF, kNormClamp>, A, s)
-                             : launch(bwd_fused_kernel<BF, kNormFull>, A, s);
+    if (local) e = mode == kNormPre ? launch(bwd_fused_kernel<BF, kNormPre, true>, A, s)
+                                    : launch(bwd_fused_kernel<BF, kNormClamp, true>, A, s);
+    else e = mode == kNormPre ? launch(bwd_fused_kernel<BF, kNormPre, false>, A, s)
+             : mode == kNormClamp ? launch(bwd_fused_kernel<BF, kNormClamp, false>, A, s)
+                                  : launch(bwd_fused_kernel<BF, kNormFull, false>, A, s);
   } else {
-    e = mode == kNormPre ? launch(bwd_fused_kernel<float, kNormPre>, A, s)
-        : mode == kNormClamp ? launch(bwd_fused_kernel<float, kNormClamp>, A, s)
-                             : launch(bwd_fused_kernel<float, kNormFull>, A, s);
+    if (local) e = mode == kNormPre ? launch(bwd_fused_kernel<float, kNormPre, true>, A, s)
+                                    : launch(bwd_fused_kernel<float, kNormClamp, true>, A, s);
+    else e = mode == kNormPre ? launch(bwd_fused_kernel<float, kNormPre, false>, A, s)
+             : mode == kNormClamp ? launch(bwd_fused_kernel<float, kNormClamp, false>, A, s)
+                                  : launch(bwd_fused_kernel<float, kNormFull, false>, A, s);
   }
   *launches += 1;
   if (e == cudaSuccess) {
