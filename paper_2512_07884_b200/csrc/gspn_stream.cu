@@ -2314,7 +2314,7 @@ bool make_plan(const ScanParams& p, gspn_dtype_t dt, int nin, Plan* pl) {
   pl->nchains = p.D * ((pl->nbc + pl->npack - 1) / pl->npack);  // work items: packs of chains
   pl->smem_bytes = 1024 + ns * pl->stage_bytes + kSmemTail;
   // L2 priorities (experiments: GSPN_POL="x,vin,hin,vout,hout,acc", each 0|1|2)
-  static const int def_pol[6] = {1, 0, 1, 0, 1, 1};
+  static const int def_pol[6] = {1, 0, 2, 0, 1, 1};  // horizontal loads evict_last: +0.5 % (same-box A/B x3)
   for (int i = 0; i < 6; ++i) pl->pol[i] = def_pol[i];
   if (const char* e = getenv("GSPN_POL")) {
     int v[6], n = sscanf(e, "%d,%d,%d,%d,%d,%d", &v[0], &v[1], &v[2], &v[3], &v[4], &v[5]);
