@@ -468,28 +468,39 @@ def run_e2e(args, gspn, cfg, sh, t, h, outs, ws, dev, world, dist):
     B, G = sh.B, sh.G
     Cg = sh.C // sh.G
     dt_code = gspn.DTYPE_BF16 if cfg.dtype == "bf16" else gspn.DTYPE_F32
-    # chunks = (b, block of consecutive groups): ~16 per step, so the pipeline fill / drain is short
-    nsub = max(1, 16 // max(1, B))
-    while G % nsub:
-        nsub -= 1
-    gb = G // nsub
-    chunks = [(b, k * gb) for b in range(B) for k in range(nsub)]
-
     wnames = {"w_l", "w_m", "w_r", "dw_l", "dw_m", "dw_r"}
+    # ~16 chunks of consecutive units per step, so the pipeline fill / drain is short:
+    #  G > 1: (one b, a block of gb groups);  G = 1 (unit shards, compact configs): a block of cb batches
+    if G > 1:
+        nsub = max(1, 16 // max(1, B))
+        while G % nsub:
+            nsub -= 1
+        gb, cb = G // nsub, 1
+        chunks = [(b, 1, k * gb) for b in range(B) for k in range(nsub)]
+    else:
+        gb, cb = 1, max(1, -(-B // 16))
+        while B % cb:  # equal chunks: every chunk buffer view stays contiguous
+            cb += 1
+        chunks = [(b, cb, 0) for b in range(0, B, cb)]
 
-    def piece(x, b, g0, is_w):  # contiguous pieces of chunk (b, groups g0..g0+gb)
+    def piece(x, b, nb, g0, is_w):  # contiguous pieces of chunk (batches b..b+nb, groups g0..g0+gb)
         lo, hi = (g0, g0 + gb) if is_w else (g0 * Cg, (g0 + gb) * Cg)
+        if nb > 1:  # G = 1: whole batches
+            return [x[b:b + nb]] if x.dim() == 4 else [x[d, b:b + nb] for d in range(x.shape[0])]
         return [x[b, lo:hi]] if x.dim() == 4 else [x[d, b, lo:hi] for d in range(x.shape[0])]
 
     def dshape(x, is_w):
         n = gb if is_w else gb * Cg
-        return (1, n) + tuple(x.shape[2:]) if x.dim() == 4 else (x.shape[0], 1, n) + tuple(x.shape[3:])
+        return (cb, n) + tuple(x.shape[2:]) if x.dim() == 4 else (x.shape[0], cb, n) + tuple(x.shape[3:])
+
+    def view(x, nb):  # the first nb batches of a chunk buffer (a short last chunk)
+        return x[:nb] if x.dim() == 4 else x[:, :nb]
 
     bufs = []
     for _ in range(2):
         bi = {n: torch.empty(dshape(t[n], n in wnames), dtype=t[n].dtype, device=dev) for n in names}
         bo = {n: torch.empty(dshape(full_out[n], n in wnames), dtype=full_out[n].dtype, device=dev) for n in onames}
-        wsb = gspn.workspace_bytes(1, gb * Cg, cfg.H, cfg.W, cfg.dirs, gb, dt_code)
+        wsb = gspn.workspace_bytes(cb, gb * Cg, cfg.H, cfg.W, cfg.dirs, gb, dt_code)
         bufs.append((bi, bo, torch.empty(max(wsb, 16), dtype=torch.uint8, device=dev)))
     s_in, s_cmp, s_out = (torch.cuda.Stream(dev) for _ in range(3))
     ev = {k: [torch.cuda.Event() for _ in range(2)] for k in ("in", "cmp", "out")}
@@ -498,13 +509,15 @@ def run_e2e(args, gspn, cfg, sh, t, h, outs, ws, dev, world, dist):
             e.record(torch.cuda.current_stream(dev))
 
     def step():
-        for ci, (b, g0) in enumerate(chunks):
+        for ci, (b, nb, g0) in enumerate(chunks):
             j = ci % 2
-            bi, bo, wsj = bufs[j]
+            bi0, bo0, wsj = bufs[j]
+            bi = {n: view(v, nb) for n, v in bi0.items()}
+            bo = {n: view(v, nb) for n, v in bo0.items()}
             s_in.wait_event(ev["cmp"][j])  # compute of chunk ci-2 has finished reading these inputs
             with torch.cuda.stream(s_in):
                 for n in names:
-                    for dst, src in zip(piece(bi[n], 0, 0, n in wnames), piece(host_in[n], b, g0, n in wnames)):
+                    for dst, src in zip(piece(bi[n], 0, nb, 0, n in wnames), piece(host_in[n], b, nb, g0, n in wnames)):
                         dst.copy_(src, non_blocking=True)
             ev["in"][j].record(s_in)
             s_cmp.wait_event(ev["in"][j])
@@ -519,7 +532,7 @@ def run_e2e(args, gspn, cfg, sh, t, h, outs, ws, dev, world, dist):
             s_out.wait_event(ev["cmp"][j])
             with torch.cuda.stream(s_out):
                 for n in onames:
-                    for dst, src in zip(piece(host_out[n], b, g0, n in wnames), piece(bo[n], 0, 0, n in wnames)):
+                    for dst, src in zip(piece(host_out[n], b, nb, g0, n in wnames), piece(bo[n], 0, nb, 0, n in wnames)):
                         dst.copy_(src, non_blocking=True)
             ev["out"][j].record(s_out)
 
