@@ -53,6 +53,13 @@ namespace {
 
 using namespace ptx;
 
+// Experiment knobs (A/B tooling under tools/): read only when GSPN_EXPERIMENTS is set, so a stray
+// environment variable can never change what the product path computes or how it is scheduled.
+const char* knob(const char* name) {
+  static const bool on = getenv("GSPN_EXPERIMENTS") != nullptr;
+  return on ? getenv(name) : nullptr;
+}
+
 constexpr int kMaxIn = 6;
 constexpr int kMaxOut = 4;
 constexpr int kEdgeW = 16;     // edge-buffer slots (>= consumer warps + 1)
@@ -1798,7 +1805,7 @@ cudaError_t launch_out_pc(const ScanParams& p, const void* g, cudaStream_t s) {
   const int64_t n = p.B * p.C * ((p.H + R - 1) / R) * (p.W / V);
   const unsigned blocks = static_cast<unsigned>((n + 255) / 256);
   int grp = 2;  // directions whose loads are in flight together (experiments: GSPN_OUTK=1|2|4)
-  if (const char* e = getenv("GSPN_OUTK")) grp = atoi(e);
+  if (const char* e = knob("GSPN_OUTK")) grp = atoi(e);
   const T* gt = static_cast<const T*>(g);
   if (grp == 1) bwd_out_pc_kernel<T, V, R, 1><<<blocks, 256, 0, s>>>(p, gt);
   else if (grp == 4) bwd_out_pc_kernel<T, V, R, 4><<<blocks, 256, 0, s>>>(p, gt);
@@ -2271,7 +2278,7 @@ bool make_plan(const ScanParams& p, gspn_dtype_t dt, int nin, Plan* pl) {
     const int nwc_c = (kPpad - 2 * GH) / pl->own;
     pl->ownc = nwc_c * pl->own;
     pl->cl = static_cast<int>((maxP + pl->ownc - 1) / pl->ownc);
-    if (pl->cl > 8 || getenv("GSPN_NOCLUSTER")) return false;
+    if (pl->cl > 8 || knob("GSPN_NOCLUSTER")) return false;
     pl->nwc = nwc_c;
     cover = kPpad;
     pl->bhs = pl->ownc / 2;  // <= 256 rows per TMA store box
@@ -2293,7 +2300,7 @@ bool make_plan(const ScanParams& p, gspn_dtype_t dt, int nin, Plan* pl) {
   pl->nbc = p.B * p.C;
   pl->vstep = kRowB;
   const int64_t PH = std::max<int64_t>(p.H, p.W);  // packing needs both orientations to fit
-  if (pl->cl == 1 && p.G == p.C && PH <= kPpad / 2 && pl->nbc > 1 && !getenv("GSPN_NOPACK")) {
+  if (pl->cl == 1 && p.G == p.C && PH <= kPpad / 2 && pl->nbc > 1 && !knob("GSPN_NOPACK")) {
     // a divisor of B C: no partial pack, so a packed TMA store never spills into the next direction
     int np = static_cast<int>(std::min<int64_t>({kPpad / PH, 256, pl->nbc}));
     while (pl->nbc % np != 0) --np;
@@ -2316,11 +2323,11 @@ bool make_plan(const ScanParams& p, gspn_dtype_t dt, int nin, Plan* pl) {
   // L2 priorities (experiments: GSPN_POL="x,vin,hin,vout,hout,acc", each 0|1|2)
   static const int def_pol[6] = {1, 0, 2, 0, 1, 1};  // horizontal loads evict_last: +0.5 % (same-box A/B x3)
   for (int i = 0; i < 6; ++i) pl->pol[i] = def_pol[i];
-  if (const char* e = getenv("GSPN_POL")) {
+  if (const char* e = knob("GSPN_POL")) {
     int v[6], n = sscanf(e, "%d,%d,%d,%d,%d,%d", &v[0], &v[1], &v[2], &v[3], &v[4], &v[5]);
     for (int i = 0; i < n && i < 6; ++i) pl->pol[i] = v[i];
   }
-  if (const char* e = getenv("GSPN_NULL")) pl->null_compute = atoi(e) != 0;
+  if (const char* e = knob("GSPN_NULL")) pl->null_compute = atoi(e) != 0;
   return true;
 }
 
@@ -2359,7 +2366,7 @@ cudaError_t launch(KernelT kernel, const StreamArgs& A, cudaStream_t s) {
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   int64_t grid = static_cast<int64_t>(sm_count()) * per_sm;
-  if (const char* ev = getenv("GSPN_GRID")) {  // experiments only: cap the persistent grid
+  if (const char* ev = knob("GSPN_GRID")) {  // experiments only: cap the persistent grid
     const int64_t g = atoll(ev);
     if (g > 0 && g < grid) grid = g;
   }
@@ -2471,7 +2478,7 @@ bool launch_out_tma(const ScanParams& p, const void* g, gspn_dtype_t dt, cudaStr
   static OutArgs A;
   static std::mutex mu;
   std::lock_guard<std::mutex> lock(mu);
-  if (getenv("GSPN_OUT_REG")) return false;  // experiments: register-staged kernel
+  if (knob("GSPN_OUT_REG")) return false;  // experiments: register-staged kernel
   memset(&A, 0, sizeof A);
   A.p = p;
   const int es = dt == GSPN_BF16 ? 2 : 4;
@@ -2583,7 +2590,7 @@ bool launch_bwd_fused(const ScanParams& p0, gspn_dtype_t dt, cudaStream_t s, int
   static StreamArgs A;
   static std::mutex mu;
   std::lock_guard<std::mutex> lock(mu);
-  if (p0.G != p0.C || getenv("GSPN_NOFUSE")) return false;
+  if (p0.G != p0.C || knob("GSPN_NOFUSE")) return false;
   const int es = dt == GSPN_BF16 ? 2 : 4;
   if ((p0.B * p0.C * p0.H * p0.W * es) % 16 != 0) return false;  // dx kernel: 16-byte vectors per slab
   memset(&A, 0, sizeof A);
@@ -2592,11 +2599,11 @@ bool launch_bwd_fused(const ScanParams& p0, gspn_dtype_t dt, cudaStream_t s, int
   // Horizontal chains' dw in the recurrence measured slower than the split (6.45 vs 3.98 ms bwd on
   // config 4's horizontal directions; profiles/r1_notes.md): by default only vertical chains are fused
   // and the output kernel forms the horizontal chains' dw (GSPN_FUSE_H=1: fuse both, experiments).
-  const bool fuse_h = getenv("GSPN_FUSE_H") != nullptr;
+  const bool fuse_h = knob("GSPN_FUSE_H") != nullptr;
   if (!make_plan(p, dt, fuse_h ? B_NINF : B_NIN + 1, &A.plan)) return false;
   Plan& pl = A.plan;
   const bool local = p.kchunk > 0;
-  if (pl.cl > 1 || (fuse_h && (pl.npack > 1 || local)) || (getenv("GSPN_NOFUSE_PACKED") && pl.npack > 1)) return false;
+  if (pl.cl > 1 || (fuse_h && (pl.npack > 1 || local)) || (knob("GSPN_NOFUSE_PACKED") && pl.npack > 1)) return false;
   pl.fuse_h = fuse_h ? 1 : 0;
   // make_plan counted pl.nin tiles per stage for both orientations: vertical loads B_NIN + 1 (no B_H1),
   // horizontal B_NIN (dh, w) unless fully fused

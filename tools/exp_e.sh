@@ -1,4 +1,5 @@
 #!/bin/bash
+export GSPN_EXPERIMENTS=1  # enable the library's experiment knobs (GSPN_*)
 bash tools/gpu_check.sh
 M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum
 for E in 2 4; do

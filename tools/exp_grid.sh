@@ -1,4 +1,5 @@
 #!/bin/bash
+export GSPN_EXPERIMENTS=1  # enable the library's experiment knobs (GSPN_*)
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
 M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sector_hit_rate.pct

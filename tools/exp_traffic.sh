@@ -1,4 +1,5 @@
 #!/bin/bash
+export GSPN_EXPERIMENTS=1  # enable the library's experiment knobs (GSPN_*)
 # DRAM traffic of the fwd/bwd stream kernels per direction subset and L2 policy (ncu metrics pass)
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1

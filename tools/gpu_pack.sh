@@ -1,4 +1,5 @@
 #!/bin/bash
+export GSPN_EXPERIMENTS=1  # enable the library's experiment knobs (GSPN_*)
 bash tools/gpu_check.sh
 timeout 600 python bench.py --config 2 --no-cpu-baseline --no-e2e > gpurun_out/bench_c2.log 2>&1
 GSPN_NOPACK=1 timeout 600 python bench.py --config 2 --no-cpu-baseline --no-e2e > gpurun_out/bench_c2_nopack.log 2>&1
