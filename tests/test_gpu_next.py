@@ -338,3 +338,34 @@ def test_proxy_parity(case):
     assert normwise(from_torch(dx), oracle.proxy_mix(dxp_st, Pf.T)) <= tol
     assert normwise(from_torch(dQ), oracle.proxy_wgrad(dyf, xp_st)) <= tol
     assert normwise(from_torch(dP), oracle.proxy_wgrad(dxp_st, xf)) <= tol
+
+
+@pytest.mark.parametrize("shape", [(1, 2, 2, 300, 264, 0xF, "bf16", 50), (2, 4, 4, 56, 56, 0xF, "f32", 20)],
+                         ids=lambda s: "B{}C{}G{}H{}W{}d{:x}{}k{}".format(*s))
+def test_fused_local_prenormalized(shape):
+    """Hybrid fused backward with GSPN-local segments and pre-normalised taps together."""
+    import torch
+
+    B, C, G, H, W, dirs, dt, k = shape
+    cfg = small_config(B, C, G, H, W, dirs, dt, cfg_id=607)
+    inp = host_inputs(cfg)
+    f = {n: v[1] for n, v in inp.items()}
+    dev = _dev()
+    t = {n: to_torch(v[0], dt, dev) for n, v in inp.items()}
+    S = t["w_l"].float() + t["w_m"].float() + t["w_r"].float()
+    for n in ("w_l", "w_m", "w_r"):
+        t[n] = (t[n].float() / S).to(t[n].dtype)
+        f[n] = from_torch(t[n])
+    fl = gspn.FLAG_PRENORMALIZED
+    h = gspn.fwd(t["x"], t["w_l"], t["w_m"], t["w_r"], t["lam"], dirs, G, flags=fl, kchunk=k)
+    grads = gspn.bwd(t["x"], t["w_l"], t["w_m"], t["w_r"], t["lam"], h, t["dh"], dirs, G, flags=fl, kchunk=k)
+    assert gspn.last_path() == "stream-fused"
+    h_ref = oracle.fwd(f["x"], f["w_l"], f["w_m"], f["w_r"], f["lam"], dirs, G, flags=oracle.PRENORMALIZED,
+                       kchunk=k)
+    g_ref = oracle.bwd(f["x"], f["w_l"], f["w_m"], f["w_r"], f["lam"], from_torch(h), f["dh"], dirs, G,
+                       flags=oracle.PRENORMALIZED, kchunk=k)
+    tol = TOL[dt]
+    assert normwise(from_torch(h), h_ref) <= tol
+    for name, a, r in zip(("dx", "dw_l", "dw_m", "dw_r", "dlam"), grads, g_ref):
+        assert normwise(from_torch(a), r) <= tol, name
+    torch.cuda.synchronize()
