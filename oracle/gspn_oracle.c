@@ -37,6 +37,8 @@
 
 enum { ORACLE_OK = 0, ORACLE_BAD_ARG = 1, ORACLE_NONPOSITIVE_SUM = 5, ORACLE_NOMEM = 6 };
 
+/* Detail of the last failed call. Workers write only their job's own buffer (under the job mutex);
+ * run() copies it here after every worker has joined, so no two threads ever write g_detail. */
 static char g_detail[256];
 
 const char* gspn_oracle_detail(void) { return g_detail; }
@@ -86,7 +88,17 @@ typedef struct {
   int64_t next_unit; /* guarded by mu */
   pthread_mutex_t mu;
   int status;
+  char detail[256]; /* first failure's detail, written under mu */
 } job_t;
+
+/* Records the first failing position of a job (thread-safe: under the job mutex). */
+static void set_detail(job_t* J, unsigned dir, int64_t b, int64_t g, int64_t t, int64_t r) {
+  pthread_mutex_lock(&J->mu);
+  if (!J->detail[0])
+    snprintf(J->detail, sizeof J->detail, "row sum S<=0 at dir=%u b=%lld g=%lld t=%lld r=%lld", dir, (long long)b,
+             (long long)g, (long long)t, (long long)r);
+  pthread_mutex_unlock(&J->mu);
+}
 
 static int dir_list(unsigned dirs, unsigned* out) {
   int n = 0;
@@ -129,8 +141,7 @@ static int forward_unit(job_t* J, int64_t b, int64_t g) {
           const int64_t p = pixel(dl[k], J->H, J->W, t, r);
           double a, bb, cc, S;
           if (taps(wl[p], wm[p], wr[p], r, P, J->flags, &a, &bb, &cc, &S)) {
-            snprintf(g_detail, sizeof g_detail, "row sum S<=0 at dir=%u b=%lld g=%lld t=%lld r=%lld", dl[k],
-                     (long long)b, (long long)g, (long long)t, (long long)r);
+            set_detail(J, dl[k], b, g, t, r);
             return ORACLE_NONPOSITIVE_SUM;
           }
           double acc = 0.0; /* w_i h_{i-1}: zero at t = 0 because h_{-1} = 0 */
@@ -220,8 +231,7 @@ static int backward_unit(job_t* J, int64_t b, int64_t g) {
         const int64_t p = pixel(dl[k], J->H, J->W, t, r);
         double a, bb, cc, S;
         if (taps(wl[p], wm[p], wr[p], r, P, J->flags, &a, &bb, &cc, &S)) {
-          snprintf(g_detail, sizeof g_detail, "row sum S<=0 at dir=%u b=%lld g=%lld t=%lld r=%lld", dl[k],
-                   (long long)b, (long long)g, (long long)t, (long long)r);
+          set_detail(J, dl[k], b, g, t, r);
           st = ORACLE_NONPOSITIVE_SUM;
           goto done;
         }
@@ -281,6 +291,7 @@ static int run(job_t* J, int threads) {
   worker(J);
   for (int i = 0; i < started; ++i) pthread_join(tid[i], NULL);
   pthread_mutex_destroy(&J->mu);
+  if (J->status) memcpy(g_detail, J->detail, sizeof g_detail);
   return J->status;
 }
 

@@ -383,3 +383,106 @@ def test_threads_do_not_change_results():
     for a, b in zip(oracle.bwd(x, wl, wm, wr, lam, h1, dh, ALL, 2, threads=1),
                     oracle.bwd(x, wl, wm, wr, lam, h1, dh, ALL, 2, threads=3)):
         np.testing.assert_array_equal(a, b)
+
+
+# ---------------------------------------------------------------- backward under GSPN_FLAG_PRENORMALIZED
+
+def _loss_flags(x, wl, wm, wr, lam, dh, dirs, G, flags):
+    return float(np.sum(oracle.fwd(x, wl, wm, wr, lam, dirs, G, flags=flags) * dh))
+
+
+@pytest.mark.parametrize("G", [3, 1])
+@pytest.mark.parametrize("dirs", [0x1, 0x2, 0x4, 0x8])
+def test_backward_prenormalized_matches_finite_differences(G, dirs):
+    """PRENORMALIZED (R1): the taps act as given, out-of-range ones dropped, so dw = (Da, Db, Dc) masked
+    at the chain ends and zero at t = 0. Pinned against central differences of the (separately pinned,
+    test_prenormalized_flag_matches_raw) prenormalised forward, per direction, G = C and G = 1. Taps
+    are drawn unnormalised (row sums != 1) so a Jacobian applied by mistake would show."""
+    rng = np.random.default_rng(40 + G + 7 * dirs)
+    B, C, H, W = 1, 3, 4, 5
+    x, wl, wm, wr, lam = rand_inputs(rng, B, C, G, H, W, dirs)
+    dh = rng.uniform(-1, 1, lam.shape)
+    F = oracle.PRENORMALIZED
+    h = oracle.fwd(x, wl, wm, wr, lam, dirs, G, flags=F)
+    grads = oracle.bwd(x, wl, wm, wr, lam, h, dh, dirs, G, flags=F)
+    inputs = [x, wl, wm, wr, lam]
+    eps = 1e-6
+    for gi, (arr, grad) in enumerate(zip(inputs, grads)):
+        fd = np.zeros_like(arr)
+        it = np.nditer(arr, flags=["multi_index"])
+        for _ in it:
+            idx = it.multi_index
+            old = arr[idx]
+            arr[idx] = old + eps
+            lp = _loss_flags(*inputs, dh, dirs, G, F)
+            arr[idx] = old - eps
+            lm = _loss_flags(*inputs, dh, dirs, G, F)
+            arr[idx] = old
+            fd[idx] = (lp - lm) / (2 * eps)
+        err = np.abs(fd - grad).max() / max(np.abs(fd).max(), 1e-30)
+        assert err < 1e-7, f"dirs {dirs:#x} input {gi}: FD rel err {err}"
+
+
+def test_backward_prenormalized_out_of_range_taps_are_zero():
+    """The taps that fall off the chain (w_l at r = 0, w_r at r = P-1) and every tap of step 0 (h_{-1} = 0)
+    reach nothing, so their gradient is exactly 0 -- also when the flag skips the normalisation."""
+    rng = np.random.default_rng(46)
+    H, W = 5, 6
+    x, wl, wm, wr, lam = rand_inputs(rng, 1, 2, 1, H, W, ALL)
+    F = oracle.PRENORMALIZED
+    h = oracle.fwd(x, wl, wm, wr, lam, ALL, 1, flags=F)
+    dh = rng.uniform(-1, 1, h.shape)
+    _, dwl, dwm, dwr, _ = oracle.bwd(x, wl, wm, wr, lam, h, dh, ALL, 1, flags=F)
+    for k, d in enumerate(dir_list(ALL)):
+        a, b, c = (sv.to_scan(t[k, 0, 0], d) for t in (dwl, dwm, dwr))
+        assert not np.any(a[:, 0]) and not np.any(c[:, -1])
+        assert not np.any(a[0]) and not np.any(b[0]) and not np.any(c[0])
+        assert np.all(np.abs(b[1:]) > 0)
+
+
+def test_backward_prenormalized_length_one_and_zero_upstream():
+    rng = np.random.default_rng(47)
+    F = oracle.PRENORMALIZED
+    x, wl, wm, wr, lam = rand_inputs(rng, 1, 2, 2, 1, 5, 0x3)
+    h = oracle.fwd(x, wl, wm, wr, lam, 0x3, 2, flags=F)
+    dh = rng.uniform(-1, 1, h.shape)
+    dx, dwl, dwm, dwr, dlam = oracle.bwd(x, wl, wm, wr, lam, h, dh, 0x3, 2, flags=F)
+    np.testing.assert_allclose(dlam, dh * x[None], atol=1e-15)
+    np.testing.assert_allclose(dx, (dh * lam).sum(0), atol=1e-15)
+    assert not np.any(dwl) and not np.any(dwm) and not np.any(dwr)
+    x, wl, wm, wr, lam = rand_inputs(rng, 1, 2, 1, 4, 4, ALL)
+    h = oracle.fwd(x, wl, wm, wr, lam, ALL, 1, flags=F)
+    for gr in oracle.bwd(x, wl, wm, wr, lam, h, np.zeros_like(h), ALL, 1, flags=F):
+        assert not np.any(gr)
+
+
+def test_backward_prenormalized_equals_raw_chain_rule():
+    """Raw-tap gradients = the prenormalised gradients pushed through the normalisation Jacobian:
+    dw_k = (Dn_k - sum_j n_j Dn_j) / S, with n the normalised taps and Dn the PRENORMALIZED dw evaluated at
+    n. A second, independent route to the raw branch through the prenormalised one."""
+    rng = np.random.default_rng(48)
+    H, W = 4, 6
+    x, wl, wm, wr, lam = rand_inputs(rng, 1, 2, 2, H, W, ALL)
+    h = oracle.fwd(x, wl, wm, wr, lam, ALL, 2)
+    dh = rng.uniform(-1, 1, h.shape)
+    raw = oracle.bwd(x, wl, wm, wr, lam, h, dh, ALL, 2)
+    nl, nm, nr, S = (np.zeros_like(wl) for _ in range(4))
+    for k, d in enumerate(dir_list(ALL)):
+        for g in range(2):
+            a, b, c = (sv.to_scan(t[k, 0, g], d).copy() for t in (wl, wm, wr))
+            a[:, 0] = 0.0
+            c[:, -1] = 0.0
+            s = a + b + c
+            nl[k, 0, g], nm[k, 0, g], nr[k, 0, g] = (sv.from_scan(t / s, d) for t in (a, b, c))
+            S[k, 0, g] = sv.from_scan(s, d)
+    pre = oracle.bwd(x, nl, nm, nr, lam, h, dh, ALL, 2, flags=oracle.PRENORMALIZED)
+    np.testing.assert_allclose(pre[0], raw[0], atol=1e-13)
+    np.testing.assert_allclose(pre[4], raw[4], atol=1e-13)
+    q = nl * pre[1] + nm * pre[2] + nr * pre[3]
+    for k, (Dn, n) in enumerate(zip(pre[1:4], (nl, nm, nr))):
+        ref = (Dn - q) / S
+        if k == 0:
+            ref = np.where(nl == 0, 0.0, ref)
+        if k == 2:
+            ref = np.where(nr == 0, 0.0, ref)
+        np.testing.assert_allclose(raw[1 + k], ref, atol=1e-13)
