@@ -64,19 +64,31 @@ def popcount(d: int) -> int:
     return bin(int(d) & 0xF).count("1")
 
 
+def _check_shapes(named):
+    """named: (name, tensor, expected shape). The C ABI sees only pointers, so a mis-shaped tensor would
+    become an out-of-bounds device access: every tensor the call reads or writes is checked here."""
+    for name, t, shape in named:
+        if tuple(t.shape) != tuple(shape):
+            raise ValueError(f"{name} shape {tuple(t.shape)} != expected {tuple(shape)}")
+
+
+def _scan_shapes(x, dirs, G):
+    """(B, C, H, W, D) and the expected shapes of x, w_*, lam-like tensors (gspn.h layouts)."""
+    if x.dim() != 4:
+        raise ValueError(f"x must be [B, C, H, W], got {tuple(x.shape)}")
+    B, C, H, W = x.shape
+    D = popcount(dirs)
+    return (B, C, H, W, D), (B, C, H, W), (D, B, G, H, W), (D, B, C, H, W)
+
+
 def fwd(x, w_l, w_m, w_r, lam, dirs: int = DIR_ALL, groups: int | None = None, flags: int = 0, out=None,
         stream=None, kchunk: int = 0):
     """Forward scan. groups defaults to C (per-channel weights); kchunk > 0: GSPN-local (gspn_fwd_local)."""
     torch = _torch()
-    B, C, H, W = x.shape
-    G = C if groups is None else int(groups)
-    D = popcount(dirs)
-    if tuple(lam.shape) != (D, B, C, H, W):
-        raise ValueError(f"lam shape {tuple(lam.shape)} != {(D, B, C, H, W)}")
-    for n, w in (("w_l", w_l), ("w_m", w_m), ("w_r", w_r)):
-        if tuple(w.shape) != (D, B, G, H, W):
-            raise ValueError(f"{n} shape {tuple(w.shape)} != {(D, B, G, H, W)}")
+    G = x.shape[1] if groups is None else int(groups)
+    (B, C, H, W, D), sx, sw, sl = _scan_shapes(x, dirs, G)
     h = torch.empty_like(lam) if out is None else out
+    _check_shapes([("lam", lam, sl), ("w_l", w_l, sw), ("w_m", w_m, sw), ("w_r", w_r, sw), ("h (out)", h, sl)])
     _check_tensors([("x", x), ("w_l", w_l), ("w_m", w_m), ("w_r", w_r), ("lam", lam), ("h", h)], x.dtype, x.device)
     ptrs = (x.data_ptr(), w_l.data_ptr(), w_m.data_ptr(), w_r.data_ptr(), lam.data_ptr(), h.data_ptr())
     if kchunk:
@@ -99,13 +111,18 @@ def bwd(x, w_l, w_m, w_r, lam, h, dh, dirs: int = DIR_ALL, groups: int | None = 
         outs=None, workspace=None, stream=None, kchunk: int = 0):
     """Backward scan: returns (dx, dw_l, dw_m, dw_r, dlam)."""
     torch = _torch()
-    B, C, H, W = x.shape
-    G = C if groups is None else int(groups)
+    G = x.shape[1] if groups is None else int(groups)
+    (B, C, H, W, D), sx, sw, sl = _scan_shapes(x, dirs, G)
     dt = _dtype_code(x)
     if outs is None:
         outs = (torch.empty_like(x), torch.empty_like(w_l), torch.empty_like(w_m), torch.empty_like(w_r),
                 torch.empty_like(lam))
+    if len(outs) != 5:
+        raise ValueError("outs must be (dx, dw_l, dw_m, dw_r, dlam)")
     dx, dwl, dwm, dwr, dlam = outs
+    _check_shapes([("w_l", w_l, sw), ("w_m", w_m, sw), ("w_r", w_r, sw), ("lam", lam, sl), ("h", h, sl),
+                   ("dh", dh, sl), ("dx (out)", dx, sx), ("dw_l (out)", dwl, sw), ("dw_m (out)", dwm, sw),
+                   ("dw_r (out)", dwr, sw), ("dlam (out)", dlam, sl)])
     _check_tensors([("x", x), ("w_l", w_l), ("w_m", w_m), ("w_r", w_r), ("lam", lam), ("h", h), ("dh", dh),
                     ("dx", dx), ("dw_l", dwl), ("dw_m", dwm), ("dw_r", dwr), ("dlam", dlam)], x.dtype, x.device)
     need = workspace_bytes(B, C, H, W, dirs, G, dt)
@@ -128,6 +145,7 @@ def merge_fwd(h, u, dirs: int = DIR_ALL, mean: bool = False, out=None, stream=No
     if D != popcount(dirs) or tuple(u.shape) != tuple(h.shape):
         raise ValueError(f"h {tuple(h.shape)} / u {tuple(u.shape)} do not match dirs=0x{dirs:x}")
     y = torch.empty(h.shape[1:], dtype=h.dtype, device=h.device) if out is None else out
+    _check_shapes([("y (out)", y, h.shape[1:])])
     _check_tensors([("h", h), ("u", u), ("y", y)], h.dtype, h.device)
     check(lib().gspn_merge_fwd(h.data_ptr(), u.data_ptr(), y.data_ptr(), B, C, H, W, dirs, _dtype_code(h),
                                FLAG_MERGE_MEAN if mean else 0, _stream_ptr(stream, h.device)))
@@ -141,6 +159,7 @@ def merge_bwd(h, u, dy, dirs: int = DIR_ALL, mean: bool = False, outs=None, stre
     if D != popcount(dirs) or tuple(u.shape) != tuple(h.shape) or tuple(dy.shape) != tuple(h.shape[1:]):
         raise ValueError("h / u / dy shapes do not match")
     dh, du = (torch.empty_like(h), torch.empty_like(h)) if outs is None else outs
+    _check_shapes([("dh (out)", dh, h.shape), ("du (out)", du, h.shape)])
     _check_tensors([("h", h), ("u", u), ("dy", dy), ("dh", dh), ("du", du)], h.dtype, h.device)
     check(lib().gspn_merge_bwd(h.data_ptr(), u.data_ptr(), dy.data_ptr(), dh.data_ptr(), du.data_ptr(), B, C, H, W,
                                dirs, _dtype_code(h), FLAG_MERGE_MEAN if mean else 0, _stream_ptr(stream, h.device)))
@@ -160,6 +179,7 @@ def proxy_mix(inp, M, transpose: bool = False, out=None, stream=None):
             raise ValueError(f"M {tuple(M.shape)} does not match Ci={Ci}")
         Co = M.shape[0]
     out = torch.empty((B, Co, H, W), dtype=inp.dtype, device=inp.device) if out is None else out
+    _check_shapes([("M", M, (Ci, Co) if transpose else (Co, Ci)), ("out", out, (B, Co, H, W))])
     _check_tensors([("in", inp), ("M", M), ("out", out)], inp.dtype, inp.device)
     check(lib().gspn_proxy_mix(inp.data_ptr(), M.data_ptr(), out.data_ptr(), B, Ci, Co, H, W, _dtype_code(inp),
                                FLAG_PROXY_TRANSPOSE if transpose else 0, _stream_ptr(stream, inp.device)))
@@ -172,6 +192,9 @@ def proxy_wgrad(dout, inp, out=None, stream=None):
     B, Co, H, W = dout.shape
     Ci = inp.shape[1]
     dM = torch.empty((Co, Ci), dtype=torch.float32, device=dout.device) if out is None else out
+    if inp.dim() != 4:
+        raise ValueError(f"in must be [B, Ci, H, W], got {tuple(inp.shape)}")
+    _check_shapes([("in", inp, (B, Ci, H, W)), ("dM (out)", dM, (Co, Ci))])
     _check_tensors([("dout", dout), ("in", inp)], dout.dtype, dout.device)
     _check_tensors([("dM", dM)], torch.float32, dout.device)
     check(lib().gspn_proxy_wgrad(dout.data_ptr(), inp.data_ptr(), dM.data_ptr(), B, Ci, Co, H, W, _dtype_code(dout),

@@ -1,5 +1,6 @@
 // gspn_api.cu — the C ABI declared in include/gspn.h: host-side validation (before any CUDA call),
 // workspace carving, path selection (TMA streaming fast path, else the generic path) and launch.
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <exception>
@@ -327,6 +328,16 @@ gspn_status_t guarded(F&& f) {
 
 }  // namespace
 
+// The proxy kernels index pixels and (batch, channel) pairs in 32-bit: reject extents beyond INT32_MAX
+// instead of letting the casts truncate (offsets themselves are formed in 64-bit).
+static gspn_status_t check_proxy_extent(int64_t B, int64_t Ci, int64_t Co, int64_t H, int64_t W) {
+  const int64_t lim = INT32_MAX;
+  if (H > lim / W) return fail(GSPN_ERR_UNSUPPORTED, "%s: H*W above INT32_MAX (H = %lld)", "shape", H);
+  if (B > lim / std::max(Ci, Co) || Ci > lim / Co)
+    return fail(GSPN_ERR_UNSUPPORTED, "%s: B*C or Ci*Co above INT32_MAX", "shape");
+  return GSPN_OK;
+}
+
 extern "C" {
 
 gspn_status_t gspn_merge_fwd(const void* h, const void* u, void* y, int64_t B, int64_t C, int64_t H, int64_t W,
@@ -391,6 +402,7 @@ gspn_status_t gspn_proxy_mix(const void* in, const void* M, void* out, int64_t B
     if ((st = check_dims(B, Ci, H, W, 1, 1, dtype, 0))) return st;
     if (Co < 1) return fail(GSPN_ERR_INVALID_ARG, "%s must be >= 1 (got %lld)", "Co", Co);
     if ((H * W) % 2 != 0) return fail(GSPN_ERR_UNSUPPORTED, "%s: H*W must be even (got %lld)", "shape", H * W);
+    if ((st = check_proxy_extent(B, Ci, Co, H, W))) return st;
     if (Ci * Co > 49152) return fail(GSPN_ERR_UNSUPPORTED, "%s: Co*Ci above 49152 (%lld)", "M", Ci * Co);
     const size_t s = dtype == GSPN_BF16 ? 2 : 4;
     const Span ins[2] = {span("in", in, (size_t)(B * Ci * H * W) * s), span("M", M, (size_t)(Ci * Co) * s)};
@@ -415,6 +427,7 @@ gspn_status_t gspn_proxy_wgrad(const void* dout, const void* in, float* dM, int6
     if ((st = check_ptr(dout, "dout")) || (st = check_ptr(in, "in")) || (st = check_ptr(dM, "dM"))) return st;
     if ((st = check_dims(B, Ci, H, W, 1, 1, dtype, 0))) return st;
     if (Co < 1) return fail(GSPN_ERR_INVALID_ARG, "%s must be >= 1 (got %lld)", "Co", Co);
+    if ((st = check_proxy_extent(B, Ci, Co, H, W))) return st;
     if ((Co + Ci) * 33 + Co * Ci > 49152)
       return fail(GSPN_ERR_UNSUPPORTED, "%s: (Co+Ci)*33 + Co*Ci above 49152 (Co*Ci = %lld)", "shape", Ci * Co);
     const size_t s = dtype == GSPN_BF16 ? 2 : 4;

@@ -178,7 +178,7 @@ int generic_threads(int64_t P) {
 
 int grid_stride_blocks(int64_t n) {
   int64_t b = (n + 255) / 256;
-  if (b > 148 * 16) b = 148 * 16;
+  if (b > int64_t{16} * device_sm_count()) b = int64_t{16} * device_sm_count();
   if (b < 1) b = 1;
   return (int)b;
 }

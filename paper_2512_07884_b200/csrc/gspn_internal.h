@@ -7,6 +7,10 @@
 
 namespace gspn {
 
+// Attributes of the current device, cached per device (gspn_device.cu).
+int device_sm_count();
+int device_smem_optin();
+
 int64_t generic_max_P();
 cudaError_t launch_fwd_generic(const ScanParams& p, gspn_dtype_t dt, cudaStream_t s, int* launches);
 cudaError_t launch_bwd_generic(const ScanParams& p, gspn_dtype_t dt, cudaStream_t s, int* launches);

@@ -148,13 +148,7 @@ __global__ void __launch_bounds__(256) merge_bwd_scalar(const T* __restrict__ h,
 }
 
 int grid_for(int64_t work) {
-  static int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
+  const int sms = device_sm_count();
   const int64_t full = (work + 255) / 256;
   const int64_t cap = (int64_t)sms * 8;  // 8 x 256 threads resident per SM
   return static_cast<int>(full < cap ? (full < 1 ? 1 : full) : cap);

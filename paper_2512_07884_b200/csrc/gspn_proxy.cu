@@ -236,16 +236,7 @@ __global__ void __launch_bounds__(256) wgrad_kernel(const T* __restrict__ dout, 
   for (int e = threadIdx.x; e < npairs; e += blockDim.x) atomicAdd(dM + e, acc[e]);
 }
 
-int sms() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
+int sms() { return device_sm_count(); }
 
 template <typename T>
 cudaError_t mix_t(const void* in, const void* M, void* out, int B, int Ci, int Co, int HW, bool trans, cudaStream_t s) {

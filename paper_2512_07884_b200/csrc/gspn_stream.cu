@@ -42,6 +42,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <mutex>
 
 #include "gspn_common.cuh"
@@ -2228,27 +2229,8 @@ bool encode(CUtensorMap* m, const void* base, gspn_dtype_t dt, int64_t W, int64_
   return r == CUDA_SUCCESS;
 }
 
-int sm_count() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
-
-int smem_optin() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    if (n <= 0) n = 227 * 1024;
-  }
-  return n;
-}
+int sm_count() { return device_sm_count(); }
+int smem_optin() { return device_smem_optin(); }
 
 constexpr int kSmemTail = 26624;  // mbarriers (3 per stage), exchange rows (3 x 2 x 16 x 64 floats = 24 KB), cluster edges
 
@@ -2382,7 +2364,7 @@ cudaError_t launch(KernelT kernel, const StreamArgs& A, cudaStream_t s) {
     cfg.stream = s;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cfg.gridDim = dim3(static_cast<unsigned>(A.plan.cl * 148), 1, 1);
+    cfg.gridDim = dim3(static_cast<unsigned>(A.plan.cl * sm_count()), 1, 1);
     int ncl = 0;
     e = cudaOccupancyMaxActiveClusters(&ncl, kernel, &cfg);
     if (e != cudaSuccess) return e;
@@ -2449,9 +2431,9 @@ size_t stream_bwd_workspace_bytes(int64_t B, int64_t C, int64_t H, int64_t W, in
 
 cudaError_t launch_fwd_stream(const ScanParams& p, gspn_dtype_t dt, cudaStream_t s, int* launches, bool* handled) {
   *handled = false;
-  static StreamArgs A;  // large (~2 KB): keep off the stack; the launch copies it into the parameter buffer
-  static std::mutex mu;
-  std::lock_guard<std::mutex> lock(mu);
+  // per call, on the heap (~2 KB): no shared launch state; the launch copies it into the parameter buffer
+  std::unique_ptr<StreamArgs> hold(new StreamArgs());
+  StreamArgs& A = *hold;
   memset(&A, 0, sizeof A);
   A.p = p;
   if (!make_plan(p, dt, F_NIN, &A.plan)) return cudaSuccess;
@@ -2475,10 +2457,9 @@ cudaError_t launch_fwd_stream(const ScanParams& p, gspn_dtype_t dt, cudaStream_t
 bool launch_out_tma(const ScanParams& p, const void* g, gspn_dtype_t dt, cudaStream_t s, cudaError_t* err,
                     bool vert_done = false, bool dry_run = false) {
   const bool grouped = p.G != p.C;
-  static OutArgs A;
-  static std::mutex mu;
-  std::lock_guard<std::mutex> lock(mu);
   if (knob("GSPN_OUT_REG")) return false;  // experiments: register-staged kernel
+  std::unique_ptr<OutArgs> hold(new OutArgs());
+  OutArgs& A = *hold;
   memset(&A, 0, sizeof A);
   A.p = p;
   const int es = dt == GSPN_BF16 ? 2 : 4;
@@ -2587,10 +2568,9 @@ cudaError_t launch_dx(const ScanParams& p, const void* g, cudaStream_t s) {
 // one persistent launch for the recurrence + tap gradients, one elementwise launch for dlam / dx.
 // Returns false (nothing launched) when the shape takes the split path.
 bool launch_bwd_fused(const ScanParams& p0, gspn_dtype_t dt, cudaStream_t s, int* launches, cudaError_t* err) {
-  static StreamArgs A;
-  static std::mutex mu;
-  std::lock_guard<std::mutex> lock(mu);
   if (p0.G != p0.C || knob("GSPN_NOFUSE")) return false;
+  std::unique_ptr<StreamArgs> hold(new StreamArgs());
+  StreamArgs& A = *hold;
   const int es = dt == GSPN_BF16 ? 2 : 4;
   if ((p0.B * p0.C * p0.H * p0.W * es) % 16 != 0) return false;  // dx kernel: 16-byte vectors per slab
   memset(&A, 0, sizeof A);
@@ -2660,9 +2640,8 @@ cudaError_t launch_bwd_stream(const ScanParams& p0, gspn_dtype_t dt, cudaStream_
     }
   }
   *path = "stream";
-  static StreamArgs A;
-  static std::mutex mu;
-  std::lock_guard<std::mutex> lock(mu);
+  std::unique_ptr<StreamArgs> hold(new StreamArgs());
+  StreamArgs& A = *hold;
   memset(&A, 0, sizeof A);
   A.p = p0;
   ScanParams& p = A.p;

@@ -176,3 +176,73 @@ def test_missing_library_fails_loudly(monkeypatch):
     monkeypatch.setattr(_lib, "LIBGSPN", "/nonexistent/libgspn.so")
     with pytest.raises(ImportError, match="not built"):
         _lib.lib()
+
+
+# ---------------------------------------------------------------- binding shape checks (before any CUDA call)
+
+def _bind_inputs(B=1, C=4, G=4, H=8, W=8, dirs=0xF):
+    import torch
+
+    D = bin(dirs).count("1")
+    x = torch.zeros(B, C, H, W)
+    w = [torch.zeros(D, B, G, H, W) for _ in range(3)]
+    lam = torch.zeros(D, B, C, H, W)
+    return x, w, lam
+
+
+@pytest.mark.parametrize("bad", ["w_l", "lam", "h", "dh", "dx", "dw_m", "dlam", "dirs"])
+def test_bwd_rejects_mis_shaped_tensors(bad):
+    """A mis-shaped tensor must raise ValueError in the binding: the ABI sees only pointers."""
+    import torch
+
+    x, (wl, wm, wr), lam = _bind_inputs()
+    h, dh = torch.zeros_like(lam), torch.zeros_like(lam)
+    outs = [torch.zeros_like(x), torch.zeros_like(wl), torch.zeros_like(wm), torch.zeros_like(wr),
+            torch.zeros_like(lam)]
+    dirs = 0xF
+    if bad == "w_l":
+        wl = torch.zeros(4, 1, 2, 8, 8)
+    elif bad == "lam":
+        lam = torch.zeros(4, 1, 4, 8, 9)
+    elif bad == "h":
+        h = torch.zeros(3, 1, 4, 8, 8)
+    elif bad == "dh":
+        dh = torch.zeros(1, 4, 8, 8)  # the merged dy passed as dh
+    elif bad == "dx":
+        outs[0] = torch.zeros(1, 4, 8, 7)
+    elif bad == "dw_m":
+        outs[2] = torch.zeros(4, 1, 1, 8, 8)
+    elif bad == "dlam":
+        outs[4] = torch.zeros(4, 2, 4, 8, 8)
+    elif bad == "dirs":
+        dirs = 0x3  # D = 2 does not match the 4 direction slabs
+    with pytest.raises(ValueError, match="shape"):
+        gspn.bwd(x, wl, wm, wr, lam, h, dh, dirs, 4, outs=tuple(outs))
+
+
+def test_fwd_and_aux_reject_mis_shaped_outputs():
+    import torch
+
+    x, (wl, wm, wr), lam = _bind_inputs()
+    with pytest.raises(ValueError, match="shape"):
+        gspn.fwd(x, wl, wm, wr, lam, 0xF, 4, out=torch.zeros(4, 1, 4, 8, 7))
+    h = torch.zeros_like(lam)
+    with pytest.raises(ValueError, match="shape"):
+        gspn.merge_fwd(h, h, 0xF, out=torch.zeros(1, 4, 8, 9))
+    with pytest.raises(ValueError, match="shape"):
+        gspn.merge_bwd(h, h, torch.zeros(1, 4, 8, 8), 0xF, outs=(torch.zeros_like(h), torch.zeros(4, 1, 4, 8, 1)))
+    with pytest.raises(ValueError, match="shape"):
+        gspn.proxy_mix(torch.zeros(2, 6, 4, 4), torch.zeros(3, 6), out=torch.zeros(2, 3, 4, 5))
+    with pytest.raises(ValueError, match="shape"):
+        gspn.proxy_wgrad(torch.zeros(2, 3, 4, 4), torch.zeros(2, 6, 4, 5))
+    with pytest.raises(ValueError, match="shape"):
+        gspn.proxy_wgrad(torch.zeros(2, 3, 4, 4), torch.zeros(2, 6, 4, 4), out=torch.zeros(6, 3))
+
+
+def test_proxy_rejects_32bit_overflowing_extents():
+    """The proxy kernels index pixels in 32 bits: H*W >= 2^31 must be refused, not truncated."""
+    L = gspn.lib()
+    st = L.gspn_proxy_mix(A, A, A + (1 << 40), 1, 1, 1, 46341, 46342, 1, 0, None)
+    assert st == 2 and "INT32_MAX" in detail()
+    st = L.gspn_proxy_wgrad(A, A + (1 << 40), A + (1 << 41), 1, 1, 1, 46341, 46342, 1, None)
+    assert st == 2 and "INT32_MAX" in detail()
