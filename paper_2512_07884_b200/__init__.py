@@ -24,6 +24,7 @@ FLAG_PRENORMALIZED = 0x1
 FLAG_FORCE_GENERIC = 0x2
 FLAG_MERGE_MEAN = 0x4
 FLAG_PROXY_TRANSPOSE = 0x8
+FLAG_FORCE_SPLIT = 0x10
 DTYPE_F32, DTYPE_BF16 = 0, 1
 
 

@@ -41,7 +41,7 @@ gspn_status_t check_dims(int64_t B, int64_t C, int64_t H, int64_t W, uint32_t di
   if (C % G != 0) return fail(GSPN_ERR_INVALID_ARG, "%s: C %% groups != 0 (groups=%lld)", "groups", G);
   if (dirs == 0 || dirs > 15) return fail(GSPN_ERR_INVALID_ARG, "%s must be in [1, 15] (got %lld)", "dirs", dirs);
   if (dt != GSPN_F32 && dt != GSPN_BF16) return fail(GSPN_ERR_INVALID_ARG, "%s unknown (%lld)", "dtype", (long long)dt);
-  if (flags & ~(GSPN_FLAG_PRENORMALIZED | GSPN_FLAG_FORCE_GENERIC))
+  if (flags & ~(GSPN_FLAG_PRENORMALIZED | GSPN_FLAG_FORCE_GENERIC | GSPN_FLAG_FORCE_SPLIT))
     return fail(GSPN_ERR_INVALID_ARG, "%s has unknown bits (0x%llx)", "flags", flags);
   // Overflow guard: the largest tensor (D*B*C*H*W elements) must stay far below 2^62 bytes, and the
   // chain count must fit a 1-D grid.
@@ -176,8 +176,9 @@ gspn_status_t gspn_fwd_local(const void* x, const void* w_l, const void* w_m, co
     cudaError_t e = cudaSuccess;
     const char* path = "generic";
     if (!(flags & GSPN_FLAG_FORCE_GENERIC)) {
-      e = gspn::launch_fwd_stream(p, dtype, cs, &launches, &handled);
-      if (handled) path = "stream";
+      const char* spath = "stream";
+      e = gspn::launch_fwd_stream(p, dtype, cs, &launches, &handled, &spath);
+      if (handled) path = spath;
       if (e == cudaSuccess && !handled && gspn::small_eligible(p)) {
         e = gspn::launch_fwd_small(p, dtype, cs, &launches);
         handled = true;

@@ -24,8 +24,10 @@ cudaError_t launch_fwd_small(const ScanParams& p, gspn_dtype_t dt, cudaStream_t 
 cudaError_t launch_bwd_small(const ScanParams& p, gspn_dtype_t dt, cudaStream_t s, int* launches);
 
 // Fast TMA-streaming path (gspn_stream.cu). *handled = false when the shape is not eligible.
-cudaError_t launch_fwd_stream(const ScanParams& p, gspn_dtype_t dt, cudaStream_t s, int* launches, bool* handled);
-// Backward: *path = "stream-fused" (recurrence + tap gradients in one pass, G = C) or "stream" (split).
+// *path = "stream" or "stream-cluster" (P-split over a thread-block cluster)
+cudaError_t launch_fwd_stream(const ScanParams& p, gspn_dtype_t dt, cudaStream_t s, int* launches, bool* handled,
+                              const char** path);
+// Backward: *path = "stream-fused" (recurrence + tap gradients in one pass, G = C) or "stream" (split; "stream-cluster" when P-split).
 cudaError_t launch_bwd_stream(const ScanParams& p, gspn_dtype_t dt, cudaStream_t s, int* launches, bool* handled,
                               const char** path);
 size_t stream_bwd_workspace_bytes(int64_t B, int64_t C, int64_t H, int64_t W, int64_t D, int64_t G, gspn_dtype_t dt);

@@ -2254,10 +2254,16 @@ bool make_plan(const ScanParams& p, gspn_dtype_t dt, int nin, Plan* pl) {
   pl->nwc = static_cast<int>((maxP + pl->own - 1) / pl->own);  // warp w owns [w own, (w+1) own)
   // positions any lane reads (clamped to the tile); the TMA boxes cover them so no lane reads stale rows
   int cover = static_cast<int>(std::min<int64_t>(kPpad, (pl->nwc - 1) * pl->own - GH + 64));
-  if (pl->nwc > 11) {
+  const bool force_split = (p.flags & GSPN_FLAG_FORCE_SPLIT) != 0;
+  if (pl->nwc > 11 || force_split) {
     // P-split over a cluster: each CTA owns the positions its warps own while their ghosts stay
-    // inside its 512-position tile (10 x 48 bf16 / 9 x 56 fp32)
-    const int nwc_c = (kPpad - 2 * GH) / pl->own;
+    // inside its 512-position tile (10 x 48 bf16 / 9 x 56 fp32). GSPN_FLAG_FORCE_SPLIT (tests): at
+    // least 2 CTAs per chain, so the cluster path can be checked bitwise against the unsplit one.
+    int nwc_c = (kPpad - 2 * GH) / pl->own;
+    if (force_split) {
+      const int64_t half = (maxP + 1) / 2;
+      nwc_c = std::max(1, std::min<int>(nwc_c, static_cast<int>((half + pl->own - 1) / pl->own)));
+    }
     pl->ownc = nwc_c * pl->own;
     pl->cl = static_cast<int>((maxP + pl->ownc - 1) / pl->ownc);
     if (pl->cl > 8 || knob("GSPN_NOCLUSTER")) return false;
@@ -2429,7 +2435,8 @@ size_t stream_bwd_workspace_bytes(int64_t B, int64_t C, int64_t H, int64_t W, in
   return ws_layout(B, C, H, W, D, dt).total;
 }
 
-cudaError_t launch_fwd_stream(const ScanParams& p, gspn_dtype_t dt, cudaStream_t s, int* launches, bool* handled) {
+cudaError_t launch_fwd_stream(const ScanParams& p, gspn_dtype_t dt, cudaStream_t s, int* launches, bool* handled,
+                              const char** path) {
   *handled = false;
   // per call, on the heap (~2 KB): no shared launch state; the launch copies it into the parameter buffer
   std::unique_ptr<StreamArgs> hold(new StreamArgs());
@@ -2446,6 +2453,7 @@ cudaError_t launch_fwd_stream(const ScanParams& p, gspn_dtype_t dt, cudaStream_t
   const int mode = norm_mode(p, A.plan);
   cudaError_t e;
   const bool cl = A.plan.cl > 1;
+  *path = cl ? "stream-cluster" : "stream";
   const bool local = p.kchunk > 0;
   if (dt == GSPN_BF16) e = cl ? launch_fwd<BF, true>(mode, local, A, s) : launch_fwd<BF, false>(mode, local, A, s);
   else e = cl ? launch_fwd<float, true>(mode, local, A, s) : launch_fwd<float, false>(mode, local, A, s);
@@ -2659,6 +2667,7 @@ cudaError_t launch_bwd_stream(const ScanParams& p0, gspn_dtype_t dt, cudaStream_
   using BF = __nv_bfloat16;
   const int mode = norm_mode(p, A.plan);
   const bool cl = A.plan.cl > 1;
+  if (cl) *path = "stream-cluster";
   const bool local = p.kchunk > 0;
   if (dt == GSPN_BF16) e = cl ? launch_bwd<BF, true>(mode, local, A, s) : launch_bwd<BF, false>(mode, local, A, s);
   else e = cl ? launch_bwd<float, true>(mode, local, A, s) : launch_bwd<float, false>(mode, local, A, s);

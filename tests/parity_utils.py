@@ -2,6 +2,9 @@
 the CUDA path), the oracle run on them, and the normwise error metric (R16)."""
 from __future__ import annotations
 
+import json
+import os
+
 import numpy as np
 
 import synth
@@ -20,6 +23,30 @@ def normwise(got: np.ndarray, ref: np.ndarray) -> float:
     if den == 0.0:
         return 0.0 if num == 0.0 else float("inf")
     return float(num / den)
+
+
+def record(test: str, name: str, err: float, tol: float) -> None:
+    """Append one measured normwise error to $GSPN_ERRLOG (JSON lines; the GPU scripts set it to
+    gpurun_out/parity_errors.jsonl, summarised under profiles/), so the margin to the tolerance is on record."""
+    path = os.environ.get("GSPN_ERRLOG")
+    if not path:
+        return
+    with open(path, "a") as f:
+        f.write(json.dumps({"test": test, "tensor": name, "normwise": err, "tol": tol}) + "\n")
+
+
+def check(test: str, name: str, got, ref, tol: float, per_slab: bool = True) -> float:
+    """normwise(got, ref) <= tol per direction slab (5-D tensors) or whole; records and returns the max."""
+    got, ref = np.asarray(got), np.asarray(ref)
+    if per_slab and got.ndim == 5:
+        errs = [normwise(got[k], ref[k]) for k in range(got.shape[0])]
+    else:
+        errs = [normwise(got, ref)]
+    e = max(errs)
+    record(test, name, e, tol)
+    for k, ek in enumerate(errs):
+        assert ek <= tol, f"{test}: {name}[slab {k}] normwise {ek:.3e} > {tol}"
+    return e
 
 
 def small_config(B, C, G, H, W, dirs, dtype, cfg_id=90) -> Config:

@@ -16,7 +16,7 @@ import paper_2512_07884_b200 as gspn
 import synth
 from synth.configs import get_config
 from synth.device import make_inputs
-from tests.parity_utils import TOL, from_torch, normwise, unit_inputs
+from tests.parity_utils import TOL, check, from_torch, normwise, record, unit_inputs
 
 pytestmark = pytest.mark.gpu
 NTHREADS = oracle.default_threads()
@@ -55,18 +55,15 @@ def _check_unit(cfg, t, h, grads, u, kchunk=0):
     gr = oracle.bwd(f["x"], f["w_l"], f["w_m"], f["w_r"], f["lam"], h_ref, f["dh"], cfg.dirs, 1, threads=1,
                     kchunk=kchunk)
     tol = TOL[cfg.dtype]
-    got_h = from_torch(h[:, b:b + 1, c0:c0 + Cg])
-    for k in range(cfg.D):
-        assert normwise(got_h[k], h_ref[k]) <= tol, f"unit {u} h slab {k}"
+    import os
+
+    test = os.environ.get("PYTEST_CURRENT_TEST", "?").split(" ")[0] + f"[unit {u}]"
+    check(test, "h", from_torch(h[:, b:b + 1, c0:c0 + Cg]), h_ref, tol)
     got = [from_torch(grads[0][b:b + 1, c0:c0 + Cg])] + \
           [from_torch(grads[i][:, b:b + 1, g:g + 1]) for i in (1, 2, 3)] + \
           [from_torch(grads[4][:, b:b + 1, c0:c0 + Cg])]
     for name, a, r in zip(("dx", "dw_l", "dw_m", "dw_r", "dlam"), got, gr):
-        if a.ndim == 5:
-            for k in range(cfg.D):
-                assert normwise(a[k], r[k]) <= tol, f"unit {u} {name} slab {k}: {normwise(a[k], r[k]):.3e}"
-        else:
-            assert normwise(a, r) <= tol, f"unit {u} {name}: {normwise(a, r):.3e}"
+        check(test, name, a, r, tol)
 
 
 def _dot(a, b):
@@ -94,9 +91,13 @@ def _check_identities(cfg, t, h, grads):
     assert float(e.abs().max()) <= 4 * tol * float(mag.max())
 
 
-@pytest.mark.parametrize("name,nunits", [("1", 8), ("2", 4), ("3a", 64), ("3b", 3), ("4", 3)])
-def test_config_sampled_parity(name, nunits, cuda_device):
+@pytest.mark.parametrize("name,nunits,dtype", [("1", 8, None), ("2", 4, None), ("3a", 64, None), ("3a", 64, "f32"),
+                                               ("3b", 3, None), ("4", 3, None)])
+def test_config_sampled_parity(name, nunits, dtype, cuda_device):
+    """dtype None: the config's own I/O dtype; "f32": the fp32 parity run SURVEY §8 asks for (3a)."""
     cfg = get_config(name)
+    if dtype:
+        cfg = cfg.with_(dtype=dtype)
     t, h, grads = _run(cfg, cuda_device)
     for u in _sample_units(cfg, nunits):
         _check_unit(cfg, t, h, grads, u)
@@ -114,14 +115,18 @@ def test_config_sampled_parity_local(name, nunits, kchunk, cuda_device):
 
 
 @pytest.mark.slow
-def test_config5_parity(cuda_device):
-    """Config 5: one unit of 40 channels over 2048^2. h, dx, dlam on sampled channels from per-channel
-    oracle runs; dw (summed over all 40 channels) from the sum of per-channel oracle runs, which equals
-    the grouped result because the normalisation Jacobian is linear in the tap gradients
-    (tests/test_oracle.py::test_grouped_dw_is_channel_sum_of_per_channel)."""
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_config5_parity(dtype, cuda_device):
+    """Config 5: one unit of 40 channels over 2048^2 (L = P = 2048), bf16 and the fp32 parity run. h, dx,
+    dlam on sampled channels from per-channel oracle runs; dw (summed over all 40 channels) from the sum
+    of per-channel oracle runs, which equals the grouped result because the normalisation Jacobian is
+    linear in the tap gradients (tests/test_oracle.py::test_grouped_dw_is_channel_sum_of_per_channel).
+    The oracle runs on the UNROUNDED fp64 h (end to end); the measured margins go to $GSPN_ERRLOG."""
+    import os
     from concurrent.futures import ThreadPoolExecutor
 
-    cfg = get_config("5")
+    cfg = get_config("5").with_(dtype=dtype)
+    test = os.environ.get("PYTEST_CURRENT_TEST", "?").split(" ")[0]
     t, h, grads = _run(cfg, cuda_device)
     _check_identities(cfg, t, h, grads)
     HW = cfg.H * cfg.W
@@ -155,15 +160,8 @@ def test_config5_parity(cuda_device):
             for i in range(3):
                 dw_sum[i] += gr[1 + i]
             if c in sampled:
-                gh = from_torch(h[:, 0:1, c:c + 1])
-                for k in range(D):
-                    assert normwise(gh[k], hr[k]) <= tol
-                assert normwise(from_torch(grads[0][0:1, c:c + 1]), gr[0]) <= tol
-                gl = from_torch(grads[4][:, 0:1, c:c + 1])
-                for k in range(D):
-                    assert normwise(gl[k], gr[4][k]) <= tol
-    for i in range(3):
-        got = from_torch(grads[1 + i])
-        for k in range(D):
-            e = normwise(got[k], dw_sum[i][k])
-            assert e <= tol, f"dw[{i}] slab {k}: {e:.3e}"
+                check(test, f"h[c={c}]", from_torch(h[:, 0:1, c:c + 1]), hr, tol)
+                check(test, f"dx[c={c}]", from_torch(grads[0][0:1, c:c + 1]), gr[0], tol)
+                check(test, f"dlam[c={c}]", from_torch(grads[4][:, 0:1, c:c + 1]), gr[4], tol)
+    for i, n in enumerate(("dw_l", "dw_m", "dw_r")):
+        check(test, n, from_torch(grads[1 + i]), dw_sum[i], tol)
