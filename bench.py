@@ -6,10 +6,14 @@
 One "step" = one gspn_fwd + one gspn_bwd call (every SURVEY.md §8(a) row) over one batch of synthetic,
 device-generated inputs already resident in HBM. Metric (BASELINE.json): algorithmic HBM GB/s of the
 fwd+bwd scan, (bytes_fwd + bytes_bwd) / device time, bytes per SURVEY.md §8(d). Multi-GPU: one process
-per GPU (torchrun), units (b, g) sharded across ranks with no data-path collective; by default each
-rank owns one full configuration's worth of units (weak scaling); --scaling strong splits the one
-configuration instead (config 5 then needs the dw all-reduce over NCCL). Timing: CUDA events on the
-launching stream, barrier + synchronize around the timed region, max over ranks.
+per GPU; `--gpus N` without a torchrun environment re-executes itself under torch.distributed.run with
+N ranks. By default (--scaling strong) the ranks split ONE configuration: units (b, g) sharded
+contiguously with no data-path collective, or -- for the single-unit config 5 -- channels, with the fp32
+partial dw all-reduced over NCCL on a side stream (timed separately); --scaling weak gives every rank a
+whole configuration (also measured and reported under `weak` at N > 1). The optional h all-gather
+(north_star's "final output all-gather") is timed separately. Timing: CUDA events on the launching
+stream, barrier + synchronize around the timed region, max over ranks; per-step median / p10 / p90.
+At N = 1 the line also carries short runs of the other BASELINE configs (`configs`).
 
 --impl reference times the fp64 CPU oracle (oracle/, the tier's reference arm) on bounded samples of
 the same workload on this host's cores; it never touches the GPU path.
@@ -41,7 +45,11 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="4")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
+                    help="strong (default): the N ranks split one configuration; weak: one configuration per rank")
+    ap.add_argument("--no-others", action="store_true",
+                    help="skip the short runs of the other BASELINE configs reported under `configs` (N = 1)")
+    ap.add_argument("--other-steps", type=int, default=10)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-next", action="store_true", help="skip the SURVEY §8(f) rows (merge, GSPN-local)")
@@ -164,16 +172,17 @@ def oracle_time(sm, seconds: float):
     passes, t0 = 0, time.perf_counter()
     while True:
         h = oracle.fwd(sm["x"], *sm["ws"], sm["lam"], sm["dirs"], 1, threads=sm["threads"])
-        oracle.bwd(sm["x"], *sm["ws"], sm["lam"], h, sm["dh"], sm["dirs"], 1, threads=sm["threads"])
+        g = oracle.bwd(sm["x"], *sm["ws"], sm["lam"], h, sm["dh"], sm["dirs"], 1, threads=sm["threads"])
         passes += 1
         wall = time.perf_counter() - t0
         if wall >= seconds:
             break
-    return passes * sm["bytes"], wall, sm["threads"], f"{sm['desc']}; {passes} pass(es)"
+    last = {"h": h, "dx": g[0], "dw_l": g[1], "dw_m": g[2], "dw_r": g[3], "dlam": g[4]}
+    return passes * sm["bytes"], wall, sm["threads"], f"{sm['desc']}; {passes} pass(es)", last
 
 
 def oracle_sample(cfg, seconds: float):
-    return oracle_time(oracle_prepare(cfg), seconds)
+    return oracle_time(oracle_prepare(cfg), seconds)[:4]
 
 
 def run_reference(args):
@@ -189,7 +198,7 @@ def run_reference(args):
         oracle_time(sm, per_step / 2)
     vals, walls, desc, threads = [], [], "", 1
     for _ in range(args.steps):
-        b, w, threads, desc = oracle_time(sm, per_step)
+        b, w, threads, desc, _ = oracle_time(sm, per_step)
         vals.append(b / w / 1e9)
         walls.append(w)
     value = statistics.median(vals)
@@ -208,18 +217,178 @@ def run_reference(args):
 
 # ------------------------------------------------------------------------------------------ our arm
 
+def pct(vals, q):
+    v = sorted(vals)
+    if not v:
+        return None
+    k = (len(v) - 1) * q
+    lo, hi = int(k), min(int(k) + 1, len(v) - 1)
+    return v[lo] + (v[hi] - v[lo]) * (k - lo)
+
+
+def summary(vals):
+    return {"median": pct(vals, 0.5), "p10": pct(vals, 0.1), "p90": pct(vals, 0.9)}
+
+
+class Workload:
+    """One rank's share of a configuration: device-generated inputs, outputs, workspace and the step."""
+
+    def __init__(self, gspn, base, scaling, rank, world, dev, flags=0):
+        import torch
+
+        from synth.device import make_inputs, shard_for
+
+        self.gspn, self.dev = gspn, dev
+        self.base = base
+        self.gcfg = base.with_(B=base.B * world) if scaling == "weak" else base
+        self.sh = shard_for(self.gcfg, rank, world)
+        sh, g = self.sh, self.gcfg
+        self.t = make_inputs(g, dev, sh)
+        self.dt_code = gspn.DTYPE_BF16 if g.dtype == "bf16" else gspn.DTYPE_F32
+        # a single unit split by channel: each rank's dw is a partial sum over its channels, reduced in fp32
+        self.channel_split = sh.kind == "channels"
+        self.flags = flags | (gspn.FLAG_DW_F32 if self.channel_split else 0)
+        self.h = torch.empty_like(self.t["lam"])
+        if self.channel_split:
+            self.dwbuf = torch.empty((3,) + tuple(self.t["w_l"].shape), dtype=torch.float32, device=dev)
+            dw = (self.dwbuf[0], self.dwbuf[1], self.dwbuf[2])
+        else:
+            self.dwbuf = None
+            dw = (torch.empty_like(self.t["w_l"]), torch.empty_like(self.t["w_m"]), torch.empty_like(self.t["w_r"]))
+        self.outs = (torch.empty_like(self.t["x"]),) + dw + (torch.empty_like(self.t["lam"]),)
+        wsb = gspn.workspace_bytes(sh.B, sh.C, g.H, g.W, g.dirs, sh.G, self.dt_code)
+        self.ws = torch.empty(max(wsb, 16), dtype=torch.uint8, device=dev)
+        self.bytes_f = gspn.algorithmic_bytes(sh.B, sh.C, g.H, g.W, g.dirs, sh.G, self.dt_code, False)
+        self.bytes_b = gspn.algorithmic_bytes(sh.B, sh.C, g.H, g.W, g.dirs, sh.G, self.dt_code, True)
+        self.work_bytes = sum(v.numel() * v.element_size() for v in self.t.values() if v is not None) + \
+            self.h.numel() * self.h.element_size() + sum(o.numel() * o.element_size() for o in self.outs)
+        self.launches = {"fwd": 0, "bwd": 0}
+        self.paths = {"fwd": None, "bwd": None}
+
+    def fwd(self):
+        t, g = self.t, self.gcfg
+        self.gspn.fwd(t["x"], t["w_l"], t["w_m"], t["w_r"], t["lam"], g.dirs, self.sh.G,
+                      flags=self.flags & ~self.gspn.FLAG_DW_F32, out=self.h)
+        self.launches["fwd"] = self.gspn.last_launch_count()
+        self.paths["fwd"] = self.gspn.last_path()
+
+    def bwd(self):
+        t, g = self.t, self.gcfg
+        self.gspn.bwd(t["x"], t["w_l"], t["w_m"], t["w_r"], t["lam"], self.h, t["dh"], g.dirs, self.sh.G,
+                      flags=self.flags, outs=self.outs, workspace=self.ws)
+        self.launches["bwd"] = self.gspn.last_launch_count()
+        self.paths["bwd"] = self.gspn.last_path()
+
+    def free(self):
+        for k in list(self.__dict__):
+            if k not in ("gspn", "dev", "base", "gcfg", "sh", "bytes_f", "bytes_b", "launches", "paths", "dt_code",
+                         "channel_split", "flags", "work_bytes"):
+                setattr(self, k, None)
+
+
+def time_steps(wl, steps, warmup, stream, dev, world, dist, comm=None):
+    """W untimed warm-up steps, then EXACTLY `steps` timed steps bracketed by barrier + synchronize.
+    Per-step CUDA events on the launching stream: [start, fwd done, bwd done]; the config-5 fp32 dw
+    all-reduce (channel split) runs on the side stream `comm`, overlapping the next step's fwd, and is
+    timed there. Returns per-step lists (ms) and the region time (ms per step), max over ranks."""
+    import torch
+
+    flush = wl.work_bytes < 4 * L2_BYTES
+    flush_buf = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=dev) if flush else None
+    comm_done = torch.cuda.Event()
+    comm_done.record(stream)
+
+    def step(evs=None):
+        if evs:
+            evs[0].record(stream)
+        wl.fwd()
+        if evs:
+            evs[1].record(stream)
+        stream.wait_event(comm_done)  # the previous step's reduction has read dw
+        wl.bwd()
+        if evs:
+            evs[2].record(stream)
+        if wl.channel_split:
+            comm.wait_stream(stream)
+            with torch.cuda.stream(comm):
+                if evs:
+                    evs[3].record(comm)
+                dist.all_reduce(wl.dwbuf)  # fp32 partial dw, NCCL over NVLink
+                if evs:
+                    evs[4].record(comm)
+            comm_done.record(comm)
+
+    for _ in range(warmup):
+        step()
+        if flush:
+            flush_buf.zero_()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    evs_all = []
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(steps):
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(5 if wl.channel_split else 3)]
+        step(evs)
+        evs_all.append(evs)
+        if flush:
+            flush_buf.zero_()
+    if wl.channel_split:
+        stream.wait_event(comm_done)
+    ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    f_ms = [e[0].elapsed_time(e[1]) for e in evs_all]
+    b_ms = [e[1].elapsed_time(e[2]) for e in evs_all]
+    c_ms = [e[3].elapsed_time(e[4]) for e in evs_all] if wl.channel_split else []
+    region = ev0.elapsed_time(ev1) / steps
+    vec = torch.tensor([region, pct(f_ms, 0.5), pct(b_ms, 0.5), pct(c_ms, 0.5) or 0.0], dtype=torch.float64,
+                       device=dev)
+    if world > 1:
+        dist.all_reduce(vec, op=dist.ReduceOp.MAX)
+    region, fmed, bmed, cmed = [float(v) for v in vec.tolist()]
+    return {"f": f_ms, "b": b_ms, "c": c_ms, "step": [a + b for a, b in zip(f_ms, b_ms)], "region": region,
+            "f_med": fmed, "b_med": bmed, "c_med": cmed, "flush": flush}
+
+
+def unit_slices(wl, n):
+    """Host copies of the outputs of units (b, g) 0..n-1 (a full, unsharded workload), laid out like the
+    oracle sample of `oracle_prepare` (units as the batch dimension, C/G channels, G = 1)."""
+    import torch
+
+    g = wl.gcfg
+    Cg = g.C // g.G
+    h, (dx, dwl, dwm, dwr, dlam) = wl.h, wl.outs
+    out = {k: [] for k in ("h", "dx", "dw_l", "dw_m", "dw_r", "dlam")}
+    for u in range(n):
+        b, gr = divmod(u, g.G)
+        c0 = gr * Cg
+        out["h"].append(h[:, b, c0:c0 + Cg])
+        out["dlam"].append(dlam[:, b, c0:c0 + Cg])
+        out["dx"].append(dx[b, c0:c0 + Cg])
+        for name, t in (("dw_l", dwl), ("dw_m", dwm), ("dw_r", dwr)):
+            out[name].append(t[:, b, gr:gr + 1])
+    res = {}
+    for k, v in out.items():
+        st = torch.stack(v, dim=0 if k == "dx" else 1)
+        res[k] = st.to(torch.float64).cpu().numpy()
+    return res
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
 
     import paper_2512_07884_b200 as gspn
     from synth.configs import get_config
-    from synth.device import make_inputs, shard_for
 
     rank, world, local = dist_env()
-    if world != args.gpus:
-        if rank == 0:
-            print(f"warning: WORLD_SIZE={world} but --gpus {args.gpus}; using WORLD_SIZE", file=sys.stderr)
+    if world != args.gpus and rank == 0:
+        print(f"warning: WORLD_SIZE={world} but --gpus {args.gpus}; using WORLD_SIZE", file=sys.stderr)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -228,101 +397,83 @@ def run_ours(args):
     base = get_config(args.config)
     if args.dirs is not None:
         base = base.with_(dirs=args.dirs)
-    if args.scaling == "weak":
-        gcfg = base.with_(B=base.B * world)  # each rank owns one configuration's worth of units
-    else:
-        gcfg = base
-    sh = shard_for(gcfg, rank, world)
-    t = make_inputs(gcfg, dev, sh)
-    D = gcfg.D
-    dt_code = gspn.DTYPE_BF16 if gcfg.dtype == "bf16" else gspn.DTYPE_F32
-    h = torch.empty_like(t["lam"])
-    outs = (torch.empty_like(t["x"]), torch.empty_like(t["w_l"]), torch.empty_like(t["w_m"]),
-            torch.empty_like(t["w_r"]), torch.empty_like(t["lam"]))
-    wsb = gspn.workspace_bytes(sh.B, sh.C, gcfg.H, gcfg.W, gcfg.dirs, sh.G, dt_code)
-    ws = torch.empty(max(wsb, 16), dtype=torch.uint8, device=dev)
-    bytes_f = gspn.algorithmic_bytes(sh.B, sh.C, gcfg.H, gcfg.W, gcfg.dirs, sh.G, dt_code, False)
-    bytes_b = gspn.algorithmic_bytes(sh.B, sh.C, gcfg.H, gcfg.W, gcfg.dirs, sh.G, dt_code, True)
-    need_allreduce = sh.kind == "channels"  # one unit split by channel: dw partial sums must be reduced
-    work_bytes = sum(v.numel() * v.element_size() for v in t.values() if v is not None) + \
-        h.numel() * h.element_size() + sum(o.numel() * o.element_size() for o in outs)
-    flush = work_bytes < 4 * L2_BYTES
-    flush_buf = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=dev) if flush else None
+    wl = Workload(gspn, base, args.scaling, rank, world, dev, args.flags)
+    gcfg, sh = wl.gcfg, wl.sh
     stream = torch.cuda.current_stream(dev)
-    launches = {"fwd": 0, "bwd": 0}
+    comm = torch.cuda.Stream(dev) if wl.channel_split else None
 
-    def step(evs=None):
-        if evs:
-            evs[0].record(stream)
-        gspn.fwd(t["x"], t["w_l"], t["w_m"], t["w_r"], t["lam"], gcfg.dirs, sh.G, flags=args.flags, out=h)
-        launches["fwd"] = gspn.last_launch_count()
-        if evs:
-            evs[1].record(stream)
-        gspn.bwd(t["x"], t["w_l"], t["w_m"], t["w_r"], t["lam"], h, t["dh"], gcfg.dirs, sh.G, flags=args.flags,
-                 outs=outs, workspace=ws)
-        launches["bwd"] = gspn.last_launch_count()
-        if need_allreduce:
-            for o in outs[1:4]:
-                dist.all_reduce(o)  # bf16/fp32 in place; NCCL over NVLink
-        if evs:
-            evs[2].record(stream)
-
-    for _ in range(args.warmup):
-        step()
-        if flush:
-            flush_buf.zero_()
-    torch.cuda.synchronize(dev)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
     clocks = ClockSampler(local)
     clocks.start()
-    evs_all = []
     t_wall0 = time.perf_counter()
-    ev_start = torch.cuda.Event(enable_timing=True)
-    ev_end = torch.cuda.Event(enable_timing=True)
-    ev_start.record(stream)
-    for _ in range(args.steps):
-        evs = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-        step(evs)
-        evs_all.append(evs)
-        if flush:
-            flush_buf.zero_()
-    ev_end.record(stream)
-    torch.cuda.synchronize(dev)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
+    tm = time_steps(wl, args.steps, args.warmup, stream, dev, world, dist, comm)
     t_wall = time.perf_counter() - t_wall0
     clk = clocks.stop()
-    f_ms = [e[0].elapsed_time(e[1]) for e in evs_all]
-    b_ms = [e[1].elapsed_time(e[2]) for e in evs_all]
-    step_ms = sum(f_ms[i] + b_ms[i] for i in range(args.steps)) / args.steps
-    region_ms = ev_start.elapsed_time(ev_end) / args.steps
-    mean_f, mean_b = sum(f_ms) / len(f_ms), sum(b_ms) / len(b_ms)
-    stats = torch.tensor([step_ms, mean_f, mean_b], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(stats, op=dist.ReduceOp.MAX)
-    step_ms, mean_f, mean_b = [float(v) for v in stats.tolist()]
-    total_bytes = (bytes_f + bytes_b) * world  # every rank processes the same amount of work
-    if args.scaling == "strong":
-        total_bytes = gcfg.fwd_bytes() + gcfg.bwd_bytes()
+    launches = dict(wl.launches)
+    paths = dict(wl.paths)
+    total_bytes = gcfg.fwd_bytes() + gcfg.bwd_bytes()  # the whole job (all ranks)
+    # the timed region; when L2 is flushed between steps (small configs) the flush memsets sit inside it, so
+    # the step is then the sum of the per-call event medians (max over ranks)
+    step_ms = tm["f_med"] + tm["b_med"] if tm["flush"] else tm["region"]
+    # per-unit parity sample of this run's outputs (compared with the oracle in the cpu_baseline leg)
+    par_units = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        par_units = unit_slices(wl, min(2, gcfg.B * gcfg.G))
 
+    # ---- N > 1: the h all-gather (north_star "final output all-gather"), timed separately
+    weak, allgather = None, None
+    if world > 1:
+        hsz = wl.h.numel()
+        full = torch.empty(hsz * world, dtype=wl.h.dtype, device=dev)
+        ag = []
+        for i in range(4):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            dist.all_gather_into_tensor(full, wl.h.reshape(-1))
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            if i:
+                ag.append(e0.elapsed_time(e1))
+        agv = torch.tensor([pct(ag, 0.5)], dtype=torch.float64, device=dev)
+        dist.all_reduce(agv, op=dist.ReduceOp.MAX)
+        nbytes = full.numel() * full.element_size()
+        allgather = {"ms": float(agv.item()), "bytes_total": nbytes,
+                     "note": "h [D,B,C,H,W] shards gathered to every rank (rank-major), NCCL, outside `value`"}
+        del full
     # ---- SURVEY §8(f) rows on the same workload (after the headline region; not part of `value`)
     nxt = None
-    if not args.no_next:
-        nxt = measure_next(args, gspn, gcfg, sh, t, h, outs, ws, dev, stream)
+    if not args.no_next and world == 1:
+        nxt = measure_next(args, gspn, gcfg, sh, wl.t, wl.h, wl.outs, wl.ws, dev, stream)
 
     # ---- end to end through the public API with host buffers (pinned), copies inside the timed region
     e2e = None
-    if not args.no_e2e:
-        e2e = run_e2e(args, gspn, gcfg, sh, t, h, outs, ws, dev, world, dist)
+    if not args.no_e2e and wl.t is not None:
+        e2e = run_e2e(args, gspn, gcfg, sh, wl.t, wl.h, wl.outs, wl.ws, dev, world, dist)
+    if wl.t is not None:
+        wl.free()
+        torch.cuda.empty_cache()
 
-    cpu = None
+    if world > 1:
+        if args.scaling == "strong":
+            ww = Workload(gspn, base, "weak", rank, world, dev, args.flags)
+            tw = time_steps(ww, args.steps, args.warmup, stream, dev, world, dist,
+                            torch.cuda.Stream(dev) if ww.channel_split else None)
+            wb = ww.gcfg.fwd_bytes() + ww.gcfg.bwd_bytes()
+            weak = {"value": wb / (tw["region"] * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": tw["region"],
+                    "config": f"{world} x config {base.name} (B={ww.gcfg.B})"}
+            ww.free()
+
+    # ---- the other BASELINE configs, short runs on the same device (N = 1 only)
+    others = None
+    if world == 1 and not args.no_others:
+        others = measure_others(args, gspn, base.name, dev, stream)
+
+    cpu, parity = None, None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            b_cpu, w_cpu, thr, desc = oracle_sample(base, args.cpu_seconds)
+            sm = oracle_prepare(base)
+            b_cpu, w_cpu, thr, desc, last = oracle_time(sm, args.cpu_seconds)
             cpu = {"value": b_cpu / w_cpu / 1e9, "unit": "GB/s", "cores": thr, "kind": "oracle", "sample": desc}
+            parity = parity_vs_oracle(par_units, last, gcfg.dtype)
         except Exception as ex:  # the baseline is reported, never required
             cpu = {"value": None, "unit": "GB/s", "cores": None, "kind": "oracle", "sample": f"failed: {ex}"}
 
@@ -332,7 +483,9 @@ def run_ours(args):
     if rank != 0:
         return 0
     peak, peak_src = peaks()
-    dominant = "bwd" if bytes_b / max(mean_b, 1e-9) <= bytes_f / max(mean_f, 1e-9) or mean_b >= mean_f else "fwd"
+    mean_f, mean_b = tm["f_med"], tm["b_med"]
+    bytes_f, bytes_b = wl.bytes_f, wl.bytes_b
+    dominant = "bwd" if mean_b >= mean_f else "fwd"
     dom_ms = mean_b if dominant == "bwd" else mean_f
     dom_bytes = bytes_b if dominant == "bwd" else bytes_f
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
@@ -353,30 +506,93 @@ def run_ours(args):
         "config": {
             "workload": f"config {base.name} (BASELINE.json configs[{base.cfg_id - 1}]): {base.text}",
             "B": gcfg.B, "C": gcfg.C, "G": gcfg.G, "H": gcfg.H, "W": gcfg.W, "dirs": gcfg.dirs,
-            "per_rank": {"B": sh.B, "C": sh.C, "G": sh.G, "kind": sh.kind},
-            "fwd_ms": mean_f, "bwd_ms": mean_b, "region_ms_per_step": region_ms,
+            "per_rank": {"B": sh.B, "C": sh.C, "G": sh.G, "kind": sh.kind, "units": sh.units,
+                         "fwd_bytes": bytes_f, "bwd_bytes": bytes_b},
+            "fwd_ms": mean_f, "bwd_ms": mean_b,
+            "step_ms": summary(tm["step"]), "fwd_ms_pct": summary(tm["f"]), "bwd_ms_pct": summary(tm["b"]),
             "fwd_gbs": bytes_f / (mean_f * 1e-3) / 1e9, "bwd_gbs": bytes_b / (mean_b * 1e-3) / 1e9,
             "algorithmic_bytes_per_step": total_bytes,
-            "l2": ("L2 flushed (2x126 MB memset) between steps, outside the event pairs" if flush else
-                   f"inputs+outputs {work_bytes / 1e9:.1f} GB > 126 MB L2, no flush"),
-            "path": gspn.last_path(),
+            "l2": ("L2 flushed (2x126 MB memset) between steps, outside the event pairs" if tm["flush"] else
+                   f"inputs+outputs {wl.work_bytes / 1e9:.1f} GB > 126 MB L2, no flush"),
+            "path": paths,
             "wall_s_timed_region": t_wall,
         },
         "roofline": {
-            "bound": "hbm", "kernel": f"gspn_{dominant} ({gspn.last_path()} path)",
+            "bound": "hbm", "kernel": f"gspn_{dominant} ({paths[dominant]} path, {launches[dominant]} launch(es))",
             "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "peak_source": peak_src,
-            "traffic": traffic_for(base.name, dominant),
+            "traffic": traffic_for(base.name, dominant) if world == 1 else None,
             "algorithmic_bytes_per_launch": dom_bytes,
+            "step_frac": value / world / peak,
         },
         "clocks": clk,
         "gpu_launches": args.steps * (launches["fwd"] + launches["bwd"]),
+        "launches_per_call": launches,
         "e2e": e2e,
         "cpu_baseline": cpu,
+        "parity": parity,
         "next": nxt,
+        "configs": others,
     }
+    if wl.channel_split:
+        line["collective"] = {"dw_allreduce_ms": tm["c_med"], "dtype": "f32",
+                              "bytes": 3 * gcfg.D * gcfg.H * gcfg.W * 4,
+                              "note": "NCCL all-reduce of the fp32 partial dw on a side stream; overlaps the next "
+                                      "step's fwd, completes inside the timed region"}
+    if weak is not None:
+        line["weak"] = weak
+    if allgather is not None:
+        line["h_allgather"] = allgather
     print(json.dumps(line), flush=True)
     return 0
+
+
+def parity_vs_oracle(gpu, ref, dtype):
+    """normwise max|gpu - ref| / max|ref| per output (R16) on the first units of the headline
+    run vs the oracle's last pass over the same units (its own unrounded h: end to end)."""
+    if gpu is None or ref is None:
+        return None
+    import numpy as np
+
+    n = gpu["h"].shape[1]
+    out = {"units": n, "tol": 1e-5 if dtype == "f32" else 2e-2, "kind": "normwise, end to end vs fp64 oracle"}
+    for k in ("h", "dx", "dw_l", "dw_m", "dw_r", "dlam"):
+        r = ref[k][:n] if k == "dx" else ref[k][:, :n]
+        g = gpu[k].reshape(r.shape)
+        den = float(np.abs(r).max())
+        out[k] = float(np.abs(g - r).max() / den) if den > 0 else 0.0
+    return out
+
+
+def measure_others(args, gspn, skip, dev, stream):
+    """Short device-timed runs (one GPU, full configuration) of the other BASELINE configs, so every
+    config gets a driver-measured line: median / p10 / p90 step time, GB/s, fraction of the peak."""
+    import torch
+
+    from synth.configs import CONFIGS
+
+    peak, _ = peaks()
+    res = {}
+    for name, cfg in CONFIGS.items():
+        if name == skip:
+            continue
+        try:
+            wl = Workload(gspn, cfg, "strong", 0, 1, dev)
+            tm = time_steps(wl, max(3, args.other_steps), max(3, args.warmup), stream, dev, 1, None)
+            tb = cfg.fwd_bytes() + cfg.bwd_bytes()
+            # flushed runs: the region also holds the L2 flushes, so the step is timed by its own events
+            ms = pct(tm["step"], 0.5) if tm["flush"] else tm["region"]
+            gbs = tb / (ms * 1e-3) / 1e9
+            res[name] = {"ms_per_step": ms, "step_ms": summary(tm["step"]), "fwd_ms": tm["f_med"],
+                         "bwd_ms": tm["b_med"], "value": gbs, "unit": "GB/s", "frac": gbs / peak,
+                         "path": dict(wl.paths), "launches_per_call": dict(wl.launches),
+                         "l2": "flushed between steps" if tm["flush"] else "working set > 4x L2"}
+            wl.free()
+            del wl
+            torch.cuda.empty_cache()
+        except Exception as ex:
+            res[name] = {"error": str(ex)}
+    return res
 
 
 def measure_next(args, gspn, cfg, sh, t, h, outs, ws, dev, stream):
@@ -564,8 +780,25 @@ def run_e2e(args, gspn, cfg, sh, t, h, outs, ws, dev, world, dist):
                     "H2D of x,w,lam,dh | fwd + bwd | D2H of h,dx,dw,dlam overlap across chunks"}
 
 
+def maybe_spawn(args):
+    """`--gpus N` outside torchrun: re-execute under torch.distributed.run with N ranks on this node."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    rc = maybe_spawn(args)
+    if rc is not None:
+        return rc
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

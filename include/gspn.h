@@ -68,6 +68,9 @@ typedef enum { GSPN_F32 = 0, GSPN_BF16 = 1 } gspn_dtype_t;
 #define GSPN_FLAG_PRENORMALIZED 0x1u /* taps already row-normalised: no division (out-of-range taps still dropped) */
 #define GSPN_FLAG_FORCE_GENERIC 0x2u /* testing: force the generic (non-TMA) kernels */
 #define GSPN_FLAG_MERGE_MEAN 0x4u    /* gspn_merge_*: combine the directions by Mean instead of Sum */
+#define GSPN_FLAG_DW_F32 0x20u       /* gspn_bwd: dw_l/dw_m/dw_r are fp32 tensors whatever dtype (partial group sums
+                                       to be reduced across devices in fp32); groups < C only,
+                                       GSPN_ERR_UNSUPPORTED for groups == C */
 #define GSPN_FLAG_FORCE_SPLIT 0x10u  /* testing: split every chain over a 2+-CTA cluster (P-split) even when one
                                        CTA could hold it; results must be bitwise those of the unsplit scan */
 

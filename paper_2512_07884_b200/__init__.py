@@ -25,6 +25,7 @@ FLAG_FORCE_GENERIC = 0x2
 FLAG_MERGE_MEAN = 0x4
 FLAG_PROXY_TRANSPOSE = 0x8
 FLAG_FORCE_SPLIT = 0x10
+FLAG_DW_F32 = 0x20
 DTYPE_F32, DTYPE_BF16 = 0, 1
 
 
@@ -115,9 +116,10 @@ def bwd(x, w_l, w_m, w_r, lam, h, dh, dirs: int = DIR_ALL, groups: int | None = 
     G = x.shape[1] if groups is None else int(groups)
     (B, C, H, W, D), sx, sw, sl = _scan_shapes(x, dirs, G)
     dt = _dtype_code(x)
+    dw_dtype = torch.float32 if flags & FLAG_DW_F32 else x.dtype  # fp32 partial dw (cross-device reduction)
     if outs is None:
-        outs = (torch.empty_like(x), torch.empty_like(w_l), torch.empty_like(w_m), torch.empty_like(w_r),
-                torch.empty_like(lam))
+        outs = (torch.empty_like(x), torch.empty_like(w_l, dtype=dw_dtype), torch.empty_like(w_m, dtype=dw_dtype),
+                torch.empty_like(w_r, dtype=dw_dtype), torch.empty_like(lam))
     if len(outs) != 5:
         raise ValueError("outs must be (dx, dw_l, dw_m, dw_r, dlam)")
     dx, dwl, dwm, dwr, dlam = outs
@@ -125,7 +127,8 @@ def bwd(x, w_l, w_m, w_r, lam, h, dh, dirs: int = DIR_ALL, groups: int | None = 
                    ("dh", dh, sl), ("dx (out)", dx, sx), ("dw_l (out)", dwl, sw), ("dw_m (out)", dwm, sw),
                    ("dw_r (out)", dwr, sw), ("dlam (out)", dlam, sl)])
     _check_tensors([("x", x), ("w_l", w_l), ("w_m", w_m), ("w_r", w_r), ("lam", lam), ("h", h), ("dh", dh),
-                    ("dx", dx), ("dw_l", dwl), ("dw_m", dwm), ("dw_r", dwr), ("dlam", dlam)], x.dtype, x.device)
+                    ("dx", dx), ("dlam", dlam)], x.dtype, x.device)
+    _check_tensors([("dw_l", dwl), ("dw_m", dwm), ("dw_r", dwr)], dw_dtype, x.device)
     need = workspace_bytes(B, C, H, W, dirs, G, dt)
     if workspace is None or workspace.numel() < need:
         workspace = torch.empty(max(need, 16), dtype=torch.uint8, device=x.device)

@@ -41,7 +41,7 @@ gspn_status_t check_dims(int64_t B, int64_t C, int64_t H, int64_t W, uint32_t di
   if (C % G != 0) return fail(GSPN_ERR_INVALID_ARG, "%s: C %% groups != 0 (groups=%lld)", "groups", G);
   if (dirs == 0 || dirs > 15) return fail(GSPN_ERR_INVALID_ARG, "%s must be in [1, 15] (got %lld)", "dirs", dirs);
   if (dt != GSPN_F32 && dt != GSPN_BF16) return fail(GSPN_ERR_INVALID_ARG, "%s unknown (%lld)", "dtype", (long long)dt);
-  if (flags & ~(GSPN_FLAG_PRENORMALIZED | GSPN_FLAG_FORCE_GENERIC | GSPN_FLAG_FORCE_SPLIT))
+  if (flags & ~(GSPN_FLAG_PRENORMALIZED | GSPN_FLAG_FORCE_GENERIC | GSPN_FLAG_FORCE_SPLIT | GSPN_FLAG_DW_F32))
     return fail(GSPN_ERR_INVALID_ARG, "%s has unknown bits (0x%llx)", "flags", flags);
   // Overflow guard: the largest tensor (D*B*C*H*W elements) must stay far below 2^62 bytes, and the
   // chain count must fit a 1-D grid.
@@ -234,12 +234,18 @@ gspn_status_t gspn_bwd_local(const void* x, const void* w_l, const void* w_m, co
         return GSPN_ERR_INVALID_ARG;
       }
     }
+    if ((flags & GSPN_FLAG_DW_F32) && groups == C) {
+      snprintf(t_detail, sizeof t_detail, "GSPN_FLAG_DW_F32 needs groups < C (got groups == C == %lld)", (long long)C);
+      return GSPN_ERR_UNSUPPORTED;
+    }
     const size_t s = dtype == GSPN_BF16 ? 2 : 4;
+    const size_t sw = (flags & GSPN_FLAG_DW_F32) ? 4 : s;  // dw element size
     const size_t nx = (size_t)(B * C * H * W) * s, nl = (size_t)D * nx, nw = (size_t)(D * B * groups * H * W) * s;
+    const size_t nwo = (size_t)(D * B * groups * H * W) * sw;
     const Span ins[7] = {span("x", x, nx),   span("w_l", w_l, nw), span("w_m", w_m, nw), span("w_r", w_r, nw),
                          span("lam", lam, nl), span("h", h, nl),     span("dh", dh, nl)};
-    Span outs[6] = {span("dx", dx, nx),     span("dw_l", dw_l, nw), span("dw_m", dw_m, nw),
-                    span("dw_r", dw_r, nw), span("dlam", dlam, nl), span("workspace", workspace, need)};
+    Span outs[6] = {span("dx", dx, nx),     span("dw_l", dw_l, nwo), span("dw_m", dw_m, nwo),
+                    span("dw_r", dw_r, nwo), span("dlam", dlam, nl), span("workspace", workspace, need)};
     if ((st = check_aliasing(outs, need > 0 ? 6 : 5, ins, 7))) return st;
     if (H > gspn::generic_max_P() || W > gspn::generic_max_P()) {
       snprintf(t_detail, sizeof t_detail, "H or W above %lld is not tiled", (long long)gspn::generic_max_P());
@@ -276,7 +282,12 @@ gspn_status_t gspn_bwd_local(const void* x, const void* w_l, const void* w_m, co
         p.dwa_m = reinterpret_cast<float*>(ws + off); off += nwb;
         p.dwa_r = reinterpret_cast<float*>(ws + off); off += nwb;
       }
-      if (!(flags & GSPN_FLAG_FORCE_GENERIC) && gspn::small_eligible(p)) {
+      if (!(flags & GSPN_FLAG_FORCE_GENERIC) && gspn::small_eligible(p) && gspn::small_grouped(p, dtype)) {
+        // small planes, grouped weights: taps once per group, dw formed in-kernel, one launch
+        stream_path = "small";
+        handled = true;
+        e = gspn::launch_bwd_small_grouped(p, dtype, cs, &launches);
+      } else if (!(flags & GSPN_FLAG_FORCE_GENERIC) && gspn::small_eligible(p)) {
         // small-plane path: dx summed inside the CTA; only the group sums (G < C) use the workspace
         stream_path = "small";
         handled = true;

@@ -163,9 +163,15 @@ __global__ void finish_dw_kernel(ScanParams p) {
     float ol, om, orr;
     jacobian(to_f(static_cast<const T*>(p.wl)[e]), to_f(static_cast<const T*>(p.wm)[e]),
              to_f(static_cast<const T*>(p.wr)[e]), hl, hr, prenorm, Da, Db, Dc, ol, om, orr);
-    static_cast<T*>(p.dwl)[e] = from_f<T>(hl ? ol : 0.f);
-    static_cast<T*>(p.dwm)[e] = from_f<T>(om);
-    static_cast<T*>(p.dwr)[e] = from_f<T>(hr ? orr : 0.f);
+    if (p.flags & GSPN_FLAG_DW_F32) {  // fp32 partial sums (cross-device reduction)
+      static_cast<float*>(p.dwl)[e] = hl ? ol : 0.f;
+      static_cast<float*>(p.dwm)[e] = om;
+      static_cast<float*>(p.dwr)[e] = hr ? orr : 0.f;
+    } else {
+      static_cast<T*>(p.dwl)[e] = from_f<T>(hl ? ol : 0.f);
+      static_cast<T*>(p.dwm)[e] = from_f<T>(om);
+      static_cast<T*>(p.dwr)[e] = from_f<T>(hr ? orr : 0.f);
+    }
   }
 }
 

@@ -22,6 +22,10 @@ cudaError_t launch_finish_dw(const ScanParams& p, gspn_dtype_t dt, cudaStream_t 
 bool small_eligible(const ScanParams& p);
 cudaError_t launch_fwd_small(const ScanParams& p, gspn_dtype_t dt, cudaStream_t s, int* launches);
 cudaError_t launch_bwd_small(const ScanParams& p, gspn_dtype_t dt, cudaStream_t s, int* launches);
+// Grouped weights (G < C) on small planes: one CTA per unit (b, g), taps normalised once per group,
+// dw formed in-kernel (no workspace, one launch). small_grouped(): eligible (fits shared memory).
+bool small_grouped(const ScanParams& p, gspn_dtype_t dt);
+cudaError_t launch_bwd_small_grouped(const ScanParams& p, gspn_dtype_t dt, cudaStream_t s, int* launches);
 
 // Fast TMA-streaming path (gspn_stream.cu). *handled = false when the shape is not eligible.
 // *path = "stream" or "stream-cluster" (P-split over a thread-block cluster)

@@ -15,6 +15,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "gspn_common.cuh"
 #include "gspn_internal.h"
 
@@ -217,6 +219,248 @@ __global__ void __launch_bounds__(128) bwd_small_kernel(ScanParams p) {
   }
 }
 
+// ---------------------------------------------------------------------------------------------------
+// Grouped weights (G < C: configs 3a / 3b, the compact-channel variant of PAPER.md:140-148 Eq. 3).
+// One CTA per unit (b, g). The normalised taps of every direction are computed ONCE per (d, b, g, t, r)
+// into shared memory (fp32, scan order, so lane r of every direction reads consecutive words) and
+// reused by all C/G channels of the group -- the per-channel re-normalisation of
+// the per-plane kernels above is gone. Warps take the group's channels in turn; a warp stages its
+// channel's x plane once and runs the D directions on it (lane = position, neighbours by shuffle), its
+// lam / h / dh planes staged whole with 16-byte vectors and written back the same way.
+// Backward: dlam is written in place over the dh plane, dx accumulates over the directions in a
+// warp-private fp32 plane, and the group sums Da / Db / Dc go into CTA-wide fp32 shared-memory
+// accumulators (red.shared.add: warps of different channels meet there, so the summation order -- and
+// the last bits of dw -- is not fixed, gspn.h); the Jacobian and the dw stores follow once per unit.
+constexpr int kGrpWarpsF = 16, kGrpWarpsB = 12;
+
+template <typename T>
+__device__ __forceinline__ void warp_plane_in(T* dst, const T* src, int n, int lane) {
+  if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15u) == 0 &&
+      (n * static_cast<int>(sizeof(T))) % 16 == 0) {
+    const int nv = n * static_cast<int>(sizeof(T)) / 16;
+    const uint4* s = reinterpret_cast<const uint4*>(src);
+    uint4* d = reinterpret_cast<uint4*>(dst);
+    for (int i = lane; i < nv; i += 32) d[i] = __ldg(s + i);
+  } else {
+    for (int i = lane; i < n; i += 32) dst[i] = src[i];
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void warp_plane_out(T* dst, const T* src, int n, int lane) {
+  if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15u) == 0 &&
+      (n * static_cast<int>(sizeof(T))) % 16 == 0) {
+    const int nv = n * static_cast<int>(sizeof(T)) / 16;
+    const uint4* s = reinterpret_cast<const uint4*>(src);
+    uint4* d = reinterpret_cast<uint4*>(dst);
+    for (int i = lane; i < nv; i += 32) d[i] = s[i];
+  } else {
+    for (int i = lane; i < n; i += 32) dst[i] = src[i];
+  }
+}
+
+// Normalised taps of unit (b, g), all directions: TA/TB/TC[k HW + t P + r] (R1/R2).
+template <typename T>
+__device__ void unit_taps(const ScanParams& p, int64_t b, int64_t g, float* TA, float* TB, float* TC) {
+  const int H = static_cast<int>(p.H), W = static_cast<int>(p.W), HW = H * W, D = static_cast<int>(p.D);
+  const bool prenorm = p.flags & GSPN_FLAG_PRENORMALIZED;
+  for (int idx = threadIdx.x; idx < D * HW; idx += blockDim.x) {
+    const int k = idx / HW, q = idx - k * HW;
+    const DirGeom gm = dir_geom(p.dirbit[k], H, W);
+    const int P = static_cast<int>(gm.P), t = q / P, r = q - t * P;
+    const int pix = static_cast<int>(gm.base + t * gm.ts + r * gm.rs);
+    const int64_t w = ((k * p.B + b) * p.G + g) * HW + pix;
+    const Taps tp = make_taps(to_f(static_cast<const T*>(p.wl)[w]), to_f(static_cast<const T*>(p.wm)[w]),
+                              to_f(static_cast<const T*>(p.wr)[w]), r >= 1, r <= P - 2, prenorm);
+    TA[idx] = tp.a;
+    TB[idx] = tp.b;
+    TC[idx] = tp.c;
+  }
+}
+
+__host__ __device__ __forceinline__ size_t align16(size_t v) { return (v + 15) / 16 * 16; }
+
+template <typename T, bool kLocal>
+__global__ void __launch_bounds__(kGrpWarpsF * 32) fwd_grp_small_kernel(ScanParams p) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const int H = static_cast<int>(p.H), W = static_cast<int>(p.W), HW = H * W, D = static_cast<int>(p.D);
+  const int np = padded(HW, sizeof(T));
+  const int64_t G = p.G, Cg = p.C / p.G;
+  const int64_t b = blockIdx.x / G, g = blockIdx.x % G;
+  float* TA = reinterpret_cast<float*>(sm);
+  float* TB = TA + D * HW;
+  float* TC = TB + D * HW;
+  T* wbuf = reinterpret_cast<T*>(sm + align16(static_cast<size_t>(3 * D * HW) * 4));
+  unit_taps<T>(p, b, g, TA, TB, TC);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  T* X = wbuf + static_cast<size_t>(warp) * 2 * np;
+  T* Lm = X + np;
+  const int kc = static_cast<int>(p.kchunk);
+  for (int64_t cc = warp; cc < Cg; cc += nw) {
+    const int64_t c = g * Cg + cc;
+    warp_plane_in(X, static_cast<const T*>(p.x) + (b * p.C + c) * HW, HW, lane);
+    for (int k = 0; k < D; ++k) {
+      const int64_t chain = (k * p.B + b) * p.C + c;
+      warp_plane_in(Lm, static_cast<const T*>(p.lam) + chain * HW, HW, lane);
+      __syncwarp();
+      const uint32_t dir = p.dirbit[k];
+      const DirGeom gm = dir_geom(dir, H, W);
+      const int L = static_cast<int>(gm.L), P = static_cast<int>(gm.P);
+      const int ts = static_cast<int>(gm.ts);
+      const bool in = lane < P;
+      const int r = in ? lane : 0;
+      const float* ta = TA + k * HW + r;
+      const float* tb = TB + k * HW + r;
+      const float* tc = TC + k * HW + r;
+      int off = static_cast<int>(gm.base) + r * static_cast<int>(gm.rs);
+      float hv = 0.f;
+      for (int t = 0; t < L; ++t, off += ts) {
+        if constexpr (kLocal) {
+          if (seg_start_step(dir, t, L, kc)) hv = 0.f;  // warp-uniform: h_{t-1} does not propagate
+        }
+        const float up = __shfl_up_sync(0xffffffffu, hv, 1);    // lane 0: tap a = 0
+        const float dn = __shfl_down_sync(0xffffffffu, hv, 1);  // lane P-1: tap c = 0; lanes >= P carry 0
+        const float v = fmaf(ta[t * P], up, fmaf(tb[t * P], hv, fmaf(tc[t * P], dn, to_f(Lm[off]) * to_f(X[off]))));
+        if (in) Lm[off] = from_f<T>(v);  // h over lam at the lane's own pixel (neighbours travel by shuffle)
+        hv = in ? v : 0.f;
+      }
+      __syncwarp();
+      warp_plane_out(static_cast<T*>(p.hout) + chain * HW, Lm, HW, lane);
+      __syncwarp();
+    }
+  }
+}
+
+template <typename T, bool kLocal>
+__global__ void __launch_bounds__(kGrpWarpsB * 32) bwd_grp_small_kernel(ScanParams p) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const int H = static_cast<int>(p.H), W = static_cast<int>(p.W), HW = H * W, D = static_cast<int>(p.D);
+  const int np = padded(HW, sizeof(T));
+  const int64_t G = p.G, Cg = p.C / p.G;
+  const int64_t b = blockIdx.x / G, g = blockIdx.x % G;
+  float* TA = reinterpret_cast<float*>(sm);
+  float* TB = TA + D * HW;
+  float* TC = TB + D * HW;
+  float* DA = TC + D * HW;  // group sums of the normalised-tap gradients, scan order [k][t P + r]
+  float* DB = DA + D * HW;
+  float* DC = DB + D * HW;
+  uint8_t* wb = sm + align16(static_cast<size_t>(6 * D * HW) * 4);
+  const size_t per_warp = align16(static_cast<size_t>(HW) * 4) + 4 * static_cast<size_t>(np) * sizeof(T);
+  unit_taps<T>(p, b, g, TA, TB, TC);
+  for (int i = threadIdx.x; i < 3 * D * HW; i += blockDim.x) DA[i] = 0.f;
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  float* DX = reinterpret_cast<float*>(wb + warp * per_warp);
+  T* X = reinterpret_cast<T*>(wb + warp * per_warp + align16(static_cast<size_t>(HW) * 4));
+  T* Lm = X + np;
+  T* DH = Lm + np;
+  T* Hs = DH + np;
+  const int kc = static_cast<int>(p.kchunk);
+  for (int64_t cc = warp; cc < Cg; cc += nw) {
+    const int64_t c = g * Cg + cc;
+    const int64_t bc = b * p.C + c;
+    warp_plane_in(X, static_cast<const T*>(p.x) + bc * HW, HW, lane);
+    for (int i = lane; i < HW; i += 32) DX[i] = 0.f;
+    for (int k = 0; k < D; ++k) {
+      const int64_t chain = (k * p.B + b) * p.C + c;
+      warp_plane_in(Lm, static_cast<const T*>(p.lam) + chain * HW, HW, lane);
+      warp_plane_in(DH, static_cast<const T*>(p.dh) + chain * HW, HW, lane);
+      warp_plane_in(Hs, static_cast<const T*>(p.h) + chain * HW, HW, lane);
+      __syncwarp();
+      const uint32_t dir = p.dirbit[k];
+      const DirGeom gm = dir_geom(dir, H, W);
+      const int L = static_cast<int>(gm.L), P = static_cast<int>(gm.P);
+      const int ts = static_cast<int>(gm.ts), rs = static_cast<int>(gm.rs);
+      const bool in = lane < P;
+      const int r = in ? lane : 0;
+      const bool hl = in && r >= 1, hr = in && r <= P - 2;
+      const int qk = k * HW + r;
+      int off = static_cast<int>(gm.base) + (L - 1) * ts + r * rs;
+      float ea = 0.f, eb = 0.f, ec = 0.f;  // (a g, b g, c g) of step t+1 at this position
+      for (int t = L - 1; t >= 0; --t, off -= ts) {
+        const float from_r = __shfl_down_sync(0xffffffffu, ea, 1);  // a_{t+1}[r+1] g_{t+1}[r+1]
+        const float from_l = __shfl_up_sync(0xffffffffu, ec, 1);    // c_{t+1}[r-1] g_{t+1}[r-1]
+        const float gt = in ? to_f(DH[off]) + eb + ((hr ? from_r : 0.f) + (hl ? from_l : 0.f)) : 0.f;
+        const int q = qk + t * P;
+        if (in) {
+          DH[off] = from_f<T>(gt * to_f(X[off]));       // dlam (dh at this pixel already read)
+          DX[off] = fmaf(gt, to_f(Lm[off]), DX[off]);   // dx: sum over the directions, fp32
+          if (!seg_start_step(dir, t, L, kc)) {         // h_{t-1} (0 at t = 0 / a segment start)
+            const int prev = off - ts;
+            atomicAdd(&DB[q], gt * to_f(Hs[prev]));
+            if (hl) atomicAdd(&DA[q], gt * to_f(Hs[prev - rs]));
+            if (hr) atomicAdd(&DC[q], gt * to_f(Hs[prev + rs]));
+          }
+        }
+        ea = TA[q] * gt;
+        eb = TB[q] * gt;
+        ec = TC[q] * gt;
+        if constexpr (kLocal) {
+          if (seg_start_step(dir, t, L, kc)) ea = eb = ec = 0.f;  // h_t did not depend on h_{t-1}
+        }
+      }
+      __syncwarp();
+      warp_plane_out(static_cast<T*>(p.dlam) + chain * HW, DH, HW, lane);
+      __syncwarp();
+    }
+    T* dxo = static_cast<T*>(p.dx) + bc * HW;
+    for (int i = lane; i < HW; i += 32) dxo[i] = from_f<T>(DX[i]);
+    __syncwarp();
+  }
+  __syncthreads();
+  // dw = normalisation Jacobian of the group sums (once per unit and direction)
+  const bool prenorm = p.flags & GSPN_FLAG_PRENORMALIZED;
+  const bool f32out = p.flags & GSPN_FLAG_DW_F32;
+  for (int idx = threadIdx.x; idx < D * HW; idx += blockDim.x) {
+    const int k = idx / HW, q = idx - k * HW;
+    const DirGeom gm = dir_geom(p.dirbit[k], H, W);
+    const int P = static_cast<int>(gm.P), t = q / P, r = q - t * P;
+    const int pix = static_cast<int>(gm.base + t * gm.ts + r * gm.rs);
+    const int64_t w = ((k * p.B + b) * p.G + g) * HW + pix;
+    const bool hl = r >= 1, hr = r <= P - 2;
+    float ol, om, orr;
+    jacobian(to_f(static_cast<const T*>(p.wl)[w]), to_f(static_cast<const T*>(p.wm)[w]),
+             to_f(static_cast<const T*>(p.wr)[w]), hl, hr, prenorm, DA[idx], DB[idx], DC[idx], ol, om, orr);
+    if (f32out) {
+      static_cast<float*>(p.dwl)[w] = ol;
+      static_cast<float*>(p.dwm)[w] = om;
+      static_cast<float*>(p.dwr)[w] = orr;
+    } else {
+      static_cast<T*>(p.dwl)[w] = from_f<T>(ol);
+      static_cast<T*>(p.dwm)[w] = from_f<T>(om);
+      static_cast<T*>(p.dwr)[w] = from_f<T>(orr);
+    }
+  }
+}
+
+size_t grp_fwd_smem(const ScanParams& p, int es, int nw) {
+  const int np = padded(static_cast<int>(p.H * p.W), es);
+  return align16(static_cast<size_t>(3 * p.D * p.H * p.W) * 4) + static_cast<size_t>(nw) * 2 * np * es;
+}
+size_t grp_bwd_smem(const ScanParams& p, int es, int nw) {
+  const int np = padded(static_cast<int>(p.H * p.W), es);
+  return align16(static_cast<size_t>(6 * p.D * p.H * p.W) * 4) +
+         static_cast<size_t>(nw) * (align16(static_cast<size_t>(p.H * p.W) * 4) + 4 * static_cast<size_t>(np) * es);
+}
+
+template <typename K>
+cudaError_t launch_grp(K kern, const ScanParams& p, int nw, size_t smem, cudaStream_t s) {
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  kern<<<static_cast<unsigned>(p.B * p.G), nw * 32, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
+// warps per CTA: no more than the group has channels, and within the shared-memory budget
+int grp_warps(const ScanParams& p, int es, bool bwd) {
+  const int64_t Cg = p.C / p.G;
+  int nw = static_cast<int>(std::min<int64_t>(bwd ? kGrpWarpsB : kGrpWarpsF, Cg));
+  const size_t budget = static_cast<size_t>(device_smem_optin());
+  while (nw > 1 && (bwd ? grp_bwd_smem(p, es, nw) : grp_fwd_smem(p, es, nw)) > budget) --nw;
+  return (bwd ? grp_bwd_smem(p, es, nw) : grp_fwd_smem(p, es, nw)) <= budget ? nw : 0;
+}
+
 size_t fwd_smem(const ScanParams& p, int es) {
   const int np = padded(static_cast<int>(p.H * p.W), es);
   return static_cast<size_t>(np) * (1 + 5 * p.D) * es;
@@ -238,9 +482,22 @@ cudaError_t launch_small(K kern, const ScanParams& p, size_t smem, cudaStream_t 
 
 bool small_eligible(const ScanParams& p) { return p.H <= kSmallMax && p.W <= kSmallMax && p.D <= 4; }
 
+bool small_grouped(const ScanParams& p, gspn_dtype_t dt) {
+  return p.G < p.C && grp_warps(p, dt == GSPN_BF16 ? 2 : 4, true) > 0 && grp_warps(p, dt == GSPN_BF16 ? 2 : 4, false) > 0;
+}
+
 cudaError_t launch_fwd_small(const ScanParams& p, gspn_dtype_t dt, cudaStream_t s, int* launches) {
   *launches += 1;
   const bool local = p.kchunk > 0;
+  if (small_grouped(p, dt)) {
+    const int es = dt == GSPN_BF16 ? 2 : 4, nw = grp_warps(p, es, false);
+    const size_t sm = grp_fwd_smem(p, es, nw);
+    if (dt == GSPN_BF16)
+      return local ? launch_grp(fwd_grp_small_kernel<__nv_bfloat16, true>, p, nw, sm, s)
+                   : launch_grp(fwd_grp_small_kernel<__nv_bfloat16, false>, p, nw, sm, s);
+    return local ? launch_grp(fwd_grp_small_kernel<float, true>, p, nw, sm, s)
+                 : launch_grp(fwd_grp_small_kernel<float, false>, p, nw, sm, s);
+  }
   if (dt == GSPN_BF16)
     return local ? launch_small(fwd_small_kernel<__nv_bfloat16, true>, p, fwd_smem(p, 2), s)
                  : launch_small(fwd_small_kernel<__nv_bfloat16, false>, p, fwd_smem(p, 2), s);
@@ -248,7 +505,21 @@ cudaError_t launch_fwd_small(const ScanParams& p, gspn_dtype_t dt, cudaStream_t 
                : launch_small(fwd_small_kernel<float, false>, p, fwd_smem(p, 4), s);
 }
 
-// G < C: p.dwa_* must point at zeroed fp32 workspace; the caller then runs the generic finish_dw.
+// Grouped weights: the whole backward (dw included) in one launch, no workspace.
+cudaError_t launch_bwd_small_grouped(const ScanParams& p, gspn_dtype_t dt, cudaStream_t s, int* launches) {
+  *launches += 1;
+  const bool local = p.kchunk > 0;
+  const int es = dt == GSPN_BF16 ? 2 : 4, nw = grp_warps(p, es, true);
+  const size_t sm = grp_bwd_smem(p, es, nw);
+  if (dt == GSPN_BF16)
+    return local ? launch_grp(bwd_grp_small_kernel<__nv_bfloat16, true>, p, nw, sm, s)
+                 : launch_grp(bwd_grp_small_kernel<__nv_bfloat16, false>, p, nw, sm, s);
+  return local ? launch_grp(bwd_grp_small_kernel<float, true>, p, nw, sm, s)
+               : launch_grp(bwd_grp_small_kernel<float, false>, p, nw, sm, s);
+}
+
+// Per-plane kernels (G = C directly; G < C only when the grouped kernel does not fit): for G < C p.dwa_*
+// must point at zeroed fp32 workspace and the caller then runs the generic finish_dw.
 cudaError_t launch_bwd_small(const ScanParams& p, gspn_dtype_t dt, cudaStream_t s, int* launches) {
   *launches += 1;
   const bool pc = p.G == p.C, lo = p.kchunk > 0;

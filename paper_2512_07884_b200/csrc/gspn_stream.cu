@@ -1538,6 +1538,14 @@ __device__ __forceinline__ void finish_taps(const ScanParams& p, uint32_t dir, i
     jacobian<true>(wl[q], wm[q], wr[q], hl, hr, prenorm, hl ? Da[q] : 0.f, Db[q], hr ? Dc[q] : 0.f, ol[q], om[q], orr[q]);
   }
   local_dw_mask<V>(p, dir, i, j0, ol, om, orr);
+  if (p.flags & GSPN_FLAG_DW_F32) {  // fp32 partial group sums (G < C only)
+    for (int q = 0; q < V; ++q) {
+      static_cast<float*>(p.dwl)[woff + q] = ol[q];
+      static_cast<float*>(p.dwm)[woff + q] = om[q];
+      static_cast<float*>(p.dwr)[woff + q] = orr[q];
+    }
+    return;
+  }
   GVec<T, V>::store(static_cast<T*>(p.dwl) + woff, ol);
   GVec<T, V>::store(static_cast<T*>(p.dwm) + woff, om);
   GVec<T, V>::store(static_cast<T*>(p.dwr) + woff, orr);
@@ -2064,6 +2072,7 @@ __global__ void __launch_bounds__((kOutConsumers + 1) * 32, 1) bwd_out_grp_tma_k
   const int64_t H = p.H, W = p.W, HW = H * W;
   const int64_t kstride = p.B * p.C * HW;   // direction slabs of lam / g / h / dlam
   const int64_t kwstride = p.B * p.G * HW;  // direction slabs of w / dw
+  const bool dw_f32 = (p.flags & GSPN_FLAG_DW_F32) != 0;
   const int nchunk = static_cast<int>(W / V);
   constexpr int es = static_cast<int>(sizeof(T));
   const uint32_t rowb = static_cast<uint32_t>(BX * es);
@@ -2173,9 +2182,15 @@ __global__ void __launch_bounds__((kOutConsumers + 1) * 32, 1) bwd_out_grp_tma_k
                          om[q], orr[q]);
         }
         if constexpr (kLocal) local_dw_mask<V>(p, dir, i, j0, ol, om, orr);
-        GVec<T, V>::store(static_cast<T*>(p.dwl) + woff, ol);
-        GVec<T, V>::store(static_cast<T*>(p.dwm) + woff, om);
-        GVec<T, V>::store(static_cast<T*>(p.dwr) + woff, orr);
+        if (dw_f32) {  // fp32 partial group sums (GSPN_FLAG_DW_F32: reduced across devices in fp32)
+          GVec<float, V>::store(static_cast<float*>(p.dwl) + woff, ol);
+          GVec<float, V>::store(static_cast<float*>(p.dwm) + woff, om);
+          GVec<float, V>::store(static_cast<float*>(p.dwr) + woff, orr);
+        } else {
+          GVec<T, V>::store(static_cast<T*>(p.dwl) + woff, ol);
+          GVec<T, V>::store(static_cast<T*>(p.dwm) + woff, om);
+          GVec<T, V>::store(static_cast<T*>(p.dwr) + woff, orr);
+        }
       }
     }
   }

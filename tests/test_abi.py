@@ -72,14 +72,14 @@ def test_fwd_aliasing_rejected():
     assert "overlaps" in detail()
 
 
-def bwd_call(ws=A + (40 << 30), ws_bytes=1 << 40, **kw):
+def bwd_call(ws=A + (40 << 30), ws_bytes=1 << 40, flags=0, groups=2, **kw):
     base = 1 << 30
     p = dict(x=A, wl=A + base, wm=A + 2 * base, wr=A + 3 * base, lam=A + 4 * base, h=A + 5 * base,
              dh=A + 6 * base, dx=A + 7 * base, dwl=A + 8 * base, dwm=A + 9 * base, dwr=A + 10 * base,
              dlam=A + 11 * base)
     p.update(kw)
     return gspn.lib().gspn_bwd(p["x"], p["wl"], p["wm"], p["wr"], p["lam"], p["h"], p["dh"], p["dx"], p["dwl"],
-                               p["dwm"], p["dwr"], p["dlam"], 2, 4, 16, 16, 0xF, 2, 1, 0, ws, ws_bytes, None)
+                               p["dwm"], p["dwr"], p["dlam"], 2, 4, 16, 16, 0xF, groups, 1, flags, ws, ws_bytes, None)
 
 
 def test_bwd_validation():
@@ -89,6 +89,14 @@ def test_bwd_validation():
     assert bwd_call(ws_bytes=16) == 1 and "workspace too small" in detail()
     assert bwd_call(dx=A + 4 * (1 << 30)) == 1 and "overlaps" in detail()  # dx on lam
     assert bwd_call(dwm=A + 8 * (1 << 30)) == 1 and "overlaps" in detail()  # dw_m on dw_l
+    assert bwd_call(flags=0x40) == 1 and "unknown bits" in detail()
+
+
+def test_dw_f32_flag_validation():
+    """GSPN_FLAG_DW_F32: fp32 dw partial sums, grouped weights only; the dw spans are sized in fp32."""
+    assert bwd_call(flags=0x20, groups=4) == 2 and "DW_F32" in detail()  # groups == C: unsupported
+    # bf16 dw of [4,2,2,16,16] = 4 KB would fit between dw_l and dw_m 6 KB apart; fp32 (8 KB) overlaps
+    assert bwd_call(flags=0x20, dwm=A + 8 * (1 << 30) + 6144) == 1 and "overlaps" in detail()
 
 
 def test_workspace_and_bytes():

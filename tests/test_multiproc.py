@@ -111,3 +111,22 @@ def test_channel_split_allreduce_equals_unsharded(tmp_path):
     for key, ref in (("dwl", dwl), ("dwm", dwm), ("dwr", dwr)):
         for p in parts:
             np.testing.assert_allclose(p[key], ref, rtol=0, atol=1e-13 * max(1.0, np.abs(ref).max()))
+
+
+def test_bench_gpus_flag_spawns_ranks():
+    """`bench.py --gpus 2` outside torchrun re-executes itself under torch.distributed.run (2 ranks, rendezvous on
+    127.0.0.1). Exercised through the CPU-only reference arm: rank 0 alone prints one JSON line, rank 1 exits 0."""
+    import json
+    import subprocess
+    import sys
+
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR",
+                                                          "MASTER_PORT")}
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2",
+                          "--steps", "1", "--warmup", "0", "--config", "1", "--cpu-seconds", "0.2"],
+                         capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    rec = json.loads(lines[0])
+    assert rec["impl"] == "reference" and rec["n_gpus"] == 2
