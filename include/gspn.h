@@ -95,6 +95,12 @@ gspn_status_t gspn_fwd(const void* x, const void* w_l, const void* w_m, const vo
  *   workspace: caller-owned device scratch of at least gspn_bwd_workspace_bytes(...) bytes (16-byte
  *   aligned; may be NULL when that size is 0). Its contents on entry are ignored; the library
  *   initialises it on `stream`. No output may overlap any input, another output or the workspace.
+ * Determinism: gspn_fwd is bitwise deterministic and independent of the tiling (P-split clusters, chain
+ *   packing). gspn_bwd sums dx over the directions and dw over a group's channels in a fixed order on the
+ *   streaming and grouped small-plane paths (bitwise run-to-run); the generic kernels
+ *   (GSPN_FLAG_FORCE_GENERIC, or shapes no fast path tiles) and the per-plane small kernels used for
+ *   groups < C when the grouped kernel does not fit shared memory add with fp32 atomics, so their
+ *   dx / dw may differ in the last bits between runs.
  */
 gspn_status_t gspn_bwd(const void* x, const void* w_l, const void* w_m, const void* w_r, const void* lam,
                        const void* h, const void* dh, void* dx, void* dw_l, void* dw_m, void* dw_r, void* dlam,

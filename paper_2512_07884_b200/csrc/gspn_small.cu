@@ -227,20 +227,27 @@ __global__ void __launch_bounds__(128) bwd_small_kernel(ScanParams p) {
 // the per-plane kernels above is gone. Warps take the group's channels in turn; a warp stages its
 // channel's x plane once and runs the D directions on it (lane = position, neighbours by shuffle), its
 // lam / h / dh planes staged whole with 16-byte vectors and written back the same way.
-// Backward: dlam is written in place over the dh plane, dx accumulates over the directions in a
-// warp-private fp32 plane, and the group sums Da / Db / Dc go into CTA-wide fp32 shared-memory
-// accumulators (red.shared.add: warps of different channels meet there, so the summation order -- and
-// the last bits of dw -- is not fixed, gspn.h); the Jacobian and the dw stores follow once per unit.
-constexpr int kGrpWarpsF = 16, kGrpWarpsB = 12;
+// Backward: see bwd_grp_small_kernel (dlam in place over the dh plane; dx and the group sums reduced in a
+// fixed order -- bitwise deterministic); the Jacobian and the dw stores follow once per unit.
+constexpr int kGrpWarpsF = 12, kGrpWarpsB = 8;
 
+// One plane (<= 32 x 32 elements) global -> shared by one warp: every 16-byte load is issued before the
+// first store, so the warp waits for one memory latency, not one per vector.
 template <typename T>
 __device__ __forceinline__ void warp_plane_in(T* dst, const T* src, int n, int lane) {
+  constexpr int kV = kSmallMax * kSmallMax * static_cast<int>(sizeof(T)) / 16 / 32;
   if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15u) == 0 &&
       (n * static_cast<int>(sizeof(T))) % 16 == 0) {
     const int nv = n * static_cast<int>(sizeof(T)) / 16;
     const uint4* s = reinterpret_cast<const uint4*>(src);
     uint4* d = reinterpret_cast<uint4*>(dst);
-    for (int i = lane; i < nv; i += 32) d[i] = __ldg(s + i);
+    uint4 v[kV];
+#pragma unroll
+    for (int i = 0; i < kV; ++i)
+      if (lane + 32 * i < nv) v[i] = __ldg(s + lane + 32 * i);
+#pragma unroll
+    for (int i = 0; i < kV; ++i)
+      if (lane + 32 * i < nv) d[lane + 32 * i] = v[i];
   } else {
     for (int i = lane; i < n; i += 32) dst[i] = src[i];
   }
@@ -259,9 +266,10 @@ __device__ __forceinline__ void warp_plane_out(T* dst, const T* src, int n, int 
   }
 }
 
-// Normalised taps of unit (b, g), all directions: TA/TB/TC[k HW + t P + r] (R1/R2).
+// Normalised taps of unit (b, g), all directions: TP[k HW + t P + r] = (a, b, c, 0) (DESIGN.md
+// R1/R2), one 16-byte read per lane and step.
 template <typename T>
-__device__ void unit_taps(const ScanParams& p, int64_t b, int64_t g, float* TA, float* TB, float* TC) {
+__device__ void unit_taps(const ScanParams& p, int64_t b, int64_t g, float4* TP) {
   const int H = static_cast<int>(p.H), W = static_cast<int>(p.W), HW = H * W, D = static_cast<int>(p.D);
   const bool prenorm = p.flags & GSPN_FLAG_PRENORMALIZED;
   for (int idx = threadIdx.x; idx < D * HW; idx += blockDim.x) {
@@ -272,156 +280,263 @@ __device__ void unit_taps(const ScanParams& p, int64_t b, int64_t g, float* TA, 
     const int64_t w = ((k * p.B + b) * p.G + g) * HW + pix;
     const Taps tp = make_taps(to_f(static_cast<const T*>(p.wl)[w]), to_f(static_cast<const T*>(p.wm)[w]),
                               to_f(static_cast<const T*>(p.wr)[w]), r >= 1, r <= P - 2, prenorm);
-    TA[idx] = tp.a;
-    TB[idx] = tp.b;
-    TC[idx] = tp.c;
+    TP[idx] = make_float4(tp.a, tp.b, tp.c, 0.f);
   }
+}
+
+__device__ __forceinline__ void named_barrier(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
 __host__ __device__ __forceinline__ size_t align16(size_t v) { return (v + 15) / 16 * 16; }
 
+// A whole plane (<= 32 x 32) held in registers as 16-byte vectors, kV per lane: loaded while the warp
+// computes the previous plane (software pipelining of the staging), stored to shared memory after.
+template <typename T>
+struct PlaneRegs {
+  static constexpr int kV = kSmallMax * kSmallMax * static_cast<int>(sizeof(T)) / 16 / 32;
+  uint4 v[kV];
+  __device__ __forceinline__ void load(const T* src, int n, int lane, bool vec) {
+    if (!vec) return;
+    const uint4* s = reinterpret_cast<const uint4*>(src);
+    const int nv = n * static_cast<int>(sizeof(T)) / 16;
+#pragma unroll
+    for (int i = 0; i < kV; ++i)
+      if (lane + 32 * i < nv) v[i] = __ldg(s + lane + 32 * i);
+  }
+  __device__ __forceinline__ void store(T* dst, const T* src, int n, int lane, bool vec) const {
+    if (!vec) {  // unaligned plane size: plain element copy
+      for (int i = lane; i < n; i += 32) dst[i] = src[i];
+      return;
+    }
+    uint4* d = reinterpret_cast<uint4*>(dst);
+    const int nv = n * static_cast<int>(sizeof(T)) / 16;
+#pragma unroll
+    for (int i = 0; i < kV; ++i)
+      if (lane + 32 * i < nv) d[lane + 32 * i] = v[i];
+  }
+};
+
+template <typename T>
+__device__ __forceinline__ bool plane_vec(const ScanParams& p) {
+  // every plane of every tensor starts 16-byte aligned and is a whole number of 16-byte vectors
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p.x) | reinterpret_cast<uintptr_t>(p.lam) |
+                      reinterpret_cast<uintptr_t>(p.h) | reinterpret_cast<uintptr_t>(p.dh) |
+                      reinterpret_cast<uintptr_t>(p.hout) | reinterpret_cast<uintptr_t>(p.dlam);
+  return (a & 15u) == 0 && (p.H * p.W * static_cast<int64_t>(sizeof(T))) % 16 == 0;
+}
+
 template <typename T, bool kLocal>
-__global__ void __launch_bounds__(kGrpWarpsF * 32) fwd_grp_small_kernel(ScanParams p) {
+__global__ void __launch_bounds__(kGrpWarpsF * 32, 2) fwd_grp_small_kernel(ScanParams p) {
   extern __shared__ __align__(16) uint8_t sm[];
   const int H = static_cast<int>(p.H), W = static_cast<int>(p.W), HW = H * W, D = static_cast<int>(p.D);
   const int np = padded(HW, sizeof(T));
   const int64_t G = p.G, Cg = p.C / p.G;
   const int64_t b = blockIdx.x / G, g = blockIdx.x % G;
-  float* TA = reinterpret_cast<float*>(sm);
-  float* TB = TA + D * HW;
-  float* TC = TB + D * HW;
-  T* wbuf = reinterpret_cast<T*>(sm + align16(static_cast<size_t>(3 * D * HW) * 4));
-  unit_taps<T>(p, b, g, TA, TB, TC);
-  __syncthreads();
+  float4* TP = reinterpret_cast<float4*>(sm);
+  T* wbuf = reinterpret_cast<T*>(sm + static_cast<size_t>(D * HW) * 16);
+  const bool vec = plane_vec<T>(p);
+  unit_taps<T>(p, b, g, TP);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   T* X = wbuf + static_cast<size_t>(warp) * 2 * np;
   T* Lm = X + np;
   const int kc = static_cast<int>(p.kchunk);
-  for (int64_t cc = warp; cc < Cg; cc += nw) {
+  const T* lam_g = static_cast<const T*>(p.lam);
+  // items (channel cc, direction k) of this warp, in order; lam of the next item is prefetched
+  const int64_t nitems = ((Cg - warp + nw - 1) / nw) * D;
+  auto chain_of = [&](int64_t it) {
+    const int64_t cc = warp + (it / D) * nw;
+    return ((it % D) * p.B + b) * p.C + g * Cg + cc;
+  };
+  PlaneRegs<T> pre;
+  if (nitems > 0) pre.load(lam_g + chain_of(0) * HW, HW, lane, vec);
+  __syncthreads();  // taps ready
+  for (int64_t it = 0; it < nitems; ++it) {
+    const int k = static_cast<int>(it % D);
+    const int64_t cc = warp + (it / D) * nw;
     const int64_t c = g * Cg + cc;
-    warp_plane_in(X, static_cast<const T*>(p.x) + (b * p.C + c) * HW, HW, lane);
-    for (int k = 0; k < D; ++k) {
-      const int64_t chain = (k * p.B + b) * p.C + c;
-      warp_plane_in(Lm, static_cast<const T*>(p.lam) + chain * HW, HW, lane);
+    const int64_t chain = chain_of(it);
+    if (k == 0) {  // a new channel: its x plane, shared by the D directions
       __syncwarp();
-      const uint32_t dir = p.dirbit[k];
-      const DirGeom gm = dir_geom(dir, H, W);
-      const int L = static_cast<int>(gm.L), P = static_cast<int>(gm.P);
-      const int ts = static_cast<int>(gm.ts);
-      const bool in = lane < P;
-      const int r = in ? lane : 0;
-      const float* ta = TA + k * HW + r;
-      const float* tb = TB + k * HW + r;
-      const float* tc = TC + k * HW + r;
-      int off = static_cast<int>(gm.base) + r * static_cast<int>(gm.rs);
-      float hv = 0.f;
-      for (int t = 0; t < L; ++t, off += ts) {
-        if constexpr (kLocal) {
-          if (seg_start_step(dir, t, L, kc)) hv = 0.f;  // warp-uniform: h_{t-1} does not propagate
-        }
-        const float up = __shfl_up_sync(0xffffffffu, hv, 1);    // lane 0: tap a = 0
-        const float dn = __shfl_down_sync(0xffffffffu, hv, 1);  // lane P-1: tap c = 0; lanes >= P carry 0
-        const float v = fmaf(ta[t * P], up, fmaf(tb[t * P], hv, fmaf(tc[t * P], dn, to_f(Lm[off]) * to_f(X[off]))));
-        if (in) Lm[off] = from_f<T>(v);  // h over lam at the lane's own pixel (neighbours travel by shuffle)
-        hv = in ? v : 0.f;
-      }
-      __syncwarp();
-      warp_plane_out(static_cast<T*>(p.hout) + chain * HW, Lm, HW, lane);
-      __syncwarp();
+      warp_plane_in(X, static_cast<const T*>(p.x) + (b * p.C + c) * HW, HW, lane);
     }
+    pre.store(Lm, lam_g + chain * HW, HW, lane, vec);
+    if (it + 1 < nitems) pre.load(lam_g + chain_of(it + 1) * HW, HW, lane, vec);
+    __syncwarp();
+    const uint32_t dir = p.dirbit[k];
+    const DirGeom gm = dir_geom(dir, H, W);
+    const int L = static_cast<int>(gm.L), P = static_cast<int>(gm.P);
+    const int ts = static_cast<int>(gm.ts);
+    const bool in = lane < P;
+    const int r = in ? lane : 0;
+    const float4* tq = TP + k * HW + r;
+    const int off0 = static_cast<int>(gm.base) + r * static_cast<int>(gm.rs);
+    const T* xp = X + off0;
+    T* lp = Lm + off0;
+    float hv = 0.f;
+#pragma unroll 4
+    for (int t = 0; t < L; ++t) {
+      if constexpr (kLocal) {
+        if (seg_start_step(dir, t, L, kc)) hv = 0.f;  // warp-uniform: h_{t-1} does not propagate
+      }
+      const float up = __shfl_up_sync(0xffffffffu, hv, 1);    // lane 0: tap a = 0
+      const float dn = __shfl_down_sync(0xffffffffu, hv, 1);  // lane P-1: tap c = 0; lanes >= P carry 0
+      const float4 q = *tq;
+      const float v = fmaf(q.x, up, fmaf(q.y, hv, fmaf(q.z, dn, to_f(*lp) * to_f(*xp))));
+      if (in) *lp = from_f<T>(v);  // h over lam at the lane's own pixel (neighbours travel by shuffle)
+      hv = in ? v : 0.f;
+      tq += P;
+      xp += ts;
+      lp += ts;
+    }
+    __syncwarp();
+    warp_plane_out(static_cast<T*>(p.hout) + chain * HW, Lm, HW, lane);
   }
 }
 
+// Backward, grouped weights. Warps form `nslot` slots of D warps; warp (slot j, k) runs direction k on the
+// channels j, j + nslot, ... of the group, so the D directions of a channel run side by side. Per channel a
+// slot shares the x plane, each warp writes g_k lam_k into its own fp32 plane, and after a slot barrier the
+// slot sums those planes in direction order into dx (no atomics, fixed order). The tap-gradient group sums
+// of a warp's direction accumulate in its own fp32 partial planes (scan order, lane r owns position r)
+// across all its channels; the slots' partials are added in slot order after the channel loop. Every
+// reduction has a fixed order: the backward is bitwise deterministic.
 template <typename T, bool kLocal>
-__global__ void __launch_bounds__(kGrpWarpsB * 32) bwd_grp_small_kernel(ScanParams p) {
+__global__ void __launch_bounds__(kGrpWarpsB * 32, 1) bwd_grp_small_kernel(ScanParams p) {
   extern __shared__ __align__(16) uint8_t sm[];
   const int H = static_cast<int>(p.H), W = static_cast<int>(p.W), HW = H * W, D = static_cast<int>(p.D);
   const int np = padded(HW, sizeof(T));
   const int64_t G = p.G, Cg = p.C / p.G;
   const int64_t b = blockIdx.x / G, g = blockIdx.x % G;
-  float* TA = reinterpret_cast<float*>(sm);
-  float* TB = TA + D * HW;
-  float* TC = TB + D * HW;
-  float* DA = TC + D * HW;  // group sums of the normalised-tap gradients, scan order [k][t P + r]
-  float* DB = DA + D * HW;
-  float* DC = DB + D * HW;
-  uint8_t* wb = sm + align16(static_cast<size_t>(6 * D * HW) * 4);
-  const size_t per_warp = align16(static_cast<size_t>(HW) * 4) + 4 * static_cast<size_t>(np) * sizeof(T);
-  unit_taps<T>(p, b, g, TA, TB, TC);
-  for (int i = threadIdx.x; i < 3 * D * HW; i += blockDim.x) DA[i] = 0.f;
-  __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  float* DX = reinterpret_cast<float*>(wb + warp * per_warp);
-  T* X = reinterpret_cast<T*>(wb + warp * per_warp + align16(static_cast<size_t>(HW) * 4));
-  T* Lm = X + np;
+  const int nslot = nw / D, k = warp % D, slot = warp / D;
+  float4* TP = reinterpret_cast<float4*>(sm);
+  uint8_t* sb = sm + align16(static_cast<size_t>(D * HW) * 16);
+  const size_t xb = align16(static_cast<size_t>(np) * sizeof(T));
+  const size_t pl_b = align16(3 * static_cast<size_t>(np) * sizeof(T));  // lam, dh, h planes
+  const size_t pk_b = align16(static_cast<size_t>(HW) * 4);              // g_k lam_k (fp32)
+  const size_t per_warp = pl_b + 4 * pk_b;                               // + partial Da / Db / Dc
+  const size_t per_slot = xb + D * per_warp;
+  T* X = reinterpret_cast<T*>(sb + slot * per_slot);
+  uint8_t* wbase = sb + slot * per_slot + xb;
+  uint8_t* mine = wbase + k * per_warp;
+  T* Lm = reinterpret_cast<T*>(mine);
   T* DH = Lm + np;
   T* Hs = DH + np;
+  float* Pk = reinterpret_cast<float*>(mine + pl_b);
+  float* SA = reinterpret_cast<float*>(mine + pl_b + pk_b);  // partial group sums, [t P + r]
+  float* SB = SA + pk_b / 4;
+  float* SC = SB + pk_b / 4;
+  unit_taps<T>(p, b, g, TP);
+  for (int i = lane; i < HW; i += 32) SA[i] = SB[i] = SC[i] = 0.f;
+  __syncthreads();
   const int kc = static_cast<int>(p.kchunk);
-  for (int64_t cc = warp; cc < Cg; cc += nw) {
-    const int64_t c = g * Cg + cc;
+  const uint32_t dir = p.dirbit[k];
+  const DirGeom gm = dir_geom(dir, H, W);
+  const int L = static_cast<int>(gm.L), P = static_cast<int>(gm.P);
+  const int ts = static_cast<int>(gm.ts), rs = static_cast<int>(gm.rs);
+  const bool in = lane < P;
+  const int r = in ? lane : 0;
+  const bool hl = in && r >= 1, hr = in && r <= P - 2;
+  const int dl = hl ? -rs : 0, dr = hr ? rs : 0;  // h_{t-1} neighbour offsets (clamped in range)
+  const int off_r = static_cast<int>(gm.base) + r * rs;
+  const int nch = static_cast<int>((Cg - slot + nslot - 1) / nslot);
+  const int bar_id = 1 + slot, bar_n = D * 32;
+  const bool vec = plane_vec<T>(p);
+  const T *x_g = static_cast<const T*>(p.x), *lam_g = static_cast<const T*>(p.lam);
+  const T *dh_g = static_cast<const T*>(p.dh), *h_g = static_cast<const T*>(p.h);
+  auto chan = [&](int i) { return g * Cg + slot + static_cast<int64_t>(i) * nslot; };
+  PlaneRegs<T> px_, pl_, pd_, ph_;  // the next channel's planes, loaded during this channel's recurrence
+  if (nch > 0) {
+    const int64_t c0 = chan(0), cb = (b * p.C + c0) * HW, ck = ((k * p.B + b) * p.C + c0) * HW;
+    if (k == 0) px_.load(x_g + cb, HW, lane, vec);
+    pl_.load(lam_g + ck, HW, lane, vec);
+    pd_.load(dh_g + ck, HW, lane, vec);
+    ph_.load(h_g + ck, HW, lane, vec);
+  }
+  for (int i = 0; i < nch; ++i) {
+    const int64_t c = chan(i);
     const int64_t bc = b * p.C + c;
-    warp_plane_in(X, static_cast<const T*>(p.x) + bc * HW, HW, lane);
-    for (int i = lane; i < HW; i += 32) DX[i] = 0.f;
-    for (int k = 0; k < D; ++k) {
-      const int64_t chain = (k * p.B + b) * p.C + c;
-      warp_plane_in(Lm, static_cast<const T*>(p.lam) + chain * HW, HW, lane);
-      warp_plane_in(DH, static_cast<const T*>(p.dh) + chain * HW, HW, lane);
-      warp_plane_in(Hs, static_cast<const T*>(p.h) + chain * HW, HW, lane);
-      __syncwarp();
-      const uint32_t dir = p.dirbit[k];
-      const DirGeom gm = dir_geom(dir, H, W);
-      const int L = static_cast<int>(gm.L), P = static_cast<int>(gm.P);
-      const int ts = static_cast<int>(gm.ts), rs = static_cast<int>(gm.rs);
-      const bool in = lane < P;
-      const int r = in ? lane : 0;
-      const bool hl = in && r >= 1, hr = in && r <= P - 2;
-      const int qk = k * HW + r;
-      int off = static_cast<int>(gm.base) + (L - 1) * ts + r * rs;
-      float ea = 0.f, eb = 0.f, ec = 0.f;  // (a g, b g, c g) of step t+1 at this position
-      for (int t = L - 1; t >= 0; --t, off -= ts) {
-        const float from_r = __shfl_down_sync(0xffffffffu, ea, 1);  // a_{t+1}[r+1] g_{t+1}[r+1]
-        const float from_l = __shfl_up_sync(0xffffffffu, ec, 1);    // c_{t+1}[r-1] g_{t+1}[r-1]
-        const float gt = in ? to_f(DH[off]) + eb + ((hr ? from_r : 0.f) + (hl ? from_l : 0.f)) : 0.f;
-        const int q = qk + t * P;
-        if (in) {
-          DH[off] = from_f<T>(gt * to_f(X[off]));       // dlam (dh at this pixel already read)
-          DX[off] = fmaf(gt, to_f(Lm[off]), DX[off]);   // dx: sum over the directions, fp32
-          if (!seg_start_step(dir, t, L, kc)) {         // h_{t-1} (0 at t = 0 / a segment start)
-            const int prev = off - ts;
-            atomicAdd(&DB[q], gt * to_f(Hs[prev]));
-            if (hl) atomicAdd(&DA[q], gt * to_f(Hs[prev - rs]));
-            if (hr) atomicAdd(&DC[q], gt * to_f(Hs[prev + rs]));
-          }
-        }
-        ea = TA[q] * gt;
-        eb = TB[q] * gt;
-        ec = TC[q] * gt;
-        if constexpr (kLocal) {
-          if (seg_start_step(dir, t, L, kc)) ea = eb = ec = 0.f;  // h_t did not depend on h_{t-1}
-        }
-      }
-      __syncwarp();
-      warp_plane_out(static_cast<T*>(p.dlam) + chain * HW, DH, HW, lane);
-      __syncwarp();
+    const int64_t chain = (k * p.B + b) * p.C + c;
+    if (k == 0) px_.store(X, x_g + bc * HW, HW, lane, vec);
+    pl_.store(Lm, lam_g + chain * HW, HW, lane, vec);
+    pd_.store(DH, dh_g + chain * HW, HW, lane, vec);
+    ph_.store(Hs, h_g + chain * HW, HW, lane, vec);
+    if (i + 1 < nch) {
+      const int64_t cn = chan(i + 1), cb = (b * p.C + cn) * HW, ck = ((k * p.B + b) * p.C + cn) * HW;
+      if (k == 0) px_.load(x_g + cb, HW, lane, vec);
+      pl_.load(lam_g + ck, HW, lane, vec);
+      pd_.load(dh_g + ck, HW, lane, vec);
+      ph_.load(h_g + ck, HW, lane, vec);
     }
-    T* dxo = static_cast<T*>(p.dx) + bc * HW;
-    for (int i = lane; i < HW; i += 32) dxo[i] = from_f<T>(DX[i]);
+    named_barrier(bar_id, bar_n);  // x staged; the previous channel's dx has read every Pk
+    float ea = 0.f, eb = 0.f, ec = 0.f;  // (a g, b g, c g) of step t+1 at this position
+    int off = off_r + (L - 1) * ts;
+    int q = (L - 1) * P + r;  // scan-order index of (t, r)
+    const float4* tq = TP + k * HW + q;
+#pragma unroll 2
+    for (int t = L - 1; t >= 0; --t) {
+      const float from_r = __shfl_down_sync(0xffffffffu, ea, 1);  // a_{t+1}[r+1] g_{t+1}[r+1]
+      const float from_l = __shfl_up_sync(0xffffffffu, ec, 1);    // c_{t+1}[r-1] g_{t+1}[r-1]
+      const float gsum = to_f(DH[off]) + eb + ((hr ? from_r : 0.f) + (hl ? from_l : 0.f));
+      const float gt = in ? gsum : 0.f;
+      const float4 tp = *tq;
+      const float dlam = gt * to_f(X[off]);
+      const float pk = gt * to_f(Lm[off]);
+      const bool seg = seg_start_step(dir, t, L, kc);  // warp-uniform; t = 0 always: h_{-1} = 0
+      const float gh = seg ? 0.f : gt;
+      const int prev = seg ? off : off - ts;  // any in-plane pixel when h_{t-1} is not used
+      const float sb_ = fmaf(gh, to_f(Hs[prev]), SB[q]);
+      const float sa_ = fmaf(hl ? gh : 0.f, to_f(Hs[prev + dl]), SA[q]);
+      const float sc_ = fmaf(hr ? gh : 0.f, to_f(Hs[prev + dr]), SC[q]);
+      if (in) {
+        DH[off] = from_f<T>(dlam);  // dlam over dh (read above)
+        Pk[off] = pk;               // g_k lam_k, summed over k into dx below
+        SA[q] = sa_;
+        SB[q] = sb_;
+        SC[q] = sc_;
+      }
+      ea = tp.x * gt;
+      eb = tp.y * gt;
+      ec = tp.z * gt;
+      if constexpr (kLocal) {
+        if (seg) ea = eb = ec = 0.f;  // h_t did not depend on h_{t-1}
+      }
+      off -= ts;
+      q -= P;
+      tq -= P;
+    }
     __syncwarp();
+    warp_plane_out(static_cast<T*>(p.dlam) + chain * HW, DH, HW, lane);
+    named_barrier(bar_id, bar_n);  // every direction's g lam of this channel is in its Pk
+    T* dxo = static_cast<T*>(p.dx) + bc * HW;
+    for (int px = k * 32 + lane; px < HW; px += bar_n) {
+      float acc = 0.f;
+      for (int kk = 0; kk < D; ++kk) acc += reinterpret_cast<const float*>(wbase + kk * per_warp + pl_b)[px];
+      dxo[px] = from_f<T>(acc);
+    }
   }
   __syncthreads();
-  // dw = normalisation Jacobian of the group sums (once per unit and direction)
+  // dw = normalisation Jacobian of the group sums (slot partials added in slot order)
   const bool prenorm = p.flags & GSPN_FLAG_PRENORMALIZED;
   const bool f32out = p.flags & GSPN_FLAG_DW_F32;
   for (int idx = threadIdx.x; idx < D * HW; idx += blockDim.x) {
-    const int k = idx / HW, q = idx - k * HW;
-    const DirGeom gm = dir_geom(p.dirbit[k], H, W);
-    const int P = static_cast<int>(gm.P), t = q / P, r = q - t * P;
-    const int pix = static_cast<int>(gm.base + t * gm.ts + r * gm.rs);
-    const int64_t w = ((k * p.B + b) * p.G + g) * HW + pix;
-    const bool hl = r >= 1, hr = r <= P - 2;
+    const int kk = idx / HW, q = idx - kk * HW;
+    const DirGeom gk = dir_geom(p.dirbit[kk], H, W);
+    const int Pq = static_cast<int>(gk.P), t = q / Pq, rr = q - t * Pq;
+    const int pix = static_cast<int>(gk.base + t * gk.ts + rr * gk.rs);
+    const int64_t w = ((kk * p.B + b) * p.G + g) * HW + pix;
+    float Da = 0.f, Db = 0.f, Dc = 0.f;
+    for (int j = 0; j < nslot; ++j) {
+      const float* part = reinterpret_cast<const float*>(sb + j * per_slot + xb + kk * per_warp + pl_b + pk_b);
+      Da += part[q];
+      Db += part[pk_b / 4 + q];
+      Dc += part[2 * (pk_b / 4) + q];
+    }
+    const bool l_on = rr >= 1, r_on = rr <= Pq - 2;
     float ol, om, orr;
     jacobian(to_f(static_cast<const T*>(p.wl)[w]), to_f(static_cast<const T*>(p.wm)[w]),
-             to_f(static_cast<const T*>(p.wr)[w]), hl, hr, prenorm, DA[idx], DB[idx], DC[idx], ol, om, orr);
+             to_f(static_cast<const T*>(p.wr)[w]), l_on, r_on, prenorm, Da, Db, Dc, ol, om, orr);
     if (f32out) {
       static_cast<float*>(p.dwl)[w] = ol;
       static_cast<float*>(p.dwm)[w] = om;
@@ -436,12 +551,14 @@ __global__ void __launch_bounds__(kGrpWarpsB * 32) bwd_grp_small_kernel(ScanPara
 
 size_t grp_fwd_smem(const ScanParams& p, int es, int nw) {
   const int np = padded(static_cast<int>(p.H * p.W), es);
-  return align16(static_cast<size_t>(3 * p.D * p.H * p.W) * 4) + static_cast<size_t>(nw) * 2 * np * es;
+  return static_cast<size_t>(p.D * p.H * p.W) * 16 + static_cast<size_t>(nw) * 2 * np * es;
 }
 size_t grp_bwd_smem(const ScanParams& p, int es, int nw) {
   const int np = padded(static_cast<int>(p.H * p.W), es);
-  return align16(static_cast<size_t>(6 * p.D * p.H * p.W) * 4) +
-         static_cast<size_t>(nw) * (align16(static_cast<size_t>(p.H * p.W) * 4) + 4 * static_cast<size_t>(np) * es);
+  const size_t HW = static_cast<size_t>(p.H * p.W), D = static_cast<size_t>(p.D);
+  const size_t per_warp = align16(3 * static_cast<size_t>(np) * es) + 4 * align16(HW * 4);
+  const size_t per_slot = align16(static_cast<size_t>(np) * es) + D * per_warp;
+  return align16(D * HW * 16) + static_cast<size_t>(nw / p.D) * per_slot;
 }
 
 template <typename K>
@@ -455,10 +572,16 @@ cudaError_t launch_grp(K kern, const ScanParams& p, int nw, size_t smem, cudaStr
 // warps per CTA: no more than the group has channels, and within the shared-memory budget
 int grp_warps(const ScanParams& p, int es, bool bwd) {
   const int64_t Cg = p.C / p.G;
-  int nw = static_cast<int>(std::min<int64_t>(bwd ? kGrpWarpsB : kGrpWarpsF, Cg));
   const size_t budget = static_cast<size_t>(device_smem_optin());
-  while (nw > 1 && (bwd ? grp_bwd_smem(p, es, nw) : grp_fwd_smem(p, es, nw)) > budget) --nw;
-  return (bwd ? grp_bwd_smem(p, es, nw) : grp_fwd_smem(p, es, nw)) <= budget ? nw : 0;
+  if (bwd) {  // D warps per slot, at most one slot per channel
+    const int D = static_cast<int>(p.D);
+    int ns = static_cast<int>(std::min<int64_t>(kGrpWarpsB / D, Cg));
+    while (ns > 1 && grp_bwd_smem(p, es, ns * D) > budget) --ns;
+    return grp_bwd_smem(p, es, ns * D) <= budget ? ns * D : 0;
+  }
+  int nw = static_cast<int>(std::min<int64_t>(kGrpWarpsF, Cg));
+  while (nw > 1 && grp_fwd_smem(p, es, nw) > budget) --nw;
+  return grp_fwd_smem(p, es, nw) <= budget ? nw : 0;
 }
 
 size_t fwd_smem(const ScanParams& p, int es) {

@@ -35,6 +35,7 @@
 // (a g, b g, c g) of the previous step, so g_t = dh_t + (b g)[r] + (a g)[r+1] + (c g)[r-1]. The output
 // kernels (a7) form dlam = g x, dx = sum_k g lam, and Da = g h_{t-1}[r-1], Db = g h_{t-1}[r],
 // Dc = g h_{t-1}[r+1] summed over the group's channels, then apply the normalisation Jacobian.
+#include <cooperative_groups.h>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -592,7 +593,7 @@ __device__ __forceinline__ void init_barriers(const Smem& m, const Plan& pl) {
       mbar_init(smem_u32(&m.empty[s]), 1);      // storer
       mbar_init(smem_u32(&m.done[s]), pl.nwc);  // one arrive per consumer warp
     }
-    for (int i = 0; i < 4; ++i) mbar_init(smem_u32(&m.xb[i]), 32);  // one arrive per lane of the sending warp
+    for (int i = 0; i < 4; ++i) mbar_init(smem_u32(&m.xb[i]), 1);  // the receiver's arrive.expect_tx
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -601,40 +602,47 @@ __device__ __forceinline__ void init_barriers(const Smem& m, const Plan& pl) {
 
 // ---- P-split ghost exchange between the CTAs of a cluster (after the intra-CTA publish).
 // Warp 0 of CTA s sends its first GH owned values to CTA s-1 (they are that CTA's right ghosts), the
-// last warp sends its last GH owned values to CTA s+1; every lane of a sending warp then arrives on
-// the receiver's barrier (release at cluster scope). Parity-double-buffered like the local edges;
+// last warp sends its last GH owned values to CTA s+1 with st.async, each store completing its bytes on
+// the receiver's barrier, which the receiver arms per half (arrive.expect_tx). Parity-double-buffered like
+// the local edges;
 // a sender cannot run two halves ahead because it needs the receiver's edges of the half between.
 // side 0: towards rank - 1, side 1: towards rank + 1.
 __device__ __forceinline__ bool xgo(int side, int wi, int nwc, int rank, int cl) {
   return side == 0 ? (wi == 0 && rank > 0) : (wi == nwc - 1 && rank < cl - 1);
 }
 
+// st.async: the remote store itself signals the receiver's mbarrier (complete_tx) when the value has landed,
+// so the sender needs no release fence -- a release at cluster scope would also wait for this thread's
+// outstanding global stores (the h / g rows of the vertical chains) on every exchange.
 template <typename T>
 __device__ __forceinline__ void xput(const Smem& m, int par, int side, uint32_t tr, int a, int lane, bool vert,
                                      const float (&v)[kE]) {
   using C = Cfg<T>;
   constexpr int WARP = 32 * kE;
   float* dst = (side == 0 ? m.xr : m.xl) + (a * 2 + par) * 8;  // left-going data = receiver's right ghosts
+  const uint32_t bar = mapa(smem_u32(&m.xb[(side == 0 ? 2 : 0) + par]), tr);
   if (vert) {
     const int o = kE * lane;
     const int lo = side == 0 ? C::GH : WARP - 2 * C::GH;
     if (o >= lo && o < lo + C::GH) {
 #pragma unroll
-      for (int e = 0; e < kE; ++e) st_cluster_f32(mapa(smem_u32(dst + o - lo + e), tr), v[e]);
+      for (int e = 0; e < kE; ++e) st_async_f32(mapa(smem_u32(dst + o - lo + e), tr), v[e], bar);
     }
   } else {
     const int lo = side == 0 ? C::GH : 32 - 2 * C::GH;
-    if (lane >= lo && lane < lo + C::GH) st_cluster_f32(mapa(smem_u32(dst + lane - lo), tr), side == 0 ? v[0] : v[kE - 1]);
+    if (lane >= lo && lane < lo + C::GH)
+      st_async_f32(mapa(smem_u32(dst + lane - lo), tr), side == 0 ? v[0] : v[kE - 1], bar);
   }
 }
 
-__device__ __forceinline__ void xarrive(const Smem& m, int par, int side, uint32_t tr) {
-  __syncwarp();
-  mbar_arrive_remote(mapa(smem_u32(&m.xb[(side == 0 ? 2 : 0) + par]), tr));
-}
+__device__ __forceinline__ void xarrive(const Smem&, int, int, uint32_t) {}
 
-__device__ __forceinline__ void xwait(const Smem& m, int par, int side, uint32_t xphase) {
-  mbar_wait_cluster(smem_u32(&m.xb[(side == 0 ? 0 : 2) + par]), xphase);
+// The receiving warp arms its barrier for this half's bytes (GH values per exchanged array) and waits.
+template <typename T>
+__device__ __forceinline__ void xwait(const Smem& m, int par, int side, uint32_t xphase, int narr) {
+  const uint32_t bar = smem_u32(&m.xb[(side == 0 ? 0 : 2) + par]);
+  if ((threadIdx.x & 31) == 0) mbar_arrive_tx(bar, static_cast<uint32_t>(narr * Cfg<T>::GH * 4));
+  mbar_wait_cluster(bar, xphase);
 }
 
 template <typename T>
@@ -868,7 +876,7 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) fwd_stream_kernel(const
 #pragma unroll
           for (int side = 0; side < 2; ++side) {
             if (!xgo(side, warp, pl.nwc, rank, pl.cl)) continue;
-            xwait(m, par, side, (xphase >> par) & 1u);
+            xwait<T>(m, par, side, (xphase >> par) & 1u, 1);
             xget<T>(m, par, side, 0, lane, ch.vert, h);
           }
           xphase ^= 1u << par;
@@ -1062,7 +1070,7 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_stream_kernel(const
 #pragma unroll
           for (int side = 0; side < 2; ++side) {
             if (!xgo(side, warp, pl.nwc, rank, pl.cl)) continue;
-            xwait(m, par, side, (xphase >> par) & 1u);
+            xwait<T>(m, par, side, (xphase >> par) & 1u, 3);
             xget<T>(m, par, side, 0, lane, ch.vert, S.ea);
             xget<T>(m, par, side, 1, lane, ch.vert, S.eb);
             xget<T>(m, par, side, 2, lane, ch.vert, S.ec);
@@ -1263,14 +1271,13 @@ __device__ void producer_fused(const StreamArgs& A, uint8_t* ring, uint64_t* ful
   }
 }
 
+// Body of the fused backward recurrence (every role returns from here when its work is done); the
+// barriers of `m` must be initialised. Shared by bwd_fused_kernel and the single-launch bwd_one_kernel.
 template <typename T, int kPre, bool kLocal>
-__global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_fused_kernel(const __grid_constant__ StreamArgs A) {
+__device__ __forceinline__ void bwd_fused_body(const StreamArgs& A, const Smem& m) {
   using C = Cfg<T>;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
   const Plan& pl = A.plan;
-  const Smem m = carve(smem_raw, pl);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  init_barriers<false>(m, pl);
   if (warp == pl.nwc) {
     if (lane == 0) {
       for (int o = 0; o < 2; ++o)
@@ -1376,6 +1383,14 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_fused_kernel(const 
       if (++stage == pl.nstages) { stage = 0; phase ^= 1; }
     }
   }
+}
+
+template <typename T, int kPre, bool kLocal>
+__global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_fused_kernel(const __grid_constant__ StreamArgs A) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const Smem m = carve(smem_raw, A.plan);
+  init_barriers<false>(m, A.plan);
+  bwd_fused_body<T, kPre, kLocal>(A, m);
 }
 
 // dlam_k = g_k x and dx = sum_k g_k lam_k (a7), elementwise over [B, C, H, W] with all D directions per
@@ -1854,25 +1869,18 @@ __device__ __forceinline__ void sm_ld4v(const uint8_t* p, float (&v)[4]) {
 
 // kVertDone: the fused recurrence already wrote dw of the vertical directions (hybrid backward): their
 // w and h tiles are neither loaded nor used, only dlam and dx are formed for them.
+// Body of the TMA-staged output kernel: warps [0, ncons) consume, warp ncons produces, any other warp
+// returns at once. full[] / empty[] (A.nstages each, at the end of the ring) must be initialised with
+// counts 1 / ncons. Shared by bwd_out_tma_kernel and the second phase of bwd_one_kernel.
 template <typename T, bool kLocal, bool kVertDone>
-__global__ void __launch_bounds__((kOutConsumers + 1) * 32, 1) bwd_out_tma_kernel(const __grid_constant__ OutArgs A) {
+__device__ __forceinline__ void out_tma_body(const OutArgs& A, uint8_t* ring, uint64_t* full, uint64_t* empty,
+                                             int ncons) {
   constexpr int V = 4;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* ring = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t* full = reinterpret_cast<uint64_t*>(ring + static_cast<size_t>(A.nstages) * A.stage_bytes);
-  uint64_t* empty = full + A.nstages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const ScanParams& p = A.p;
   const int D = p.D, RB = A.RB, BX = A.BX;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < A.nstages; ++s) {
-      mbar_init(smem_u32(&full[s]), 1);
-      mbar_init(smem_u32(&empty[s]), kOutConsumers);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  if (warp == kOutConsumers) {  // producer
+  if (warp > ncons) return;
+  if (warp == ncons) {  // producer
     if (lane == 0) {
       const uint64_t pol = policy_of(0);  // every input is read once
       int stage = 0;
@@ -1910,7 +1918,7 @@ __global__ void __launch_bounds__((kOutConsumers + 1) * 32, 1) bwd_out_tma_kerne
   const int64_t H = p.H, W = p.W, HW = H * W;
   const int64_t kstride = p.B * p.C * HW;  // between direction slabs of lam / g / h / w (G = C) / outputs
   const int nchunk = static_cast<int>(W / V);
-  const int nthreads = kOutConsumers * 32;
+  const int nthreads = ncons * 32;
   constexpr int es = static_cast<int>(sizeof(T));
   const uint32_t rowb = static_cast<uint32_t>(BX * es);  // bytes per box row
   int stage = 0;
@@ -2012,6 +2020,73 @@ __global__ void __launch_bounds__((kOutConsumers + 1) * 32, 1) bwd_out_tma_kerne
     if (lane == 0) mbar_arrive(smem_u32(&empty[stage]));
     if (++stage == A.nstages) { stage = 0; phase ^= 1; }
   }
+}
+
+template <typename T, bool kLocal, bool kVertDone>
+__global__ void __launch_bounds__((kOutConsumers + 1) * 32, 1) bwd_out_tma_kernel(const __grid_constant__ OutArgs A) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* ring = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + static_cast<size_t>(A.nstages) * A.stage_bytes);
+  uint64_t* empty = full + A.nstages;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < A.nstages; ++s) {
+      mbar_init(smem_u32(&full[s]), 1);
+      mbar_init(smem_u32(&empty[s]), kOutConsumers);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  out_tma_body<T, kLocal, kVertDone>(A, ring, full, empty, kOutConsumers);
+}
+
+// ---- Single-launch backward (north_star "one persistent kernel per call"; "Kernel Fuse";
+// SURVEY.md §8(c) reading 17). One cooperative persistent launch: phase 1 is the fused adjoint recurrence
+// (bwd_fused_body: g, and dw of the vertical chains), then a grid-wide barrier (every g must be complete
+// before any (b, c, rows) unit sums dx over the directions), then phase 2 is the TMA-staged output pass
+// (out_tma_body: dlam, dx, and dw of the horizontal chains) on the same CTAs, their shared memory re-carved
+// as the output ring. Phase 2's consumers are phase 1's consumer warps, its producer phase 1's producer.
+struct OneArgs {
+  StreamArgs s;
+  OutArgs o;
+};
+
+__device__ __forceinline__ void mbar_inval(uint32_t bar) {
+  asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
+template <typename T, int kPre, bool kLocal>
+__global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_one_kernel(const __grid_constant__ OneArgs A) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const Plan& pl = A.s.plan;
+  const Smem m = carve(smem_raw, pl);
+  init_barriers<false>(m, pl);
+  bwd_fused_body<T, kPre, kLocal>(A.s, m);
+  // g (generic stores of the vertical chains, TMA stores of the horizontal ones -- the storer waited for
+  // their completion) must be visible to the other CTAs' TMA loads of phase 2
+  fence_proxy_async_global();
+  __syncthreads();
+  cooperative_groups::this_grid().sync();
+  const OutArgs& O = A.o;
+  uint64_t* full = reinterpret_cast<uint64_t*>(m.ring + static_cast<size_t>(O.nstages) * O.stage_bytes);
+  uint64_t* empty = full + O.nstages;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < pl.nstages; ++s) {
+      mbar_inval(smem_u32(&m.full[s]));
+      mbar_inval(smem_u32(&m.empty[s]));
+      mbar_inval(smem_u32(&m.done[s]));
+    }
+    for (int i = 0; i < 4; ++i) mbar_inval(smem_u32(&m.xb[i]));
+    for (int s = 0; s < O.nstages; ++s) {
+      mbar_init(smem_u32(&full[s]), 1);
+      mbar_init(smem_u32(&empty[s]), pl.nwc);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  fence_proxy_async();        // phase-1 generic writes of the ring before phase-2 TMA writes into it
+  fence_proxy_async_global();
+  __syncthreads();
+  out_tma_body<T, kLocal, true>(O, m.ring, full, empty, pl.nwc);
 }
 
 // ---- Grouped weights (G < C): a unit is (b, group, RB rows); the ring streams one channel of the
@@ -2476,20 +2551,17 @@ cudaError_t launch_fwd_stream(const ScanParams& p, gspn_dtype_t dt, cudaStream_t
   return e;
 }
 
-// TMA-staged output kernel (G = C). Returns false if the shape does not fit (caller falls back).
-bool launch_out_tma(const ScanParams& p, const void* g, gspn_dtype_t dt, cudaStream_t s, cudaError_t* err,
-                    bool vert_done = false, bool dry_run = false) {
+// Plan + tensor maps of the TMA-staged output kernel for `ncons` consumer warps within `budget` bytes of
+// shared memory. Returns false if the shape does not fit.
+bool setup_out_tma(const ScanParams& p, const void* g, gspn_dtype_t dt, bool vert_done, int ncons, int budget,
+                   OutArgs& A) {
   const bool grouped = p.G != p.C;
-  if (knob("GSPN_OUT_REG")) return false;  // experiments: register-staged kernel
-  std::unique_ptr<OutArgs> hold(new OutArgs());
-  OutArgs& A = *hold;
   memset(&A, 0, sizeof A);
   A.p = p;
   const int es = dt == GSPN_BF16 ? 2 : 4;
   A.BX = static_cast<int>(std::min<int64_t>(p.W, 256));
   A.nbx = static_cast<int>((p.W + A.BX - 1) / A.BX);
   const int D = static_cast<int>(p.D);
-  const int budget = smem_optin() - 1024 - 256;
   auto pad = [](int64_t v) { return (v + 127) / 128 * 128; };
   const int nrb_t = grouped ? 2 : 5;  // RB-row tiles per direction: g, lam (+ w_l, w_m, w_r)
   auto stage_of = [&](int rb) {
@@ -2497,10 +2569,10 @@ bool launch_out_tma(const ScanParams& p, const void* g, gspn_dtype_t dt, cudaStr
   };
   // enough rows per unit to give every consumer thread a 4-column chunk, 2+ stages
   int RB = 1;
-  while (RB < 16 && RB * (p.W / 4) < kOutConsumers * 32) RB <<= 1;
+  while (RB < 16 && RB * (p.W / 4) < ncons * 32) RB <<= 1;
   if (grouped) {  // exactly one chunk per thread: the group sums live in its registers
-    while (RB > 1 && RB * (p.W / 4) > kOutConsumers * 32) RB >>= 1;
-    if (p.W / 4 > kOutConsumers * 32) return false;
+    while (RB > 1 && RB * (p.W / 4) > ncons * 32) RB >>= 1;
+    if (p.W / 4 > ncons * 32) return false;
   }
   while (RB > 1 && 2 * stage_of(RB) > budget) RB >>= 1;
   if (2 * stage_of(RB) > budget) return false;
@@ -2537,9 +2609,21 @@ bool launch_out_tma(const ScanParams& p, const void* g, gspn_dtype_t dt, cudaStr
             encode(&A.wm, p.wm, dt, p.W, p.H, nc, A.BX, RB, false) &&
             encode(&A.wr, p.wr, dt, p.W, p.H, nc, A.BX, RB, false) &&
             encode(&A.h, p.h, dt, p.W, p.H, nc, A.BX, RB + 2, false);
-  if (!ok) return false;
+  return ok;
+}
+
+uint32_t out_tma_smem(const OutArgs& A) { return 1024 + A.nstages * A.stage_bytes + 2 * 8 * A.nstages; }
+
+// TMA-staged output kernel. Returns false if the shape does not fit (caller falls back).
+bool launch_out_tma(const ScanParams& p, const void* g, gspn_dtype_t dt, cudaStream_t s, cudaError_t* err,
+                    bool vert_done = false, bool dry_run = false) {
+  const bool grouped = p.G != p.C;
+  if (knob("GSPN_OUT_REG")) return false;  // experiments: register-staged kernel
+  std::unique_ptr<OutArgs> hold(new OutArgs());
+  OutArgs& A = *hold;
+  if (!setup_out_tma(p, g, dt, vert_done, kOutConsumers, smem_optin() - 1024 - 256, A)) return false;
   if (dry_run) return true;
-  const uint32_t smem = 1024 + A.nstages * A.stage_bytes + 2 * 8 * A.nstages;
+  const uint32_t smem = out_tma_smem(A);
   using BF = __nv_bfloat16;
   auto kern = p.kchunk > 0
       ? (grouped ? (dt == GSPN_BF16 ? bwd_out_grp_tma_kernel<BF, true> : bwd_out_grp_tma_kernel<float, true>)
@@ -2565,6 +2649,35 @@ bool launch_out_tma(const ScanParams& p, const void* g, gspn_dtype_t dt, cudaStr
   }
   *err = e;
   return true;
+}
+
+// Cooperative persistent launch of bwd_one_kernel: every CTA resident at once (the grid barrier needs
+// it), grid = resident CTAs capped at the larger of the two phases' work-item counts.
+template <typename KernelT>
+cudaError_t launch_one(KernelT kernel, const OneArgs& A, cudaStream_t s) {
+  const uint32_t smem = std::max<uint32_t>(A.s.plan.smem_bytes, out_tma_smem(A.o));
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  const int threads = (A.s.plan.nwc + 2) * 32;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  int64_t grid = static_cast<int64_t>(sm_count()) * per_sm;
+  grid = std::min<int64_t>(grid, std::max<int64_t>(A.s.plan.nchains, A.o.nunits));
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.gridDim = dim3(static_cast<unsigned>(grid), 1, 1);
+  cfg.blockDim = dim3(threads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, kernel, A);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
 }
 
 // dlam and dx of the fused backward (one elementwise launch over [B, C, H, W]).
@@ -2623,6 +2736,30 @@ bool launch_bwd_fused(const ScanParams& p0, gspn_dtype_t dt, cudaStream_t s, int
   cudaError_t e0 = cudaSuccess;
   if (!pl.fuse_h && !launch_out_tma(p, A.g, dt, s, &e0, true, true)) return false;  // output kernel must fit
   const int mode = norm_mode(p, pl);
+  if (!pl.fuse_h && !knob("GSPN_TWO_LAUNCH")) {  // single launch: recurrence | grid barrier | outputs
+    std::unique_ptr<OneArgs> one(new OneArgs());
+    one->s = A;
+    if (setup_out_tma(p, A.g, dt, true, pl.nwc, smem_optin() - 1024 - 256, one->o)) {
+      cudaError_t e;
+      using BF = __nv_bfloat16;
+      if (dt == GSPN_BF16) {
+        if (local) e = mode == kNormPre ? launch_one(bwd_one_kernel<BF, kNormPre, true>, *one, s)
+                                        : launch_one(bwd_one_kernel<BF, kNormClamp, true>, *one, s);
+        else e = mode == kNormPre ? launch_one(bwd_one_kernel<BF, kNormPre, false>, *one, s)
+                 : mode == kNormClamp ? launch_one(bwd_one_kernel<BF, kNormClamp, false>, *one, s)
+                                      : launch_one(bwd_one_kernel<BF, kNormFull, false>, *one, s);
+      } else {
+        if (local) e = mode == kNormPre ? launch_one(bwd_one_kernel<float, kNormPre, true>, *one, s)
+                                        : launch_one(bwd_one_kernel<float, kNormClamp, true>, *one, s);
+        else e = mode == kNormPre ? launch_one(bwd_one_kernel<float, kNormPre, false>, *one, s)
+                 : mode == kNormClamp ? launch_one(bwd_one_kernel<float, kNormClamp, false>, *one, s)
+                                      : launch_one(bwd_one_kernel<float, kNormFull, false>, *one, s);
+      }
+      *launches += 1;
+      *err = e;
+      return true;
+    }
+  }
   cudaError_t e;
   if (dt == GSPN_BF16) {
     using BF = __nv_bfloat16;
