@@ -643,23 +643,31 @@ def measure_next(args, gspn, cfg, sh, t, h, outs, ws, dev, stream):
     out["local"] = {"kchunk": k, "fwd_ms": lf, "bwd_ms": lb, "gbs": 3 * bf / ((lf + lb) * 1e-3) / 1e9,
                     "path": lpath}
     out["local"]["frac"] = out["local"]["gbs"] / peak
-    # NEXT-4: proxy projections on BASELINE configs[2]'s compact block (B=64, C=384 -> C_proxy=8, 28 x 28)
-    pB, pC, pCp, pH, pW = 64, 384, 8, 28, 28
+    # NEXT-4: proxy projections (gspn_proxy_mix / _wgrad) on the compact blocks of BASELINE configs[2]
+    # (B=64, C=384 -> C_proxy=8, 28 x 28) and configs[4] (B=1, C=320 -> 40, 2048 x 2048): tcgen05 path
+    # (default for bf16) and the SIMT kernel; bytes = s B HW (C + C_proxy) per mix / wgrad.
     dtp = torch.bfloat16
     g = torch.Generator(device=dev).manual_seed(7884)
-    xin = (torch.rand((pB, pC, pH, pW), generator=g, device=dev) * 2 - 1).to(dtp)
-    Pd = ((torch.rand((pCp, pC), generator=g, device=dev) * 2 - 1) / pC ** 0.5).to(dtp)
-    Qu = ((torch.rand((pC, pCp), generator=g, device=dev) * 2 - 1) / pCp ** 0.5).to(dtp)
-    xp = torch.empty((pB, pCp, pH, pW), dtype=dtp, device=dev)
-    yo = torch.empty_like(xin)
-    dPd = torch.empty((pCp, pC), dtype=torch.float32, device=dev)
-    md = timed(lambda: gspn.proxy_mix(xin, Pd, out=xp), reps)
-    mu = timed(lambda: gspn.proxy_mix(xp, Qu, out=yo), reps)
-    mw = timed(lambda: gspn.proxy_wgrad(xp, xin, out=dPd), reps)
-    nb = 2 * pB * pH * pW * (pC + pCp)
-    out["proxy"] = {"shape": f"B={pB} C={pC} C_proxy={pCp} {pH}x{pW} bf16",
-                    "down_ms": md, "down_gbs": nb / (md * 1e-3) / 1e9, "up_ms": mu, "up_gbs": nb / (mu * 1e-3) / 1e9,
-                    "wgrad_ms": mw, "wgrad_gbs": nb / (mw * 1e-3) / 1e9, "bytes": nb}
+    out["proxy"] = {}
+    for tag, (pB, pC, pCp, pH, pW) in (("cfg3", (64, 384, 8, 28, 28)), ("cfg5", (1, 320, 40, 2048, 2048))):
+        xin = (torch.rand((pB, pC, pH, pW), generator=g, device=dev) * 2 - 1).to(dtp)
+        Pd = ((torch.rand((pCp, pC), generator=g, device=dev) * 2 - 1) / pC ** 0.5).to(dtp)
+        Qu = ((torch.rand((pC, pCp), generator=g, device=dev) * 2 - 1) / pCp ** 0.5).to(dtp)
+        xp = torch.empty((pB, pCp, pH, pW), dtype=dtp, device=dev)
+        yo = torch.empty_like(xin)
+        dPd = torch.empty((pCp, pC), dtype=torch.float32, device=dev)
+        nb = 2 * pB * pH * pW * (pC + pCp)
+        rec = {"shape": f"B={pB} C={pC} C_proxy={pCp} {pH}x{pW} bf16", "bytes": nb}
+        for impl, simt in (("umma", False), ("simt", True)):
+            md = timed(lambda: gspn.proxy_mix(xin, Pd, out=xp, simt=simt), reps)
+            pth = gspn.last_path()
+            mu = timed(lambda: gspn.proxy_mix(xp, Qu, out=yo, simt=simt), reps)
+            rec[impl] = {"path": pth, "down_ms": md, "down_gbs": nb / (md * 1e-3) / 1e9, "down_frac": nb / (md * 1e-3) / 1e9 / peak,
+                         "up_ms": mu, "up_gbs": nb / (mu * 1e-3) / 1e9, "up_frac": nb / (mu * 1e-3) / 1e9 / peak}
+        mw = timed(lambda: gspn.proxy_wgrad(xp, xin, out=dPd), reps)
+        rec["wgrad"] = {"path": gspn.last_path(), "ms": mw, "gbs": nb / (mw * 1e-3) / 1e9, "frac": nb / (mw * 1e-3) / 1e9 / peak}
+        out["proxy"][tag] = rec
+        del xin, Pd, Qu, xp, yo, dPd
     return out
 
 

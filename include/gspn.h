@@ -158,6 +158,25 @@ gspn_status_t gspn_merge_bwd(const void* h, const void* u, const void* dy, void*
                              gspn_stream_t stream);
 
 /*
+ * Backward through the scan AND the output gate + direction merge in one call (SURVEY.md §8(f) NEXT-1,
+ * PAPER.md:84-88 Eq. 2): given the merge's upstream gradient dy [B,C,H,W] and the gate u [D,B,C,H,W],
+ * the scan's upstream gradient is dh_d = s u_d (.) dy (s = 1, or 1/D with GSPN_FLAG_MERGE_MEAN) and the
+ * gate's gradient du_d = s h_d (.) dy [D,B,C,H,W] is written alongside dx, dw, dlam (gspn_bwd's outputs).
+ * On the fused path (per-channel weights, unpacked or packed, not P-split) dh is formed inside the single
+ * backward launch and never stored (gspn_last_path() "stream-fused-merged"); otherwise the merge adjoint
+ * writes dh into the workspace and gspn_bwd follows ("merged-unfused"). flags: GSPN_FLAG_PRENORMALIZED,
+ * GSPN_FLAG_MERGE_MEAN, GSPN_FLAG_FORCE_GENERIC. workspace: >= gspn_bwd_merged_workspace_bytes(...).
+ * Other conventions as gspn_bwd.
+ */
+gspn_status_t gspn_bwd_merged(const void* x, const void* w_l, const void* w_m, const void* w_r, const void* lam,
+                              const void* h, const void* u, const void* dy, void* dx, void* dw_l, void* dw_m,
+                              void* dw_r, void* dlam, void* du, int64_t B, int64_t C, int64_t H, int64_t W,
+                              uint32_t dirs, int64_t groups, gspn_dtype_t dtype, uint32_t flags, void* workspace,
+                              size_t workspace_bytes, gspn_stream_t stream);
+size_t gspn_bwd_merged_workspace_bytes(int64_t B, int64_t C, int64_t H, int64_t W, uint32_t dirs, int64_t groups,
+                                       gspn_dtype_t dtype);
+
+/*
  * Compact-channel proxy projections (§4.2 "project the input tensor
  * x in R^{N x C x H x W} into a lower-dimensional proxy subspace x_proxy in R^{N x C_proxy x H x W}",
  * PAPER.md:172 "expand back to C with a learned 1x1 projection"). A 1x1 projection mixes channels at
@@ -166,16 +185,21 @@ gspn_status_t gspn_merge_bwd(const void* h, const void* u, const void* dy, void*
  *   M [Co, Ci] row-major in dtype, or, with GSPN_FLAG_PROXY_TRANSPOSE, M stored [Ci, Co] (its transpose
  *   is used): the data gradient of a projection by M is the projection of the upstream gradient by M^T.
  *   Down-projection: M = P_down [C_proxy, C]; up-projection: M = P_up [C, C_proxy]. fp32 accumulation.
- *   H*W must be even; Co*Ci <= 49152 (M staged in shared memory). One launch.
+ *   H*W must be even. One launch. bf16 with Co <= 512 and H*W % 8 == 0 runs on the tensor cores
+ *   (tcgen05.mma, fp32 accumulator in TMEM; gspn_last_path() "proxy-umma"), anything else on SIMT FMAs
+ *   ("proxy"), which needs Co*Ci <= 49152 (M staged in shared memory).
  */
 #define GSPN_FLAG_PROXY_TRANSPOSE 0x8u
+#define GSPN_FLAG_PROXY_SIMT 0x10u /* testing: gspn_proxy_mix on the SIMT kernel instead of tcgen05 */
 gspn_status_t gspn_proxy_mix(const void* in, const void* M, void* out, int64_t B, int64_t Ci, int64_t Co, int64_t H,
                              int64_t W, gspn_dtype_t dtype, uint32_t flags, gspn_stream_t stream);
 /*
  * Weight gradient of gspn_proxy_mix:  dM[o, i] = sum_{b, pixels} dout[b, o, :] . in[b, i, :]
  *   dout [B, Co, H, W], in [B, Ci, H, W] (dtype) -> dM [Co, Ci] in FP32 (overwritten; a reduction over
- *   B H W terms). (Co + Ci) * 33 + Co * Ci <= 49152. A memset and one launch (fp32 atomics across CTAs,
- *   so the summation order -- not the result beyond fp32 rounding -- varies between runs).
+ *   B H W terms). SIMT path: (Co + Ci) * 33 + Co * Ci <= 49152. A memset and one launch (fp32 atomics across CTAs,
+ *   so the summation order -- not the result beyond fp32 rounding -- varies between runs). bf16 with
+ *   Co, Ci <= 512 and H*W % 8 == 0 runs on the tensor cores (each CTA's share of the pixels accumulated in
+ *   TMEM; gspn_last_path() "proxy-umma").
  */
 gspn_status_t gspn_proxy_wgrad(const void* dout, const void* in, float* dM, int64_t B, int64_t Ci, int64_t Co,
                                int64_t H, int64_t W, gspn_dtype_t dtype, gspn_stream_t stream);

@@ -26,6 +26,7 @@ FLAG_MERGE_MEAN = 0x4
 FLAG_PROXY_TRANSPOSE = 0x8
 FLAG_FORCE_SPLIT = 0x10
 FLAG_DW_F32 = 0x20
+FLAG_PROXY_SIMT = 0x10  # proxy_mix only
 DTYPE_F32, DTYPE_BF16 = 0, 1
 
 
@@ -170,8 +171,40 @@ def merge_bwd(h, u, dy, dirs: int = DIR_ALL, mean: bool = False, outs=None, stre
     return dh, du
 
 
-def proxy_mix(inp, M, transpose: bool = False, out=None, stream=None):
-    """out [B,Co,H,W] = sum_i M[o,i] inp[b,i]; M [Co, Ci] (or [Ci, Co] used transposed)."""
+def bwd_merged(x, w_l, w_m, w_r, lam, h, u, dy, dirs: int = DIR_ALL, groups: int | None = None, mean: bool = False,
+               flags: int = 0, outs=None, workspace=None, stream=None):
+    """Backward through the scan and the output gate + direction merge (gspn_bwd_merged, NEXT-1):
+    returns (dx, dw_l, dw_m, dw_r, dlam, du)."""
+    torch = _torch()
+    G = x.shape[1] if groups is None else int(groups)
+    (B, C, H, W, D), sx, sw, sl = _scan_shapes(x, dirs, G)
+    dt = _dtype_code(x)
+    if outs is None:
+        outs = (torch.empty_like(x), torch.empty_like(w_l), torch.empty_like(w_m), torch.empty_like(w_r),
+                torch.empty_like(lam), torch.empty_like(lam))
+    if len(outs) != 6:
+        raise ValueError("outs must be (dx, dw_l, dw_m, dw_r, dlam, du)")
+    dx, dwl, dwm, dwr, dlam, du = outs
+    _check_shapes([("w_l", w_l, sw), ("w_m", w_m, sw), ("w_r", w_r, sw), ("lam", lam, sl), ("h", h, sl),
+                   ("u", u, sl), ("dy", dy, sx), ("dx (out)", dx, sx), ("dw_l (out)", dwl, sw),
+                   ("dw_m (out)", dwm, sw), ("dw_r (out)", dwr, sw), ("dlam (out)", dlam, sl), ("du (out)", du, sl)])
+    _check_tensors([("x", x), ("w_l", w_l), ("w_m", w_m), ("w_r", w_r), ("lam", lam), ("h", h), ("u", u), ("dy", dy),
+                    ("dx", dx), ("dw_l", dwl), ("dw_m", dwm), ("dw_r", dwr), ("dlam", dlam), ("du", du)],
+                   x.dtype, x.device)
+    need = int(lib().gspn_bwd_merged_workspace_bytes(B, C, H, W, dirs, G, dt))
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(max(need, 16), dtype=torch.uint8, device=x.device)
+    check(lib().gspn_bwd_merged(x.data_ptr(), w_l.data_ptr(), w_m.data_ptr(), w_r.data_ptr(), lam.data_ptr(),
+                                h.data_ptr(), u.data_ptr(), dy.data_ptr(), dx.data_ptr(), dwl.data_ptr(),
+                                dwm.data_ptr(), dwr.data_ptr(), dlam.data_ptr(), du.data_ptr(), B, C, H, W, dirs, G, dt,
+                                flags | (FLAG_MERGE_MEAN if mean else 0), workspace.data_ptr(), workspace.numel(),
+                                _stream_ptr(stream, x.device)))
+    return dx, dwl, dwm, dwr, dlam, du
+
+
+def proxy_mix(inp, M, transpose: bool = False, out=None, stream=None, simt: bool = False):
+    """out [B,Co,H,W] = sum_i M[o,i] inp[b,i]; M [Co, Ci] (or [Ci, Co] used transposed). bf16 shapes the
+    tensor-core kernel tiles run on tcgen05 unless simt=True (testing)."""
     torch = _torch()
     B, Ci, H, W = inp.shape
     if transpose:
@@ -186,7 +219,8 @@ def proxy_mix(inp, M, transpose: bool = False, out=None, stream=None):
     _check_shapes([("M", M, (Ci, Co) if transpose else (Co, Ci)), ("out", out, (B, Co, H, W))])
     _check_tensors([("in", inp), ("M", M), ("out", out)], inp.dtype, inp.device)
     check(lib().gspn_proxy_mix(inp.data_ptr(), M.data_ptr(), out.data_ptr(), B, Ci, Co, H, W, _dtype_code(inp),
-                               FLAG_PROXY_TRANSPOSE if transpose else 0, _stream_ptr(stream, inp.device)))
+                               (FLAG_PROXY_TRANSPOSE if transpose else 0) | (FLAG_PROXY_SIMT if simt else 0),
+                               _stream_ptr(stream, inp.device)))
     return out
 
 

@@ -352,6 +352,88 @@ static gspn_status_t check_proxy_extent(int64_t B, int64_t Ci, int64_t Co, int64
 
 extern "C" {
 
+size_t gspn_bwd_merged_workspace_bytes(int64_t B, int64_t C, int64_t H, int64_t W, uint32_t dirs, int64_t groups,
+                                       gspn_dtype_t dtype) {
+  const size_t a = gspn_bwd_workspace_bytes(B, C, H, W, dirs, groups, dtype);
+  if (a == 0 && check_dims(B, C, H, W, dirs, groups, dtype, 0) != GSPN_OK) return 0;
+  const size_t s = dtype == GSPN_BF16 ? 2 : 4;
+  return align_up(a) + align_up((size_t)popcount4(dirs) * (size_t)(B * C * H * W) * s);  // + dh (unfused fallback)
+}
+
+gspn_status_t gspn_bwd_merged(const void* x, const void* w_l, const void* w_m, const void* w_r, const void* lam,
+                              const void* h, const void* u, const void* dy, void* dx, void* dw_l, void* dw_m,
+                              void* dw_r, void* dlam, void* du, int64_t B, int64_t C, int64_t H, int64_t W,
+                              uint32_t dirs, int64_t groups, gspn_dtype_t dtype, uint32_t flags, void* workspace,
+                              size_t workspace_bytes, gspn_stream_t stream) {
+  return guarded([&]() -> gspn_status_t {
+    gspn_status_t st;
+    if ((st = check_ptr(x, "x")) || (st = check_ptr(w_l, "w_l")) || (st = check_ptr(w_m, "w_m")) ||
+        (st = check_ptr(w_r, "w_r")) || (st = check_ptr(lam, "lam")) || (st = check_ptr(h, "h")) ||
+        (st = check_ptr(u, "u")) || (st = check_ptr(dy, "dy")) || (st = check_ptr(dx, "dx")) ||
+        (st = check_ptr(dw_l, "dw_l")) || (st = check_ptr(dw_m, "dw_m")) || (st = check_ptr(dw_r, "dw_r")) ||
+        (st = check_ptr(dlam, "dlam")) || (st = check_ptr(du, "du")))
+      return st;
+    if (flags & ~(GSPN_FLAG_PRENORMALIZED | GSPN_FLAG_MERGE_MEAN | GSPN_FLAG_FORCE_GENERIC))
+      return fail(GSPN_ERR_INVALID_ARG, "%s has unknown bits (0x%llx)", "flags", flags);
+    const uint32_t sflags = flags & ~GSPN_FLAG_MERGE_MEAN;
+    if ((st = check_dims(B, C, H, W, dirs, groups, dtype, sflags))) return st;
+    const int64_t D = popcount4(dirs);
+    const size_t need_bwd = gspn_bwd_workspace_bytes(B, C, H, W, dirs, groups, dtype);
+    const size_t need = gspn_bwd_merged_workspace_bytes(B, C, H, W, dirs, groups, dtype);
+    if ((st = check_ptr(workspace, "workspace"))) return st;
+    if (workspace_bytes < need) {
+      snprintf(t_detail, sizeof t_detail, "workspace too small: %zu < %zu bytes", workspace_bytes, need);
+      return GSPN_ERR_INVALID_ARG;
+    }
+    const size_t s = dtype == GSPN_BF16 ? 2 : 4;
+    const size_t nx = (size_t)(B * C * H * W) * s, nl = (size_t)D * nx, nw = (size_t)(D * B * groups * H * W) * s;
+    const Span ins[8] = {span("x", x, nx),     span("w_l", w_l, nw), span("w_m", w_m, nw), span("w_r", w_r, nw),
+                         span("lam", lam, nl), span("h", h, nl),     span("u", u, nl),     span("dy", dy, nx)};
+    const Span outs[7] = {span("dx", dx, nx),     span("dw_l", dw_l, nw), span("dw_m", dw_m, nw),
+                          span("dw_r", dw_r, nw), span("dlam", dlam, nl), span("du", du, nl),
+                          span("workspace", workspace, need)};
+    if ((st = check_aliasing(outs, 7, ins, 8))) return st;
+    const bool mean = (flags & GSPN_FLAG_MERGE_MEAN) != 0;
+    cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+    int launches = 0;
+    bool handled = false;
+    cudaError_t e = cudaSuccess;
+    const char* path = "stream-fused-merged";
+    if (!(flags & GSPN_FLAG_FORCE_GENERIC) && H <= gspn::generic_max_P() && W <= gspn::generic_max_P()) {
+      gspn::ScanParams p;
+      memset(&p, 0, sizeof p);
+      p.x = x; p.wl = w_l; p.wm = w_m; p.wr = w_r; p.lam = lam; p.h = h; p.dh = u;
+      p.dx = dx; p.dwl = dw_l; p.dwm = dw_m; p.dwr = dw_r; p.dlam = dlam;
+      p.dy = dy; p.du = du; p.merge_scale = mean ? 1.f / static_cast<float>(D) : 1.f;
+      p.B = B; p.C = C; p.H = H; p.W = W; p.G = groups; p.D = D; p.flags = sflags;
+      fill_dirs(p, dirs);
+      p.ws = workspace;
+      p.ws_bytes = need_bwd;
+      const char* spath = nullptr;
+      e = gspn::launch_bwd_stream(p, dtype, cs, &launches, &handled, &spath);
+    }
+    if (e == cudaSuccess && !handled) {
+      // unfused: dh = s u dy (and du) by the merge adjoint into the workspace, then the plain backward
+      path = "merged-unfused";
+      void* dh = static_cast<char*>(workspace) + align_up(need_bwd);
+      e = gspn::launch_merge_bwd(h, u, dy, dh, du, B * C * H * W, static_cast<int>(D), mean, dtype, cs);
+      if (e == cudaSuccess) {
+        const gspn_status_t sb = gspn_bwd(x, w_l, w_m, w_r, lam, h, dh, dx, dw_l, dw_m, dw_r, dlam, B, C, H, W, dirs,
+                                          groups, dtype, sflags, workspace, need_bwd, stream);
+        if (sb != GSPN_OK) return sb;
+        launches = 1 + t_launches;
+      }
+    }
+    if (e != cudaSuccess) {
+      snprintf(t_detail, sizeof t_detail, "CUDA error: %s", cudaGetErrorString(e));
+      return GSPN_ERR_CUDA;
+    }
+    t_path = path;
+    t_launches = launches;
+    return GSPN_OK;
+  });
+}
+
 gspn_status_t gspn_merge_fwd(const void* h, const void* u, void* y, int64_t B, int64_t C, int64_t H, int64_t W,
                              uint32_t dirs, gspn_dtype_t dtype, uint32_t flags, gspn_stream_t stream) {
   return guarded([&]() -> gspn_status_t {
@@ -410,23 +492,29 @@ gspn_status_t gspn_proxy_mix(const void* in, const void* M, void* out, int64_t B
   return guarded([&]() -> gspn_status_t {
     gspn_status_t st;
     if ((st = check_ptr(in, "in")) || (st = check_ptr(M, "M")) || (st = check_ptr(out, "out"))) return st;
-    if (flags & ~GSPN_FLAG_PROXY_TRANSPOSE) return fail(GSPN_ERR_INVALID_ARG, "%s has unknown bits (0x%llx)", "flags", flags);
+    if (flags & ~(GSPN_FLAG_PROXY_TRANSPOSE | GSPN_FLAG_PROXY_SIMT))
+      return fail(GSPN_ERR_INVALID_ARG, "%s has unknown bits (0x%llx)", "flags", flags);
     if ((st = check_dims(B, Ci, H, W, 1, 1, dtype, 0))) return st;
     if (Co < 1) return fail(GSPN_ERR_INVALID_ARG, "%s must be >= 1 (got %lld)", "Co", Co);
     if ((H * W) % 2 != 0) return fail(GSPN_ERR_UNSUPPORTED, "%s: H*W must be even (got %lld)", "shape", H * W);
     if ((st = check_proxy_extent(B, Ci, Co, H, W))) return st;
-    if (Ci * Co > 49152) return fail(GSPN_ERR_UNSUPPORTED, "%s: Co*Ci above 49152 (%lld)", "M", Ci * Co);
+    // tcgen05 (TMEM accumulator, TMA-streamed activations) for bf16 shapes it tiles; SIMT otherwise
+    const bool umma = !(flags & GSPN_FLAG_PROXY_SIMT) && gspn::umma_mix_eligible(B, Ci, Co, H * W, dtype);
+    if (!umma && Ci * Co > 49152) return fail(GSPN_ERR_UNSUPPORTED, "%s: Co*Ci above 49152 (%lld)", "M", Ci * Co);
     const size_t s = dtype == GSPN_BF16 ? 2 : 4;
     const Span ins[2] = {span("in", in, (size_t)(B * Ci * H * W) * s), span("M", M, (size_t)(Ci * Co) * s)};
     const Span outs[1] = {span("out", out, (size_t)(B * Co * H * W) * s)};
     if ((st = check_aliasing(outs, 1, ins, 2))) return st;
-    const cudaError_t e = gspn::launch_proxy_mix(in, M, out, B, Ci, Co, H * W, flags & GSPN_FLAG_PROXY_TRANSPOSE, dtype,
-                                                 reinterpret_cast<cudaStream_t>(stream));
+    const cudaError_t e =
+        umma ? gspn::launch_umma_mix(in, M, out, B, Ci, Co, H * W, flags & GSPN_FLAG_PROXY_TRANSPOSE,
+                                     reinterpret_cast<cudaStream_t>(stream))
+             : gspn::launch_proxy_mix(in, M, out, B, Ci, Co, H * W, flags & GSPN_FLAG_PROXY_TRANSPOSE, dtype,
+                                      reinterpret_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) {
       snprintf(t_detail, sizeof t_detail, "CUDA error: %s", cudaGetErrorString(e));
       return GSPN_ERR_CUDA;
     }
-    t_path = "proxy";
+    t_path = umma ? "proxy-umma" : "proxy";
     t_launches = 1;
     return GSPN_OK;
   });
@@ -440,19 +528,26 @@ gspn_status_t gspn_proxy_wgrad(const void* dout, const void* in, float* dM, int6
     if ((st = check_dims(B, Ci, H, W, 1, 1, dtype, 0))) return st;
     if (Co < 1) return fail(GSPN_ERR_INVALID_ARG, "%s must be >= 1 (got %lld)", "Co", Co);
     if ((st = check_proxy_extent(B, Ci, Co, H, W))) return st;
-    if ((Co + Ci) * 33 + Co * Ci > 49152)
+    const bool umma = gspn::umma_wgrad_eligible(B, Ci, Co, H * W, dtype);
+    if (!umma && (Co + Ci) * 33 + Co * Ci > 49152)
       return fail(GSPN_ERR_UNSUPPORTED, "%s: (Co+Ci)*33 + Co*Ci above 49152 (Co*Ci = %lld)", "shape", Ci * Co);
     const size_t s = dtype == GSPN_BF16 ? 2 : 4;
     const Span ins[2] = {span("dout", dout, (size_t)(B * Co * H * W) * s), span("in", in, (size_t)(B * Ci * H * W) * s)};
     const Span outs[1] = {span("dM", dM, (size_t)(Ci * Co) * sizeof(float))};
     if ((st = check_aliasing(outs, 1, ins, 2))) return st;
-    const cudaError_t e = gspn::launch_proxy_wgrad(dout, in, dM, B, Ci, Co, H * W, dtype,
-                                                   reinterpret_cast<cudaStream_t>(stream));
+    const cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+    cudaError_t e;
+    if (umma) {  // tcgen05: per-CTA partial sums in TMEM, added into the zeroed fp32 dM
+      e = cudaMemsetAsync(dM, 0, (size_t)(Ci * Co) * sizeof(float), cs);
+      if (e == cudaSuccess) e = gspn::launch_umma_wgrad(dout, in, dM, B, Ci, Co, H * W, cs);
+    } else {
+      e = gspn::launch_proxy_wgrad(dout, in, dM, B, Ci, Co, H * W, dtype, cs);
+    }
     if (e != cudaSuccess) {
       snprintf(t_detail, sizeof t_detail, "CUDA error: %s", cudaGetErrorString(e));
       return GSPN_ERR_CUDA;
     }
-    t_path = "proxy";
+    t_path = umma ? "proxy-umma" : "proxy";
     t_launches = 1;
     return GSPN_OK;
   });

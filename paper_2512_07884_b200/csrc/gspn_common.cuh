@@ -33,6 +33,11 @@ struct ScanParams {
   size_t ws_bytes;
   int64_t B, C, H, W, G, D;
   int64_t kchunk;          // GSPN-local segment length along the scan axis (0: global scan)
+  // merged backward (gspn_bwd_merged, NEXT-1): `dh` points at the gate u, the upstream gradient is
+  // dh_d = merge_scale u_d dy, and du_d = merge_scale h_d dy is written to `du`
+  const void* dy;          // [B,C,H,W]
+  void* du;                // [D,B,C,H,W]
+  float merge_scale;       // 1 (Sum) or 1/D (Mean)
   uint32_t dirbit[4];      // direction bit (GSPN_DIR_*) of slab k
   uint32_t flags;
 };

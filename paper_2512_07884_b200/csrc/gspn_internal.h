@@ -42,6 +42,14 @@ cudaError_t launch_merge_fwd(const void* h, const void* u, void* y, int64_t N, i
 cudaError_t launch_merge_bwd(const void* h, const void* u, const void* dy, void* dh, void* du, int64_t N, int D,
                              bool mean, gspn_dtype_t dt, cudaStream_t st);
 
+// Proxy projections on tcgen05 (gspn_umma.cu): bf16, Co <= 512, H W % 8 == 0.
+bool umma_mix_eligible(int64_t B, int64_t Ci, int64_t Co, int64_t HW, gspn_dtype_t dt);
+cudaError_t launch_umma_mix(const void* in, const void* M, void* out, int64_t B, int64_t Ci, int64_t Co, int64_t HW,
+                            bool trans, cudaStream_t s);
+bool umma_wgrad_eligible(int64_t B, int64_t Ci, int64_t Co, int64_t HW, gspn_dtype_t dt);
+cudaError_t launch_umma_wgrad(const void* dout, const void* in, float* dM, int64_t B, int64_t Ci, int64_t Co,
+                              int64_t HW, cudaStream_t s);
+
 // Proxy projections (gspn_proxy.cu).
 size_t proxy_mix_smem(int64_t Ci, int64_t Co);
 size_t proxy_wgrad_smem(int64_t Ci, int64_t Co);

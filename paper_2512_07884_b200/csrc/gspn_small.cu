@@ -471,30 +471,38 @@ __global__ void __launch_bounds__(kGrpWarpsB * 32, 1) bwd_grp_small_kernel(ScanP
     }
     named_barrier(bar_id, bar_n);  // x staged; the previous channel's dx has read every Pk
     float ea = 0.f, eb = 0.f, ec = 0.f;  // (a g, b g, c g) of step t+1 at this position
-    int off = off_r + (L - 1) * ts;
-    int q = (L - 1) * P + r;  // scan-order index of (t, r)
-    const float4* tq = TP + k * HW + q;
+    // one pointer per array, stepped by -ts (pixels) / -P (scan order): no per-access address arithmetic
+    const int off0 = off_r + (L - 1) * ts, q0 = (L - 1) * P + r;
+    T* dhp = DH + off0;
+    const T* xp = X + off0;
+    const T* lp = Lm + off0;
+    const T* hp = Hs + off0 - ts;  // h_{t-1} at (t-1, r)
+    float* pkp = Pk + off0;
+    float* sap = SA + q0;
+    float* sbp = SB + q0;
+    float* scp = SC + q0;
+    const float4* tq = TP + k * HW + q0;
 #pragma unroll 2
     for (int t = L - 1; t >= 0; --t) {
       const float from_r = __shfl_down_sync(0xffffffffu, ea, 1);  // a_{t+1}[r+1] g_{t+1}[r+1]
       const float from_l = __shfl_up_sync(0xffffffffu, ec, 1);    // c_{t+1}[r-1] g_{t+1}[r-1]
-      const float gsum = to_f(DH[off]) + eb + ((hr ? from_r : 0.f) + (hl ? from_l : 0.f));
+      const float gsum = to_f(*dhp) + eb + ((hr ? from_r : 0.f) + (hl ? from_l : 0.f));
       const float gt = in ? gsum : 0.f;
       const float4 tp = *tq;
-      const float dlam = gt * to_f(X[off]);
-      const float pk = gt * to_f(Lm[off]);
       const bool seg = seg_start_step(dir, t, L, kc);  // warp-uniform; t = 0 always: h_{-1} = 0
       const float gh = seg ? 0.f : gt;
-      const int prev = seg ? off : off - ts;  // any in-plane pixel when h_{t-1} is not used
-      const float sb_ = fmaf(gh, to_f(Hs[prev]), SB[q]);
-      const float sa_ = fmaf(hl ? gh : 0.f, to_f(Hs[prev + dl]), SA[q]);
-      const float sc_ = fmaf(hr ? gh : 0.f, to_f(Hs[prev + dr]), SC[q]);
+      const T* hq = seg ? dhp : hp;  // any in-plane pixel when h_{t-1} is not used (t = 0: hp is off-plane)
+      const float sb_ = fmaf(gh, to_f(hq[0]), *sbp);
+      const float sa_ = fmaf(hl ? gh : 0.f, to_f(hq[dl]), *sap);
+      const float sc_ = fmaf(hr ? gh : 0.f, to_f(hq[dr]), *scp);
+      const float dlam = gt * to_f(*xp);
+      const float pk = gt * to_f(*lp);
       if (in) {
-        DH[off] = from_f<T>(dlam);  // dlam over dh (read above)
-        Pk[off] = pk;               // g_k lam_k, summed over k into dx below
-        SA[q] = sa_;
-        SB[q] = sb_;
-        SC[q] = sc_;
+        *dhp = from_f<T>(dlam);  // dlam over dh (read above)
+        *pkp = pk;               // g_k lam_k, summed over k into dx below
+        *sap = sa_;
+        *sbp = sb_;
+        *scp = sc_;
       }
       ea = tp.x * gt;
       eb = tp.y * gt;
@@ -502,9 +510,8 @@ __global__ void __launch_bounds__(kGrpWarpsB * 32, 1) bwd_grp_small_kernel(ScanP
       if constexpr (kLocal) {
         if (seg) ea = eb = ec = 0.f;  // h_t did not depend on h_{t-1}
       }
-      off -= ts;
-      q -= P;
-      tq -= P;
+      dhp -= ts; xp -= ts; lp -= ts; hp -= ts; pkp -= ts;
+      sap -= P; sbp -= P; scp -= P; tq -= P;
     }
     __syncwarp();
     warp_plane_out(static_cast<T*>(p.dlam) + chain * HW, DH, HW, lane);

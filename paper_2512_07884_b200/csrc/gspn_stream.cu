@@ -250,6 +250,9 @@ enum BwdIn { B_DH = 0, B_WL, B_WM, B_WR, B_NIN };
 // one row). Horizontal: B_H0 = h on the tile's own (K-aligned) columns, B_H1 = the neighbouring aligned
 // tile on the side of step t-1 (its edge column is h_{t-1} of the tile's first step).
 enum BwdFusedIn { B_H0 = B_NIN, B_H1, B_NINF };
+// Merged backward (NEXT-1, hybrid path only): the B_DH slot holds the gate u, B_DY (= B_H1, unused by the
+// hybrid) the upstream gradient dy of the direction merge; dh = s u dy is formed on the fly.
+constexpr int B_DY = B_H1;
 
 template <bool kBwd>
 __device__ __forceinline__ int64_t plane_of(const Chain& ch, int slot) {
@@ -944,11 +947,11 @@ __device__ __forceinline__ void bwd_half_vert(const Lanes<T>& ln, const uint8_t*
   }
 }
 
-template <typename T, int kPre, bool kRev, bool kLocal>
+template <typename T, int kPre, bool kRev, bool kLocal, bool kMerged = false>
 __device__ __forceinline__ void bwd_half_horiz(const Lanes<T>& ln, const uint8_t* st, int cm, int lane, BwdState& S,
-                                               uint4 (&OG)[kE], uint32_t rm) {
+                                               uint4 (&OG)[kE], uint32_t rm, float ms = 1.f) {
   constexpr int KS = Cfg<T>::KS;
-  uint4 DH[kE], WL[kE], WM[kE], WR[kE];
+  uint4 DH[kE], WL[kE], WM[kE], WR[kE], DY[kE];
 #pragma unroll
   for (int q = 0; q < kE; ++q) {
     const uint32_t off = ln.hoff[q] ^ (static_cast<uint32_t>(cm) << 4);
@@ -956,6 +959,7 @@ __device__ __forceinline__ void bwd_half_horiz(const Lanes<T>& ln, const uint8_t
     WL[q] = *reinterpret_cast<const uint4*>(st + B_WL * kTile + off);
     WM[q] = *reinterpret_cast<const uint4*>(st + B_WM * kTile + off);
     WR[q] = *reinterpret_cast<const uint4*>(st + B_WR * kTile + off);
+    if constexpr (kMerged) DY[q] = *reinterpret_cast<const uint4*>(st + B_DY * kTile + off);
   }
   float G_[kE][KS];
 #pragma unroll
@@ -966,7 +970,8 @@ __device__ __forceinline__ void bwd_half_horiz(const Lanes<T>& ln, const uint8_t
     slot_lo(S.ec, lane, nl);
 #pragma unroll
     for (int q = 0; q < kE; ++q)
-      G_[q][i] = bwd_math<kPre>(hget<T>(DH[q], i), hget_tap<T>(WL[q], i, ln.s[0][q]),
+      G_[q][i] = bwd_math<kPre>(kMerged ? ms * hget<T>(DH[q], i) * hget<T>(DY[q], i) : hget<T>(DH[q], i),
+                                hget_tap<T>(WL[q], i, ln.s[0][q]),
                                 hget_tap<T>(WM[q], i, ln.s[1][q]), hget_tap<T>(WR[q], i, ln.s[2][q]), nr[q], nl[q],
                                 S.ea[q], S.eb[q], S.ec[q]);
     if constexpr (kLocal) {
@@ -1128,16 +1133,23 @@ __device__ __forceinline__ void dw_math(float g, float l, float m, float r, floa
   }
 }
 
-template <typename T, int kPre, bool kLocal>
+template <typename T, int kPre, bool kLocal, bool kMerged = false>
 __device__ __forceinline__ void bwd_half_vert_fused(const Lanes<T>& ln, const uint8_t* p0, int stepb, int64_t gofs,
                                                     int64_t gstep, int t0, int L, BwdState& S, uint64_t pol, T* gbase,
-                                                    T* dwl, T* dwm, T* dwr, bool hl0, bool hr1, uint32_t rm) {
+                                                    T* dwl, T* dwm, T* dwr, bool hl0, bool hr1, uint32_t rm,
+                                                    float ms = 1.f) {
   constexpr int KS = Cfg<T>::KS;
 #pragma unroll
   for (int i = 0; i < KS; ++i) {
     const uint8_t* q = p0 + i * stepb;
     float dh[2], l[2], m[2], r[2], hp[2];
     vload<T>(q + B_DH * kTile, dh);
+    if constexpr (kMerged) {  // dh = s u dy (u in the dh slot)
+      float dy[2];
+      vload<T>(q + B_DY * kTile, dy);
+      dh[0] *= ms * dy[0];
+      dh[1] *= ms * dy[1];
+    }
     vload_tap<T>(q + B_WL * kTile, ln.s[0], l);
     vload_tap<T>(q + B_WM * kTile, ln.s[1], m);
     vload_tap<T>(q + B_WR * kTile, ln.s[2], r);
@@ -1219,7 +1231,7 @@ __device__ __forceinline__ void dw_half_horiz(const Lanes<T>& ln, uint8_t* st, i
   }
 }
 
-template <typename T, int kPre>
+template <typename T, int kPre, bool kMerged = false>
 __device__ void producer_fused(const StreamArgs& A, uint8_t* ring, uint64_t* full, uint64_t* empty) {
   const Plan& pl = A.plan;
   const uint64_t pol_vin = policy_of(pl.pol[1]);
@@ -1266,6 +1278,21 @@ __device__ void producer_fused(const StreamArgs& A, uint8_t* ring, uint64_t* ful
           tma_load3(st + B_H1 * pl.tile_bytes + q * pl.bh * 32, &A.in[1][B_H0], sn, q * pl.bh, chain, fb, pol);
         }
       }
+      if constexpr (kMerged) {  // dy of the plane (shared by the directions: plane index b C + c)
+        const int plane = static_cast<int>(ch.bc);
+        const uint32_t dst = st + B_DY * pl.tile_bytes;
+        const uint64_t pold = policy_of(pl.pol[0]);
+        if (pl.npack > 1) {
+          if (ch.vert) tma_load3(dst, &A.in[0][B_DY], 0, plane, s0, fb, pold);
+          else tma_load3(dst, &A.in[1][B_DY], s0, 0, plane, fb, pold);
+        } else if (ch.vert) {
+          for (int q = 0; q < pl.nbw; ++q)
+            tma_load3(dst + q * pl.K * pl.bw * pl.es, &A.in[0][B_DY], q * pl.bw, s0, plane, fb, pold);
+        } else {
+          for (int q = 0; q < pl.nbh; ++q)
+            tma_load3(dst + q * pl.bh * 32, &A.in[1][B_DY], s0, q * pl.bh, plane, fb, pold);
+        }
+      }
       if (++stage == pl.nstages) { stage = 0; phase ^= 1; }
     }
   }
@@ -1273,7 +1300,7 @@ __device__ void producer_fused(const StreamArgs& A, uint8_t* ring, uint64_t* ful
 
 // Body of the fused backward recurrence (every role returns from here when its work is done); the
 // barriers of `m` must be initialised. Shared by bwd_fused_kernel and the single-launch bwd_one_kernel.
-template <typename T, int kPre, bool kLocal>
+template <typename T, int kPre, bool kLocal, bool kMerged = false>
 __device__ __forceinline__ void bwd_fused_body(const StreamArgs& A, const Smem& m) {
   using C = Cfg<T>;
   const Plan& pl = A.plan;
@@ -1282,7 +1309,7 @@ __device__ __forceinline__ void bwd_fused_body(const StreamArgs& A, const Smem& 
     if (lane == 0) {
       for (int o = 0; o < 2; ++o)
         for (int t = 0; t < B_H1; ++t) asm volatile("prefetch.tensormap [%0];" ::"l"(&A.in[o][t]) : "memory");
-      producer_fused<T, kPre>(A, m.ring, m.full, m.empty);
+      producer_fused<T, kPre, kMerged>(A, m.ring, m.full, m.empty);
     }
     return;
   }
@@ -1302,6 +1329,7 @@ __device__ __forceinline__ void bwd_fused_body(const StreamArgs& A, const Smem& 
   T* const dwm = static_cast<T*>(A.p.dwm);
   T* const dwr = static_cast<T*>(A.p.dwr);
   const int kchunk = static_cast<int>(A.p.kchunk);
+  const float mscale = A.p.merge_scale;
   int stage = 0, par = 0;
   uint32_t phase = 0;
   for (int64_t w = blockIdx.x; w < pl.nchains; w += gridDim.x) {
@@ -1346,15 +1374,15 @@ __device__ __forceinline__ void bwd_fused_body(const StreamArgs& A, const Smem& 
             const int rowl = ch.rev ? ch.L - 1 - tl : tl;
             const int vs = static_cast<int>(pl.vstep);
             if constexpr (kLocal) rm = reset_bits(rowl, ch.rev ? 1 : -1, !ch.rev, kchunk, C::KS);
-            bwd_half_vert_fused<T, kPre, kLocal>(ln, st + ln.voff + kkl * vs, ch.rev ? vs : -vs,
-                                                 ln.vout + static_cast<int64_t>(rowl) * W, ch.rev ? W : -W, t0, ch.L,
-                                                 S, pol_vout, gbase, dwl, dwm, dwr, hl0, hr1, rm);
+            bwd_half_vert_fused<T, kPre, kLocal, kMerged>(ln, st + ln.voff + kkl * vs, ch.rev ? vs : -vs,
+                                                          ln.vout + static_cast<int64_t>(rowl) * W, ch.rev ? W : -W, t0,
+                                                          ch.L, S, pol_vout, gbase, dwl, dwm, dwr, hl0, hr1, rm, mscale);
           } else {
             if constexpr (kLocal)
               rm = reset_bits(tile_start(ch, j, C::K) + cm * C::KS + (ch.rev ? 0 : C::KS - 1), ch.rev ? 1 : -1,
                               !ch.rev, kchunk, C::KS);
-            if (ch.rev) bwd_half_horiz<T, kPre, true, kLocal>(ln, st, cm, lane, S, OG, rm);
-            else bwd_half_horiz<T, kPre, false, kLocal>(ln, st, cm, lane, S, OG, rm);
+            if (ch.rev) bwd_half_horiz<T, kPre, true, kLocal, kMerged>(ln, st, cm, lane, S, OG, rm, mscale);
+            else bwd_half_horiz<T, kPre, false, kLocal, kMerged>(ln, st, cm, lane, S, OG, rm, mscale);
           }
         }
         edge_publish(m.edge + 0 * kXArr + par * kEdgeW * kXRow, warp, lane, ch.vert, S.ea);
@@ -1843,12 +1871,14 @@ cudaError_t launch_out_pc(const ScanParams& p, const void* g, cudaStream_t s) {
 // ring; 8 consumer warps compute from shared memory and store straight to global memory. Loads in
 // flight no longer cost registers (the register-staged kernel was latency-bound at 2 CTAs/SM).
 struct OutArgs {
-  CUtensorMap x, g, lam, wl, wm, wr, h;
+  CUtensorMap x, g, lam, wl, wm, wr, h, dy;
   ScanParams p;
   int RB, BX, nbx, nstages, nrb;
   uint32_t box_rb, box_h;                            // bytes per TMA box (padded to 128)
   uint32_t tile_rb, tile_h, per_k, stage_bytes, tx;  // bytes
   uint32_t koff[4];                                  // byte offset of direction k's tiles in a stage
+  uint32_t khoff[4];                                 // byte offset of direction k's h halo tile
+  uint32_t dyoff;                                    // merged backward: the dy tile (after x)
   int64_t nunits;
 };
 
@@ -1872,7 +1902,7 @@ __device__ __forceinline__ void sm_ld4v(const uint8_t* p, float (&v)[4]) {
 // Body of the TMA-staged output kernel: warps [0, ncons) consume, warp ncons produces, any other warp
 // returns at once. full[] / empty[] (A.nstages each, at the end of the ring) must be initialised with
 // counts 1 / ncons. Shared by bwd_out_tma_kernel and the second phase of bwd_one_kernel.
-template <typename T, bool kLocal, bool kVertDone>
+template <typename T, bool kLocal, bool kVertDone, bool kMerged = false>
 __device__ __forceinline__ void out_tma_body(const OutArgs& A, uint8_t* ring, uint64_t* full, uint64_t* empty,
                                              int ncons) {
   constexpr int V = 4;
@@ -1895,6 +1925,9 @@ __device__ __forceinline__ void out_tma_body(const OutArgs& A, uint8_t* ring, ui
         const uint32_t st = smem_u32(ring + static_cast<size_t>(stage) * A.stage_bytes);
         const uint32_t box_rb = A.box_rb, box_h = A.box_h;
         for (int bx = 0; bx < A.nbx; ++bx) tma_load3(st + bx * box_rb, &A.x, bx * BX, i0, static_cast<int>(bc), fb, pol);
+        if constexpr (kMerged)
+          for (int bx = 0; bx < A.nbx; ++bx)
+            tma_load3(st + A.dyoff + bx * box_rb, &A.dy, bx * BX, i0, static_cast<int>(bc), fb, pol);
         for (int k = 0; k < D; ++k) {
           const int chain = static_cast<int>((static_cast<int64_t>(k) * p.B + b) * p.C + c);
           const uint32_t base = st + A.koff[k];
@@ -1902,6 +1935,8 @@ __device__ __forceinline__ void out_tma_body(const OutArgs& A, uint8_t* ring, ui
           for (int bx = 0; bx < A.nbx; ++bx) {
             tma_load3(base + 0 * A.tile_rb + bx * box_rb, &A.g, bx * BX, i0, chain, fb, pol);
             tma_load3(base + 1 * A.tile_rb + bx * box_rb, &A.lam, bx * BX, i0, chain, fb, pol);
+            if (kMerged && skip_w)  // du = s h dy needs h at the pixel rows: the halo tile
+              tma_load3(st + A.khoff[k] + bx * A.box_h, &A.h, bx * BX, i0 - 1, chain, fb, policy_of(1));
             if (skip_w) continue;
             tma_load3(base + 2 * A.tile_rb + bx * box_rb, &A.wl, bx * BX, i0, chain, fb, pol);
             tma_load3(base + 3 * A.tile_rb + bx * box_rb, &A.wm, bx * BX, i0, chain, fb, pol);
@@ -1942,13 +1977,14 @@ __device__ __forceinline__ void out_tma_body(const OutArgs& A, uint8_t* ring, ui
       const uint32_t ohl = (j0 - bx * BX) > 0 ? oh - es : (bx - 1) * A.box_h + r * rowb + (BX - 1) * es;  // column j0-1
       const uint32_t ohh = (j0 - bx * BX) + V < BX ? oh + V * es : (bx + 1) * A.box_h + r * rowb;          // column j0+V
       const int64_t off0 = bc * HW + i * W + j0;  // x / dx; direction k adds k * kstride (chain k, b, c)
-      float xv[V], dx[V];
+      float xv[V], dx[V], dyv[V];
       sm_ld4v<T>(st + orb, xv);
+      if constexpr (kMerged) sm_ld4v<T>(st + A.dyoff + orb, dyv);
 #pragma unroll
       for (int q = 0; q < V; ++q) dx[q] = 0.f;
       for (int k = 0; k < D; ++k) {
         const uint8_t* base = st + A.koff[k];
-        const uint8_t* ht = base + 5 * A.tile_rb;
+        const uint8_t* ht = st + A.khoff[k];
         const uint32_t dir = p.dirbit[k];
         const bool vert = dir == GSPN_DIR_T2B || dir == GSPN_DIR_B2T;
         const int64_t off = off0 + k * kstride;
@@ -1961,6 +1997,13 @@ __device__ __forceinline__ void out_tma_body(const OutArgs& A, uint8_t* ring, ui
           dx[q] = fmaf(gv[q], lv[q], dx[q]);
         }
         GVec<T, V>::store(static_cast<T*>(p.dlam) + off, dl);
+        if constexpr (kMerged) {  // du_k = s h_k dy: h at image row i = halo row r + 1
+          float hv[V], du[V];
+          sm_ld4v<T>(ht + oh + rowb, hv);
+#pragma unroll
+          for (int q = 0; q < V; ++q) du[q] = p.merge_scale * hv[q] * dyv[q];
+          GVec<T, V>::store(static_cast<T*>(p.du) + off, du);
+        }
         if (kVertDone && vert) continue;
         if (vert) {
           // h_{t-1}: image row i-1 (T2B) / i+1 (B2T) = halo row r / r+2; neighbours = columns j+-1
@@ -2055,13 +2098,13 @@ __device__ __forceinline__ void mbar_inval(uint32_t bar) {
 }
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 
-template <typename T, int kPre, bool kLocal>
+template <typename T, int kPre, bool kLocal, bool kMerged = false>
 __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_one_kernel(const __grid_constant__ OneArgs A) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const Plan& pl = A.s.plan;
   const Smem m = carve(smem_raw, pl);
   init_barriers<false>(m, pl);
-  bwd_fused_body<T, kPre, kLocal>(A.s, m);
+  bwd_fused_body<T, kPre, kLocal, kMerged>(A.s, m);
   // g (generic stores of the vertical chains, TMA stores of the horizontal ones -- the storer waited for
   // their completion) must be visible to the other CTAs' TMA loads of phase 2
   fence_proxy_async_global();
@@ -2086,7 +2129,7 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_one_kernel(const __
   fence_proxy_async();        // phase-1 generic writes of the ring before phase-2 TMA writes into it
   fence_proxy_async_global();
   __syncthreads();
-  out_tma_body<T, kLocal, true>(O, m.ring, full, empty, pl.nwc);
+  out_tma_body<T, kLocal, true, kMerged>(O, m.ring, full, empty, pl.nwc);
 }
 
 // ---- Grouped weights (G < C): a unit is (b, group, RB rows); the ring streams one channel of the
@@ -2554,7 +2597,7 @@ cudaError_t launch_fwd_stream(const ScanParams& p, gspn_dtype_t dt, cudaStream_t
 // Plan + tensor maps of the TMA-staged output kernel for `ncons` consumer warps within `budget` bytes of
 // shared memory. Returns false if the shape does not fit.
 bool setup_out_tma(const ScanParams& p, const void* g, gspn_dtype_t dt, bool vert_done, int ncons, int budget,
-                   OutArgs& A) {
+                   OutArgs& A, bool merged = false) {
   const bool grouped = p.G != p.C;
   memset(&A, 0, sizeof A);
   A.p = p;
@@ -2583,21 +2626,26 @@ bool setup_out_tma(const ScanParams& p, const void* g, gspn_dtype_t dt, bool ver
   A.tile_h = A.nbx * A.box_h;
   A.per_k = nrb_t * A.tile_rb + A.tile_h;
   A.stage_bytes = A.tile_rb + D * A.per_k;
-  {  // direction k's tiles; a vertical direction of the hybrid backward holds only g and lam
+  {  // x (| dy) | direction k's tiles; a vertical direction of the hybrid backward holds only g and lam (and,
+     // merged, the h halo tile for du)
     uint32_t o = A.tile_rb;
+    A.dyoff = o;
+    if (merged) o += A.tile_rb;
     for (int k = 0; k < D; ++k) {
       A.koff[k] = o;
       const bool vd = vert_done && (p.dirbit[k] == GSPN_DIR_T2B || p.dirbit[k] == GSPN_DIR_B2T);
-      o += vd ? 2 * A.tile_rb : A.per_k;
+      A.khoff[k] = o + (vd ? 2 : nrb_t) * A.tile_rb;
+      o += vd ? 2 * A.tile_rb + (merged ? A.tile_h : 0) : A.per_k;
     }
     A.stage_bytes = o;
   }
   A.tx = static_cast<uint32_t>(A.nbx * (es * A.BX * RB * (1 + nrb_t * D) + es * A.BX * (RB + 2) * D));  // payload
-  if (vert_done) {  // vertical directions load g and lam only
+  if (vert_done) {  // vertical directions load g and lam only (+ the h halo when merged)
     int nv = 0;
     for (int k = 0; k < D; ++k) nv += (p.dirbit[k] == GSPN_DIR_T2B || p.dirbit[k] == GSPN_DIR_B2T) ? 1 : 0;
-    A.tx -= static_cast<uint32_t>(A.nbx * nv * (es * A.BX * RB * (nrb_t - 2) + es * A.BX * (RB + 2)));
+    A.tx -= static_cast<uint32_t>(A.nbx * nv * (es * A.BX * RB * (nrb_t - 2) + (merged ? 0 : es * A.BX * (RB + 2))));
   }
+  if (merged) A.tx += static_cast<uint32_t>(A.nbx * es * A.BX * RB);  // dy
   A.nstages = static_cast<int>(std::min<int64_t>(6, budget / A.stage_bytes));
   A.nrb = static_cast<int>((p.H + RB - 1) / RB);
   A.nunits = (grouped ? p.B * p.G : p.B * p.C) * A.nrb;
@@ -2609,6 +2657,7 @@ bool setup_out_tma(const ScanParams& p, const void* g, gspn_dtype_t dt, bool ver
             encode(&A.wm, p.wm, dt, p.W, p.H, nc, A.BX, RB, false) &&
             encode(&A.wr, p.wr, dt, p.W, p.H, nc, A.BX, RB, false) &&
             encode(&A.h, p.h, dt, p.W, p.H, nc, A.BX, RB + 2, false);
+  if (ok && merged) ok = encode(&A.dy, p.dy, dt, p.W, p.H, p.B * p.C, A.BX, RB, false);
   return ok;
 }
 
@@ -2715,22 +2764,24 @@ bool launch_bwd_fused(const ScanParams& p0, gspn_dtype_t dt, cudaStream_t s, int
   // Horizontal chains' dw in the recurrence measured slower than the split (6.45 vs 3.98 ms bwd on
   // config 4's horizontal directions; profiles/r1_notes.md): by default only vertical chains are fused
   // and the output kernel forms the horizontal chains' dw (GSPN_FUSE_H=1: fuse both, experiments).
-  const bool fuse_h = knob("GSPN_FUSE_H") != nullptr;
-  if (!make_plan(p, dt, fuse_h ? B_NINF : B_NIN + 1, &A.plan)) return false;
+  const bool merged = p.dy != nullptr;  // gspn_bwd_merged: dh = s u dy on the fly, du written (single launch only)
+  const bool fuse_h = !merged && knob("GSPN_FUSE_H") != nullptr;
+  if (merged && (p.kchunk > 0 || knob("GSPN_TWO_LAUNCH"))) return false;
+  if (!make_plan(p, dt, fuse_h ? B_NINF : B_NIN + 1 + (merged ? 1 : 0), &A.plan)) return false;
   Plan& pl = A.plan;
   const bool local = p.kchunk > 0;
   if (pl.cl > 1 || (fuse_h && (pl.npack > 1 || local)) || (knob("GSPN_NOFUSE_PACKED") && pl.npack > 1)) return false;
   pl.fuse_h = fuse_h ? 1 : 0;
   // make_plan counted pl.nin tiles per stage for both orientations: vertical loads B_NIN + 1 (no B_H1),
-  // horizontal B_NIN (dh, w) unless fully fused
-  pl.tx_v = pl.tx_v / pl.nin * (B_NIN + 1);
-  if (!fuse_h) pl.tx_h = pl.tx_h / pl.nin * B_NIN;
+  // horizontal B_NIN (dh, w) unless fully fused; merged: + dy for both
+  pl.tx_v = pl.tx_v / pl.nin * (B_NIN + 1 + (merged ? 1 : 0));
+  if (!fuse_h) pl.tx_h = pl.tx_h / pl.nin * (B_NIN + (merged ? 1 : 0));
   const WsLayout l = ws_layout(p.B, p.C, p.H, p.W, p.D, dt);
   if (p.ws == nullptr || p.ws_bytes < l.total) return false;
   A.g = static_cast<char*>(p.ws) + l.g;
-  const void* ins[B_NINF] = {p.dh, p.wl, p.wm, p.wr, p.h, p.h};
   const int64_t nc = p.D * p.B * p.C;
-  const int64_t in_planes[B_NINF] = {nc, nc, nc, nc, nc, nc};
+  const void* ins[B_NINF] = {p.dh, p.wl, p.wm, p.wr, p.h, merged ? p.dy : p.h};
+  const int64_t in_planes[B_NINF] = {nc, nc, nc, nc, nc, merged ? p.B * p.C : nc};
   void* outs[4] = {A.g, p.dwl, p.dwm, p.dwr};
   if (!fill_maps(&A, ins, pl.nin, outs, in_planes, nc, pl.fuse_h ? 4 : 1, dt)) return false;
   cudaError_t e0 = cudaSuccess;
@@ -2739,10 +2790,19 @@ bool launch_bwd_fused(const ScanParams& p0, gspn_dtype_t dt, cudaStream_t s, int
   if (!pl.fuse_h && !knob("GSPN_TWO_LAUNCH")) {  // single launch: recurrence | grid barrier | outputs
     std::unique_ptr<OneArgs> one(new OneArgs());
     one->s = A;
-    if (setup_out_tma(p, A.g, dt, true, pl.nwc, smem_optin() - 1024 - 256, one->o)) {
+    if (setup_out_tma(p, A.g, dt, true, pl.nwc, smem_optin() - 1024 - 256, one->o, merged)) {
       cudaError_t e;
       using BF = __nv_bfloat16;
-      if (dt == GSPN_BF16) {
+      if (merged) {
+        if (dt == GSPN_BF16)
+          e = mode == kNormPre ? launch_one(bwd_one_kernel<BF, kNormPre, false, true>, *one, s)
+              : mode == kNormClamp ? launch_one(bwd_one_kernel<BF, kNormClamp, false, true>, *one, s)
+                                   : launch_one(bwd_one_kernel<BF, kNormFull, false, true>, *one, s);
+        else
+          e = mode == kNormPre ? launch_one(bwd_one_kernel<float, kNormPre, false, true>, *one, s)
+              : mode == kNormClamp ? launch_one(bwd_one_kernel<float, kNormClamp, false, true>, *one, s)
+                                   : launch_one(bwd_one_kernel<float, kNormFull, false, true>, *one, s);
+      } else if (dt == GSPN_BF16) {
         if (local) e = mode == kNormPre ? launch_one(bwd_one_kernel<BF, kNormPre, true>, *one, s)
                                         : launch_one(bwd_one_kernel<BF, kNormClamp, true>, *one, s);
         else e = mode == kNormPre ? launch_one(bwd_one_kernel<BF, kNormPre, false>, *one, s)
@@ -2760,6 +2820,7 @@ bool launch_bwd_fused(const ScanParams& p0, gspn_dtype_t dt, cudaStream_t s, int
       return true;
     }
   }
+  if (merged) return false;  // the merged variant exists only as the single launch
   cudaError_t e;
   if (dt == GSPN_BF16) {
     using BF = __nv_bfloat16;
@@ -2800,6 +2861,7 @@ cudaError_t launch_bwd_stream(const ScanParams& p0, gspn_dtype_t dt, cudaStream_
     }
   }
   *path = "stream";
+  if (p0.dy != nullptr) return cudaSuccess;  // merged backward: single-launch fused path only (caller falls back)
   std::unique_ptr<StreamArgs> hold(new StreamArgs());
   StreamArgs& A = *hold;
   memset(&A, 0, sizeof A);

@@ -324,7 +324,7 @@ def test_proxy_parity(case):
     Q, Qf = mk((C, Cp), 1.0 / np.sqrt(Cp))
     dy, dyf = mk((B, C, H, W))
     xp = gspn.proxy_mix(x, P)
-    assert gspn.last_path() == "proxy"
+    assert gspn.last_path().startswith("proxy")
     y = gspn.proxy_mix(xp, Q)
     dxp = gspn.proxy_mix(dy, Q, transpose=True)           # d(up)/d(input) = Q^T dy
     dx = gspn.proxy_mix(dxp, P, transpose=True)           # d(down)/d(input) = P^T dxp
@@ -372,3 +372,117 @@ def test_fused_local_prenormalized(shape):
     for name, a, r in zip(("dx", "dw_l", "dw_m", "dw_r", "dlam"), grads, g_ref):
         assert normwise(from_torch(a), r) <= tol, name
     torch.cuda.synchronize()
+
+
+# (B, Ci, Co, H, W): the configs' compact blocks (320 -> 40 -> 320, 384 -> 8 -> 384) and ragged ones: K not a
+# multiple of 64, Co not a multiple of 128 (1, 2 and 4 M tiles), a partial last pixel tile
+UMMA_CASES = [
+    (2, 320, 40, 16, 24),
+    (2, 40, 320, 16, 24),
+    (3, 384, 8, 28, 28),
+    (3, 8, 384, 28, 28),
+    (1, 100, 7, 8, 17 * 8),
+    (3, 64, 130, 8, 8),
+    (1, 24, 500, 4, 16),
+    (2, 200, 256, 12, 12),
+]
+
+
+@pytest.mark.parametrize("trans", [False, True])
+@pytest.mark.parametrize("case", UMMA_CASES, ids=lambda c: "B{}Ci{}Co{}H{}W{}".format(*c))
+def test_proxy_umma_parity(case, trans):
+    """gspn_proxy_mix on tcgen05 (path "proxy-umma") vs the fp64 oracle on the same bf16 inputs, and vs the
+    SIMT kernel (GSPN_FLAG_PROXY_SIMT) on the same call."""
+    import torch
+
+    B, Ci, Co, H, W = case
+    rng = np.random.default_rng(Ci * 1000 + Co)
+    dev = _dev()
+    x = torch.from_numpy(rng.uniform(-1, 1, (B, Ci, H, W))).to(torch.bfloat16)
+    Mw = torch.from_numpy(rng.uniform(-1, 1, (Ci, Co) if trans else (Co, Ci)) / np.sqrt(Ci)).to(torch.bfloat16)
+    y = gspn.proxy_mix(x.to(dev), Mw.to(dev), transpose=trans)
+    assert gspn.last_path() == "proxy-umma"
+    ys = None
+    if Ci * Co <= 49152:  # the SIMT kernel stages M in shared memory
+        ys = gspn.proxy_mix(x.to(dev), Mw.to(dev), transpose=trans, simt=True)
+        assert gspn.last_path() == "proxy"
+    Mf = Mw.double().numpy()
+    ref = oracle.proxy_mix(x.double().numpy(), Mf.T if trans else Mf)
+    check("proxy_umma", "out", from_torch(y), ref, TOL["bf16"], per_slab=False)
+    if ys is not None:
+        check("proxy_umma", "out vs simt", from_torch(y), from_torch(ys), TOL["bf16"], per_slab=False)
+    if not trans:  # weight gradient of this projection: dM = dout in^T over every pixel (tcgen05, K = B H W)
+        dout = torch.from_numpy(rng.uniform(-1, 1, (B, Co, H, W))).to(torch.bfloat16)
+        dM = gspn.proxy_wgrad(dout.to(dev), x.to(dev))
+        assert gspn.last_path() == "proxy-umma"
+        check("proxy_umma", "wgrad", from_torch(dM), oracle.proxy_wgrad(dout.double().numpy(), x.double().numpy()),
+              TOL["bf16"], per_slab=False)
+
+
+def test_proxy_umma_config5_block_sampled():
+    """BASELINE configs[4]'s compact block at full size: 320 -> 40 (down) and 40 -> 320 (up) over 2048^2
+    pixels on tcgen05; 2048 sampled pixels of every output channel recomputed in fp64 on the host."""
+    import torch
+
+    B, C, Cp, H, W = 1, 320, 40, 2048, 2048
+    dev = _dev()
+    g = torch.Generator(device=dev).manual_seed(5)
+    x = (torch.rand((B, C, H, W), generator=g, device=dev) * 2 - 1).to(torch.bfloat16)
+    P = ((torch.rand((Cp, C), generator=g, device=dev) * 2 - 1) / C ** 0.5).to(torch.bfloat16)
+    Q = ((torch.rand((C, Cp), generator=g, device=dev) * 2 - 1) / Cp ** 0.5).to(torch.bfloat16)
+    xp = gspn.proxy_mix(x, P)
+    assert gspn.last_path() == "proxy-umma"
+    y = gspn.proxy_mix(xp, Q)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(5)
+    pix = np.concatenate([rng.integers(0, H * W, 2042), [0, 1, 255, 256, H * W - 2, H * W - 1]])
+    idx = torch.from_numpy(pix).to(dev)
+    xs = x.reshape(C, -1)[:, idx].double().cpu().numpy()            # [C, S]
+    xps = xp.reshape(Cp, -1)[:, idx].double().cpu().numpy()         # GPU xp (stored bf16) at those pixels
+    Pf, Qf = P.double().cpu().numpy(), Q.double().cpu().numpy()
+    check("proxy_umma_cfg5", "down", xps, Pf @ xs, TOL["bf16"], per_slab=False)
+    ys = y.reshape(C, -1)[:, idx].double().cpu().numpy()
+    check("proxy_umma_cfg5", "up", ys, Qf @ xps, TOL["bf16"], per_slab=False)
+
+
+# ------------------------------------------------------------------- NEXT-1 merged backward
+
+# (B, C, G, H, W, dirs, dtype, expected path): the fused single launch (per-channel: unpacked, packed, fp32,
+# single directions) and the unfused fallback (grouped, small planes)
+MERGED_CASES = [
+    (1, 2, 2, 300, 264, 0xF, "bf16", "stream-fused-merged"),
+    (2, 4, 4, 56, 56, 0xF, "bf16", "stream-fused-merged"),
+    (1, 2, 2, 512, 512, 0xF, "bf16", "stream-fused-merged"),
+    (2, 2, 2, 264, 300, 0xF, "f32", "stream-fused-merged"),
+    (1, 3, 3, 272, 288, 0x5, "bf16", "stream-fused-merged"),
+    (1, 2, 2, 300, 264, 0xA, "f32", "stream-fused-merged"),
+    (2, 4, 2, 40, 56, 0xF, "bf16", "merged-unfused"),
+    (2, 8, 1, 28, 28, 0xF, "bf16", "merged-unfused"),
+]
+
+
+@pytest.mark.parametrize("mean", [False, True], ids=["sum", "mean"])
+@pytest.mark.parametrize("case", MERGED_CASES, ids=lambda c: "B{}C{}G{}H{}W{}d{:x}{}".format(*c[:7]))
+def test_bwd_merged_parity(case, mean):
+    """gspn_bwd_merged (dh = s u dy formed in the backward launch, du written) against the oracle chain
+    merge adjoint -> scan adjoint (Eq. 2) on the GPU's own stored h (R18)."""
+    B, C, G, H, W, dirs, dt, want = case
+    cfg = small_config(B, C, G, H, W, dirs, dt, cfg_id=608)
+    inp = host_inputs(cfg)
+    f = {n: v[1] for n, v in inp.items()}
+    uv, uf = host_tensor(cfg, "u", (cfg.D, B, C, H, W))
+    gv, gf = host_tensor(cfg, "dy", (B, C, H, W))
+    dev = _dev()
+    t = {n: to_torch(v[0], dt, dev) for n, v in inp.items()}
+    u, dy = to_torch(uv, dt, dev), to_torch(gv, dt, dev)
+    h = gspn.fwd(t["x"], t["w_l"], t["w_m"], t["w_r"], t["lam"], dirs, G)
+    outs = gspn.bwd_merged(t["x"], t["w_l"], t["w_m"], t["w_r"], t["lam"], h, u, dy, dirs, G, mean=mean)
+    assert gspn.last_path() == want, gspn.last_path()
+    if want == "stream-fused-merged":
+        assert gspn.last_launch_count() == 1
+    hs = from_torch(h)
+    dh_ref, du_ref = oracle.merge_bwd(hs, uf, gf, mean)
+    g_ref = oracle.bwd(f["x"], f["w_l"], f["w_m"], f["w_r"], f["lam"], hs, dh_ref, dirs, G)
+    tol = TOL[dt]
+    for name, a, r in zip(("dx", "dw_l", "dw_m", "dw_r", "dlam", "du"), outs, list(g_ref) + [du_ref]):
+        check("bwd_merged", name, from_torch(a), r, tol)
