@@ -158,6 +158,22 @@ gspn_status_t gspn_merge_bwd(const void* h, const void* u, const void* dy, void*
                              gspn_stream_t stream);
 
 /*
+ * Forward scan AND output gate + direction merge in one call (PAPER.md:84-89
+ * Eq. 2): y = s sum_d u_d (.) h_d [B,C,H,W] with u [D,B,C,H,W] (s = 1, or 1/D with GSPN_FLAG_MERGE_MEAN).
+ * h [D,B,C,H,W] is also written when non-NULL (training keeps it for gspn_bwd_merged); with h = NULL it
+ * lives in the workspace (>= gspn_fwd_merged_workspace_bytes(...) bytes; may be NULL when h is given).
+ * Unpacked / packed chains without P-split: one cooperative launch (scan | grid barrier | merge;
+ * gspn_last_path() "stream-merged"); otherwise gspn_fwd then gspn_merge_fwd ("merged-unfused").
+ * flags: GSPN_FLAG_PRENORMALIZED, GSPN_FLAG_MERGE_MEAN, GSPN_FLAG_FORCE_GENERIC.
+ */
+gspn_status_t gspn_fwd_merged(const void* x, const void* w_l, const void* w_m, const void* w_r, const void* lam,
+                              const void* u, void* h, void* y, int64_t B, int64_t C, int64_t H, int64_t W,
+                              uint32_t dirs, int64_t groups, gspn_dtype_t dtype, uint32_t flags, void* workspace,
+                              size_t workspace_bytes, gspn_stream_t stream);
+size_t gspn_fwd_merged_workspace_bytes(int64_t B, int64_t C, int64_t H, int64_t W, uint32_t dirs, int64_t groups,
+                                       gspn_dtype_t dtype);
+
+/*
  * Backward through the scan AND the output gate + direction merge in one call (SURVEY.md §8(f) NEXT-1,
  * PAPER.md:84-88 Eq. 2): given the merge's upstream gradient dy [B,C,H,W] and the gate u [D,B,C,H,W],
  * the scan's upstream gradient is dh_d = s u_d (.) dy (s = 1, or 1/D with GSPN_FLAG_MERGE_MEAN) and the

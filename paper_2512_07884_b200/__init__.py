@@ -171,6 +171,34 @@ def merge_bwd(h, u, dy, dirs: int = DIR_ALL, mean: bool = False, outs=None, stre
     return dh, du
 
 
+def fwd_merged(x, w_l, w_m, w_r, lam, u, dirs: int = DIR_ALL, groups: int | None = None, mean: bool = False,
+               flags: int = 0, keep_h: bool = True, out=None, h_out=None, workspace=None, stream=None):
+    """Forward scan + output gate + direction merge (gspn_fwd_merged, NEXT-1): returns (y, h), h None when
+    keep_h is False (then h lives in a scratch workspace)."""
+    torch = _torch()
+    G = x.shape[1] if groups is None else int(groups)
+    (B, C, H, W, D), sx, sw, sl = _scan_shapes(x, dirs, G)
+    dt = _dtype_code(x)
+    y = torch.empty_like(x) if out is None else out
+    h = (torch.empty_like(lam) if h_out is None else h_out) if keep_h else None
+    named = [("lam", lam, sl), ("u", u, sl), ("w_l", w_l, sw), ("w_m", w_m, sw), ("w_r", w_r, sw), ("y (out)", y, sx)]
+    if h is not None:
+        named.append(("h (out)", h, sl))
+    _check_shapes(named)
+    _check_tensors([(n, t) for n, t, _ in named] + [("x", x)], x.dtype, x.device)
+    ws_ptr, ws_n = None, 0
+    if h is None:
+        need = int(lib().gspn_fwd_merged_workspace_bytes(B, C, H, W, dirs, G, dt))
+        if workspace is None or workspace.numel() < need:
+            workspace = torch.empty(max(need, 16), dtype=torch.uint8, device=x.device)
+        ws_ptr, ws_n = workspace.data_ptr(), workspace.numel()
+    check(lib().gspn_fwd_merged(x.data_ptr(), w_l.data_ptr(), w_m.data_ptr(), w_r.data_ptr(), lam.data_ptr(),
+                                u.data_ptr(), h.data_ptr() if h is not None else None, y.data_ptr(), B, C, H, W, dirs, G,
+                                dt, flags | (FLAG_MERGE_MEAN if mean else 0), ws_ptr, ws_n,
+                                _stream_ptr(stream, x.device)))
+    return y, h
+
+
 def bwd_merged(x, w_l, w_m, w_r, lam, h, u, dy, dirs: int = DIR_ALL, groups: int | None = None, mean: bool = False,
                flags: int = 0, outs=None, workspace=None, stream=None):
     """Backward through the scan and the output gate + direction merge (gspn_bwd_merged, NEXT-1):

@@ -42,6 +42,11 @@ def lib() -> ctypes.CDLL:
             L.gspn_fwd_local.restype = ctypes.c_int
             L.gspn_bwd_local.argtypes = [vp] * 12 + [i64] * 4 + [u32, i64, i64, ctypes.c_int, u32, vp, sz, vp]
             L.gspn_bwd_local.restype = ctypes.c_int
+        if hasattr(L, "gspn_fwd_merged"):
+            L.gspn_fwd_merged.argtypes = [vp] * 8 + [i64] * 4 + [u32, i64, ctypes.c_int, u32, vp, sz, vp]
+            L.gspn_fwd_merged.restype = ctypes.c_int
+            L.gspn_fwd_merged_workspace_bytes.argtypes = [i64] * 4 + [u32, i64, ctypes.c_int]
+            L.gspn_fwd_merged_workspace_bytes.restype = sz
         if hasattr(L, "gspn_bwd_merged"):
             L.gspn_bwd_merged.argtypes = [vp] * 14 + [i64] * 4 + [u32, i64, ctypes.c_int, u32, vp, sz, vp]
             L.gspn_bwd_merged.restype = ctypes.c_int

@@ -352,6 +352,78 @@ static gspn_status_t check_proxy_extent(int64_t B, int64_t Ci, int64_t Co, int64
 
 extern "C" {
 
+size_t gspn_fwd_merged_workspace_bytes(int64_t B, int64_t C, int64_t H, int64_t W, uint32_t dirs, int64_t groups,
+                                       gspn_dtype_t dtype) {
+  if (check_dims(B, C, H, W, dirs, groups, dtype, 0) != GSPN_OK) return 0;
+  const size_t s = dtype == GSPN_BF16 ? 2 : 4;
+  return align_up((size_t)popcount4(dirs) * (size_t)(B * C * H * W) * s);  // h, when the caller keeps none
+}
+
+gspn_status_t gspn_fwd_merged(const void* x, const void* w_l, const void* w_m, const void* w_r, const void* lam,
+                              const void* u, void* h, void* y, int64_t B, int64_t C, int64_t H, int64_t W,
+                              uint32_t dirs, int64_t groups, gspn_dtype_t dtype, uint32_t flags, void* workspace,
+                              size_t workspace_bytes, gspn_stream_t stream) {
+  return guarded([&]() -> gspn_status_t {
+    gspn_status_t st;
+    if ((st = check_ptr(x, "x")) || (st = check_ptr(w_l, "w_l")) || (st = check_ptr(w_m, "w_m")) ||
+        (st = check_ptr(w_r, "w_r")) || (st = check_ptr(lam, "lam")) || (st = check_ptr(u, "u")) ||
+        (st = check_ptr(y, "y")))
+      return st;
+    if (flags & ~(GSPN_FLAG_PRENORMALIZED | GSPN_FLAG_MERGE_MEAN | GSPN_FLAG_FORCE_GENERIC))
+      return fail(GSPN_ERR_INVALID_ARG, "%s has unknown bits (0x%llx)", "flags", flags);
+    const uint32_t sflags = flags & ~GSPN_FLAG_MERGE_MEAN;
+    if ((st = check_dims(B, C, H, W, dirs, groups, dtype, sflags))) return st;
+    const int64_t D = popcount4(dirs);
+    const size_t s = dtype == GSPN_BF16 ? 2 : 4;
+    const size_t nx = (size_t)(B * C * H * W) * s, nl = (size_t)D * nx, nw = (size_t)(D * B * groups * H * W) * s;
+    void* hh = h;
+    if (hh == nullptr) {  // h lives in the workspace
+      if ((st = check_ptr(workspace, "workspace"))) return st;
+      if (workspace_bytes < nl) {
+        snprintf(t_detail, sizeof t_detail, "workspace too small: %zu < %zu bytes", workspace_bytes, nl);
+        return GSPN_ERR_INVALID_ARG;
+      }
+      hh = workspace;
+    } else if ((st = check_ptr(h, "h"))) {
+      return st;
+    }
+    const Span ins[6] = {span("x", x, nx),     span("w_l", w_l, nw), span("w_m", w_m, nw),
+                         span("w_r", w_r, nw), span("lam", lam, nl), span("u", u, nl)};
+    const Span outs[2] = {span(h ? "h" : "workspace", hh, nl), span("y", y, nx)};
+    if ((st = check_aliasing(outs, 2, ins, 6))) return st;
+    if (H > gspn::generic_max_P() || W > gspn::generic_max_P())
+      return fail(GSPN_ERR_UNSUPPORTED, "%s above the tiled maximum (%lld)", "H or W", (long long)gspn::generic_max_P());
+    const bool mean = (flags & GSPN_FLAG_MERGE_MEAN) != 0;
+    cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+    int launches = 0;
+    bool handled = false;
+    cudaError_t e = cudaSuccess;
+    const char* path = "stream-merged";
+    if (!(flags & GSPN_FLAG_FORCE_GENERIC)) {
+      gspn::ScanParams p;
+      memset(&p, 0, sizeof p);
+      p.x = x; p.wl = w_l; p.wm = w_m; p.wr = w_r; p.lam = lam; p.hout = hh;
+      p.B = B; p.C = C; p.H = H; p.W = W; p.G = groups; p.D = D; p.flags = sflags;
+      fill_dirs(p, dirs);
+      e = gspn::launch_fwd_merged(p, dtype, u, y, mean ? 1.f / static_cast<float>(D) : 1.f, cs, &launches, &handled);
+    }
+    if (e == cudaSuccess && !handled) {  // the scan, then the merge
+      path = "merged-unfused";
+      const gspn_status_t sf = gspn_fwd(x, w_l, w_m, w_r, lam, hh, B, C, H, W, dirs, groups, dtype, sflags, stream);
+      if (sf != GSPN_OK) return sf;
+      launches = t_launches + 1;
+      e = gspn::launch_merge_fwd(hh, u, y, B * C * H * W, static_cast<int>(D), mean, dtype, cs);
+    }
+    if (e != cudaSuccess) {
+      snprintf(t_detail, sizeof t_detail, "CUDA error: %s", cudaGetErrorString(e));
+      return GSPN_ERR_CUDA;
+    }
+    t_path = path;
+    t_launches = launches;
+    return GSPN_OK;
+  });
+}
+
 size_t gspn_bwd_merged_workspace_bytes(int64_t B, int64_t C, int64_t H, int64_t W, uint32_t dirs, int64_t groups,
                                        gspn_dtype_t dtype) {
   const size_t a = gspn_bwd_workspace_bytes(B, C, H, W, dirs, groups, dtype);

@@ -34,6 +34,9 @@ cudaError_t launch_fwd_stream(const ScanParams& p, gspn_dtype_t dt, cudaStream_t
 // Backward: *path = "stream-fused" (recurrence + tap gradients in one pass, G = C) or "stream" (split; "stream-cluster" when P-split).
 cudaError_t launch_bwd_stream(const ScanParams& p, gspn_dtype_t dt, cudaStream_t s, int* launches, bool* handled,
                               const char** path);
+// Forward + output gate + direction merge in one cooperative launch (NEXT-1); *handled = false: fall back.
+cudaError_t launch_fwd_merged(const ScanParams& p, gspn_dtype_t dt, const void* u, void* y, float scale,
+                              cudaStream_t s, int* launches, bool* handled);
 size_t stream_bwd_workspace_bytes(int64_t B, int64_t C, int64_t H, int64_t W, int64_t D, int64_t G, gspn_dtype_t dt);
 
 // Output gate + direction merge (gspn_merge.cu). N = B*C*H*W elements per direction slab.

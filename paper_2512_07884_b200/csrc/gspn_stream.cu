@@ -796,14 +796,13 @@ __device__ __forceinline__ void fwd_half_horiz(const Lanes<T>& ln, const uint8_t
   for (int q = 0; q < kE; ++q) OUT[q] = Pk<T>::pack(O[q]);
 }
 
+// Body of the forward scan (every role returns from here when its work is done); the barriers of `m` must
+// be initialised. Shared by fwd_stream_kernel and the merged single launch fwd_one_kernel.
 template <typename T, int kPre, bool kCl, bool kLocal>
-__global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) fwd_stream_kernel(const __grid_constant__ StreamArgs A) {
+__device__ __forceinline__ void fwd_stream_body(const StreamArgs& A, const Smem& m) {
   using C = Cfg<T>;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
   const Plan& pl = A.plan;
-  const Smem m = carve(smem_raw, pl);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  init_barriers<kCl>(m, pl);
   if (warp == pl.nwc) {  // producer warp
     if (lane == 0) {
       for (int o = 0; o < 2; ++o)
@@ -899,6 +898,14 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) fwd_stream_kernel(const
     }
   }
   cluster_exit<kCl>();
+}
+
+template <typename T, int kPre, bool kCl, bool kLocal>
+__global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) fwd_stream_kernel(const __grid_constant__ StreamArgs A) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const Smem m = carve(smem_raw, A.plan);
+  init_barriers<kCl>(m, A.plan);
+  fwd_stream_body<T, kPre, kCl, kLocal>(A, m);
 }
 
 // ------------------------------------------------------------------------------ backward recurrence
@@ -2132,6 +2139,56 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_one_kernel(const __
   out_tma_body<T, kLocal, true, kMerged>(O, m.ring, full, empty, pl.nwc);
 }
 
+// ---- Forward through the output gate + direction merge in one launch (NEXT-1, Eq. 2):
+// phase 1 is the forward scan (h to the caller's buffer or the workspace), then a grid-wide barrier, then
+// phase 2 forms y = s sum_d u_d (.) h_d over [B, C, H, W] on the same CTAs (16-byte vectors, grid-stride).
+struct OneFwdArgs {
+  StreamArgs s;
+  const void* u;
+  void* y;
+  float scale;
+  int64_t N;  // B C H W (a multiple of the vector width)
+};
+
+template <typename T, int kPre, bool kLocal>
+__global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) fwd_one_kernel(const __grid_constant__ OneFwdArgs A) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const Smem m = carve(smem_raw, A.s.plan);
+  init_barriers<false>(m, A.s.plan);
+  fwd_stream_body<T, kPre, false, kLocal>(A.s, m);
+  fence_proxy_async_global();  // h: generic stores (vertical) and completed TMA stores (horizontal)
+  __syncthreads();
+  cooperative_groups::this_grid().sync();
+  constexpr int V = 16 / static_cast<int>(sizeof(T));
+  const int D = static_cast<int>(A.s.p.D);
+  const T* h = static_cast<const T*>(A.s.p.hout);
+  const T* u = static_cast<const T*>(A.u);
+  T* y = static_cast<T*>(A.y);
+  const int64_t nv = A.N / V;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nv;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    uint4 hq[4], uq[4];
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      if (d >= D) break;
+      hq[d] = __ldcg(reinterpret_cast<const uint4*>(h + d * A.N + i * V));  // written by this launch: not .nc
+      uq[d] = ld_nc_v4(u + d * A.N + i * V);
+    }
+    float acc[V];
+#pragma unroll
+    for (int e = 0; e < V; ++e) acc[e] = 0.f;
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      if (d >= D) break;
+#pragma unroll
+      for (int e = 0; e < V; ++e) acc[e] = fmaf(hget<T>(uq[d], e), hget<T>(hq[d], e), acc[e]);
+    }
+#pragma unroll
+    for (int e = 0; e < V; ++e) acc[e] *= A.scale;
+    st_cs_v4(y + i * V, Pk<T>::pack(acc));
+  }
+}
+
 // ---- Grouped weights (G < C): a unit is (b, group, RB rows); the ring streams one channel of the
 // group per stage (x, and per direction g, lam and the h halo tile), every thread keeps the group sums
 // Da/Db/Dc of its 4-column chunk for all directions in registers, and after the group's last channel
@@ -2662,6 +2719,68 @@ bool setup_out_tma(const ScanParams& p, const void* g, gspn_dtype_t dt, bool ver
 }
 
 uint32_t out_tma_smem(const OutArgs& A) { return 1024 + A.nstages * A.stage_bytes + 2 * 8 * A.nstages; }
+
+// Forward + merge in one cooperative launch (gspn_fwd_merged). *handled = false when the shape takes
+// another path (P-split chains, or B C H W not a multiple of the vector width): the caller falls back.
+cudaError_t launch_fwd_merged(const ScanParams& p, gspn_dtype_t dt, const void* u, void* y, float scale,
+                              cudaStream_t s, int* launches, bool* handled) {
+  *handled = false;
+  const int V = dt == GSPN_BF16 ? 8 : 4;
+  const int64_t N = p.B * p.C * p.H * p.W;
+  if (N % V != 0) return cudaSuccess;
+  std::unique_ptr<OneFwdArgs> hold(new OneFwdArgs());
+  OneFwdArgs& A = *hold;
+  memset(&A, 0, sizeof A);
+  A.s.p = p;
+  if (!make_plan(p, dt, F_NIN, &A.s.plan) || A.s.plan.cl > 1) return cudaSuccess;
+  const void* ins[F_NIN] = {p.x, p.lam, p.wl, p.wm, p.wr};
+  const int64_t in_planes[F_NIN] = {p.B * p.C, p.D * p.B * p.C, p.D * p.B * p.G, p.D * p.B * p.G, p.D * p.B * p.G};
+  void* outs[1] = {p.hout};
+  if (!fill_maps(&A.s, ins, F_NIN, outs, in_planes, p.D * p.B * p.C, 1, dt)) return cudaSuccess;
+  A.u = u;
+  A.y = y;
+  A.scale = scale;
+  A.N = N;
+  *handled = true;
+  const int mode = norm_mode(p, A.s.plan);
+  const bool local = p.kchunk > 0;
+  auto go = [&](auto kernel) -> cudaError_t {
+    const uint32_t smem = A.s.plan.smem_bytes;
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    const int threads = (A.s.plan.nwc + 2) * 32;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    const int64_t grid = static_cast<int64_t>(sm_count()) * per_sm;  // every CTA resident (grid barrier)
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.gridDim = dim3(static_cast<unsigned>(grid), 1, 1);
+    cfg.blockDim = dim3(threads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kernel, A);
+    return e != cudaSuccess ? e : cudaGetLastError();
+  };
+  using BF = __nv_bfloat16;
+  cudaError_t e;
+  if (dt == GSPN_BF16) {
+    if (local) e = mode == kNormPre ? go(fwd_one_kernel<BF, kNormPre, true>) : go(fwd_one_kernel<BF, kNormClamp, true>);
+    else e = mode == kNormPre ? go(fwd_one_kernel<BF, kNormPre, false>)
+             : mode == kNormClamp ? go(fwd_one_kernel<BF, kNormClamp, false>) : go(fwd_one_kernel<BF, kNormFull, false>);
+  } else {
+    if (local) e = mode == kNormPre ? go(fwd_one_kernel<float, kNormPre, true>) : go(fwd_one_kernel<float, kNormClamp, true>);
+    else e = mode == kNormPre ? go(fwd_one_kernel<float, kNormPre, false>)
+             : mode == kNormClamp ? go(fwd_one_kernel<float, kNormClamp, false>) : go(fwd_one_kernel<float, kNormFull, false>);
+  }
+  *launches += 1;
+  return e;
+}
 
 // TMA-staged output kernel. Returns false if the shape does not fit (caller falls back).
 bool launch_out_tma(const ScanParams& p, const void* g, gspn_dtype_t dt, cudaStream_t s, cudaError_t* err,

@@ -486,3 +486,37 @@ def test_bwd_merged_parity(case, mean):
     tol = TOL[dt]
     for name, a, r in zip(("dx", "dw_l", "dw_m", "dw_r", "dlam", "du"), outs, list(g_ref) + [du_ref]):
         check("bwd_merged", name, from_torch(a), r, tol)
+
+
+FWD_MERGED_CASES = [
+    (1, 2, 2, 300, 264, 0xF, "bf16", "stream-merged"),
+    (2, 4, 4, 56, 56, 0xF, "bf16", "stream-merged"),
+    (2, 3, 1, 64, 80, 0xF, "f32", "stream-merged"),
+    (1, 2, 2, 24, 1000, 0xF, "bf16", "merged-unfused"),   # P-split chains: scan then merge
+    (2, 8, 1, 28, 28, 0x9, "bf16", "merged-unfused"),     # small planes
+]
+
+
+@pytest.mark.parametrize("keep_h", [True, False], ids=["h", "noh"])
+@pytest.mark.parametrize("mean", [False, True], ids=["sum", "mean"])
+@pytest.mark.parametrize("case", FWD_MERGED_CASES, ids=lambda c: "B{}C{}G{}H{}W{}d{:x}{}".format(*c[:7]))
+def test_fwd_merged_parity(case, mean, keep_h):
+    """gspn_fwd_merged: y = s sum_d u_d h_d from the scan's own h in the same launch, vs the
+    oracle merge of the oracle forward; h (when kept) vs the oracle forward."""
+    B, C, G, H, W, dirs, dt, want = case
+    cfg = small_config(B, C, G, H, W, dirs, dt, cfg_id=609)
+    inp = host_inputs(cfg)
+    f = {n: v[1] for n, v in inp.items()}
+    uv, uf = host_tensor(cfg, "u", (cfg.D, B, C, H, W))
+    dev = _dev()
+    t = {n: to_torch(v[0], dt, dev) for n, v in inp.items()}
+    u = to_torch(uv, dt, dev)
+    y, h = gspn.fwd_merged(t["x"], t["w_l"], t["w_m"], t["w_r"], t["lam"], u, dirs, G, mean=mean, keep_h=keep_h)
+    assert gspn.last_path() == want, gspn.last_path()
+    if want == "stream-merged":
+        assert gspn.last_launch_count() == 1
+    h_ref = oracle.fwd(f["x"], f["w_l"], f["w_m"], f["w_r"], f["lam"], dirs, G)
+    tol = TOL[dt]
+    check("fwd_merged", "y", from_torch(y), oracle.merge_fwd(h_ref, uf, mean), tol, per_slab=False)
+    if keep_h:
+        check("fwd_merged", "h", from_torch(h), h_ref, tol)

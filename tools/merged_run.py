@@ -46,6 +46,9 @@ mf = timed(lambda: gspn.merge_fwd(h, u, dirs, out=y))
 mb = timed(lambda: gspn.merge_bwd(h, u, dy, dirs, outs=(dh, du)))
 b = timed(lambda: gspn.bwd(*a, h, dh, dirs, G, outs=outs, workspace=ws))
 bm = timed(lambda: gspn.bwd_merged(*a, h, u, dy, dirs, G, outs=outs_m, workspace=wsm))
-print(gspn.last_path(), gspn.last_launch_count())
+pb = (gspn.last_path(), gspn.last_launch_count())
+fm = timed(lambda: gspn.fwd_merged(*a, u, dirs, G, out=y, h_out=h))
+pf = (gspn.last_path(), gspn.last_launch_count())
+print(pb, pf)
 print(f"fwd {f:.3f} merge_fwd {mf:.3f} merge_bwd {mb:.3f} bwd {b:.3f} | unfused step {f + mf + mb + b:.3f} ms"
-      f" | bwd_merged {bm:.3f} -> step {f + mf + bm:.3f} ms")
+      f" | fwd_merged {fm:.3f} bwd_merged {bm:.3f} -> fused step {fm + bm:.3f} ms")
