@@ -632,6 +632,23 @@ def measure_next(args, gspn, cfg, sh, t, h, outs, ws, dev, stream):
     for name, ms, nbytes in (("merge_fwd", mf, s * N * (2 * D + 1)), ("merge_bwd", mb, s * N * (4 * D + 1))):
         gbs = nbytes / (ms * 1e-3) / 1e9
         out[name] = {"ms": ms, "gbs": gbs, "frac": gbs / peak, "bytes": nbytes, "launches": 1}
+    # NEXT-1 fused: the scan's backward through the merge in one launch (dh = s u dy never stored), and the
+    # forward + merge in one cooperative launch; vs the unfused chain fwd, merge_fwd, merge_bwd, bwd
+    wsm = torch.empty(max(16, int(gspn.lib().gspn_bwd_merged_workspace_bytes(sh.B, sh.C, cfg.H, cfg.W, cfg.dirs, sh.G,
+                                                                               gspn.DTYPE_BF16 if cfg.dtype == "bf16"
+                                                                               else gspn.DTYPE_F32))),
+                      dtype=torch.uint8, device=dev)
+    a = (t["x"], t["w_l"], t["w_m"], t["w_r"], t["lam"])
+    fm = timed(lambda: gspn.fwd_merged(*a, u, cfg.dirs, sh.G, out=y, h_out=h), reps)
+    pfm = (gspn.last_path(), gspn.last_launch_count())
+    bm = timed(lambda: gspn.bwd_merged(*a, h, u, dy, cfg.dirs, sh.G, outs=tuple(outs) + (du,), workspace=wsm), reps)
+    pbm = (gspn.last_path(), gspn.last_launch_count())
+    f0 = timed(lambda: gspn.fwd(*a, cfg.dirs, sh.G, out=h), reps)
+    b0 = timed(lambda: gspn.bwd(*a, h, dh2, cfg.dirs, sh.G, outs=outs, workspace=ws), reps)
+    out["merged_step"] = {"fwd_merged_ms": fm, "fwd_merged_path": pfm, "bwd_merged_ms": bm, "bwd_merged_path": pbm,
+                          "fused_step_ms": fm + bm, "unfused_step_ms": f0 + mf + mb + b0,
+                          "unfused": {"fwd": f0, "merge_fwd": mf, "merge_bwd": mb, "bwd": b0}}
+    del wsm
     del u, dy, y, dh2, du
     k = max(1, min(cfg.H, cfg.W) // 4)
     lf = timed(lambda: gspn.fwd(t["x"], t["w_l"], t["w_m"], t["w_r"], t["lam"], cfg.dirs, sh.G, out=h, kchunk=k), reps)

@@ -121,7 +121,16 @@ struct alignas(64) StreamArgs {
   ScanParams p;
   Plan plan;
   void* g;                      // bwd: adjoint state g [D,B,C,H,W] (I/O dtype, workspace)
+  unsigned* ready;              // single-launch bwd: per (pack of) plane(s), chains whose g is complete
 };
+
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 // ------------------------------------------------------------------------------ element access
 
@@ -314,11 +323,13 @@ __device__ void storer_loop(const StreamArgs& A, uint8_t* ring, uint64_t* done, 
   const uint64_t pol = policy_of(pl.pol[4]);
   int stage = 0;
   uint32_t phase = 0;
+  int64_t pending = -1;  // single-launch bwd: plane pack of the previous chain, published one chain later
   for (int64_t w = work_first<kCl>(pl); w < pl.nchains; w += work_stride<kCl>(pl)) {
     const Chain ch = make_chain<kCl>(A.p, pl, w);
     for (int jj = 0; jj < ch.ntiles; ++jj) {
       const int j = bwd ? (ch.ntiles - 1 - jj) : jj;
       mbar_wait_sleep(smem_u32(&done[stage]), phase);
+      if (ch.vert && A.ready != nullptr) bulk_commit();  // an empty group: one group per tile either way
       if (!ch.vert) {
         const int s0 = tile_start(ch, j, pl.K);
         const uint8_t* st = ring + static_cast<size_t>(stage) * pl.stage_bytes;
@@ -342,8 +353,25 @@ __device__ void storer_loop(const StreamArgs& A, uint8_t* ring, uint64_t* done, 
       mbar_arrive(smem_u32(&empty[stage]));
       if (++stage == pl.nstages) { stage = 0; phase ^= 1; }
     }
+    // Single-launch bwd: publish the PREVIOUS chain's plane once its stores are complete -- every bulk group
+    // but this chain's last 8 (one per tile) -- so the storer never waits for its own latest stores.
+    if (A.ready != nullptr) {
+      if (pending >= 0) {
+        if (ch.ntiles >= 8) bulk_wait_group8();
+        else bulk_wait_all();
+        fence_acq_rel_gpu();  // the consumers' g stores (observed through `done`) are gpu-visible
+        fence_proxy_async_global();
+        atomicAdd(A.ready + pending, 1u);
+      }
+      pending = ch.bc / pl.npack;
+    }
   }
   bulk_wait_all();
+  if (A.ready != nullptr && pending >= 0) {
+    fence_acq_rel_gpu();
+    fence_proxy_async_global();
+    atomicAdd(A.ready + pending, 1u);
+  }
 }
 
 // ------------------------------------------------------------------------------ per-lane geometry
@@ -1887,6 +1915,8 @@ struct OutArgs {
   uint32_t khoff[4];                                 // byte offset of direction k's h halo tile
   uint32_t dyoff;                                    // merged backward: the dy tile (after x)
   int64_t nunits;
+  const unsigned* ready;                             // single launch: wait for D chains of the unit's plane
+  int npack;
 };
 
 constexpr int kOutConsumers = 16;
@@ -1927,6 +1957,11 @@ __device__ __forceinline__ void out_tma_body(const OutArgs& A, uint8_t* ring, ui
         const int i0 = static_cast<int>(u % A.nrb) * RB;
         const int64_t b = bc / p.C, c = bc % p.C;
         mbar_wait_sleep(smem_u32(&empty[stage]), phase ^ 1);
+        if (A.ready != nullptr) {  // every direction's g of this plane written (chains on other CTAs)
+          const unsigned* r = A.ready + bc / A.npack;
+          while (ld_acquire_gpu(r) < static_cast<unsigned>(D)) __nanosleep(128);
+          fence_proxy_async_global();
+        }
         const uint32_t fb = smem_u32(&full[stage]);
         mbar_arrive_tx(fb, A.tx);
         const uint32_t st = smem_u32(ring + static_cast<size_t>(stage) * A.stage_bytes);
@@ -2103,20 +2138,28 @@ struct OneArgs {
 __device__ __forceinline__ void mbar_inval(uint32_t bar) {
   asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
 }
-__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
-
 template <typename T, int kPre, bool kLocal, bool kMerged = false>
 __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_one_kernel(const __grid_constant__ OneArgs A) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const Plan& pl = A.s.plan;
   const Smem m = carve(smem_raw, pl);
+  // plane-readiness counters start at 0 before any chain can finish
+  if (A.s.ready != nullptr) {
+    const int64_t npl = (pl.nbc + pl.npack - 1) / pl.npack;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < npl;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+      A.s.ready[i] = 0u;
+    __threadfence();
+  }
   init_barriers<false>(m, pl);
+  if (A.s.ready != nullptr) cooperative_groups::this_grid().sync();  // counters zeroed before any chain ends
   bwd_fused_body<T, kPre, kLocal, kMerged>(A.s, m);
-  // g (generic stores of the vertical chains, TMA stores of the horizontal ones -- the storer waited for
-  // their completion) must be visible to the other CTAs' TMA loads of phase 2
+  // Grid-wide barrier between the phases (default). With readiness counters (experiments: GSPN_PLANE_READY)
+  // a unit's producer instead waits until the D chains of its plane have published their g (storer:
+  // completed stores, gpu-scope fence, counter), so CTAs that finish phase 1 early start phase 2.
   fence_proxy_async_global();
   __syncthreads();
-  cooperative_groups::this_grid().sync();
+  if (A.s.ready == nullptr) cooperative_groups::this_grid().sync();
   const OutArgs& O = A.o;
   uint64_t* full = reinterpret_cast<uint64_t*>(m.ring + static_cast<size_t>(O.nstages) * O.stage_bytes);
   uint64_t* empty = full + O.nstages;
@@ -2607,15 +2650,17 @@ int norm_mode(const ScanParams& p, const Plan& pl) {
 constexpr size_t kAlign = 256;
 size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
 
-// Backward workspace: the adjoint state g [D, B, C, H, W] in the I/O dtype.
+// Backward workspace: the adjoint state g [D, B, C, H, W] in the I/O dtype, then one readiness counter per
+// (b, c) plane (single-launch backward).
 struct WsLayout {
-  size_t g, total;
+  size_t g, ready, total;
 };
 
 WsLayout ws_layout(int64_t B, int64_t C, int64_t H, int64_t W, int64_t D, gspn_dtype_t dt) {
   WsLayout l;
   l.g = 0;
-  l.total = align_up(static_cast<size_t>(D * B * C * H * W) * (dt == GSPN_BF16 ? 2 : 4));
+  l.ready = align_up(static_cast<size_t>(D * B * C * H * W) * (dt == GSPN_BF16 ? 2 : 4));
+  l.total = l.ready + align_up(static_cast<size_t>(B * C) * sizeof(unsigned));
   return l;
 }
 
@@ -2910,6 +2955,14 @@ bool launch_bwd_fused(const ScanParams& p0, gspn_dtype_t dt, cudaStream_t s, int
     std::unique_ptr<OneArgs> one(new OneArgs());
     one->s = A;
     if (setup_out_tma(p, A.g, dt, true, pl.nwc, smem_optin() - 1024 - 256, one->o, merged)) {
+      // Per-plane readiness instead of the grid-wide barrier (experiments only): measured slower, 7.03-7.08
+      // vs 6.78-6.82 ms on config 4 (3 same-box pairs; profiles/r2_notes.md) -- early phase-2 units compete
+      // with the last chains for bandwidth and every chain pays a gpu-scope fence.
+      if (knob("GSPN_PLANE_READY")) {
+        one->s.ready = reinterpret_cast<unsigned*>(static_cast<char*>(p.ws) + l.ready);
+        one->o.ready = one->s.ready;
+        one->o.npack = pl.npack;
+      }
       cudaError_t e;
       using BF = __nv_bfloat16;
       if (merged) {

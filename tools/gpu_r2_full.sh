@@ -1,0 +1,13 @@
+#!/bin/bash
+# round 2: full GPU suite (+ error log), default bench line, launch list, ncu captures of the top kernels
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/r2_build.log 2>&1 || { tail -30 gpurun_out/r2_build.log; exit 1; }
+export GSPN_ERRLOG=gpurun_out/parity_errors_full.jsonl
+rm -f $GSPN_ERRLOG
+timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/r2_full_test.log 2>&1; echo "pytest rc=$?" >> gpurun_out/r2_full_test.log
+tail -4 gpurun_out/r2_full_test.log
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r2_smoke.log 2>&1; echo "smoke rc=$?"; tail -3 gpurun_out/r2_smoke.log
+timeout 900 python bench.py > gpurun_out/r2_bench_default.log 2>&1; echo "bench rc=$?"
+grep '^{' gpurun_out/r2_bench_default.log | tail -1 > gpurun_out/r2_bench_default.json
+ncu --metrics gpu__time_duration.sum --clock-control none -c 40 --csv --log-file gpurun_out/r2_cfg4_launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-others --no-next --no-cpu-baseline > /dev/null 2>&1; echo "ncu launches rc=$?"
+ncu --set full --clock-control none --import-source on -k regex:"bwd_one|fwd_stream" -s 2 -c 2 -o gpurun_out/r2_cfg4_prof -f python bench.py --steps 2 --warmup 1 --no-e2e --no-others --no-next --no-cpu-baseline > /dev/null 2>&1; echo "ncu full rc=$?"
+ncu --set full --clock-control none --import-source on -k regex:"stream_kernel|bwd_out" -s 3 -c 3 -o gpurun_out/r2_cfg5_prof -f python bench.py --config 5 --steps 1 --warmup 1 --no-e2e --no-others --no-next --no-cpu-baseline > /dev/null 2>&1; echo "ncu cfg5 rc=$?"
