@@ -272,7 +272,7 @@ __device__ __forceinline__ int64_t plane_of(const Chain& ch, int slot) {
 
 // ------------------------------------------------------------------------------ producer / storer
 
-template <bool kBwd, bool kCl>
+template <bool kBwd, bool kCl, bool kXG = false>
 __device__ void producer_loop(const StreamArgs& A, uint8_t* ring, uint64_t* full, uint64_t* empty) {
   const Plan& pl = A.plan;
   const uint64_t pol_xin = policy_of(pl.pol[0]);
@@ -292,9 +292,10 @@ __device__ void producer_loop(const StreamArgs& A, uint8_t* ring, uint64_t* full
       const int s0 = tile_start(ch, j, pl.K);
       const uint32_t st = smem_u32(ring + static_cast<size_t>(stage) * pl.stage_bytes);
       for (int t = 0; t < pl.nin; ++t) {
-        const int plane = static_cast<int>(plane_of<kBwd>(ch, t));
+        const int tt = t + (kXG ? 1 : 0);  // kXG: the stage holds lam, w_l, w_m, w_r (x comes from L2)
+        const int plane = static_cast<int>(plane_of<kBwd>(ch, tt));
         // x is re-read by the plane's other directions; vertical streams are read exactly once
-        const uint64_t pol = (!kBwd && t == F_X) ? pol_xin : (ch.vert ? pol_vin : pol_hin);
+        const uint64_t pol = (!kBwd && tt == F_X) ? pol_xin : (ch.vert ? pol_vin : pol_hin);
         const uint32_t dst = st + t * pl.tile_bytes;
         if (pl.npack > 1) {  // one 3D box: vertical (W, planes, rows), horizontal (cols, H, planes)
           if (ch.vert) tma_load3(dst, &A.in[0][t], 0, plane, s0, fb, pol);
@@ -406,6 +407,10 @@ struct Lanes {
   int64_t vout;          // vertical: element offset of the lane's first position in row 0 of its plane
   // tap unpack masks [tap l/m/r][element e | slot q][half / (and, or)]
   uint32_t s[3][kE][2];
+  // forward with x read from global memory (kXG): element offsets of the lane's x in row / column 0
+  int64_t xoff;          // vertical: the lane's 2 positions of plane row 0
+  int64_t xho[kE];       // horizontal: start of each slot's row
+  bool xv_ok, xh_ok[kE];
 };
 
 // r: tile position; psub: positions per chain; nvalid: chains present (packing). A chain's taps at its
@@ -457,6 +462,8 @@ __device__ __forceinline__ Lanes<T> make_lanes(const Plan& pl, const ScanParams&
     }
     const int rv = r0 < 0 ? 0 : r0;
     ln.vout = (ch.chain + rv / ch.psub) * (p.H * p.W) + rv % ch.psub;  // P % kE == 0: both positions in one chain
+    ln.xv_ok = r0 >= 0 && r0 < nval;
+    ln.xoff = (ch.bc + rv / ch.psub) * (p.H * p.W) + rv % ch.psub;
   }
   // horizontal
 #pragma unroll
@@ -467,6 +474,9 @@ __device__ __forceinline__ Lanes<T> make_lanes(const Plan& pl, const ScanParams&
     ln.own_h[q] = off >= lo && off < WARP - C::GH && rt < kPpad;  // rows >= P: outside the store box
     const uint32_t rc = static_cast<uint32_t>(rt < 0 ? 0 : (rt >= kPpad ? kPpad - 1 : rt));
     ln.hoff[q] = rc * 32 + (((rc >> 2) & 1u) << 4);
+    ln.xh_ok[q] = r >= 0 && r < nval;
+    const int rr = r < 0 ? 0 : r;
+    ln.xho[q] = (ch.bc + rr / ch.psub) * (p.H * p.W) + static_cast<int64_t>(rr % ch.psub) * p.W;
   }
   if (ch.vert) {
 #pragma unroll
@@ -742,13 +752,53 @@ __device__ __forceinline__ float fwd_math(float x, float lam, float l, float m, 
   return fmaf(acc, inv, lam * x);
 }
 
+// x of one half-tile held in registers (forward with x read from global memory, kXG): x is shared by the
+// D directions of a plane, so it is mostly served by L2; leaving it out of the TMA stage frees a ring slot
+// (4 tiles per stage instead of 5: 3 stages instead of 2). Loaded one half ahead of its use.
+template <typename T>
+struct XPre {
+  static constexpr int kV = Cfg<T>::KS * static_cast<int>(sizeof(T)) / 2;  // vertical: 2 elements per step
+  uint32_t v[kV];
+  uint4 h[kE];  // horizontal: the KS-step chunk of each slot's row
+};
+
+template <typename T>
+__device__ __forceinline__ void x_fetch(XPre<T>& xp, const Lanes<T>& ln, const Chain& ch, const T* xg, int j, int half,
+                                        int64_t W) {
+  using C = Cfg<T>;
+  if (ch.vert) {
+    const int t0 = j * C::K + half * C::KS;
+#pragma unroll
+    for (int ss = 0; ss < C::KS; ++ss) {
+      const int t = t0 + ss;
+      const bool ok = ln.xv_ok && t < ch.L;
+      const int row = ch.rev ? ch.L - 1 - t : t;
+      const T* a = xg + ln.xoff + static_cast<int64_t>(ok ? row : 0) * W;
+      if constexpr (sizeof(T) == 2) {
+        xp.v[ss] = ok ? __ldg(reinterpret_cast<const unsigned int*>(a)) : 0u;
+      } else {
+        const uint2 u = ok ? __ldg(reinterpret_cast<const uint2*>(a)) : make_uint2(0u, 0u);
+        xp.v[2 * ss] = u.x;
+        xp.v[2 * ss + 1] = u.y;
+      }
+    }
+  } else {
+    const int cm = ch.rev ? 1 - half : half;
+    const int64_t c0 = tile_start(ch, j, C::K) + cm * C::KS;
+#pragma unroll
+    for (int q = 0; q < kE; ++q)
+      xp.h[q] = ln.xh_ok[q] ? ld_nc_v4(xg + ln.xho[q] + c0) : make_uint4(0u, 0u, 0u, 0u);
+  }
+}
+
 // Vertical half-tile: KS steps; p0 = the lane's operands at the half's first step, stepb = +-kRowB.
 // New states go straight to global memory (gp advances by gstep rows per step).
-template <typename T, int kPre, bool kLocal>
+template <typename T, int kPre, bool kLocal, bool kXG = false>
 __device__ __forceinline__ void fwd_half_vert(const Lanes<T>& ln, const uint8_t* p0, int stepb, T* gp,
                                               int64_t gstep, int t0, int L, float (&h)[kE], uint64_t pol,
-                                              uint32_t rm) {
+                                              uint32_t rm, const XPre<T>* xp = nullptr) {
   constexpr int KS = Cfg<T>::KS;
+  constexpr int o = kXG ? 1 : 0;  // kXG: x is not in the stage, the other tiles move down one slot
 #pragma unroll
   for (int ss = 0; ss < KS; ++ss) {
     if constexpr (kLocal) {  // segment start: h_{t-1} does not propagate (warp-uniform)
@@ -756,11 +806,21 @@ __device__ __forceinline__ void fwd_half_vert(const Lanes<T>& ln, const uint8_t*
     }
     const uint8_t* q = p0 + ss * stepb;
     float x[2], lam[2], l[2], m[2], r[2];
-    vload<T>(q + F_X * kTile, x);
-    vload<T>(q + F_LAM * kTile, lam);
-    vload_tap<T>(q + F_WL * kTile, ln.s[0], l);
-    vload_tap<T>(q + F_WM * kTile, ln.s[1], m);
-    vload_tap<T>(q + F_WR * kTile, ln.s[2], r);
+    if constexpr (kXG) {
+      if constexpr (sizeof(T) == 2) {
+        x[0] = __uint_as_float(xp->v[ss] << 16);
+        x[1] = __uint_as_float(xp->v[ss] & 0xFFFF0000u);
+      } else {
+        x[0] = __uint_as_float(xp->v[2 * ss]);
+        x[1] = __uint_as_float(xp->v[2 * ss + 1]);
+      }
+    } else {
+      vload<T>(q + F_X * kTile, x);
+    }
+    vload<T>(q + (F_LAM - o) * kTile, lam);
+    vload_tap<T>(q + (F_WL - o) * kTile, ln.s[0], l);
+    vload_tap<T>(q + (F_WM - o) * kTile, ln.s[1], m);
+    vload_tap<T>(q + (F_WR - o) * kTile, ln.s[2], r);
     const float left = __shfl_up_sync(0xffffffffu, h[1], 1);    // lane 0: own value (ghost or masked)
     const float right = __shfl_down_sync(0xffffffffu, h[0], 1);  // lane 31: own value
     const float h0 = fwd_math<kPre>(x[0], lam[0], l[0], m[0], r[0], left, h[0], h[1]);
@@ -789,19 +849,22 @@ __device__ __forceinline__ void slot_hi(const float (&v)[kE], int lane, float (&
 
 // Horizontal half-tile: one 16-byte chunk (KS steps) per tensor per slot; kRev walks the chunk
 // backwards (R2L). The new states come back packed in memory order for the in-place write.
-template <typename T, int kPre, bool kRev, bool kLocal>
+template <typename T, int kPre, bool kRev, bool kLocal, bool kXG = false>
 __device__ __forceinline__ void fwd_half_horiz(const Lanes<T>& ln, const uint8_t* st, int cm, int lane,
-                                               float (&h)[kE], uint4 (&OUT)[kE], uint32_t rm) {
+                                               float (&h)[kE], uint4 (&OUT)[kE], uint32_t rm,
+                                               const XPre<T>* xp = nullptr) {
   constexpr int KS = Cfg<T>::KS;
+  constexpr int o = kXG ? 1 : 0;
   uint4 X[kE], LAM[kE], WL[kE], WM[kE], WR[kE];
 #pragma unroll
   for (int q = 0; q < kE; ++q) {
     const uint32_t off = ln.hoff[q] ^ (static_cast<uint32_t>(cm) << 4);
-    X[q] = *reinterpret_cast<const uint4*>(st + F_X * kTile + off);
-    LAM[q] = *reinterpret_cast<const uint4*>(st + F_LAM * kTile + off);
-    WL[q] = *reinterpret_cast<const uint4*>(st + F_WL * kTile + off);
-    WM[q] = *reinterpret_cast<const uint4*>(st + F_WM * kTile + off);
-    WR[q] = *reinterpret_cast<const uint4*>(st + F_WR * kTile + off);
+    if constexpr (kXG) X[q] = xp->h[q];
+    else X[q] = *reinterpret_cast<const uint4*>(st + F_X * kTile + off);
+    LAM[q] = *reinterpret_cast<const uint4*>(st + (F_LAM - o) * kTile + off);
+    WL[q] = *reinterpret_cast<const uint4*>(st + (F_WL - o) * kTile + off);
+    WM[q] = *reinterpret_cast<const uint4*>(st + (F_WM - o) * kTile + off);
+    WR[q] = *reinterpret_cast<const uint4*>(st + (F_WR - o) * kTile + off);
   }
   float O[kE][KS];
 #pragma unroll
@@ -826,23 +889,24 @@ __device__ __forceinline__ void fwd_half_horiz(const Lanes<T>& ln, const uint8_t
 
 // Body of the forward scan (every role returns from here when its work is done); the barriers of `m` must
 // be initialised. Shared by fwd_stream_kernel and the merged single launch fwd_one_kernel.
-template <typename T, int kPre, bool kCl, bool kLocal>
+template <typename T, int kPre, bool kCl, bool kLocal, bool kXG = false>
 __device__ __forceinline__ void fwd_stream_body(const StreamArgs& A, const Smem& m) {
   using C = Cfg<T>;
   const Plan& pl = A.plan;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int kOutSlot = kXG ? 0 : F_X;  // in-place horizontal outputs: over the x (or, kXG, lam) chunk
   if (warp == pl.nwc) {  // producer warp
     if (lane == 0) {
       for (int o = 0; o < 2; ++o)
-        for (int t = 0; t < F_NIN; ++t) asm volatile("prefetch.tensormap [%0];" ::"l"(&A.in[o][t]) : "memory");
-      producer_loop<false, kCl>(A, m.ring, m.full, m.empty);
+        for (int t = 0; t < pl.nin; ++t) asm volatile("prefetch.tensormap [%0];" ::"l"(&A.in[o][t]) : "memory");
+      producer_loop<false, kCl, kXG>(A, m.ring, m.full, m.empty);
     }
     cluster_exit<kCl>();
     return;
   }
   if (warp == pl.nwc + 1) {  // storer warp
     if (lane == 0) {
-      const int slots[1] = {F_X};
+      const int slots[1] = {kOutSlot};
       storer_loop<kCl>(A, m.ring, m.done, m.empty, 1, slots, false);
     }
     cluster_exit<kCl>();
@@ -857,11 +921,14 @@ __device__ __forceinline__ void fwd_stream_body(const StreamArgs& A, const Smem&
   uint32_t xphase = 0;  // P-split: phase bit of the cluster edge barriers, per parity
   int stage = 0, par = 0;
   uint32_t phase = 0;
+  const T* const xg = static_cast<const T*>(A.p.x);
   for (int64_t w = work_first<kCl>(pl); w < pl.nchains; w += work_stride<kCl>(pl)) {
     const Chain ch = make_chain<kCl>(A.p, pl, w);
     const Lanes<T> ln = make_lanes<T, kCl>(pl, A.p, ch, warp, lane);
     T* hout = static_cast<T*>(A.p.hout) + ln.vout;
     float h[kE] = {0.f, 0.f};
+    XPre<T> xcur;
+    if constexpr (kXG) x_fetch<T>(xcur, ln, ch, xg, 0, 0, W);
     for (int j = 0; j < ch.ntiles; ++j) {
       mbar_wait_sleep(smem_u32(&m.full[stage]), phase);
       __syncwarp();  // reconverge after the per-thread spin: the shuffles below need no collective fallback
@@ -871,6 +938,11 @@ __device__ __forceinline__ void fwd_stream_body(const StreamArgs& A, const Smem&
         uint4 OUT[kE];
         const int cm = ch.rev ? 1 - half : half;  // horizontal: memory chunk of this half
         const bool live = !pl.null_compute && !half_outside_k<C::K>(ch, j, half, cm);
+        XPre<T> xnext;
+        if constexpr (kXG) {  // the next half's x, loaded while this half computes
+          const int jn = half == 0 ? j : j + 1, hn = half ^ 1;
+          if (jn < ch.ntiles) x_fetch<T>(xnext, ln, ch, xg, jn, hn, W);
+        }
         if (live) {
           uint32_t rm = 0;
           if (ch.vert) {
@@ -879,17 +951,18 @@ __device__ __forceinline__ void fwd_stream_body(const StreamArgs& A, const Smem&
             const int row0 = ch.rev ? ch.L - 1 - t0 : t0;
             const int vs = static_cast<int>(pl.vstep);
             if constexpr (kLocal) rm = reset_bits(row0, ch.rev ? -1 : 1, !ch.rev, kchunk, C::KS);
-            fwd_half_vert<T, kPre, kLocal>(ln, st + ln.voff + kk0 * vs, ch.rev ? -vs : vs,
-                                           hout + static_cast<int64_t>(row0) * W, ch.rev ? -W : W, t0, ch.L, h,
-                                           pol_vout, rm);
+            fwd_half_vert<T, kPre, kLocal, kXG>(ln, st + ln.voff + kk0 * vs, ch.rev ? -vs : vs,
+                                                hout + static_cast<int64_t>(row0) * W, ch.rev ? -W : W, t0, ch.L, h,
+                                                pol_vout, rm, &xcur);
           } else {
             if constexpr (kLocal)
               rm = reset_bits(tile_start(ch, j, C::K) + cm * C::KS + (ch.rev ? C::KS - 1 : 0), ch.rev ? -1 : 1,
                               !ch.rev, kchunk, C::KS);
-            if (ch.rev) fwd_half_horiz<T, kPre, true, kLocal>(ln, st, cm, lane, h, OUT, rm);
-            else fwd_half_horiz<T, kPre, false, kLocal>(ln, st, cm, lane, h, OUT, rm);
+            if (ch.rev) fwd_half_horiz<T, kPre, true, kLocal, kXG>(ln, st, cm, lane, h, OUT, rm, &xcur);
+            else fwd_half_horiz<T, kPre, false, kLocal, kXG>(ln, st, cm, lane, h, OUT, rm, &xcur);
           }
         }
+        if constexpr (kXG) xcur = xnext;
         edge_publish(m.edge + par * kEdgeW * kXRow, warp, lane, ch.vert, h);
         if constexpr (kCl) {
 #pragma unroll
@@ -912,11 +985,11 @@ __device__ __forceinline__ void fwd_stream_body(const StreamArgs& A, const Smem&
           xphase ^= 1u << par;
         }
         par ^= 1;
-        if (!ch.vert && live) {  // new states in place over the x chunk of this half
+        if (!ch.vert && live) {  // new states in place over the x (kXG: lam) chunk of this half
 #pragma unroll
           for (int q = 0; q < kE; ++q)
             if (ln.own_h[q])
-              *reinterpret_cast<uint4*>(st + F_X * kTile + (ln.hoff[q] ^ (static_cast<uint32_t>(cm) << 4))) = OUT[q];
+              *reinterpret_cast<uint4*>(st + kOutSlot * kTile + (ln.hoff[q] ^ (static_cast<uint32_t>(cm) << 4))) = OUT[q];
         }
       }
       fence_proxy_async();  // in-place outputs -> visible to the storer's TMA (async proxy)
@@ -928,12 +1001,12 @@ __device__ __forceinline__ void fwd_stream_body(const StreamArgs& A, const Smem&
   cluster_exit<kCl>();
 }
 
-template <typename T, int kPre, bool kCl, bool kLocal>
+template <typename T, int kPre, bool kCl, bool kLocal, bool kXG = false>
 __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) fwd_stream_kernel(const __grid_constant__ StreamArgs A) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const Smem m = carve(smem_raw, A.plan);
   init_barriers<kCl>(m, A.plan);
-  fwd_stream_body<T, kPre, kCl, kLocal>(A, m);
+  fwd_stream_body<T, kPre, kCl, kLocal, kXG>(A, m);
 }
 
 // ------------------------------------------------------------------------------ backward recurrence
@@ -2621,15 +2694,15 @@ cudaError_t launch(KernelT kernel, const StreamArgs& A, cudaStream_t s) {
 
 // GSPN-local chains (kchunk > 0) run the kLocal instantiations, with the pre-normalised or the clamped
 // normaliser only (fewer instantiations; the clamped reciprocal is exact wherever S > 0).
-template <typename T, bool kCl>
+template <typename T, bool kCl, bool kXG = false>
 cudaError_t launch_fwd(int mode, bool local, const StreamArgs& A, cudaStream_t s) {
   if (local) {
-    if (mode == kNormPre) return launch(fwd_stream_kernel<T, kNormPre, kCl, true>, A, s);
-    return launch(fwd_stream_kernel<T, kNormClamp, kCl, true>, A, s);
+    if (mode == kNormPre) return launch(fwd_stream_kernel<T, kNormPre, kCl, true, kXG>, A, s);
+    return launch(fwd_stream_kernel<T, kNormClamp, kCl, true, kXG>, A, s);
   }
-  if (mode == kNormPre) return launch(fwd_stream_kernel<T, kNormPre, kCl, false>, A, s);
-  if (mode == kNormClamp) return launch(fwd_stream_kernel<T, kNormClamp, kCl, false>, A, s);
-  return launch(fwd_stream_kernel<T, kNormFull, kCl, false>, A, s);
+  if (mode == kNormPre) return launch(fwd_stream_kernel<T, kNormPre, kCl, false, kXG>, A, s);
+  if (mode == kNormClamp) return launch(fwd_stream_kernel<T, kNormClamp, kCl, false, kXG>, A, s);
+  return launch(fwd_stream_kernel<T, kNormFull, kCl, false, kXG>, A, s);
 }
 template <typename T, bool kCl>
 cudaError_t launch_bwd(int mode, bool local, const StreamArgs& A, cudaStream_t s) {
@@ -2678,11 +2751,19 @@ cudaError_t launch_fwd_stream(const ScanParams& p, gspn_dtype_t dt, cudaStream_t
   StreamArgs& A = *hold;
   memset(&A, 0, sizeof A);
   A.p = p;
-  if (!make_plan(p, dt, F_NIN, &A.plan)) return cudaSuccess;
-  const void* ins[F_NIN] = {p.x, p.lam, p.wl, p.wm, p.wr};
-  const int64_t in_planes[F_NIN] = {p.B * p.C, p.D * p.B * p.C, p.D * p.B * p.G, p.D * p.B * p.G, p.D * p.B * p.G};
+  // Experiments only (GSPN_FWD_XG): x from global memory / L2 instead of the TMA ring (4 tiles per stage,
+  // one more stage). Measured much slower on config 4 (fwd 4.72 vs 2.93 ms, profiles/r2_notes.md item 7).
+  const int K = 32 / (dt == GSPN_BF16 ? 2 : 4);
+  Plan probe;
+  if (!make_plan(p, dt, F_NIN, &probe)) return cudaSuccess;
+  const bool xg = probe.cl == 1 && p.W % K == 0 && knob("GSPN_FWD_XG");
+  const int nin = xg ? F_NIN - 1 : F_NIN;
+  if (!make_plan(p, dt, nin, &A.plan)) return cudaSuccess;
+  const void* ins_all[F_NIN] = {p.x, p.lam, p.wl, p.wm, p.wr};
+  const int64_t planes_all[F_NIN] = {p.B * p.C, p.D * p.B * p.C, p.D * p.B * p.G, p.D * p.B * p.G, p.D * p.B * p.G};
   void* outs[1] = {p.hout};
-  if (!fill_maps(&A, ins, F_NIN, outs, in_planes, p.D * p.B * p.C, 1, dt)) return cudaSuccess;
+  if (!fill_maps(&A, ins_all + (xg ? 1 : 0), nin, outs, planes_all + (xg ? 1 : 0), p.D * p.B * p.C, 1, dt))
+    return cudaSuccess;
   *handled = true;
   using BF = __nv_bfloat16;
   const int mode = norm_mode(p, A.plan);
@@ -2690,8 +2771,12 @@ cudaError_t launch_fwd_stream(const ScanParams& p, gspn_dtype_t dt, cudaStream_t
   const bool cl = A.plan.cl > 1;
   *path = cl ? "stream-cluster" : "stream";
   const bool local = p.kchunk > 0;
-  if (dt == GSPN_BF16) e = cl ? launch_fwd<BF, true>(mode, local, A, s) : launch_fwd<BF, false>(mode, local, A, s);
-  else e = cl ? launch_fwd<float, true>(mode, local, A, s) : launch_fwd<float, false>(mode, local, A, s);
+  if (dt == GSPN_BF16)
+    e = cl ? launch_fwd<BF, true>(mode, local, A, s)
+           : (xg ? launch_fwd<BF, false, true>(mode, local, A, s) : launch_fwd<BF, false>(mode, local, A, s));
+  else
+    e = cl ? launch_fwd<float, true>(mode, local, A, s)
+           : (xg ? launch_fwd<float, false, true>(mode, local, A, s) : launch_fwd<float, false>(mode, local, A, s));
   *launches += 1;
   return e;
 }

@@ -486,3 +486,15 @@ def test_backward_prenormalized_equals_raw_chain_rule():
         if k == 2:
             ref = np.where(nr == 0, 0.0, ref)
         np.testing.assert_allclose(raw[1 + k], ref, atol=1e-13)
+
+
+def test_oracle_cli_runs_config1():
+    """The stand-alone oracle CLI (python -m oracle) runs BASELINE config 1 end to end."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-m", "oracle", "--config", "1", "--threads", "2"], capture_output=True,
+                         text=True, timeout=300, cwd=root)
+    assert out.returncode == 0, out.stderr
+    assert "config 1" in out.stdout and "dlam" in out.stdout
