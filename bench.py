@@ -649,6 +649,24 @@ def measure_next(args, gspn, cfg, sh, t, h, outs, ws, dev, stream):
     pbm = (gspn.last_path(), gspn.last_launch_count())
     f0 = timed(lambda: gspn.fwd(*a, cfg.dirs, sh.G, out=h), reps)
     b0 = timed(lambda: gspn.bwd(*a, h, dh2, cfg.dirs, sh.G, outs=outs, workspace=ws), reps)
+    # NEXT-3: checkpointing forward (no h) + recompute backward vs the saved-h step
+    if cfg.G == cfg.C:
+        ckb = int(gspn.lib().gspn_ckpt_bytes(sh.B, sh.C, cfg.H, cfg.W, cfg.dirs, sh.G,
+                                             gspn.DTYPE_BF16 if cfg.dtype == "bf16" else gspn.DTYPE_F32))
+        ck = torch.empty(max(4, ckb // 4), dtype=torch.float32, device=dev)
+        wsr = torch.empty(max(16, int(gspn.lib().gspn_bwd_recompute_workspace_bytes(
+            sh.B, sh.C, cfg.H, cfg.W, cfg.dirs, sh.G, gspn.DTYPE_BF16 if cfg.dtype == "bf16" else gspn.DTYPE_F32))),
+            dtype=torch.uint8, device=dev)
+        fc = timed(lambda: gspn.fwd_ckpt(*a, cfg.dirs, sh.G, ckpt=ck), reps)
+        pfc = (gspn.last_path(), gspn.last_launch_count())
+        br = timed(lambda: gspn.bwd_recompute(*a, ck, t["dh"], cfg.dirs, sh.G, outs=outs, workspace=wsr), reps)
+        pbr = (gspn.last_path(), gspn.last_launch_count())
+        b_s = timed(lambda: gspn.bwd(*a, h, t["dh"], cfg.dirs, sh.G, outs=outs, workspace=ws), reps)
+        out["recompute"] = {"fwd_ckpt_ms": fc, "fwd_ckpt_path": pfc, "bwd_recompute_ms": br, "bwd_recompute_path": pbr,
+                            "step_ms": fc + br, "saved_h_step_ms": f0 + b_s, "ckpt_bytes": ckb,
+                            "note": "fwd writes fp32 checkpoints every half-tile instead of h; the bwd recomputes h "
+                                    "in registers and forms every direction's dw in the recurrence"}
+        del ck, wsr
     out["merged_step"] = {"fwd_merged_ms": fm, "fwd_merged_path": pfm, "bwd_merged_ms": bm, "bwd_merged_path": pbm,
                           "fused_step_ms": fm + bm, "unfused_step_ms": f0 + mf + mb + b0,
                           "unfused": {"fwd": f0, "merge_fwd": mf, "merge_bwd": mb, "bwd": b0}}

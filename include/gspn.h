@@ -193,6 +193,32 @@ size_t gspn_bwd_merged_workspace_bytes(int64_t B, int64_t C, int64_t H, int64_t 
                                        gspn_dtype_t dtype);
 
 /*
+ * Recompute-h backward (activation checkpointing inside the kernels).
+ * gspn_fwd_ckpt is gspn_fwd that also writes fp32 checkpoints of h -- one row per half-tile of KS = 16/s
+ * steps (s = element size), per chain -- into `ckpt` (gspn_ckpt_bytes(...) bytes, contents implementation-
+ * defined) and may skip h itself (h = NULL: the forward then writes s (1 + 2D) N + ... bytes less).
+ * gspn_bwd_recompute is gspn_bwd without h: each half-tile's h is recomputed in registers from the
+ * checkpoint (Eq. 1, fp32: the tap gradients see h unrounded), the tap gradients of every direction are
+ * formed inside the adjoint recurrence, and one output phase forms dlam and dx -- one cooperative launch
+ * (gspn_last_path() "stream-recompute"). Shapes without checkpoints (grouped weights, packed small planes,
+ * P-split chains, H or W not a multiple of 32/s) keep nothing in the forward ("ckpt-deferred") and the
+ * backward re-runs the forward into its workspace ("recompute-unfused"). flags: GSPN_FLAG_PRENORMALIZED,
+ * GSPN_FLAG_FORCE_GENERIC. workspace: >= gspn_bwd_recompute_workspace_bytes(...). Otherwise as gspn_fwd /
+ * gspn_bwd.
+ */
+gspn_status_t gspn_fwd_ckpt(const void* x, const void* w_l, const void* w_m, const void* w_r, const void* lam,
+                            void* h, float* ckpt, int64_t B, int64_t C, int64_t H, int64_t W, uint32_t dirs,
+                            int64_t groups, gspn_dtype_t dtype, uint32_t flags, gspn_stream_t stream);
+gspn_status_t gspn_bwd_recompute(const void* x, const void* w_l, const void* w_m, const void* w_r, const void* lam,
+                                 const float* ckpt, const void* dh, void* dx, void* dw_l, void* dw_m, void* dw_r,
+                                 void* dlam, int64_t B, int64_t C, int64_t H, int64_t W, uint32_t dirs,
+                                 int64_t groups, gspn_dtype_t dtype, uint32_t flags, void* workspace,
+                                 size_t workspace_bytes, gspn_stream_t stream);
+size_t gspn_ckpt_bytes(int64_t B, int64_t C, int64_t H, int64_t W, uint32_t dirs, int64_t groups, gspn_dtype_t dtype);
+size_t gspn_bwd_recompute_workspace_bytes(int64_t B, int64_t C, int64_t H, int64_t W, uint32_t dirs, int64_t groups,
+                                          gspn_dtype_t dtype);
+
+/*
  * Compact-channel proxy projections (§4.2 "project the input tensor
  * x in R^{N x C x H x W} into a lower-dimensional proxy subspace x_proxy in R^{N x C_proxy x H x W}",
  * PAPER.md:172 "expand back to C with a learned 1x1 projection"). A 1x1 projection mixes channels at

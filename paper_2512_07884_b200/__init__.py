@@ -171,6 +171,59 @@ def merge_bwd(h, u, dy, dirs: int = DIR_ALL, mean: bool = False, outs=None, stre
     return dh, du
 
 
+def fwd_ckpt(x, w_l, w_m, w_r, lam, dirs: int = DIR_ALL, groups: int | None = None, flags: int = 0,
+             keep_h: bool = False, ckpt=None, h_out=None, stream=None):
+    """Forward with fp32 checkpoints for the recompute backward (gspn_fwd_ckpt, NEXT-3): returns (ckpt, h),
+    h None unless keep_h."""
+    torch = _torch()
+    G = x.shape[1] if groups is None else int(groups)
+    (B, C, H, W, D), sx, sw, sl = _scan_shapes(x, dirs, G)
+    dt = _dtype_code(x)
+    nb = int(lib().gspn_ckpt_bytes(B, C, H, W, dirs, G, dt))
+    if ckpt is None or ckpt.numel() * 4 < nb:
+        ckpt = torch.empty(max(nb // 4, 4), dtype=torch.float32, device=x.device)
+    h = (torch.empty_like(lam) if h_out is None else h_out) if keep_h else None
+    named = [("lam", lam, sl), ("w_l", w_l, sw), ("w_m", w_m, sw), ("w_r", w_r, sw)]
+    if h is not None:
+        named.append(("h (out)", h, sl))
+    _check_shapes(named)
+    _check_tensors([(n, t) for n, t, _ in named] + [("x", x)], x.dtype, x.device)
+    _check_tensors([("ckpt", ckpt)], torch.float32, x.device)
+    check(lib().gspn_fwd_ckpt(x.data_ptr(), w_l.data_ptr(), w_m.data_ptr(), w_r.data_ptr(), lam.data_ptr(),
+                              h.data_ptr() if h is not None else None, ckpt.data_ptr(), B, C, H, W, dirs, G, dt, flags,
+                              _stream_ptr(stream, x.device)))
+    return ckpt, h
+
+
+def bwd_recompute(x, w_l, w_m, w_r, lam, ckpt, dh, dirs: int = DIR_ALL, groups: int | None = None, flags: int = 0,
+                  outs=None, workspace=None, stream=None):
+    """Backward from checkpoints instead of h (gspn_bwd_recompute, NEXT-3): returns (dx, dw_l, dw_m, dw_r, dlam)."""
+    torch = _torch()
+    G = x.shape[1] if groups is None else int(groups)
+    (B, C, H, W, D), sx, sw, sl = _scan_shapes(x, dirs, G)
+    dt = _dtype_code(x)
+    if outs is None:
+        outs = (torch.empty_like(x), torch.empty_like(w_l), torch.empty_like(w_m), torch.empty_like(w_r),
+                torch.empty_like(lam))
+    dx, dwl, dwm, dwr, dlam = outs
+    _check_shapes([("w_l", w_l, sw), ("w_m", w_m, sw), ("w_r", w_r, sw), ("lam", lam, sl), ("dh", dh, sl),
+                   ("dx (out)", dx, sx), ("dw_l (out)", dwl, sw), ("dw_m (out)", dwm, sw), ("dw_r (out)", dwr, sw),
+                   ("dlam (out)", dlam, sl)])
+    _check_tensors([("x", x), ("w_l", w_l), ("w_m", w_m), ("w_r", w_r), ("lam", lam), ("dh", dh), ("dx", dx),
+                    ("dw_l", dwl), ("dw_m", dwm), ("dw_r", dwr), ("dlam", dlam)], x.dtype, x.device)
+    _check_tensors([("ckpt", ckpt)], torch.float32, x.device)
+    if ckpt.numel() * 4 < int(lib().gspn_ckpt_bytes(B, C, H, W, dirs, G, dt)):
+        raise ValueError("ckpt smaller than gspn_ckpt_bytes")
+    need = int(lib().gspn_bwd_recompute_workspace_bytes(B, C, H, W, dirs, G, dt))
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(max(need, 16), dtype=torch.uint8, device=x.device)
+    check(lib().gspn_bwd_recompute(x.data_ptr(), w_l.data_ptr(), w_m.data_ptr(), w_r.data_ptr(), lam.data_ptr(),
+                                   ckpt.data_ptr(), dh.data_ptr(), dx.data_ptr(), dwl.data_ptr(), dwm.data_ptr(),
+                                   dwr.data_ptr(), dlam.data_ptr(), B, C, H, W, dirs, G, dt, flags,
+                                   workspace.data_ptr(), workspace.numel(), _stream_ptr(stream, x.device)))
+    return dx, dwl, dwm, dwr, dlam
+
+
 def fwd_merged(x, w_l, w_m, w_r, lam, u, dirs: int = DIR_ALL, groups: int | None = None, mean: bool = False,
                flags: int = 0, keep_h: bool = True, out=None, h_out=None, workspace=None, stream=None):
     """Forward scan + output gate + direction merge (gspn_fwd_merged, NEXT-1): returns (y, h), h None when

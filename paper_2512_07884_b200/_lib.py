@@ -42,6 +42,14 @@ def lib() -> ctypes.CDLL:
             L.gspn_fwd_local.restype = ctypes.c_int
             L.gspn_bwd_local.argtypes = [vp] * 12 + [i64] * 4 + [u32, i64, i64, ctypes.c_int, u32, vp, sz, vp]
             L.gspn_bwd_local.restype = ctypes.c_int
+        if hasattr(L, "gspn_fwd_ckpt"):
+            L.gspn_fwd_ckpt.argtypes = [vp] * 7 + [i64] * 4 + [u32, i64, ctypes.c_int, u32, vp]
+            L.gspn_fwd_ckpt.restype = ctypes.c_int
+            L.gspn_bwd_recompute.argtypes = [vp] * 12 + [i64] * 4 + [u32, i64, ctypes.c_int, u32, vp, sz, vp]
+            L.gspn_bwd_recompute.restype = ctypes.c_int
+            for fn in ("gspn_ckpt_bytes", "gspn_bwd_recompute_workspace_bytes"):
+                getattr(L, fn).argtypes = [i64] * 4 + [u32, i64, ctypes.c_int]
+                getattr(L, fn).restype = sz
         if hasattr(L, "gspn_fwd_merged"):
             L.gspn_fwd_merged.argtypes = [vp] * 8 + [i64] * 4 + [u32, i64, ctypes.c_int, u32, vp, sz, vp]
             L.gspn_fwd_merged.restype = ctypes.c_int

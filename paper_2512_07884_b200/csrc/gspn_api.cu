@@ -352,6 +352,150 @@ static gspn_status_t check_proxy_extent(int64_t B, int64_t Ci, int64_t Co, int64
 
 extern "C" {
 
+size_t gspn_ckpt_bytes(int64_t B, int64_t C, int64_t H, int64_t W, uint32_t dirs, int64_t groups,
+                       gspn_dtype_t dtype) {
+  if (check_dims(B, C, H, W, dirs, groups, dtype, 0) != GSPN_OK) return 0;
+  const int64_t KS = dtype == GSPN_BF16 ? 8 : 4;  // one fp32 checkpoint per half-tile of KS steps
+  const int64_t L = (H > W ? H : W);
+  return align_up((size_t)popcount4(dirs) * (size_t)(B * C) * (size_t)(((L + KS - 1) / KS) * L) * sizeof(float));
+}
+
+size_t gspn_bwd_recompute_workspace_bytes(int64_t B, int64_t C, int64_t H, int64_t W, uint32_t dirs, int64_t groups,
+                                          gspn_dtype_t dtype) {
+  const size_t a = gspn_bwd_workspace_bytes(B, C, H, W, dirs, groups, dtype);
+  if (check_dims(B, C, H, W, dirs, groups, dtype, 0) != GSPN_OK) return 0;
+  const size_t s = dtype == GSPN_BF16 ? 2 : 4;
+  return align_up(a) + align_up((size_t)popcount4(dirs) * (size_t)(B * C * H * W) * s);  // + h (fallback)
+}
+
+static void scan_params(gspn::ScanParams& p, const void* x, const void* w_l, const void* w_m, const void* w_r,
+                        const void* lam, int64_t B, int64_t C, int64_t H, int64_t W, uint32_t dirs, int64_t groups,
+                        uint32_t flags) {
+  memset(&p, 0, sizeof p);
+  p.x = x; p.wl = w_l; p.wm = w_m; p.wr = w_r; p.lam = lam;
+  p.B = B; p.C = C; p.H = H; p.W = W; p.G = groups; p.D = popcount4(dirs); p.flags = flags;
+  fill_dirs(p, dirs);
+}
+
+gspn_status_t gspn_fwd_ckpt(const void* x, const void* w_l, const void* w_m, const void* w_r, const void* lam,
+                            void* h, float* ckpt, int64_t B, int64_t C, int64_t H, int64_t W, uint32_t dirs,
+                            int64_t groups, gspn_dtype_t dtype, uint32_t flags, gspn_stream_t stream) {
+  return guarded([&]() -> gspn_status_t {
+    gspn_status_t st;
+    if ((st = check_ptr(x, "x")) || (st = check_ptr(w_l, "w_l")) || (st = check_ptr(w_m, "w_m")) ||
+        (st = check_ptr(w_r, "w_r")) || (st = check_ptr(lam, "lam")) || (st = check_ptr(ckpt, "ckpt")))
+      return st;
+    if (h != nullptr && (st = check_ptr(h, "h"))) return st;
+    if (flags & ~(GSPN_FLAG_PRENORMALIZED | GSPN_FLAG_FORCE_GENERIC))
+      return fail(GSPN_ERR_INVALID_ARG, "%s has unknown bits (0x%llx)", "flags", flags);
+    if ((st = check_dims(B, C, H, W, dirs, groups, dtype, flags))) return st;
+    const size_t s = dtype == GSPN_BF16 ? 2 : 4;
+    const int64_t D = popcount4(dirs);
+    const size_t nx = (size_t)(B * C * H * W) * s, nl = (size_t)D * nx, nw = (size_t)(D * B * groups * H * W) * s;
+    const Span ins[5] = {span("x", x, nx), span("w_l", w_l, nw), span("w_m", w_m, nw), span("w_r", w_r, nw),
+                         span("lam", lam, nl)};
+    const Span outs[2] = {span("ckpt", ckpt, gspn_ckpt_bytes(B, C, H, W, dirs, groups, dtype)),
+                          span("h", h ? h : ckpt, h ? nl : 0)};
+    if ((st = check_aliasing(outs, h ? 2 : 1, ins, 5))) return st;
+    if (H > gspn::generic_max_P() || W > gspn::generic_max_P())
+      return fail(GSPN_ERR_UNSUPPORTED, "%s above the tiled maximum (%lld)", "H or W", (long long)gspn::generic_max_P());
+    gspn::ScanParams p;
+    scan_params(p, x, w_l, w_m, w_r, lam, B, C, H, W, dirs, groups, flags);
+    cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+    int launches = 0;
+    cudaError_t e = cudaSuccess;
+    const char* path;
+    if (!(flags & GSPN_FLAG_FORCE_GENERIC) && gspn::ckpt_eligible(p, dtype)) {
+      p.hout = h;
+      p.ckpt = ckpt;
+      bool handled = false;
+      const char* spath = nullptr;
+      e = gspn::launch_fwd_stream(p, dtype, cs, &launches, &handled, &spath);
+      if (e == cudaSuccess && !handled) e = cudaErrorNotSupported;
+      path = "stream-ckpt";
+    } else if (h != nullptr) {  // no checkpoints on this path: the recompute backward re-runs the forward
+      const gspn_status_t sf = gspn_fwd(x, w_l, w_m, w_r, lam, h, B, C, H, W, dirs, groups, dtype, flags, stream);
+      if (sf != GSPN_OK) return sf;
+      launches = t_launches;
+      path = "ckpt-deferred";
+    } else {
+      path = "ckpt-deferred";  // nothing to keep: the backward recomputes h from the inputs
+    }
+    if (e != cudaSuccess) {
+      snprintf(t_detail, sizeof t_detail, "CUDA error: %s", cudaGetErrorString(e));
+      return GSPN_ERR_CUDA;
+    }
+    t_path = path;
+    t_launches = launches;
+    return GSPN_OK;
+  });
+}
+
+gspn_status_t gspn_bwd_recompute(const void* x, const void* w_l, const void* w_m, const void* w_r, const void* lam,
+                                 const float* ckpt, const void* dh, void* dx, void* dw_l, void* dw_m, void* dw_r,
+                                 void* dlam, int64_t B, int64_t C, int64_t H, int64_t W, uint32_t dirs,
+                                 int64_t groups, gspn_dtype_t dtype, uint32_t flags, void* workspace,
+                                 size_t workspace_bytes, gspn_stream_t stream) {
+  return guarded([&]() -> gspn_status_t {
+    gspn_status_t st;
+    if ((st = check_ptr(x, "x")) || (st = check_ptr(w_l, "w_l")) || (st = check_ptr(w_m, "w_m")) ||
+        (st = check_ptr(w_r, "w_r")) || (st = check_ptr(lam, "lam")) || (st = check_ptr(ckpt, "ckpt")) ||
+        (st = check_ptr(dh, "dh")) || (st = check_ptr(dx, "dx")) || (st = check_ptr(dw_l, "dw_l")) ||
+        (st = check_ptr(dw_m, "dw_m")) || (st = check_ptr(dw_r, "dw_r")) || (st = check_ptr(dlam, "dlam")))
+      return st;
+    if (flags & ~(GSPN_FLAG_PRENORMALIZED | GSPN_FLAG_FORCE_GENERIC))
+      return fail(GSPN_ERR_INVALID_ARG, "%s has unknown bits (0x%llx)", "flags", flags);
+    if ((st = check_dims(B, C, H, W, dirs, groups, dtype, flags))) return st;
+    const size_t need_bwd = gspn_bwd_workspace_bytes(B, C, H, W, dirs, groups, dtype);
+    const size_t need = gspn_bwd_recompute_workspace_bytes(B, C, H, W, dirs, groups, dtype);
+    if ((st = check_ptr(workspace, "workspace"))) return st;
+    if (workspace_bytes < need) {
+      snprintf(t_detail, sizeof t_detail, "workspace too small: %zu < %zu bytes", workspace_bytes, need);
+      return GSPN_ERR_INVALID_ARG;
+    }
+    const size_t s = dtype == GSPN_BF16 ? 2 : 4;
+    const int64_t D = popcount4(dirs);
+    const size_t nx = (size_t)(B * C * H * W) * s, nl = (size_t)D * nx, nw = (size_t)(D * B * groups * H * W) * s;
+    const Span ins[7] = {span("x", x, nx),     span("w_l", w_l, nw), span("w_m", w_m, nw), span("w_r", w_r, nw),
+                         span("lam", lam, nl), span("dh", dh, nl),
+                         span("ckpt", ckpt, gspn_ckpt_bytes(B, C, H, W, dirs, groups, dtype))};
+    const Span outs[6] = {span("dx", dx, nx),     span("dw_l", dw_l, nw), span("dw_m", dw_m, nw),
+                          span("dw_r", dw_r, nw), span("dlam", dlam, nl), span("workspace", workspace, need)};
+    if ((st = check_aliasing(outs, 6, ins, 7))) return st;
+    gspn::ScanParams p;
+    scan_params(p, x, w_l, w_m, w_r, lam, B, C, H, W, dirs, groups, flags);
+    p.dh = dh; p.dx = dx; p.dwl = dw_l; p.dwm = dw_m; p.dwr = dw_r; p.dlam = dlam;
+    p.ckpt = const_cast<float*>(ckpt);
+    p.ws = workspace;
+    p.ws_bytes = need_bwd;
+    cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+    int launches = 0;
+    cudaError_t e = cudaSuccess;
+    const char* path = "stream-recompute";
+    bool handled = false;
+    if (!(flags & GSPN_FLAG_FORCE_GENERIC) && H <= gspn::generic_max_P() && W <= gspn::generic_max_P())
+      handled = gspn::launch_bwd_recompute(p, dtype, cs, &launches, &e);
+    if (!handled) {  // no checkpoints for this shape: the whole forward again (h into the workspace), then gspn_bwd
+      path = "recompute-unfused";
+      void* hws = static_cast<char*>(workspace) + align_up(need_bwd);
+      gspn_status_t sf = gspn_fwd(x, w_l, w_m, w_r, lam, hws, B, C, H, W, dirs, groups, dtype, flags, stream);
+      if (sf != GSPN_OK) return sf;
+      launches = t_launches;
+      sf = gspn_bwd(x, w_l, w_m, w_r, lam, hws, dh, dx, dw_l, dw_m, dw_r, dlam, B, C, H, W, dirs, groups, dtype, flags,
+                    workspace, need_bwd, stream);
+      if (sf != GSPN_OK) return sf;
+      launches += t_launches;
+    }
+    if (e != cudaSuccess) {
+      snprintf(t_detail, sizeof t_detail, "CUDA error: %s", cudaGetErrorString(e));
+      return GSPN_ERR_CUDA;
+    }
+    t_path = path;
+    t_launches = launches;
+    return GSPN_OK;
+  });
+}
+
 size_t gspn_fwd_merged_workspace_bytes(int64_t B, int64_t C, int64_t H, int64_t W, uint32_t dirs, int64_t groups,
                                        gspn_dtype_t dtype) {
   if (check_dims(B, C, H, W, dirs, groups, dtype, 0) != GSPN_OK) return 0;

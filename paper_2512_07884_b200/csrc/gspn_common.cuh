@@ -38,6 +38,10 @@ struct ScanParams {
   const void* dy;          // [B,C,H,W]
   void* du;                // [D,B,C,H,W]
   float merge_scale;       // 1 (Sum) or 1/D (Mean)
+  // recompute-h backward (NEXT-3): fp32 checkpoints of h every half-tile KS = 16 / s steps, per chain
+  // [D,B,C][L/KS][P] (chain stride H W / KS): the forward writes them (and may skip h), the backward
+  // recomputes each half-tile's h from them instead of reading h
+  float* ckpt;
   uint32_t dirbit[4];      // direction bit (GSPN_DIR_*) of slab k
   uint32_t flags;
 };

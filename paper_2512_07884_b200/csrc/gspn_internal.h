@@ -37,6 +37,10 @@ cudaError_t launch_bwd_stream(const ScanParams& p, gspn_dtype_t dt, cudaStream_t
 // Forward + output gate + direction merge in one cooperative launch (NEXT-1); *handled = false: fall back.
 cudaError_t launch_fwd_merged(const ScanParams& p, gspn_dtype_t dt, const void* u, void* y, float scale,
                               cudaStream_t s, int* launches, bool* handled);
+// Recompute-h backward (NEXT-3): forward checkpoints (p.ckpt) and the one-launch backward reading them.
+bool ckpt_eligible(const ScanParams& p, gspn_dtype_t dt);
+size_t ckpt_floats(const ScanParams& p, gspn_dtype_t dt);
+bool launch_bwd_recompute(const ScanParams& p, gspn_dtype_t dt, cudaStream_t s, int* launches, cudaError_t* err);
 size_t stream_bwd_workspace_bytes(int64_t B, int64_t C, int64_t H, int64_t W, int64_t D, int64_t G, gspn_dtype_t dt);
 
 // Output gate + direction merge (gspn_merge.cu). N = B*C*H*W elements per direction slab.

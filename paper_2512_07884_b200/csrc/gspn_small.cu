@@ -382,7 +382,8 @@ __global__ void __launch_bounds__(kGrpWarpsF * 32, 2) fwd_grp_small_kernel(ScanP
       const float up = __shfl_up_sync(0xffffffffu, hv, 1);    // lane 0: tap a = 0
       const float dn = __shfl_down_sync(0xffffffffu, hv, 1);  // lane P-1: tap c = 0; lanes >= P carry 0
       const float4 q = *tq;
-      const float v = fmaf(q.x, up, fmaf(q.y, hv, fmaf(q.z, dn, to_f(*lp) * to_f(*xp))));
+      // lanes >= P read x instead of lam: x is never written, lam at position 0 is (by lane 0)
+      const float v = fmaf(q.x, up, fmaf(q.y, hv, fmaf(q.z, dn, to_f(in ? *lp : *xp) * to_f(*xp))));
       if (in) *lp = from_f<T>(v);  // h over lam at the lane's own pixel (neighbours travel by shuffle)
       hv = in ? v : 0.f;
       tq += P;
@@ -486,15 +487,18 @@ __global__ void __launch_bounds__(kGrpWarpsB * 32, 1) bwd_grp_small_kernel(ScanP
     for (int t = L - 1; t >= 0; --t) {
       const float from_r = __shfl_down_sync(0xffffffffu, ea, 1);  // a_{t+1}[r+1] g_{t+1}[r+1]
       const float from_l = __shfl_up_sync(0xffffffffu, ec, 1);    // c_{t+1}[r-1] g_{t+1}[r-1]
-      const float gsum = to_f(*dhp) + eb + ((hr ? from_r : 0.f) + (hl ? from_l : 0.f));
+      // lanes >= P alias position 0: they read only arrays nobody writes (x, the taps), so lane 0's
+      // in-place writes below never race with them
+      const float gsum = to_f(in ? *dhp : *xp) + eb + ((hr ? from_r : 0.f) + (hl ? from_l : 0.f));
       const float gt = in ? gsum : 0.f;
       const float4 tp = *tq;
       const bool seg = seg_start_step(dir, t, L, kc);  // warp-uniform; t = 0 always: h_{-1} = 0
       const float gh = seg ? 0.f : gt;
-      const T* hq = seg ? dhp : hp;  // any in-plane pixel when h_{t-1} is not used (t = 0: hp is off-plane)
-      const float sb_ = fmaf(gh, to_f(hq[0]), *sbp);
-      const float sa_ = fmaf(hl ? gh : 0.f, to_f(hq[dl]), *sap);
-      const float sc_ = fmaf(hr ? gh : 0.f, to_f(hq[dr]), *scp);
+      const T* hq = seg ? xp : hp;  // any in-plane pixel when h_{t-1} is not used (t = 0: hp is off-plane)
+      const float* ro = reinterpret_cast<const float*>(tq);  // read-only stand-in for lanes >= P
+      const float sb_ = fmaf(gh, to_f(hq[0]), in ? *sbp : *ro);
+      const float sa_ = fmaf(hl ? gh : 0.f, to_f(hq[dl]), in ? *sap : *ro);
+      const float sc_ = fmaf(hr ? gh : 0.f, to_f(hq[dr]), in ? *scp : *ro);
       const float dlam = gt * to_f(*xp);
       const float pk = gt * to_f(*lp);
       if (in) {

@@ -113,6 +113,7 @@ struct Plan {
   int pol[6];
   int null_compute;    // experiments only (GSPN_NULL=1): consumers skip the arithmetic
   int fuse_h;          // fused backward: horizontal chains also form dw in the recurrence (else g only)
+  int no_h;            // forward with checkpoints only (gspn_fwd_ckpt with h = NULL): h is not stored
 };
 
 struct alignas(64) StreamArgs {
@@ -827,8 +828,8 @@ __device__ __forceinline__ void fwd_half_vert(const Lanes<T>& ln, const uint8_t*
     const float h1 = fwd_math<kPre>(x[1], lam[1], l[1], m[1], r[1], h[0], h[1], right);
     h[0] = h0;
     h[1] = h1;
-    GStore<T, 2>::st_if(ln.own_v && t0 + ss < L, gp, h, pol);
-    gp += gstep;
+    GStore<T, 2>::st_if(ln.own_v && t0 + ss < L && gp != nullptr, gp, h, pol);
+    if (gp != nullptr) gp += gstep;
   }
 }
 
@@ -907,7 +908,7 @@ __device__ __forceinline__ void fwd_stream_body(const StreamArgs& A, const Smem&
   if (warp == pl.nwc + 1) {  // storer warp
     if (lane == 0) {
       const int slots[1] = {kOutSlot};
-      storer_loop<kCl>(A, m.ring, m.done, m.empty, 1, slots, false);
+      storer_loop<kCl>(A, m.ring, m.done, m.empty, pl.no_h ? 0 : 1, slots, false);
     }
     cluster_exit<kCl>();
     return;
@@ -922,10 +923,12 @@ __device__ __forceinline__ void fwd_stream_body(const StreamArgs& A, const Smem&
   int stage = 0, par = 0;
   uint32_t phase = 0;
   const T* const xg = static_cast<const T*>(A.p.x);
+  float* const ckpt = A.p.ckpt;                           // NEXT-3 checkpoints (unpacked, unsplit chains)
+  const int64_t ckstride = A.p.H * A.p.W / C::KS;        // floats per chain
   for (int64_t w = work_first<kCl>(pl); w < pl.nchains; w += work_stride<kCl>(pl)) {
     const Chain ch = make_chain<kCl>(A.p, pl, w);
     const Lanes<T> ln = make_lanes<T, kCl>(pl, A.p, ch, warp, lane);
-    T* hout = static_cast<T*>(A.p.hout) + ln.vout;
+    T* hout = pl.no_h ? nullptr : static_cast<T*>(A.p.hout) + ln.vout;
     float h[kE] = {0.f, 0.f};
     XPre<T> xcur;
     if constexpr (kXG) x_fetch<T>(xcur, ln, ch, xg, 0, 0, W);
@@ -952,8 +955,8 @@ __device__ __forceinline__ void fwd_stream_body(const StreamArgs& A, const Smem&
             const int vs = static_cast<int>(pl.vstep);
             if constexpr (kLocal) rm = reset_bits(row0, ch.rev ? -1 : 1, !ch.rev, kchunk, C::KS);
             fwd_half_vert<T, kPre, kLocal, kXG>(ln, st + ln.voff + kk0 * vs, ch.rev ? -vs : vs,
-                                                hout + static_cast<int64_t>(row0) * W, ch.rev ? -W : W, t0, ch.L, h,
-                                                pol_vout, rm, &xcur);
+                                                hout ? hout + static_cast<int64_t>(row0) * W : nullptr,
+                                                ch.rev ? -W : W, t0, ch.L, h, pol_vout, rm, &xcur);
           } else {
             if constexpr (kLocal)
               rm = reset_bits(tile_start(ch, j, C::K) + cm * C::KS + (ch.rev ? C::KS - 1 : 0), ch.rev ? -1 : 1,
@@ -963,6 +966,24 @@ __device__ __forceinline__ void fwd_stream_body(const StreamArgs& A, const Smem&
           }
         }
         if constexpr (kXG) xcur = xnext;
+        if (ckpt != nullptr && live) {  // h at the half's last step: the checkpoint of the next half (NEXT-3)
+          const int hsteps = C::KS;
+          if (ch.vert) {
+            const int t0 = j * C::K + half * C::KS;
+            if (ln.own_v)
+              *reinterpret_cast<float2*>(ckpt + ch.chain * ckstride + static_cast<int64_t>(t0 / hsteps) * ch.P +
+                                         (ln.A + 2 * lane)) = make_float2(h[0], h[1]);
+          } else {
+            const int c0 = tile_start(ch, j, C::K) + cm * C::KS;
+            const int t0 = ch.rev ? ch.L - c0 - C::KS : c0;
+#pragma unroll
+            for (int q = 0; q < kE; ++q) {
+              const int r = ln.A + 32 * q + lane;
+              if (ln.own_h[q] && r < ch.P)
+                ckpt[ch.chain * ckstride + static_cast<int64_t>(t0 / hsteps) * ch.P + r] = h[q];
+            }
+          }
+        }
         edge_publish(m.edge + par * kEdgeW * kXRow, warp, lane, ch.vert, h);
         if constexpr (kCl) {
 #pragma unroll
@@ -1521,6 +1542,315 @@ __device__ __forceinline__ void bwd_fused_body(const StreamArgs& A, const Smem& 
   }
 }
 
+// ------------------------------------------------------------------------------ recompute-h backward
+//
+// NEXT-3: the backward reads fp32 checkpoints of h (one per half-tile,
+// written by the forward, gspn_fwd_ckpt) instead of the stored h. Per half-tile, in the reverse sweep,
+// every lane first re-runs the forward recurrence (Eq. 1) over the half's first KS-1 steps from the
+// checkpoint h_{t0-1} -- x, lam and the taps come with the stage -- keeping h_{t0-1} .. h_{t0+KS-2} in
+// registers, then runs the adjoint steps with the tap gradients of BOTH orientations in the recurrence
+// (dw = u (m d1 + r d2) etc. from h_{t-1} of the lane and its neighbours by shuffle). A warp's window
+// (64 positions, 48 owned) starts from exact checkpoint values everywhere, so after KS - 1 <= 7 recomputed
+// steps its owned positions and their neighbours are still exact (GH = KS). The output phase then forms
+// only dlam and dx for every direction. Unpacked, unsplit chains with H, W multiples of K.
+enum BwdRcIn { R_DH = 0, R_WL, R_WM, R_WR, R_X, R_LAM, R_NIN };
+
+template <typename T, int kPre>
+__device__ void producer_rc(const StreamArgs& A, uint8_t* ring, uint64_t* full, uint64_t* empty) {
+  const Plan& pl = A.plan;
+  const uint64_t pol_vin = policy_of(pl.pol[1]);
+  const uint64_t pol_hin = policy_of(pl.pol[2]);
+  const uint64_t pol_x = policy_of(pl.pol[0]);
+  int stage = 0;
+  uint32_t phase = 0;
+  for (int64_t w = blockIdx.x; w < pl.nchains; w += gridDim.x) {
+    const Chain ch = make_chain<false>(A.p, pl, w);
+    for (int jj = 0; jj < ch.ntiles; ++jj) {
+      const int j = ch.ntiles - 1 - jj;
+      mbar_wait_sleep(smem_u32(&empty[stage]), phase ^ 1);
+      const uint32_t fb = smem_u32(&full[stage]);
+      mbar_arrive_tx(fb, ch.vert ? pl.tx_v : pl.tx_h);
+      const int s0 = tile_start(ch, j, pl.K);
+      const uint32_t st = smem_u32(ring + static_cast<size_t>(stage) * pl.stage_bytes);
+      for (int t = 0; t < R_NIN; ++t) {
+        const int plane = static_cast<int>(t == R_X ? ch.bc : ch.chain);
+        const uint64_t pol = t == R_X ? pol_x : (ch.vert ? pol_vin : pol_hin);
+        const uint32_t dst = st + t * pl.tile_bytes;
+        if (ch.vert) {
+          for (int q = 0; q < pl.nbw; ++q) tma_load3(dst + q * pl.K * pl.bw * pl.es, &A.in[0][t], q * pl.bw, s0, plane, fb, pol);
+        } else {
+          for (int q = 0; q < pl.nbh; ++q) tma_load3(dst + q * pl.bh * 32, &A.in[1][t], s0, q * pl.bh, plane, fb, pol);
+        }
+      }
+      if (++stage == pl.nstages) { stage = 0; phase ^= 1; }
+    }
+  }
+}
+
+// Vertical half: pf = the lane's operands at the half's FIRST scan step, sf = +-row stride in scan order.
+template <typename T, int kPre>
+__device__ __forceinline__ void rc_half_vert(const Lanes<T>& ln, const uint8_t* pf, int sf, int64_t gofs_last,
+                                             int64_t gstep, BwdState& S, uint64_t pol, T* gbase, T* dwl, T* dwm,
+                                             T* dwr, bool hl0, bool hr1, const float (&hck)[2]) {
+  constexpr int KS = Cfg<T>::KS;
+  float hr[KS][2];  // hr[s] = h_{t0-1+s}
+  hr[0][0] = hck[0];
+  hr[0][1] = hck[1];
+#pragma unroll
+  for (int s = 0; s < KS - 1; ++s) {
+    const uint8_t* q = pf + s * sf;
+    float x[2], lam[2], l[2], m[2], r[2];
+    vload<T>(q + R_X * kTile, x);
+    vload<T>(q + R_LAM * kTile, lam);
+    vload_tap<T>(q + R_WL * kTile, ln.s[0], l);
+    vload_tap<T>(q + R_WM * kTile, ln.s[1], m);
+    vload_tap<T>(q + R_WR * kTile, ln.s[2], r);
+    const float left = __shfl_up_sync(0xffffffffu, hr[s][1], 1);
+    const float right = __shfl_down_sync(0xffffffffu, hr[s][0], 1);
+    hr[s + 1][0] = fwd_math<kPre>(x[0], lam[0], l[0], m[0], r[0], left, hr[s][0], hr[s][1]);
+    hr[s + 1][1] = fwd_math<kPre>(x[1], lam[1], l[1], m[1], r[1], hr[s][0], hr[s][1], right);
+  }
+  int64_t gofs = gofs_last;
+#pragma unroll
+  for (int i = 0; i < KS; ++i) {  // adjoint, steps t0 + KS - 1 down to t0
+    const int s = KS - 1 - i;
+    const uint8_t* q = pf + s * sf;
+    float dh[2], l[2], m[2], r[2];
+    vload<T>(q + R_DH * kTile, dh);
+    vload_tap<T>(q + R_WL * kTile, ln.s[0], l);
+    vload_tap<T>(q + R_WM * kTile, ln.s[1], m);
+    vload_tap<T>(q + R_WR * kTile, ln.s[2], r);
+    const float nr1 = __shfl_down_sync(0xffffffffu, S.ea[0], 1);
+    const float nl0 = __shfl_up_sync(0xffffffffu, S.ec[1], 1);
+    const float hleft = __shfl_up_sync(0xffffffffu, hr[s][1], 1);    // h_{t-1}[r0 - 1]
+    const float hright = __shfl_down_sync(0xffffffffu, hr[s][0], 1);  // h_{t-1}[r0 + 2]
+    const float ea0 = S.ea[1], ec1 = S.ec[0];
+    float g[2], ol[2], om[2], orr[2];
+    g[0] = bwd_math<kPre>(dh[0], l[0], m[0], r[0], ea0, nl0, S.ea[0], S.eb[0], S.ec[0]);
+    g[1] = bwd_math<kPre>(dh[1], l[1], m[1], r[1], nr1, ec1, S.ea[1], S.eb[1], S.ec[1]);
+    dw_math<kPre>(g[0], l[0], m[0], r[0], hleft, hr[s][0], hr[s][1], ol[0], om[0], orr[0]);
+    dw_math<kPre>(g[1], l[1], m[1], r[1], hr[s][0], hr[s][1], hright, ol[1], om[1], orr[1]);
+    ol[0] = hl0 ? ol[0] : 0.f;
+    orr[1] = hr1 ? orr[1] : 0.f;
+    GStore<T, 2>::st_if(ln.own_v, gbase + gofs, g, pol);
+    GStore<T, 2>::st_if(ln.own_v, dwl + gofs, ol, pol);
+    GStore<T, 2>::st_if(ln.own_v, dwm + gofs, om, pol);
+    GStore<T, 2>::st_if(ln.own_v, dwr + gofs, orr, pol);
+    gofs += gstep;
+  }
+}
+
+// Pack helpers for the horizontal outputs built one element per step.
+template <typename T> struct PkAcc;
+template <> struct PkAcc<__nv_bfloat16> {
+  uint32_t w[4];
+  __device__ __forceinline__ void put(int i, float v) {  // i compile-time after unrolling
+    const uint32_t b = static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(v)));
+    w[i >> 1] = (i & 1) ? ((w[i >> 1] & 0xFFFFu) | (b << 16)) : ((w[i >> 1] & 0xFFFF0000u) | b);
+  }
+  __device__ __forceinline__ uint4 get() const { return make_uint4(w[0], w[1], w[2], w[3]); }
+};
+template <> struct PkAcc<float> {
+  uint32_t w[4];
+  __device__ __forceinline__ void put(int i, float v) { w[i] = __float_as_uint(v); }
+  __device__ __forceinline__ uint4 get() const { return make_uint4(w[0], w[1], w[2], w[3]); }
+};
+
+template <typename T, int kPre, bool kRev>
+__device__ __forceinline__ void rc_half_horiz(const Lanes<T>& ln, const uint8_t* st, int cm, int lane, BwdState& S,
+                                              const float (&hck)[kE], const bool (&hl)[kE], const bool (&hrr)[kE],
+                                              uint4 (&OG)[kE], uint4 (&OL)[kE], uint4 (&OM)[kE], uint4 (&OR)[kE]) {
+  constexpr int KS = Cfg<T>::KS;
+  uint4 DH[kE], WL[kE], WM[kE], WR[kE], X[kE], LAM[kE];
+#pragma unroll
+  for (int q = 0; q < kE; ++q) {
+    const uint32_t off = ln.hoff[q] ^ (static_cast<uint32_t>(cm) << 4);
+    DH[q] = *reinterpret_cast<const uint4*>(st + R_DH * kTile + off);
+    WL[q] = *reinterpret_cast<const uint4*>(st + R_WL * kTile + off);
+    WM[q] = *reinterpret_cast<const uint4*>(st + R_WM * kTile + off);
+    WR[q] = *reinterpret_cast<const uint4*>(st + R_WR * kTile + off);
+    X[q] = *reinterpret_cast<const uint4*>(st + R_X * kTile + off);
+    LAM[q] = *reinterpret_cast<const uint4*>(st + R_LAM * kTile + off);
+  }
+  float hr[KS][kE];  // hr[s] = h_{t0-1+s} (scan order)
+#pragma unroll
+  for (int q = 0; q < kE; ++q) hr[0][q] = hck[q];
+#pragma unroll
+  for (int s = 0; s < KS - 1; ++s) {
+    const int i = kRev ? KS - 1 - s : s;
+    float lo[kE], hi[kE];
+    slot_lo(hr[s], lane, lo);
+    slot_hi(hr[s], lane, hi);
+#pragma unroll
+    for (int q = 0; q < kE; ++q)
+      hr[s + 1][q] = fwd_math<kPre>(hget<T>(X[q], i), hget<T>(LAM[q], i), hget_tap<T>(WL[q], i, ln.s[0][q]),
+                                    hget_tap<T>(WM[q], i, ln.s[1][q]), hget_tap<T>(WR[q], i, ln.s[2][q]), lo[q],
+                                    hr[s][q], hi[q]);
+  }
+  PkAcc<T> ag[kE], al[kE], am[kE], ar[kE];
+#pragma unroll
+  for (int ss = KS - 1; ss >= 0; --ss) {  // adjoint, scan order descending
+    const int i = kRev ? KS - 1 - ss : ss;
+    float nr[kE], nl[kE], hlo[kE], hhi[kE];
+    slot_hi(S.ea, lane, nr);
+    slot_lo(S.ec, lane, nl);
+    slot_lo(hr[ss], lane, hlo);  // h_{t-1}[r-1]
+    slot_hi(hr[ss], lane, hhi);  // h_{t-1}[r+1]
+#pragma unroll
+    for (int q = 0; q < kE; ++q) {
+      const float l = hget_tap<T>(WL[q], i, ln.s[0][q]), m = hget_tap<T>(WM[q], i, ln.s[1][q]);
+      const float r = hget_tap<T>(WR[q], i, ln.s[2][q]);
+      const float g = bwd_math<kPre>(hget<T>(DH[q], i), l, m, r, nr[q], nl[q], S.ea[q], S.eb[q], S.ec[q]);
+      float ol, om, orr;
+      dw_math<kPre>(g, l, m, r, hlo[q], hr[ss][q], hhi[q], ol, om, orr);
+      ag[q].put(i, g);
+      al[q].put(i, hl[q] ? ol : 0.f);
+      am[q].put(i, om);
+      ar[q].put(i, hrr[q] ? orr : 0.f);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < kE; ++q) {
+    OG[q] = ag[q].get();
+    OL[q] = al[q].get();
+    OM[q] = am[q].get();
+    OR[q] = ar[q].get();
+  }
+}
+
+template <typename T, int kPre>
+__device__ __forceinline__ void bwd_rc_body(const StreamArgs& A, const Smem& m) {
+  using C = Cfg<T>;
+  const Plan& pl = A.plan;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == pl.nwc) {
+    if (lane == 0) {
+      for (int o = 0; o < 2; ++o)
+        for (int t = 0; t < R_NIN; ++t) asm volatile("prefetch.tensormap [%0];" ::"l"(&A.in[o][t]) : "memory");
+      producer_rc<T, kPre>(A, m.ring, m.full, m.empty);
+    }
+    return;
+  }
+  if (warp == pl.nwc + 1) {  // storer: horizontal tiles' g and dw (in place over dh and the taps)
+    if (lane == 0) {
+      const int slots[4] = {R_DH, R_WL, R_WM, R_WR};
+      storer_loop<false>(A, m.ring, m.done, m.empty, 4, slots, true);
+    }
+    return;
+  }
+  const uint64_t pol_vout = policy_of(pl.pol[3]);
+  const int nthreads = pl.nwc * 32;
+  const int64_t W = A.p.W;
+  const XSrc xs = make_xsrc<T>(warp, pl.nwc, lane);
+  T* const gbase = static_cast<T*>(A.g);
+  T* const dwl = static_cast<T*>(A.p.dwl);
+  T* const dwm = static_cast<T*>(A.p.dwm);
+  T* const dwr = static_cast<T*>(A.p.dwr);
+  const float* const ckpt = A.p.ckpt;
+  const int64_t ckstride = A.p.H * A.p.W / C::KS;
+  int stage = 0, par = 0;
+  uint32_t phase = 0;
+  for (int64_t w = blockIdx.x; w < pl.nchains; w += gridDim.x) {
+    const Chain ch = make_chain<false>(A.p, pl, w);
+    const Lanes<T> ln = make_lanes<T, false>(pl, A.p, ch, warp, lane);
+    const bool hl0 = tap_on<T>(ln.s[0][0]), hr1 = tap_on<T>(ln.s[2][1]);
+    bool hl[kE], hrr[kE];
+#pragma unroll
+    for (int q = 0; q < kE; ++q) {
+      hl[q] = tap_on<T>(ln.s[0][q]);
+      hrr[q] = tap_on<T>(ln.s[2][q]);
+    }
+    const float* ckc = ckpt + ch.chain * ckstride;
+    const int r0 = ln.A + 2 * lane;                 // vertical: the lane's first position
+    const bool v_in = r0 >= 0 && r0 < ch.P;
+    // checkpoint h_{t0-1} of the half with first scan step t0 (0 at t0 = 0): loaded one half ahead
+    auto ck_load = [&](int t0, float (&o)[2]) {
+      o[0] = o[1] = 0.f;
+      if (t0 <= 0) return;
+      const float* row = ckc + static_cast<int64_t>(t0 / C::KS - 1) * ch.P;
+      if (ch.vert) {
+        if (v_in) {
+          const float2 u = __ldcg(reinterpret_cast<const float2*>(row + r0));
+          o[0] = u.x;
+          o[1] = u.y;
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < kE; ++q) {
+          const int r = ln.A + 32 * q + lane;
+          if (r >= 0 && r < ch.P) o[q] = __ldcg(row + r);
+        }
+      }
+    };
+    auto first_step = [&](int j, int half) {  // scan index of the half's first step
+      if (ch.vert) return j * C::K + half * C::KS;
+      const int cm = ch.rev ? 1 - half : half;
+      const int c0 = tile_start(ch, j, C::K) + cm * C::KS;
+      return ch.rev ? ch.L - c0 - C::KS : c0;
+    };
+    float ckn[2];
+    ck_load(first_step(ch.ntiles - 1, 1), ckn);
+    BwdState S;
+#pragma unroll
+    for (int e = 0; e < kE; ++e) S.ea[e] = S.eb[e] = S.ec[e] = 0.f;
+    for (int jj = 0; jj < ch.ntiles; ++jj) {
+      const int j = ch.ntiles - 1 - jj;
+      mbar_wait_sleep(smem_u32(&m.full[stage]), phase);
+      __syncwarp();
+      uint8_t* st = m.ring + static_cast<size_t>(stage) * pl.stage_bytes;
+#pragma unroll 1
+      for (int half = 1; half >= 0; --half) {
+        const int cm = ch.rev ? 1 - half : half;
+        const float ckc_[2] = {ckn[0], ckn[1]};
+        {  // the next half's checkpoint (reverse order), in flight while this half computes
+          const int jn = half == 1 ? j : j - 1, hn = half ^ 1;
+          if (jn >= 0) ck_load(first_step(jn, hn), ckn);
+        }
+        uint4 OG[kE], OL[kE], OM[kE], OR[kE];
+        const bool live = !pl.null_compute;
+        if (live) {
+          if (ch.vert) {
+            const int t0 = j * C::K + half * C::KS;
+            const int kkf = ch.rev ? C::K - 1 - half * C::KS : half * C::KS;  // tile row of the first step
+            const int vs = static_cast<int>(pl.vstep);
+            const int tl = t0 + C::KS - 1;
+            const int rowl = ch.rev ? ch.L - 1 - tl : tl;
+            rc_half_vert<T, kPre>(ln, st + ln.voff + kkf * vs, ch.rev ? -vs : vs,
+                                  ln.vout + static_cast<int64_t>(rowl) * W, ch.rev ? W : -W, S, pol_vout, gbase, dwl,
+                                  dwm, dwr, hl0, hr1, ckc_);
+          } else {
+            if (ch.rev) rc_half_horiz<T, kPre, true>(ln, st, cm, lane, S, ckc_, hl, hrr, OG, OL, OM, OR);
+            else rc_half_horiz<T, kPre, false>(ln, st, cm, lane, S, ckc_, hl, hrr, OG, OL, OM, OR);
+          }
+        }
+        edge_publish(m.edge + 0 * kXArr + par * kEdgeW * kXRow, warp, lane, ch.vert, S.ea);
+        edge_publish(m.edge + 1 * kXArr + par * kEdgeW * kXRow, warp, lane, ch.vert, S.eb);
+        edge_publish(m.edge + 2 * kXArr + par * kEdgeW * kXRow, warp, lane, ch.vert, S.ec);
+        named_bar(kBarEdge, nthreads);  // edges published; every warp has read this half's input rows
+        edge_reload(m.edge + 0 * kXArr + par * kEdgeW * kXRow, xs, ch.vert, S.ea);
+        edge_reload(m.edge + 1 * kXArr + par * kEdgeW * kXRow, xs, ch.vert, S.eb);
+        edge_reload(m.edge + 2 * kXArr + par * kEdgeW * kXRow, xs, ch.vert, S.ec);
+        par ^= 1;
+        if (!ch.vert && live) {  // g and dw in place over this half's dh / tap chunks (owned rows)
+#pragma unroll
+          for (int q = 0; q < kE; ++q) {
+            if (!ln.own_h[q]) continue;
+            const uint32_t off = ln.hoff[q] ^ (static_cast<uint32_t>(cm) << 4);
+            *reinterpret_cast<uint4*>(st + R_DH * kTile + off) = OG[q];
+            *reinterpret_cast<uint4*>(st + R_WL * kTile + off) = OL[q];
+            *reinterpret_cast<uint4*>(st + R_WM * kTile + off) = OM[q];
+            *reinterpret_cast<uint4*>(st + R_WR * kTile + off) = OR[q];
+          }
+        }
+      }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&m.done[stage]));
+      if (++stage == pl.nstages) { stage = 0; phase ^= 1; }
+    }
+  }
+}
+
 template <typename T, int kPre, bool kLocal>
 __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_fused_kernel(const __grid_constant__ StreamArgs A) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -2012,7 +2342,7 @@ __device__ __forceinline__ void sm_ld4v(const uint8_t* p, float (&v)[4]) {
 // Body of the TMA-staged output kernel: warps [0, ncons) consume, warp ncons produces, any other warp
 // returns at once. full[] / empty[] (A.nstages each, at the end of the ring) must be initialised with
 // counts 1 / ncons. Shared by bwd_out_tma_kernel and the second phase of bwd_one_kernel.
-template <typename T, bool kLocal, bool kVertDone, bool kMerged = false>
+template <typename T, bool kLocal, bool kVertDone, bool kMerged = false, bool kAllDone = false>
 __device__ __forceinline__ void out_tma_body(const OutArgs& A, uint8_t* ring, uint64_t* full, uint64_t* empty,
                                              int ncons) {
   constexpr int V = 4;
@@ -2046,7 +2376,7 @@ __device__ __forceinline__ void out_tma_body(const OutArgs& A, uint8_t* ring, ui
         for (int k = 0; k < D; ++k) {
           const int chain = static_cast<int>((static_cast<int64_t>(k) * p.B + b) * p.C + c);
           const uint32_t base = st + A.koff[k];
-          const bool skip_w = kVertDone && (p.dirbit[k] == GSPN_DIR_T2B || p.dirbit[k] == GSPN_DIR_B2T);
+          const bool skip_w = kAllDone || (kVertDone && (p.dirbit[k] == GSPN_DIR_T2B || p.dirbit[k] == GSPN_DIR_B2T));
           for (int bx = 0; bx < A.nbx; ++bx) {
             tma_load3(base + 0 * A.tile_rb + bx * box_rb, &A.g, bx * BX, i0, chain, fb, pol);
             tma_load3(base + 1 * A.tile_rb + bx * box_rb, &A.lam, bx * BX, i0, chain, fb, pol);
@@ -2119,7 +2449,7 @@ __device__ __forceinline__ void out_tma_body(const OutArgs& A, uint8_t* ring, ui
           for (int q = 0; q < V; ++q) du[q] = p.merge_scale * hv[q] * dyv[q];
           GVec<T, V>::store(static_cast<T*>(p.du) + off, du);
         }
-        if (kVertDone && vert) continue;
+        if ((kVertDone && vert) || kAllDone) continue;
         if (vert) {
           // h_{t-1}: image row i-1 (T2B) / i+1 (B2T) = halo row r / r+2; neighbours = columns j+-1
           const uint32_t ro = dir == GSPN_DIR_T2B ? 0u : 2u * rowb;
@@ -2253,6 +2583,40 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_one_kernel(const __
   fence_proxy_async_global();
   __syncthreads();
   out_tma_body<T, kLocal, true, kMerged>(O, m.ring, full, empty, pl.nwc);
+}
+
+// ---- Recompute-h backward in one launch (NEXT-3): bwd_rc_body (adjoint + tap gradients of both
+// orientations, h recomputed per half-tile from the forward's checkpoints) | grid barrier | dlam and dx.
+template <typename T, int kPre>
+__global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_rc_kernel(const __grid_constant__ OneArgs A) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const Plan& pl = A.s.plan;
+  const Smem m = carve(smem_raw, pl);
+  init_barriers<false>(m, pl);
+  bwd_rc_body<T, kPre>(A.s, m);
+  fence_proxy_async_global();
+  __syncthreads();
+  cooperative_groups::this_grid().sync();
+  const OutArgs& O = A.o;
+  uint64_t* full = reinterpret_cast<uint64_t*>(m.ring + static_cast<size_t>(O.nstages) * O.stage_bytes);
+  uint64_t* empty = full + O.nstages;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < pl.nstages; ++s) {
+      mbar_inval(smem_u32(&m.full[s]));
+      mbar_inval(smem_u32(&m.empty[s]));
+      mbar_inval(smem_u32(&m.done[s]));
+    }
+    for (int i = 0; i < 4; ++i) mbar_inval(smem_u32(&m.xb[i]));
+    for (int s = 0; s < O.nstages; ++s) {
+      mbar_init(smem_u32(&full[s]), 1);
+      mbar_init(smem_u32(&empty[s]), pl.nwc);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  fence_proxy_async();
+  fence_proxy_async_global();
+  __syncthreads();
+  out_tma_body<T, false, true, false, true>(O, m.ring, full, empty, pl.nwc);
 }
 
 // ---- Forward through the output gate + direction merge in one launch (NEXT-1, Eq. 2):
@@ -2759,10 +3123,13 @@ cudaError_t launch_fwd_stream(const ScanParams& p, gspn_dtype_t dt, cudaStream_t
   const bool xg = probe.cl == 1 && p.W % K == 0 && knob("GSPN_FWD_XG");
   const int nin = xg ? F_NIN - 1 : F_NIN;
   if (!make_plan(p, dt, nin, &A.plan)) return cudaSuccess;
+  if (p.ckpt != nullptr && (A.plan.cl > 1 || A.plan.npack > 1)) return cudaSuccess;  // checkpoints: see ckpt_eligible
+  A.plan.no_h = p.hout == nullptr ? 1 : 0;
   const void* ins_all[F_NIN] = {p.x, p.lam, p.wl, p.wm, p.wr};
   const int64_t planes_all[F_NIN] = {p.B * p.C, p.D * p.B * p.C, p.D * p.B * p.G, p.D * p.B * p.G, p.D * p.B * p.G};
   void* outs[1] = {p.hout};
-  if (!fill_maps(&A, ins_all + (xg ? 1 : 0), nin, outs, planes_all + (xg ? 1 : 0), p.D * p.B * p.C, 1, dt))
+  if (!fill_maps(&A, ins_all + (xg ? 1 : 0), nin, outs, planes_all + (xg ? 1 : 0), p.D * p.B * p.C,
+                 p.hout != nullptr ? 1 : 0, dt))
     return cudaSuccess;
   *handled = true;
   using BF = __nv_bfloat16;
@@ -2784,7 +3151,7 @@ cudaError_t launch_fwd_stream(const ScanParams& p, gspn_dtype_t dt, cudaStream_t
 // Plan + tensor maps of the TMA-staged output kernel for `ncons` consumer warps within `budget` bytes of
 // shared memory. Returns false if the shape does not fit.
 bool setup_out_tma(const ScanParams& p, const void* g, gspn_dtype_t dt, bool vert_done, int ncons, int budget,
-                   OutArgs& A, bool merged = false) {
+                   OutArgs& A, bool merged = false, bool all_done = false) {
   const bool grouped = p.G != p.C;
   memset(&A, 0, sizeof A);
   A.p = p;
@@ -2820,7 +3187,7 @@ bool setup_out_tma(const ScanParams& p, const void* g, gspn_dtype_t dt, bool ver
     if (merged) o += A.tile_rb;
     for (int k = 0; k < D; ++k) {
       A.koff[k] = o;
-      const bool vd = vert_done && (p.dirbit[k] == GSPN_DIR_T2B || p.dirbit[k] == GSPN_DIR_B2T);
+      const bool vd = all_done || (vert_done && (p.dirbit[k] == GSPN_DIR_T2B || p.dirbit[k] == GSPN_DIR_B2T));
       A.khoff[k] = o + (vd ? 2 : nrb_t) * A.tile_rb;
       o += vd ? 2 * A.tile_rb + (merged ? A.tile_h : 0) : A.per_k;
     }
@@ -2829,7 +3196,7 @@ bool setup_out_tma(const ScanParams& p, const void* g, gspn_dtype_t dt, bool ver
   A.tx = static_cast<uint32_t>(A.nbx * (es * A.BX * RB * (1 + nrb_t * D) + es * A.BX * (RB + 2) * D));  // payload
   if (vert_done) {  // vertical directions load g and lam only (+ the h halo when merged)
     int nv = 0;
-    for (int k = 0; k < D; ++k) nv += (p.dirbit[k] == GSPN_DIR_T2B || p.dirbit[k] == GSPN_DIR_B2T) ? 1 : 0;
+    for (int k = 0; k < D; ++k) nv += (all_done || p.dirbit[k] == GSPN_DIR_T2B || p.dirbit[k] == GSPN_DIR_B2T) ? 1 : 0;
     A.tx -= static_cast<uint32_t>(A.nbx * nv * (es * A.BX * RB * (nrb_t - 2) + (merged ? 0 : es * A.BX * (RB + 2))));
   }
   if (merged) A.tx += static_cast<uint32_t>(A.nbx * es * A.BX * RB);  // dy
@@ -2910,6 +3277,22 @@ cudaError_t launch_fwd_merged(const ScanParams& p, gspn_dtype_t dt, const void* 
   }
   *launches += 1;
   return e;
+}
+
+// NEXT-3 eligibility (forward checkpoints and the recompute backward must agree): per-channel weights,
+// unpacked, unsplit chains, H and W multiples of K, global scan, the backward plan (6 tiles) fits.
+bool ckpt_eligible(const ScanParams& p, gspn_dtype_t dt) {
+  if (p.G != p.C || p.kchunk > 0) return false;
+  const int K = 32 / (dt == GSPN_BF16 ? 2 : 4);
+  if (p.H % K != 0 || p.W % K != 0) return false;
+  Plan pl;
+  if (!make_plan(p, dt, R_NIN, &pl)) return false;
+  return pl.cl == 1 && pl.npack == 1;
+}
+
+size_t ckpt_floats(const ScanParams& p, gspn_dtype_t dt) {
+  const int KS = 16 / (dt == GSPN_BF16 ? 2 : 4);
+  return static_cast<size_t>(p.D * p.B * p.C) * static_cast<size_t>(p.H * p.W / KS);
 }
 
 // TMA-staged output kernel. Returns false if the shape does not fit (caller falls back).
@@ -2996,6 +3379,41 @@ cudaError_t launch_dx(const ScanParams& p, const void* g, cudaStream_t s) {
     default: bwd_dx_kernel<T, 4><<<b, 256, 0, s>>>(x, lam, gt, dl, dx, N, nv); break;
   }
   return cudaGetLastError();
+}
+
+// Recompute-h backward, one cooperative launch. Returns false (nothing launched) if not eligible.
+bool launch_bwd_recompute(const ScanParams& p0, gspn_dtype_t dt, cudaStream_t s, int* launches, cudaError_t* err) {
+  if (!ckpt_eligible(p0, dt)) return false;
+  std::unique_ptr<OneArgs> one(new OneArgs());
+  StreamArgs& A = one->s;
+  memset(&A, 0, sizeof A);
+  A.p = p0;
+  ScanParams& p = A.p;
+  if (!make_plan(p, dt, R_NIN, &A.plan)) return false;
+  Plan& pl = A.plan;
+  const WsLayout l = ws_layout(p.B, p.C, p.H, p.W, p.D, dt);
+  if (p.ws == nullptr || p.ws_bytes < l.total || p.ckpt == nullptr) return false;
+  A.g = static_cast<char*>(p.ws) + l.g;
+  const int64_t nc = p.D * p.B * p.C;
+  const void* ins[R_NIN] = {p.dh, p.wl, p.wm, p.wr, p.x, p.lam};
+  const int64_t in_planes[R_NIN] = {nc, nc, nc, nc, p.B * p.C, nc};
+  void* outs[4] = {A.g, p.dwl, p.dwm, p.dwr};
+  if (!fill_maps(&A, ins, R_NIN, outs, in_planes, nc, 4, dt)) return false;
+  if (!setup_out_tma(p, A.g, dt, true, pl.nwc, smem_optin() - 1024 - 256, one->o, false, true)) return false;
+  const int mode = norm_mode(p, pl);
+  using BF = __nv_bfloat16;
+  cudaError_t e;
+  if (dt == GSPN_BF16)
+    e = mode == kNormPre ? launch_one(bwd_rc_kernel<BF, kNormPre>, *one, s)
+        : mode == kNormClamp ? launch_one(bwd_rc_kernel<BF, kNormClamp>, *one, s)
+                             : launch_one(bwd_rc_kernel<BF, kNormFull>, *one, s);
+  else
+    e = mode == kNormPre ? launch_one(bwd_rc_kernel<float, kNormPre>, *one, s)
+        : mode == kNormClamp ? launch_one(bwd_rc_kernel<float, kNormClamp>, *one, s)
+                             : launch_one(bwd_rc_kernel<float, kNormFull>, *one, s);
+  *launches += 1;
+  *err = e;
+  return true;
 }
 
 // Fused backward for per-channel weights on unpacked, unsplit chains (the bench's config 4 shape):

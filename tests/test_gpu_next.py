@@ -520,3 +520,74 @@ def test_fwd_merged_parity(case, mean, keep_h):
     check("fwd_merged", "y", from_torch(y), oracle.merge_fwd(h_ref, uf, mean), tol, per_slab=False)
     if keep_h:
         check("fwd_merged", "h", from_torch(h), h_ref, tol)
+
+
+# ------------------------------------------------------------------- NEXT-3 recompute-h backward
+
+# (B, C, G, H, W, dirs, dtype, fwd path, bwd path): checkpointed shapes (unpacked, unsplit, H and W multiples
+# of the 32-byte tile) and the fallbacks (grouped, packed small planes, P-split)
+RECOMPUTE_CASES = [
+    (1, 2, 2, 512, 512, 0xF, "bf16", "stream-ckpt", "stream-recompute"),
+    (1, 2, 2, 320, 288, 0xF, "bf16", "stream-ckpt", "stream-recompute"),
+    (2, 2, 2, 264, 272, 0xF, "f32", "stream-ckpt", "stream-recompute"),
+    (1, 3, 3, 288, 320, 0x5, "bf16", "stream-ckpt", "stream-recompute"),
+    (1, 2, 2, 272, 288, 0xA, "f32", "stream-ckpt", "stream-recompute"),
+    (2, 4, 2, 40, 56, 0xF, "bf16", "ckpt-deferred", "recompute-unfused"),
+    (2, 4, 4, 56, 56, 0xF, "bf16", "ckpt-deferred", "recompute-unfused"),
+    (1, 2, 2, 24, 1000, 0xF, "bf16", "ckpt-deferred", "recompute-unfused"),
+]
+
+
+@pytest.mark.parametrize("case", RECOMPUTE_CASES, ids=lambda c: "B{}C{}G{}H{}W{}d{:x}{}".format(*c[:7]))
+def test_recompute_bwd_parity(case):
+    """gspn_fwd_ckpt (checkpoints, no h) -> gspn_bwd_recompute vs the oracle backward on the oracle's own
+    UNROUNDED h: the recompute sees h in fp32, so even bf16 dw is held to the unrounded reference (cf. R18)."""
+    import torch
+
+    B, C, G, H, W, dirs, dt, fpath, bpath = case
+    cfg = small_config(B, C, G, H, W, dirs, dt, cfg_id=611)
+    inp = host_inputs(cfg)
+    f = {n: v[1] for n, v in inp.items()}
+    dev = _dev()
+    t = {n: to_torch(v[0], dt, dev) for n, v in inp.items()}
+    a = (t["x"], t["w_l"], t["w_m"], t["w_r"], t["lam"])
+    ckpt, _ = gspn.fwd_ckpt(*a, dirs, G)
+    assert gspn.last_path() == fpath, gspn.last_path()
+    grads = gspn.bwd_recompute(*a, ckpt, t["dh"], dirs, G)
+    assert gspn.last_path() == bpath, gspn.last_path()
+    if bpath == "stream-recompute":
+        assert gspn.last_launch_count() == 1
+    h_ref = oracle.fwd(f["x"], f["w_l"], f["w_m"], f["w_r"], f["lam"], dirs, G)
+    g_ref = oracle.bwd(f["x"], f["w_l"], f["w_m"], f["w_r"], f["lam"], h_ref, f["dh"], dirs, G)
+    tol = TOL[dt]
+    for name, got, ref in zip(("dx", "dw_l", "dw_m", "dw_r", "dlam"), grads, g_ref):
+        check("recompute_bwd", name, from_torch(got), ref, tol)
+    # the checkpointing forward computes the same h as gspn_fwd (when it is kept)
+    ck2, hk = gspn.fwd_ckpt(*a, dirs, G, keep_h=True)
+    h0 = gspn.fwd(*a, dirs, G)
+    assert torch.equal(hk, h0)
+
+
+def test_recompute_dw_error_at_l2048():
+    """dw at L = 2048 (H = 2048, W = 512, vertical directions: P = 512 fits one CTA) through the saved-h
+    backward and through the recompute backward, both against the oracle on its own unrounded h; the
+    recompute path sees fp32 h, so its bf16 dw error must not exceed the saved-h path's."""
+    B, C, G, H, W, dirs, dt = 1, 2, 2, 2048, 512, 0x3, "bf16"
+    cfg = small_config(B, C, G, H, W, dirs, dt, cfg_id=612)
+    inp = host_inputs(cfg)
+    f = {n: v[1] for n, v in inp.items()}
+    dev = _dev()
+    t = {n: to_torch(v[0], dt, dev) for n, v in inp.items()}
+    a = (t["x"], t["w_l"], t["w_m"], t["w_r"], t["lam"])
+    h = gspn.fwd(*a, dirs, G)
+    g_saved = gspn.bwd(*a, h, t["dh"], dirs, G)
+    ckpt, _ = gspn.fwd_ckpt(*a, dirs, G)
+    g_rc = gspn.bwd_recompute(*a, ckpt, t["dh"], dirs, G)
+    assert gspn.last_path() == "stream-recompute"
+    h_ref = oracle.fwd(f["x"], f["w_l"], f["w_m"], f["w_r"], f["lam"], dirs, G, threads=oracle.default_threads())
+    g_ref = oracle.bwd(f["x"], f["w_l"], f["w_m"], f["w_r"], f["lam"], h_ref, f["dh"], dirs, G,
+                       threads=oracle.default_threads())
+    for i, name in ((1, "dw_l"), (2, "dw_m"), (3, "dw_r")):
+        e_saved = check("L2048_saved_h", name, from_torch(g_saved[i]), g_ref[i], TOL[dt])
+        e_rc = check("L2048_recompute", name, from_torch(g_rc[i]), g_ref[i], TOL[dt])
+        assert e_rc <= e_saved * 1.05, (name, e_rc, e_saved)
