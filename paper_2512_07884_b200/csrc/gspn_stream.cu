@@ -1644,15 +1644,21 @@ __device__ __forceinline__ void rc_half_vert(const Lanes<T>& ln, const uint8_t* 
 template <typename T> struct PkAcc;
 template <> struct PkAcc<__nv_bfloat16> {
   uint32_t w[4];
-  __device__ __forceinline__ void put(int i, float v) {  // i compile-time after unrolling
-    const uint32_t b = static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(v)));
-    w[i >> 1] = (i & 1) ? ((w[i >> 1] & 0xFFFFu) | (b << 16)) : ((w[i >> 1] & 0xFFFF0000u) | b);
+  float pend;  // the first element of a pair, until its partner arrives (elements come pairwise, either order)
+  // i compile-time after unrolling; `first`: i is the first of its pair to be produced
+  __device__ __forceinline__ void put(int i, float v, bool first) {
+    if (first) {
+      pend = v;
+    } else {
+      const float lo = (i & 1) ? pend : v, hi = (i & 1) ? v : pend;
+      w[i >> 1] = pack_bf16x2(lo, hi);  // one cvt.rn.bf16x2 per pair
+    }
   }
   __device__ __forceinline__ uint4 get() const { return make_uint4(w[0], w[1], w[2], w[3]); }
 };
 template <> struct PkAcc<float> {
   uint32_t w[4];
-  __device__ __forceinline__ void put(int i, float v) { w[i] = __float_as_uint(v); }
+  __device__ __forceinline__ void put(int i, float v, bool) { w[i] = __float_as_uint(v); }
   __device__ __forceinline__ uint4 get() const { return make_uint4(w[0], w[1], w[2], w[3]); }
 };
 
@@ -1703,10 +1709,11 @@ __device__ __forceinline__ void rc_half_horiz(const Lanes<T>& ln, const uint8_t*
       const float g = bwd_math<kPre>(hget<T>(DH[q], i), l, m, r, nr[q], nl[q], S.ea[q], S.eb[q], S.ec[q]);
       float ol, om, orr;
       dw_math<kPre>(g, l, m, r, hlo[q], hr[ss][q], hhi[q], ol, om, orr);
-      ag[q].put(i, g);
-      al[q].put(i, hl[q] ? ol : 0.f);
-      am[q].put(i, om);
-      ar[q].put(i, hrr[q] ? orr : 0.f);
+      const bool first = kRev ? (i & 1) == 0 : (i & 1) == 1;  // ss descends: i descends (L2R) / ascends (R2L)
+      ag[q].put(i, g, first);
+      al[q].put(i, hl[q] ? ol : 0.f, first);
+      am[q].put(i, om, first);
+      ar[q].put(i, hrr[q] ? orr : 0.f, first);
     }
   }
 #pragma unroll
