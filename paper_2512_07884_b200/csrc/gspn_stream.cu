@@ -1360,7 +1360,92 @@ __device__ __forceinline__ void dw_half_horiz(const Lanes<T>& ln, uint8_t* st, i
   }
 }
 
-template <typename T, int kPre, bool kMerged = false>
+// Pack helpers for the horizontal outputs built one element per step.
+template <typename T> struct PkAcc;
+template <> struct PkAcc<__nv_bfloat16> {
+  uint32_t w[4];
+  float pend;  // the first element of a pair, until its partner arrives (elements come pairwise, either order)
+  // i compile-time after unrolling; `first`: i is the first of its pair to be produced
+  __device__ __forceinline__ void put(int i, float v, bool first) {
+    if (first) {
+      pend = v;
+    } else {
+      const float lo = (i & 1) ? pend : v, hi = (i & 1) ? v : pend;
+      w[i >> 1] = pack_bf16x2(lo, hi);  // one cvt.rn.bf16x2 per pair
+    }
+  }
+  __device__ __forceinline__ uint4 get() const { return make_uint4(w[0], w[1], w[2], w[3]); }
+};
+template <> struct PkAcc<float> {
+  uint32_t w[4];
+  __device__ __forceinline__ void put(int i, float v, bool) { w[i] = __float_as_uint(v); }
+  __device__ __forceinline__ uint4 get() const { return make_uint4(w[0], w[1], w[2], w[3]); }
+};
+
+// Horizontal half of the fused backward with the tap gradients in the recurrence (kHF): h_{t-1} of the
+// lane's rows is the previous element of the lane's own h chunk; at the chunk edge it is the edge element
+// of the neighbouring chunk towards step t-1 -- the h tile holds 48-byte rows, the tile's two chunks plus
+// that neighbour (L2R: [chunk -1 | 0 | 1], R2L: [0 | 1 | +1]). The neighbouring rows' h_{t-1} come by
+// shuffle; g and dw are packed per step and written in place after the half's barrier (the storer sends
+// the 4 tiles).
+template <typename T, int kPre, bool kRev, bool kMerged = false>
+__device__ __forceinline__ void bwd_half_horiz_hf(const Lanes<T>& ln, const uint8_t* st, int cm, int lane, BwdState& S,
+                                                  const bool (&hl)[kE], const bool (&hrr)[kE], uint4 (&OG)[kE],
+                                                  uint4 (&OL)[kE], uint4 (&OM)[kE], uint4 (&OR)[kE], float ms = 1.f) {
+  constexpr int KS = Cfg<T>::KS;
+  uint4 DH[kE], WL[kE], WM[kE], WR[kE], HP[kE], DY[kE];
+  float HE[kE];  // h_{t-1} of the half's first scan step (edge element of the neighbouring chunk)
+  const uint32_t own = static_cast<uint32_t>(kRev ? cm : cm + 1) * 16u;
+  const uint32_t edge = static_cast<uint32_t>(kRev ? cm + 1 : cm) * 16u + (kRev ? 0u : KS - 1u) * sizeof(T);
+#pragma unroll
+  for (int q = 0; q < kE; ++q) {
+    const uint32_t off = ln.hoff[q] ^ (static_cast<uint32_t>(cm) << 4);
+    const uint32_t hrow = (ln.hoff[q] >> 5) * 48u;
+    DH[q] = *reinterpret_cast<const uint4*>(st + B_DH * kTile + off);
+    WL[q] = *reinterpret_cast<const uint4*>(st + B_WL * kTile + off);
+    WM[q] = *reinterpret_cast<const uint4*>(st + B_WM * kTile + off);
+    WR[q] = *reinterpret_cast<const uint4*>(st + B_WR * kTile + off);
+    HP[q] = *reinterpret_cast<const uint4*>(st + B_H0 * kTile + hrow + own);
+    HE[q] = to_f(*reinterpret_cast<const T*>(st + B_H0 * kTile + hrow + edge));
+    if constexpr (kMerged) DY[q] = *reinterpret_cast<const uint4*>(st + B_DY * kTile + off);
+  }
+  PkAcc<T> ag[kE], al[kE], am[kE], ar[kE];
+#pragma unroll
+  for (int ss = KS - 1; ss >= 0; --ss) {  // scan order descending
+    const int i = kRev ? KS - 1 - ss : ss;
+    float nr[kE], nl[kE], hv[kE], hlo[kE], hhi[kE];
+    slot_hi(S.ea, lane, nr);
+    slot_lo(S.ec, lane, nl);
+#pragma unroll
+    for (int q = 0; q < kE; ++q)  // h_{t-1} at the lane's rows
+      hv[q] = kRev ? (i < KS - 1 ? hget<T>(HP[q], i + 1) : HE[q]) : (i > 0 ? hget<T>(HP[q], i - 1) : HE[q]);
+    slot_lo(hv, lane, hlo);
+    slot_hi(hv, lane, hhi);
+    const bool first = kRev ? (i & 1) == 0 : (i & 1) == 1;
+#pragma unroll
+    for (int q = 0; q < kE; ++q) {
+      const float l = hget_tap<T>(WL[q], i, ln.s[0][q]), m = hget_tap<T>(WM[q], i, ln.s[1][q]);
+      const float r = hget_tap<T>(WR[q], i, ln.s[2][q]);
+      const float dh = kMerged ? ms * hget<T>(DH[q], i) * hget<T>(DY[q], i) : hget<T>(DH[q], i);
+      const float g = bwd_math<kPre>(dh, l, m, r, nr[q], nl[q], S.ea[q], S.eb[q], S.ec[q]);
+      float ol, om, orr;
+      dw_math<kPre>(g, l, m, r, hlo[q], hv[q], hhi[q], ol, om, orr);
+      ag[q].put(i, g, first);
+      al[q].put(i, hl[q] ? ol : 0.f, first);
+      am[q].put(i, om, first);
+      ar[q].put(i, hrr[q] ? orr : 0.f, first);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < kE; ++q) {
+    OG[q] = ag[q].get();
+    OL[q] = al[q].get();
+    OM[q] = am[q].get();
+    OR[q] = ar[q].get();
+  }
+}
+
+template <typename T, int kPre, bool kMerged = false, bool kHF = false>
 __device__ void producer_fused(const StreamArgs& A, uint8_t* ring, uint64_t* full, uint64_t* empty) {
   const Plan& pl = A.plan;
   const uint64_t pol_vin = policy_of(pl.pol[1]);
@@ -1400,6 +1485,16 @@ __device__ void producer_fused(const StreamArgs& A, uint8_t* ring, uint64_t* ful
           for (int q = 0; q < pl.nbw; ++q)
             tma_load3(dst + q * pl.K * pl.bw * pl.es, &A.in[0][B_H0], q * pl.bw, sh, chain, fb, pol);
         }
+      } else if (kHF) {  // h of the tile's columns plus the 16-byte chunk towards step t-1 (48-byte rows, no
+                         // swizzle): TMA needs a 16-byte aligned inner coordinate, so the box cannot start one
+                         // column earlier; L2R [s0 - KS, s0 + K), R2L [s0, s0 + K + KS) (edges: zero fill = h_{-1})
+        const int sh = ch.rev ? s0 : s0 - pl.K / 2;
+        if (pl.npack > 1) {
+          tma_load3(st + B_H0 * pl.tile_bytes, &A.in[1][B_H0], sh, 0, chain, fb, pol);
+        } else {
+          for (int q = 0; q < pl.nbh; ++q)
+            tma_load3(st + B_H0 * pl.tile_bytes + q * pl.bh * 48, &A.in[1][B_H0], sh, q * pl.bh, chain, fb, pol);
+        }
       } else if (pl.fuse_h) {  // this tile's columns and the neighbouring tile towards step t-1 (zero fill)
         const int sn = ch.rev ? s0 + pl.K : s0 - pl.K;
         for (int q = 0; q < pl.nbh; ++q) {
@@ -1429,7 +1524,7 @@ __device__ void producer_fused(const StreamArgs& A, uint8_t* ring, uint64_t* ful
 
 // Body of the fused backward recurrence (every role returns from here when its work is done); the
 // barriers of `m` must be initialised. Shared by bwd_fused_kernel and the single-launch bwd_one_kernel.
-template <typename T, int kPre, bool kLocal, bool kMerged = false>
+template <typename T, int kPre, bool kLocal, bool kMerged = false, bool kHF = false>
 __device__ __forceinline__ void bwd_fused_body(const StreamArgs& A, const Smem& m) {
   using C = Cfg<T>;
   const Plan& pl = A.plan;
@@ -1438,14 +1533,14 @@ __device__ __forceinline__ void bwd_fused_body(const StreamArgs& A, const Smem& 
     if (lane == 0) {
       for (int o = 0; o < 2; ++o)
         for (int t = 0; t < B_H1; ++t) asm volatile("prefetch.tensormap [%0];" ::"l"(&A.in[o][t]) : "memory");
-      producer_fused<T, kPre, kMerged>(A, m.ring, m.full, m.empty);
+      producer_fused<T, kPre, kMerged, kHF>(A, m.ring, m.full, m.empty);
     }
     return;
   }
   if (warp == pl.nwc + 1) {  // storer: horizontal tiles' g and dw_l/m/r (written over dh, w_l, w_m, w_r)
     if (lane == 0) {
       const int slots[4] = {B_DH, B_WL, B_WM, B_WR};
-      storer_loop<false>(A, m.ring, m.done, m.empty, pl.fuse_h ? 4 : 1, slots, true);
+      storer_loop<false>(A, m.ring, m.done, m.empty, (pl.fuse_h || kHF) ? 4 : 1, slots, true);
     }
     return;
   }
@@ -1491,7 +1586,7 @@ __device__ __forceinline__ void bwd_fused_body(const StreamArgs& A, const Smem& 
       uint8_t* st = m.ring + static_cast<size_t>(stage) * pl.stage_bytes;
 #pragma unroll 1
       for (int half = 1; half >= 0; --half) {
-        uint4 OG[kE];
+        uint4 OG[kE], OL[kE], OM[kE], OR[kE];
         const int cm = ch.rev ? 1 - half : half;
         const bool live = !pl.null_compute && !half_outside_k<C::K>(ch, j, half, cm);
         if (live) {
@@ -1510,8 +1605,13 @@ __device__ __forceinline__ void bwd_fused_body(const StreamArgs& A, const Smem& 
             if constexpr (kLocal)
               rm = reset_bits(tile_start(ch, j, C::K) + cm * C::KS + (ch.rev ? 0 : C::KS - 1), ch.rev ? 1 : -1,
                               !ch.rev, kchunk, C::KS);
-            if (ch.rev) bwd_half_horiz<T, kPre, true, kLocal, kMerged>(ln, st, cm, lane, S, OG, rm, mscale);
-            else bwd_half_horiz<T, kPre, false, kLocal, kMerged>(ln, st, cm, lane, S, OG, rm, mscale);
+            if constexpr (kHF) {
+              if (ch.rev) bwd_half_horiz_hf<T, kPre, true, kMerged>(ln, st, cm, lane, S, hl, hr, OG, OL, OM, OR, mscale);
+              else bwd_half_horiz_hf<T, kPre, false, kMerged>(ln, st, cm, lane, S, hl, hr, OG, OL, OM, OR, mscale);
+            } else {
+              if (ch.rev) bwd_half_horiz<T, kPre, true, kLocal, kMerged>(ln, st, cm, lane, S, OG, rm, mscale);
+              else bwd_half_horiz<T, kPre, false, kLocal, kMerged>(ln, st, cm, lane, S, OG, rm, mscale);
+            }
           }
         }
         edge_publish(m.edge + 0 * kXArr + par * kEdgeW * kXRow, warp, lane, ch.vert, S.ea);
@@ -1522,7 +1622,17 @@ __device__ __forceinline__ void bwd_fused_body(const StreamArgs& A, const Smem& 
         edge_reload(m.edge + 1 * kXArr + par * kEdgeW * kXRow, xs, ch.vert, S.eb);
         edge_reload(m.edge + 2 * kXArr + par * kEdgeW * kXRow, xs, ch.vert, S.ec);
         par ^= 1;
-        if (!ch.vert && live) {
+        if (!ch.vert && live && kHF) {  // g and dw in place over dh / w chunks (storer: 4 tiles)
+#pragma unroll
+          for (int q = 0; q < kE; ++q) {
+            if (!ln.own_h[q]) continue;
+            const uint32_t off = ln.hoff[q] ^ (static_cast<uint32_t>(cm) << 4);
+            *reinterpret_cast<uint4*>(st + B_DH * kTile + off) = OG[q];
+            *reinterpret_cast<uint4*>(st + B_WL * kTile + off) = OL[q];
+            *reinterpret_cast<uint4*>(st + B_WM * kTile + off) = OM[q];
+            *reinterpret_cast<uint4*>(st + B_WR * kTile + off) = OR[q];
+          }
+        } else if (!ch.vert && live) {
           if (pl.fuse_h) {  // tap gradients; g and dw in place over this half's dh / w chunks
             if (ch.rev) dw_half_horiz<T, kPre, true>(ln, st, cm, OG, hrow, hl, hr);
             else dw_half_horiz<T, kPre, false>(ln, st, cm, OG, hrow, hl, hr);
@@ -1639,28 +1749,6 @@ __device__ __forceinline__ void rc_half_vert(const Lanes<T>& ln, const uint8_t* 
     gofs += gstep;
   }
 }
-
-// Pack helpers for the horizontal outputs built one element per step.
-template <typename T> struct PkAcc;
-template <> struct PkAcc<__nv_bfloat16> {
-  uint32_t w[4];
-  float pend;  // the first element of a pair, until its partner arrives (elements come pairwise, either order)
-  // i compile-time after unrolling; `first`: i is the first of its pair to be produced
-  __device__ __forceinline__ void put(int i, float v, bool first) {
-    if (first) {
-      pend = v;
-    } else {
-      const float lo = (i & 1) ? pend : v, hi = (i & 1) ? v : pend;
-      w[i >> 1] = pack_bf16x2(lo, hi);  // one cvt.rn.bf16x2 per pair
-    }
-  }
-  __device__ __forceinline__ uint4 get() const { return make_uint4(w[0], w[1], w[2], w[3]); }
-};
-template <> struct PkAcc<float> {
-  uint32_t w[4];
-  __device__ __forceinline__ void put(int i, float v, bool) { w[i] = __float_as_uint(v); }
-  __device__ __forceinline__ uint4 get() const { return make_uint4(w[0], w[1], w[2], w[3]); }
-};
 
 template <typename T, int kPre, bool kRev>
 __device__ __forceinline__ void rc_half_horiz(const Lanes<T>& ln, const uint8_t* st, int cm, int lane, BwdState& S,
@@ -2548,7 +2636,7 @@ struct OneArgs {
 __device__ __forceinline__ void mbar_inval(uint32_t bar) {
   asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
 }
-template <typename T, int kPre, bool kLocal, bool kMerged = false>
+template <typename T, int kPre, bool kLocal, bool kMerged = false, bool kHF = false>
 __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_one_kernel(const __grid_constant__ OneArgs A) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const Plan& pl = A.s.plan;
@@ -2563,7 +2651,7 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_one_kernel(const __
   }
   init_barriers<false>(m, pl);
   if (A.s.ready != nullptr) cooperative_groups::this_grid().sync();  // counters zeroed before any chain ends
-  bwd_fused_body<T, kPre, kLocal, kMerged>(A.s, m);
+  bwd_fused_body<T, kPre, kLocal, kMerged, kHF>(A.s, m);
   // Grid-wide barrier between the phases (default). With readiness counters (experiments: GSPN_PLANE_READY)
   // a unit's producer instead waits until the D chains of its plane have published their g (storer:
   // completed stores, gpu-scope fence, counter), so CTAs that finish phase 1 early start phase 2.
@@ -2589,7 +2677,7 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_one_kernel(const __
   fence_proxy_async();        // phase-1 generic writes of the ring before phase-2 TMA writes into it
   fence_proxy_async_global();
   __syncthreads();
-  out_tma_body<T, kLocal, true, kMerged>(O, m.ring, full, empty, pl.nwc);
+  out_tma_body<T, kLocal, true, kMerged, kHF>(O, m.ring, full, empty, pl.nwc);
 }
 
 // ---- Recompute-h backward in one launch (NEXT-3): bwd_rc_body (adjoint + tap gradients of both
@@ -3441,7 +3529,16 @@ bool launch_bwd_fused(const ScanParams& p0, gspn_dtype_t dt, cudaStream_t s, int
   const bool merged = p.dy != nullptr;  // gspn_bwd_merged: dh = s u dy on the fly, du written (single launch only)
   const bool fuse_h = !merged && knob("GSPN_FUSE_H") != nullptr;
   if (merged && (p.kchunk > 0 || knob("GSPN_TWO_LAUNCH"))) return false;
-  if (!make_plan(p, dt, fuse_h ? B_NINF : B_NIN + 1 + (merged ? 1 : 0), &A.plan)) return false;
+  // GSPN_HF (experiments): horizontal chains form their tap gradients in the recurrence too (kHF), from an
+  // h tile with 48-byte rows (the tile's columns + one chunk towards step t-1); the output phase then forms
+  // only dlam and dx. ~12% fewer algorithmic bytes, but measured slower than the hybrid (config 4 bwd
+  // 6.90-6.94 vs 6.84-6.87 ms, config 2 0.64 vs 0.57 ms; profiles/r2_notes.md): the 6-slot stage leaves two
+  // stages in flight and the storer's four tile stores hold each stage longer. Direct 16-byte stores from
+  // registers instead of the in-place + TMA store: 11.5 ms (scattered partial-sector writes).
+  // (kHF: the h tile has 48-byte rows = 1.5 slots; the stage holds 6 slots, merged would need 7: hybrid)
+  bool hf = !fuse_h && !merged && p.kchunk == 0 && !knob("GSPN_TWO_LAUNCH") && knob("GSPN_HF");
+  if (hf && (!make_plan(p, dt, B_NIN + 2, &A.plan) || A.plan.nstages < 2 || A.plan.cl > 1)) hf = false;
+  if (!hf && !make_plan(p, dt, fuse_h ? B_NINF : B_NIN + 1 + (merged ? 1 : 0), &A.plan)) return false;
   Plan& pl = A.plan;
   const bool local = p.kchunk > 0;
   if (pl.cl > 1 || (fuse_h && (pl.npack > 1 || local)) || (knob("GSPN_NOFUSE_PACKED") && pl.npack > 1)) return false;
@@ -3449,7 +3546,7 @@ bool launch_bwd_fused(const ScanParams& p0, gspn_dtype_t dt, cudaStream_t s, int
   // make_plan counted pl.nin tiles per stage for both orientations: vertical loads B_NIN + 1 (no B_H1),
   // horizontal B_NIN (dh, w) unless fully fused; merged: + dy for both
   pl.tx_v = pl.tx_v / pl.nin * (B_NIN + 1 + (merged ? 1 : 0));
-  if (!fuse_h) pl.tx_h = pl.tx_h / pl.nin * (B_NIN + (merged ? 1 : 0));
+  if (!fuse_h) pl.tx_h = pl.tx_h / pl.nin * (B_NIN + (merged ? 1 : 0)) + (hf ? pl.tx_h / pl.nin / 2 * 3 : 0);
   const WsLayout l = ws_layout(p.B, p.C, p.H, p.W, p.D, dt);
   if (p.ws == nullptr || p.ws_bytes < l.total) return false;
   A.g = static_cast<char*>(p.ws) + l.g;
@@ -3457,14 +3554,17 @@ bool launch_bwd_fused(const ScanParams& p0, gspn_dtype_t dt, cudaStream_t s, int
   const void* ins[B_NINF] = {p.dh, p.wl, p.wm, p.wr, p.h, merged ? p.dy : p.h};
   const int64_t in_planes[B_NINF] = {nc, nc, nc, nc, nc, merged ? p.B * p.C : nc};
   void* outs[4] = {A.g, p.dwl, p.dwm, p.dwr};
-  if (!fill_maps(&A, ins, pl.nin, outs, in_planes, nc, pl.fuse_h ? 4 : 1, dt)) return false;
+  if (!fill_maps(&A, ins, pl.nin, outs, in_planes, nc, (pl.fuse_h || hf) ? 4 : 1, dt)) return false;
+  if (hf && !(pl.npack > 1 ? encode(&A.in[1][B_H0], p.h, dt, p.W, p.H, nc, pl.K + pl.K / 2, p.H, false, pl.npack)
+                           : encode(&A.in[1][B_H0], p.h, dt, p.W, p.H, nc, pl.K + pl.K / 2, pl.bh, false)))
+    return false;  // h with 48-byte rows (the tile's columns + one chunk towards step t-1)
   cudaError_t e0 = cudaSuccess;
   if (!pl.fuse_h && !launch_out_tma(p, A.g, dt, s, &e0, true, true)) return false;  // output kernel must fit
   const int mode = norm_mode(p, pl);
   if (!pl.fuse_h && !knob("GSPN_TWO_LAUNCH")) {  // single launch: recurrence | grid barrier | outputs
     std::unique_ptr<OneArgs> one(new OneArgs());
     one->s = A;
-    if (setup_out_tma(p, A.g, dt, true, pl.nwc, smem_optin() - 1024 - 256, one->o, merged)) {
+    if (setup_out_tma(p, A.g, dt, true, pl.nwc, smem_optin() - 1024 - 256, one->o, merged, hf)) {
       // Per-plane readiness instead of the grid-wide barrier (experiments only): measured slower, 7.03-7.08
       // vs 6.78-6.82 ms on config 4 (3 same-box pairs; profiles/r2_notes.md) -- early phase-2 units compete
       // with the last chains for bandwidth and every chain pays a gpu-scope fence.
@@ -3475,7 +3575,16 @@ bool launch_bwd_fused(const ScanParams& p0, gspn_dtype_t dt, cudaStream_t s, int
       }
       cudaError_t e;
       using BF = __nv_bfloat16;
-      if (merged) {
+      if (hf) {
+        if (dt == GSPN_BF16)
+          e = mode == kNormPre ? launch_one(bwd_one_kernel<BF, kNormPre, false, false, true>, *one, s)
+              : mode == kNormClamp ? launch_one(bwd_one_kernel<BF, kNormClamp, false, false, true>, *one, s)
+                                   : launch_one(bwd_one_kernel<BF, kNormFull, false, false, true>, *one, s);
+        else
+          e = mode == kNormPre ? launch_one(bwd_one_kernel<float, kNormPre, false, false, true>, *one, s)
+              : mode == kNormClamp ? launch_one(bwd_one_kernel<float, kNormClamp, false, false, true>, *one, s)
+                                   : launch_one(bwd_one_kernel<float, kNormFull, false, false, true>, *one, s);
+      } else if (merged) {
         if (dt == GSPN_BF16)
           e = mode == kNormPre ? launch_one(bwd_one_kernel<BF, kNormPre, false, true>, *one, s)
               : mode == kNormClamp ? launch_one(bwd_one_kernel<BF, kNormClamp, false, true>, *one, s)

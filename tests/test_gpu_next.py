@@ -591,3 +591,20 @@ def test_recompute_dw_error_at_l2048():
         e_saved = check("L2048_saved_h", name, from_torch(g_saved[i]), g_ref[i], TOL[dt])
         e_rc = check("L2048_recompute", name, from_torch(g_rc[i]), g_ref[i], TOL[dt])
         assert e_rc <= e_saved * 1.05, (name, e_rc, e_saved)
+
+
+def test_experiment_hf_backward_matches_default():
+    """The kHF backward (GSPN_EXPERIMENTS + GSPN_HF: horizontal dw in the recurrence; measured slower, kept
+    as an experiment) agrees with the default hybrid within the dtype tolerance -- packed fp32, unpacked
+    bf16 with a ragged P, config-4-like, grouped-free 3-channel shapes. Runs in a child process: the
+    experiment knobs are read from the environment once per process."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "hf_cmp.py"), "1,8,8,16,16,15,f32",
+                        "1,2,2,300,264,15,bf16", "2,2,2,512,512,15,bf16", "1,3,3,200,136,15,bf16"],
+                       capture_output=True, text=True, timeout=600, cwd=root)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr[-2000:]
