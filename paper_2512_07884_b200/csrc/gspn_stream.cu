@@ -2415,9 +2415,20 @@ struct OutArgs {
   int64_t nunits;
   const unsigned* ready;                             // single launch: wait for D chains of the unit's plane
   int npack;
+  // wide rows (W > 256, W % 256 == 0): 4D maps {256, W / 256, H, planes}, so ONE TMA box brings whole image
+  // rows (the tile is [rows][W]) instead of W / 256 boxes per tensor; BX = W, nbx = 1 for the consumers
+  int wide;
 };
 
 constexpr int kOutConsumers = 16;
+
+// Rows [row, row + box rows) of one plane of an output-kernel tensor: box bx of a 3D map, or (wide) all of
+// the row in one 4D box.
+__device__ __forceinline__ void out_load(const OutArgs& A, uint32_t dst, const CUtensorMap* map, int bx, int row,
+                                         int plane, uint32_t bar, uint64_t pol) {
+  if (A.wide) tma_load4(dst, map, 0, 0, row, plane, bar, pol);
+  else tma_load3(dst, map, bx * A.BX, row, plane, bar, pol);
+}
 
 // 4 consecutive elements at a shared-memory address (8- or 16-byte aligned).
 template <typename T>
@@ -2464,24 +2475,24 @@ __device__ __forceinline__ void out_tma_body(const OutArgs& A, uint8_t* ring, ui
         mbar_arrive_tx(fb, A.tx);
         const uint32_t st = smem_u32(ring + static_cast<size_t>(stage) * A.stage_bytes);
         const uint32_t box_rb = A.box_rb, box_h = A.box_h;
-        for (int bx = 0; bx < A.nbx; ++bx) tma_load3(st + bx * box_rb, &A.x, bx * BX, i0, static_cast<int>(bc), fb, pol);
+        for (int bx = 0; bx < A.nbx; ++bx) out_load(A, st + bx * box_rb, &A.x, bx, i0, static_cast<int>(bc), fb, pol);
         if constexpr (kMerged)
           for (int bx = 0; bx < A.nbx; ++bx)
-            tma_load3(st + A.dyoff + bx * box_rb, &A.dy, bx * BX, i0, static_cast<int>(bc), fb, pol);
+            out_load(A, st + A.dyoff + bx * box_rb, &A.dy, bx, i0, static_cast<int>(bc), fb, pol);
         for (int k = 0; k < D; ++k) {
           const int chain = static_cast<int>((static_cast<int64_t>(k) * p.B + b) * p.C + c);
           const uint32_t base = st + A.koff[k];
           const bool skip_w = kAllDone || (kVertDone && (p.dirbit[k] == GSPN_DIR_T2B || p.dirbit[k] == GSPN_DIR_B2T));
           for (int bx = 0; bx < A.nbx; ++bx) {
-            tma_load3(base + 0 * A.tile_rb + bx * box_rb, &A.g, bx * BX, i0, chain, fb, pol);
-            tma_load3(base + 1 * A.tile_rb + bx * box_rb, &A.lam, bx * BX, i0, chain, fb, pol);
+            out_load(A, base + 0 * A.tile_rb + bx * box_rb, &A.g, bx, i0, chain, fb, pol);
+            out_load(A, base + 1 * A.tile_rb + bx * box_rb, &A.lam, bx, i0, chain, fb, pol);
             if (kMerged && skip_w)  // du = s h dy needs h at the pixel rows: the halo tile
-              tma_load3(st + A.khoff[k] + bx * A.box_h, &A.h, bx * BX, i0 - 1, chain, fb, policy_of(1));
+              out_load(A, st + A.khoff[k] + bx * A.box_h, &A.h, bx, i0 - 1, chain, fb, policy_of(1));
             if (skip_w) continue;
-            tma_load3(base + 2 * A.tile_rb + bx * box_rb, &A.wl, bx * BX, i0, chain, fb, pol);
-            tma_load3(base + 3 * A.tile_rb + bx * box_rb, &A.wm, bx * BX, i0, chain, fb, pol);
-            tma_load3(base + 4 * A.tile_rb + bx * box_rb, &A.wr, bx * BX, i0, chain, fb, pol);
-            tma_load3(base + 5 * A.tile_rb + bx * box_h, &A.h, bx * BX, i0 - 1, chain, fb, policy_of(1));
+            out_load(A, base + 2 * A.tile_rb + bx * box_rb, &A.wl, bx, i0, chain, fb, pol);
+            out_load(A, base + 3 * A.tile_rb + bx * box_rb, &A.wm, bx, i0, chain, fb, pol);
+            out_load(A, base + 4 * A.tile_rb + bx * box_rb, &A.wr, bx, i0, chain, fb, pol);
+            out_load(A, base + 5 * A.tile_rb + bx * box_h, &A.h, bx, i0 - 1, chain, fb, policy_of(1));
           }
         }
         if (++stage == A.nstages) { stage = 0; phase ^= 1; }
@@ -2802,14 +2813,14 @@ __global__ void __launch_bounds__((kOutConsumers + 1) * 32, 1) bwd_out_grp_tma_k
           const uint32_t fb = smem_u32(&full[stage]);
           mbar_arrive_tx(fb, A.tx);
           const uint32_t st = smem_u32(ring + static_cast<size_t>(stage) * A.stage_bytes);
-          for (int bx = 0; bx < A.nbx; ++bx) tma_load3(st + bx * A.box_rb, &A.x, bx * BX, i0, static_cast<int>(bc), fb, pol);
+          for (int bx = 0; bx < A.nbx; ++bx) out_load(A, st + bx * A.box_rb, &A.x, bx, i0, static_cast<int>(bc), fb, pol);
           for (int k = 0; k < D; ++k) {
             const int chain = static_cast<int>(static_cast<int64_t>(k) * p.B * p.C + bc);
             const uint32_t base = st + A.tile_rb + k * A.per_k;
             for (int bx = 0; bx < A.nbx; ++bx) {
-              tma_load3(base + bx * A.box_rb, &A.g, bx * BX, i0, chain, fb, pol);
-              tma_load3(base + A.tile_rb + bx * A.box_rb, &A.lam, bx * BX, i0, chain, fb, pol);
-              tma_load3(base + 2 * A.tile_rb + bx * A.box_h, &A.h, bx * BX, i0 - 1, chain, fb, policy_of(1));
+              out_load(A, base + bx * A.box_rb, &A.g, bx, i0, chain, fb, pol);
+              out_load(A, base + A.tile_rb + bx * A.box_rb, &A.lam, bx, i0, chain, fb, pol);
+              out_load(A, base + 2 * A.tile_rb + bx * A.box_h, &A.h, bx, i0 - 1, chain, fb, policy_of(1));
             }
           }
           if (++stage == A.nstages) { stage = 0; phase ^= 1; }
@@ -2991,6 +3002,24 @@ bool encode(CUtensorMap* m, const void* base, gspn_dtype_t dt, int64_t W, int64_
                   const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                   swizzle32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE,
                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// Output-kernel maps: 3D {W, H, planes} with box {bx, rows, 1}, or (wide) 4D {256, W / 256, H, planes} with box
+// {256, W / 256, rows, 1}: whole rows in one box, landing as [rows][W].
+bool encode_rows(CUtensorMap* m, const void* base, gspn_dtype_t dt, int64_t W, int64_t H, int64_t planes, int bx,
+                 int rows, bool wide) {
+  if (!wide) return encode(m, base, dt, W, H, planes, bx, rows, false);
+  auto fn = get_encode();
+  if (!fn) return false;
+  const size_t s = dt == GSPN_BF16 ? 2 : 4;
+  cuuint64_t dims[4] = {256u, static_cast<cuuint64_t>(W / 256), static_cast<cuuint64_t>(H), static_cast<cuuint64_t>(planes)};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(256 * s), static_cast<cuuint64_t>(W * s), static_cast<cuuint64_t>(W * H * s)};
+  cuuint32_t box[4] = {256u, static_cast<cuuint32_t>(W / 256), static_cast<cuuint32_t>(rows), 1u};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = fn(m, dt == GSPN_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+                  const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
@@ -3251,7 +3280,8 @@ bool setup_out_tma(const ScanParams& p, const void* g, gspn_dtype_t dt, bool ver
   memset(&A, 0, sizeof A);
   A.p = p;
   const int es = dt == GSPN_BF16 ? 2 : 4;
-  A.BX = static_cast<int>(std::min<int64_t>(p.W, 256));
+  A.wide = (p.W > 256 && p.W % 256 == 0 && p.W / 256 <= 256 && !knob("GSPN_OUT_NARROW")) ? 1 : 0;
+  A.BX = A.wide ? static_cast<int>(p.W) : static_cast<int>(std::min<int64_t>(p.W, 256));
   A.nbx = static_cast<int>((p.W + A.BX - 1) / A.BX);
   const int D = static_cast<int>(p.D);
   auto pad = [](int64_t v) { return (v + 127) / 128 * 128; };
@@ -3299,14 +3329,15 @@ bool setup_out_tma(const ScanParams& p, const void* g, gspn_dtype_t dt, bool ver
   A.nrb = static_cast<int>((p.H + RB - 1) / RB);
   A.nunits = (grouped ? p.B * p.G : p.B * p.C) * A.nrb;
   const int64_t nc = p.D * p.B * p.C;
-  bool ok = encode(&A.x, p.x, dt, p.W, p.H, p.B * p.C, A.BX, RB, false) &&
-            encode(&A.g, g, dt, p.W, p.H, nc, A.BX, RB, false) &&
-            encode(&A.lam, p.lam, dt, p.W, p.H, nc, A.BX, RB, false) &&
-            encode(&A.wl, p.wl, dt, p.W, p.H, nc, A.BX, RB, false) &&
-            encode(&A.wm, p.wm, dt, p.W, p.H, nc, A.BX, RB, false) &&
-            encode(&A.wr, p.wr, dt, p.W, p.H, nc, A.BX, RB, false) &&
-            encode(&A.h, p.h, dt, p.W, p.H, nc, A.BX, RB + 2, false);
-  if (ok && merged) ok = encode(&A.dy, p.dy, dt, p.W, p.H, p.B * p.C, A.BX, RB, false);
+  const bool wd = A.wide != 0;
+  bool ok = encode_rows(&A.x, p.x, dt, p.W, p.H, p.B * p.C, A.BX, RB, wd) &&
+            encode_rows(&A.g, g, dt, p.W, p.H, nc, A.BX, RB, wd) &&
+            encode_rows(&A.lam, p.lam, dt, p.W, p.H, nc, A.BX, RB, wd) &&
+            encode_rows(&A.wl, p.wl, dt, p.W, p.H, nc, A.BX, RB, wd) &&
+            encode_rows(&A.wm, p.wm, dt, p.W, p.H, nc, A.BX, RB, wd) &&
+            encode_rows(&A.wr, p.wr, dt, p.W, p.H, nc, A.BX, RB, wd) &&
+            encode_rows(&A.h, p.h, dt, p.W, p.H, nc, A.BX, RB + 2, wd);
+  if (ok && merged) ok = encode_rows(&A.dy, p.dy, dt, p.W, p.H, p.B * p.C, A.BX, RB, wd);
   return ok;
 }
 
