@@ -26,6 +26,11 @@ cudaError_t launch_bwd_small(const ScanParams& p, gspn_dtype_t dt, cudaStream_t 
 // dw formed in-kernel (no workspace, one launch). small_grouped(): eligible (fits shared memory).
 bool small_grouped(const ScanParams& p, gspn_dtype_t dt);
 cudaError_t launch_bwd_small_grouped(const ScanParams& p, gspn_dtype_t dt, cudaStream_t s, int* launches);
+// Grouped small planes on thread-block clusters (gspn_small_cl.cu): one CTA per (unit, direction), channels
+// streamed through bulk-copied batch buffers; taken by the two launchers above when eligible.
+bool small_cl_eligible(const ScanParams& p, gspn_dtype_t dt, bool bwd);
+cudaError_t launch_fwd_small_cl(const ScanParams& p, gspn_dtype_t dt, cudaStream_t s, int* launches);
+cudaError_t launch_bwd_small_cl(const ScanParams& p, gspn_dtype_t dt, cudaStream_t s, int* launches);
 
 // Fast TMA-streaming path (gspn_stream.cu). *handled = false when the shape is not eligible.
 // *path = "stream" or "stream-cluster" (P-split over a thread-block cluster)

@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "gspn_common.cuh"
 #include "gspn_internal.h"
@@ -24,6 +25,12 @@ namespace gspn {
 namespace {
 
 constexpr int kSmallMax = 32;
+
+// Experiment knob (A/B tooling): read only when GSPN_EXPERIMENTS is set.
+bool knob_set(const char* name) {
+  static const bool on = getenv("GSPN_EXPERIMENTS") != nullptr;
+  return on && getenv(name) != nullptr;
+}
 
 // Copy n elements (one plane) global -> shared; 16-byte vectors when both sides allow it.
 template <typename T>
@@ -621,6 +628,7 @@ bool small_grouped(const ScanParams& p, gspn_dtype_t dt) {
 }
 
 cudaError_t launch_fwd_small(const ScanParams& p, gspn_dtype_t dt, cudaStream_t s, int* launches) {
+  if (small_cl_eligible(p, dt, false) && !knob_set("GSPN_NO_SMALL_CL")) return launch_fwd_small_cl(p, dt, s, launches);
   *launches += 1;
   const bool local = p.kchunk > 0;
   if (small_grouped(p, dt)) {
@@ -641,6 +649,7 @@ cudaError_t launch_fwd_small(const ScanParams& p, gspn_dtype_t dt, cudaStream_t 
 
 // Grouped weights: the whole backward (dw included) in one launch, no workspace.
 cudaError_t launch_bwd_small_grouped(const ScanParams& p, gspn_dtype_t dt, cudaStream_t s, int* launches) {
+  if (small_cl_eligible(p, dt, true) && !knob_set("GSPN_NO_SMALL_CL")) return launch_bwd_small_cl(p, dt, s, launches);
   *launches += 1;
   const bool local = p.kchunk > 0;
   const int es = dt == GSPN_BF16 ? 2 : 4, nw = grp_warps(p, es, true);
