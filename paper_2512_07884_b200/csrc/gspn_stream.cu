@@ -114,6 +114,7 @@ struct Plan {
   int null_compute;    // experiments only (GSPN_NULL=1): consumers skip the arithmetic
   int fuse_h;          // fused backward: horizontal chains also form dw in the recurrence (else g only)
   int no_h;            // forward with checkpoints only (gspn_fwd_ckpt with h = NULL): h is not stored
+  int nseg, kt;        // GSPN-local segment items: segments per chain slot, tiles per segment (nseg = 1: off)
 };
 
 struct alignas(64) StreamArgs {
@@ -189,6 +190,7 @@ struct Chain {
   int64_t bc, chain, wplane;  // first plane of the (pack of) chain(s): x, lam/h/dh, w
   int L, P, ntiles;
   int psub, nvalid;           // positions per chain; chains of the pack that exist
+  int j0, j1;                 // scan-order tiles of this work item: [j0, j1) (a GSPN-local segment, or all)
 };
 
 // Work items are handed out round-robin over the persistent grid (CTAs, or clusters in P-split mode).
@@ -211,14 +213,18 @@ __device__ __forceinline__ int tile_base(const Plan& pl) {
 }
 
 template <bool kCl>
-__device__ __forceinline__ Chain make_chain(const ScanParams& p, const Plan& pl, int64_t w) {
+__device__ __forceinline__ Chain make_chain(const ScanParams& p, const Plan& pl, int64_t wi) {
   Chain ch;
+  // GSPN-local segments as work items (the GSPN-2 grid over (chunk, n, c)): item wi is
+  // segment wi % nseg of chain slot wi / nseg (nseg = 1: one item per chain)
+  const int64_t w = wi / pl.nseg;
+  const int seg = static_cast<int>(wi - w * pl.nseg);
   const int64_t bc = (w / p.D) * pl.npack;
   // Round i of the persistent grid covers slots [i G, (i+1) G): whole planes when D divides G. The
   // direction is rotated by i so every CTA cycles through all D directions (vertical and horizontal
   // chains run at different speeds; a fixed direction per CTA would leave the fast ones idle).
   const int64_t G = work_stride<kCl>(pl);
-  ch.k = static_cast<int>(G % p.D == 0 ? (w + w / G) % p.D : w % p.D);
+  ch.k = static_cast<int>(pl.nseg == 1 && G % p.D == 0 ? (w + w / G) % p.D : w % p.D);
   const uint32_t dir = p.dirbit[ch.k];
   ch.vert = (dir == GSPN_DIR_T2B) || (dir == GSPN_DIR_B2T);
   ch.rev = (dir == GSPN_DIR_B2T) || (dir == GSPN_DIR_R2L);
@@ -231,6 +237,13 @@ __device__ __forceinline__ Chain make_chain(const ScanParams& p, const Plan& pl,
   ch.P = ch.psub * pl.npack;
   ch.nvalid = static_cast<int>(pl.nbc - bc < pl.npack ? pl.nbc - bc : pl.npack);
   ch.ntiles = (ch.L + pl.K - 1) / pl.K;
+  ch.j0 = 0;
+  ch.j1 = ch.ntiles;
+  if (pl.nseg > 1) {  // canonical tiles [c0, c1) of segment seg; reversed directions walk them backwards
+    const int c0 = min(seg * pl.kt, ch.ntiles), c1 = min((seg + 1) * pl.kt, ch.ntiles);
+    ch.j0 = ch.rev ? ch.ntiles - c1 : c0;
+    ch.j1 = ch.rev ? ch.ntiles - c0 : c1;
+  }
   return ch;
 }
 
@@ -285,8 +298,8 @@ __device__ void producer_loop(const StreamArgs& A, uint8_t* ring, uint64_t* full
   for (int64_t w = work_first<kCl>(pl); w < pl.nchains; w += work_stride<kCl>(pl)) {
     const Chain ch = make_chain<kCl>(A.p, pl, w);
     const int o = ch.vert ? 0 : 1;
-    for (int jj = 0; jj < ch.ntiles; ++jj) {
-      const int j = kBwd ? (ch.ntiles - 1 - jj) : jj;
+    for (int jj = 0; jj < ch.j1 - ch.j0; ++jj) {
+      const int j = kBwd ? (ch.j1 - 1 - jj) : (ch.j0 + jj);
       mbar_wait_sleep(smem_u32(&empty[stage]), phase ^ 1);
       const uint32_t fb = smem_u32(&full[stage]);
       mbar_arrive_tx(fb, ch.vert ? pl.tx_v : pl.tx_h);
@@ -328,8 +341,8 @@ __device__ void storer_loop(const StreamArgs& A, uint8_t* ring, uint64_t* done, 
   int64_t pending = -1;  // single-launch bwd: plane pack of the previous chain, published one chain later
   for (int64_t w = work_first<kCl>(pl); w < pl.nchains; w += work_stride<kCl>(pl)) {
     const Chain ch = make_chain<kCl>(A.p, pl, w);
-    for (int jj = 0; jj < ch.ntiles; ++jj) {
-      const int j = bwd ? (ch.ntiles - 1 - jj) : jj;
+    for (int jj = 0; jj < ch.j1 - ch.j0; ++jj) {
+      const int j = bwd ? (ch.j1 - 1 - jj) : (ch.j0 + jj);
       mbar_wait_sleep(smem_u32(&done[stage]), phase);
       if (ch.vert && A.ready != nullptr) bulk_commit();  // an empty group: one group per tile either way
       if (!ch.vert) {
@@ -359,7 +372,7 @@ __device__ void storer_loop(const StreamArgs& A, uint8_t* ring, uint64_t* done, 
     // but this chain's last 8 (one per tile) -- so the storer never waits for its own latest stores.
     if (A.ready != nullptr) {
       if (pending >= 0) {
-        if (ch.ntiles >= 8) bulk_wait_group8();
+        if (ch.j1 - ch.j0 >= 8) bulk_wait_group8();
         else bulk_wait_all();
         fence_acq_rel_gpu();  // the consumers' g stores (observed through `done`) are gpu-visible
         fence_proxy_async_global();
@@ -931,8 +944,8 @@ __device__ __forceinline__ void fwd_stream_body(const StreamArgs& A, const Smem&
     T* hout = pl.no_h ? nullptr : static_cast<T*>(A.p.hout) + ln.vout;
     float h[kE] = {0.f, 0.f};
     XPre<T> xcur;
-    if constexpr (kXG) x_fetch<T>(xcur, ln, ch, xg, 0, 0, W);
-    for (int j = 0; j < ch.ntiles; ++j) {
+    if constexpr (kXG) x_fetch<T>(xcur, ln, ch, xg, ch.j0, 0, W);
+    for (int j = ch.j0; j < ch.j1; ++j) {
       mbar_wait_sleep(smem_u32(&m.full[stage]), phase);
       __syncwarp();  // reconverge after the per-thread spin: the shuffles below need no collective fallback
       uint8_t* st = m.ring + static_cast<size_t>(stage) * pl.stage_bytes;
@@ -944,7 +957,7 @@ __device__ __forceinline__ void fwd_stream_body(const StreamArgs& A, const Smem&
         XPre<T> xnext;
         if constexpr (kXG) {  // the next half's x, loaded while this half computes
           const int jn = half == 0 ? j : j + 1, hn = half ^ 1;
-          if (jn < ch.ntiles) x_fetch<T>(xnext, ln, ch, xg, jn, hn, W);
+          if (jn < ch.j1) x_fetch<T>(xnext, ln, ch, xg, jn, hn, W);
         }
         if (live) {
           uint32_t rm = 0;
@@ -1152,8 +1165,8 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_stream_kernel(const
     BwdState S;
 #pragma unroll
     for (int e = 0; e < kE; ++e) S.ea[e] = S.eb[e] = S.ec[e] = 0.f;
-    for (int jj = 0; jj < ch.ntiles; ++jj) {
-      const int j = ch.ntiles - 1 - jj;
+    for (int jj = 0; jj < ch.j1 - ch.j0; ++jj) {
+      const int j = ch.j1 - 1 - jj;
       mbar_wait_sleep(smem_u32(&m.full[stage]), phase);
       __syncwarp();  // reconverge after the per-thread spin: the shuffles below need no collective fallback
       uint8_t* st = m.ring + static_cast<size_t>(stage) * pl.stage_bytes;
@@ -1455,8 +1468,8 @@ __device__ void producer_fused(const StreamArgs& A, uint8_t* ring, uint64_t* ful
   for (int64_t w = blockIdx.x; w < pl.nchains; w += gridDim.x) {
     const Chain ch = make_chain<false>(A.p, pl, w);
     const int chain = static_cast<int>(ch.chain);
-    for (int jj = 0; jj < ch.ntiles; ++jj) {
-      const int j = ch.ntiles - 1 - jj;
+    for (int jj = 0; jj < ch.j1 - ch.j0; ++jj) {
+      const int j = ch.j1 - 1 - jj;
       mbar_wait_sleep(smem_u32(&empty[stage]), phase ^ 1);
       const uint32_t fb = smem_u32(&full[stage]);
       mbar_arrive_tx(fb, ch.vert ? pl.tx_v : pl.tx_h);
@@ -1579,8 +1592,8 @@ __device__ __forceinline__ void bwd_fused_body(const StreamArgs& A, const Smem& 
     BwdState S;
 #pragma unroll
     for (int e = 0; e < kE; ++e) S.ea[e] = S.eb[e] = S.ec[e] = 0.f;
-    for (int jj = 0; jj < ch.ntiles; ++jj) {
-      const int j = ch.ntiles - 1 - jj;
+    for (int jj = 0; jj < ch.j1 - ch.j0; ++jj) {
+      const int j = ch.j1 - 1 - jj;
       mbar_wait_sleep(smem_u32(&m.full[stage]), phase);
       __syncwarp();
       uint8_t* st = m.ring + static_cast<size_t>(stage) * pl.stage_bytes;
@@ -1675,8 +1688,8 @@ __device__ void producer_rc(const StreamArgs& A, uint8_t* ring, uint64_t* full, 
   uint32_t phase = 0;
   for (int64_t w = blockIdx.x; w < pl.nchains; w += gridDim.x) {
     const Chain ch = make_chain<false>(A.p, pl, w);
-    for (int jj = 0; jj < ch.ntiles; ++jj) {
-      const int j = ch.ntiles - 1 - jj;
+    for (int jj = 0; jj < ch.j1 - ch.j0; ++jj) {
+      const int j = ch.j1 - 1 - jj;
       mbar_wait_sleep(smem_u32(&empty[stage]), phase ^ 1);
       const uint32_t fb = smem_u32(&full[stage]);
       mbar_arrive_tx(fb, ch.vert ? pl.tx_v : pl.tx_h);
@@ -1888,8 +1901,8 @@ __device__ __forceinline__ void bwd_rc_body(const StreamArgs& A, const Smem& m) 
     BwdState S;
 #pragma unroll
     for (int e = 0; e < kE; ++e) S.ea[e] = S.eb[e] = S.ec[e] = 0.f;
-    for (int jj = 0; jj < ch.ntiles; ++jj) {
-      const int j = ch.ntiles - 1 - jj;
+    for (int jj = 0; jj < ch.j1 - ch.j0; ++jj) {
+      const int j = ch.j1 - 1 - jj;
       mbar_wait_sleep(smem_u32(&m.full[stage]), phase);
       __syncwarp();
       uint8_t* st = m.ring + static_cast<size_t>(stage) * pl.stage_bytes;
@@ -3101,6 +3114,18 @@ bool make_plan(const ScanParams& p, gspn_dtype_t dt, int nin, Plan* pl) {
   if (ns < 2) return false;
   pl->nstages = ns;
   pl->nchains = p.D * ((pl->nbc + pl->npack - 1) / pl->npack);  // work items: packs of chains
+  // GSPN-local (kchunk > 0): each segment is an independent work item when segment boundaries fall on tile
+  // boundaries in scan order (kchunk, H and W multiples of K): more, shorter items for the persistent grid,
+  // bitwise the same arithmetic (a segment starts from h = 0 / g = 0 either way)
+  pl->nseg = 1;
+  pl->kt = 0;
+  if (p.kchunk > 0 && p.kchunk % pl->K == 0 && p.H % pl->K == 0 && p.W % pl->K == 0 && !knob("GSPN_NO_SEGITEMS") &&
+      !knob("GSPN_PLANE_READY")) {
+    const int64_t Lmax = std::max<int64_t>(p.H, p.W);
+    pl->nseg = static_cast<int>((Lmax + p.kchunk - 1) / p.kchunk);
+    pl->kt = static_cast<int>(p.kchunk / pl->K);
+    pl->nchains *= pl->nseg;
+  }
   pl->smem_bytes = 1024 + ns * pl->stage_bytes + kSmemTail;
   // L2 priorities (experiments: GSPN_POL="x,vin,hin,vout,hout,acc", each 0|1|2)
   static const int def_pol[6] = {1, 0, 2, 0, 1, 1};  // horizontal loads evict_last: +0.5 % (same-box A/B x3)

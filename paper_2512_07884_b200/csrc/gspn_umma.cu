@@ -20,6 +20,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -47,6 +48,8 @@ struct UmmaMixArgs {
   int MT, KC, NT, nstages, ntn;
   int64_t ntiles;
   uint32_t a_bytes, stage_bytes, o_bytes, tmem_cols, idesc;
+  int orows;  // rows of an output staging box / TMA store box: min(128, Co) rounded up to 8
+  int nob;    // output staging buffers (2 when they fit: a tile's stores overlap the next tile's drain)
 };
 
 // named barrier of the 4 epilogue warps
@@ -96,28 +99,13 @@ __global__ void __launch_bounds__(kMixThreads, 1) umma_mix_kernel(const __grid_c
   uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sa = base;                                   // weights: MT x KC chunks of [128 rows][128 B], swizzled
   uint8_t* ring = base + A.a_bytes;                     // B stages: NT/64 boxes of [64 rows][128 B]
-  uint8_t* ob = ring + static_cast<size_t>(A.nstages) * A.stage_bytes;  // output staging: MT x NT/64 boxes
-  uint64_t* full = reinterpret_cast<uint64_t*>(ob + A.o_bytes);
+  uint8_t* ob = ring + static_cast<size_t>(A.nstages) * A.stage_bytes;  // output staging: 2 x MT x NT/64 boxes
+  uint64_t* full = reinterpret_cast<uint64_t*>(ob + A.nob * A.o_bytes);
   uint64_t* empty = full + A.nstages;
   uint64_t* tfull = empty + A.nstages;  // [2] accumulator ready
   uint64_t* tempty = tfull + 2;         // [2] accumulator drained
   uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-  // weights -> K-major 128-byte-swizzled chunks: element (row m, k) of chunk (mt, kc) at byte
-  // (m / 8) 1024 + (m % 8) 128 + ((2 k / 16) ^ (m % 8)) 16 + (2 k) % 16; zero outside [Co) x [Ci)
-  const int nA = A.MT * A.KC * 128 * kKC;
-  for (int e = threadIdx.x; e < nA; e += blockDim.x) {
-    const int chunk = e / (128 * kKC), rem = e - chunk * 128 * kKC;
-    const int m = rem / kKC, k = rem - m * kKC;
-    const int mt = chunk / A.KC, kc = chunk - mt * A.KC;
-    const int o = mt * 128 + m, i = kc * kKC + k;
-    __nv_bfloat16 v = __float2bfloat16_rn(0.f);
-    if (o < A.Co && i < A.Ci) v = A.trans ? A.M[static_cast<int64_t>(i) * A.Co + o] : A.M[static_cast<int64_t>(o) * A.Ci + i];
-    const uint32_t byte = (m >> 3) * 1024u + (m & 7) * 128u + ((((2u * k) >> 4) ^ (m & 7)) << 4) + ((2u * k) & 15u);
-    *reinterpret_cast<__nv_bfloat16*>(sa + static_cast<size_t>(chunk) * kAChunk + byte) = v;
-  }
-  fence_proxy_async();  // generic-proxy weight writes -> visible to the tensor cores (async proxy)
   if (threadIdx.x == 0) {
     for (int s = 0; s < A.nstages; ++s) {
       mbar_init(smem_u32(&full[s]), 1);
@@ -139,6 +127,39 @@ __global__ void __launch_bounds__(kMixThreads, 1) umma_mix_kernel(const __grid_c
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
+  if (warp != 0) {
+    // weights -> K-major 128-byte-swizzled chunks: element (row m, k) of chunk (mt, kc) at byte
+    // (m / 8) 1024 + (m % 8) 128 + ((2 k / 16) ^ (m % 8)) 16 + (2 k) % 16; zero outside [Co) x [Ci). Staged by
+    // warps 1-5 while the producer already streams the first activation tiles.
+    const int nthr = blockDim.x - 32, tid = threadIdx.x - 32;
+    if (!A.trans && A.Ci % 8 == 0) {  // 8 consecutive k = one 16-byte piece on both sides
+      const int nv = A.MT * A.KC * 128 * (kKC / 8);
+      for (int e = tid; e < nv; e += nthr) {
+        const int chunk = e / (128 * (kKC / 8)), rem = e - chunk * 128 * (kKC / 8);
+        const int m = rem / (kKC / 8), k = (rem - m * (kKC / 8)) * 8;
+        const int mt = chunk / A.KC, kc = chunk - mt * A.KC;
+        const int o = mt * 128 + m, i = kc * kKC + k;
+        uint4 v = make_uint4(0u, 0u, 0u, 0u);
+        if (o < A.Co && i < A.Ci) v = __ldg(reinterpret_cast<const uint4*>(A.M + static_cast<int64_t>(o) * A.Ci + i));
+        const uint32_t byte = (m >> 3) * 1024u + (m & 7) * 128u + ((((2u * k) >> 4) ^ (m & 7)) << 4);
+        *reinterpret_cast<uint4*>(sa + static_cast<size_t>(chunk) * kAChunk + byte) = v;
+      }
+    } else {
+      const int nA = A.MT * A.KC * 128 * kKC;
+      for (int e = tid; e < nA; e += nthr) {
+        const int chunk = e / (128 * kKC), rem = e - chunk * 128 * kKC;
+        const int m = rem / kKC, k = rem - m * kKC;
+        const int mt = chunk / A.KC, kc = chunk - mt * A.KC;
+        const int o = mt * 128 + m, i = kc * kKC + k;
+        __nv_bfloat16 v = __float2bfloat16_rn(0.f);
+        if (o < A.Co && i < A.Ci) v = A.trans ? A.M[static_cast<int64_t>(i) * A.Co + o] : A.M[static_cast<int64_t>(o) * A.Ci + i];
+        const uint32_t byte = (m >> 3) * 1024u + (m & 7) * 128u + ((((2u * k) >> 4) ^ (m & 7)) << 4) + ((2u * k) & 15u);
+        *reinterpret_cast<__nv_bfloat16*>(sa + static_cast<size_t>(chunk) * kAChunk + byte) = v;
+      }
+    }
+    fence_proxy_async();  // generic-proxy weight writes -> visible to the tensor cores (async proxy)
+    asm volatile("bar.sync 2, %0;" ::"r"(nthr) : "memory");
+  }
 
   if (warp == 0) {  // ---- TMA producer
     if (lane == 0) {
@@ -199,14 +220,21 @@ __global__ void __launch_bounds__(kMixThreads, 1) umma_mix_kernel(const __grid_c
       const int b = static_cast<int>(t / A.ntn), px0 = static_cast<int>(t % A.ntn) * A.NT;
       mbar_wait(smem_u32(&tfull[buf]), static_cast<uint32_t>((it >> 1) & 1));
       tc_fence_after();
-      if (leader) bulk_wait_read0();  // the previous tile's stores have read the staging tile
+      if (leader) {  // the stores that last used this staging buffer have read it
+        if (A.nob == 2) bulk_wait_read1();
+        else bulk_wait_read0();
+      }
       epi_bar();
+      uint8_t* obuf = ob + static_cast<size_t>(A.nob == 2 ? buf : 0) * A.o_bytes;
+      const uint32_t obox = static_cast<uint32_t>(A.orows) * 128u;
       for (int mt = 0; mt < A.MT; ++mt) {
+        if (32 * sp >= A.orows) break;  // warp-uniform: rows past the store box (zero weights)
         const uint32_t tcol = tmem + (static_cast<uint32_t>(32 * sp) << 16) + static_cast<uint32_t>((buf * A.MT + mt) * A.NT);
         for (int c0 = 0; c0 < A.NT; c0 += 16) {
           uint32_t v[16];
           tmem_ld16(tcol + c0, v);
-          uint8_t* box = ob + static_cast<size_t>(mt * nbox + c0 / 64) * kAChunk + row * 128;
+          if (row >= A.orows) continue;
+          uint8_t* box = obuf + static_cast<size_t>(mt * nbox + c0 / 64) * obox + row * 128;
           const int q = (c0 & 63) >> 3;  // 16-byte chunk of the 128-byte row
           *reinterpret_cast<uint4*>(box + ((q ^ (row & 7)) << 4)) =
               make_uint4(pack2(v[0], v[1]), pack2(v[2], v[3]), pack2(v[4], v[5]), pack2(v[6], v[7]));
@@ -222,7 +250,7 @@ __global__ void __launch_bounds__(kMixThreads, 1) umma_mix_kernel(const __grid_c
       if (leader) {
         for (int mt = 0; mt < A.MT; ++mt)
           for (int j = 0; j < nbox; ++j)
-            tma_store3(&A.out_map, smem_u32(ob + static_cast<size_t>(mt * nbox + j) * kAChunk), px0 + 64 * j, mt * 128,
+            tma_store3(&A.out_map, smem_u32(obuf + static_cast<size_t>(mt * nbox + j) * obox), px0 + 64 * j, mt * 128,
                        b, policy_of(0));
         bulk_commit();
       }
@@ -362,16 +390,31 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
+int knob_mix_nt() {  // experiments only (GSPN_EXPERIMENTS + GSPN_MIX_NT=64|128|256)
+  static const int v = [] {
+    const char* e = getenv("GSPN_EXPERIMENTS") ? getenv("GSPN_MIX_NT") : nullptr;
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
 bool plan_mix(int64_t B, int64_t Ci, int64_t Co, int64_t HW, UmmaMixArgs& A) {
   if (Co > 512 || Ci > 4096 || HW % 8 != 0 || HW > (1ll << 31) - 1 || B > 65535) return false;
   A.MT = static_cast<int>((Co + 127) / 128);
   A.KC = static_cast<int>((Ci + kKC - 1) / kKC);
-  A.NT = A.MT <= 2 ? 128 : 64;  // TMEM: 2 MT NT <= 512 columns; staging + ring leave >= 4 B stages
+  // TMEM: 2 MT NT <= 512 columns (NT = 256 for MT = 1 measured the same as 128: knob GSPN_MIX_NT)
+  A.NT = knob_mix_nt() && A.MT == 1 ? knob_mix_nt() : A.MT <= 2 ? 128 : 64;
   A.a_bytes = static_cast<uint32_t>(A.MT * A.KC) * kAChunk;
   A.stage_bytes = static_cast<uint32_t>(A.NT / 64) * kBBox;
-  A.o_bytes = static_cast<uint32_t>(A.MT * (A.NT / 64)) * kAChunk;
+  A.orows = static_cast<int>(std::min<int64_t>(128, (Co + 7) / 8 * 8));
+  A.o_bytes = static_cast<uint32_t>(A.MT * (A.NT / 64) * A.orows) * 128u;  // one staging buffer (two are kept)
   const int budget = device_smem_optin() - 1024 - 256;
-  const int ns = (budget - static_cast<int>(A.a_bytes + A.o_bytes)) / static_cast<int>(A.stage_bytes);
+  A.nob = 2;
+  int ns = (budget - static_cast<int>(A.a_bytes + 2 * A.o_bytes)) / static_cast<int>(A.stage_bytes);
+  if (ns < 4) {  // keep the ring deep: one staging buffer
+    A.nob = 1;
+    ns = (budget - static_cast<int>(A.a_bytes + A.o_bytes)) / static_cast<int>(A.stage_bytes);
+  }
   if (ns < 2) return false;
   A.nstages = std::min(ns, 8);
   const int cols = 2 * A.MT * A.NT;
@@ -495,12 +538,12 @@ cudaError_t launch_umma_mix(const void* in, const void* M, void* out, int64_t B,
   {
     cuuint64_t odims[3] = {static_cast<cuuint64_t>(HW), static_cast<cuuint64_t>(Co), static_cast<cuuint64_t>(B)};
     cuuint64_t ostr[2] = {static_cast<cuuint64_t>(HW * 2), static_cast<cuuint64_t>(Co * HW * 2)};
-    cuuint32_t obox[3] = {64, 128, 1};
+    cuuint32_t obox[3] = {64, static_cast<cuuint32_t>(A.orows), 1};
     if (fn(&A.out_map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, out, odims, ostr, obox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorNotSupported;
   }
-  const uint32_t smem = 1024 + A.a_bytes + A.nstages * A.stage_bytes + A.o_bytes + (2 * A.nstages + 4) * 8 + 16;
+  const uint32_t smem = 1024 + A.a_bytes + A.nstages * A.stage_bytes + A.nob * A.o_bytes + (2 * A.nstages + 4) * 8 + 16;
   cudaError_t e = cudaFuncSetAttribute(umma_mix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
