@@ -29,7 +29,10 @@ def lib() -> ctypes.CDLL:
         if not os.path.exists(LIBGSPN):
             raise ImportError(f"libgspn.so not built ({LIBGSPN}); run __graft_entry__.build() or "
                               "python -m paper_2512_07884_b200.build")
-        L = ctypes.CDLL(LIBGSPN)
+        path = LIBGSPN
+        if os.environ.get("GSPN_EXPERIMENTS") and os.environ.get("GSPN_LIB"):  # A/B tooling only: another build
+            path = os.environ["GSPN_LIB"]
+        L = ctypes.CDLL(path)
         vp, i64, u32, sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint32, ctypes.c_size_t
         L.gspn_fwd.argtypes = [vp] * 6 + [i64] * 4 + [u32, i64, ctypes.c_int, u32, vp]
         L.gspn_fwd.restype = ctypes.c_int

@@ -2437,9 +2437,11 @@ constexpr int kOutConsumers = 16;
 
 // Rows [row, row + box rows) of one plane of an output-kernel tensor: box bx of a 3D map, or (wide) all of
 // the row in one 4D box.
+// kWide is a template parameter (a runtime branch here measured 13 % slower on config 2's output phase).
+template <bool kWide>
 __device__ __forceinline__ void out_load(const OutArgs& A, uint32_t dst, const CUtensorMap* map, int bx, int row,
                                          int plane, uint32_t bar, uint64_t pol) {
-  if (A.wide) tma_load4(dst, map, 0, 0, row, plane, bar, pol);
+  if constexpr (kWide) tma_load4(dst, map, 0, 0, row, plane, bar, pol);
   else tma_load3(dst, map, bx * A.BX, row, plane, bar, pol);
 }
 
@@ -2461,7 +2463,7 @@ __device__ __forceinline__ void sm_ld4v(const uint8_t* p, float (&v)[4]) {
 // Body of the TMA-staged output kernel: warps [0, ncons) consume, warp ncons produces, any other warp
 // returns at once. full[] / empty[] (A.nstages each, at the end of the ring) must be initialised with
 // counts 1 / ncons. Shared by bwd_out_tma_kernel and the second phase of bwd_one_kernel.
-template <typename T, bool kLocal, bool kVertDone, bool kMerged = false, bool kAllDone = false>
+template <typename T, bool kLocal, bool kVertDone, bool kMerged = false, bool kAllDone = false, bool kWide = false>
 __device__ __forceinline__ void out_tma_body(const OutArgs& A, uint8_t* ring, uint64_t* full, uint64_t* empty,
                                              int ncons) {
   constexpr int V = 4;
@@ -2488,24 +2490,24 @@ __device__ __forceinline__ void out_tma_body(const OutArgs& A, uint8_t* ring, ui
         mbar_arrive_tx(fb, A.tx);
         const uint32_t st = smem_u32(ring + static_cast<size_t>(stage) * A.stage_bytes);
         const uint32_t box_rb = A.box_rb, box_h = A.box_h;
-        for (int bx = 0; bx < A.nbx; ++bx) out_load(A, st + bx * box_rb, &A.x, bx, i0, static_cast<int>(bc), fb, pol);
+        for (int bx = 0; bx < A.nbx; ++bx) out_load<kWide>(A, st + bx * box_rb, &A.x, bx, i0, static_cast<int>(bc), fb, pol);
         if constexpr (kMerged)
           for (int bx = 0; bx < A.nbx; ++bx)
-            out_load(A, st + A.dyoff + bx * box_rb, &A.dy, bx, i0, static_cast<int>(bc), fb, pol);
+            out_load<kWide>(A, st + A.dyoff + bx * box_rb, &A.dy, bx, i0, static_cast<int>(bc), fb, pol);
         for (int k = 0; k < D; ++k) {
           const int chain = static_cast<int>((static_cast<int64_t>(k) * p.B + b) * p.C + c);
           const uint32_t base = st + A.koff[k];
           const bool skip_w = kAllDone || (kVertDone && (p.dirbit[k] == GSPN_DIR_T2B || p.dirbit[k] == GSPN_DIR_B2T));
           for (int bx = 0; bx < A.nbx; ++bx) {
-            out_load(A, base + 0 * A.tile_rb + bx * box_rb, &A.g, bx, i0, chain, fb, pol);
-            out_load(A, base + 1 * A.tile_rb + bx * box_rb, &A.lam, bx, i0, chain, fb, pol);
+            out_load<kWide>(A, base + 0 * A.tile_rb + bx * box_rb, &A.g, bx, i0, chain, fb, pol);
+            out_load<kWide>(A, base + 1 * A.tile_rb + bx * box_rb, &A.lam, bx, i0, chain, fb, pol);
             if (kMerged && skip_w)  // du = s h dy needs h at the pixel rows: the halo tile
-              out_load(A, st + A.khoff[k] + bx * A.box_h, &A.h, bx, i0 - 1, chain, fb, policy_of(1));
+              out_load<kWide>(A, st + A.khoff[k] + bx * A.box_h, &A.h, bx, i0 - 1, chain, fb, policy_of(1));
             if (skip_w) continue;
-            out_load(A, base + 2 * A.tile_rb + bx * box_rb, &A.wl, bx, i0, chain, fb, pol);
-            out_load(A, base + 3 * A.tile_rb + bx * box_rb, &A.wm, bx, i0, chain, fb, pol);
-            out_load(A, base + 4 * A.tile_rb + bx * box_rb, &A.wr, bx, i0, chain, fb, pol);
-            out_load(A, base + 5 * A.tile_rb + bx * box_h, &A.h, bx, i0 - 1, chain, fb, policy_of(1));
+            out_load<kWide>(A, base + 2 * A.tile_rb + bx * box_rb, &A.wl, bx, i0, chain, fb, pol);
+            out_load<kWide>(A, base + 3 * A.tile_rb + bx * box_rb, &A.wm, bx, i0, chain, fb, pol);
+            out_load<kWide>(A, base + 4 * A.tile_rb + bx * box_rb, &A.wr, bx, i0, chain, fb, pol);
+            out_load<kWide>(A, base + 5 * A.tile_rb + bx * box_h, &A.h, bx, i0 - 1, chain, fb, policy_of(1));
           }
         }
         if (++stage == A.nstages) { stage = 0; phase ^= 1; }
@@ -2660,7 +2662,7 @@ struct OneArgs {
 __device__ __forceinline__ void mbar_inval(uint32_t bar) {
   asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
 }
-template <typename T, int kPre, bool kLocal, bool kMerged = false, bool kHF = false>
+template <typename T, int kPre, bool kLocal, bool kMerged = false, bool kHF = false, bool kWide = false>
 __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_one_kernel(const __grid_constant__ OneArgs A) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const Plan& pl = A.s.plan;
@@ -2701,7 +2703,7 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_one_kernel(const __
   fence_proxy_async();        // phase-1 generic writes of the ring before phase-2 TMA writes into it
   fence_proxy_async_global();
   __syncthreads();
-  out_tma_body<T, kLocal, true, kMerged, kHF>(O, m.ring, full, empty, pl.nwc);
+  out_tma_body<T, kLocal, true, kMerged, kHF, kWide>(O, m.ring, full, empty, pl.nwc);
 }
 
 // ---- Recompute-h backward in one launch (NEXT-3): bwd_rc_body (adjoint + tap gradients of both
@@ -2792,7 +2794,7 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) fwd_one_kernel(const __
 // group per stage (x, and per direction g, lam and the h halo tile), every thread keeps the group sums
 // Da/Db/Dc of its 4-column chunk for all directions in registers, and after the group's last channel
 // reads w from global memory once and writes dw. One chunk per consumer thread (RB W / 4 <= 512).
-template <typename T, bool kLocal>
+template <typename T, bool kLocal, bool kWide = false>
 __global__ void __launch_bounds__((kOutConsumers + 1) * 32, 1) bwd_out_grp_tma_kernel(const __grid_constant__ OutArgs A) {
   constexpr int V = 4;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -2826,14 +2828,14 @@ __global__ void __launch_bounds__((kOutConsumers + 1) * 32, 1) bwd_out_grp_tma_k
           const uint32_t fb = smem_u32(&full[stage]);
           mbar_arrive_tx(fb, A.tx);
           const uint32_t st = smem_u32(ring + static_cast<size_t>(stage) * A.stage_bytes);
-          for (int bx = 0; bx < A.nbx; ++bx) out_load(A, st + bx * A.box_rb, &A.x, bx, i0, static_cast<int>(bc), fb, pol);
+          for (int bx = 0; bx < A.nbx; ++bx) out_load<kWide>(A, st + bx * A.box_rb, &A.x, bx, i0, static_cast<int>(bc), fb, pol);
           for (int k = 0; k < D; ++k) {
             const int chain = static_cast<int>(static_cast<int64_t>(k) * p.B * p.C + bc);
             const uint32_t base = st + A.tile_rb + k * A.per_k;
             for (int bx = 0; bx < A.nbx; ++bx) {
-              out_load(A, base + bx * A.box_rb, &A.g, bx, i0, chain, fb, pol);
-              out_load(A, base + A.tile_rb + bx * A.box_rb, &A.lam, bx, i0, chain, fb, pol);
-              out_load(A, base + 2 * A.tile_rb + bx * A.box_h, &A.h, bx, i0 - 1, chain, fb, policy_of(1));
+              out_load<kWide>(A, base + bx * A.box_rb, &A.g, bx, i0, chain, fb, pol);
+              out_load<kWide>(A, base + A.tile_rb + bx * A.box_rb, &A.lam, bx, i0, chain, fb, pol);
+              out_load<kWide>(A, base + 2 * A.tile_rb + bx * A.box_h, &A.h, bx, i0 - 1, chain, fb, policy_of(1));
             }
           }
           if (++stage == A.nstages) { stage = 0; phase ^= 1; }
@@ -3300,12 +3302,13 @@ cudaError_t launch_fwd_stream(const ScanParams& p, gspn_dtype_t dt, cudaStream_t
 // Plan + tensor maps of the TMA-staged output kernel for `ncons` consumer warps within `budget` bytes of
 // shared memory. Returns false if the shape does not fit.
 bool setup_out_tma(const ScanParams& p, const void* g, gspn_dtype_t dt, bool vert_done, int ncons, int budget,
-                   OutArgs& A, bool merged = false, bool all_done = false) {
+                   OutArgs& A, bool merged = false, bool all_done = false, bool allow_wide = false) {
   const bool grouped = p.G != p.C;
   memset(&A, 0, sizeof A);
   A.p = p;
   const int es = dt == GSPN_BF16 ? 2 : 4;
-  A.wide = (p.W > 256 && p.W % 256 == 0 && p.W / 256 <= 256 && !knob("GSPN_OUT_NARROW")) ? 1 : 0;
+  // only where the caller launches a kWide instantiation
+  A.wide = (allow_wide && p.W > 256 && p.W % 256 == 0 && p.W / 256 <= 256 && !knob("GSPN_OUT_NARROW")) ? 1 : 0;
   A.BX = A.wide ? static_cast<int>(p.W) : static_cast<int>(std::min<int64_t>(p.W, 256));
   A.nbx = static_cast<int>((p.W + A.BX - 1) / A.BX);
   const int D = static_cast<int>(p.D);
@@ -3453,17 +3456,19 @@ bool launch_out_tma(const ScanParams& p, const void* g, gspn_dtype_t dt, cudaStr
   if (knob("GSPN_OUT_REG")) return false;  // experiments: register-staged kernel
   std::unique_ptr<OutArgs> hold(new OutArgs());
   OutArgs& A = *hold;
-  if (!setup_out_tma(p, g, dt, vert_done, kOutConsumers, smem_optin() - 1024 - 256, A)) return false;
+  if (!setup_out_tma(p, g, dt, vert_done, kOutConsumers, smem_optin() - 1024 - 256, A, false, false, grouped)) return false;
   if (dry_run) return true;
   const uint32_t smem = out_tma_smem(A);
   using BF = __nv_bfloat16;
   auto kern = p.kchunk > 0
-      ? (grouped ? (dt == GSPN_BF16 ? bwd_out_grp_tma_kernel<BF, true> : bwd_out_grp_tma_kernel<float, true>)
+      ? (grouped ? (A.wide ? (dt == GSPN_BF16 ? bwd_out_grp_tma_kernel<BF, true, true> : bwd_out_grp_tma_kernel<float, true, true>)
+                           : (dt == GSPN_BF16 ? bwd_out_grp_tma_kernel<BF, true> : bwd_out_grp_tma_kernel<float, true>))
                  : vert_done ? (dt == GSPN_BF16 ? bwd_out_tma_kernel<BF, true, true>
                                                 : bwd_out_tma_kernel<float, true, true>)
                              : (dt == GSPN_BF16 ? bwd_out_tma_kernel<BF, true, false>
                                                 : bwd_out_tma_kernel<float, true, false>))
-      : (grouped ? (dt == GSPN_BF16 ? bwd_out_grp_tma_kernel<BF, false> : bwd_out_grp_tma_kernel<float, false>)
+      : (grouped ? (A.wide ? (dt == GSPN_BF16 ? bwd_out_grp_tma_kernel<BF, false, true> : bwd_out_grp_tma_kernel<float, false, true>)
+                           : (dt == GSPN_BF16 ? bwd_out_grp_tma_kernel<BF, false> : bwd_out_grp_tma_kernel<float, false>))
                  : vert_done ? (dt == GSPN_BF16 ? bwd_out_tma_kernel<BF, false, true>
                                                 : bwd_out_tma_kernel<float, false, true>)
                              : (dt == GSPN_BF16 ? bwd_out_tma_kernel<BF, false, false>
@@ -3620,7 +3625,8 @@ bool launch_bwd_fused(const ScanParams& p0, gspn_dtype_t dt, cudaStream_t s, int
   if (!pl.fuse_h && !knob("GSPN_TWO_LAUNCH")) {  // single launch: recurrence | grid barrier | outputs
     std::unique_ptr<OneArgs> one(new OneArgs());
     one->s = A;
-    if (setup_out_tma(p, A.g, dt, true, pl.nwc, smem_optin() - 1024 - 256, one->o, merged, hf)) {
+    const bool allow_wide = !merged && !hf && !local && dt == GSPN_BF16;  // the kWide instantiations
+    if (setup_out_tma(p, A.g, dt, true, pl.nwc, smem_optin() - 1024 - 256, one->o, merged, hf, allow_wide)) {
       // Per-plane readiness instead of the grid-wide barrier (experiments only): measured slower, 7.03-7.08
       // vs 6.78-6.82 ms on config 4 (3 same-box pairs; profiles/r2_notes.md) -- early phase-2 units compete
       // with the last chains for bandwidth and every chain pays a gpu-scope fence.
@@ -3652,6 +3658,10 @@ bool launch_bwd_fused(const ScanParams& p0, gspn_dtype_t dt, cudaStream_t s, int
       } else if (dt == GSPN_BF16) {
         if (local) e = mode == kNormPre ? launch_one(bwd_one_kernel<BF, kNormPre, true>, *one, s)
                                         : launch_one(bwd_one_kernel<BF, kNormClamp, true>, *one, s);
+        else if (one->o.wide)  // whole image rows per TMA box in the output phase (W > 256)
+          e = mode == kNormPre ? launch_one(bwd_one_kernel<BF, kNormPre, false, false, false, true>, *one, s)
+              : mode == kNormClamp ? launch_one(bwd_one_kernel<BF, kNormClamp, false, false, false, true>, *one, s)
+                                   : launch_one(bwd_one_kernel<BF, kNormFull, false, false, false, true>, *one, s);
         else e = mode == kNormPre ? launch_one(bwd_one_kernel<BF, kNormPre, false>, *one, s)
                  : mode == kNormClamp ? launch_one(bwd_one_kernel<BF, kNormClamp, false>, *one, s)
                                       : launch_one(bwd_one_kernel<BF, kNormFull, false>, *one, s);

@@ -608,3 +608,22 @@ def test_experiment_hf_backward_matches_default():
                        capture_output=True, text=True, timeout=600, cwd=root)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr[-2000:]
+
+
+@pytest.mark.gpu
+def test_segment_items_bitwise_equal_global_schedule():
+    """NEXT-2 as a scheduler: GSPN-local segments as independent work items give the same
+    bits as the same kchunk run chain by chain -- packed small planes, an unpacked bf16 plane with a short last
+    segment, grouped weights on the split backward, fp32, and a P-split (cluster) chain. Child process: the
+    experiment knob that turns segment items off is read from the environment."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "seg_cmp.py"), "1,8,8,64,64,15,bf16,16",
+                        "1,2,2,512,512,15,bf16,128", "1,2,2,400,336,15,bf16,96", "1,4,1,256,256,15,bf16,64",
+                        "1,2,2,128,96,15,f32,32", "1,2,1,1040,1040,15,bf16,256"],
+                       capture_output=True, text=True, timeout=900, cwd=root)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr[-2000:]
