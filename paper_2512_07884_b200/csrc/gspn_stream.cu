@@ -115,6 +115,8 @@ struct Plan {
   int fuse_h;          // fused backward: horizontal chains also form dw in the recurrence (else g only)
   int no_h;            // forward with checkpoints only (gspn_fwd_ckpt with h = NULL): h is not stored
   int nseg, kt;        // GSPN-local segment items: segments per chain slot, tiles per segment (nseg = 1: off)
+  int hcp;             // forward: horizontal tap tiles by cp.async (producer_loop kHcp); full barriers count 33
+  uint32_t tx_hc;      // TMA bytes of a horizontal stage when its tap tiles come by cp.async
 };
 
 struct alignas(64) StreamArgs {
@@ -286,8 +288,18 @@ __device__ __forceinline__ int64_t plane_of(const Chain& ch, int slot) {
 
 // ------------------------------------------------------------------------------ producer / storer
 
-template <bool kBwd, bool kCl, bool kXG = false>
-__device__ void producer_loop(const StreamArgs& A, uint8_t* ring, uint64_t* full, uint64_t* empty) {
+__device__ __forceinline__ void cp_async16_zfill(uint32_t dst, const void* src, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive_noinc(uint32_t bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
+}
+
+// kHcp (forward, plain chains): the three tap tiles of a horizontal chain come through the LSU path
+// (cp.async, 16 bytes per lane, all 32 lanes of the producer warp, completion on the stage's full barrier)
+// instead of TMA, halving the TMA row requests of a horizontal stage (32-byte rows: request-rate bound).
+template <bool kBwd, bool kCl, bool kXG = false, bool kHcp = false>
+__device__ void producer_loop(const StreamArgs& A, uint8_t* ring, uint64_t* full, uint64_t* empty, int lane = 0) {
   const Plan& pl = A.plan;
   const uint64_t pol_xin = policy_of(pl.pol[0]);
   const uint64_t pol_vin = policy_of(pl.pol[1]);
@@ -302,10 +314,34 @@ __device__ void producer_loop(const StreamArgs& A, uint8_t* ring, uint64_t* full
       const int j = kBwd ? (ch.j1 - 1 - jj) : (ch.j0 + jj);
       mbar_wait_sleep(smem_u32(&empty[stage]), phase ^ 1);
       const uint32_t fb = smem_u32(&full[stage]);
-      mbar_arrive_tx(fb, ch.vert ? pl.tx_v : pl.tx_h);
       const int s0 = tile_start(ch, j, pl.K);
       const uint32_t st = smem_u32(ring + static_cast<size_t>(stage) * pl.stage_bytes);
+      if constexpr (kHcp) {
+        if (!ch.vert) {  // tap tiles by cp.async: rows r = lane + 32 i, two 16-byte chunks each, 32-byte swizzle
+          const int rows = pl.nbh * pl.bh;
+          const int64_t HW = A.p.H * A.p.W;
+          const void* tap[3] = {A.p.wl, A.p.wm, A.p.wr};
+          for (int q = 0; q < 3; ++q) {
+            const char* src0 = static_cast<const char*>(tap[q]) + (ch.wplane * HW + s0) * pl.es;
+            const uint32_t dst0 = st + (F_WL + q) * pl.tile_bytes;
+            for (int r = lane; r < rows; r += 32) {
+              const bool in = base + r < A.p.H;
+              const char* src = src0 + (in ? static_cast<int64_t>(base + r) * A.p.W * pl.es : 0);
+              const uint32_t sw = static_cast<uint32_t>((r >> 2) & 1);
+              cp_async16_zfill(dst0 + r * 32 + ((0u ^ sw) << 4), src, in ? 16u : 0u);
+              cp_async16_zfill(dst0 + r * 32 + ((1u ^ sw) << 4), src + 16, in ? 16u : 0u);
+            }
+          }
+        }
+        cp_async_arrive_noinc(fb);  // every lane, every stage: the barrier counts 1 + 32 arrivals
+        if (lane != 0) {
+          if (++stage == pl.nstages) { stage = 0; phase ^= 1; }
+          continue;
+        }
+      }
+      mbar_arrive_tx(fb, ch.vert ? pl.tx_v : (kHcp ? pl.tx_hc : pl.tx_h));
       for (int t = 0; t < pl.nin; ++t) {
+        if (kHcp && !ch.vert && t >= F_WL) continue;
         const int tt = t + (kXG ? 1 : 0);  // kXG: the stage holds lam, w_l, w_m, w_r (x comes from L2)
         const int plane = static_cast<int>(plane_of<kBwd>(ch, tt));
         // x is re-read by the plane's other directions; vertical streams are read exactly once
@@ -644,7 +680,7 @@ __device__ __forceinline__ void init_barriers(const Smem& m, const Plan& pl) {
   }
   if (threadIdx.x == 0) {
     for (int s = 0; s < pl.nstages; ++s) {
-      mbar_init(smem_u32(&m.full[s]), 1);       // producer arrive + TMA bytes
+      mbar_init(smem_u32(&m.full[s]), pl.hcp ? 33 : 1);  // producer arrive + TMA bytes (+ 32 cp.async lanes)
       mbar_init(smem_u32(&m.empty[s]), 1);      // storer
       mbar_init(smem_u32(&m.done[s]), pl.nwc);  // one arrive per consumer warp
     }
@@ -910,9 +946,13 @@ __device__ __forceinline__ void fwd_stream_body(const StreamArgs& A, const Smem&
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int kOutSlot = kXG ? 0 : F_X;  // in-place horizontal outputs: over the x (or, kXG, lam) chunk
   if (warp == pl.nwc) {  // producer warp
-    if (lane == 0) {
+    if (lane == 0)
       for (int o = 0; o < 2; ++o)
         for (int t = 0; t < pl.nin; ++t) asm volatile("prefetch.tensormap [%0];" ::"l"(&A.in[o][t]) : "memory");
+    if constexpr (!kCl && !kXG) {
+      if (pl.hcp) producer_loop<false, false, false, true>(A, m.ring, m.full, m.empty, lane);
+      else if (lane == 0) producer_loop<false, kCl, kXG>(A, m.ring, m.full, m.empty);
+    } else if (lane == 0) {
       producer_loop<false, kCl, kXG>(A, m.ring, m.full, m.empty);
     }
     cluster_exit<kCl>();
@@ -2998,6 +3038,15 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 
 // 3D map over a [planes][H][W] tensor. plane_mid: dims ordered (W, planes, H) instead of (W, H, planes)
 // (packed vertical tiles: one box = K rows of npack consecutive planes, step-major in shared memory).
+// L2 promotion of the swizzled (horizontal-tile) maps: experiments only, GSPN_L2PROMO = 64 | 128 | 256.
+CUtensorMapL2promotion horiz_promotion() {
+  const char* e = knob("GSPN_L2PROMO");
+  const int v = e ? atoi(e) : 0;
+  return v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+         : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+         : v == 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_NONE;
+}
+
 bool encode(CUtensorMap* m, const void* base, gspn_dtype_t dt, int64_t W, int64_t H, int64_t planes, int box0,
             int box1, bool swizzle32, int box2 = 1, bool plane_mid = false) {
   auto fn = get_encode();
@@ -3016,7 +3065,7 @@ bool encode(CUtensorMap* m, const void* base, gspn_dtype_t dt, int64_t W, int64_
   CUresult r = fn(m, dt == GSPN_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
                   const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                   swizzle32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE,
-                  CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  swizzle32 ? horiz_promotion() : CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
@@ -3069,6 +3118,7 @@ bool make_plan(const ScanParams& p, gspn_dtype_t dt, int nin, Plan* pl) {
     // inside its 512-position tile (10 x 48 bf16 / 9 x 56 fp32). GSPN_FLAG_FORCE_SPLIT (tests): at
     // least 2 CTAs per chain, so the cluster path can be checked bitwise against the unsplit one.
     int nwc_c = (kPpad - 2 * GH) / pl->own;
+    if (const char* e = knob("GSPN_CL_NWC")) nwc_c = std::max(1, std::min(nwc_c, atoi(e)));  // experiments
     if (force_split) {
       const int64_t half = (maxP + 1) / 2;
       nwc_c = std::max(1, std::min<int>(nwc_c, static_cast<int>((half + pl->own - 1) / pl->own)));
@@ -3113,7 +3163,8 @@ bool make_plan(const ScanParams& p, gspn_dtype_t dt, int nin, Plan* pl) {
   const int budget = smem_optin() - 1024 /*alignment*/ - kSmemTail;
   int ns = budget / static_cast<int>(pl->stage_bytes);
   if (ns > 6) ns = 6;
-  if (ns < 2) return false;
+  if (const char* e = knob("GSPN_NSTAGES")) ns = std::max(1, std::min(ns, atoi(e)));  // experiments
+  if (ns < 1 || (ns < 2 && !knob("GSPN_NSTAGES"))) return false;
   pl->nstages = ns;
   pl->nchains = p.D * ((pl->nbc + pl->npack - 1) / pl->npack);  // work items: packs of chains
   // GSPN-local (kchunk > 0): each segment is an independent work item when segment boundaries fall on tile
@@ -3276,6 +3327,10 @@ cudaError_t launch_fwd_stream(const ScanParams& p, gspn_dtype_t dt, cudaStream_t
   if (!make_plan(p, dt, nin, &A.plan)) return cudaSuccess;
   if (p.ckpt != nullptr && (A.plan.cl > 1 || A.plan.npack > 1)) return cudaSuccess;  // checkpoints: see ckpt_eligible
   A.plan.no_h = p.hout == nullptr ? 1 : 0;
+  if (!xg && A.plan.cl == 1 && A.plan.npack == 1 && p.W % K == 0 && knob("GSPN_HCP")) {
+    A.plan.hcp = 1;
+    A.plan.tx_hc = static_cast<uint32_t>((nin - 3) * A.plan.nbh * A.plan.bh * 32);
+  }
   const void* ins_all[F_NIN] = {p.x, p.lam, p.wl, p.wm, p.wr};
   const int64_t planes_all[F_NIN] = {p.B * p.C, p.D * p.B * p.C, p.D * p.B * p.G, p.D * p.B * p.G, p.D * p.B * p.G};
   void* outs[1] = {p.hout};
