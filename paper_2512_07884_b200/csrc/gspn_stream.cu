@@ -849,6 +849,11 @@ __device__ __forceinline__ void fwd_half_vert(const Lanes<T>& ln, const uint8_t*
                                               uint32_t rm, const XPre<T>* xp = nullptr) {
   constexpr int KS = Cfg<T>::KS;
   constexpr int o = kXG ? 1 : 0;  // kXG: x is not in the stage, the other tiles move down one slot
+  // store predicate and pointer stepping hoisted out of the step loop (the null check is taken once)
+  const bool on = ln.own_v && gp != nullptr;
+  const int nv = L - t0;  // steps of this half inside [0, L)
+  uintptr_t ga = reinterpret_cast<uintptr_t>(gp);
+  const intptr_t gsb = static_cast<intptr_t>(gstep) * static_cast<intptr_t>(sizeof(T));
 #pragma unroll
   for (int ss = 0; ss < KS; ++ss) {
     if constexpr (kLocal) {  // segment start: h_{t-1} does not propagate (warp-uniform)
@@ -877,8 +882,8 @@ __device__ __forceinline__ void fwd_half_vert(const Lanes<T>& ln, const uint8_t*
     const float h1 = fwd_math<kPre>(x[1], lam[1], l[1], m[1], r[1], h[0], h[1], right);
     h[0] = h0;
     h[1] = h1;
-    GStore<T, 2>::st_if(ln.own_v && t0 + ss < L && gp != nullptr, gp, h, pol);
-    if (gp != nullptr) gp += gstep;
+    GStore<T, 2>::st_if(on && ss < nv, reinterpret_cast<T*>(ga), h, pol);
+    ga += gsb;
   }
 }
 
