@@ -180,6 +180,18 @@ __device__ __forceinline__ void st_global_b32_if(bool pred, void* p, uint32_t a,
       "l"(pol), "r"(static_cast<uint32_t>(pred))
       : "memory");
 }
+// Streaming stores (.cs: evict-first in L1 and L2) without a cache-policy operand: no per-store policy
+// descriptor has to be moved into uniform registers inside the unrolled step loops.
+__device__ __forceinline__ void st_global_cs_b32_if(bool pred, void* p, uint32_t a) {
+  asm volatile("{\n.reg .pred q;\nsetp.ne.u32 q, %2, 0;\n@q st.global.cs.b32 [%0], %1;\n}" ::"l"(p), "r"(a),
+               "r"(static_cast<uint32_t>(pred))
+               : "memory");
+}
+__device__ __forceinline__ void st_global_cs_v2_if(bool pred, void* p, uint32_t a, uint32_t b) {
+  asm volatile("{\n.reg .pred q;\nsetp.ne.u32 q, %3, 0;\n@q st.global.cs.v2.b32 [%0], {%1, %2};\n}" ::"l"(p), "r"(a),
+               "r"(b), "r"(static_cast<uint32_t>(pred))
+               : "memory");
+}
 __device__ __forceinline__ void st_global_v2_if(bool pred, void* p, uint32_t a, uint32_t b, uint64_t pol) {
   asm volatile(
       "{\n.reg .pred q;\nsetp.ne.u32 q, %4, 0;\n@q st.global.L2::cache_hint.v2.b32 [%0], {%1, %2}, %3;\n}" ::"l"(p),

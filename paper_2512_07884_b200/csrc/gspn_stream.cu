@@ -150,7 +150,12 @@ template <> struct GStore<__nv_bfloat16, 2> {
     st_global_b32(p, pack_bf16x2(v[0], v[1]), pol);
   }
   static __device__ __forceinline__ void st_if(bool pred, __nv_bfloat16* p, const float (&v)[2], uint64_t pol) {
+#ifdef GSPN_STORE_HINT
     st_global_b32_if(pred, p, pack_bf16x2(v[0], v[1]), pol);
+#else
+    (void)pol;
+    st_global_cs_b32_if(pred, p, pack_bf16x2(v[0], v[1]));
+#endif
   }
 };
 template <> struct GStore<float, 2> {
@@ -158,7 +163,12 @@ template <> struct GStore<float, 2> {
     st_global_v2(p, __float_as_uint(v[0]), __float_as_uint(v[1]), pol);
   }
   static __device__ __forceinline__ void st_if(bool pred, float* p, const float (&v)[2], uint64_t pol) {
+#ifdef GSPN_STORE_HINT
     st_global_v2_if(pred, p, __float_as_uint(v[0]), __float_as_uint(v[1]), pol);
+#else
+    (void)pol;
+    st_global_cs_v2_if(pred, p, __float_as_uint(v[0]), __float_as_uint(v[1]));
+#endif
   }
 };
 
