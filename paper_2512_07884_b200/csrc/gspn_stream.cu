@@ -3398,6 +3398,7 @@ bool setup_out_tma(const ScanParams& p, const void* g, gspn_dtype_t dt, bool ver
     while (RB > 1 && RB * (p.W / 4) > ncons * 32) RB >>= 1;
     if (p.W / 4 > ncons * 32) return false;
   }
+  if (const char* e = knob("GSPN_OUT_RB"); e && !grouped) RB = std::max(1, std::min(128, atoi(e)));  // experiments
   while (RB > 1 && 2 * stage_of(RB) > budget) RB >>= 1;
   if (2 * stage_of(RB) > budget) return false;
   if (!grouped && !knob("GSPN_OUT_NOBAL")) {
