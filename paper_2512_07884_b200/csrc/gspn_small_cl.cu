@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "gspn_common.cuh"
 #include "gspn_internal.h"
@@ -81,14 +82,15 @@ __device__ void taps_from_raw(const ScanParams& p, const DirGeom& gm, const T* R
 struct ClLayout {
   uint32_t tp, raw, buf, bufb, part, bars, total;
 };
-__host__ __device__ __forceinline__ ClLayout cl_layout(int HW, int es, int kb, int nplanes, uint32_t min_part) {
+__host__ __device__ __forceinline__ ClLayout cl_layout(int HW, int es, int kb, int nplanes, uint32_t min_part,
+                                                      int nbuf = 2) {
   ClLayout L;
   const uint32_t pb = static_cast<uint32_t>(HW * es);
   L.tp = 0;
   L.raw = static_cast<uint32_t>(HW) * 16u;
   L.buf = L.raw + 3u * pb;
   L.bufb = static_cast<uint32_t>(kb * nplanes) * pb;
-  L.part = L.buf + 2u * L.bufb;  // backward: per-warp fp32 tap-gradient partial sums (min_part bytes)
+  L.part = L.buf + static_cast<uint32_t>(nbuf) * L.bufb;  // backward: per-warp fp32 tap-gradient partial sums
   L.bars = L.part + (min_part + 15u) / 16u * 16u;
   L.total = L.bars + 8 * 8;  // up to 7 mbarriers
   return L;
@@ -281,7 +283,9 @@ __device__ __forceinline__ uint4 pack_vec(const float (&v)[16 / sizeof(T)]) {
   }
 }
 
-template <typename T, bool kLocal>
+// kKc channels per compute warp per batch (2: a unit of <= 8 channels in ONE batch with a single buffer, the
+// two chains interleaved step by step for ILP; 1: batches of kBwdWarps channels, double-buffered).
+template <typename T, bool kLocal, int kKc>
 __global__ void __launch_bounds__((kBwdWarps + 1) * 32, 2) bwd_grp_cl_kernel(ScanParams p, int kb) {
   extern __shared__ __align__(128) uint8_t sm[];
   constexpr int V = 16 / static_cast<int>(sizeof(T));
@@ -290,7 +294,7 @@ __global__ void __launch_bounds__((kBwdWarps + 1) * 32, 2) bwd_grp_cl_kernel(Sca
   const int k = static_cast<int>(cluster_ctarank());
   const int64_t unit = blockIdx.x / D, b = unit / p.G, g = unit % p.G;
   const uint32_t pb = static_cast<uint32_t>(HW) * sizeof(T);
-  const ClLayout Ly = cl_layout(HW, sizeof(T), kb, 4, static_cast<uint32_t>(kBwdWarps * 3 * HW * 4));
+  const ClLayout Ly = cl_layout(HW, sizeof(T), kb, 4, static_cast<uint32_t>(kBwdWarps * 3 * HW * 4), kKc == 2 ? 1 : 2);
   float4* TP = reinterpret_cast<float4*>(sm + Ly.tp);
   const T* RAW = reinterpret_cast<const T*>(sm + Ly.raw);
   // [0] taps, [1, 2] full (TMA bytes), [3, 4] ready (one arrive per cluster CTA: its g of the batch in the
@@ -358,50 +362,68 @@ __global__ void __launch_bounds__((kBwdWarps + 1) * 32, 2) bwd_grp_cl_kernel(Sca
     const int sb = i & 1;
     const uint32_t par = (i >> 1) & 1;
     mbar_wait_sleep(smem_u32(&bars[1 + sb]), par);
-    if (warp < nch(i)) {
-      const T* X = reinterpret_cast<const T*>(sm + slot(sb, warp, 0));
-      const T* DH = reinterpret_cast<const T*>(sm + slot(sb, warp, 2));
-      const T* HS = reinterpret_cast<const T*>(sm + slot(sb, warp, 3));
-      uint8_t* DHw = sm + slot(sb, warp, 2);
-      uint8_t* HSw = sm + slot(sb, warp, 3);
-      // lanes >= P read only x (never written)
-      const T* DHr = in ? DH : X;
-      const T* HSr = in ? HS : X;
+    if (warp * kKc < nch(i)) {
+      const T* DHr[kKc];
+      const T* HSr[kKc];
+      uint8_t* DHw[kKc];
+      uint8_t* HSw[kKc];
+      bool act[kKc];
+      float ea[kKc], eb[kKc], ec[kKc], dhv[kKc], hv[kKc];
+      int off = offr + (L - 1) * ts;
+#pragma unroll
+      for (int j = 0; j < kKc; ++j) {
+        act[j] = warp * kKc + j < nch(i);
+        const int c = act[j] ? warp * kKc + j : warp * kKc;
+        const T* X = reinterpret_cast<const T*>(sm + slot(sb, c, 0));
+        // lanes >= P read only x (never written)
+        DHr[j] = in ? reinterpret_cast<const T*>(sm + slot(sb, c, 2)) : X;
+        HSr[j] = in ? reinterpret_cast<const T*>(sm + slot(sb, c, 3)) : X;
+        DHw[j] = sm + slot(sb, c, 2);
+        HSw[j] = sm + slot(sb, c, 3);
+        ea[j] = eb[j] = ec[j] = 0.f;
+        dhv[j] = to_f(DHr[j][off]);
+        hv[j] = L >= 2 ? to_f(HSr[j][off - ts]) : 0.f;
+      }
       // the warp's tap-gradient partial sums at (t, r), scan order: this lane owns these words
       float* pa = part + (warp * 3 + 0) * HW + (L - 1) * P + r;
-      float ea = 0.f, eb = 0.f, ec = 0.f;
-      int off = offr + (L - 1) * ts;
-      float dhv = to_f(DHr[off]);
-      float hv = L >= 2 ? to_f(HSr[off - ts]) : 0.f;
 #pragma unroll 4
       for (int s = 0; s < L; ++s) {
         const int t = L - 1 - s;
-        // operands of step t-1 (pixels of rows t-1 / t-2: not written at this step)
-        const float ndh = t >= 1 ? to_f(DHr[off - ts]) : 0.f;
-        const float nh = t >= 2 ? to_f(HSr[off - 2 * ts]) : 0.f;
         const float4 q = TP[t * P + r];
-        const float from_r = __shfl_down_sync(0xffffffffu, ea, 1);  // a_{t+1}[r+1] g_{t+1}[r+1]
-        const float from_l = __shfl_up_sync(0xffffffffu, ec, 1);    // c_{t+1}[r-1] g_{t+1}[r-1]
-        const float gt = in ? dhv + eb + ((hr ? from_r : 0.f) + (hl ? from_l : 0.f)) : 0.f;
         bool seg = t == 0;
         if constexpr (kLocal) seg = seg_start_step(dir, t, L, kcn);
-        const float hc = (seg || !in) ? 0.f : hv;  // h_{t-1}[r] (0 at a segment start: h_{t-1} not propagated)
-        const float hlv = __shfl_up_sync(0xffffffffu, hc, 1), hrv = __shfl_down_sync(0xffffffffu, hc, 1);
+        float sa = 0.f, sbb = 0.f, sc = 0.f;
+#pragma unroll
+        for (int j = 0; j < kKc; ++j) {
+          // operands of step t-1 (pixels of rows t-1 / t-2: not written at this step)
+          const float ndh = t >= 1 ? to_f(DHr[j][off - ts]) : 0.f;
+          const float nh = t >= 2 ? to_f(HSr[j][off - 2 * ts]) : 0.f;
+          const float from_r = __shfl_down_sync(0xffffffffu, ea[j], 1);  // a_{t+1}[r+1] g_{t+1}[r+1]
+          const float from_l = __shfl_up_sync(0xffffffffu, ec[j], 1);    // c_{t+1}[r-1] g_{t+1}[r-1]
+          const float gt = in ? dhv[j] + eb[j] + ((hr ? from_r : 0.f) + (hl ? from_l : 0.f)) : 0.f;
+          const float hc = (seg || !in) ? 0.f : hv[j];  // h_{t-1}[r] (0 at a segment start)
+          const float hlv = __shfl_up_sync(0xffffffffu, hc, 1), hrv = __shfl_down_sync(0xffffffffu, hc, 1);
+          if (act[j]) {
+            sa = fmaf(gt, hl ? hlv : 0.f, sa);
+            sbb = fmaf(gt, hc, sbb);
+            sc = fmaf(gt, hr ? hrv : 0.f, sc);
+          }
+          ea[j] = q.x * gt;
+          eb[j] = q.y * gt;
+          ec[j] = q.z * gt;
+          if constexpr (kLocal) {
+            if (seg) ea[j] = eb[j] = ec[j] = 0.f;  // h_t did not depend on h_{t-1}
+          }
+          if (in && act[j]) g_put<T>(DHw[j], HSw[j], off, gt);  // over dh[t] (read) and h[t] (last read at t+1)
+          dhv[j] = ndh;
+          hv[j] = nh;
+        }
         if (in) {
-          pa[0] = fmaf(gt, hl ? hlv : 0.f, pa[0]);
-          pa[HW] = fmaf(gt, hc, pa[HW]);
-          pa[2 * HW] = fmaf(gt, hr ? hrv : 0.f, pa[2 * HW]);
+          pa[0] += sa;
+          pa[HW] += sbb;
+          pa[2 * HW] += sc;
         }
         pa -= P;
-        ea = q.x * gt;
-        eb = q.y * gt;
-        ec = q.z * gt;
-        if constexpr (kLocal) {
-          if (seg) ea = eb = ec = 0.f;  // h_t did not depend on h_{t-1}
-        }
-        if (in) g_put<T>(DHw, HSw, off, gt);  // over dh[t] (read above) and h[t] (last read at step t+1)
-        dhv = ndh;
-        hv = nh;
         off -= ts;
       }
     }
@@ -499,15 +521,21 @@ __global__ void __launch_bounds__((kBwdWarps + 1) * 32, 2) bwd_grp_cl_kernel(Sca
 }
 
 // channels per batch within the shared-memory budget (2+ CTAs per SM when possible)
-int cl_batch(const ScanParams& p, int es, bool bwd) {
+int cl_batch(const ScanParams& p, int es, bool bwd, int kc = 1) {
   const int HW = static_cast<int>(p.H * p.W);
   const int64_t Cg = p.C / p.G;
   const uint32_t budget = static_cast<uint32_t>(device_smem_optin());
-  const int maxkb = bwd ? kBwdWarps : kFwdWarps * kFwdKc;
+  const int maxkb = bwd ? kBwdWarps * kc : kFwdWarps * kFwdKc;
   const uint32_t minb2 = bwd ? static_cast<uint32_t>(kBwdWarps * 3 * HW * 4) : 0u;
+  const int nbuf = bwd && kc == 2 ? 1 : 2;
   int kb = static_cast<int>(std::min<int64_t>(maxkb, Cg));
-  while (kb > 1 && cl_layout(HW, es, kb, bwd ? 4 : 2, minb2).total > budget) --kb;
-  return cl_layout(HW, es, kb, bwd ? 4 : 2, minb2).total <= budget ? kb : 0;
+  while (kb > 1 && cl_layout(HW, es, kb, bwd ? 4 : 2, minb2, nbuf).total > budget) --kb;
+  return cl_layout(HW, es, kb, bwd ? 4 : 2, minb2, nbuf).total <= budget ? kb : 0;
+}
+
+bool knob_set_cl(const char* name) {  // experiment knob (A/B tooling): read only when GSPN_EXPERIMENTS is set
+  static const bool on = getenv("GSPN_EXPERIMENTS") != nullptr;
+  return on && getenv(name) != nullptr;
 }
 
 template <typename K>
@@ -569,16 +597,28 @@ cudaError_t launch_fwd_small_cl(const ScanParams& p, gspn_dtype_t dt, cudaStream
 
 cudaError_t launch_bwd_small_cl(const ScanParams& p, gspn_dtype_t dt, cudaStream_t s, int* launches) {
   *launches += 1;
-  const int es = dt == GSPN_BF16 ? 2 : 4, kb = cl_batch(p, es, true);
+  const int es = dt == GSPN_BF16 ? 2 : 4;
   const int HW = static_cast<int>(p.H * p.W);
-  const size_t smem = cl_layout(HW, es, kb, 4, static_cast<uint32_t>(kBwdWarps * 3 * HW * 4)).total;
+  const int64_t Cg = p.C / p.G;
+  // a unit of <= 2 kBwdWarps channels: one batch, two chains per warp, one buffer (3a: 8 channels)
+  const bool two = Cg <= 2 * kBwdWarps && cl_batch(p, es, true, 2) >= Cg && !knob_set_cl("GSPN_CL_KC1");
+  const int kb = two ? static_cast<int>(Cg) : cl_batch(p, es, true, 1);
+  const size_t smem = cl_layout(HW, es, kb, 4, static_cast<uint32_t>(kBwdWarps * 3 * HW * 4), two ? 1 : 2).total;
   const int threads = (kBwdWarps + 1) * 32;
   const bool local = p.kchunk > 0;
+  using BF = __nv_bfloat16;
+  if (two) {
+    if (dt == GSPN_BF16)
+      return local ? launch_cl(bwd_grp_cl_kernel<BF, true, 2>, p, threads, kb, smem, s)
+                   : launch_cl(bwd_grp_cl_kernel<BF, false, 2>, p, threads, kb, smem, s);
+    return local ? launch_cl(bwd_grp_cl_kernel<float, true, 2>, p, threads, kb, smem, s)
+                 : launch_cl(bwd_grp_cl_kernel<float, false, 2>, p, threads, kb, smem, s);
+  }
   if (dt == GSPN_BF16)
-    return local ? launch_cl(bwd_grp_cl_kernel<__nv_bfloat16, true>, p, threads, kb, smem, s)
-                 : launch_cl(bwd_grp_cl_kernel<__nv_bfloat16, false>, p, threads, kb, smem, s);
-  return local ? launch_cl(bwd_grp_cl_kernel<float, true>, p, threads, kb, smem, s)
-               : launch_cl(bwd_grp_cl_kernel<float, false>, p, threads, kb, smem, s);
+    return local ? launch_cl(bwd_grp_cl_kernel<BF, true, 1>, p, threads, kb, smem, s)
+                 : launch_cl(bwd_grp_cl_kernel<BF, false, 1>, p, threads, kb, smem, s);
+  return local ? launch_cl(bwd_grp_cl_kernel<float, true, 1>, p, threads, kb, smem, s)
+               : launch_cl(bwd_grp_cl_kernel<float, false, 1>, p, threads, kb, smem, s);
 }
 
 }  // namespace gspn
