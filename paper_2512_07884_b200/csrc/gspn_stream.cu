@@ -224,8 +224,10 @@ __device__ __forceinline__ int tile_base(const Plan& pl) {
   else return 0;
 }
 
+// 64-bit index arithmetic: the backward kernels keep this form (with the 32-bit one below the config-4
+// backward measured 1.5 % slower, 3 same-box reps, although its forward gained 3 %).
 template <bool kCl>
-__device__ __forceinline__ Chain make_chain(const ScanParams& p, const Plan& pl, int64_t wi) {
+__device__ __forceinline__ Chain make_chain64(const ScanParams& p, const Plan& pl, int64_t wi) {
   Chain ch;
   // GSPN-local segments as work items (the GSPN-2 grid over (chunk, n, c)): item wi is
   // segment wi % nseg of chain slot wi / nseg (nseg = 1: one item per chain)
@@ -257,6 +259,55 @@ __device__ __forceinline__ Chain make_chain(const ScanParams& p, const Plan& pl,
     ch.j1 = ch.rev ? ch.ntiles - c0 : c1;
   }
   return ch;
+}
+
+template <bool kCl>
+__device__ __forceinline__ Chain make_chain32(const ScanParams& p, const Plan& pl, int64_t wi) {
+  Chain ch;
+  // GSPN-local segments as work items (the GSPN-2 grid over (chunk, n, c)): item wi is
+  // segment wi % nseg of chain slot wi / nseg (nseg = 1: one item per chain). Every index here is < 2^31
+  // (make_plan checks), so the divisions are 32-bit: a 64-bit division costs ~60 instructions, and every
+  // warp of a CTA runs this once per work item (16 % of config 2's forward instructions when 64-bit).
+  const uint32_t uw = static_cast<uint32_t>(wi);
+  const uint32_t nseg = static_cast<uint32_t>(pl.nseg);
+  const uint32_t w = nseg == 1 ? uw : uw / nseg;
+  const int seg = static_cast<int>(uw - w * nseg);
+  const uint32_t D = static_cast<uint32_t>(p.D);
+  const uint32_t bcu = (w / D) * static_cast<uint32_t>(pl.npack);
+  const int64_t bc = bcu;
+  // Round i of the persistent grid covers slots [i G, (i+1) G): whole planes when D divides G. The
+  // direction is rotated by i so every CTA cycles through all D directions (vertical and horizontal
+  // chains run at different speeds; a fixed direction per CTA would leave the fast ones idle).
+  const uint32_t G = static_cast<uint32_t>(work_stride<kCl>(pl));
+  ch.k = static_cast<int>(nseg == 1 && G % D == 0 ? (w + w / G) % D : w % D);
+  const uint32_t dir = p.dirbit[ch.k];
+  ch.vert = (dir == GSPN_DIR_T2B) || (dir == GSPN_DIR_B2T);
+  ch.rev = (dir == GSPN_DIR_B2T) || (dir == GSPN_DIR_R2L);
+  ch.bc = bc;
+  const uint32_t Cu = static_cast<uint32_t>(p.C);
+  const uint32_t bu = bcu / Cu, cu = bcu - bu * Cu, gu = cu / (Cu / static_cast<uint32_t>(p.G));
+  ch.chain = (static_cast<int64_t>(ch.k) * p.B + bu) * p.C + cu;
+  ch.wplane = (static_cast<int64_t>(ch.k) * p.B + bu) * p.G + gu;
+  ch.L = static_cast<int>(ch.vert ? p.H : p.W);
+  ch.psub = static_cast<int>(ch.vert ? p.W : p.H);
+  ch.P = ch.psub * pl.npack;
+  ch.nvalid = static_cast<int>(pl.nbc - bc < pl.npack ? pl.nbc - bc : pl.npack);
+  ch.ntiles = (ch.L + pl.K - 1) / pl.K;
+  ch.j0 = 0;
+  ch.j1 = ch.ntiles;
+  if (pl.nseg > 1) {  // canonical tiles [c0, c1) of segment seg; reversed directions walk them backwards
+    const int c0 = min(seg * pl.kt, ch.ntiles), c1 = min((seg + 1) * pl.kt, ch.ntiles);
+    ch.j0 = ch.rev ? ch.ntiles - c1 : c0;
+    ch.j1 = ch.rev ? ch.ntiles - c0 : c1;
+  }
+  return ch;
+}
+
+// Work item -> chain: the forward roles use the 32-bit form, the backward roles the 64-bit one (measured).
+template <bool kCl, bool kFwd = false>
+__device__ __forceinline__ Chain make_chain(const ScanParams& p, const Plan& pl, int64_t wi) {
+  if constexpr (kFwd) return make_chain32<kCl>(p, pl, wi);
+  else return make_chain64<kCl>(p, pl, wi);
 }
 
 // Canonical start coordinate (row for vertical, column for horizontal) of tile j (j counts tiles in
@@ -318,7 +369,7 @@ __device__ void producer_loop(const StreamArgs& A, uint8_t* ring, uint64_t* full
   uint32_t phase = 0;
   const int base = tile_base<kCl>(pl);
   for (int64_t w = work_first<kCl>(pl); w < pl.nchains; w += work_stride<kCl>(pl)) {
-    const Chain ch = make_chain<kCl>(A.p, pl, w);
+    const Chain ch = make_chain<kCl, !kBwd>(A.p, pl, w);
     const int o = ch.vert ? 0 : 1;
     for (int jj = 0; jj < ch.j1 - ch.j0; ++jj) {
       const int j = kBwd ? (ch.j1 - 1 - jj) : (ch.j0 + jj);
@@ -377,7 +428,7 @@ __device__ void producer_loop(const StreamArgs& A, uint8_t* ring, uint64_t* full
 // input rows) the storer sends them out with TMA, waits until the bulk copy has read shared memory,
 // and only then hands the stage back to the producer. Vertical tiles store from registers, so their
 // stage is released as soon as the consumers are done with it.
-template <bool kCl>
+template <bool kCl, bool kFwdS = false>
 __device__ void storer_loop(const StreamArgs& A, uint8_t* ring, uint64_t* done, uint64_t* empty, int nout,
                             const int* slots, bool bwd) {
   const Plan& pl = A.plan;
@@ -386,7 +437,7 @@ __device__ void storer_loop(const StreamArgs& A, uint8_t* ring, uint64_t* done, 
   uint32_t phase = 0;
   int64_t pending = -1;  // single-launch bwd: plane pack of the previous chain, published one chain later
   for (int64_t w = work_first<kCl>(pl); w < pl.nchains; w += work_stride<kCl>(pl)) {
-    const Chain ch = make_chain<kCl>(A.p, pl, w);
+    const Chain ch = make_chain<kCl, kFwdS>(A.p, pl, w);
     for (int jj = 0; jj < ch.j1 - ch.j0; ++jj) {
       const int j = bwd ? (ch.j1 - 1 - jj) : (ch.j0 + jj);
       mbar_wait_sleep(smem_u32(&done[stage]), phase);
@@ -976,7 +1027,7 @@ __device__ __forceinline__ void fwd_stream_body(const StreamArgs& A, const Smem&
   if (warp == pl.nwc + 1) {  // storer warp
     if (lane == 0) {
       const int slots[1] = {kOutSlot};
-      storer_loop<kCl>(A, m.ring, m.done, m.empty, pl.no_h ? 0 : 1, slots, false);
+      storer_loop<kCl, true>(A, m.ring, m.done, m.empty, pl.no_h ? 0 : 1, slots, false);
     }
     cluster_exit<kCl>();
     return;
@@ -994,7 +1045,7 @@ __device__ __forceinline__ void fwd_stream_body(const StreamArgs& A, const Smem&
   float* const ckpt = A.p.ckpt;                           // NEXT-3 checkpoints (unpacked, unsplit chains)
   const int64_t ckstride = A.p.H * A.p.W / C::KS;        // floats per chain
   for (int64_t w = work_first<kCl>(pl); w < pl.nchains; w += work_stride<kCl>(pl)) {
-    const Chain ch = make_chain<kCl>(A.p, pl, w);
+    const Chain ch = make_chain<kCl, true>(A.p, pl, w);
     const Lanes<T> ln = make_lanes<T, kCl>(pl, A.p, ch, warp, lane);
     T* hout = pl.no_h ? nullptr : static_cast<T*>(A.p.hout) + ln.vout;
     float h[kE] = {0.f, 0.f};
@@ -3182,6 +3233,7 @@ bool make_plan(const ScanParams& p, gspn_dtype_t dt, int nin, Plan* pl) {
   if (ns < 1 || (ns < 2 && !knob("GSPN_NSTAGES"))) return false;
   pl->nstages = ns;
   pl->nchains = p.D * ((pl->nbc + pl->npack - 1) / pl->npack);  // work items: packs of chains
+  if (pl->nchains >= (int64_t{1} << 31) || pl->nbc >= (int64_t{1} << 31)) return false;  // 32-bit make_chain
   // GSPN-local (kchunk > 0): each segment is an independent work item when segment boundaries fall on tile
   // boundaries in scan order (kchunk, H and W multiples of K): more, shorter items for the persistent grid,
   // bitwise the same arithmetic (a segment starts from h = 0 / g = 0 either way)
@@ -3192,7 +3244,8 @@ bool make_plan(const ScanParams& p, gspn_dtype_t dt, int nin, Plan* pl) {
     const int64_t Lmax = std::max<int64_t>(p.H, p.W);
     pl->nseg = static_cast<int>((Lmax + p.kchunk - 1) / p.kchunk);
     pl->kt = static_cast<int>(p.kchunk / pl->K);
-    pl->nchains *= pl->nseg;
+    if (pl->nchains * pl->nseg < (int64_t{1} << 31)) pl->nchains *= pl->nseg;
+    else pl->nseg = 1;
   }
   pl->smem_bytes = 1024 + ns * pl->stage_bytes + kSmemTail;
   // L2 priorities (experiments: GSPN_POL="x,vin,hin,vout,hout,acc", each 0|1|2)
