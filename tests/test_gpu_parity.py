@@ -50,6 +50,10 @@ SHAPES = [
     (1, 2, 2, 24, 1000, 0xF, "bf16"),
     (1, 1, 1, 700, 48, 0xF, "bf16"),
     (1, 2, 2, 20, 1040, 0xF, "f32"),
+    # output phase with whole image rows per TMA box (W > 256, W % 256 == 0: 3 and 5 boxes of 256 per row),
+    # per-channel (single-launch backward) and grouped (grouped output kernel, P-split recurrence)
+    (1, 2, 2, 24, 768, 0xF, "bf16"),
+    (1, 4, 1, 20, 1280, 0xF, "bf16"),
 ]
 FLAGS = [0, gspn.FLAG_FORCE_GENERIC]
 
