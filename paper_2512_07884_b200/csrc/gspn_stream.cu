@@ -2583,8 +2583,9 @@ __device__ __forceinline__ void out_tma_body(const OutArgs& A, uint8_t* ring, ui
       int stage = 0;
       uint32_t phase = 0;
       for (int64_t u = blockIdx.x; u < A.nunits; u += gridDim.x) {
-        const int64_t bc = u / A.nrb;
-        const int i0 = static_cast<int>(u % A.nrb) * RB;
+        const uint32_t uq = static_cast<uint32_t>(u) / static_cast<uint32_t>(A.nrb);  // 32-bit: nunits < 2^31
+        const int64_t bc = uq;
+        const int i0 = static_cast<int>(static_cast<uint32_t>(u) - uq * static_cast<uint32_t>(A.nrb)) * RB;
         const int64_t b = bc / p.C, c = bc % p.C;
         mbar_wait_sleep(smem_u32(&empty[stage]), phase ^ 1);
         if (A.ready != nullptr) {  // every direction's g of this plane written (chains on other CTAs)
@@ -2631,8 +2632,9 @@ __device__ __forceinline__ void out_tma_body(const OutArgs& A, uint8_t* ring, ui
   int stage = 0;
   uint32_t phase = 0;
   for (int64_t u = blockIdx.x; u < A.nunits; u += gridDim.x) {
-    const int64_t bc = u / A.nrb;
-    const int i0 = static_cast<int>(u % A.nrb) * RB;
+    const uint32_t uq = static_cast<uint32_t>(u) / static_cast<uint32_t>(A.nrb);  // 32-bit: nunits < 2^31
+    const int64_t bc = uq;
+    const int i0 = static_cast<int>(static_cast<uint32_t>(u) - uq * static_cast<uint32_t>(A.nrb)) * RB;
     mbar_wait_sleep(smem_u32(&full[stage]), phase);
     const uint8_t* st = ring + static_cast<size_t>(stage) * A.stage_bytes;
     for (int idx = threadIdx.x; idx < RB * nchunk; idx += nthreads) {
@@ -2925,8 +2927,9 @@ __global__ void __launch_bounds__((kOutConsumers + 1) * 32, 1) bwd_out_grp_tma_k
       int stage = 0;
       uint32_t phase = 0;
       for (int64_t u = blockIdx.x; u < A.nunits; u += gridDim.x) {
-        const int64_t bg = u / A.nrb;
-        const int i0 = static_cast<int>(u % A.nrb) * RB;
+        const uint32_t uq = static_cast<uint32_t>(u) / static_cast<uint32_t>(A.nrb);  // 32-bit: nunits < 2^31
+        const int64_t bg = uq;
+        const int i0 = static_cast<int>(static_cast<uint32_t>(u) - uq * static_cast<uint32_t>(A.nrb)) * RB;
         const int64_t b = bg / p.G, grp = bg % p.G;
         for (int64_t cc = 0; cc < Cg; ++cc) {
           const int64_t bc = b * p.C + grp * Cg + cc;
@@ -2971,8 +2974,9 @@ __global__ void __launch_bounds__((kOutConsumers + 1) * 32, 1) bwd_out_grp_tma_k
   int stage = 0;
   uint32_t phase = 0;
   for (int64_t u = blockIdx.x; u < A.nunits; u += gridDim.x) {
-    const int64_t bg = u / A.nrb;
-    const int i0 = static_cast<int>(u % A.nrb) * RB;
+    const uint32_t uq = static_cast<uint32_t>(u) / static_cast<uint32_t>(A.nrb);  // 32-bit: nunits < 2^31
+    const int64_t bg = uq;
+    const int i0 = static_cast<int>(static_cast<uint32_t>(u) - uq * static_cast<uint32_t>(A.nrb)) * RB;
     const int64_t b = bg / p.G, grp = bg % p.G;
     const int64_t i = i0 + r;
     const bool valid = r < RB && i < H;
@@ -3488,6 +3492,7 @@ bool setup_out_tma(const ScanParams& p, const void* g, gspn_dtype_t dt, bool ver
   A.nstages = static_cast<int>(std::min<int64_t>(6, budget / A.stage_bytes));
   A.nrb = static_cast<int>((p.H + RB - 1) / RB);
   A.nunits = (grouped ? p.B * p.G : p.B * p.C) * A.nrb;
+  if (A.nunits >= (int64_t{1} << 31)) return false;  // 32-bit unit decode in the kernels
   const int64_t nc = p.D * p.B * p.C;
   const bool wd = A.wide != 0;
   bool ok = encode_rows(&A.x, p.x, dt, p.W, p.H, p.B * p.C, A.BX, RB, wd) &&
