@@ -359,7 +359,7 @@ __device__ __forceinline__ void cp_async_arrive_noinc(uint32_t bar) {
 // kHcp (forward, plain chains): the three tap tiles of a horizontal chain come through the LSU path
 // (cp.async, 16 bytes per lane, all 32 lanes of the producer warp, completion on the stage's full barrier)
 // instead of TMA, halving the TMA row requests of a horizontal stage (32-byte rows: request-rate bound).
-template <bool kBwd, bool kCl, bool kXG = false, bool kHcp = false>
+template <bool kBwd, bool kCl, bool kXG = false, bool kHcp = false, bool k32 = !kBwd>
 __device__ void producer_loop(const StreamArgs& A, uint8_t* ring, uint64_t* full, uint64_t* empty, int lane = 0) {
   const Plan& pl = A.plan;
   const uint64_t pol_xin = policy_of(pl.pol[0]);
@@ -369,7 +369,7 @@ __device__ void producer_loop(const StreamArgs& A, uint8_t* ring, uint64_t* full
   uint32_t phase = 0;
   const int base = tile_base<kCl>(pl);
   for (int64_t w = work_first<kCl>(pl); w < pl.nchains; w += work_stride<kCl>(pl)) {
-    const Chain ch = make_chain<kCl, !kBwd>(A.p, pl, w);
+    const Chain ch = make_chain<kCl, k32>(A.p, pl, w);
     const int o = ch.vert ? 0 : 1;
     for (int jj = 0; jj < ch.j1 - ch.j0; ++jj) {
       const int j = kBwd ? (ch.j1 - 1 - jj) : (ch.j0 + jj);
@@ -1232,6 +1232,12 @@ __device__ __forceinline__ void bwd_half_horiz(const Lanes<T>& ln, const uint8_t
 
 template <typename T, int kPre, bool kCl, bool kLocal>
 __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_stream_kernel(const __grid_constant__ StreamArgs A) {
+  // 32-bit work-item decode (experiments: GSPN built with -DGSPN_BS64 keeps the 64-bit one)
+#ifdef GSPN_BS64
+  constexpr bool kBS32 = false;
+#else
+  constexpr bool kBS32 = true;
+#endif
   using C = Cfg<T>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const Plan& pl = A.plan;
@@ -1242,7 +1248,7 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_stream_kernel(const
     if (lane == 0) {
       for (int o = 0; o < 2; ++o)
         for (int t = 0; t < B_NIN; ++t) asm volatile("prefetch.tensormap [%0];" ::"l"(&A.in[o][t]) : "memory");
-      producer_loop<true, kCl>(A, m.ring, m.full, m.empty);
+      producer_loop<true, kCl, false, false, kBS32>(A, m.ring, m.full, m.empty);
     }
     cluster_exit<kCl>();
     return;
@@ -1250,7 +1256,7 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_stream_kernel(const
   if (warp == pl.nwc + 1) {  // storer warp: horizontal tiles' g (written over the dh slot)
     if (lane == 0) {
       const int slots[1] = {B_DH};
-      storer_loop<kCl>(A, m.ring, m.done, m.empty, 1, slots, true);
+      storer_loop<kCl, kBS32>(A, m.ring, m.done, m.empty, 1, slots, true);
     }
     cluster_exit<kCl>();
     return;
@@ -1265,7 +1271,7 @@ __global__ void __launch_bounds__((kMaxNWC + 2) * 32, 1) bwd_stream_kernel(const
   int stage = 0, par = 0;
   uint32_t phase = 0;
   for (int64_t w = work_first<kCl>(pl); w < pl.nchains; w += work_stride<kCl>(pl)) {
-    const Chain ch = make_chain<kCl>(A.p, pl, w);
+    const Chain ch = make_chain<kCl, kBS32>(A.p, pl, w);
     const Lanes<T> ln = make_lanes<T, kCl>(pl, A.p, ch, warp, lane);
     T* gout = static_cast<T*>(A.g) + ln.vout;
     BwdState S;
