@@ -15,8 +15,10 @@
 // I/O: the high half over dh[t], the low half over h[t] -- h[t] was last read at step t+1); the tap gradients
 // Da / Db / Dc of the direction are summed over ALL the group's channels in registers (one accumulator per
 // step and lane), so dw is formed in-CTA through the normalisation Jacobian with no workspace and no atomics.
-// dx = sum_d g_d lam_d needs the D directions: after each batch the cluster synchronises and CTA k sums
-// its share of the batch's pixels over the D CTAs' shared memory (distributed shared memory, fixed order).
+// dx = sum_d g_d lam_d needs the D directions: after each batch the CTAs signal each other through mbarriers
+// (release / acquire at cluster scope; waited by spinning -- a suspend-time hint on a barrier completed by a
+// remote arrive measured slower) and CTA k sums its share of the batch's pixels over the D CTAs' shared memory
+// (distributed shared memory, fixed order). A unit of <= 8 channels runs as one batch with two chains per warp.
 // Every reduction has a fixed order: bitwise deterministic.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -46,14 +48,6 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
 __device__ __forceinline__ void bulk_s2g(void* dst, uint32_t src, uint32_t bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src), "r"(bytes)
                : "memory");
-}
-__device__ __forceinline__ void mbar_wait_cluster_sleep(uint32_t bar, uint32_t parity) {
-  asm volatile(
-      "{\n.reg .pred p;\n"
-      "WAITCS%=: mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1, %2;\n"
-      "@!p bra WAITCS%=;\n}" ::"r"(bar),
-      "r"(parity), "r"(1000000u)
-      : "memory");
 }
 __device__ __forceinline__ uint4 ld_cluster_v4(uint32_t addr) {
   uint4 v;
